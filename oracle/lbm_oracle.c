@@ -1,0 +1,636 @@
+/*
+ * lbm_oracle.c — plain, slow, obviously correct fp64 CPU oracle of the fused lattice
+ * Boltzmann stream–collide time step (Bauer, Köstler, Rüde, arXiv 2001.11806 "lbmpy").
+ *
+ * TEST INFRASTRUCTURE ONLY. Only tests/, __graft_entry__.smoke() and bench.py's
+ * cpu_baseline / --impl reference legs may load this library. The product path
+ * (paper_2001_11806_b200/) shares no code with it and never calls it.
+ *
+ * Citations: P:<n> = /root/reference/PAPER.md line n; G<k>/O<k> = SURVEY.md §8(c) readings
+ * (restated in DESIGN.md).
+ *
+ *   Eq. (1)  SRT/BGK
+ *   Eq. (2)  density / velocity
+ *   Eq. (3)  discrete equilibrium (2nd order, compressible rho0 = rho)
+ *   Eq. (4)  MRT step f' = M^-1 [S m_eq + (I-S) M f]
+ *   TRT as MRT with even/odd rates
+ *   Eq. (9)  cumulant generating function    P:398-402 (multi-step moments->cumulants P:409-415)
+ *   UBB (link-wise, fluid->boundary c)       P:517-537, reading G8
+ *   Two-array pull / push, AA pattern
+ *
+ * Layout: SoA, element (q, z, y, x) at q*Sq + (z+g)*ny*nx + y*nx + x, x fastest, with
+ * g = 1 ghost plane per z side when cfg->zghost (slab mode) and g = 0 otherwise; x and y
+ * always wrap (non-periodic axes carry wall cells on their faces, G9); z wraps when g = 0.
+ *
+ * Floating point: plain C, fp64, no FMA contraction (-ffp-contract=off), OpenMP static
+ * schedule over z (the paper's scheme).
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+#define ORA_SRT 0
+#define ORA_TRT 1
+#define ORA_MRT 2
+#define ORA_CUMULANT 3
+#define ORA_IDENTITY 4
+
+#define FLAG_FLUID 0
+#define FLAG_NOSLIP 1
+#define FLAG_UBB 2
+
+typedef struct {
+    int32_t Q;          /* 19 or 27 */
+    int32_t op;         /* ORA_* */
+    int64_t nx, ny, nz; /* local extent without ghost planes */
+    int32_t zghost;     /* 1: storage has planes z = -1 and z = nz (slab mode) */
+    int32_t nthreads;   /* OpenMP threads (<= 0: runtime default) */
+    double rates[8];    /* SRT [w]; TRT [we, wo]; MRT unused (S below); CUMULANT [ws, wb, w3, w4, w5, w6] */
+    double force[3];    /* Guo body force (SRT/TRT) */
+    double ubb_u[3];    /* UBB wall velocity */
+    double ubb_rho;     /* UBB reference density rho_w (G8: 1) */
+    const double *M;    /* MRT: Q x Q moment matrix, row-major (M_kq = P_k(c_q)) */
+    const double *Minv; /* MRT: its inverse */
+    const double *S;    /* MRT: Q relaxation rates (diagonal of S) */
+} ora_cfg;
+
+/* ------------------------------------------------------------------------------------ */
+/* Stencils (ordering G10: centre, then |c|_1, then lexicographic -1<0<1).     */
+/* ------------------------------------------------------------------------------------ */
+typedef struct {
+    int Q;
+    int c[27][3];
+    double w[27];
+    int opp[27];
+} ora_stencil_t;
+
+static int lex_less(const int *a, const int *b) {
+    int la = abs(a[0]) + abs(a[1]) + abs(a[2]);
+    int lb = abs(b[0]) + abs(b[1]) + abs(b[2]);
+    if (la != lb) return la < lb;
+    for (int i = 0; i < 3; ++i)
+        if (a[i] != b[i]) return a[i] < b[i];
+    return 0;
+}
+
+static void build_stencil(int Q, ora_stencil_t *s) {
+    int n = 0;
+    for (int x = -1; x <= 1; ++x)
+        for (int y = -1; y <= 1; ++y)
+            for (int z = -1; z <= 1; ++z) {
+                int l1 = abs(x) + abs(y) + abs(z);
+                if (Q == 19 && l1 == 3) continue; /* D3Q19 = D3Q27 minus the 8 corners */
+                s->c[n][0] = x; s->c[n][1] = y; s->c[n][2] = z;
+                ++n;
+            }
+    /* insertion sort into the ABI order */
+    for (int i = 1; i < n; ++i) {
+        int t[3] = {s->c[i][0], s->c[i][1], s->c[i][2]};
+        int j = i - 1;
+        while (j >= 0 && lex_less(t, s->c[j])) {
+            memcpy(s->c[j + 1], s->c[j], sizeof(t));
+            --j;
+        }
+        memcpy(s->c[j + 1], t, sizeof(t));
+    }
+    s->Q = n;
+    for (int i = 0; i < n; ++i) {
+        int c2 = s->c[i][0] * s->c[i][0] + s->c[i][1] * s->c[i][1] + s->c[i][2] * s->c[i][2];
+        if (Q == 19) s->w[i] = (c2 == 0) ? 1.0 / 3.0 : (c2 == 1) ? 1.0 / 18.0 : 1.0 / 36.0;
+        else s->w[i] = (c2 == 0) ? 8.0 / 27.0 : (c2 == 1) ? 2.0 / 27.0 : (c2 == 2) ? 1.0 / 54.0 : 1.0 / 216.0;
+        for (int j = 0; j < n; ++j)
+            if (s->c[j][0] == -s->c[i][0] && s->c[j][1] == -s->c[i][1] && s->c[j][2] == -s->c[i][2])
+                s->opp[i] = j;
+    }
+}
+
+void ora_stencil(int Q, int *c_out, double *w_out, int *opp_out) {
+    ora_stencil_t s;
+    build_stencil(Q, &s);
+    for (int i = 0; i < s.Q; ++i) {
+        for (int d = 0; d < 3; ++d) c_out[3 * i + d] = s.c[i][d];
+        w_out[i] = s.w[i];
+        opp_out[i] = s.opp[i];
+    }
+}
+
+/* ------------------------------------------------------------------------------------ */
+/* Macroscopic values Eq. (2) and equilibrium Eq. (3).                                     */
+/* ------------------------------------------------------------------------------------ */
+
+/* rho = sum_q f_q; u = (sum_q c_q f_q + fsign * F/2) / rho (compressible rho0 = rho).
+ * fsign = +1 for a pre-collision state (Guo), -1 for a post-collision state (G11). */
+static void macroscopic(const ora_stencil_t *s, const double *f, const double *F, double fsign,
+                        double *rho, double u[3]) {
+    double r = 0.0, j[3] = {0.0, 0.0, 0.0};
+    for (int q = 0; q < s->Q; ++q) {
+        r += f[q];
+        for (int d = 0; d < 3; ++d) j[d] += s->c[q][d] * f[q];
+    }
+    for (int d = 0; d < 3; ++d) u[d] = (j[d] + fsign * 0.5 * F[d]) / r;
+    *rho = r;
+}
+
+/* Eq. (3), second order, compressible: f_eq = w rho [1 + c.u/cs2 + (c.u)^2/(2 cs4) - u.u/(2 cs2)]
+ * with cs2 = 1/3 (G1). */
+static void equilibrium(const ora_stencil_t *s, double rho, const double u[3], double *feq) {
+    const double cs2 = 1.0 / 3.0;
+    double uu = u[0] * u[0] + u[1] * u[1] + u[2] * u[2];
+    for (int q = 0; q < s->Q; ++q) {
+        double cu = s->c[q][0] * u[0] + s->c[q][1] * u[1] + s->c[q][2] * u[2];
+        double second = 0.0; /* (1/(2 cs^4)) u_a u_b (c_a c_b - cs2 delta_ab) */
+        for (int a = 0; a < 3; ++a)
+            for (int b = 0; b < 3; ++b)
+                second += u[a] * u[b] * (s->c[q][a] * s->c[q][b] - (a == b ? cs2 : 0.0));
+        second /= 2.0 * cs2 * cs2;
+        feq[q] = s->w[q] * rho + s->w[q] * rho * (cu / cs2 + second);
+    }
+    (void)uu;
+}
+
+/* Product equilibrium (G2): the fixed point of the cumulant collision for D3Q27,
+ * prod_axes p(c_i; u_i), p(+-1) = (1/3 + u^2 +- u)/2, p(0) = 2/3 - u^2. */
+static void product_equilibrium(const ora_stencil_t *s, double rho, const double u[3], double *feq) {
+    for (int q = 0; q < s->Q; ++q) {
+        double v = rho;
+        for (int d = 0; d < 3; ++d) {
+            int c = s->c[q][d];
+            double p = (c == 0) ? (2.0 / 3.0 - u[d] * u[d]) : 0.5 * (1.0 / 3.0 + u[d] * u[d] + c * u[d]);
+            v *= p;
+        }
+        feq[q] = v;
+    }
+}
+
+/* ------------------------------------------------------------------------------------ */
+/* Collision operators                                                                     */
+/* ------------------------------------------------------------------------------------ */
+
+/* Guo source (G4), split by moment parity:
+ * S_q = (1 - wo/2) w_q 3 (c_q.F) + (1 - we/2) w_q [9 (c_q.u)(c_q.F) - 3 u.F]. */
+static double guo_source(const ora_stencil_t *s, int q, const double u[3], const double F[3],
+                         double we, double wo) {
+    double cF = s->c[q][0] * F[0] + s->c[q][1] * F[1] + s->c[q][2] * F[2];
+    double cu = s->c[q][0] * u[0] + s->c[q][1] * u[1] + s->c[q][2] * u[2];
+    double uF = u[0] * F[0] + u[1] * F[1] + u[2] * F[2];
+    return (1.0 - wo / 2.0) * s->w[q] * 3.0 * cF + (1.0 - we / 2.0) * s->w[q] * (9.0 * cu * cF - 3.0 * uF);
+}
+
+static int has_force(const ora_cfg *cfg) {
+    return cfg->force[0] != 0.0 || cfg->force[1] != 0.0 || cfg->force[2] != 0.0;
+}
+
+/* SRT, Eq. (1): f* = omega f_eq + (1 - omega) f (+ Guo source with we = wo = omega). */
+static void collide_srt(const ora_cfg *cfg, const ora_stencil_t *s, const double *f, double *out) {
+    double rho, u[3], feq[27];
+    double w = cfg->rates[0];
+    macroscopic(s, f, cfg->force, +1.0, &rho, u);
+    equilibrium(s, rho, u, feq);
+    for (int q = 0; q < s->Q; ++q) {
+        out[q] = w * feq[q] + (1.0 - w) * f[q];
+        if (has_force(cfg)) out[q] += guo_source(s, q, u, cfg->force, w, w);
+    }
+}
+
+/* TRT: f+- = (f_q +- f_qbar)/2, f* = f - we (f+ - feq+) - wo (f- - feq-) + S_q. */
+static void collide_trt(const ora_cfg *cfg, const ora_stencil_t *s, const double *f, double *out) {
+    double rho, u[3], feq[27];
+    double we = cfg->rates[0], wo = cfg->rates[1];
+    macroscopic(s, f, cfg->force, +1.0, &rho, u);
+    equilibrium(s, rho, u, feq);
+    for (int q = 0; q < s->Q; ++q) {
+        int qb = s->opp[q];
+        double fp = 0.5 * (f[q] + f[qb]), fm = 0.5 * (f[q] - f[qb]);
+        double ep = 0.5 * (feq[q] + feq[qb]), em = 0.5 * (feq[q] - feq[qb]);
+        out[q] = f[q] - we * (fp - ep) - wo * (fm - em);
+        if (has_force(cfg)) out[q] += guo_source(s, q, u, cfg->force, we, wo);
+    }
+}
+
+/* MRT, Eq. (4): f* = M^-1 [ S m_eq + (I - S) M f ], m_eq = M f_eq (Eq. 3; G1). */
+static void collide_mrt(const ora_cfg *cfg, const ora_stencil_t *s, const double *f, double *out) {
+    int Q = s->Q;
+    double rho, u[3], feq[27], m[27], meq[27], mp[27];
+    macroscopic(s, f, cfg->force, +1.0, &rho, u);
+    equilibrium(s, rho, u, feq);
+    for (int k = 0; k < Q; ++k) {
+        m[k] = 0.0;
+        meq[k] = 0.0;
+        for (int q = 0; q < Q; ++q) {
+            m[k] += cfg->M[k * Q + q] * f[q];
+            meq[k] += cfg->M[k * Q + q] * feq[q];
+        }
+        mp[k] = cfg->S[k] * meq[k] + (1.0 - cfg->S[k]) * m[k];
+    }
+    for (int q = 0; q < Q; ++q) {
+        out[q] = 0.0;
+        for (int k = 0; k < Q; ++k) out[q] += cfg->Minv[q * Q + k] * mp[k];
+    }
+}
+
+/* ---- Cumulant (O5): truncated power series in Q[xi]/(xi_x^3, xi_y^3, xi_z^3). ---------- */
+/* A series is 27 coefficients indexed a*9 + b*3 + c for xi_x^a xi_y^b xi_z^c, a,b,c <= 2. */
+static void ser_mul(const double *A, const double *B, double *C) {
+    double t[27];
+    for (int i = 0; i < 27; ++i) t[i] = 0.0;
+    for (int a1 = 0; a1 < 3; ++a1)
+        for (int b1 = 0; b1 < 3; ++b1)
+            for (int c1 = 0; c1 < 3; ++c1) {
+                double x = A[a1 * 9 + b1 * 3 + c1];
+                if (x == 0.0) continue;
+                for (int a2 = 0; a1 + a2 < 3; ++a2)
+                    for (int b2 = 0; b1 + b2 < 3; ++b2)
+                        for (int c2 = 0; c1 + c2 < 3; ++c2)
+                            t[(a1 + a2) * 9 + (b1 + b2) * 3 + (c1 + c2)] += x * B[a2 * 9 + b2 * 3 + c2];
+            }
+    for (int i = 0; i < 27; ++i) C[i] = t[i];
+}
+
+static const double fact3[3] = {1.0, 1.0, 2.0};
+
+/* ln(1 + X) = sum_{n=1}^{6} (-1)^{n+1} X^n / n, exact in the truncated ring (X^7 = 0). */
+static void ser_log1p(const double *X, double *K) {
+    double P[27];
+    memcpy(P, X, sizeof(P));
+    for (int i = 0; i < 27; ++i) K[i] = X[i];
+    for (int n = 2; n <= 6; ++n) {
+        ser_mul(P, X, P);
+        double sgn = (n % 2 == 0) ? -1.0 : 1.0;
+        for (int i = 0; i < 27; ++i) K[i] += sgn * P[i] / n;
+    }
+}
+
+/* exp(K) = sum_{n=0}^{6} K^n / n! for K without constant term (K^7 = 0). */
+static void ser_exp(const double *K, double *E) {
+    double P[27];
+    memcpy(P, K, sizeof(P));
+    for (int i = 0; i < 27; ++i) E[i] = K[i];
+    E[0] += 1.0;
+    double nf = 1.0;
+    for (int n = 2; n <= 6; ++n) {
+        ser_mul(P, K, P);
+        nf *= n;
+        for (int i = 0; i < 27; ++i) E[i] += P[i] / nf;
+    }
+}
+
+/* Cumulants kappa_abc of f (O5 steps 1-4). kappa[a*9+b*3+c]; returns rho. */
+static double cumulants(const ora_stencil_t *s, const double *f, double *kappa) {
+    double m[27], Mser[27];
+    for (int a = 0; a < 3; ++a)
+        for (int b = 0; b < 3; ++b)
+            for (int c = 0; c < 3; ++c) {
+                double v = 0.0; /* raw moment m_abc = sum_q f_q cx^a cy^b cz^c (Eq. 5) */
+                for (int q = 0; q < s->Q; ++q)
+                    v += f[q] * pow(s->c[q][0], a) * pow(s->c[q][1], b) * pow(s->c[q][2], c);
+                m[a * 9 + b * 3 + c] = v;
+            }
+    double rho = m[0];
+    for (int a = 0; a < 3; ++a)
+        for (int b = 0; b < 3; ++b)
+            for (int c = 0; c < 3; ++c)
+                Mser[a * 9 + b * 3 + c] = m[a * 9 + b * 3 + c] / (rho * fact3[a] * fact3[b] * fact3[c]);
+    Mser[0] -= 1.0; /* X = M - 1 */
+    double K[27];
+    ser_log1p(Mser, K);
+    for (int a = 0; a < 3; ++a)
+        for (int b = 0; b < 3; ++b)
+            for (int c = 0; c < 3; ++c)
+                kappa[a * 9 + b * 3 + c] = fact3[a] * fact3[b] * fact3[c] * K[a * 9 + b * 3 + c];
+    return rho;
+}
+
+/* Inverse of cumulants(): f from (rho, kappa) (O5 steps 6-7). */
+static void from_cumulants(const ora_stencil_t *s, double rho, const double *kappa, double *f) {
+    double K[27], E[27], m[27];
+    for (int a = 0; a < 3; ++a)
+        for (int b = 0; b < 3; ++b)
+            for (int c = 0; c < 3; ++c)
+                K[a * 9 + b * 3 + c] = kappa[a * 9 + b * 3 + c] / (fact3[a] * fact3[b] * fact3[c]);
+    K[0] = 0.0;
+    ser_exp(K, E);
+    for (int a = 0; a < 3; ++a)
+        for (int b = 0; b < 3; ++b)
+            for (int c = 0; c < 3; ++c)
+                m[a * 9 + b * 3 + c] = rho * fact3[a] * fact3[b] * fact3[c] * E[a * 9 + b * 3 + c];
+    /* (V x V x V)^-1 m: per axis f(-1) = (m2 - m1)/2, f(0) = m0 - m2, f(1) = (m2 + m1)/2. */
+    for (int q = 0; q < s->Q; ++q) {
+        double v = 0.0;
+        for (int a = 0; a < 3; ++a)
+            for (int b = 0; b < 3; ++b)
+                for (int c = 0; c < 3; ++c) {
+                    int e[3] = {a, b, c};
+                    double coef = 1.0;
+                    for (int d = 0; d < 3; ++d) {
+                        int cd = s->c[q][d];
+                        double k; /* weight of moment order e[d] in f(cd) */
+                        if (cd == 0) k = (e[d] == 0) ? 1.0 : (e[d] == 2) ? -1.0 : 0.0;
+                        else if (cd == 1) k = (e[d] == 0) ? 0.0 : 0.5;
+                        else k = (e[d] == 0) ? 0.0 : (e[d] == 1) ? -0.5 : 0.5;
+                        coef *= k;
+                    }
+                    v += coef * m[a * 9 + b * 3 + c];
+                }
+        f[q] = v;
+    }
+}
+
+/* Cumulant collision (O5 step 5, G7 rates): order 1 unchanged; 2nd-order trace
+ * T -> T + wb (3 cs2 - T); deviator and off-diagonals -> (1 - ws); order n >= 3 -> (1 - w_n). */
+static void collide_cumulant(const ora_cfg *cfg, const ora_stencil_t *s, const double *f, double *out) {
+    double kap[27];
+    double rho = cumulants(s, f, kap);
+    const double ws = cfg->rates[0], wb = cfg->rates[1];
+    const double cs2 = 1.0 / 3.0;
+    int i200 = 18, i020 = 6, i002 = 2;
+    double T = kap[i200] + kap[i020] + kap[i002];
+    double Tn = T + wb * (3.0 * cs2 - T);
+    double d200 = kap[i200] - T / 3.0, d020 = kap[i020] - T / 3.0, d002 = kap[i002] - T / 3.0;
+    kap[i200] = Tn / 3.0 + (1.0 - ws) * d200;
+    kap[i020] = Tn / 3.0 + (1.0 - ws) * d020;
+    kap[i002] = Tn / 3.0 + (1.0 - ws) * d002;
+    kap[9 + 3] *= (1.0 - ws);  /* kappa_110 */
+    kap[9 + 1] *= (1.0 - ws);  /* kappa_101 */
+    kap[3 + 1] *= (1.0 - ws);  /* kappa_011 */
+    for (int a = 0; a < 3; ++a)
+        for (int b = 0; b < 3; ++b)
+            for (int c = 0; c < 3; ++c) {
+                int n = a + b + c;
+                if (n >= 3) kap[a * 9 + b * 3 + c] *= (1.0 - cfg->rates[n - 1]); /* w3..w6 = rates[2..5] */
+            }
+    from_cumulants(s, rho, kap, out);
+}
+
+static void collide(const ora_cfg *cfg, const ora_stencil_t *s, const double *f, double *out) {
+    switch (cfg->op) {
+        case ORA_SRT: collide_srt(cfg, s, f, out); break;
+        case ORA_TRT: collide_trt(cfg, s, f, out); break;
+        case ORA_MRT: collide_mrt(cfg, s, f, out); break;
+        case ORA_CUMULANT: collide_cumulant(cfg, s, f, out); break;
+        default: for (int q = 0; q < s->Q; ++q) out[q] = f[q]; break; /* IDENTITY */
+    }
+}
+
+/* ------------------------------------------------------------------------------------ */
+/* Addressing                                                                              */
+/* ------------------------------------------------------------------------------------ */
+static inline int64_t plane_cells(const ora_cfg *cfg) {
+    return (cfg->nz + 2 * cfg->zghost) * cfg->ny * cfg->nx;
+}
+static inline int64_t wrap(int64_t i, int64_t n) { return ((i % n) + n) % n; }
+/* storage cell index of local (x, y, z); x, y wrap; z wraps unless ghost planes exist */
+static inline int64_t cell(const ora_cfg *cfg, int64_t x, int64_t y, int64_t z) {
+    x = wrap(x, cfg->nx);
+    y = wrap(y, cfg->ny);
+    if (!cfg->zghost) z = wrap(z, cfg->nz);
+    return ((z + cfg->zghost) * cfg->ny + y) * cfg->nx + x;
+}
+
+/* Pull-streaming value of direction q at fluid cell (x,y,z) from array `a` (O6):
+ * neighbour n = x - c_q; fluid -> a_q(n); NOSLIP -> a_qbar(x); UBB -> a_qbar(x) + 6 w rho_w c.u_w */
+static double pull_value(const ora_cfg *cfg, const ora_stencil_t *s, const double *a, const uint8_t *flags,
+                         int64_t x, int64_t y, int64_t z, int q) {
+    int64_t Sq = plane_cells(cfg);
+    int64_t self = cell(cfg, x, y, z);
+    int64_t nb = cell(cfg, x - s->c[q][0], y - s->c[q][1], z - s->c[q][2]);
+    uint8_t fl = flags ? flags[nb] : FLAG_FLUID;
+    if (fl == FLAG_FLUID) return a[q * Sq + nb];
+    double v = a[s->opp[q] * Sq + self];
+    if (fl == FLAG_UBB) {
+        double cu = s->c[q][0] * cfg->ubb_u[0] + s->c[q][1] * cfg->ubb_u[1] + s->c[q][2] * cfg->ubb_u[2];
+        v += 6.0 * s->w[q] * cfg->ubb_rho * cu;
+    }
+    return v;
+}
+
+static void set_threads(const ora_cfg *cfg) {
+#ifdef _OPENMP
+    extern void omp_set_num_threads(int);
+    if (cfg->nthreads > 0) omp_set_num_threads(cfg->nthreads);
+#else
+    (void)cfg;
+#endif
+}
+
+/* ------------------------------------------------------------------------------------ */
+/* Time steps                                                                              */
+/* ------------------------------------------------------------------------------------ */
+
+/* Fused stream-pull-collide, two arrays: dst = C(S(src)) on fluid cells. Wall
+ * cells of dst are not written. Returns 0. */
+int ora_step_pull(const ora_cfg *cfg, const double *src, double *dst, const uint8_t *flags) {
+    ora_stencil_t s;
+    build_stencil(cfg->Q, &s);
+    int64_t Sq = plane_cells(cfg);
+    set_threads(cfg);
+#pragma omp parallel for schedule(static)
+    for (int64_t z = 0; z < cfg->nz; ++z)
+        for (int64_t y = 0; y < cfg->ny; ++y)
+            for (int64_t x = 0; x < cfg->nx; ++x) {
+                int64_t self = cell(cfg, x, y, z);
+                if (flags && flags[self] != FLAG_FLUID) continue;
+                double f[27], out[27];
+                for (int q = 0; q < s.Q; ++q) f[q] = pull_value(cfg, &s, src, flags, x, y, z, q);
+                collide(cfg, &s, f, out);
+                for (int q = 0; q < s.Q; ++q) dst[q * Sq + self] = out[q];
+            }
+    return 0;
+}
+
+/* Collision only, in place (fluid cells): a = C(a). */
+int ora_collide_all(const ora_cfg *cfg, double *a, const uint8_t *flags) {
+    ora_stencil_t s;
+    build_stencil(cfg->Q, &s);
+    int64_t Sq = plane_cells(cfg);
+    set_threads(cfg);
+#pragma omp parallel for schedule(static)
+    for (int64_t z = 0; z < cfg->nz; ++z)
+        for (int64_t y = 0; y < cfg->ny; ++y)
+            for (int64_t x = 0; x < cfg->nx; ++x) {
+                int64_t self = cell(cfg, x, y, z);
+                if (flags && flags[self] != FLAG_FLUID) continue;
+                double f[27], out[27];
+                for (int q = 0; q < s.Q; ++q) f[q] = a[q * Sq + self];
+                collide(cfg, &s, f, out);
+                for (int q = 0; q < s.Q; ++q) a[q * Sq + self] = out[q];
+            }
+    return 0;
+}
+
+/* Streaming only (S with boundary conditions), two arrays: dst = S(src) on fluid cells. */
+int ora_stream(const ora_cfg *cfg, const double *src, double *dst, const uint8_t *flags) {
+    ora_stencil_t s;
+    build_stencil(cfg->Q, &s);
+    int64_t Sq = plane_cells(cfg);
+    set_threads(cfg);
+#pragma omp parallel for schedule(static)
+    for (int64_t z = 0; z < cfg->nz; ++z)
+        for (int64_t y = 0; y < cfg->ny; ++y)
+            for (int64_t x = 0; x < cfg->nx; ++x) {
+                int64_t self = cell(cfg, x, y, z);
+                if (flags && flags[self] != FLAG_FLUID) continue;
+                for (int q = 0; q < s.Q; ++q) dst[q * Sq + self] = pull_value(cfg, &s, src, flags, x, y, z, q);
+            }
+    return 0;
+}
+
+/* Fused collide-stream-push, two arrays: f <- S(C(f)), tmp is scratch of f's size. */
+int ora_step_push(const ora_cfg *cfg, double *f, double *tmp, const uint8_t *flags) {
+    int64_t n = (int64_t)cfg->Q * plane_cells(cfg);
+    memcpy(tmp, f, (size_t)n * sizeof(double));
+    ora_collide_all(cfg, tmp, flags);
+    return ora_stream(cfg, tmp, f, flags);
+}
+
+/* AA pattern (Fig. 3), single array, periodic (no flags), no ghost planes.
+ * Even step: in-place collision with reversed storage: read a[x](q), write a[x](qbar). */
+int ora_aa_even(const ora_cfg *cfg, double *a) {
+    if (cfg->zghost) return -1;
+    ora_stencil_t s;
+    build_stencil(cfg->Q, &s);
+    int64_t Sq = plane_cells(cfg);
+    set_threads(cfg);
+#pragma omp parallel for schedule(static)
+    for (int64_t z = 0; z < cfg->nz; ++z)
+        for (int64_t y = 0; y < cfg->ny; ++y)
+            for (int64_t x = 0; x < cfg->nx; ++x) {
+                int64_t self = cell(cfg, x, y, z);
+                double f[27], out[27];
+                for (int q = 0; q < s.Q; ++q) f[q] = a[q * Sq + self];
+                collide(cfg, &s, f, out);
+                for (int q = 0; q < s.Q; ++q) a[s.opp[q] * Sq + self] = out[q];
+            }
+    return 0;
+}
+
+/* Odd step: stream-pull, collide, stream-push: read a[x - c_q](qbar), write a[x + c_q](q).
+ * Each cell reads and writes the same set of slots, so cells are independent. */
+int ora_aa_odd(const ora_cfg *cfg, double *a) {
+    if (cfg->zghost) return -1;
+    ora_stencil_t s;
+    build_stencil(cfg->Q, &s);
+    int64_t Sq = plane_cells(cfg);
+    set_threads(cfg);
+#pragma omp parallel for schedule(static)
+    for (int64_t z = 0; z < cfg->nz; ++z)
+        for (int64_t y = 0; y < cfg->ny; ++y)
+            for (int64_t x = 0; x < cfg->nx; ++x) {
+                double f[27], out[27];
+                for (int q = 0; q < s.Q; ++q)
+                    f[q] = a[s.opp[q] * Sq + cell(cfg, x - s.c[q][0], y - s.c[q][1], z - s.c[q][2])];
+                collide(cfg, &s, f, out);
+                for (int q = 0; q < s.Q; ++q)
+                    a[q * Sq + cell(cfg, x + s.c[q][0], y + s.c[q][1], z + s.c[q][2])] = out[q];
+            }
+    return 0;
+}
+
+/* ------------------------------------------------------------------------------------ */
+/* Initialisation and readout                                                              */
+/* ------------------------------------------------------------------------------------ */
+
+/* f = f_eq(rho(x), u(x)) on every storage cell of the local extent (Eq. 3), or the product
+ * equilibrium for the cumulant (G2). rho: cells; u: [3][cells] (local extent, no ghosts). */
+int ora_init_equilibrium(const ora_cfg *cfg, const double *rho, const double *u, double *f) {
+    ora_stencil_t s;
+    build_stencil(cfg->Q, &s);
+    int64_t Sq = plane_cells(cfg);
+    int64_t n = cfg->nx * cfg->ny * cfg->nz;
+    for (int64_t z = 0; z < cfg->nz; ++z)
+        for (int64_t y = 0; y < cfg->ny; ++y)
+            for (int64_t x = 0; x < cfg->nx; ++x) {
+                int64_t i = (z * cfg->ny + y) * cfg->nx + x;
+                double uu[3] = {u[i], u[n + i], u[2 * n + i]}, feq[27];
+                if (cfg->op == ORA_CUMULANT) product_equilibrium(&s, rho[i], uu, feq);
+                else equilibrium(&s, rho[i], uu, feq);
+                int64_t self = cell(cfg, x, y, z);
+                for (int q = 0; q < s.Q; ++q) f[q * Sq + self] = feq[q];
+            }
+    return 0;
+}
+
+/* rho, u per local cell. fsign = +1 pre-collision state, -1 post-collision (pull) state. */
+int ora_macroscopic(const ora_cfg *cfg, const double *f, double fsign, double *rho, double *u) {
+    ora_stencil_t s;
+    build_stencil(cfg->Q, &s);
+    int64_t Sq = plane_cells(cfg);
+    int64_t n = cfg->nx * cfg->ny * cfg->nz;
+    for (int64_t z = 0; z < cfg->nz; ++z)
+        for (int64_t y = 0; y < cfg->ny; ++y)
+            for (int64_t x = 0; x < cfg->nx; ++x) {
+                int64_t i = (z * cfg->ny + y) * cfg->nx + x, self = cell(cfg, x, y, z);
+                double fc[27], r, uu[3];
+                for (int q = 0; q < s.Q; ++q) fc[q] = f[q * Sq + self];
+                macroscopic(&s, fc, cfg->force, fsign, &r, uu);
+                rho[i] = r;
+                u[i] = uu[0]; u[n + i] = uu[1]; u[2 * n + i] = uu[2];
+            }
+    return 0;
+}
+
+/* Single-cell helpers for tests and sampled full-size parity. */
+void ora_collide_cell(const ora_cfg *cfg, const double *f, double *out) {
+    ora_stencil_t s;
+    build_stencil(cfg->Q, &s);
+    collide(cfg, &s, f, out);
+}
+void ora_equilibrium_cell(int Q, double rho, const double *u, double *feq) {
+    ora_stencil_t s;
+    build_stencil(Q, &s);
+    equilibrium(&s, rho, u, feq);
+}
+void ora_product_equilibrium_cell(int Q, double rho, const double *u, double *feq) {
+    ora_stencil_t s;
+    build_stencil(Q, &s);
+    product_equilibrium(&s, rho, u, feq);
+}
+double ora_cumulants_cell(int Q, const double *f, double *kappa) {
+    ora_stencil_t s;
+    build_stencil(Q, &s);
+    return cumulants(&s, f, kappa);
+}
+void ora_from_cumulants_cell(int Q, double rho, const double *kappa, double *f) {
+    ora_stencil_t s;
+    build_stencil(Q, &s);
+    from_cumulants(&s, rho, kappa, f);
+}
+/* One pull update of the single fluid cell (x,y,z): out[q] = C(S(src))_q at that cell. */
+void ora_pull_cell(const ora_cfg *cfg, const double *src, const uint8_t *flags, int64_t x, int64_t y,
+                   int64_t z, double *out) {
+    ora_stencil_t s;
+    build_stencil(cfg->Q, &s);
+    double f[27];
+    for (int q = 0; q < s.Q; ++q) f[q] = pull_value(cfg, &s, src, flags, x, y, z, q);
+    collide(cfg, &s, f, out);
+}
+
+/* ------------------------------------------------------------------------------------ */
+/* Halo reference (O7): crossing populations of plane z in canonical order                 */
+/* (q ascending over {q : c_qz = dir}, then y, then x).                                    */
+/* ------------------------------------------------------------------------------------ */
+int64_t ora_pack_face(const ora_cfg *cfg, const double *f, int64_t z, int dir, double *out) {
+    ora_stencil_t s;
+    build_stencil(cfg->Q, &s);
+    int64_t Sq = plane_cells(cfg), n = 0;
+    for (int q = 0; q < s.Q; ++q) {
+        if (s.c[q][2] != dir) continue;
+        for (int64_t y = 0; y < cfg->ny; ++y)
+            for (int64_t x = 0; x < cfg->nx; ++x)
+                out[n++] = f[q * Sq + ((z + cfg->zghost) * cfg->ny + y) * cfg->nx + x];
+    }
+    return n;
+}
+/* Inverse: write a packed face into plane z (e.g. a ghost plane, z = -1 or z = nz). */
+int64_t ora_unpack_face(const ora_cfg *cfg, double *f, int64_t z, int dir, const double *in) {
+    ora_stencil_t s;
+    build_stencil(cfg->Q, &s);
+    int64_t Sq = plane_cells(cfg), n = 0;
+    for (int q = 0; q < s.Q; ++q) {
+        if (s.c[q][2] != dir) continue;
+        for (int64_t y = 0; y < cfg->ny; ++y)
+            for (int64_t x = 0; x < cfg->nx; ++x)
+                f[q * Sq + ((z + cfg->zghost) * cfg->ny + y) * cfg->nx + x] = in[n++];
+    }
+    return n;
+}

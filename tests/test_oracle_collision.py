@@ -1,0 +1,216 @@
+"""Oracle pins: collision operators (CPU, no GPU).
+
+Pins per SURVEY §8(c): conservation, equilibrium fixed points, degeneration SRT = TRT = MRT,
+the closed form of weighted MRT at config-2 rates, and for the cumulant operator the
+generating-function definition Eq. (9) evaluated by an independent route (Cauchy/FFT Taylor
+coefficients), round trip, product-equilibrium fixed point and the Gaussian (Isserlis) closed
+form at config-3 rates.
+"""
+from itertools import combinations, product
+
+import numpy as np
+import pytest
+
+import oracle as O
+
+RNG = np.random.default_rng(1234)
+
+
+def _random_state(Q, amp=0.02):
+    rho = 1 + RNG.uniform(-0.05, 0.05)
+    u = RNG.uniform(-0.05, 0.05, 3)
+    feq = O.equilibrium_cell(Q, rho, u)
+    _, w, _ = O.stencil_arrays(Q)
+    return feq + amp * w * RNG.uniform(-1, 1, Q)
+
+
+METHODS = [
+    O.Method(Q=19, op="srt", rates=(1.8,)),
+    O.Method(Q=27, op="srt", rates=(0.7,)),
+    O.Method(Q=19, op="trt", rates=(1.6, 0.5)),
+    O.Method(Q=27, op="trt", rates=(1.3, 1.1)),
+    O.Method(Q=19, op="mrt", rates=(1.9, 1.3, 1.1, 0.8)),
+    O.Method(Q=27, op="cumulant", rates=(1.95, 1.2, 1.1, 0.9, 1.3, 0.7)),
+]
+
+
+@pytest.mark.parametrize("m", METHODS, ids=lambda m: f"{m.op}{m.Q}")
+def test_collision_conserves_mass_momentum(m):
+    c, _, _ = O.stencil_arrays(m.Q)
+    for _ in range(10):
+        f = _random_state(m.Q)
+        g = O.collide_cell(m, f)
+        assert abs(g.sum() - f.sum()) < 1e-15
+        np.testing.assert_allclose(c.T @ g, c.T @ f, atol=1e-16)
+        assert np.abs(g - f).max() > 1e-6  # it does something
+
+
+@pytest.mark.parametrize("m", METHODS, ids=lambda m: f"{m.op}{m.Q}")
+def test_equilibrium_is_fixed_point(m):
+    rho, u = 1.02, np.array([0.03, -0.02, 0.05])
+    feq = (O.product_equilibrium_cell if m.op == "cumulant" else O.equilibrium_cell)(m.Q, rho, u)
+    np.testing.assert_allclose(O.collide_cell(m, feq), feq, rtol=0, atol=1e-15)
+
+
+def test_srt_literal_eq1():
+    """Eq. (1): f* = omega f_eq + (1-omega) f with rho, u from Eq. (2)."""
+    m = METHODS[0]
+    c, w, _ = O.stencil_arrays(19)
+    f = _random_state(19)
+    rho = f.sum()
+    u = c.T @ f / rho
+    cu = c @ u
+    feq = w * rho * (1 + 3 * cu + 4.5 * cu ** 2 - 1.5 * u @ u)
+    np.testing.assert_allclose(O.collide_cell(m, f), 1.8 * feq + (1 - 1.8) * f, rtol=0, atol=1e-15)
+
+
+@pytest.mark.parametrize("force", [(0, 0, 0), (1e-3, -2e-3, 5e-4)])
+def test_trt_equal_rates_is_srt(force):
+    for Q in (19, 27):
+        f = _random_state(Q)
+        a = O.collide_cell(O.Method(Q=Q, op="trt", rates=(1.37, 1.37), force=force), f)
+        b = O.collide_cell(O.Method(Q=Q, op="srt", rates=(1.37,), force=force), f)
+        np.testing.assert_allclose(a, b, rtol=0, atol=1e-16)
+
+
+def test_mrt_equal_rates_is_srt():
+    f = _random_state(19)
+    a = O.collide_cell(O.Method(Q=19, op="mrt", rates=(1.37, 1.37, 1.37, 1.37)), f)
+    b = O.collide_cell(O.Method(Q=19, op="srt", rates=(1.37,)), f)
+    np.testing.assert_allclose(a, b, rtol=0, atol=1e-15)
+
+
+def test_mrt_config2_closed_form():
+    """G6: with omega_shear = ws and every other rate 1, weighted MRT gives
+    f* = f_eq - (ws - 1) (9/2) w_q c_q c_q : dev(Pi_neq), Pi_neq = sum_q c c (f - f_eq)."""
+    c, w, _ = O.stencil_arrays(19)
+    m = O.Method(Q=19, op="mrt", rates=(1.9, 1.0, 1.0, 1.0))
+    for _ in range(5):
+        f = _random_state(19)
+        rho = f.sum()
+        u = c.T @ f / rho
+        feq = O.equilibrium_cell(19, rho, u)
+        Pi = np.einsum("qa,qb,q->ab", c, c, f - feq)
+        dev = Pi - np.trace(Pi) / 3 * np.eye(3)
+        ref = feq - (1.9 - 1) * 4.5 * w * np.einsum("qa,qb,ab->q", c, c, dev)
+        np.testing.assert_allclose(O.collide_cell(m, f), ref, rtol=0, atol=1e-16)
+
+
+def test_mrt_unweighted_differs_at_config2_rates():
+    f = _random_state(19)
+    a = O.collide_cell(O.Method(Q=19, op="mrt", rates=(1.9, 1.0, 1.0, 1.0)), f)
+    b = O.collide_cell(O.Method(Q=19, op="mrt", rates=(1.9, 1.0, 1.0, 1.0), mrt_weighted=False), f)
+    assert np.abs(a - b).max() > 1e-7  # G5: the reading matters
+
+
+def test_trt_guo_momentum_gain_and_source_parity():
+    """G4: one collision adds exactly F to the momentum and leaves the mass unchanged."""
+    F = np.array([1e-3, -2e-3, 5e-4])
+    for Q in (19, 27):
+        c, _, _ = O.stencil_arrays(Q)
+        f = _random_state(Q)
+        g = O.collide_cell(O.Method(Q=Q, op="trt", rates=(1.6, 0.5), force=F), f)
+        assert abs(g.sum() - f.sum()) < 1e-15
+        np.testing.assert_allclose(c.T @ g - c.T @ f, F, rtol=1e-12, atol=1e-17)
+
+
+# ---------------------------------------------------------------------------------------
+# Cumulants
+# ---------------------------------------------------------------------------------------
+def _taylor_coeffs_of_K(f, c, r=0.3, N=16):
+    """[xi^abc] K(xi), K = ln sum_q f_q exp(c_q . xi) (Eq. 9), by the Cauchy integral on a
+    polydisc of radius r (trapezoidal rule = FFT; aliasing error ~ r^N)."""
+    th = 2 * np.pi * np.arange(N) / N
+    z = r * np.exp(1j * th)
+    X, Y, Z = np.meshgrid(z, z, z, indexing="ij")
+    S = sum(fq * np.exp(cq[0] * X + cq[1] * Y + cq[2] * Z) for fq, cq in zip(f, c))
+    K = np.log(S)
+    coef = np.fft.fftn(K) / N ** 3
+    out = np.zeros((3, 3, 3))
+    for a, b, cc in product(range(3), repeat=3):
+        out[a, b, cc] = (coef[a, b, cc] / r ** (a + b + cc)).real
+    return out
+
+
+def test_cumulants_match_generating_function_eq9():
+    c, _, _ = O.stencil_arrays(27)
+    fact = np.array([1.0, 1.0, 2.0])
+    for _ in range(3):
+        f = _random_state(27, amp=0.2)
+        rho, kap = O.cumulants_cell(f)
+        tay = _taylor_coeffs_of_K(f, c)
+        ref = tay * fact[:, None, None] * fact[None, :, None] * fact[None, None, :]
+        assert abs(rho - f.sum()) < 1e-15
+        ref[0, 0, 0] = 0.0
+        k2 = kap.copy()
+        k2[0, 0, 0] = 0.0
+        np.testing.assert_allclose(k2, ref, rtol=0, atol=1e-12)
+
+
+def test_cumulant_second_order_is_central_moment():
+    c, _, _ = O.stencil_arrays(27)
+    f = _random_state(27, amp=0.3)
+    rho, kap = O.cumulants_cell(f)
+    u = c.T @ f / rho
+    d = c - u
+    Sig = np.einsum("qa,qb,q->ab", d, d, f) / rho
+    e2 = {(0, 0): (2, 0, 0), (1, 1): (0, 2, 0), (2, 2): (0, 0, 2), (0, 1): (1, 1, 0), (0, 2): (1, 0, 1), (1, 2): (0, 1, 1)}
+    for (a, b), e in e2.items():
+        assert abs(kap[e] - Sig[a, b]) < 1e-15
+    np.testing.assert_allclose([kap[1, 0, 0], kap[0, 1, 0], kap[0, 0, 1]], u, atol=1e-16)
+
+
+def test_cumulant_round_trip():
+    for _ in range(5):
+        f = _random_state(27, amp=0.3)
+        rho, kap = O.cumulants_cell(f)
+        np.testing.assert_allclose(O.from_cumulants_cell(rho, kap), f, rtol=0, atol=1e-15)
+
+
+def test_cumulant_all_rates_one_gives_product_equilibrium():
+    m = O.Method(Q=27, op="cumulant", rates=(1, 1, 1, 1, 1, 1))
+    c, _, _ = O.stencil_arrays(27)
+    f = _random_state(27, amp=0.3)
+    rho = f.sum()
+    u = c.T @ f / rho
+    np.testing.assert_allclose(O.collide_cell(m, f), O.product_equilibrium_cell(27, rho, u), rtol=0, atol=1e-16)
+
+
+def _gaussian_raw_moment(e, mean, cov):
+    """E[X^a Y^b Z^c] for a Gaussian by Isserlis' theorem (independent of the series)."""
+    idx = [d for d in range(3) for _ in range(e[d])]
+    n = len(idx)
+    tot = 0.0
+    for k in range(n + 1):
+        for S in combinations(range(n), k):  # positions taking the fluctuation
+            rest = [i for i in range(n) if i not in S]
+            mterm = np.prod([mean[idx[i]] for i in rest]) if rest else 1.0
+            tot += mterm * _pairings([idx[i] for i in S], cov)
+    return tot
+
+
+def _pairings(ax, cov):
+    if not ax:
+        return 1.0
+    if len(ax) % 2:
+        return 0.0
+    first, rest = ax[0], ax[1:]
+    return sum(cov[first, rest[j]] * _pairings(rest[:j] + rest[j + 1:], cov) for j in range(len(rest)))
+
+
+def test_cumulant_config3_isserlis_closed_form():
+    """G7: ws = 1.95, every other rate 1 -> f* = V^-1 [rho E_{N(u, S')} X^a Y^b Z^c] with
+    S' = cs2 I + (1 - ws) dev(S), S = second-order cumulants (central second moments / rho)."""
+    c, _, _ = O.stencil_arrays(27)
+    m = O.Method(Q=27, op="cumulant", rates=(1.95,))
+    A = np.array([[np.prod(np.asarray(cq, float) ** np.array(e)) for cq in c] for e in product(range(3), repeat=3)])
+    for _ in range(3):
+        f = _random_state(27, amp=0.2)
+        rho = f.sum()
+        u = c.T @ f / rho
+        d = c - u
+        Sig = np.einsum("qa,qb,q->ab", d, d, f) / rho
+        Sp = np.eye(3) / 3 + (1 - 1.95) * (Sig - np.trace(Sig) / 3 * np.eye(3))
+        mom = np.array([rho * _gaussian_raw_moment(e, u, Sp) for e in product(range(3), repeat=3)])
+        ref = np.linalg.solve(A, mom)
+        np.testing.assert_allclose(O.collide_cell(m, f), ref, rtol=0, atol=2e-15)
