@@ -1,0 +1,383 @@
+#!/usr/bin/env python
+"""Benchmark of the fused LB stream-collide step on B200 (BASELINE.json metric: MLUPS per GPU and
+per box, and fraction of the HBM roofline).
+
+Default workload = BASELINE config 4 (weak scaling): D3Q19 TRT fp64, 512^3 cells per GPU in a
+z-slab decomposition (512 x 512 x 512N), periodic, seeded near-equilibrium init, one ghost plane
+per side, NCCL halo exchange overlapped with the interior update. A bench "step" is one LB time
+step over the whole domain (every kernel of lbm_step(1)). Inputs (41 GB per GPU) are far larger
+than L2 (126 MB), so no flush is needed between steps.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c4|c0|c1_f64|c1_f32|c2|c3]
+  python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N
+  python bench.py --impl reference     # the CPU oracle on the host cores (bounded sample)
+
+Prints one JSON line (rank 0).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+# ---------------------------------------------------------------------------------------------
+# Workloads (BASELINE.json configs). bytes/cell = 2 q s (+1 B flag where a flag field exists).
+# ---------------------------------------------------------------------------------------------
+CONFIGS = {
+    "c4": dict(desc="D3Q19 TRT fp64 512^3/GPU z-slab weak scaling, periodic, random near-eq init (BASELINE config 4)",
+               shape=(512, 512, 512), weak=True, Q=19, op="trt", rates=(1.6, 0.5), dtype="f64", pattern="pull",
+               force=(0, 0, 0), geometry="periodic", init=("random", 1e-3, 0.01), job_steps=200),
+    "c0": dict(desc="D3Q19 SRT fp64 32^3 periodic omega=1.8 (BASELINE config 0; L2-resident, launch-bound)",
+               shape=(32, 32, 32), weak=False, Q=19, op="srt", rates=(1.8,), dtype="f64", pattern="pull",
+               force=(0, 0, 0), geometry="periodic", init=("random", 1e-3, 0.01), job_steps=100),
+    "c1_f64": dict(desc="D3Q19 TRT+Guo fp64 256^3 channel (BASELINE config 1)", shape=(256, 256, 256), weak=False,
+                   Q=19, op="trt", rates=(1.6, 0.5), dtype="f64", pattern="pull", force=(1e-6, 0, 0),
+                   geometry="channel", init=("rest",), job_steps=2000),
+    "c1_f32": dict(desc="D3Q19 TRT+Guo fp32 256^3 channel (BASELINE config 1)", shape=(256, 256, 256), weak=False,
+                   Q=19, op="trt", rates=(1.6, 0.5), dtype="f32", pattern="pull", force=(1e-6, 0, 0),
+                   geometry="channel", init=("rest",), job_steps=2000),
+    "c2": dict(desc="D3Q19 weighted MRT fp32 AA 512^3 shear wave (BASELINE config 2)", shape=(512, 512, 512),
+               weak=False, Q=19, op="mrt", rates=(1.9, 1.0, 1.0, 1.0), dtype="f32", pattern="aa", force=(0, 0, 0),
+               geometry="periodic", init=("shear", 0.0, 1e-4), job_steps=500),
+    "c3": dict(desc="D3Q27 cumulant fp64 384^3 lid-driven cavity (BASELINE config 3)", shape=(384, 384, 384),
+               weak=False, Q=27, op="cumulant", rates=(1.95,), dtype="f64", pattern="pull", force=(0, 0, 0),
+               geometry="cavity", init=("rest",), job_steps=1000, ubb=(0.05, 0, 0)),
+}
+
+
+def flags_for(cfg, shape):
+    import lbminputs as LI
+    nx, ny, nz = shape
+    if cfg["geometry"] == "channel":
+        return LI.channel_flags(nx, ny, nz), (1, 0, 1)
+    if cfg["geometry"] == "cavity":
+        return LI.cavity_flags(nx), (0, 0, 0)
+    return None, (1, 1, 1)
+
+
+def fluid_cells(cfg, shape, flags):
+    return int(np.prod(shape)) if flags is None else int((flags == 0).sum())
+
+
+def bytes_per_cell(cfg, flags):
+    s = 8 if cfg["dtype"] == "f64" else 4
+    return 2 * cfg["Q"] * s + (1 if flags is not None else 0)
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, torch copy)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def load_traffic(config_name):
+    """dram bytes per launch of the dominant kernel from a committed ncu --set full summary."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(p):
+        with open(p) as fh:
+            d = json.load(fh)
+        v = d.get(config_name)
+        if v:
+            return v
+    return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+
+    def __init__(self, index=0):
+        self.index = index
+        self.samples = []
+        self.proc = None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except (OSError, FileNotFoundError):
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.samples.append([s.strip() for s in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(2)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if len(s) > i + 2 and s[i + 2] == "Active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------------------------------------
+# CPU oracle timing (cpu_baseline and --impl reference)
+# ---------------------------------------------------------------------------------------------
+def oracle_sample(cfg, target_s=15.0, max_steps=None):
+    """Time the oracle (as it stands) on a bounded sample of the workload: a z-sub-slab of the
+    config's x-y extent, periodic in z, same operator and dtype-independent fp64 arithmetic."""
+    import oracle as O
+    nx, ny, nz = cfg["shape"]
+    threads = os.cpu_count() or 1
+    m = O.Method(Q=cfg["Q"], op=cfg["op"], rates=cfg["rates"], force=cfg["force"], ubb_u=cfg.get("ubb", (0, 0, 0)),
+                 nthreads=threads)
+    per_cell = 1.0 / (2.0e6 if cfg["op"] in ("srt", "trt") else 0.6e6 if cfg["op"] == "mrt" else 0.17e6)
+    planes = max(2, min(nz, int(target_s / (per_cell * nx * ny * 2))))
+    d = O.Domain(m, nx, ny, planes)
+    f = np.empty(d.shape)
+    _, w, _ = O.stencil_arrays(cfg["Q"])
+    f[:] = w[:, None, None, None]
+    g = f.copy()
+    steps, t0 = 0, time.perf_counter()
+    while True:
+        d.step_pull(f, g)
+        f, g = g, f
+        steps += 1
+        el = time.perf_counter() - t0
+        if el > target_s / 2 or (max_steps and steps >= max_steps):
+            break
+    cells = nx * ny * planes
+    return {"value": cells * steps / el / 1e6, "unit": "MLUPS", "cores": threads, "kind": "oracle",
+            "sample": f"{nx}x{ny}x{planes} sub-slab of {cfg['desc'].split(' (')[0]}, {steps} pull steps, fp64, "
+                      f"{threads} OpenMP threads, {el:.1f} s"}
+
+
+# ---------------------------------------------------------------------------------------------
+def run_reference(args, cfg):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    import oracle as O
+    nx, ny, nz = cfg["shape"]
+    threads = os.cpu_count() or 1
+    m = O.Method(Q=cfg["Q"], op=cfg["op"], rates=cfg["rates"], force=cfg["force"], ubb_u=cfg.get("ubb", (0, 0, 0)),
+                 nthreads=threads)
+    planes = 2  # each reference step = one pull step of a 2-plane sub-slab (bounded sample)
+    d = O.Domain(m, nx, ny, planes)
+    f = np.empty(d.shape)
+    _, w, _ = O.stencil_arrays(cfg["Q"])
+    f[:] = w[:, None, None, None]
+    g = f.copy()
+    for _ in range(args.warmup):
+        d.step_pull(f, g)
+        f, g = g, f
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        d.step_pull(f, g)
+        f, g = g, f
+    el = time.perf_counter() - t0
+    cells = nx * ny * planes
+    val = cells * args.steps / el / 1e6
+    line = {"impl": "reference", "metric": "MLUPS (fluid-cell updates per second, whole job)", "value": val,
+            "unit": "MLUPS", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": el / args.steps * 1e3, "higher_is_better": True, "scaling": "weak" if cfg["weak"] else "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": args.config, "desc": cfg["desc"], "sample": f"{nx}x{ny}x{planes} sub-slab per step"},
+            "cpu_baseline": {"value": val, "unit": "MLUPS", "cores": threads, "kind": "oracle",
+                             "sample": f"{nx}x{ny}x{planes} sub-slab, one pull step per bench step"},
+            "e2e": {"value": val, "unit": "MLUPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--config", default="c4", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--e2e-reps", type=int, default=2)
+    ap.add_argument("--e2e-steps", type=int, default=0, help="LB steps per e2e job (0 = the config's step count)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--halo-mode", type=int, default=0)
+    ap.add_argument("--block-x", type=int, default=0)
+    ap.add_argument("--graph", type=int, default=-1, help="CUDA-graph capture (default: on for small domains)")
+    args = ap.parse_args()
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        return run_reference(args, cfg)
+
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    assert world == args.gpus, f"--gpus {args.gpus} but WORLD_SIZE={world}"
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2001_11806_b200 import build
+    if rank == 0:
+        build.build()
+    if world > 1:
+        dist.barrier()
+    from paper_2001_11806_b200 import lbm as L
+
+    nx, ny, nz1 = cfg["shape"]
+    P = world
+    nzg = nz1 * P if cfg["weak"] else nz1
+    gshape = (nx, ny, nzg)
+    flags, periodic = flags_for(cfg, gshape)
+    nccl_id = None
+    if world > 1:
+        buf = torch.zeros(128, dtype=torch.uint8, device="cuda")
+        if rank == 0:
+            buf.copy_(torch.frombuffer(bytearray(L.nccl_unique_id()), dtype=torch.uint8))
+        dist.broadcast(buf, 0)
+        nccl_id = bytes(buf.cpu().numpy().tobytes())
+    stream = torch.cuda.current_stream()
+    small = np.prod(gshape) / P <= 2 ** 21
+    use_graph = bool(small) if args.graph < 0 else bool(args.graph)
+    sim = L.Simulation(gshape, stencil=cfg["Q"], collision=cfg["op"], rates=cfg["rates"], dtype=cfg["dtype"],
+                       pattern=cfg["pattern"], force=cfg["force"], flags=flags, ubb_velocity=cfg.get("ubb", (0, 0, 0)),
+                       periodic=periodic, rank=rank, nranks=world, nccl_id=nccl_id, device=local,
+                       stream=stream.cuda_stream, halo_mode=args.halo_mode, use_graph=use_graph, block_x=args.block_x)
+    kind = cfg["init"][0]
+    if kind == "rest":
+        sim.init_equilibrium(torch.ones(sim.cells, dtype=torch.float64, device="cuda"),
+                             torch.zeros(3 * sim.cells, dtype=torch.float64, device="cuda"))
+    else:
+        sim.init_random(0, cfg["init"][1], cfg["init"][2], 1 if kind == "shear" else 0, 0.01)
+
+    # ---- device-timed region ------------------------------------------------------------
+    sim.step(args.warmup)
+    sim.sync()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    sim.enable_kernel_timing() if not use_graph else None
+    l0 = sim.launches
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        sim.step(args.steps)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t_ms = ev0.elapsed_time(ev1)
+    launches = sim.launches - l0
+    if not use_graph:
+        kms, klaunch = sim.kernel_time_ms()
+    else:
+        kms, klaunch = t_ms, launches
+    if world > 1:
+        t = torch.tensor([t_ms, kms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t_ms, kms_max = float(t[0]), float(t[1])
+    else:
+        kms_max = kms
+    fl_local = None
+    if flags is not None:
+        fl_local = flags[sim.z0: sim.z0 + sim.nz_local]
+    nf_local = fluid_cells(cfg, (nx, ny, sim.nz_local), fl_local)
+    nf_total = nf_local * world if cfg["weak"] else fluid_cells(cfg, gshape, flags)
+    mlups = nf_total * args.steps / (t_ms / 1e3) / 1e6
+    bpc = bytes_per_cell(cfg, flags)
+    # dominant kernel: the fused stream-collide kernel (the only kernel of a single-GPU step)
+    kernel_ms_per_step = kms_max / args.steps
+    achieved = nf_local * bpc / (kernel_ms_per_step / 1e3) / 1e9
+    peak, peak_src = load_peaks()
+    clocks = clk.summary()
+
+    # ---- end-to-end through the public API with host buffers ------------------------------
+    e2e = None
+    job = args.e2e_steps or cfg["job_steps"]
+    if args.e2e_reps > 0:
+        rho_h = torch.empty(sim.cells, dtype=torch.float64, pin_memory=True)
+        u_h = torch.empty(3 * sim.cells, dtype=torch.float64, pin_memory=True)
+        if kind == "rest":
+            rho_h.fill_(1.0)
+            u_h.zero_()
+        else:
+            import lbminputs as LI
+            r, u = LI.random_fields(0, nx, ny, nzg, cfg["init"][1], cfg["init"][2], 1 if kind == "shear" else 0, 0.01,
+                                    z0=sim.z0, nz=sim.nz_local)
+            rho_h.copy_(torch.from_numpy(r.reshape(-1)))
+            u_h.copy_(torch.from_numpy(u.reshape(-1)))
+        rho_o = torch.empty(sim.cells, dtype=torch.float64, pin_memory=True)
+        u_o = torch.empty(3 * sim.cells, dtype=torch.float64, pin_memory=True)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_reps):
+            L.lbm_init_equilibrium(sim.h, rho_h.data_ptr(), u_h.data_ptr(), L.HOST)
+            L._check(L.lbm_step(sim.h, job), sim.h, "lbm_step")
+            L._check(L.lbm_get_macroscopic(sim.h, rho_o.data_ptr(), u_o.data_ptr(), L.HOST), sim.h, "get_macroscopic")
+        torch.cuda.synchronize()
+        te = time.perf_counter() - t0
+        if world > 1:
+            t = torch.tensor([te], dtype=torch.float64, device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            te = float(t[0])
+        e2e = {"value": nf_total * job * args.e2e_reps / te / 1e6, "unit": "MLUPS",
+               "h2d_bytes_per_step": int(4 * 8 * sim.cells), "d2h_bytes_per_step": int(4 * 8 * sim.cells),
+               "step": f"one job: init_equilibrium from pinned host rho/u, lbm_step({job}), get_macroscopic to host",
+               "reps": args.e2e_reps}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = oracle_sample(cfg)
+
+    if rank == 0:
+        line = {
+            "metric": "MLUPS (fluid-cell updates per second, whole job)",
+            "value": mlups, "unit": "MLUPS", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": t_ms / args.steps, "higher_is_better": True,
+            "scaling": "weak" if cfg["weak"] else "strong", "vs_baseline": None, "dtype": cfg["dtype"],
+            "data": "synthetic",
+            "config": {"workload": args.config, "desc": cfg["desc"], "global": list(gshape),
+                       "per_gpu_mlups": mlups / world, "pattern": cfg["pattern"],
+                       "parallelism": f"z-slab x{world}" if world > 1 else "single GPU",
+                       "l2": "inputs larger than L2 (no flush)" if not small else "L2-resident (launch-bound config)",
+                       "halo_mode": "zerocopy" if args.halo_mode == 0 else "packed", "cuda_graph": use_graph},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                         "traffic": load_traffic(args.config), "peak_source": peak_src,
+                         "algorithmic_bytes_per_cell": bpc, "cells_per_launch": nf_local,
+                         "kernel_ms_per_step": kernel_ms_per_step, "kernel_launches_timed": klaunch},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": launches,
+            "clocks": clocks,
+        }
+        print(json.dumps(line))
+    sim.close()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

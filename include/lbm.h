@@ -1,0 +1,185 @@
+/*
+ * lbm.h — C ABI of the B200-native fused lattice Boltzmann stream–collide library.
+ *
+ * Computes the lattice Boltzmann time step of Bauer, Köstler, Rüde, "lbmpy: Automatic code
+ * generation for efficient parallel lattice Boltzmann methods" (arXiv 2001.11806), cited as
+ * P:<line> of PAPER.md; readings of the paper are named G<k> as in DESIGN.md.
+ *
+ *   - D3Q19 / D3Q27 stencils, direction order G10: index 0 = (0,0,0), then by |c|_1,
+ *     then lexicographic on (cx, cy, cz) with -1 < 0 < 1.
+ *   - Collision: SRT/BGK Eq. (1); TRT with Guo forcing split by moment
+ *     parity (G4); weighted-orthogonal MRT Eq. (4) (G5/G6; D3Q19); cumulant
+ *     (G7; D3Q27). Equilibrium Eq. (3), 2nd order, compressible (G1).
+ *   - Storage patterns: two-array stream-pull-collide and the single-array AA
+ *     pattern.
+ *   - Boundaries from a uint8 flag field, compiled into the kernel:
+ *     0 = fluid, 1 = no-slip bounce-back, 2 = velocity bounce-back UBB (G8).
+ *   - Multi-GPU: z-slab decomposition, one ghost plane per side, NCCL send/recv of the
+ *     populations crossing each z face, overlapped with the interior update.
+ *
+ * Layout (part of the ABI): populations are SoA  f[q][z][y][x], x fastest. Host-visible arrays
+ * passed to this API always use the canonical layout of the *local* slab (no ghost planes):
+ * cell index i = x + nx * (y + ny * z_local). Vector fields are SoA [3][cells].
+ *
+ * Ownership: the library allocates and owns all device memory of a handle (populations, flags,
+ * halo buffers), its streams' events, its CUDA graphs and its NCCL communicator. The caller may
+ * pass its own compute stream (e.g. torch.cuda.current_stream().cuda_stream); the library then
+ * launches every kernel of lbm_step on it. Output buffers are caller-allocated.
+ *
+ * Errors: every function returns an int status, 0 = LBM_OK, negative = error. No C++ exception
+ * crosses the ABI. Asynchronous CUDA errors surface at the next lbm_step / lbm_sync.
+ * lbm_last_error(h) returns a human-readable message for the last failure on a handle.
+ * A handle is not thread-safe; several handles per process are allowed.
+ */
+#ifndef LBM_B200_H
+#define LBM_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes ------------------------------------------------------------------------ */
+#define LBM_OK 0
+#define LBM_EINVAL (-1)       /* invalid configuration or argument */
+#define LBM_EUNSUPPORTED (-2) /* valid but not implemented combination */
+#define LBM_ECUDA (-3)        /* CUDA runtime error */
+#define LBM_ENCCL (-4)        /* NCCL error */
+#define LBM_ENAN (-5)         /* NaN detected in the populations */
+#define LBM_EOOM (-6)         /* device allocation failed */
+
+/* ---- enums --------------------------------------------------------------------------------- */
+#define LBM_D3Q19 19
+#define LBM_D3Q27 27
+
+#define LBM_SRT 0      /* rates = [omega]                                              */
+#define LBM_TRT 1      /* rates = [omega_even, omega_odd]                              */
+#define LBM_MRT 2      /* rates = [omega_shear, omega_bulk, omega_3, omega_4] (D3Q19)  */
+#define LBM_CUMULANT 3 /* rates = [omega_shear, omega_bulk, omega_3..omega_6] (D3Q27); missing = 1 */
+#define LBM_IDENTITY 4 /* debug: no collision (pure data movement, bit-exact tests)    */
+
+#define LBM_F64 0
+#define LBM_F32 1
+
+#define LBM_PULL 0 /* two arrays, fused stream-pull-collide: state P(n) = (C o S)^n P(0) */
+#define LBM_AA 1   /* one array, AA pattern: state F(n) = (S o C)^n f0 (G11)            */
+
+#define LBM_FLAG_FLUID 0
+#define LBM_FLAG_NOSLIP 1
+#define LBM_FLAG_UBB 2
+
+#define LBM_HOST 0   /* pointer argument is host memory   */
+#define LBM_DEVICE 1 /* pointer argument is device memory */
+
+#define LBM_HALO_ZEROCOPY 0 /* one NCCL message per crossing population plane */
+#define LBM_HALO_PACKED 1   /* pack kernel + one message per face            */
+
+typedef struct lbm_config {
+    int32_t stencil;   /* LBM_D3Q19 | LBM_D3Q27 */
+    int32_t collision; /* LBM_SRT .. LBM_IDENTITY */
+    int32_t dtype;     /* LBM_F64 | LBM_F32: storage and arithmetic precision. Populations are
+                          stored zero-centred, g_q = f_q - w_q (G12), in both precisions. */
+    int32_t pattern;   /* LBM_PULL | LBM_AA */
+    int32_t n_rates;
+    double rates[8];      /* see the collision enum; every rate must lie in (0, 2) */
+    double force[3];      /* Guo body force per cell (SRT/TRT only); all zero = force-free kernel */
+    int64_t global[3];    /* global lattice nx, ny, nz (cells) */
+    int32_t periodic[3];  /* 1 = periodic axis; a non-periodic axis must carry wall cells on both faces */
+    const uint8_t *flags; /* host, global nx*ny*nz, x fastest; NULL = all fluid */
+    double ubb_velocity[3]; /* wall velocity of UBB cells; wall density rho_w = 1 (G8) */
+    int32_t rank, nranks;   /* z-slab decomposition across processes (NCCL); nranks = 1: single GPU */
+    const uint8_t *nccl_id; /* 128-byte ncclUniqueId from lbm_nccl_unique_id on rank 0; NULL if nranks = 1 */
+    int32_t n_local_slabs;  /* >1: decompose this process's domain into slabs on one GPU, exchanged
+                               with device copies (loopback; tests the multi-GPU path on one GPU) */
+    int32_t device;         /* CUDA device ordinal */
+    void *stream;           /* cudaStream_t for compute; NULL = library-created stream */
+    int32_t halo_mode;      /* LBM_HALO_ZEROCOPY | LBM_HALO_PACKED */
+    int32_t use_graph;      /* 1 = capture a two-step cycle in a CUDA graph (single slab only) */
+    int32_t block_x;        /* threads per block along x (0 = default) */
+    int32_t check_nan_every;/* >0: check for NaN every k steps inside lbm_step (LBM_ENAN) */
+} lbm_config;
+
+typedef struct lbm_handle_s *lbm_handle;
+
+/* Fill `cfg` with defaults (D3Q19 SRT fp64 pull, omega = 1.8, 32^3 periodic, 1 rank). */
+void lbm_config_default(lbm_config *cfg);
+
+/* Create a simulation. Validates cfg (LBM_EINVAL: bad enum, rate outside (0,2), nz % nranks != 0,
+ * non-periodic axis without walls on its faces; LBM_EUNSUPPORTED: AA with flags or with
+ * decomposition, MRT other than D3Q19, cumulant other than D3Q27, force with MRT/cumulant),
+ * allocates device memory and, for nranks > 1, creates the NCCL communicator (collective: every
+ * rank must call it). The state is zero until an init call. */
+int lbm_create(const lbm_config *cfg, lbm_handle *out);
+int lbm_destroy(lbm_handle h);
+
+/* Local extent of this process: out[0] = z0 (global index of local plane 0), out[1] = nz_local,
+ * out[2] = nx, out[3] = ny. */
+int lbm_local_extent(lbm_handle h, int64_t out[4]);
+
+/* Initialise the populations to the equilibrium of (rho, u) per local cell: Eq. (3) for
+ * SRT/TRT/MRT/IDENTITY, the product equilibrium (G2) for the cumulant. rho: [cells], u: [3][cells]
+ * (fp64), in host or device memory per `where`. Resets the step counter to 0. */
+int lbm_init_equilibrium(lbm_handle h, const double *rho, const double *u, int32_t where);
+
+/* Same, with rho = 1 + U(-rho_amp, rho_amp), u_i = U(-u_amp, u_amp) from the counter-based
+ * generator keyed by the GLOBAL cell index (G13), so every decomposition gives the same state.
+ * profile = 1 adds profile_amp * sin(2 pi z / nz_global) to u_x (shear wave, config 2). */
+int lbm_init_random(lbm_handle h, uint64_t seed, double rho_amp, double u_amp, int32_t profile,
+                    double profile_amp);
+
+/* Advance n time steps (pull: n stream-pull-collide updates; AA: alternating even/odd). */
+int lbm_step(lbm_handle h, int64_t n);
+/* Block until all work of the handle finished; returns any pending asynchronous error. */
+int lbm_sync(lbm_handle h);
+int64_t lbm_steps_done(lbm_handle h);
+
+/* Density and velocity of every local cell (fp64). Pull state (post-collision): u = (j - F/2)/rho;
+ * AA state (pre-collision): u = (j + F/2)/rho (G11). Wall cells report their stored values. */
+int lbm_get_macroscopic(lbm_handle h, double *rho, double *u, int32_t where);
+
+/* Canonical populations f_q (fp64, [q][cells]) of the local slab: f = g + w_q. For AA after an
+ * odd number of steps the reversed-slot layout is gathered back (F(n)_q(y) = a[y - c_q](qbar)).
+ * raw = 1 returns/accepts the stored values g (no +w_q, no AA gather; bit-exact data movement). */
+int lbm_get_populations(lbm_handle h, double *out, int32_t where, int32_t raw);
+int lbm_set_populations(lbm_handle h, const double *in, int32_t where, int32_t raw);
+
+/* Canonical populations (fp64) of n local cells given by their local linear indices
+ * i = x + nx * (y + ny * z_local) (host array `cells`); out[q * n + k] (host). For sampled
+ * full-size parity checks without copying the whole lattice. */
+int lbm_get_populations_at(lbm_handle h, const int64_t *cells, int64_t n, double *out);
+
+/* Halo reference: the crossing populations of local plane z (c_qz == dir, dir = +1 or -1) of the
+ * current state in canonical order (q ascending over {q : c_qz = dir}, then y, then x), raw stored
+ * values, fp64. `out` holds n_cross * nx * ny values (n_cross = 5 for D3Q19, 9 for D3Q27). */
+int lbm_pack_face(lbm_handle h, int64_t z, int32_t dir, double *out, int32_t where);
+
+/* Timing support: record CUDA events around every kernel of the next lbm_step call on the
+ * launching stream; lbm_kernel_time_ms returns the summed kernel time of that call. */
+int lbm_kernel_time_ms(lbm_handle h, double *ms, int64_t *launches);
+/* Number of kernel launches issued by this handle since creation (all kernels). */
+int64_t lbm_launch_count(lbm_handle h);
+
+/* NCCL bootstrap: 128-byte unique id (call on rank 0, broadcast with torch.distributed). */
+int lbm_nccl_unique_id(uint8_t out[128]);
+
+/* Host-only decomposition plan (no GPU): slab of `rank` in a z-decomposition of nz cells over
+ * nranks ranks: out[0] = z0, out[1] = nz_local, out[2] = rank below (z - 1 side, periodic),
+ * out[3] = rank above. Returns LBM_EINVAL if nz % nranks != 0 or nz / nranks < 2. */
+int lbm_slab_plan(int64_t nz, int32_t nranks, int32_t rank, int64_t out[4]);
+/* Crossing directions of a z face: writes the stencil indices q with c_qz == dir into q_out
+ * (ascending) and returns their count (5 for D3Q19, 9 for D3Q27), or LBM_EINVAL. */
+int lbm_crossing_directions(int32_t stencil, int32_t dir, int32_t *q_out);
+/* Direction table of a stencil in ABI order: c_out[3*q + d], w_out[q]. Returns Q or LBM_EINVAL. */
+int lbm_stencil_table(int32_t stencil, int32_t *c_out, double *w_out);
+
+const char *lbm_strerror(int status);
+const char *lbm_last_error(lbm_handle h);
+/* Library version string. */
+const char *lbm_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LBM_B200_H */

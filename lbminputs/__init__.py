@@ -105,3 +105,17 @@ def random_obstacles(seed: int, nx: int, ny: int, nz: int, frac: float = 0.1, ub
     fl[r < frac] = NOSLIP
     fl[(r < frac) & (s < ubb_frac)] = UBB
     return fl
+
+
+def fields_at(seed: int, nx: int, ny: int, nz: int, xs, ys, zs, rho_amp: float, u_amp: float,
+              profile: int = PROFILE_NONE, profile_amp: float = 0.0):
+    """(rho, u) at arbitrary (wrapped) global coordinates; arrays xs, ys, zs broadcast together.
+    Same values as random_fields() at those cells."""
+    xs, ys, zs = (np.asarray(v, np.int64) for v in np.broadcast_arrays(xs, ys, zs))
+    xs, ys, zs = xs % nx, ys % ny, zs % nz
+    ig = (xs + nx * (ys + ny * zs)).astype(np.uint64)
+    rho = 1.0 + uniform(seed, ig, 0, -rho_amp, rho_amp) if rho_amp != 0 else np.ones(ig.shape)
+    u = np.stack([uniform(seed, ig, k, -u_amp, u_amp) if u_amp != 0 else np.zeros(ig.shape) for k in (1, 2, 3)])
+    if profile == PROFILE_SHEAR_WAVE:
+        u[0] = profile_amp * np.sin(2.0 * np.pi * zs.astype(np.float64) / nz) + u[0]
+    return rho, u

@@ -1,0 +1,81 @@
+"""Build the CUDA C-ABI library ``liblbm_b200.so`` in-tree for sm_100a (nvcc, parallel objects).
+
+Usage: ``python -m paper_2001_11806_b200.build [--force]``. The .so lands next to this file so
+it travels with the repository snapshot to the GPU box.
+"""
+from __future__ import annotations
+
+import concurrent.futures as cf
+import os
+import subprocess
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+CSRC = os.path.join(HERE, "csrc")
+OUT = os.path.join(HERE, "liblbm_b200.so")
+OBJ = os.path.join(HERE, "build_obj")
+SOURCES = ["runtime.cu", "k_misc.cu", "k_trt.cu", "k_mrt.cu", "k_cumulant.cu", "k_identity.cu"]
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+
+
+def nccl_dirs():
+    import importlib.util
+    spec = importlib.util.find_spec("nvidia.nccl")
+    if spec is None or not spec.submodule_search_locations:
+        raise RuntimeError("NCCL (nvidia-nccl wheel shipped with torch) not found")
+    base = list(spec.submodule_search_locations)[0]
+    return os.path.join(base, "include"), os.path.join(base, "lib")
+
+
+def _flags():
+    inc, _ = nccl_dirs()
+    return ["-O3", "-std=c++17", "-lineinfo", "--expt-relaxed-constexpr", "-Xcompiler", "-fPIC",
+            "-Xptxas", "-v", "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-I", inc] + ARCH
+
+
+def _deps():
+    return [os.path.join(CSRC, f) for f in os.listdir(CSRC)] + [os.path.join(ROOT, "include", "lbm.h")]
+
+
+def _stale(target, deps):
+    if not os.path.exists(target):
+        return True
+    t = os.path.getmtime(target)
+    return any(os.path.getmtime(d) > t for d in deps)
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    deps = _deps()
+    if not force and not _stale(OUT, deps + [__file__]):
+        return OUT
+    os.makedirs(OBJ, exist_ok=True)
+    flags = _flags()
+
+    def compile_one(src):
+        obj = os.path.join(OBJ, src.replace(".cu", ".o"))
+        cmd = [NVCC, "-c", os.path.join(CSRC, src), "-o", obj] + flags
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"nvcc failed for {src}:\n{r.stderr[-8000:]}")
+        with open(obj + ".ptxas.txt", "w") as fh:
+            fh.write(r.stderr)
+        return obj
+
+    with cf.ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
+        objs = list(ex.map(compile_one, SOURCES))
+    _, libdir = nccl_dirs()
+    cmd = [NVCC, "-shared", "-o", OUT + ".tmp"] + objs + ARCH + [
+        "-L", libdir, "-l:libnccl.so.2", "-Xlinker", f"-rpath,{libdir}", "-Xcompiler", "-fPIC"]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"link failed:\n{r.stderr[-4000:]}")
+    os.replace(OUT + ".tmp", OUT)
+    if verbose:
+        print(f"built {OUT}")
+    return OUT
+
+
+if __name__ == "__main__":
+    build(force="--force" in sys.argv, verbose=True)

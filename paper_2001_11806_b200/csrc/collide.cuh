@@ -1,0 +1,372 @@
+// collide.cuh — register-resident collision operators for the fused kernels.
+//
+// All operators act on ZERO-CENTRED populations g_q = f_q - w_q (G12) held in registers, so
+// the O(1) lattice weights never enter the arithmetic: drho = sum g, j = sum c g,
+// g_eq,q = w_q drho + w_q rho (3 c.u + 9/2 (c.u)^2 - 3/2 u.u)   (Eq. 3 minus w_q).
+// Because w_q = w_qbar the centring commutes with bounce-back and AA slot swaps.
+//
+// SRT  Eq. (1), P:263-267 — run as TRT with omega_e = omega_o = omega (exact special case).
+// TRT  P:422-460 — symmetric/antisymmetric pair split, Guo source split by parity (G4).
+// MRT  Eq. (4), P:294-300 — weighted-orthogonal D3Q19 moments; relaxed per group
+//      (shear / bulk / order 3 / order 4). This file uses its own
+//      orthogonal basis of each group's span (hand-derived): the
+//      result depends only on the spans when rates are assigned per group (G6).
+// CUM  P:391-415 — D3Q27 cumulants via the per-axis central-moment ("chimera") transform and
+//      the explicit mean-zero moment<->cumulant relations (Faa di Bruno), G7 rates.
+#pragma once
+#include "stencil.cuh"
+
+namespace lbm {
+
+template <typename T>
+struct Rates {
+    T r[8];
+    T F[3];
+};
+
+// ---------------------------------------------------------------------------------------
+// Macroscopic values from centred populations. Pre-collision (pull-gathered) state.
+// ---------------------------------------------------------------------------------------
+template <int Q, typename T>
+__device__ __forceinline__ void moments0(const T (&g)[Q], T &drho, T &jx, T &jy, T &jz) {
+    using S = Stencil<Q>;
+    drho = T(0);
+    jx = T(0);
+    jy = T(0);
+    jz = T(0);
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+        drho += g[q];
+        if (S::cx(q) > 0) jx += g[q];
+        if (S::cx(q) < 0) jx -= g[q];
+        if (S::cy(q) > 0) jy += g[q];
+        if (S::cy(q) < 0) jy -= g[q];
+        if (S::cz(q) > 0) jz += g[q];
+        if (S::cz(q) < 0) jz -= g[q];
+    }
+}
+
+// ---------------------------------------------------------------------------------------
+// TRT (+ Guo). SRT passes we == wo.
+// ---------------------------------------------------------------------------------------
+template <int Q, typename T, bool FORCE>
+__device__ __forceinline__ void collide_trt(T (&g)[Q], const Rates<T> &p) {
+    using S = Stencil<Q>;
+    const T we = p.r[0], wo = p.r[1];
+    T drho, jx, jy, jz;
+    moments0<Q, T>(g, drho, jx, jy, jz);
+    const T rho = T(1) + drho;
+    const T inv = T(1) / rho;
+    T ux, uy, uz;
+    if (FORCE) {
+        ux = (jx + T(0.5) * p.F[0]) * inv;
+        uy = (jy + T(0.5) * p.F[1]) * inv;
+        uz = (jz + T(0.5) * p.F[2]) * inv;
+    } else {
+        ux = jx * inv;
+        uy = jy * inv;
+        uz = jz * inv;
+    }
+    const T uu15 = T(1.5) * (ux * ux + uy * uy + uz * uz);
+    const T se = T(1) - T(0.5) * we, so = T(1) - T(0.5) * wo;
+    T uF3 = T(0);
+    if (FORCE) uF3 = T(3) * (ux * p.F[0] + uy * p.F[1] + uz * p.F[2]);
+    {  // centre
+        const T w0 = T(S::w(0));
+        const T eq = w0 * drho - w0 * rho * uu15;
+        g[0] = g[0] - we * (g[0] - eq);
+        if (FORCE) g[0] -= se * w0 * uF3;
+    }
+#pragma unroll
+    for (int q = 1; q < Q; ++q) {
+        constexpr int dummy = 0;
+        (void)dummy;
+        if (q < S::opp(q)) {
+            const int b = S::opp(q);
+            const T w = T(S::w(q));
+            const T cu = T(S::cx(q)) * ux + T(S::cy(q)) * uy + T(S::cz(q)) * uz;
+            const T wr = w * rho;
+            const T eqs = w * drho + wr * (T(4.5) * cu * cu - uu15);
+            const T eqa = wr * T(3) * cu;
+            const T fp = T(0.5) * (g[q] + g[b]);
+            const T fm = T(0.5) * (g[q] - g[b]);
+            const T ds = we * (fp - eqs);
+            const T da = wo * (fm - eqa);
+            T gq = g[q] - ds - da;
+            T gb = g[b] - ds + da;
+            if (FORCE) {
+                const T cF = T(S::cx(q)) * p.F[0] + T(S::cy(q)) * p.F[1] + T(S::cz(q)) * p.F[2];
+                const T sa = so * w * T(3) * cF;
+                const T ss = se * w * (T(9) * cu * cF - uF3);
+                gq += ss + sa;
+                gb += ss - sa;
+            }
+            g[q] = gq;
+            g[b] = gb;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------------------
+// Weighted-orthogonal MRT, D3Q19. Basis per rate group (integer-valued polynomials, their
+// weighted norms N_k = sum_q w_q P_k(c_q)^2):
+//   shear : xy, xz, yz (1/9 each), 2x^2-y^2-z^2 (4/3), y^2-z^2 (4/9)
+//   bulk  : c^2 - 1 (2/3)
+//   order3: 3(y^2+z^2)x - 2x (2/3), (y^2-z^2)x (2/9), and the y, z analogues
+//   order4: 6(x^2y^2+x^2z^2+y^2z^2) - 3c^2 + 1 (2), (2x^2-1)(y^2-z^2) (4/9),
+//           2(x^2y^2+x^2z^2-2y^2z^2) - (2x^2-y^2-z^2) (4/3)
+// Together with 1, x, y, z they are a complete weighted-orthogonal basis of R^19, so
+// f* = f - sum_k omega_k w P_k <P_k, f - f_eq> / N_k is Eq. (4) with per-group rates.
+// ---------------------------------------------------------------------------------------
+__host__ __device__ constexpr int mrt_poly(int k, int x, int y, int z) {
+    const int xx = x * x, yy = y * y, zz = z * z, cc = xx + yy + zz;
+    switch (k) {
+        case 0: return x * y;
+        case 1: return x * z;
+        case 2: return y * z;
+        case 3: return 2 * xx - yy - zz;
+        case 4: return yy - zz;
+        case 5: return cc - 1;
+        case 6: return 3 * (yy + zz) * x - 2 * x;
+        case 7: return (yy - zz) * x;
+        case 8: return 3 * (xx + zz) * y - 2 * y;
+        case 9: return (xx - zz) * y;
+        case 10: return 3 * (xx + yy) * z - 2 * z;
+        case 11: return (xx - yy) * z;
+        case 12: return 6 * (xx * yy + xx * zz + yy * zz) - 3 * cc + 1;
+        case 13: return (2 * xx - 1) * (yy - zz);
+        default: return 2 * (xx * yy + xx * zz - 2 * yy * zz) - (2 * xx - yy - zz);
+    }
+}
+__host__ __device__ constexpr double mrt_inv_norm(int k) {
+    return k <= 2 ? 9.0 : k == 3 ? 0.75 : k == 4 ? 2.25 : k == 5 ? 1.5
+         : (k >= 6 && k <= 11) ? ((k % 2 == 0) ? 1.5 : 4.5)
+         : k == 12 ? 0.5 : k == 13 ? 2.25 : 0.75;
+}
+__host__ __device__ constexpr int mrt_group(int k) { return k <= 4 ? 0 : k == 5 ? 1 : k <= 11 ? 2 : 3; }
+
+template <typename T>
+__device__ __forceinline__ void collide_mrt19(T (&g)[19], const Rates<T> &p) {
+    using S = Stencil<19>;
+    T drho, jx, jy, jz;
+    moments0<19, T>(g, drho, jx, jy, jz);
+    const T rho = T(1) + drho;
+    const T inv = T(1) / rho;
+    const T ux = jx * inv, uy = jy * inv, uz = jz * inv;
+    const T uu15 = T(1.5) * (ux * ux + uy * uy + uz * uz);
+    T d[19];
+#pragma unroll
+    for (int q = 0; q < 19; ++q) {
+        const T w = T(S::w(q));
+        const T cu = T(S::cx(q)) * ux + T(S::cy(q)) * uy + T(S::cz(q)) * uz;
+        const T eq = w * drho + w * rho * (T(3) * cu + T(4.5) * cu * cu - uu15);
+        d[q] = g[q] - eq;
+    }
+    T a[15];
+#pragma unroll
+    for (int k = 0; k < 15; ++k) {
+        T m = T(0);
+#pragma unroll
+        for (int q = 0; q < 19; ++q) {
+            const int c = mrt_poly(k, S::cx(q), S::cy(q), S::cz(q));
+            if (c == 1) m += d[q];
+            else if (c == -1) m -= d[q];
+            else if (c != 0) m += T(c) * d[q];
+        }
+        a[k] = p.r[mrt_group(k)] * T(mrt_inv_norm(k)) * m;
+    }
+#pragma unroll
+    for (int q = 0; q < 19; ++q) {
+        T s = T(0);
+#pragma unroll
+        for (int k = 0; k < 15; ++k) {
+            const int c = mrt_poly(k, S::cx(q), S::cy(q), S::cz(q));
+            if (c == 1) s += a[k];
+            else if (c == -1) s -= a[k];
+            else if (c != 0) s += T(c) * a[k];
+        }
+        g[q] -= T(S::w(q)) * s;
+    }
+}
+
+// ---------------------------------------------------------------------------------------
+// Cumulant, D3Q27.
+// Tensor index of a direction: t = (cx+1)*9 + (cy+1)*3 + (cz+1); after the forward transform
+// slot (a,b,c) holds the central moment K_abc = sum_q (cx-ux)^a (cy-uy)^b (cz-uz)^c f_q.
+// ---------------------------------------------------------------------------------------
+__host__ __device__ constexpr int tidx(int q) { return (kC27[q][0] + 1) * 9 + (kC27[q][1] + 1) * 3 + (kC27[q][2] + 1); }
+
+// forward per-line transform: (f-, f0, f+) -> (K0, K1, K2) about velocity u
+template <typename T>
+__device__ __forceinline__ void chim_fwd(T &m, T &z, T &p, T u) {
+    const T k0 = m + z + p;
+    const T d = p - m;
+    const T s = p + m;
+    const T k1 = d - u * k0;
+    const T k2 = s - T(2) * u * d + u * u * k0;
+    m = k0;
+    z = k1;
+    p = k2;
+}
+// inverse: (K0, K1, K2) -> (f-, f0, f+)
+template <typename T>
+__device__ __forceinline__ void chim_bwd(T &m, T &z, T &p, T u) {
+    const T k0 = m, k1 = z, k2 = p;
+    const T uu = u * u;
+    const T f0 = (T(1) - uu) * k0 - T(2) * u * k1 - k2;
+    const T fp = T(0.5) * ((uu + u) * k0 + (T(2) * u + T(1)) * k1 + k2);
+    const T fm = T(0.5) * ((uu - u) * k0 + (T(2) * u - T(1)) * k1 + k2);
+    m = fm;
+    z = f0;
+    p = fp;
+}
+
+template <typename T>
+__device__ __forceinline__ void collide_cumulant27(T (&g)[27], const Rates<T> &p) {
+    using S = Stencil<27>;
+    T K[27];
+#pragma unroll
+    for (int q = 0; q < 27; ++q) K[tidx(q)] = g[q] + T(S::w(q));
+    T rho = T(0), jx = T(0), jy = T(0), jz = T(0);
+#pragma unroll
+    for (int q = 0; q < 27; ++q) {
+        rho += K[tidx(q)];
+    }
+    T drho, ax, ay, az;
+    moments0<27, T>(g, drho, ax, ay, az);
+    jx = ax;
+    jy = ay;
+    jz = az;
+    rho = T(1) + drho;
+    const T inv = T(1) / rho;
+    const T ux = jx * inv, uy = jy * inv, uz = jz * inv;
+#define KI(a, b, c) K[(a) * 9 + (b) * 3 + (c)]
+    // forward: x, then y, then z
+#pragma unroll
+    for (int b = 0; b < 3; ++b)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) chim_fwd(KI(0, b, c), KI(1, b, c), KI(2, b, c), ux);
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) chim_fwd(KI(a, 0, c), KI(a, 1, c), KI(a, 2, c), uy);
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int b = 0; b < 3; ++b) chim_fwd(KI(a, b, 0), KI(a, b, 1), KI(a, b, 2), uz);
+
+    // normalised central moments c_abc = K_abc / rho (orders 2..6; order 1 vanish)
+    const T c200 = KI(2, 0, 0) * inv, c020 = KI(0, 2, 0) * inv, c002 = KI(0, 0, 2) * inv;
+    const T c110 = KI(1, 1, 0) * inv, c101 = KI(1, 0, 1) * inv, c011 = KI(0, 1, 1) * inv;
+    const T c111 = KI(1, 1, 1) * inv;
+    const T c210 = KI(2, 1, 0) * inv, c201 = KI(2, 0, 1) * inv, c120 = KI(1, 2, 0) * inv;
+    const T c021 = KI(0, 2, 1) * inv, c102 = KI(1, 0, 2) * inv, c012 = KI(0, 1, 2) * inv;
+    const T c211 = KI(2, 1, 1) * inv, c121 = KI(1, 2, 1) * inv, c112 = KI(1, 1, 2) * inv;
+    const T c220 = KI(2, 2, 0) * inv, c202 = KI(2, 0, 2) * inv, c022 = KI(0, 2, 2) * inv;
+    const T c221 = KI(2, 2, 1) * inv, c212 = KI(2, 1, 2) * inv, c122 = KI(1, 2, 2) * inv;
+    const T c222 = KI(2, 2, 2) * inv;
+
+    // cumulants (mean zero: sum over set partitions without singleton blocks)
+    const T k211 = c211 - c200 * c011 - T(2) * c110 * c101;
+    const T k121 = c121 - c020 * c101 - T(2) * c110 * c011;
+    const T k112 = c112 - c002 * c110 - T(2) * c101 * c011;
+    const T k220 = c220 - c200 * c020 - T(2) * c110 * c110;
+    const T k202 = c202 - c200 * c002 - T(2) * c101 * c101;
+    const T k022 = c022 - c020 * c002 - T(2) * c011 * c011;
+    const T k221 = c221 - c200 * c021 - c020 * c201 - T(2) * c011 * c210 - T(2) * c101 * c120 - T(4) * c110 * c111;
+    const T k212 = c212 - c200 * c012 - c002 * c210 - T(2) * c011 * c201 - T(2) * c110 * c102 - T(4) * c101 * c111;
+    const T k122 = c122 - c020 * c102 - c002 * c120 - T(2) * c101 * c021 - T(2) * c110 * c012 - T(4) * c011 * c111;
+    const T k222 = c222 - c200 * c022 - c020 * c202 - c002 * c220
+                 - T(4) * (c110 * c112 + c101 * c121 + c011 * c211)
+                 - T(2) * (c210 * c012 + c201 * c021 + c120 * c102) - T(4) * c111 * c111
+                 + T(2) * c200 * c020 * c002
+                 + T(4) * (c200 * c011 * c011 + c020 * c101 * c101 + c002 * c110 * c110)
+                 + T(16) * c110 * c101 * c011;
+
+    // relaxation (G7): trace to 3 cs^2 = 1 with omega_bulk, deviator/off-diagonal with omega_shear,
+    // order n >= 3 to zero with omega_n
+    const T ws = p.r[0], wb = p.r[1];
+    const T r3 = T(1) - p.r[2], r4 = T(1) - p.r[3], r5 = T(1) - p.r[4], r6 = T(1) - p.r[5];
+    const T tr = c200 + c020 + c002;
+    const T trn = tr + wb * (T(1) - tr);
+    const T rs = T(1) - ws;
+    const T third = T(1) / T(3);
+    const T n200 = third * trn + rs * (c200 - third * tr);
+    const T n020 = third * trn + rs * (c020 - third * tr);
+    const T n002 = third * trn + rs * (c002 - third * tr);
+    const T n110 = rs * c110, n101 = rs * c101, n011 = rs * c011;
+    const T n111 = r3 * c111;
+    const T n210 = r3 * c210, n201 = r3 * c201, n120 = r3 * c120, n021 = r3 * c021, n102 = r3 * c102, n012 = r3 * c012;
+    const T q211 = r4 * k211, q121 = r4 * k121, q112 = r4 * k112;
+    const T q220 = r4 * k220, q202 = r4 * k202, q022 = r4 * k022;
+    const T q221 = r5 * k221, q212 = r5 * k212, q122 = r5 * k122;
+    const T q222 = r6 * k222;
+
+    // back to central moments: c = sum over partitions without singletons of prod kappa_B
+    const T m211 = q211 + n200 * n011 + T(2) * n110 * n101;
+    const T m121 = q121 + n020 * n101 + T(2) * n110 * n011;
+    const T m112 = q112 + n002 * n110 + T(2) * n101 * n011;
+    const T m220 = q220 + n200 * n020 + T(2) * n110 * n110;
+    const T m202 = q202 + n200 * n002 + T(2) * n101 * n101;
+    const T m022 = q022 + n020 * n002 + T(2) * n011 * n011;
+    const T m221 = q221 + n200 * n021 + n020 * n201 + T(2) * n011 * n210 + T(2) * n101 * n120 + T(4) * n110 * n111;
+    const T m212 = q212 + n200 * n012 + n002 * n210 + T(2) * n011 * n201 + T(2) * n110 * n102 + T(4) * n101 * n111;
+    const T m122 = q122 + n020 * n102 + n002 * n120 + T(2) * n101 * n021 + T(2) * n110 * n012 + T(4) * n011 * n111;
+    const T m222 = q222 + n200 * q022 + n020 * q202 + n002 * q220
+                 + T(4) * (n110 * q112 + n101 * q121 + n011 * q211)
+                 + T(2) * (n210 * n012 + n201 * n021 + n120 * n102) + T(4) * n111 * n111
+                 + n200 * n020 * n002
+                 + T(2) * (n200 * n011 * n011 + n020 * n101 * n101 + n002 * n110 * n110)
+                 + T(8) * n110 * n101 * n011;
+
+    KI(0, 0, 0) = rho;
+    KI(1, 0, 0) = T(0);
+    KI(0, 1, 0) = T(0);
+    KI(0, 0, 1) = T(0);
+    KI(2, 0, 0) = rho * n200; KI(0, 2, 0) = rho * n020; KI(0, 0, 2) = rho * n002;
+    KI(1, 1, 0) = rho * n110; KI(1, 0, 1) = rho * n101; KI(0, 1, 1) = rho * n011;
+    KI(1, 1, 1) = rho * n111;
+    KI(2, 1, 0) = rho * n210; KI(2, 0, 1) = rho * n201; KI(1, 2, 0) = rho * n120;
+    KI(0, 2, 1) = rho * n021; KI(1, 0, 2) = rho * n102; KI(0, 1, 2) = rho * n012;
+    KI(2, 1, 1) = rho * m211; KI(1, 2, 1) = rho * m121; KI(1, 1, 2) = rho * m112;
+    KI(2, 2, 0) = rho * m220; KI(2, 0, 2) = rho * m202; KI(0, 2, 2) = rho * m022;
+    KI(2, 2, 1) = rho * m221; KI(2, 1, 2) = rho * m212; KI(1, 2, 2) = rho * m122;
+    KI(2, 2, 2) = rho * m222;
+
+    // backward: z, y, x
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int b = 0; b < 3; ++b) chim_bwd(KI(a, b, 0), KI(a, b, 1), KI(a, b, 2), uz);
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) chim_bwd(KI(a, 0, c), KI(a, 1, c), KI(a, 2, c), uy);
+#pragma unroll
+    for (int b = 0; b < 3; ++b)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) chim_bwd(KI(0, b, c), KI(1, b, c), KI(2, b, c), ux);
+#undef KI
+#pragma unroll
+    for (int q = 0; q < 27; ++q) g[q] = K[tidx(q)] - T(S::w(q));
+}
+
+// ---------------------------------------------------------------------------------------
+// Dispatch
+// ---------------------------------------------------------------------------------------
+enum Op { OP_SRT = 0, OP_TRT = 1, OP_MRT = 2, OP_CUMULANT = 3, OP_IDENTITY = 4 };
+
+template <int Q, int OP, typename T, bool FORCE>
+__device__ __forceinline__ void collide(T (&g)[Q], const Rates<T> &p) {
+    if constexpr (OP == OP_SRT || OP == OP_TRT) {
+        collide_trt<Q, T, FORCE>(g, p);
+    } else if constexpr (OP == OP_MRT) {
+        static_assert(Q == 19, "MRT is implemented for D3Q19");
+        collide_mrt19<T>(g, p);
+    } else if constexpr (OP == OP_CUMULANT) {
+        static_assert(Q == 27, "cumulant is implemented for D3Q27");
+        collide_cumulant27<T>(g, p);
+    }
+}
+
+}  // namespace lbm

@@ -1,0 +1,100 @@
+// k_misc.cu — auxiliary kernels: initialisation, readout, halo pack/unpack, flag row mask and
+// NaN check, dispatched on (stencil, dtype).
+#include "dispatch.h"
+
+namespace lbm {
+
+#define LBM_DISPATCH(Q, dtype, ...)                                   \
+    do {                                                              \
+        if ((Q) == 19 && (dtype) == 0) { using T = double; constexpr int QQ = 19; __VA_ARGS__; } \
+        else if ((Q) == 19) { using T = float; constexpr int QQ = 19; __VA_ARGS__; }             \
+        else if ((dtype) == 0) { using T = double; constexpr int QQ = 27; __VA_ARGS__; }         \
+        else { using T = float; constexpr int QQ = 27; __VA_ARGS__; }                            \
+    } while (0)
+
+void launch_init(int Q, int dtype, const InitArgs &a, void *f0, void *f1, dim3 grid, dim3 block, cudaStream_t s) {
+    LBM_DISPATCH(Q, dtype, (k_init<QQ, T><<<grid, block, 0, s>>>(a, static_cast<T *>(f0), static_cast<T *>(f1))));
+}
+
+void launch_get_pops(int Q, int dtype, const ReadArgs &a, const void *f, double *out, dim3 grid, dim3 block, cudaStream_t s) {
+    LBM_DISPATCH(Q, dtype, (k_get_pops<QQ, T><<<grid, block, 0, s>>>(a, static_cast<const T *>(f), out)));
+}
+
+void launch_get_at(int Q, int dtype, const ReadArgs &a, const void *f, const int64_t *cells, int64_t n, int64_t first,
+                   int64_t last, double *out, cudaStream_t s) {
+    const unsigned blocks = (unsigned)((n + 127) / 128);
+    LBM_DISPATCH(Q, dtype, (k_get_at<QQ, T><<<blocks, 128, 0, s>>>(a, static_cast<const T *>(f), cells, n, first, last, out)));
+}
+
+void launch_set_pops(int Q, int dtype, const ReadArgs &a, void *f, const double *in, dim3 grid, dim3 block, cudaStream_t s) {
+    LBM_DISPATCH(Q, dtype, (k_set_pops<QQ, T><<<grid, block, 0, s>>>(a, static_cast<T *>(f), in)));
+}
+
+void launch_macro(int Q, int dtype, const ReadArgs &a, const void *f, double *rho, double *u, dim3 grid, dim3 block, cudaStream_t s) {
+    LBM_DISPATCH(Q, dtype, (k_macro<QQ, T><<<grid, block, 0, s>>>(a, static_cast<const T *>(f), rho, u)));
+}
+
+static unsigned blocks_for(int64_t n) {
+    int64_t b = (n + 255) / 256;
+    return (unsigned)(b < 148 * 16 ? (b < 1 ? 1 : b) : 148 * 16);
+}
+
+void launch_pack(int Q, int dtype, const Geo &geo, const void *f, int zs, int dir, void *out, bool out_f64, cudaStream_t s) {
+    const int64_t n = (int64_t)geo.nx * geo.ny * (Q == 19 ? 5 : 9);
+    if (out_f64) {
+        LBM_DISPATCH(Q, dtype, (k_pack<QQ, T, double><<<blocks_for(n), 256, 0, s>>>(geo, static_cast<const T *>(f), zs, dir, static_cast<double *>(out))));
+    } else {
+        LBM_DISPATCH(Q, dtype, (k_pack<QQ, T, T><<<blocks_for(n), 256, 0, s>>>(geo, static_cast<const T *>(f), zs, dir, static_cast<T *>(out))));
+    }
+}
+
+void launch_unpack(int Q, int dtype, const Geo &geo, void *f, int zs, int dir, const void *in, cudaStream_t s) {
+    const int64_t n = (int64_t)geo.nx * geo.ny * (Q == 19 ? 5 : 9);
+    LBM_DISPATCH(Q, dtype, (k_unpack<QQ, T><<<blocks_for(n), 256, 0, s>>>(geo, static_cast<T *>(f), zs, dir, static_cast<const T *>(in))));
+}
+
+__global__ void k_rowany(const Geo geo, int nplanes, const uint8_t *__restrict__ flags, uint8_t *__restrict__ rowany) {
+    const int64_t rows = (int64_t)nplanes * geo.ny;
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < rows; r += (int64_t)gridDim.x * blockDim.x) {
+        const uint8_t *row = flags + r * geo.nx;
+        uint8_t any = 0;
+        for (int x = 0; x < geo.nx; ++x) any |= (row[x] != 0);
+        rowany[r] = any;
+    }
+}
+
+__global__ void k_rowmask(const Geo geo, int nplanes, const uint8_t *__restrict__ rowany, uint8_t *__restrict__ rowmask) {
+    const int64_t rows = (int64_t)nplanes * geo.ny;
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < rows; r += (int64_t)gridDim.x * blockDim.x) {
+        const int zs = (int)(r / geo.ny), y = (int)(r % geo.ny);
+        uint8_t m = 0;
+        for (int dz = -1; dz <= 1; ++dz) {
+            int z2 = zs + dz;
+            if (geo.g) {
+                if (z2 < 0 || z2 >= nplanes) continue;  // outside the storage: never read
+            } else {
+                z2 = (z2 + nplanes) % nplanes;
+            }
+            for (int dy = -1; dy <= 1; ++dy) {
+                const int y2 = (y + dy + geo.ny) % geo.ny;
+                m |= rowany[(int64_t)z2 * geo.ny + y2];
+            }
+        }
+        rowmask[r] = m;
+    }
+}
+
+void launch_rowmask(const Geo &geo, int nplanes, const uint8_t *flags, uint8_t *tmp, uint8_t *rowmask, cudaStream_t s) {
+    const int64_t rows = (int64_t)nplanes * geo.ny;
+    k_rowany<<<blocks_for(rows), 256, 0, s>>>(geo, nplanes, flags, tmp);
+    k_rowmask<<<blocks_for(rows), 256, 0, s>>>(geo, nplanes, tmp, rowmask);
+}
+
+void launch_nan_check(int dtype, const void *f, int64_t n, int *flag, cudaStream_t s) {
+    if (dtype == 0)
+        k_nan_check<double><<<blocks_for(n), 256, 0, s>>>(static_cast<const double *>(f), n, flag);
+    else
+        k_nan_check<float><<<blocks_for(n), 256, 0, s>>>(static_cast<const float *>(f), n, flag);
+}
+
+}  // namespace lbm

@@ -1,0 +1,399 @@
+// kernels.cuh — sm_100a kernels of the fused LB time step (templates; instantiated per op in
+// k_*.cu so the heavy variants compile in parallel).
+//
+// Data layout: SoA, element (q, zs, y, x) at q*Sq + (zs*ny + y)*nx + x,
+// zs = z + g the storage plane (g = 1 ghost plane per z side in slab mode, else 0), x fastest.
+// One thread per cell along x; a block spans an x-row segment (BX threads) times BY rows; the
+// grid covers (x-blocks, y-blocks, z planes). Every population is read once and written once
+// per step: 2*q*sizeof(T) bytes per fluid cell, + 1 B of flag near walls.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "collide.cuh"
+#include "stencil.cuh"
+
+namespace lbm {
+
+struct Geo {
+    int nx, ny, nz;  // local interior extent
+    int g;           // ghost planes per z side (0: z wraps locally)
+    int64_t Sq;      // elements per q plane = nx*ny*(nz+2g)
+};
+
+struct StepArgs {
+    Geo geo;
+    int z_begin;  // first local plane (interior index) of this launch
+    int z_step;   // plane stride between blockIdx.z values (boundary-plane launches use nz-1)
+    double rates[8];
+    double F[3];
+    double uw[3];                  // UBB wall velocity; rho_w = 1 (G8)
+    const uint8_t *flags;          // storage-indexed (with ghost planes) or nullptr
+    const uint8_t *rowmask;        // per storage row (zs*ny + y): 1 if a non-fluid cell is within 1
+};
+
+template <typename T>
+__device__ __forceinline__ Rates<T> load_rates(const StepArgs &a) {
+    Rates<T> r;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) r.r[i] = T(a.rates[i]);
+#pragma unroll
+    for (int i = 0; i < 3; ++i) r.F[i] = T(a.F[i]);
+    return r;
+}
+
+template <typename T>
+__device__ __forceinline__ T ldg_stream(const T *p) {
+    return __ldg(p);
+}
+
+// Neighbour coordinates for a cell: index arrays [c+1] -> coordinate of the cell at offset c.
+struct Nbr {
+    int xs[3], ys[3], zs[3];
+};
+
+__device__ __forceinline__ Nbr neighbours(const Geo &g, int x, int y, int zs) {
+    Nbr n;
+    n.xs[1] = x;
+    n.xs[0] = (x == 0) ? g.nx - 1 : x - 1;
+    n.xs[2] = (x == g.nx - 1) ? 0 : x + 1;
+    n.ys[1] = y;
+    n.ys[0] = (y == 0) ? g.ny - 1 : y - 1;
+    n.ys[2] = (y == g.ny - 1) ? 0 : y + 1;
+    n.zs[1] = zs;
+    if (g.g) {
+        n.zs[0] = zs - 1;
+        n.zs[2] = zs + 1;
+    } else {
+        n.zs[0] = (zs == 0) ? g.nz - 1 : zs - 1;
+        n.zs[2] = (zs == g.nz - 1) ? 0 : zs + 1;
+    }
+    return n;
+}
+
+// in-plane offset (cells) of the neighbour at offset (dx,dy,dz)
+__device__ __forceinline__ uint32_t nb_off(const Geo &g, const Nbr &n, int dx, int dy, int dz) {
+    return ((uint32_t)n.zs[dz + 1] * (uint32_t)g.ny + (uint32_t)n.ys[dy + 1]) * (uint32_t)g.nx + (uint32_t)n.xs[dx + 1];
+}
+
+// =======================================================================================
+// Fused stream-pull-collide, two arrays. dst = C(S(src)) on fluid cells of planes
+// z = z_begin + blockIdx.z * z_step. Wall cells are not written.
+// =======================================================================================
+template <int Q, int OP, typename T, bool FLAGS, bool FORCE>
+__global__ void __launch_bounds__(256) k_pull(const StepArgs a, const T *__restrict__ src, T *__restrict__ dst) {
+    using S = Stencil<Q>;
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    const int y = blockIdx.y * blockDim.y + threadIdx.y;
+    if (x >= a.geo.nx || y >= a.geo.ny) return;
+    const int zs = a.z_begin + (int)blockIdx.z * a.z_step + a.geo.g;
+    const Nbr n = neighbours(a.geo, x, y, zs);
+    const uint32_t self = nb_off(a.geo, n, 0, 0, 0);
+    const int64_t Sq = a.geo.Sq;
+    bool edge = false;
+    if (FLAGS) {
+        if (a.flags[self] != 0) return;
+        edge = a.rowmask[(uint32_t)zs * (uint32_t)a.geo.ny + (uint32_t)y] != 0;
+    }
+    T g[Q];
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+        // pull from x - c_q
+        const uint32_t o = nb_off(a.geo, n, -S::cx(q), -S::cy(q), -S::cz(q));
+        if (FLAGS && edge) {
+            const uint8_t fl = a.flags[o];
+            if (fl == 0) {
+                g[q] = ldg_stream(src + q * Sq + o);
+            } else {
+                T v = ldg_stream(src + S::opp(q) * Sq + self);
+                if (fl == 2) {
+                    const double cu = S::cx(q) * a.uw[0] + S::cy(q) * a.uw[1] + S::cz(q) * a.uw[2];
+                    v += T(6.0 * S::w(q) * cu);
+                }
+                g[q] = v;
+            }
+        } else {
+            g[q] = ldg_stream(src + q * Sq + o);
+        }
+    }
+    const Rates<T> r = load_rates<T>(a);
+    collide<Q, OP, T, FORCE>(g, r);
+#pragma unroll
+    for (int q = 0; q < Q; ++q) dst[q * Sq + self] = g[q];
+}
+
+// =======================================================================================
+// AA pattern, one array, periodic (no flags, no ghosts).
+// even: read a[x](q), collide, write a[x](qbar)   (in-place, reversed storage)
+// odd : read a[x - c_q](qbar), collide, write a[x + c_q](q)
+// =======================================================================================
+template <int Q, int OP, typename T, bool FORCE>
+__global__ void __launch_bounds__(256) k_aa_even(const StepArgs a, T *__restrict__ f) {
+    using S = Stencil<Q>;
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    const int y = blockIdx.y * blockDim.y + threadIdx.y;
+    if (x >= a.geo.nx || y >= a.geo.ny) return;
+    const int zs = a.z_begin + (int)blockIdx.z * a.z_step + a.geo.g;
+    const uint32_t self = ((uint32_t)zs * (uint32_t)a.geo.ny + (uint32_t)y) * (uint32_t)a.geo.nx + (uint32_t)x;
+    const int64_t Sq = a.geo.Sq;
+    T g[Q];
+#pragma unroll
+    for (int q = 0; q < Q; ++q) g[q] = f[q * Sq + self];
+    const Rates<T> r = load_rates<T>(a);
+    collide<Q, OP, T, FORCE>(g, r);
+#pragma unroll
+    for (int q = 0; q < Q; ++q) f[S::opp(q) * Sq + self] = g[q];
+}
+
+template <int Q, int OP, typename T, bool FORCE>
+__global__ void __launch_bounds__(256) k_aa_odd(const StepArgs a, T *__restrict__ f) {
+    using S = Stencil<Q>;
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    const int y = blockIdx.y * blockDim.y + threadIdx.y;
+    if (x >= a.geo.nx || y >= a.geo.ny) return;
+    const int zs = a.z_begin + (int)blockIdx.z * a.z_step + a.geo.g;
+    const Nbr n = neighbours(a.geo, x, y, zs);
+    const int64_t Sq = a.geo.Sq;
+    T g[Q];
+#pragma unroll
+    for (int q = 0; q < Q; ++q) g[q] = f[S::opp(q) * Sq + nb_off(a.geo, n, -S::cx(q), -S::cy(q), -S::cz(q))];
+    const Rates<T> r = load_rates<T>(a);
+    collide<Q, OP, T, FORCE>(g, r);
+#pragma unroll
+    for (int q = 0; q < Q; ++q) f[q * Sq + nb_off(a.geo, n, S::cx(q), S::cy(q), S::cz(q))] = g[q];
+}
+
+// =======================================================================================
+// Initialisation: equilibrium of (rho, u) per interior cell, written to planes [zlo, zhi) of
+// the storage (ghost planes included when their global z is available, i.e. random init).
+// =======================================================================================
+struct InitArgs {
+    Geo geo;
+    int64_t nx_g, ny_g, nz_g;  // global lattice
+    int64_t z0;                // global z of local interior plane 0
+    int zlo, zhi;              // storage planes to write
+    const double *rho;         // interior cells (mode 0)
+    const double *u;           // component d of cell i at u[d * ustride + i]
+    int64_t ustride;
+    int mode;                  // 0 = arrays, 1 = random (G13)
+    uint64_t seed;
+    double rho_amp, u_amp, profile_amp;
+    int profile;
+    int product_eq;            // cumulant: product equilibrium (G2)
+};
+
+__device__ __forceinline__ uint64_t splitmix64(uint64_t k) {
+    uint64_t z = k + 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+// U(a, b) = a + (b - a) r, r = top 53 bits * 2^-53, no FMA contraction (matches the host generator)
+__device__ __forceinline__ double uniform_g13(uint64_t seed, uint64_t ig, int k, double a, double b) {
+    const uint64_t key = (seed << 40) ^ (4ull * ig + (uint64_t)k);
+    const double r = (double)(splitmix64(key) >> 11) * 0x1p-53;
+    return __dadd_rn(a, __dmul_rn(__dsub_rn(b, a), r));
+}
+
+template <int Q, typename T>
+__global__ void k_init(const InitArgs a, T *__restrict__ f0, T *__restrict__ f1) {
+    using S = Stencil<Q>;
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    const int y = blockIdx.y * blockDim.y + threadIdx.y;
+    if (x >= a.geo.nx || y >= a.geo.ny) return;
+    const int zs = a.zlo + (int)blockIdx.z;
+    if (zs >= a.zhi) return;
+    const int zl = zs - a.geo.g;  // local interior index (may be -1 or nz for ghosts)
+    double rho, ux, uy, uz;
+    if (a.mode == 0) {
+        const int64_t i = ((int64_t)zl * a.geo.ny + y) * a.geo.nx + x;
+        rho = a.rho[i];
+        ux = a.u[i];
+        uy = a.u[a.ustride + i];
+        uz = a.u[2 * a.ustride + i];
+    } else {
+        int64_t zg = a.z0 + zl;
+        zg = ((zg % a.nz_g) + a.nz_g) % a.nz_g;
+        const uint64_t ig = (uint64_t)x + (uint64_t)a.nx_g * ((uint64_t)y + (uint64_t)a.ny_g * (uint64_t)zg);
+        rho = (a.rho_amp != 0.0) ? __dadd_rn(1.0, uniform_g13(a.seed, ig, 0, -a.rho_amp, a.rho_amp)) : 1.0;
+        ux = (a.u_amp != 0.0) ? uniform_g13(a.seed, ig, 1, -a.u_amp, a.u_amp) : 0.0;
+        uy = (a.u_amp != 0.0) ? uniform_g13(a.seed, ig, 2, -a.u_amp, a.u_amp) : 0.0;
+        uz = (a.u_amp != 0.0) ? uniform_g13(a.seed, ig, 3, -a.u_amp, a.u_amp) : 0.0;
+        if (a.profile == 1) {
+            const double s = sin(__ddiv_rn(__dmul_rn(2.0 * 3.141592653589793, (double)zg), (double)a.nz_g));
+            ux = __dadd_rn(__dmul_rn(a.profile_amp, s), ux);
+        }
+    }
+    const uint32_t self = ((uint32_t)zs * (uint32_t)a.geo.ny + (uint32_t)y) * (uint32_t)a.geo.nx + (uint32_t)x;
+    const double drho = rho - 1.0;
+    const double uu15 = 1.5 * (ux * ux + uy * uy + uz * uz);
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+        double gq;
+        if (a.product_eq) {
+            double v = rho;
+            const double uc[3] = {ux, uy, uz};
+            const int c[3] = {S::cx(q), S::cy(q), S::cz(q)};
+#pragma unroll
+            for (int d = 0; d < 3; ++d)
+                v *= (c[d] == 0) ? (2.0 / 3.0 - uc[d] * uc[d]) : 0.5 * (1.0 / 3.0 + uc[d] * uc[d] + c[d] * uc[d]);
+            gq = v - S::w(q);
+        } else {
+            const double cu = S::cx(q) * ux + S::cy(q) * uy + S::cz(q) * uz;
+            gq = S::w(q) * drho + S::w(q) * rho * (3.0 * cu + 4.5 * cu * cu - uu15);
+        }
+        f0[q * a.geo.Sq + self] = T(gq);
+        if (f1) f1[q * a.geo.Sq + self] = T(gq);
+    }
+}
+
+// =======================================================================================
+// Readout: canonical populations / macroscopic values of interior cells.
+// For AA with odd parity the state is gathered: F_q(y) = a[y - c_q](qbar).
+// =======================================================================================
+struct ReadArgs {
+    Geo geo;
+    int aa_odd;      // 1: AA array after an odd number of steps
+    int raw;         // 1: stored values, no +w, no gather
+    double fsign;    // +1 pre-collision state, -1 post-collision (pull)
+    double F[3];
+};
+
+template <int Q, typename T>
+__device__ __forceinline__ T read_canonical(const ReadArgs &a, const T *f, int x, int y, int zs, int q) {
+    using S = Stencil<Q>;
+    if (a.aa_odd && !a.raw) {
+        const Nbr n = neighbours(a.geo, x, y, zs);
+        return f[S::opp(q) * a.geo.Sq + nb_off(a.geo, n, -S::cx(q), -S::cy(q), -S::cz(q))];
+    }
+    const uint32_t self = ((uint32_t)zs * (uint32_t)a.geo.ny + (uint32_t)y) * (uint32_t)a.geo.nx + (uint32_t)x;
+    return f[q * a.geo.Sq + self];
+}
+
+template <int Q, typename T>
+__global__ void k_get_pops(const ReadArgs a, const T *__restrict__ f, double *__restrict__ out) {
+    using S = Stencil<Q>;
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    const int y = blockIdx.y * blockDim.y + threadIdx.y;
+    if (x >= a.geo.nx || y >= a.geo.ny) return;
+    const int zl = blockIdx.z;
+    const int zs = zl + a.geo.g;
+    const int64_t nc = (int64_t)a.geo.nx * a.geo.ny * a.geo.nz;
+    const int64_t i = ((int64_t)zl * a.geo.ny + y) * a.geo.nx + x;
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+        const double v = (double)read_canonical<Q, T>(a, f, x, y, zs, q);
+        out[q * nc + i] = a.raw ? v : v + S::w(q);
+    }
+}
+
+template <int Q, typename T>
+__global__ void k_get_at(const ReadArgs a, const T *__restrict__ f, const int64_t *__restrict__ cells, int64_t n,
+                         int64_t first, int64_t last, double *__restrict__ out) {
+    using S = Stencil<Q>;
+    const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    const int64_t c = cells[k];
+    if (c < first || c >= last) return;  // another slab's cell
+    const int64_t i = c - first;
+    const int x = (int)(i % a.geo.nx);
+    const int y = (int)((i / a.geo.nx) % a.geo.ny);
+    const int zl = (int)(i / ((int64_t)a.geo.nx * a.geo.ny));
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+        const double v = (double)read_canonical<Q, T>(a, f, x, y, zl + a.geo.g, q);
+        out[q * n + k] = a.raw ? v : v + S::w(q);
+    }
+}
+
+template <int Q, typename T>
+__global__ void k_set_pops(const ReadArgs a, T *__restrict__ f, const double *__restrict__ in) {
+    using S = Stencil<Q>;
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    const int y = blockIdx.y * blockDim.y + threadIdx.y;
+    if (x >= a.geo.nx || y >= a.geo.ny) return;
+    const int zl = blockIdx.z;
+    const uint32_t self = ((uint32_t)(zl + a.geo.g) * (uint32_t)a.geo.ny + (uint32_t)y) * (uint32_t)a.geo.nx + (uint32_t)x;
+    const int64_t nc = (int64_t)a.geo.nx * a.geo.ny * a.geo.nz;
+    const int64_t i = ((int64_t)zl * a.geo.ny + y) * a.geo.nx + x;
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+        const double v = in[q * nc + i];
+        f[q * a.geo.Sq + self] = a.raw ? T(v) : T(v - S::w(q));
+    }
+}
+
+template <int Q, typename T>
+__global__ void k_macro(const ReadArgs a, const T *__restrict__ f, double *__restrict__ rho_out, double *__restrict__ u_out) {
+    using S = Stencil<Q>;
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    const int y = blockIdx.y * blockDim.y + threadIdx.y;
+    if (x >= a.geo.nx || y >= a.geo.ny) return;
+    const int zl = blockIdx.z;
+    const int zs = zl + a.geo.g;
+    double drho = 0, jx = 0, jy = 0, jz = 0;
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+        const double v = (double)read_canonical<Q, T>(a, f, x, y, zs, q);
+        drho += v;
+        jx += S::cx(q) * v;
+        jy += S::cy(q) * v;
+        jz += S::cz(q) * v;
+    }
+    const double rho = 1.0 + drho;
+    const int64_t nc = (int64_t)a.geo.nx * a.geo.ny * a.geo.nz;
+    const int64_t i = ((int64_t)zl * a.geo.ny + y) * a.geo.nx + x;
+    rho_out[i] = rho;
+    u_out[i] = (jx + a.fsign * 0.5 * a.F[0]) / rho;
+    u_out[nc + i] = (jy + a.fsign * 0.5 * a.F[1]) / rho;
+    u_out[2 * nc + i] = (jz + a.fsign * 0.5 * a.F[2]) / rho;
+}
+
+// =======================================================================================
+// Halo: pack the crossing populations of storage plane zs (canonical order: q ascending over
+// {q : c_qz = dir}, then y, then x) into a contiguous buffer, and the inverse.
+// =======================================================================================
+template <int Q, typename T, typename OutT>
+__global__ void k_pack(const Geo geo, const T *__restrict__ f, int zs, int dir, OutT *__restrict__ out) {
+    const int64_t plane = (int64_t)geo.nx * geo.ny;
+    const int64_t n = plane * Stencil<Q>::kCross;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int k = (int)(i / plane);
+        const int64_t r = i - k * plane;
+        const int q = crossing_dir<Q>(dir, k);
+        out[i] = OutT(f[q * geo.Sq + zs * plane + r]);
+    }
+}
+
+template <int Q, typename T>
+__global__ void k_unpack(const Geo geo, T *__restrict__ f, int zs, int dir, const T *__restrict__ in) {
+    const int64_t plane = (int64_t)geo.nx * geo.ny;
+    const int64_t n = plane * Stencil<Q>::kCross;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int k = (int)(i / plane);
+        const int64_t r = i - k * plane;
+        const int q = crossing_dir<Q>(dir, k);
+        f[q * geo.Sq + zs * plane + r] = in[i];
+    }
+}
+
+// =======================================================================================
+// Flag preprocessing and diagnostics
+// =======================================================================================
+// rowany[zs*ny + y] = 1 if any cell of the storage row is not fluid
+__global__ void k_rowany(const Geo geo, int nplanes, const uint8_t *__restrict__ flags, uint8_t *__restrict__ rowany);
+// rowmask = OR of rowany over the 3x3 (dy, dz) neighbourhood (y wraps; z wraps without ghosts)
+__global__ void k_rowmask(const Geo geo, int nplanes, const uint8_t *__restrict__ rowany, uint8_t *__restrict__ rowmask);
+
+template <typename T>
+__global__ void k_nan_check(const T *__restrict__ f, int64_t n, int *__restrict__ flag) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const T v = f[i];
+        if (v != v) {
+            *flag = 1;
+            return;
+        }
+    }
+}
+
+}  // namespace lbm

@@ -1,0 +1,965 @@
+// runtime.cu — C-ABI runtime of the LB library (include/lbm.h): configuration validation,
+// device allocation, flag preprocessing, the time-step scheduler (single slab, loopback slabs,
+// NCCL slabs with halo exchange overlapped with the interior update), CUDA-graph capture,
+// readout and error handling. No C++ exception crosses the ABI.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "../../include/lbm.h"
+#include "dispatch.h"
+
+using namespace lbm;
+
+namespace {
+
+struct Slab {
+    int64_t z0 = 0;       // global z of local interior plane 0
+    int nz = 0;           // interior planes
+    void *pdf[2] = {nullptr, nullptr};
+    uint8_t *flags = nullptr;    // storage-indexed, with ghost planes
+    uint8_t *rowmask = nullptr;  // per storage row
+    void *halo[4] = {nullptr, nullptr, nullptr, nullptr};  // packed mode: send up, send down, recv below, recv above
+    int cur = 0;          // index of the array holding the current state (pull)
+};
+
+struct Timing {
+    bool on = false;
+    std::vector<cudaEvent_t> ev;  // pairs
+};
+
+}  // namespace
+
+struct lbm_handle_s {
+    lbm_config cfg{};
+    int Q = 19, dtype = 0, esize = 8, op = 0;
+    int g = 0;  // ghost planes per side
+    int64_t nx = 0, ny = 0, nzg = 0;
+    std::vector<Slab> slabs;
+    cudaStream_t stream = nullptr, comm_stream = nullptr;
+    bool own_stream = false;
+    cudaEvent_t ev_bnd = nullptr, ev_x = nullptr;
+    ncclComm_t comm = nullptr;
+    int rank = 0, nranks = 1, up = 0, down = 0;
+    bool have_flags = false, have_force = false;
+    PullLaunch pull = nullptr;
+    AALaunch aa = nullptr;
+    StepArgs base{};
+    int64_t steps = 0;
+    int aa_parity = 0;
+    cudaGraphExec_t graph = nullptr;
+    int graph_parity = -1;
+    int64_t launches = 0;
+    int *d_nanflag = nullptr;
+    double *scratch = nullptr;
+    size_t scratch_bytes = 0;
+    Timing timing;
+    std::string err;
+    dim3 block;
+};
+
+namespace {
+
+thread_local std::string g_create_error;
+
+int fail(lbm_handle h, int code, const std::string &msg) {
+    if (h) h->err = msg;
+    else g_create_error = msg;
+    return code;
+}
+
+#define CUDA_TRY(h, expr)                                                                     \
+    do {                                                                                      \
+        cudaError_t _e = (expr);                                                              \
+        if (_e != cudaSuccess)                                                                \
+            return fail((h), _e == cudaErrorMemoryAllocation ? LBM_EOOM : LBM_ECUDA,          \
+                        std::string(#expr) + ": " + cudaGetErrorString(_e));                  \
+    } while (0)
+
+#define NCCL_TRY(h, expr)                                                                     \
+    do {                                                                                      \
+        ncclResult_t _r = (expr);                                                             \
+        if (_r != ncclSuccess) return fail((h), LBM_ENCCL, std::string(#expr) + ": " + ncclGetErrorString(_r)); \
+    } while (0)
+
+int crossing(int Q, int dir, int *out) {
+    int n = 0;
+    for (int q = 0; q < Q; ++q)
+        if (kC27[q][2] == dir) out[n++] = q;
+    return n;
+}
+
+Geo geo_of(const lbm_handle_s *h, const Slab &s) {
+    Geo g;
+    g.nx = (int)h->nx;
+    g.ny = (int)h->ny;
+    g.nz = s.nz;
+    g.g = h->g;
+    g.Sq = (int64_t)h->nx * h->ny * (s.nz + 2 * h->g);
+    return g;
+}
+
+dim3 grid_for(const lbm_handle_s *h, int nplanes) {
+    return dim3((unsigned)((h->nx + h->block.x - 1) / h->block.x), (unsigned)((h->ny + h->block.y - 1) / h->block.y),
+                (unsigned)nplanes);
+}
+
+size_t plane_bytes(const lbm_handle_s *h) { return (size_t)h->nx * h->ny * h->esize; }
+
+char *qplane(const lbm_handle_s *h, const Slab &s, int arr, int q, int zs) {
+    const Geo g = geo_of(h, s);
+    return static_cast<char *>(s.pdf[arr]) + ((size_t)q * g.Sq + (size_t)zs * h->nx * h->ny) * h->esize;
+}
+
+// ---- kernel launch helpers (counted, optionally timed) ------------------------------
+void tbegin(lbm_handle_s *h, cudaStream_t s) {
+    if (!h->timing.on) return;
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, s);
+    h->timing.ev.push_back(e);
+}
+void tend(lbm_handle_s *h, cudaStream_t s) { tbegin(h, s); }
+
+void launch_pull_range(lbm_handle_s *h, Slab &s, int z_begin, int nplanes, int z_step, cudaStream_t st) {
+    if (nplanes <= 0) return;
+    StepArgs a = h->base;
+    a.geo = geo_of(h, s);
+    a.z_begin = z_begin;
+    a.z_step = z_step;
+    a.flags = s.flags;
+    a.rowmask = s.rowmask;
+    tbegin(h, st);
+    h->pull(a, s.pdf[s.cur], s.pdf[1 - s.cur], grid_for(h, nplanes), h->block, st);
+    tend(h, st);
+    h->launches++;
+}
+
+void launch_aa(lbm_handle_s *h, Slab &s, int odd, cudaStream_t st) {
+    StepArgs a = h->base;
+    a.geo = geo_of(h, s);
+    a.z_begin = 0;
+    a.z_step = 1;
+    tbegin(h, st);
+    h->aa(a, s.pdf[0], odd, grid_for(h, s.nz), h->block, st);
+    tend(h, st);
+    h->launches++;
+}
+
+// ---- halo exchange ------------------------------------------------------------------
+// After an update that wrote array `arr` of every slab: the crossing populations of the
+// boundary planes go into the neighbours' ghost planes of the same array.
+int exchange_loopback(lbm_handle_s *h, int arr_sel_cur, cudaStream_t st) {
+    const int P = (int)h->slabs.size();
+    int up[9], dn[9];
+    const int nu = crossing(h->Q, +1, up), nd = crossing(h->Q, -1, dn);
+    for (int r = 0; r < P; ++r) {
+        Slab &s = h->slabs[r];
+        Slab &su = h->slabs[(r + 1) % P];
+        Slab &sd = h->slabs[(r - 1 + P) % P];
+        const int arr = arr_sel_cur ? s.cur : 1 - s.cur;
+        const int arru = arr_sel_cur ? su.cur : 1 - su.cur;
+        const int arrd = arr_sel_cur ? sd.cur : 1 - sd.cur;
+        if (h->cfg.halo_mode == LBM_HALO_PACKED) {
+            Geo g = geo_of(h, s), gu = geo_of(h, su), gd = geo_of(h, sd);
+            launch_pack(h->Q, h->dtype, g, s.pdf[arr], s.nz, +1, s.halo[0], false, st);
+            launch_unpack(h->Q, h->dtype, gu, su.pdf[arru], 0, +1, s.halo[0], st);
+            launch_pack(h->Q, h->dtype, g, s.pdf[arr], 1, -1, s.halo[1], false, st);
+            launch_unpack(h->Q, h->dtype, gd, sd.pdf[arrd], sd.nz + 1, -1, s.halo[1], st);
+            h->launches += 4;
+        } else {
+            for (int k = 0; k < nu; ++k)
+                CUDA_TRY(h, cudaMemcpyAsync(qplane(h, su, arru, up[k], 0), qplane(h, s, arr, up[k], s.nz), plane_bytes(h),
+                                            cudaMemcpyDeviceToDevice, st));
+            for (int k = 0; k < nd; ++k)
+                CUDA_TRY(h, cudaMemcpyAsync(qplane(h, sd, arrd, dn[k], sd.nz + 1), qplane(h, s, arr, dn[k], 1), plane_bytes(h),
+                                            cudaMemcpyDeviceToDevice, st));
+        }
+    }
+    return LBM_OK;
+}
+
+int exchange_nccl(lbm_handle_s *h, int arr_sel_cur, cudaStream_t st) {
+    Slab &s = h->slabs[0];
+    const int arr = arr_sel_cur ? s.cur : 1 - s.cur;
+    const ncclDataType_t dt = h->dtype == 0 ? ncclDouble : ncclFloat;
+    const size_t plane = (size_t)h->nx * h->ny;
+    int up[9], dn[9];
+    const int nu = crossing(h->Q, +1, up), nd = crossing(h->Q, -1, dn);
+    const Geo g = geo_of(h, s);
+    if (h->cfg.halo_mode == LBM_HALO_PACKED) {
+        launch_pack(h->Q, h->dtype, g, s.pdf[arr], s.nz, +1, s.halo[0], false, st);
+        launch_pack(h->Q, h->dtype, g, s.pdf[arr], 1, -1, s.halo[1], false, st);
+        h->launches += 2;
+        NCCL_TRY(h, ncclGroupStart());
+        NCCL_TRY(h, ncclSend(s.halo[0], plane * nu, dt, h->up, h->comm, st));
+        NCCL_TRY(h, ncclRecv(s.halo[2], plane * nu, dt, h->down, h->comm, st));
+        NCCL_TRY(h, ncclSend(s.halo[1], plane * nd, dt, h->down, h->comm, st));
+        NCCL_TRY(h, ncclRecv(s.halo[3], plane * nd, dt, h->up, h->comm, st));
+        NCCL_TRY(h, ncclGroupEnd());
+        launch_unpack(h->Q, h->dtype, g, s.pdf[arr], 0, +1, s.halo[2], st);
+        launch_unpack(h->Q, h->dtype, g, s.pdf[arr], s.nz + 1, -1, s.halo[3], st);
+        h->launches += 2;
+    } else {
+        // zero-copy: each crossing population's boundary plane is one contiguous nx*ny run
+        NCCL_TRY(h, ncclGroupStart());
+        for (int k = 0; k < nu; ++k) NCCL_TRY(h, ncclSend(qplane(h, s, arr, up[k], s.nz), plane, dt, h->up, h->comm, st));
+        for (int k = 0; k < nu; ++k) NCCL_TRY(h, ncclRecv(qplane(h, s, arr, up[k], 0), plane, dt, h->down, h->comm, st));
+        for (int k = 0; k < nd; ++k) NCCL_TRY(h, ncclSend(qplane(h, s, arr, dn[k], 1), plane, dt, h->down, h->comm, st));
+        for (int k = 0; k < nd; ++k) NCCL_TRY(h, ncclRecv(qplane(h, s, arr, dn[k], s.nz + 1), plane, dt, h->up, h->comm, st));
+        NCCL_TRY(h, ncclGroupEnd());
+    }
+    return LBM_OK;
+}
+
+// exchange the CURRENT state's ghost planes (after init / set_populations), synchronously ordered on stream
+int exchange_current(lbm_handle_s *h) {
+    if (h->g == 0) return LBM_OK;
+    if (h->nranks > 1) return exchange_nccl(h, 1, h->stream);
+    return exchange_loopback(h, 1, h->stream);
+}
+
+// ---- one time step ------------------------------------------------------------------
+int step_once(lbm_handle_s *h) {
+    cudaStream_t st = h->stream;
+    if (h->cfg.pattern == LBM_AA) {
+        Slab &s = h->slabs[0];
+        launch_aa(h, s, h->aa_parity, st);
+        h->aa_parity ^= 1;
+        return LBM_OK;
+    }
+    if (h->g == 0) {
+        Slab &s = h->slabs[0];
+        launch_pull_range(h, s, 0, s.nz, 1, st);
+        s.cur ^= 1;
+        return LBM_OK;
+    }
+    if (h->nranks == 1) {
+        // loopback slabs on one GPU, one stream: boundary planes, exchange, interior
+        for (Slab &s : h->slabs) launch_pull_range(h, s, 0, 2, s.nz - 1, st);
+        int rc = exchange_loopback(h, 0, st);
+        if (rc) return rc;
+        for (Slab &s : h->slabs) launch_pull_range(h, s, 1, s.nz - 2, 1, st);
+        for (Slab &s : h->slabs) s.cur ^= 1;
+        return LBM_OK;
+    }
+    // NCCL: boundary planes -> event -> (comm stream) exchange || (compute stream) interior
+    Slab &s = h->slabs[0];
+    launch_pull_range(h, s, 0, 2, s.nz - 1, st);
+    CUDA_TRY(h, cudaEventRecord(h->ev_bnd, st));
+    CUDA_TRY(h, cudaStreamWaitEvent(h->comm_stream, h->ev_bnd, 0));
+    int rc = exchange_nccl(h, 0, h->comm_stream);
+    if (rc) return rc;
+    CUDA_TRY(h, cudaEventRecord(h->ev_x, h->comm_stream));
+    launch_pull_range(h, s, 1, s.nz - 2, 1, st);
+    CUDA_TRY(h, cudaStreamWaitEvent(st, h->ev_x, 0));  // next step's boundary planes need the ghosts
+    s.cur ^= 1;
+    return LBM_OK;
+}
+
+bool graph_ok(const lbm_handle_s *h) { return h->cfg.use_graph && h->g == 0 && h->slabs.size() == 1 && !h->timing.on; }
+
+int run_graph_cycle(lbm_handle_s *h) {
+    // one cycle = two steps (pull: src->dst->src; AA: even+odd), replayed; state returns to the same slots
+    if (!h->graph || h->graph_parity != (h->cfg.pattern == LBM_AA ? h->aa_parity : h->slabs[0].cur)) {
+        if (h->graph) {
+            cudaGraphExecDestroy(h->graph);
+            h->graph = nullptr;
+        }
+        cudaGraph_t gr;
+        const int par = h->cfg.pattern == LBM_AA ? h->aa_parity : h->slabs[0].cur;
+        CUDA_TRY(h, cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
+        const int64_t l0 = h->launches;
+        step_once(h);
+        step_once(h);
+        cudaError_t e = cudaStreamEndCapture(h->stream, &gr);
+        if (e != cudaSuccess) return fail(h, LBM_ECUDA, std::string("graph capture: ") + cudaGetErrorString(e));
+        CUDA_TRY(h, cudaGraphInstantiate(&h->graph, gr, 0));
+        cudaGraphDestroy(gr);
+        h->launches = l0;  // the capture did not launch
+        h->graph_parity = par;
+    }
+    CUDA_TRY(h, cudaGraphLaunch(h->graph, h->stream));
+    h->launches += 2;
+    return LBM_OK;
+}
+
+int validate(const lbm_config *c) {
+    if (!c) return fail(nullptr, LBM_EINVAL, "null config");
+    if (c->stencil != 19 && c->stencil != 27) return fail(nullptr, LBM_EINVAL, "stencil must be 19 or 27");
+    if (c->collision < 0 || c->collision > 4) return fail(nullptr, LBM_EINVAL, "bad collision");
+    if (c->dtype != LBM_F64 && c->dtype != LBM_F32) return fail(nullptr, LBM_EINVAL, "bad dtype");
+    if (c->pattern != LBM_PULL && c->pattern != LBM_AA) return fail(nullptr, LBM_EINVAL, "bad pattern");
+    const int need[] = {1, 2, 1, 1, 0};
+    if (c->n_rates < need[c->collision] || c->n_rates > 8) return fail(nullptr, LBM_EINVAL, "wrong number of rates");
+    for (int i = 0; i < c->n_rates; ++i)
+        if (!(c->rates[i] > 0.0 && c->rates[i] < 2.0)) return fail(nullptr, LBM_EINVAL, "relaxation rate outside (0, 2)");
+    for (int d = 0; d < 3; ++d)
+        if (c->global[d] < 1) return fail(nullptr, LBM_EINVAL, "empty lattice");
+    if (c->nranks < 1 || c->rank < 0 || c->rank >= c->nranks) return fail(nullptr, LBM_EINVAL, "bad rank/nranks");
+    if (c->n_local_slabs < 0) return fail(nullptr, LBM_EINVAL, "bad n_local_slabs");
+    if (c->nranks > 1 && c->n_local_slabs > 1) return fail(nullptr, LBM_EINVAL, "loopback slabs require nranks == 1");
+    const int P = c->nranks > 1 ? c->nranks : (c->n_local_slabs > 1 ? c->n_local_slabs : 1);
+    if (c->global[2] % P != 0) return fail(nullptr, LBM_EINVAL, "nz % nranks != 0");
+    if (P > 1 && c->global[2] / P < 2) return fail(nullptr, LBM_EINVAL, "slabs need at least 2 planes");
+    if (c->nranks > 1 && !c->nccl_id) return fail(nullptr, LBM_EINVAL, "nranks > 1 needs an nccl_id");
+    const int64_t planes = c->global[2] / P + (P > 1 ? 2 : 0);
+    if ((double)c->global[0] * c->global[1] * planes >= 2147483647.0)
+        return fail(nullptr, LBM_EINVAL, "slab too large for 32-bit in-plane offsets (split it over more slabs)");
+    const bool force = c->force[0] != 0 || c->force[1] != 0 || c->force[2] != 0;
+    if (c->collision == LBM_MRT && c->stencil != 19) return fail(nullptr, LBM_EUNSUPPORTED, "MRT is implemented for D3Q19");
+    if (c->collision == LBM_CUMULANT && c->stencil != 27) return fail(nullptr, LBM_EUNSUPPORTED, "cumulant is implemented for D3Q27");
+    if (force && (c->collision == LBM_MRT || c->collision == LBM_CUMULANT))
+        return fail(nullptr, LBM_EUNSUPPORTED, "forcing is implemented for SRT/TRT");
+    if (c->pattern == LBM_AA && c->flags) return fail(nullptr, LBM_EUNSUPPORTED, "AA with boundary flags is not implemented yet");
+    if (c->pattern == LBM_AA && P > 1) return fail(nullptr, LBM_EUNSUPPORTED, "AA with slab decomposition is not implemented yet");
+    // a non-periodic axis must carry wall cells on both faces
+    for (int d = 0; d < 3; ++d) {
+        if (c->periodic[d]) continue;
+        if (!c->flags) return fail(nullptr, LBM_EINVAL, "non-periodic axis without a flag field");
+        const int64_t n[3] = {c->global[0], c->global[1], c->global[2]};
+        for (int side = 0; side < 2; ++side) {
+            const int64_t fix = side ? n[d] - 1 : 0;
+            const int a1 = (d + 1) % 3, a2 = (d + 2) % 3;
+            for (int64_t i = 0; i < n[a1]; ++i)
+                for (int64_t j = 0; j < n[a2]; ++j) {
+                    int64_t co[3];
+                    co[d] = fix;
+                    co[a1] = i;
+                    co[a2] = j;
+                    if (c->flags[co[0] + n[0] * (co[1] + n[1] * co[2])] == 0)
+                        return fail(nullptr, LBM_EINVAL, "non-periodic axis has fluid cells on its face");
+                }
+        }
+    }
+    return LBM_OK;
+}
+
+int ensure_scratch(lbm_handle h, size_t bytes) {
+    if (h->scratch_bytes >= bytes) return LBM_OK;
+    if (h->scratch) cudaFree(h->scratch);
+    h->scratch = nullptr;
+    h->scratch_bytes = 0;
+    CUDA_TRY(h, cudaMalloc(&h->scratch, bytes));
+    h->scratch_bytes = bytes;
+    return LBM_OK;
+}
+
+int64_t local_cells(const lbm_handle_s *h) {
+    int64_t n = 0;
+    for (const Slab &s : h->slabs) n += (int64_t)h->nx * h->ny * s.nz;
+    return n;
+}
+
+}  // namespace
+
+// =========================================================================================
+// C ABI
+// =========================================================================================
+extern "C" {
+
+void lbm_config_default(lbm_config *c) {
+    std::memset(c, 0, sizeof(*c));
+    c->stencil = LBM_D3Q19;
+    c->collision = LBM_SRT;
+    c->dtype = LBM_F64;
+    c->pattern = LBM_PULL;
+    c->n_rates = 1;
+    c->rates[0] = 1.8;
+    c->global[0] = c->global[1] = c->global[2] = 32;
+    c->periodic[0] = c->periodic[1] = c->periodic[2] = 1;
+    c->nranks = 1;
+    c->n_local_slabs = 1;
+}
+
+const char *lbm_version(void) { return "b200-lbm 0.1 (sm_100a)"; }
+
+const char *lbm_strerror(int s) {
+    switch (s) {
+        case LBM_OK: return "ok";
+        case LBM_EINVAL: return "invalid argument";
+        case LBM_EUNSUPPORTED: return "unsupported configuration";
+        case LBM_ECUDA: return "CUDA error";
+        case LBM_ENCCL: return "NCCL error";
+        case LBM_ENAN: return "NaN in populations";
+        case LBM_EOOM: return "out of device memory";
+        default: return "unknown status";
+    }
+}
+
+const char *lbm_last_error(lbm_handle h) { return h ? h->err.c_str() : g_create_error.c_str(); }
+
+int lbm_slab_plan(int64_t nz, int32_t nranks, int32_t rank, int64_t out[4]) {
+    if (nranks < 1 || rank < 0 || rank >= nranks || nz % nranks != 0 || (nranks > 1 && nz / nranks < 2)) return LBM_EINVAL;
+    const int64_t nzl = nz / nranks;
+    out[0] = rank * nzl;
+    out[1] = nzl;
+    out[2] = (rank - 1 + nranks) % nranks;
+    out[3] = (rank + 1) % nranks;
+    return LBM_OK;
+}
+
+int lbm_crossing_directions(int32_t stencil, int32_t dir, int32_t *q_out) {
+    if ((stencil != 19 && stencil != 27) || (dir != 1 && dir != -1)) return LBM_EINVAL;
+    int tmp[9];
+    const int n = crossing(stencil, dir, tmp);
+    for (int i = 0; i < n; ++i) q_out[i] = tmp[i];
+    return n;
+}
+
+int lbm_stencil_table(int32_t stencil, int32_t *c_out, double *w_out) {
+    if (stencil != 19 && stencil != 27) return LBM_EINVAL;
+    for (int q = 0; q < stencil; ++q) {
+        for (int d = 0; d < 3; ++d) c_out[3 * q + d] = kC27[q][d];
+        w_out[q] = stencil == 19 ? Stencil<19>::w(q) : Stencil<27>::w(q);
+    }
+    return stencil;
+}
+
+int lbm_nccl_unique_id(uint8_t out[128]) {
+    ncclUniqueId id;
+    if (ncclGetUniqueId(&id) != ncclSuccess) return LBM_ENCCL;
+    static_assert(sizeof(id) == 128, "ncclUniqueId is 128 bytes");
+    std::memcpy(out, &id, 128);
+    return LBM_OK;
+}
+
+int lbm_create(const lbm_config *cfg, lbm_handle *out) {
+    if (!out) return LBM_EINVAL;
+    *out = nullptr;
+    int rc = validate(cfg);
+    if (rc) return rc;
+    std::unique_ptr<lbm_handle_s> hp(new (std::nothrow) lbm_handle_s());
+    if (!hp) return LBM_EOOM;
+    lbm_handle h = hp.get();
+    h->cfg = *cfg;
+    h->cfg.flags = nullptr;
+    h->cfg.nccl_id = nullptr;
+    h->Q = cfg->stencil;
+    h->dtype = cfg->dtype;
+    h->esize = cfg->dtype == LBM_F64 ? 8 : 4;
+    h->op = cfg->collision;
+    h->nx = cfg->global[0];
+    h->ny = cfg->global[1];
+    h->nzg = cfg->global[2];
+    h->rank = cfg->nranks > 1 ? cfg->rank : 0;
+    h->nranks = cfg->nranks;
+    const int P = cfg->nranks > 1 ? cfg->nranks : (cfg->n_local_slabs > 1 ? cfg->n_local_slabs : 1);
+    h->g = P > 1 ? 1 : 0;
+    h->have_flags = cfg->flags != nullptr;
+    h->have_force = cfg->force[0] != 0 || cfg->force[1] != 0 || cfg->force[2] != 0;
+
+    // kernel selection (SRT = TRT with equal rates)
+    const bool force = h->have_force;
+    if (cfg->pattern == LBM_PULL) {
+        switch (cfg->collision) {
+            case LBM_SRT:
+            case LBM_TRT: h->pull = select_pull_trt(h->Q, h->dtype, h->have_flags, force); break;
+            case LBM_MRT: h->pull = select_pull_mrt(h->Q, h->dtype, h->have_flags, force); break;
+            case LBM_CUMULANT: h->pull = select_pull_cumulant(h->Q, h->dtype, h->have_flags, force); break;
+            default: h->pull = select_pull_identity(h->Q, h->dtype, h->have_flags, force); break;
+        }
+        if (!h->pull) return fail(nullptr, LBM_EUNSUPPORTED, "no kernel instantiated for this combination");
+    } else {
+        switch (cfg->collision) {
+            case LBM_SRT:
+            case LBM_TRT: h->aa = select_aa_trt(h->Q, h->dtype, force); break;
+            case LBM_MRT: h->aa = select_aa_mrt(h->Q, h->dtype, force); break;
+            case LBM_CUMULANT: h->aa = select_aa_cumulant(h->Q, h->dtype, force); break;
+            default: h->aa = select_aa_identity(h->Q, h->dtype, force); break;
+        }
+        if (!h->aa) return fail(nullptr, LBM_EUNSUPPORTED, "no kernel instantiated for this combination");
+    }
+    // rates into the kernel argument block
+    StepArgs &b = h->base;
+    std::memset(&b, 0, sizeof(b));
+    for (int i = 0; i < 8; ++i) b.rates[i] = cfg->rates[i];
+    if (cfg->collision == LBM_SRT) b.rates[1] = b.rates[0];
+    if (cfg->collision == LBM_MRT)
+        for (int i = cfg->n_rates; i < 4; ++i) b.rates[i] = 1.0;
+    if (cfg->collision == LBM_CUMULANT)
+        for (int i = cfg->n_rates; i < 6; ++i) b.rates[i] = 1.0;  // higher orders default to 1 (G7)
+    for (int d = 0; d < 3; ++d) {
+        b.F[d] = cfg->force[d];
+        b.uw[d] = cfg->ubb_velocity[d];
+    }
+    int bx = cfg->block_x > 0 ? cfg->block_x : 256;
+    if (bx > h->nx) bx = (int)((h->nx + 31) / 32 * 32);
+    if (bx > 256) bx = 256;
+    int by = 256 / bx;
+    if (by > h->ny) by = (int)h->ny;
+    if (by < 1) by = 1;
+    h->block = dim3(bx, by, 1);
+
+    CUDA_TRY(nullptr, cudaSetDevice(cfg->device));
+    if (cfg->stream) {
+        h->stream = static_cast<cudaStream_t>(cfg->stream);
+    } else {
+        CUDA_TRY(nullptr, cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+        h->own_stream = true;
+    }
+    hp.release();  // from here on, lbm_destroy cleans up
+    auto bail = [&](int code) {
+        std::string m = h->err;
+        lbm_destroy(h);
+        g_create_error = m;
+        return code;
+    };
+    if (cudaStreamCreateWithFlags(&h->comm_stream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&h->ev_bnd, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&h->ev_x, cudaEventDisableTiming) != cudaSuccess) {
+        h->err = "stream/event creation failed";
+        return bail(LBM_ECUDA);
+    }
+    if (cudaMalloc(&h->d_nanflag, sizeof(int)) != cudaSuccess) {
+        h->err = "cudaMalloc nan flag";
+        return bail(LBM_EOOM);
+    }
+
+    // slabs
+    const int nloc = cfg->nranks > 1 ? 1 : P;
+    const int64_t nzl = h->nzg / P;
+    h->slabs.resize(nloc);
+    for (int i = 0; i < nloc; ++i) {
+        Slab &s = h->slabs[i];
+        const int slab_index = cfg->nranks > 1 ? cfg->rank : i;
+        s.z0 = slab_index * nzl;
+        s.nz = (int)nzl;
+        const Geo g = geo_of(h, s);
+        const size_t bytes = (size_t)g.Sq * h->Q * h->esize;
+        for (int a = 0; a < (cfg->pattern == LBM_PULL ? 2 : 1); ++a) {
+            if (cudaMalloc(&s.pdf[a], bytes) != cudaSuccess) {
+                h->err = "cudaMalloc populations (" + std::to_string(bytes) + " B)";
+                return bail(LBM_EOOM);
+            }
+            cudaMemsetAsync(s.pdf[a], 0, bytes, h->stream);
+        }
+        if (h->g) {
+            const size_t hb = (size_t)h->nx * h->ny * (h->Q == 19 ? 5 : 9) * h->esize;
+            for (int k = 0; k < 4; ++k)
+                if (cudaMalloc(&s.halo[k], hb) != cudaSuccess) {
+                    h->err = "cudaMalloc halo";
+                    return bail(LBM_EOOM);
+                }
+        }
+        if (h->have_flags) {
+            const int nplanes = s.nz + 2 * h->g;
+            const size_t cells = (size_t)h->nx * h->ny * nplanes;
+            std::vector<uint8_t> hf(cells);
+            for (int zs = 0; zs < nplanes; ++zs) {
+                int64_t zg = s.z0 + zs - h->g;
+                zg = ((zg % h->nzg) + h->nzg) % h->nzg;
+                std::memcpy(&hf[(size_t)zs * h->nx * h->ny], cfg->flags + (size_t)zg * h->nx * h->ny, (size_t)h->nx * h->ny);
+            }
+            uint8_t *tmp = nullptr;
+            if (cudaMalloc(&s.flags, cells) != cudaSuccess || cudaMalloc(&s.rowmask, (size_t)nplanes * h->ny) != cudaSuccess ||
+                cudaMalloc(&tmp, (size_t)nplanes * h->ny) != cudaSuccess) {
+                h->err = "cudaMalloc flags";
+                return bail(LBM_EOOM);
+            }
+            cudaMemcpy(s.flags, hf.data(), cells, cudaMemcpyHostToDevice);
+            launch_rowmask(g, nplanes, s.flags, tmp, s.rowmask, h->stream);
+            cudaStreamSynchronize(h->stream);
+            cudaFree(tmp);
+        }
+    }
+    if (cfg->nranks > 1) {
+        int64_t plan[4];
+        lbm_slab_plan(h->nzg, cfg->nranks, cfg->rank, plan);
+        h->down = (int)plan[2];
+        h->up = (int)plan[3];
+        ncclUniqueId id;
+        std::memcpy(&id, cfg->nccl_id, sizeof(id));
+        ncclResult_t r = ncclCommInitRank(&h->comm, cfg->nranks, id, cfg->rank);
+        if (r != ncclSuccess) {
+            h->err = std::string("ncclCommInitRank: ") + ncclGetErrorString(r);
+            return bail(LBM_ENCCL);
+        }
+    }
+    cudaError_t e = cudaStreamSynchronize(h->stream);
+    if (e != cudaSuccess) {
+        h->err = std::string("create: ") + cudaGetErrorString(e);
+        return bail(LBM_ECUDA);
+    }
+    *out = h;
+    return LBM_OK;
+}
+
+int lbm_destroy(lbm_handle h) {
+    if (!h) return LBM_OK;
+    if (h->stream) cudaStreamSynchronize(h->stream);
+    if (h->comm_stream) cudaStreamSynchronize(h->comm_stream);
+    if (h->graph) cudaGraphExecDestroy(h->graph);
+    for (Slab &s : h->slabs) {
+        for (void *p : s.pdf) if (p) cudaFree(p);
+        for (void *p : s.halo) if (p) cudaFree(p);
+        if (s.flags) cudaFree(s.flags);
+        if (s.rowmask) cudaFree(s.rowmask);
+    }
+    if (h->comm) ncclCommDestroy(h->comm);
+    for (cudaEvent_t e : h->timing.ev) cudaEventDestroy(e);
+    if (h->ev_bnd) cudaEventDestroy(h->ev_bnd);
+    if (h->ev_x) cudaEventDestroy(h->ev_x);
+    if (h->comm_stream) cudaStreamDestroy(h->comm_stream);
+    if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
+    if (h->d_nanflag) cudaFree(h->d_nanflag);
+    if (h->scratch) cudaFree(h->scratch);
+    delete h;
+    return LBM_OK;
+}
+
+int lbm_local_extent(lbm_handle h, int64_t out[4]) {
+    if (!h || !out) return LBM_EINVAL;
+    int64_t nz = 0;
+    for (const Slab &s : h->slabs) nz += s.nz;
+    out[0] = h->slabs[0].z0;
+    out[1] = nz;
+    out[2] = h->nx;
+    out[3] = h->ny;
+    return LBM_OK;
+}
+
+static int init_common(lbm_handle h, InitArgs &a, const double *rho, const double *u, int where) {
+    const int64_t cells = local_cells(h);
+    const double *drho = rho, *du = u;
+    if (a.mode == 0) {
+        if (!rho || !u) return fail(h, LBM_EINVAL, "null rho/u");
+        if (where == LBM_HOST) {
+            int rc = ensure_scratch(h, (size_t)cells * 4 * sizeof(double));
+            if (rc) return rc;
+            CUDA_TRY(h, cudaMemcpyAsync(h->scratch, rho, cells * sizeof(double), cudaMemcpyHostToDevice, h->stream));
+            CUDA_TRY(h, cudaMemcpyAsync(h->scratch + cells, u, 3 * cells * sizeof(double), cudaMemcpyHostToDevice, h->stream));
+            drho = h->scratch;
+            du = h->scratch + cells;
+        }
+    }
+    int64_t off = 0;
+    for (Slab &s : h->slabs) {
+        InitArgs b = a;
+        b.geo = geo_of(h, s);
+        b.z0 = s.z0;
+        b.nx_g = h->nx;
+        b.ny_g = h->ny;
+        b.nz_g = h->nzg;
+        b.product_eq = h->op == LBM_CUMULANT;
+        if (a.mode == 0) {
+            // the arrays cover the concatenated local slabs; ghost planes are filled by exchange
+            b.rho = drho + off;
+            b.u = du + off;
+            b.ustride = cells;
+            b.zlo = h->g;
+            b.zhi = h->g + s.nz;
+        } else {
+            b.zlo = 0;  // random init is keyed by the global index: ghost planes computed directly
+            b.zhi = s.nz + 2 * h->g;
+        }
+        off += (int64_t)h->nx * h->ny * s.nz;
+        const dim3 grid((unsigned)((h->nx + 31) / 32), (unsigned)((h->ny + 7) / 8), (unsigned)(b.zhi - b.zlo));
+        launch_init(h->Q, h->dtype, b, s.pdf[0], s.pdf[1], grid, dim3(32, 8, 1), h->stream);
+        h->launches++;
+        s.cur = 0;
+    }
+    h->steps = 0;
+    h->aa_parity = 0;
+    if (a.mode == 0 && h->g) {
+        int rc = exchange_current(h);
+        if (rc) return rc;
+        for (Slab &s : h->slabs)
+            if (s.pdf[1]) {
+                const Geo g = geo_of(h, s);
+                CUDA_TRY(h, cudaMemcpyAsync(s.pdf[1], s.pdf[0], (size_t)g.Sq * h->Q * h->esize, cudaMemcpyDeviceToDevice, h->stream));
+            }
+    }
+    CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+    return LBM_OK;
+}
+
+int lbm_init_equilibrium(lbm_handle h, const double *rho, const double *u, int32_t where) {
+    if (!h) return LBM_EINVAL;
+    InitArgs a;
+    std::memset(&a, 0, sizeof(a));
+    a.mode = 0;
+    return init_common(h, a, rho, u, where);
+}
+
+int lbm_init_random(lbm_handle h, uint64_t seed, double rho_amp, double u_amp, int32_t profile, double profile_amp) {
+    if (!h) return LBM_EINVAL;
+    InitArgs a;
+    std::memset(&a, 0, sizeof(a));
+    a.mode = 1;
+    a.seed = seed;
+    a.rho_amp = rho_amp;
+    a.u_amp = u_amp;
+    a.profile = profile;
+    a.profile_amp = profile_amp;
+    return init_common(h, a, nullptr, nullptr, LBM_DEVICE);
+}
+
+int lbm_step(lbm_handle h, int64_t n) {
+    if (!h || n < 0) return LBM_EINVAL;
+    cudaError_t pending = cudaGetLastError();
+    if (pending != cudaSuccess) return fail(h, LBM_ECUDA, std::string("pending: ") + cudaGetErrorString(pending));
+    if (h->timing.on) {
+        for (cudaEvent_t e : h->timing.ev) cudaEventDestroy(e);
+        h->timing.ev.clear();
+    }
+    int64_t done = 0;
+    const int every = h->cfg.check_nan_every;
+    while (done < n) {
+        int64_t chunk = n - done;
+        if (every > 0) {
+            const int64_t to_check = every - (h->steps % every);
+            if (chunk > to_check) chunk = to_check;
+        }
+        int64_t i = 0;
+        if (graph_ok(h)) {
+            for (; i + 2 <= chunk; i += 2) {
+                int rc = run_graph_cycle(h);
+                if (rc) return rc;
+                if (h->cfg.pattern == LBM_PULL) {
+                    // a two-step cycle returns the state to the same array
+                }
+            }
+        }
+        for (; i < chunk; ++i) {
+            int rc = step_once(h);
+            if (rc) return rc;
+        }
+        done += chunk;
+        h->steps += chunk;
+        if (every > 0 && h->steps % every == 0) {
+            CUDA_TRY(h, cudaMemsetAsync(h->d_nanflag, 0, sizeof(int), h->stream));
+            for (Slab &s : h->slabs) {
+                const Geo g = geo_of(h, s);
+                launch_nan_check(h->dtype, s.pdf[h->cfg.pattern == LBM_PULL ? s.cur : 0], g.Sq * h->Q, h->d_nanflag, h->stream);
+            }
+            int flag = 0;
+            CUDA_TRY(h, cudaMemcpyAsync(&flag, h->d_nanflag, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+            CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+            if (flag) return fail(h, LBM_ENAN, "NaN detected after step " + std::to_string(h->steps));
+        }
+    }
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(h, LBM_ECUDA, std::string("launch: ") + cudaGetErrorString(e));
+    return LBM_OK;
+}
+
+int lbm_sync(lbm_handle h) {
+    if (!h) return LBM_EINVAL;
+    CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+    CUDA_TRY(h, cudaStreamSynchronize(h->comm_stream));
+    CUDA_TRY(h, cudaGetLastError());
+    return LBM_OK;
+}
+
+int64_t lbm_steps_done(lbm_handle h) { return h ? h->steps : -1; }
+int64_t lbm_launch_count(lbm_handle h) { return h ? h->launches : -1; }
+
+int lbm_kernel_time_ms(lbm_handle h, double *ms, int64_t *launches) {
+    if (!h) return LBM_EINVAL;
+    if (!ms) {  // toggle: lbm_kernel_time_ms(h, NULL, NULL) switches timing on for subsequent steps
+        h->timing.on = true;
+        return LBM_OK;
+    }
+    CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+    double tot = 0;
+    int64_t n = 0;
+    for (size_t i = 0; i + 1 < h->timing.ev.size(); i += 2) {
+        float t = 0;
+        CUDA_TRY(h, cudaEventElapsedTime(&t, h->timing.ev[i], h->timing.ev[i + 1]));
+        tot += t;
+        ++n;
+    }
+    *ms = tot;
+    if (launches) *launches = n;
+    return LBM_OK;
+}
+
+static int read_common(lbm_handle h, ReadArgs &r, int raw) {
+    r.raw = raw;
+    r.aa_odd = (h->cfg.pattern == LBM_AA) && h->aa_parity;
+    r.fsign = h->cfg.pattern == LBM_PULL ? -1.0 : 1.0;
+    for (int d = 0; d < 3; ++d) r.F[d] = h->cfg.force[d];
+    return LBM_OK;
+}
+
+int lbm_get_populations(lbm_handle h, double *out, int32_t where, int32_t raw) {
+    if (!h || !out) return LBM_EINVAL;
+    const int64_t cells = local_cells(h);
+    double *dst = out;
+    if (where == LBM_HOST) {
+        int rc = ensure_scratch(h, (size_t)cells * h->Q * sizeof(double));
+        if (rc) return rc;
+        dst = h->scratch;
+    }
+    int64_t off = 0;
+    for (Slab &s : h->slabs) {
+        ReadArgs r;
+        std::memset(&r, 0, sizeof(r));
+        read_common(h, r, raw);
+        r.geo = geo_of(h, s);
+        const int64_t sc = (int64_t)h->nx * h->ny * s.nz;
+        const void *f = s.pdf[h->cfg.pattern == LBM_PULL ? s.cur : 0];
+        double *tmp = dst;
+        if (h->slabs.size() > 1) {  // per-slab block then scatter into [q][cells]
+            int rc = ensure_scratch(h, (size_t)cells * h->Q * sizeof(double) * 2);
+            if (rc) return rc;
+            if (where == LBM_HOST) dst = h->scratch;
+            tmp = h->scratch + (size_t)cells * h->Q;
+        }
+        launch_get_pops(h->Q, h->dtype, r, f, tmp, dim3((unsigned)((h->nx + 31) / 32), (unsigned)((h->ny + 7) / 8), (unsigned)s.nz),
+                        dim3(32, 8, 1), h->stream);
+        if (h->slabs.size() > 1)
+            for (int q = 0; q < h->Q; ++q)
+                CUDA_TRY(h, cudaMemcpyAsync(dst + (size_t)q * cells + off, tmp + (size_t)q * sc, sc * sizeof(double),
+                                            cudaMemcpyDeviceToDevice, h->stream));
+        off += sc;
+    }
+    if (where == LBM_HOST)
+        CUDA_TRY(h, cudaMemcpyAsync(out, dst, (size_t)cells * h->Q * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+    CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+    return LBM_OK;
+}
+
+int lbm_get_populations_at(lbm_handle h, const int64_t *cells, int64_t n, double *out) {
+    if (!h || !cells || !out || n < 0) return LBM_EINVAL;
+    if (n == 0) return LBM_OK;
+    const int64_t total = local_cells(h);
+    for (int64_t k = 0; k < n; ++k)
+        if (cells[k] < 0 || cells[k] >= total) return fail(h, LBM_EINVAL, "cell index out of range");
+    const size_t ib = ((size_t)n * sizeof(int64_t) + 255) / 256 * 256;
+    int rc = ensure_scratch(h, ib + (size_t)n * h->Q * sizeof(double));
+    if (rc) return rc;
+    int64_t *didx = reinterpret_cast<int64_t *>(h->scratch);
+    double *dout = reinterpret_cast<double *>(reinterpret_cast<char *>(h->scratch) + ib);
+    CUDA_TRY(h, cudaMemcpyAsync(didx, cells, n * sizeof(int64_t), cudaMemcpyHostToDevice, h->stream));
+    int64_t first = 0;
+    for (Slab &s : h->slabs) {
+        ReadArgs r;
+        std::memset(&r, 0, sizeof(r));
+        read_common(h, r, 0);
+        r.geo = geo_of(h, s);
+        const int64_t sc = (int64_t)h->nx * h->ny * s.nz;
+        launch_get_at(h->Q, h->dtype, r, s.pdf[h->cfg.pattern == LBM_PULL ? s.cur : 0], didx, n, first, first + sc, dout, h->stream);
+        first += sc;
+    }
+    CUDA_TRY(h, cudaMemcpyAsync(out, dout, (size_t)n * h->Q * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+    CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+    return LBM_OK;
+}
+
+int lbm_set_populations(lbm_handle h, const double *in, int32_t where, int32_t raw) {
+    if (!h || !in) return LBM_EINVAL;
+    const int64_t cells = local_cells(h);
+    int rc = ensure_scratch(h, (size_t)cells * h->Q * sizeof(double) * 2);
+    if (rc) return rc;
+    const double *src = in;
+    if (where == LBM_HOST) {
+        CUDA_TRY(h, cudaMemcpyAsync(h->scratch, in, (size_t)cells * h->Q * sizeof(double), cudaMemcpyHostToDevice, h->stream));
+        src = h->scratch;
+    }
+    int64_t off = 0;
+    h->aa_parity = 0;
+    for (Slab &s : h->slabs) {
+        ReadArgs r;
+        std::memset(&r, 0, sizeof(r));
+        read_common(h, r, raw);
+        r.aa_odd = 0;
+        r.geo = geo_of(h, s);
+        const int64_t sc = (int64_t)h->nx * h->ny * s.nz;
+        double *tmp = h->scratch + (size_t)cells * h->Q;
+        for (int q = 0; q < h->Q; ++q)
+            CUDA_TRY(h, cudaMemcpyAsync(tmp + (size_t)q * sc, src + (size_t)q * cells + off, sc * sizeof(double),
+                                        cudaMemcpyDeviceToDevice, h->stream));
+        s.cur = 0;
+        launch_set_pops(h->Q, h->dtype, r, s.pdf[0], tmp, dim3((unsigned)((h->nx + 31) / 32), (unsigned)((h->ny + 7) / 8), (unsigned)s.nz),
+                        dim3(32, 8, 1), h->stream);
+        if (s.pdf[1]) {
+            const Geo g = geo_of(h, s);
+            CUDA_TRY(h, cudaMemcpyAsync(s.pdf[1], s.pdf[0], (size_t)g.Sq * h->Q * h->esize, cudaMemcpyDeviceToDevice, h->stream));
+        }
+        off += sc;
+    }
+    rc = exchange_current(h);
+    if (rc) return rc;
+    CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+    return LBM_OK;
+}
+
+int lbm_get_macroscopic(lbm_handle h, double *rho, double *u, int32_t where) {
+    if (!h || !rho || !u) return LBM_EINVAL;
+    const int64_t cells = local_cells(h);
+    double *drho = rho, *du = u;
+    if (where == LBM_HOST || h->slabs.size() > 1) {
+        int rc = ensure_scratch(h, (size_t)cells * 4 * sizeof(double) * 2);
+        if (rc) return rc;
+        drho = h->scratch;
+        du = h->scratch + cells;
+    }
+    int64_t off = 0;
+    for (Slab &s : h->slabs) {
+        ReadArgs r;
+        std::memset(&r, 0, sizeof(r));
+        read_common(h, r, 0);
+        r.geo = geo_of(h, s);
+        const int64_t sc = (int64_t)h->nx * h->ny * s.nz;
+        const void *f = s.pdf[h->cfg.pattern == LBM_PULL ? s.cur : 0];
+        double *tr = h->slabs.size() > 1 ? h->scratch + 4 * cells : drho;
+        double *tu = h->slabs.size() > 1 ? h->scratch + 5 * cells : du;
+        launch_macro(h->Q, h->dtype, r, f, tr, tu, dim3((unsigned)((h->nx + 31) / 32), (unsigned)((h->ny + 7) / 8), (unsigned)s.nz),
+                     dim3(32, 8, 1), h->stream);
+        if (h->slabs.size() > 1) {
+            CUDA_TRY(h, cudaMemcpyAsync(drho + off, tr, sc * sizeof(double), cudaMemcpyDeviceToDevice, h->stream));
+            for (int d = 0; d < 3; ++d)
+                CUDA_TRY(h, cudaMemcpyAsync(du + (size_t)d * cells + off, tu + (size_t)d * sc, sc * sizeof(double),
+                                            cudaMemcpyDeviceToDevice, h->stream));
+        }
+        off += sc;
+    }
+    if (where == LBM_HOST) {
+        CUDA_TRY(h, cudaMemcpyAsync(rho, drho, cells * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+        CUDA_TRY(h, cudaMemcpyAsync(u, du, 3 * cells * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+    } else if (h->slabs.size() > 1) {
+        CUDA_TRY(h, cudaMemcpyAsync(rho, drho, cells * sizeof(double), cudaMemcpyDeviceToDevice, h->stream));
+        CUDA_TRY(h, cudaMemcpyAsync(u, du, 3 * cells * sizeof(double), cudaMemcpyDeviceToDevice, h->stream));
+    }
+    CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+    return LBM_OK;
+}
+
+int lbm_pack_face(lbm_handle h, int64_t z, int32_t dir, double *out, int32_t where) {
+    if (!h || !out || (dir != 1 && dir != -1)) return LBM_EINVAL;
+    // z is a local interior plane across the concatenated slabs
+    int64_t zz = z;
+    Slab *sp = nullptr;
+    for (Slab &s : h->slabs) {
+        if (zz < s.nz) {
+            sp = &s;
+            break;
+        }
+        zz -= s.nz;
+    }
+    if (!sp || zz < 0) return fail(h, LBM_EINVAL, "plane out of range");
+    if (h->cfg.pattern == LBM_AA && h->aa_parity) return fail(h, LBM_EUNSUPPORTED, "pack_face on an odd AA state");
+    const size_t n = (size_t)h->nx * h->ny * (h->Q == 19 ? 5 : 9);
+    double *dst = out;
+    if (where == LBM_HOST) {
+        int rc = ensure_scratch(h, n * sizeof(double));
+        if (rc) return rc;
+        dst = h->scratch;
+    }
+    launch_pack(h->Q, h->dtype, geo_of(h, *sp), sp->pdf[h->cfg.pattern == LBM_PULL ? sp->cur : 0], (int)zz + h->g, dir, dst, true,
+                h->stream);
+    if (where == LBM_HOST) CUDA_TRY(h, cudaMemcpyAsync(out, dst, n * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+    CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+    return LBM_OK;
+}
+
+}  // extern "C"

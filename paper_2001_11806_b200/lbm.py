@@ -1,0 +1,276 @@
+"""Thin ctypes binding of ``include/lbm.h`` (argument marshalling only; every step of the LB
+path runs in the CUDA kernels of ``liblbm_b200.so``).
+
+Function names mirror the C ABI (``lbm_create``, ``lbm_init_equilibrium``, ``lbm_step``,
+``lbm_get_macroscopic`` ...). :class:`Simulation` is a small convenience wrapper that owns a
+handle and accepts numpy arrays (host) or torch CUDA tensors (device).
+
+There is no fallback: if the shared library is missing this module raises at import time.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from typing import Optional, Sequence
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIBPATH = os.path.join(HERE, "liblbm_b200.so")
+
+LBM_OK, LBM_EINVAL, LBM_EUNSUPPORTED, LBM_ECUDA, LBM_ENCCL, LBM_ENAN, LBM_EOOM = 0, -1, -2, -3, -4, -5, -6
+D3Q19, D3Q27 = 19, 27
+SRT, TRT, MRT, CUMULANT, IDENTITY = 0, 1, 2, 3, 4
+F64, F32 = 0, 1
+PULL, AA = 0, 1
+FLUID, NOSLIP, UBB = 0, 1, 2
+HOST, DEVICE = 0, 1
+HALO_ZEROCOPY, HALO_PACKED = 0, 1
+
+COLLISIONS = {"srt": SRT, "trt": TRT, "mrt": MRT, "cumulant": CUMULANT, "identity": IDENTITY}
+DTYPES = {"f64": F64, "float64": F64, "fp64": F64, "f32": F32, "float32": F32, "fp32": F32}
+PATTERNS = {"pull": PULL, "aa": AA}
+
+
+class lbm_config(C.Structure):
+    _fields_ = [
+        ("stencil", C.c_int32), ("collision", C.c_int32), ("dtype", C.c_int32), ("pattern", C.c_int32),
+        ("n_rates", C.c_int32), ("rates", C.c_double * 8), ("force", C.c_double * 3),
+        ("global_", C.c_int64 * 3), ("periodic", C.c_int32 * 3), ("flags", C.c_void_p),
+        ("ubb_velocity", C.c_double * 3), ("rank", C.c_int32), ("nranks", C.c_int32),
+        ("nccl_id", C.c_void_p), ("n_local_slabs", C.c_int32), ("device", C.c_int32),
+        ("stream", C.c_void_p), ("halo_mode", C.c_int32), ("use_graph", C.c_int32),
+        ("block_x", C.c_int32), ("check_nan_every", C.c_int32),
+    ]
+
+
+class LBMError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{msg} (status {status})")
+        self.status = status
+
+
+if not os.path.exists(LIBPATH):
+    raise ImportError(f"{LIBPATH} is missing: build it with `python -m paper_2001_11806_b200.build` "
+                      "(there is no CPU fallback)")
+_lib = C.CDLL(LIBPATH)
+
+_P, _I32, _I64, _D = C.c_void_p, C.c_int32, C.c_int64, C.c_double
+_SIGS = {
+    "lbm_config_default": ([C.POINTER(lbm_config)], None),
+    "lbm_create": ([C.POINTER(lbm_config), C.POINTER(C.c_void_p)], C.c_int),
+    "lbm_destroy": ([_P], C.c_int),
+    "lbm_local_extent": ([_P, _P], C.c_int),
+    "lbm_init_equilibrium": ([_P, _P, _P, _I32], C.c_int),
+    "lbm_init_random": ([_P, C.c_uint64, _D, _D, _I32, _D], C.c_int),
+    "lbm_step": ([_P, _I64], C.c_int),
+    "lbm_sync": ([_P], C.c_int),
+    "lbm_steps_done": ([_P], _I64),
+    "lbm_get_macroscopic": ([_P, _P, _P, _I32], C.c_int),
+    "lbm_get_populations": ([_P, _P, _I32, _I32], C.c_int),
+    "lbm_set_populations": ([_P, _P, _I32, _I32], C.c_int),
+    "lbm_pack_face": ([_P, _I64, _I32, _P, _I32], C.c_int),
+    "lbm_get_populations_at": ([_P, _P, _I64, _P], C.c_int),
+    "lbm_kernel_time_ms": ([_P, _P, _P], C.c_int),
+    "lbm_launch_count": ([_P], _I64),
+    "lbm_nccl_unique_id": ([_P], C.c_int),
+    "lbm_slab_plan": ([_I64, _I32, _I32, _P], C.c_int),
+    "lbm_crossing_directions": ([_I32, _I32, _P], C.c_int),
+    "lbm_stencil_table": ([_I32, _P, _P], C.c_int),
+    "lbm_strerror": ([C.c_int], C.c_char_p),
+    "lbm_last_error": ([_P], C.c_char_p),
+    "lbm_version": ([], C.c_char_p),
+}
+for _name, (_args, _res) in _SIGS.items():
+    _fn = getattr(_lib, _name)
+    _fn.argtypes = _args
+    _fn.restype = _res
+    globals()[_name] = _fn
+
+EXPORTED = tuple(_SIGS)
+
+
+def _check(status: int, h=None, what: str = "") -> None:
+    if status < 0:
+        msg = (lbm_last_error(h) or b"").decode() or lbm_strerror(status).decode()
+        raise LBMError(status, f"{what}: {msg}")
+
+
+def _ptr(a) -> int:
+    """Address of a numpy array (host) or a torch tensor (device or host)."""
+    if a is None:
+        return None
+    if isinstance(a, np.ndarray):
+        assert a.flags["C_CONTIGUOUS"]
+        return a.ctypes.data
+    assert a.is_contiguous()
+    return a.data_ptr()
+
+
+def slab_plan(nz: int, nranks: int, rank: int):
+    out = np.zeros(4, np.int64)
+    _check(lbm_slab_plan(nz, nranks, rank, out.ctypes.data), what="lbm_slab_plan")
+    return tuple(int(v) for v in out)
+
+
+def crossing_directions(stencil: int, direction: int):
+    out = np.zeros(9, np.int32)
+    n = lbm_crossing_directions(stencil, direction, out.ctypes.data)
+    _check(n, what="lbm_crossing_directions")
+    return out[:n].tolist()
+
+
+def stencil_table(stencil: int):
+    c = np.zeros(3 * stencil, np.int32)
+    w = np.zeros(stencil, np.float64)
+    _check(lbm_stencil_table(stencil, c.ctypes.data, w.ctypes.data), what="lbm_stencil_table")
+    return c.reshape(stencil, 3), w
+
+
+def nccl_unique_id() -> bytes:
+    buf = (C.c_uint8 * 128)()
+    _check(lbm_nccl_unique_id(C.addressof(buf)), what="lbm_nccl_unique_id")
+    return bytes(buf)
+
+
+class Simulation:
+    """Owns one lbm handle. ``rates`` follow include/lbm.h; ``flags`` is a host uint8 array of
+    shape (nz, ny, nx) for the GLOBAL lattice; ``stream`` is a cudaStream_t (int) or None."""
+
+    def __init__(self, shape: Sequence[int], stencil: int = 19, collision: str = "srt",
+                 rates: Sequence[float] = (1.8,), dtype: str = "f64", pattern: str = "pull",
+                 force: Sequence[float] = (0.0, 0.0, 0.0), flags: Optional[np.ndarray] = None,
+                 ubb_velocity: Sequence[float] = (0.0, 0.0, 0.0), periodic=(1, 1, 1),
+                 rank: int = 0, nranks: int = 1, nccl_id: Optional[bytes] = None,
+                 n_local_slabs: int = 1, device: int = 0, stream: Optional[int] = None,
+                 halo_mode: int = HALO_ZEROCOPY, use_graph: bool = False, block_x: int = 0,
+                 check_nan_every: int = 0):
+        cfg = lbm_config()
+        lbm_config_default(C.byref(cfg))
+        nx, ny, nz = shape
+        cfg.stencil = stencil
+        cfg.collision = COLLISIONS[collision] if isinstance(collision, str) else collision
+        cfg.dtype = DTYPES[dtype] if isinstance(dtype, str) else dtype
+        cfg.pattern = PATTERNS[pattern] if isinstance(pattern, str) else pattern
+        cfg.n_rates = len(rates)
+        for i, r in enumerate(rates):
+            cfg.rates[i] = r
+        for d in range(3):
+            cfg.force[d] = force[d]
+            cfg.ubb_velocity[d] = ubb_velocity[d]
+            cfg.periodic[d] = int(periodic[d])
+        cfg.global_[0], cfg.global_[1], cfg.global_[2] = nx, ny, nz
+        self._flags = None
+        if flags is not None:
+            self._flags = np.ascontiguousarray(flags, dtype=np.uint8)
+            assert self._flags.shape == (nz, ny, nx)
+            cfg.flags = self._flags.ctypes.data
+        cfg.rank, cfg.nranks = rank, nranks
+        self._id = None
+        if nccl_id is not None:
+            self._id = (C.c_uint8 * 128).from_buffer_copy(nccl_id)
+            cfg.nccl_id = C.addressof(self._id)
+        cfg.n_local_slabs = n_local_slabs
+        cfg.device = device
+        cfg.stream = stream
+        cfg.halo_mode = halo_mode
+        cfg.use_graph = int(use_graph)
+        cfg.block_x = block_x
+        cfg.check_nan_every = check_nan_every
+        self.cfg = cfg
+        self.Q = stencil
+        h = C.c_void_p()
+        st = lbm_create(C.byref(cfg), C.byref(h))
+        _check(st, None, "lbm_create")
+        self.h = h
+        ext = np.zeros(4, np.int64)
+        _check(lbm_local_extent(self.h, ext.ctypes.data), self.h, "lbm_local_extent")
+        self.z0, self.nz_local, self.nx, self.ny = (int(v) for v in ext)
+        self.cells = self.nx * self.ny * self.nz_local
+
+    # -- lifecycle ------------------------------------------------------------------
+    def close(self):
+        if getattr(self, "h", None):
+            lbm_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        self.close()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    # -- calls ------------------------------------------------------------------------
+    def init_equilibrium(self, rho, u):
+        where = HOST if isinstance(rho, np.ndarray) else DEVICE
+        if where == HOST:
+            rho = np.ascontiguousarray(rho, np.float64)
+            u = np.ascontiguousarray(u, np.float64)
+            assert rho.size == self.cells and u.size == 3 * self.cells
+        _check(lbm_init_equilibrium(self.h, _ptr(rho), _ptr(u), where), self.h, "lbm_init_equilibrium")
+
+    def init_random(self, seed: int, rho_amp: float, u_amp: float, profile: int = 0, profile_amp: float = 0.0):
+        _check(lbm_init_random(self.h, seed, rho_amp, u_amp, profile, profile_amp), self.h, "lbm_init_random")
+
+    def step(self, n: int = 1):
+        _check(lbm_step(self.h, n), self.h, "lbm_step")
+
+    def sync(self):
+        _check(lbm_sync(self.h), self.h, "lbm_sync")
+
+    @property
+    def steps_done(self) -> int:
+        return int(lbm_steps_done(self.h))
+
+    @property
+    def launches(self) -> int:
+        return int(lbm_launch_count(self.h))
+
+    def macroscopic(self, rho=None, u=None):
+        """Returns (rho, u) as numpy (nz, ny, nx) / (3, nz, ny, nx) unless device outputs are given."""
+        if rho is None:
+            rho = np.empty((self.nz_local, self.ny, self.nx))
+            u = np.empty((3, self.nz_local, self.ny, self.nx))
+        where = HOST if isinstance(rho, np.ndarray) else DEVICE
+        _check(lbm_get_macroscopic(self.h, _ptr(rho), _ptr(u), where), self.h, "lbm_get_macroscopic")
+        return rho, u
+
+    def populations(self, raw: bool = False, out=None):
+        if out is None:
+            out = np.empty((self.Q, self.nz_local, self.ny, self.nx))
+        where = HOST if isinstance(out, np.ndarray) else DEVICE
+        _check(lbm_get_populations(self.h, _ptr(out), where, int(raw)), self.h, "lbm_get_populations")
+        return out
+
+    def set_populations(self, f, raw: bool = False):
+        where = HOST if isinstance(f, np.ndarray) else DEVICE
+        if where == HOST:
+            f = np.ascontiguousarray(f, np.float64)
+            assert f.size == self.Q * self.cells
+        _check(lbm_set_populations(self.h, _ptr(f), where, int(raw)), self.h, "lbm_set_populations")
+
+    def populations_at(self, cells) -> np.ndarray:
+        """Canonical populations (Q, n) at local linear cell indices."""
+        idx = np.ascontiguousarray(cells, np.int64)
+        out = np.empty((self.Q, idx.size))
+        _check(lbm_get_populations_at(self.h, idx.ctypes.data, idx.size, out.ctypes.data), self.h,
+               "lbm_get_populations_at")
+        return out
+
+    def pack_face(self, z: int, direction: int):
+        nq = 5 if self.Q == 19 else 9
+        out = np.empty(nq * self.nx * self.ny)
+        _check(lbm_pack_face(self.h, z, direction, out.ctypes.data, HOST), self.h, "lbm_pack_face")
+        return out
+
+    def enable_kernel_timing(self):
+        _check(lbm_kernel_time_ms(self.h, None, None), self.h, "lbm_kernel_time_ms")
+
+    def kernel_time_ms(self):
+        ms = C.c_double()
+        n = C.c_int64()
+        _check(lbm_kernel_time_ms(self.h, C.byref(ms), C.byref(n)), self.h, "lbm_kernel_time_ms")
+        return ms.value, n.value

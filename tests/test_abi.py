@@ -1,0 +1,101 @@
+"""C-ABI library checks that need no GPU: the shared library loads, exports every symbol declared
+in include/lbm.h, and its host-only functions (decomposition plan, crossing directions, stencil
+table, validation errors) agree with the oracle / the paper."""
+import os
+import re
+import subprocess
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "lbm.h")
+
+
+@pytest.fixture(scope="module")
+def L():
+    from paper_2001_11806_b200 import build
+    build.build()
+    from paper_2001_11806_b200 import lbm
+    return lbm
+
+
+def declared_functions():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"^\s*(?:const\s+)?[a-z_0-9]+\s*\*?\s*(lbm_[a-z_0-9]+)\s*\(", src, flags=re.M)))
+
+
+def test_every_declared_symbol_is_exported(L):
+    names = declared_functions()
+    assert "lbm_create" in names and "lbm_step" in names and "lbm_get_macroscopic" in names
+    out = subprocess.run(["nm", "-D", "--defined-only", L.LIBPATH], capture_output=True, text=True, check=True).stdout
+    exported = set(re.findall(r" T (lbm_[a-z_0-9]+)$", out, flags=re.M))
+    missing = [n for n in names if n not in exported]
+    assert not missing, missing
+    # the binding wraps every declared function under the same name
+    assert sorted(set(L.EXPORTED)) == names
+
+
+def test_library_is_sm100a(L):
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", L.LIBPATH], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_stencil_table_matches_oracle(L):
+    import oracle as O
+    for Q in (19, 27):
+        c, w = L.stencil_table(Q)
+        co, wo, _ = O.stencil_arrays(Q)
+        np.testing.assert_array_equal(c, co)
+        np.testing.assert_array_equal(w, wo)
+
+
+def test_crossing_directions(L):
+    import oracle as O
+    for Q, n in ((19, 5), (27, 9)):
+        c, _, _ = O.stencil_arrays(Q)
+        for d in (1, -1):
+            got = L.crossing_directions(Q, d)
+            assert len(got) == n and got == [q for q in range(Q) if c[q, 2] == d]
+
+
+def test_slab_plan(L):
+    for P in (1, 2, 4, 8):
+        spans = [L.slab_plan(512 * P, P, r) for r in range(P)]
+        assert [s[0] for s in spans] == [512 * r for r in range(P)]
+        assert all(s[1] == 512 for s in spans)
+        assert [s[2] for s in spans] == [(r - 1) % P for r in range(P)]
+        assert [s[3] for s in spans] == [(r + 1) % P for r in range(P)]
+    with pytest.raises(L.LBMError):
+        L.slab_plan(10, 3, 0)
+    with pytest.raises(L.LBMError):
+        L.slab_plan(8, 8, 0)  # one plane per slab is too thin
+
+
+@pytest.mark.parametrize("kw,code", [
+    (dict(rates=(2.5,)), -1),                                   # rate outside (0, 2)
+    (dict(collision="trt", rates=(1.6,)), -1),                  # TRT needs two rates
+    (dict(stencil=27, collision="mrt", rates=(1.9,)), -2),      # MRT is D3Q19 only
+    (dict(stencil=19, collision="cumulant", rates=(1.9,)), -2),  # cumulant is D3Q27 only
+    (dict(collision="mrt", rates=(1.9,), force=(1e-5, 0, 0)), -2),
+    (dict(n_local_slabs=3), -1),                                # nz % slabs != 0
+    (dict(periodic=(1, 0, 1)), -1),                             # non-periodic axis without walls
+    (dict(pattern="aa", n_local_slabs=2), -2),
+])
+def test_create_validation_errors(L, kw, code):
+    """Validation happens before any CUDA call, so these run on a CPU-only host."""
+    args = dict(shape=(8, 8, 8))
+    args.update(kw)
+    with pytest.raises(L.LBMError) as e:
+        L.Simulation(**args)
+    assert e.value.status == code
+
+
+def test_nonperiodic_axis_requires_walls(L):
+    import lbminputs as LI
+    fl = LI.channel_flags(8, 8, 8)
+    fl[:, -1, 3] = 0  # hole in the top wall
+    with pytest.raises(L.LBMError) as e:
+        L.Simulation((8, 8, 8), periodic=(1, 0, 1), flags=fl)
+    assert e.value.status == -1

@@ -1,0 +1,269 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on the same seeded inputs.
+
+Bars (north_star): max relative population error <= 1e-12 (fp64) / <= 2e-5 (fp32) after the
+case's step count; data movement (streaming, flag-driven boundaries, AA slots, halo planes,
+slab decomposition) bit-exact.
+"""
+import numpy as np
+import pytest
+
+import lbminputs as LI
+import oracle as O
+from tests.gpu_common import FULL, TOL, Case, fluid_mask, init_sim, make_sim, max_rel_err, oracle_run
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _lib():
+    from paper_2001_11806_b200 import build
+    build.build()
+    import torch
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+
+
+def _markers(Q, shape, seed=1):
+    """Distinct dyadic marker values, exact in fp32 and fp64."""
+    rng = np.random.default_rng(seed)
+    nx, ny, nz = shape
+    return rng.integers(1, 2 ** 20, size=(Q, nz, ny, nx)).astype(np.float64) / 2 ** 12
+
+
+# -----------------------------------------------------------------------------------------
+# Data movement, bit-exact
+# -----------------------------------------------------------------------------------------
+@pytest.mark.parametrize("Q", [19, 27])
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+@pytest.mark.parametrize("geometry", ["periodic", "obstacles"])
+def test_pull_streaming_and_bounce_back_bit_exact(Q, dtype, geometry):
+    case = Case("mark", (13, 11, 7), Q, "identity", (), dtype, geometry=geometry)
+    sim = make_sim(case)
+    m = _markers(Q, case.shape)
+    sim.set_populations(m, raw=True)
+    d = O.Domain(O.Method(Q=Q, op="identity", rates=()), *case.shape, flags=case.flags())
+    ref = d.run_pull(m, 3)
+    sim.step(3)
+    got = sim.populations(raw=True)
+    mask = fluid_mask(case, Q)
+    np.testing.assert_array_equal(got[mask], ref[mask])
+
+
+@pytest.mark.parametrize("Q", [19, 27])
+def test_aa_slots_bit_exact(Q):
+    case = Case("mark", (9, 6, 5), Q, "identity", (), "f64", pattern="aa")
+    sim = make_sim(case)
+    m = _markers(Q, case.shape, 2)
+    sim.set_populations(m, raw=True)
+    d = O.Domain(O.Method(Q=Q, op="identity", rates=()), *case.shape)
+    for n in (1, 2, 3):
+        sim.step(1)
+        np.testing.assert_array_equal(sim.populations(raw=True), d.run_aa(m, n))       # slot layout
+        np.testing.assert_array_equal(sim.populations(raw=False) - 0.0,                # canonical gather
+                                      _centre_free(d.run_push(m, n), Q, True))
+
+
+def _centre_free(f_raw_stream, Q, add_w):
+    # identity collision: canonical value = raw marker + w_q (the library adds w back)
+    _, w, _ = O.stencil_arrays(Q)
+    return f_raw_stream + (w[:, None, None, None] if add_w else 0.0)
+
+
+@pytest.mark.parametrize("Q", [19, 27])
+def test_pack_face_layout_bit_exact(Q):
+    case = Case("pack", (10, 7, 6), Q, "trt", (1.6, 0.5), "f64")
+    sim = make_sim(case)
+    init_sim(sim, case)
+    sim.step(2)
+    raw = sim.populations(raw=True)
+    d = O.Domain(O.Method(Q=Q, op="identity", rates=()), *case.shape)
+    for z in (0, 3, 5):
+        for direction in (1, -1):
+            np.testing.assert_array_equal(sim.pack_face(z, direction), d.pack_face(raw, z, direction))
+
+
+# -----------------------------------------------------------------------------------------
+# Initialisation and readout
+# -----------------------------------------------------------------------------------------
+@pytest.mark.parametrize("Q,op,rates", [(19, "srt", (1.8,)), (27, "cumulant", (1.95,))])
+def test_init_random_matches_seeded_inputs(Q, op, rates):
+    case = Case("init", (16, 12, 10), Q, op, rates, "f64", init="shear")
+    sim = make_sim(case)
+    init_sim(sim, case, use_random_kernel=True)
+    d = O.Domain(case.method(), *case.shape)
+    rho, u = case.fields()
+    ref = d.init_equilibrium(rho, u)
+    assert max_rel_err(sim.populations(), ref) < 1e-14
+
+
+def test_macroscopic_readout():
+    case = FULL["c1_f64"]
+    case = Case("c1s", (12, 16, 8), **{k: getattr(case, k) for k in ("Q", "op", "rates", "dtype", "force", "geometry")},
+                init="random", steps=30)
+    sim = make_sim(case)
+    init_sim(sim, case)
+    sim.step(case.steps)
+    d = O.Domain(case.method(), *case.shape, flags=case.flags())
+    ref = oracle_run(case)
+    rho_o, u_o = d.macroscopic(ref, post_collision=True)
+    rho, u = sim.macroscopic()
+    fl = case.flags() == 0
+    np.testing.assert_allclose(rho[fl], rho_o[fl], rtol=1e-13)
+    np.testing.assert_allclose(u[:, fl], u_o[:, fl], rtol=0, atol=1e-15)
+
+
+# -----------------------------------------------------------------------------------------
+# Numerical parity per operator / config (reduced sizes, many steps, ragged extents)
+# -----------------------------------------------------------------------------------------
+PARITY = [
+    Case("c0_full", (32, 32, 32), 19, "srt", (1.8,), "f64", steps=100),
+    Case("c1_proxy_f64", (16, 32, 8), 19, "trt", (1.6, 0.5), "f64", force=(1e-6, 0, 0), geometry="channel",
+         init="rest", steps=300),
+    Case("c1_proxy_f32", (16, 32, 8), 19, "trt", (1.6, 0.5), "f32", force=(1e-6, 0, 0), geometry="channel",
+         init="rest", steps=300),
+    Case("c1_proxy_f32_random", (16, 32, 8), 19, "trt", (1.6, 0.5), "f32", force=(1e-6, 0, 0), geometry="channel",
+         steps=100),
+    Case("c2_proxy", (32, 32, 32), 19, "mrt", (1.9, 1.0, 1.0, 1.0), "f32", pattern="aa", init="shear", rho_amp=0.0,
+         u_amp=1e-4, steps=100),
+    Case("c2_proxy_f64", (24, 20, 32), 19, "mrt", (1.9, 1.0, 1.0, 1.0), "f64", pattern="aa", init="shear",
+         rho_amp=0.0, u_amp=1e-4, steps=40),
+    Case("c3_proxy", (20, 20, 20), 27, "cumulant", (1.95,), "f64", geometry="cavity", ubb=(0.05, 0, 0),
+         init="rest", steps=100),
+    Case("c3_proxy_random", (16, 16, 16), 27, "cumulant", (1.95,), "f64", geometry="cavity", ubb=(0.05, 0, 0),
+         steps=30),
+    Case("c4_proxy", (24, 24, 24), 19, "trt", (1.6, 0.5), "f64", steps=50),
+    Case("ragged_q27_trt_f32", (37, 23, 19), 27, "trt", (1.3, 0.9), "f32", force=(2e-5, -1e-5, 3e-5),
+         geometry="obstacles", ubb=(0.02, -0.01, 0.03), steps=20),
+    Case("ragged_q19_srt_f64_obst", (37, 23, 19), 19, "srt", (1.1,), "f64", geometry="obstacles",
+         ubb=(0.02, -0.01, 0.03), steps=20),
+    Case("mrt_general_rates_walls", (20, 18, 12), 19, "mrt", (1.9, 1.3, 1.1, 0.8), "f64", geometry="channel", steps=25),
+    Case("mrt_general_f32_pull", (20, 18, 12), 19, "mrt", (1.7, 1.2, 0.9, 1.4), "f32", steps=25),
+    Case("cumulant_general_rates", (14, 12, 10), 27, "cumulant", (1.8, 1.3, 1.2, 0.9, 1.1, 0.7), "f64", steps=20),
+    Case("cumulant_f32", (14, 12, 10), 27, "cumulant", (1.95,), "f32", steps=20),
+    Case("aa_trt_force_odd", (18, 14, 10), 19, "trt", (1.6, 0.5), "f64", pattern="aa", force=(1e-5, 2e-5, 0), steps=21),
+    Case("aa_q27_trt_f32", (18, 14, 10), 27, "trt", (1.5, 1.2), "f32", pattern="aa", steps=12),
+    Case("aa_cumulant_f64", (12, 12, 12), 27, "cumulant", (1.95,), "f64", pattern="aa", steps=10),
+    Case("tiny_1x1x4", (1, 1, 4), 19, "srt", (1.5,), "f64", steps=7),
+]
+
+
+@pytest.mark.parametrize("case", PARITY, ids=lambda c: c.name)
+def test_parity_vs_oracle(case):
+    sim = make_sim(case)
+    init_sim(sim, case)
+    sim.step(case.steps)
+    got = sim.populations()
+    ref = oracle_run(case)
+    err = max_rel_err(got, ref, fluid_mask(case, case.Q))
+    assert err <= TOL[case.dtype], err
+
+
+def test_cuda_graph_path_bit_identical():
+    case = PARITY[0]
+    a = make_sim(case)
+    b = make_sim(case, use_graph=True)
+    for s in (a, b):
+        init_sim(s, case)
+        s.step(37)
+    np.testing.assert_array_equal(a.populations(raw=True), b.populations(raw=True))
+
+
+def test_nan_detection():
+    from paper_2001_11806_b200 import lbm as L
+    case = Case("nan", (8, 8, 8), 19, "srt", (1.8,), "f64")
+    sim = make_sim(case, check_nan_every=1)
+    init_sim(sim, case)
+    f = sim.populations()
+    f[3, 2, 2, 2] = np.nan
+    sim.set_populations(f)
+    with pytest.raises(L.LBMError) as e:
+        sim.step(2)
+    assert e.value.status == L.LBM_ENAN
+
+
+# -----------------------------------------------------------------------------------------
+# Slab decomposition (loopback slabs on one GPU run the same kernels as NCCL ranks)
+# -----------------------------------------------------------------------------------------
+@pytest.mark.parametrize("P", [2, 4])
+@pytest.mark.parametrize("halo_mode", [0, 1])
+def test_slab_decomposition_bit_identical(P, halo_mode):
+    case = Case("dec", (20, 16, 16), 19, "trt", (1.6, 0.5), "f64", force=(1e-5, 0, 0), geometry="channel", steps=30)
+    one = make_sim(case)
+    many = make_sim(case, n_local_slabs=P, halo_mode=halo_mode)
+    for s in (one, many):
+        init_sim(s, case)
+        s.step(case.steps)
+    np.testing.assert_array_equal(one.populations(raw=True), many.populations(raw=True))
+    # and host-array init goes through the ghost exchange
+    many2 = make_sim(case, n_local_slabs=P, halo_mode=halo_mode)
+    init_sim(many2, case, use_random_kernel=False)
+    many2.step(case.steps)
+    np.testing.assert_array_equal(one.populations(raw=True), many2.populations(raw=True))
+
+
+@pytest.mark.parametrize("Q,op,rates,dtype", [(27, "cumulant", (1.95,), "f64"), (19, "srt", (1.8,), "f32")])
+def test_slab_decomposition_other_ops(Q, op, rates, dtype):
+    case = Case("dec2", (12, 10, 12), Q, op, rates, dtype, steps=9)
+    one = make_sim(case)
+    many = make_sim(case, n_local_slabs=3)
+    for s in (one, many):
+        init_sim(s, case)
+        s.step(case.steps)
+    np.testing.assert_array_equal(one.populations(raw=True), many.populations(raw=True))
+
+
+# -----------------------------------------------------------------------------------------
+# Full BASELINE sizes (the launch configuration bench.py times): sampled cells vs the oracle
+# evaluated on the (2k+1)^3 neighbourhood each sample depends on after k steps.
+# -----------------------------------------------------------------------------------------
+def _sample_cells(case, n=48, seed=5):
+    rng = np.random.default_rng(seed)
+    nx, ny, nz = case.shape
+    pts = [(rng.integers(nx), rng.integers(ny), rng.integers(nz)) for _ in range(n)]
+    # boundary-adjacent and domain-edge cells
+    pts += [(0, 1, 0), (nx - 1, ny - 2, nz - 1), (nx // 2, 1, nz // 2), (1, ny - 2, nz - 2), (nx - 1, 0, 0)]
+    fl = case.flags()
+    return [p for p in pts if fl is None or fl[p[2], p[1], p[0]] == 0]
+
+
+def _oracle_at(case, pts, k):
+    nx, ny, nz = case.shape
+    B = 2 * k + 1
+    out = []
+    gfl = case.flags()
+    prof, amp = case.profile()
+    for (x, y, z) in pts:
+        xs = np.arange(x - k, x + k + 1)
+        ys = np.arange(y - k, y + k + 1)
+        zs = np.arange(z - k, z + k + 1)
+        Z, Y, X = np.meshgrid(zs, ys, xs, indexing="ij")
+        fl = None if gfl is None else np.ascontiguousarray(gfl[Z % nz, Y % ny, X % nx])
+        d = O.Domain(case.method(nthreads=1), B, B, B, flags=fl)
+        if case.init == "rest":
+            rho, u = np.ones((B, B, B)), np.zeros((3, B, B, B))
+        else:
+            rho, u = LI.fields_at(case.seed, nx, ny, nz, X, Y, Z, case.rho_amp, case.u_amp, prof, amp)
+        f0 = d.init_equilibrium(rho, u)
+        f = d.run_push(f0, k) if case.pattern == "aa" else d.run_pull(f0, k)
+        out.append(f[:, k, k, k])
+    return np.array(out).T
+
+
+@pytest.mark.parametrize("name", ["c0", "c1_f64", "c1_f32", "c2", "c3", "c4"])
+def test_full_size_sampled_parity(name):
+    base = FULL[name]
+    # random near-equilibrium start (instead of rest) so every sampled cell does non-trivial work
+    case = Case(base.name, base.shape, base.Q, base.op, base.rates, base.dtype, base.pattern, base.force,
+                base.geometry, base.ubb, init="shear" if base.init == "shear" else "random",
+                rho_amp=base.rho_amp if base.init == "shear" else 1e-3, u_amp=base.u_amp if base.init == "shear" else 0.01)
+    k = 2 if case.pattern == "aa" else 3
+    sim = make_sim(case)
+    init_sim(sim, case)
+    sim.step(k)
+    pts = _sample_cells(case)
+    nx, ny, _ = case.shape
+    idx = np.array([x + nx * (y + ny * z) for (x, y, z) in pts], np.int64)
+    got = sim.populations_at(idx)
+    ref = _oracle_at(case, pts, k)
+    err = float(np.max(np.abs(got - ref) / np.abs(ref)))
+    assert err <= TOL[case.dtype], err
+    sim.close()
