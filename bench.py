@@ -256,7 +256,10 @@ def main():
             buf.copy_(torch.frombuffer(bytearray(L.nccl_unique_id()), dtype=torch.uint8))
         dist.broadcast(buf, 0)
         nccl_id = bytes(buf.cpu().numpy().tobytes())
-    stream = torch.cuda.current_stream()
+    # a dedicated (non-default) torch stream: the library launches every kernel on it, so CUDA
+    # events recorded on it bracket exactly our kernels (the legacy default stream's handle is 0)
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
     small = np.prod(gshape) / P <= 2 ** 21
     use_graph = bool(small) if args.graph < 0 else bool(args.graph)
     sim = L.Simulation(gshape, stencil=cfg["Q"], collision=cfg["op"], rates=cfg["rates"], dtype=cfg["dtype"],
