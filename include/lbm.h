@@ -171,6 +171,13 @@ int lbm_slab_plan(int64_t nz, int32_t nranks, int32_t rank, int64_t out[4]);
 /* Crossing directions of a z face: writes the stencil indices q with c_qz == dir into q_out
  * (ascending) and returns their count (5 for D3Q19, 9 for D3Q27), or LBM_EINVAL. */
 int lbm_crossing_directions(int32_t stencil, int32_t dir, int32_t *q_out);
+/* Host-only zero-copy halo schedule of `rank` in a decomposition over nranks ranks with nz_local
+ * interior planes: the point-to-point operations one step posts inside one NCCL group, in posting
+ * order. Row k of `out` (4 int32 each): {kind (0 = send, 1 = recv), peer rank, q, storage plane}
+ * where storage plane 0 is the lower ghost plane, 1..nz_local the interior, nz_local + 1 the upper
+ * ghost plane; each message is the contiguous nx*ny run of population q in that plane. Returns the
+ * number of operations (4 * n_cross) or LBM_EINVAL (also if cap is too small). */
+int lbm_halo_schedule(int32_t stencil, int64_t nz_local, int32_t rank, int32_t nranks, int32_t *out, int32_t cap);
 /* Direction table of a stencil in ABI order: c_out[3*q + d], w_out[q]. Returns Q or LBM_EINVAL. */
 int lbm_stencil_table(int32_t stencil, int32_t *c_out, double *w_out);
 

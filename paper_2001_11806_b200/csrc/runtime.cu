@@ -153,6 +153,24 @@ void launch_aa(lbm_handle_s *h, Slab &s, int odd, cudaStream_t st) {
     h->launches++;
 }
 
+// Zero-copy halo schedule (posting order inside one NCCL group). Per peer pair the sends of one
+// side and the receives of the other are posted in the same order, so NCCL matches them even when
+// the up and down neighbours are the same rank (P = 2).
+struct HaloOp {
+    int kind, peer, q, zs;  // kind 0 = send, 1 = recv
+};
+
+std::vector<HaloOp> halo_schedule(int Q, int nz, int up, int down) {
+    int qu[9], qd[9];
+    const int nu = crossing(Q, +1, qu), nd = crossing(Q, -1, qd);
+    std::vector<HaloOp> ops;
+    for (int k = 0; k < nu; ++k) ops.push_back({0, up, qu[k], nz});       // c_z = +1 leaves the top plane
+    for (int k = 0; k < nu; ++k) ops.push_back({1, down, qu[k], 0});      // ... and arrives in the lower ghost
+    for (int k = 0; k < nd; ++k) ops.push_back({0, down, qd[k], 1});      // c_z = -1 leaves the bottom plane
+    for (int k = 0; k < nd; ++k) ops.push_back({1, up, qd[k], nz + 1});   // ... and arrives in the upper ghost
+    return ops;
+}
+
 // ---- halo exchange ------------------------------------------------------------------
 // After an update that wrote array `arr` of every slab: the crossing populations of the
 // boundary planes go into the neighbours' ghost planes of the same array.
@@ -174,13 +192,30 @@ int exchange_loopback(lbm_handle_s *h, int arr_sel_cur, cudaStream_t st) {
             launch_pack(h->Q, h->dtype, g, s.pdf[arr], 1, -1, s.halo[1], false, st);
             launch_unpack(h->Q, h->dtype, gd, sd.pdf[arrd], sd.nz + 1, -1, s.halo[1], st);
             h->launches += 4;
-        } else {
-            for (int k = 0; k < nu; ++k)
-                CUDA_TRY(h, cudaMemcpyAsync(qplane(h, su, arru, up[k], 0), qplane(h, s, arr, up[k], s.nz), plane_bytes(h),
-                                            cudaMemcpyDeviceToDevice, st));
-            for (int k = 0; k < nd; ++k)
-                CUDA_TRY(h, cudaMemcpyAsync(qplane(h, sd, arrd, dn[k], sd.nz + 1), qplane(h, s, arr, dn[k], 1), plane_bytes(h),
-                                            cudaMemcpyDeviceToDevice, st));
+        }
+    }
+    if (h->cfg.halo_mode == LBM_HALO_PACKED) return LBM_OK;
+    (void)nu;
+    (void)nd;
+    // zero-copy: execute the same per-rank schedule NCCL uses; the k-th send of slab r to peer p
+    // is matched with the k-th receive of p from r (NCCL's in-order matching per peer pair)
+    std::vector<std::vector<HaloOp>> sched(P);
+    for (int r = 0; r < P; ++r) sched[r] = halo_schedule(h->Q, h->slabs[r].nz, (r + 1) % P, (r - 1 + P) % P);
+    for (int r = 0; r < P; ++r) {
+        for (int p = 0; p < P; ++p) {
+            std::vector<const HaloOp *> sends, recvs;
+            for (const HaloOp &op : sched[r])
+                if (op.kind == 0 && op.peer == p) sends.push_back(&op);
+            for (const HaloOp &op : sched[p])
+                if (op.kind == 1 && op.peer == r) recvs.push_back(&op);
+            if (sends.size() != recvs.size()) return fail(h, LBM_EINVAL, "halo schedule mismatch");
+            Slab &s = h->slabs[r];
+            Slab &d = h->slabs[p];
+            const int as = arr_sel_cur ? s.cur : 1 - s.cur;
+            const int ad = arr_sel_cur ? d.cur : 1 - d.cur;
+            for (size_t k = 0; k < sends.size(); ++k)
+                CUDA_TRY(h, cudaMemcpyAsync(qplane(h, d, ad, recvs[k]->q, recvs[k]->zs), qplane(h, s, as, sends[k]->q, sends[k]->zs),
+                                            plane_bytes(h), cudaMemcpyDeviceToDevice, st));
         }
     }
     return LBM_OK;
@@ -209,11 +244,13 @@ int exchange_nccl(lbm_handle_s *h, int arr_sel_cur, cudaStream_t st) {
         h->launches += 2;
     } else {
         // zero-copy: each crossing population's boundary plane is one contiguous nx*ny run
+        (void)nu;
+        (void)nd;
         NCCL_TRY(h, ncclGroupStart());
-        for (int k = 0; k < nu; ++k) NCCL_TRY(h, ncclSend(qplane(h, s, arr, up[k], s.nz), plane, dt, h->up, h->comm, st));
-        for (int k = 0; k < nu; ++k) NCCL_TRY(h, ncclRecv(qplane(h, s, arr, up[k], 0), plane, dt, h->down, h->comm, st));
-        for (int k = 0; k < nd; ++k) NCCL_TRY(h, ncclSend(qplane(h, s, arr, dn[k], 1), plane, dt, h->down, h->comm, st));
-        for (int k = 0; k < nd; ++k) NCCL_TRY(h, ncclRecv(qplane(h, s, arr, dn[k], s.nz + 1), plane, dt, h->up, h->comm, st));
+        for (const HaloOp &op : halo_schedule(h->Q, s.nz, h->up, h->down)) {
+            if (op.kind == 0) NCCL_TRY(h, ncclSend(qplane(h, s, arr, op.q, op.zs), plane, dt, op.peer, h->comm, st));
+            else NCCL_TRY(h, ncclRecv(qplane(h, s, arr, op.q, op.zs), plane, dt, op.peer, h->comm, st));
+        }
         NCCL_TRY(h, ncclGroupEnd());
     }
     return LBM_OK;
@@ -412,6 +449,19 @@ int lbm_crossing_directions(int32_t stencil, int32_t dir, int32_t *q_out) {
     const int n = crossing(stencil, dir, tmp);
     for (int i = 0; i < n; ++i) q_out[i] = tmp[i];
     return n;
+}
+
+int lbm_halo_schedule(int32_t stencil, int64_t nz_local, int32_t rank, int32_t nranks, int32_t *out, int32_t cap) {
+    if ((stencil != 19 && stencil != 27) || nranks < 1 || rank < 0 || rank >= nranks || nz_local < 2 || !out) return LBM_EINVAL;
+    const auto ops = halo_schedule(stencil, (int)nz_local, (rank + 1) % nranks, (rank - 1 + nranks) % nranks);
+    if ((int)ops.size() > cap) return LBM_EINVAL;
+    for (size_t i = 0; i < ops.size(); ++i) {
+        out[4 * i + 0] = ops[i].kind;
+        out[4 * i + 1] = ops[i].peer;
+        out[4 * i + 2] = ops[i].q;
+        out[4 * i + 3] = ops[i].zs;
+    }
+    return (int)ops.size();
 }
 
 int lbm_stencil_table(int32_t stencil, int32_t *c_out, double *w_out) {

@@ -77,6 +77,7 @@ _SIGS = {
     "lbm_slab_plan": ([_I64, _I32, _I32, _P], C.c_int),
     "lbm_crossing_directions": ([_I32, _I32, _P], C.c_int),
     "lbm_stencil_table": ([_I32, _P, _P], C.c_int),
+    "lbm_halo_schedule": ([_I32, _I64, _I32, _I32, _P, _I32], C.c_int),
     "lbm_strerror": ([C.c_int], C.c_char_p),
     "lbm_last_error": ([_P], C.c_char_p),
     "lbm_version": ([], C.c_char_p),
@@ -125,6 +126,15 @@ def stencil_table(stencil: int):
     w = np.zeros(stencil, np.float64)
     _check(lbm_stencil_table(stencil, c.ctypes.data, w.ctypes.data), what="lbm_stencil_table")
     return c.reshape(stencil, 3), w
+
+
+def halo_schedule(stencil: int, nz_local: int, rank: int, nranks: int):
+    """Zero-copy halo operations of one step in NCCL posting order: (kind, peer, q, plane) with
+    kind 0 = send, 1 = recv; plane 0 / nz_local+1 are the ghost planes."""
+    out = np.zeros((64, 4), np.int32)
+    n = lbm_halo_schedule(stencil, nz_local, rank, nranks, out.ctypes.data, 64)
+    _check(n, what="lbm_halo_schedule")
+    return [tuple(int(v) for v in r) for r in out[:n]]
 
 
 def nccl_unique_id() -> bytes:
