@@ -46,15 +46,18 @@ def _stale(target, deps):
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, defines=(), out: str = OUT) -> str:
+    """Compile and link; `defines` (e.g. ["LBM_PULL_MINB=3"]) and `out` build experiment variants."""
     deps = _deps()
-    if not force and not _stale(OUT, deps + [__file__]):
-        return OUT
-    os.makedirs(OBJ, exist_ok=True)
-    flags = _flags()
+    if not force and not _stale(out, deps + [__file__]):
+        return out
+    tag = "_".join(d.replace("=", "") for d in defines)
+    obj_dir = OBJ + ("_" + tag if tag else "")
+    os.makedirs(obj_dir, exist_ok=True)
+    flags = _flags() + [f"-D{d}" for d in defines]
 
     def compile_one(src):
-        obj = os.path.join(OBJ, src.replace(".cu", ".o"))
+        obj = os.path.join(obj_dir, src.replace(".cu", ".o"))
         cmd = [NVCC, "-c", os.path.join(CSRC, src), "-o", obj] + flags
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
@@ -66,15 +69,15 @@ def build(force: bool = False, verbose: bool = False) -> str:
     with cf.ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
         objs = list(ex.map(compile_one, SOURCES))
     _, libdir = nccl_dirs()
-    cmd = [NVCC, "-shared", "-o", OUT + ".tmp"] + objs + ARCH + [
+    cmd = [NVCC, "-shared", "-o", out + ".tmp"] + objs + ARCH + [
         "-L", libdir, "-l:libnccl.so.2", "-Xlinker", f"-rpath,{libdir}", "-Xcompiler", "-fPIC"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stderr[-4000:]}")
-    os.replace(OUT + ".tmp", OUT)
+    os.replace(out + ".tmp", out)
     if verbose:
-        print(f"built {OUT}")
-    return OUT
+        print(f"built {out}")
+    return out
 
 
 if __name__ == "__main__":

@@ -154,38 +154,72 @@ __device__ __forceinline__ void collide_mrt19(T (&g)[19], const Rates<T> &p) {
     const T inv = T(1) / rho;
     const T ux = jx * inv, uy = jy * inv, uz = jz * inv;
     const T uu15 = T(1.5) * (ux * ux + uy * uy + uz * uz);
-    T d[19];
+    // Non-equilibrium part d = g - g_eq, split over the direction pairs (q, qbar): even moment
+    // polynomials (shear, bulk, order 4) see only dp = d_q + d_qbar, odd ones (order 3) only
+    // dm = d_q - d_qbar — half the work of the plain 15 x 19 transform.
+    const T w0 = T(S::w(0));
+    const T d0 = g[0] - (w0 * drho - w0 * rho * uu15);
+    T dp[19], dm[19];
 #pragma unroll
-    for (int q = 0; q < 19; ++q) {
-        const T w = T(S::w(q));
-        const T cu = T(S::cx(q)) * ux + T(S::cy(q)) * uy + T(S::cz(q)) * uz;
-        const T eq = w * drho + w * rho * (T(3) * cu + T(4.5) * cu * cu - uu15);
-        d[q] = g[q] - eq;
+    for (int q = 1; q < 19; ++q) {
+        if (q < S::opp(q)) {
+            const int b = S::opp(q);
+            const T w = T(S::w(q));
+            const T cu = T(S::cx(q)) * ux + T(S::cy(q)) * uy + T(S::cz(q)) * uz;
+            const T wr = w * rho;
+            const T eqs = w * drho + wr * (T(4.5) * cu * cu - uu15);
+            const T eqa = wr * T(3) * cu;
+            dp[q] = (g[q] + g[b]) - T(2) * eqs;
+            dm[q] = (g[q] - g[b]) - T(2) * eqa;
+        }
     }
     T a[15];
 #pragma unroll
     for (int k = 0; k < 15; ++k) {
+        const bool odd = (k >= 6 && k <= 11);
         T m = T(0);
+        if (!odd) {
+            const int c0 = mrt_poly(k, 0, 0, 0);
+            if (c0 != 0) m = T(c0) * d0;
+        }
 #pragma unroll
-        for (int q = 0; q < 19; ++q) {
-            const int c = mrt_poly(k, S::cx(q), S::cy(q), S::cz(q));
-            if (c == 1) m += d[q];
-            else if (c == -1) m -= d[q];
-            else if (c != 0) m += T(c) * d[q];
+        for (int q = 1; q < 19; ++q) {
+            if (q < S::opp(q)) {
+                const int c = mrt_poly(k, S::cx(q), S::cy(q), S::cz(q));
+                const T v = odd ? dm[q] : dp[q];
+                if (c == 1) m += v;
+                else if (c == -1) m -= v;
+                else if (c != 0) m += T(c) * v;
+            }
         }
         a[k] = p.r[mrt_group(k)] * T(mrt_inv_norm(k)) * m;
     }
-#pragma unroll
-    for (int q = 0; q < 19; ++q) {
+    {
         T s = T(0);
 #pragma unroll
         for (int k = 0; k < 15; ++k) {
-            const int c = mrt_poly(k, S::cx(q), S::cy(q), S::cz(q));
-            if (c == 1) s += a[k];
-            else if (c == -1) s -= a[k];
-            else if (c != 0) s += T(c) * a[k];
+            const int c = mrt_poly(k, 0, 0, 0);
+            if (c != 0) s += T(c) * a[k];
         }
-        g[q] -= T(S::w(q)) * s;
+        g[0] -= w0 * s;
+    }
+#pragma unroll
+    for (int q = 1; q < 19; ++q) {
+        if (q < S::opp(q)) {
+            const int b = S::opp(q);
+            T se = T(0), so = T(0);
+#pragma unroll
+            for (int k = 0; k < 15; ++k) {
+                const int c = mrt_poly(k, S::cx(q), S::cy(q), S::cz(q));
+                T &acc = (k >= 6 && k <= 11) ? so : se;
+                if (c == 1) acc += a[k];
+                else if (c == -1) acc -= a[k];
+                else if (c != 0) acc += T(c) * a[k];
+            }
+            const T w = T(S::w(q));
+            g[q] -= w * (se + so);
+            g[b] -= w * (se - so);
+        }
     }
 }
 

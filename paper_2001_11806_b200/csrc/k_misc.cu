@@ -53,41 +53,40 @@ void launch_unpack(int Q, int dtype, const Geo &geo, void *f, int zs, int dir, c
     LBM_DISPATCH(Q, dtype, (k_unpack<QQ, T><<<blocks_for(n), 256, 0, s>>>(geo, static_cast<T *>(f), zs, dir, static_cast<const T *>(in))));
 }
 
-__global__ void k_rowany(const Geo geo, int nplanes, const uint8_t *__restrict__ flags, uint8_t *__restrict__ rowany) {
-    const int64_t rows = (int64_t)nplanes * geo.ny;
-    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < rows; r += (int64_t)gridDim.x * blockDim.x) {
-        const uint8_t *row = flags + r * geo.nx;
-        uint8_t any = 0;
-        for (int x = 0; x < geo.nx; ++x) any |= (row[x] != 0);
-        rowany[r] = any;
-    }
-}
-
-__global__ void k_rowmask(const Geo geo, int nplanes, const uint8_t *__restrict__ rowany, uint8_t *__restrict__ rowmask) {
-    const int64_t rows = (int64_t)nplanes * geo.ny;
-    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < rows; r += (int64_t)gridDim.x * blockDim.x) {
-        const int zs = (int)(r / geo.ny), y = (int)(r % geo.ny);
-        uint8_t m = 0;
-        for (int dz = -1; dz <= 1; ++dz) {
-            int z2 = zs + dz;
-            if (geo.g) {
-                if (z2 < 0 || z2 >= nplanes) continue;  // outside the storage: never read
-            } else {
-                z2 = (z2 + nplanes) % nplanes;
+__global__ void k_mark_near_wall(const Geo geo, int nplanes, const uint8_t *__restrict__ in, uint8_t *__restrict__ out) {
+    const int64_t plane = (int64_t)geo.nx * geo.ny;
+    const int64_t n = plane * nplanes;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int zs = (int)(i / plane);
+        const int y = (int)((i / geo.nx) % geo.ny);
+        const int x = (int)(i % geo.nx);
+        uint8_t v = in[i] & 3;
+        if (v == 0) {
+            bool near = false;
+            for (int dz = -1; dz <= 1; ++dz) {
+                int z2 = zs + dz;
+                if (geo.g) {
+                    if (z2 < 0 || z2 >= nplanes) continue;
+                } else {
+                    z2 = (z2 + nplanes) % nplanes;
+                }
+                for (int dy = -1; dy <= 1; ++dy) {
+                    const int y2 = (y + dy + geo.ny) % geo.ny;
+                    for (int dx = -1; dx <= 1; ++dx) {
+                        const int x2 = (x + dx + geo.nx) % geo.nx;
+                        near |= (in[(int64_t)z2 * plane + (int64_t)y2 * geo.nx + x2] & 3) != 0;
+                    }
+                }
             }
-            for (int dy = -1; dy <= 1; ++dy) {
-                const int y2 = (y + dy + geo.ny) % geo.ny;
-                m |= rowany[(int64_t)z2 * geo.ny + y2];
-            }
+            if (near) v |= 0x80;
         }
-        rowmask[r] = m;
+        out[i] = v;
     }
 }
 
-void launch_rowmask(const Geo &geo, int nplanes, const uint8_t *flags, uint8_t *tmp, uint8_t *rowmask, cudaStream_t s) {
-    const int64_t rows = (int64_t)nplanes * geo.ny;
-    k_rowany<<<blocks_for(rows), 256, 0, s>>>(geo, nplanes, flags, tmp);
-    k_rowmask<<<blocks_for(rows), 256, 0, s>>>(geo, nplanes, tmp, rowmask);
+void launch_mark_near_wall(const Geo &geo, int nplanes, const uint8_t *in, uint8_t *out, cudaStream_t s) {
+    const int64_t n = (int64_t)geo.nx * geo.ny * nplanes;
+    k_mark_near_wall<<<blocks_for(n), 256, 0, s>>>(geo, nplanes, in, out);
 }
 
 void launch_nan_check(int dtype, const void *f, int64_t n, int *flag, cudaStream_t s) {

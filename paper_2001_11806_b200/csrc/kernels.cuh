@@ -13,7 +13,32 @@
 #include "collide.cuh"
 #include "stencil.cuh"
 
+// Minimum resident 256-thread blocks per SM requested from ptxas; it caps registers per thread
+// (2 -> 128, 3 -> 80, 4 -> 64, 6 -> 40) and so sets how many population loads are in flight per SM.
+// Measured on B200 (scripts/gpu_sweep.sh): D3Q19 TRT fp64 3 (c4 1.03 of copy
+// BW, c1 0.98), D3Q19 TRT fp32 6 (c1 0.92), D3Q27 cumulant fp64 3 (c3 0.67), MRT fp32 AA 3 (c2
+// 0.75); other families use the largest value without register spills. LBM_MINB_OVERRIDE_* exist
+// for sweeps only.
 namespace lbm {
+
+template <int Q, int OP, typename T>
+struct MinBlocks {
+    static constexpr bool f64 = sizeof(T) == 8;
+    static constexpr int pull_default =
+        f64 ? ((OP == 2 || (Q == 27 && OP <= 1)) ? 2 : 3)
+            : ((OP <= 1 || OP == 4) ? (Q == 19 ? 6 : 4) : 3);
+    static constexpr int aa_default = f64 ? 2 : ((OP == 2 || (Q == 19 && OP <= 1)) ? 3 : 2);
+#ifdef LBM_MINB_OVERRIDE_PULL
+    static constexpr int pull = LBM_MINB_OVERRIDE_PULL;
+#else
+    static constexpr int pull = pull_default;
+#endif
+#ifdef LBM_MINB_OVERRIDE_AA
+    static constexpr int aa = LBM_MINB_OVERRIDE_AA;
+#else
+    static constexpr int aa = aa_default;
+#endif
+};
 
 struct Geo {
     int nx, ny, nz;  // local interior extent
@@ -28,8 +53,9 @@ struct StepArgs {
     double rates[8];
     double F[3];
     double uw[3];                  // UBB wall velocity; rho_w = 1 (G8)
-    const uint8_t *flags;          // storage-indexed (with ghost planes) or nullptr
-    const uint8_t *rowmask;        // per storage row (zs*ny + y): 1 if a non-fluid cell is within 1
+    const uint8_t *flags;          // storage-indexed (with ghost planes) or nullptr; bits 0-1 = type
+                                   // (0 fluid, 1 no-slip, 2 UBB), bit 7 = fluid cell with a non-fluid
+                                   // neighbour (only such cells read neighbour flags)
 };
 
 template <typename T>
@@ -81,7 +107,7 @@ __device__ __forceinline__ uint32_t nb_off(const Geo &g, const Nbr &n, int dx, i
 // z = z_begin + blockIdx.z * z_step. Wall cells are not written.
 // =======================================================================================
 template <int Q, int OP, typename T, bool FLAGS, bool FORCE>
-__global__ void __launch_bounds__(256) k_pull(const StepArgs a, const T *__restrict__ src, T *__restrict__ dst) {
+__global__ void __launch_bounds__(256, (MinBlocks<Q, OP, T>::pull)) k_pull(const StepArgs a, const T *__restrict__ src, T *__restrict__ dst) {
     using S = Stencil<Q>;
     const int x = blockIdx.x * blockDim.x + threadIdx.x;
     const int y = blockIdx.y * blockDim.y + threadIdx.y;
@@ -92,8 +118,9 @@ __global__ void __launch_bounds__(256) k_pull(const StepArgs a, const T *__restr
     const int64_t Sq = a.geo.Sq;
     bool edge = false;
     if (FLAGS) {
-        if (a.flags[self] != 0) return;
-        edge = a.rowmask[(uint32_t)zs * (uint32_t)a.geo.ny + (uint32_t)y] != 0;
+        const uint8_t own = a.flags[self];
+        if (own & 3) return;  // wall cells are not updated
+        edge = (own & 0x80) != 0;
     }
     T g[Q];
 #pragma unroll
@@ -101,7 +128,7 @@ __global__ void __launch_bounds__(256) k_pull(const StepArgs a, const T *__restr
         // pull from x - c_q
         const uint32_t o = nb_off(a.geo, n, -S::cx(q), -S::cy(q), -S::cz(q));
         if (FLAGS && edge) {
-            const uint8_t fl = a.flags[o];
+            const uint8_t fl = a.flags[o] & 3;
             if (fl == 0) {
                 g[q] = ldg_stream(src + q * Sq + o);
             } else {
@@ -128,7 +155,7 @@ __global__ void __launch_bounds__(256) k_pull(const StepArgs a, const T *__restr
 // odd : read a[x - c_q](qbar), collide, write a[x + c_q](q)
 // =======================================================================================
 template <int Q, int OP, typename T, bool FORCE>
-__global__ void __launch_bounds__(256) k_aa_even(const StepArgs a, T *__restrict__ f) {
+__global__ void __launch_bounds__(256, (MinBlocks<Q, OP, T>::aa)) k_aa_even(const StepArgs a, T *__restrict__ f) {
     using S = Stencil<Q>;
     const int x = blockIdx.x * blockDim.x + threadIdx.x;
     const int y = blockIdx.y * blockDim.y + threadIdx.y;
@@ -146,7 +173,7 @@ __global__ void __launch_bounds__(256) k_aa_even(const StepArgs a, T *__restrict
 }
 
 template <int Q, int OP, typename T, bool FORCE>
-__global__ void __launch_bounds__(256) k_aa_odd(const StepArgs a, T *__restrict__ f) {
+__global__ void __launch_bounds__(256, (MinBlocks<Q, OP, T>::aa)) k_aa_odd(const StepArgs a, T *__restrict__ f) {
     using S = Stencil<Q>;
     const int x = blockIdx.x * blockDim.x + threadIdx.x;
     const int y = blockIdx.y * blockDim.y + threadIdx.y;
@@ -380,10 +407,9 @@ __global__ void k_unpack(const Geo geo, T *__restrict__ f, int zs, int dir, cons
 // =======================================================================================
 // Flag preprocessing and diagnostics
 // =======================================================================================
-// rowany[zs*ny + y] = 1 if any cell of the storage row is not fluid
-__global__ void k_rowany(const Geo geo, int nplanes, const uint8_t *__restrict__ flags, uint8_t *__restrict__ rowany);
-// rowmask = OR of rowany over the 3x3 (dy, dz) neighbourhood (y wraps; z wraps without ghosts)
-__global__ void k_rowmask(const Geo geo, int nplanes, const uint8_t *__restrict__ rowany, uint8_t *__restrict__ rowmask);
+// out = in | 0x80 for fluid cells with a non-fluid cell among their 26 neighbours (x, y wrap; z wraps
+// without ghost planes; ghost planes themselves are never updated)
+__global__ void k_mark_near_wall(const Geo geo, int nplanes, const uint8_t *__restrict__ in, uint8_t *__restrict__ out);
 
 template <typename T>
 __global__ void k_nan_check(const T *__restrict__ f, int64_t n, int *__restrict__ flag) {

@@ -25,7 +25,6 @@ struct Slab {
     int nz = 0;           // interior planes
     void *pdf[2] = {nullptr, nullptr};
     uint8_t *flags = nullptr;    // storage-indexed, with ghost planes
-    uint8_t *rowmask = nullptr;  // per storage row
     void *halo[4] = {nullptr, nullptr, nullptr, nullptr};  // packed mode: send up, send down, recv below, recv above
     int cur = 0;          // index of the array holding the current state (pull)
 };
@@ -135,7 +134,6 @@ void launch_pull_range(lbm_handle_s *h, Slab &s, int z_begin, int nplanes, int z
     a.z_begin = z_begin;
     a.z_step = z_step;
     a.flags = s.flags;
-    a.rowmask = s.rowmask;
     tbegin(h, st);
     h->pull(a, s.pdf[s.cur], s.pdf[1 - s.cur], grid_for(h, nplanes), h->block, st);
     tend(h, st);
@@ -609,13 +607,12 @@ int lbm_create(const lbm_config *cfg, lbm_handle *out) {
                 std::memcpy(&hf[(size_t)zs * h->nx * h->ny], cfg->flags + (size_t)zg * h->nx * h->ny, (size_t)h->nx * h->ny);
             }
             uint8_t *tmp = nullptr;
-            if (cudaMalloc(&s.flags, cells) != cudaSuccess || cudaMalloc(&s.rowmask, (size_t)nplanes * h->ny) != cudaSuccess ||
-                cudaMalloc(&tmp, (size_t)nplanes * h->ny) != cudaSuccess) {
+            if (cudaMalloc(&s.flags, cells) != cudaSuccess || cudaMalloc(&tmp, cells) != cudaSuccess) {
                 h->err = "cudaMalloc flags";
                 return bail(LBM_EOOM);
             }
-            cudaMemcpy(s.flags, hf.data(), cells, cudaMemcpyHostToDevice);
-            launch_rowmask(g, nplanes, s.flags, tmp, s.rowmask, h->stream);
+            cudaMemcpy(tmp, hf.data(), cells, cudaMemcpyHostToDevice);
+            launch_mark_near_wall(g, nplanes, tmp, s.flags, h->stream);
             cudaStreamSynchronize(h->stream);
             cudaFree(tmp);
         }
@@ -651,7 +648,6 @@ int lbm_destroy(lbm_handle h) {
         for (void *p : s.pdf) if (p) cudaFree(p);
         for (void *p : s.halo) if (p) cudaFree(p);
         if (s.flags) cudaFree(s.flags);
-        if (s.rowmask) cudaFree(s.rowmask);
     }
     if (h->comm) ncclCommDestroy(h->comm);
     for (cudaEvent_t e : h->timing.ev) cudaEventDestroy(e);

@@ -16,7 +16,8 @@ from typing import Optional, Sequence
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIBPATH = os.path.join(HERE, "liblbm_b200.so")
+# LBM_B200_LIB selects an experiment build variant (same ABI); default: the in-tree library
+LIBPATH = os.environ.get("LBM_B200_LIB") or os.path.join(HERE, "liblbm_b200.so")
 
 LBM_OK, LBM_EINVAL, LBM_EUNSUPPORTED, LBM_ECUDA, LBM_ENCCL, LBM_ENAN, LBM_EOOM = 0, -1, -2, -3, -4, -5, -6
 D3Q19, D3Q27 = 19, 27
