@@ -220,6 +220,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=0, help="LB steps per e2e job (0 = the config's step count)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--halo-mode", type=int, default=0)
+    ap.add_argument("--nccl-self", type=int, default=0,
+                    help="N=1 only: ghost planes exchanged through a 1-rank NCCL communicator (times the multi-GPU path)")
     ap.add_argument("--block-x", type=int, default=0)
     ap.add_argument("--graph", type=int, default=-1, help="CUDA-graph capture (default: on for small domains)")
     args = ap.parse_args()
@@ -262,10 +264,13 @@ def main():
     torch.cuda.set_stream(stream)
     small = np.prod(gshape) / P <= 2 ** 21
     use_graph = bool(small) if args.graph < 0 else bool(args.graph)
+    nccl_self = bool(args.nccl_self) and world == 1
+    use_graph = use_graph and not nccl_self
     sim = L.Simulation(gshape, stencil=cfg["Q"], collision=cfg["op"], rates=cfg["rates"], dtype=cfg["dtype"],
                        pattern=cfg["pattern"], force=cfg["force"], flags=flags, ubb_velocity=cfg.get("ubb", (0, 0, 0)),
                        periodic=periodic, rank=rank, nranks=world, nccl_id=nccl_id, device=local,
-                       stream=stream.cuda_stream, halo_mode=args.halo_mode, use_graph=use_graph, block_x=args.block_x)
+                       stream=stream.cuda_stream, halo_mode=args.halo_mode, use_graph=use_graph, block_x=args.block_x,
+                       nccl_self=nccl_self)
     kind = cfg["init"][0]
     if kind == "rest":
         sim.init_equilibrium(torch.ones(sim.cells, dtype=torch.float64, device="cuda"),
@@ -363,7 +368,8 @@ def main():
             "data": "synthetic",
             "config": {"workload": args.config, "desc": cfg["desc"], "global": list(gshape),
                        "per_gpu_mlups": mlups / world, "pattern": cfg["pattern"],
-                       "parallelism": f"z-slab x{world}" if world > 1 else "single GPU",
+                       "parallelism": f"z-slab x{world}" if world > 1 else
+                       ("single GPU, NCCL self-exchange of ghost planes" if nccl_self else "single GPU"),
                        "l2": "inputs larger than L2 (no flush)" if not small else "L2-resident (launch-bound config)",
                        "halo_mode": "zerocopy" if args.halo_mode == 0 else "packed", "cuda_graph": use_graph},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,

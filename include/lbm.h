@@ -99,6 +99,9 @@ typedef struct lbm_config {
     int32_t use_graph;      /* 1 = capture a two-step cycle in a CUDA graph (single slab only) */
     int32_t block_x;        /* threads per block along x (0 = default) */
     int32_t check_nan_every;/* >0: check for NaN every k steps inside lbm_step (LBM_ENAN) */
+    int32_t nccl_self;      /* nranks == 1 only: keep ghost planes and exchange them through a
+                               1-rank NCCL communicator (self send/recv) instead of wrapping z
+                               locally — exercises and times the multi-GPU exchange path on 1 GPU */
 } lbm_config;
 
 typedef struct lbm_handle_s *lbm_handle;

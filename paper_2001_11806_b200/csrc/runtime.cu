@@ -47,6 +47,7 @@ struct lbm_handle_s {
     cudaEvent_t ev_bnd = nullptr, ev_x = nullptr;
     ncclComm_t comm = nullptr;
     int rank = 0, nranks = 1, up = 0, down = 0;
+    bool use_nccl = false;  // nranks > 1, or the 1-rank self-exchange variant
     bool have_flags = false, have_force = false;
     PullLaunch pull = nullptr;
     AALaunch aa = nullptr;
@@ -257,7 +258,7 @@ int exchange_nccl(lbm_handle_s *h, int arr_sel_cur, cudaStream_t st) {
 // exchange the CURRENT state's ghost planes (after init / set_populations), synchronously ordered on stream
 int exchange_current(lbm_handle_s *h) {
     if (h->g == 0) return LBM_OK;
-    if (h->nranks > 1) return exchange_nccl(h, 1, h->stream);
+    if (h->use_nccl) return exchange_nccl(h, 1, h->stream);
     return exchange_loopback(h, 1, h->stream);
 }
 
@@ -276,7 +277,7 @@ int step_once(lbm_handle_s *h) {
         s.cur ^= 1;
         return LBM_OK;
     }
-    if (h->nranks == 1) {
+    if (!h->use_nccl) {
         // loopback slabs on one GPU, one stream: boundary planes, exchange, interior
         for (Slab &s : h->slabs) launch_pull_range(h, s, 0, 2, s.nz - 1, st);
         int rc = exchange_loopback(h, 0, st);
@@ -345,6 +346,9 @@ int validate(const lbm_config *c) {
     if (c->global[2] % P != 0) return fail(nullptr, LBM_EINVAL, "nz % nranks != 0");
     if (P > 1 && c->global[2] / P < 2) return fail(nullptr, LBM_EINVAL, "slabs need at least 2 planes");
     if (c->nranks > 1 && !c->nccl_id) return fail(nullptr, LBM_EINVAL, "nranks > 1 needs an nccl_id");
+    if (c->nccl_self && (c->nranks != 1 || c->n_local_slabs > 1 || c->global[2] < 2))
+        return fail(nullptr, LBM_EINVAL, "nccl_self needs nranks == 1, one slab and nz >= 2");
+    if (c->nccl_self && c->pattern == LBM_AA) return fail(nullptr, LBM_EUNSUPPORTED, "AA with slab decomposition is not implemented yet");
     const int64_t planes = c->global[2] / P + (P > 1 ? 2 : 0);
     if ((double)c->global[0] * c->global[1] * planes >= 2147483647.0)
         return fail(nullptr, LBM_EINVAL, "slab too large for 32-bit in-plane offsets (split it over more slabs)");
@@ -500,7 +504,8 @@ int lbm_create(const lbm_config *cfg, lbm_handle *out) {
     h->rank = cfg->nranks > 1 ? cfg->rank : 0;
     h->nranks = cfg->nranks;
     const int P = cfg->nranks > 1 ? cfg->nranks : (cfg->n_local_slabs > 1 ? cfg->n_local_slabs : 1);
-    h->g = P > 1 ? 1 : 0;
+    h->use_nccl = cfg->nranks > 1 || cfg->nccl_self;
+    h->g = (P > 1 || h->use_nccl) ? 1 : 0;
     h->have_flags = cfg->flags != nullptr;
     h->have_force = cfg->force[0] != 0 || cfg->force[1] != 0 || cfg->force[2] != 0;
 
@@ -617,14 +622,19 @@ int lbm_create(const lbm_config *cfg, lbm_handle *out) {
             cudaFree(tmp);
         }
     }
-    if (cfg->nranks > 1) {
+    if (h->use_nccl) {
         int64_t plan[4];
-        lbm_slab_plan(h->nzg, cfg->nranks, cfg->rank, plan);
+        lbm_slab_plan(h->nzg, cfg->nranks, h->rank, plan);
         h->down = (int)plan[2];
         h->up = (int)plan[3];
         ncclUniqueId id;
-        std::memcpy(&id, cfg->nccl_id, sizeof(id));
-        ncclResult_t r = ncclCommInitRank(&h->comm, cfg->nranks, id, cfg->rank);
+        if (cfg->nranks > 1) {
+            std::memcpy(&id, cfg->nccl_id, sizeof(id));
+        } else if (ncclGetUniqueId(&id) != ncclSuccess) {  // 1-rank self-exchange communicator
+            h->err = "ncclGetUniqueId failed";
+            return bail(LBM_ENCCL);
+        }
+        ncclResult_t r = ncclCommInitRank(&h->comm, cfg->nranks, id, h->rank);
         if (r != ncclSuccess) {
             h->err = std::string("ncclCommInitRank: ") + ncclGetErrorString(r);
             return bail(LBM_ENCCL);

@@ -41,7 +41,7 @@ class lbm_config(C.Structure):
         ("ubb_velocity", C.c_double * 3), ("rank", C.c_int32), ("nranks", C.c_int32),
         ("nccl_id", C.c_void_p), ("n_local_slabs", C.c_int32), ("device", C.c_int32),
         ("stream", C.c_void_p), ("halo_mode", C.c_int32), ("use_graph", C.c_int32),
-        ("block_x", C.c_int32), ("check_nan_every", C.c_int32),
+        ("block_x", C.c_int32), ("check_nan_every", C.c_int32), ("nccl_self", C.c_int32),
     ]
 
 
@@ -155,7 +155,7 @@ class Simulation:
                  rank: int = 0, nranks: int = 1, nccl_id: Optional[bytes] = None,
                  n_local_slabs: int = 1, device: int = 0, stream: Optional[int] = None,
                  halo_mode: int = HALO_ZEROCOPY, use_graph: bool = False, block_x: int = 0,
-                 check_nan_every: int = 0):
+                 check_nan_every: int = 0, nccl_self: bool = False):
         cfg = lbm_config()
         lbm_config_default(C.byref(cfg))
         nx, ny, nz = shape
@@ -188,6 +188,7 @@ class Simulation:
         cfg.use_graph = int(use_graph)
         cfg.block_x = block_x
         cfg.check_nan_every = check_nan_every
+        cfg.nccl_self = int(nccl_self)
         self.cfg = cfg
         self.Q = stencil
         h = C.c_void_p()

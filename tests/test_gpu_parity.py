@@ -211,6 +211,24 @@ def test_slab_decomposition_other_ops(Q, op, rates, dtype):
     np.testing.assert_array_equal(one.populations(raw=True), many.populations(raw=True))
 
 
+@pytest.mark.parametrize("halo_mode", [0, 1])
+@pytest.mark.parametrize("Q,op,rates,geometry", [(19, "trt", (1.6, 0.5), "channel"), (27, "cumulant", (1.95,), "periodic")])
+def test_nccl_self_exchange_bit_identical(halo_mode, Q, op, rates, geometry):
+    """The NCCL exchange path (ghost planes, schedule, comm stream overlapped with the interior
+    launch, event ordering) on one GPU through a 1-rank communicator: bit-identical to local z wrap."""
+    case = Case("self", (16, 12, 10), Q, op, rates, "f64", geometry=geometry, steps=13)
+    one = make_sim(case)
+    nc = make_sim(case, nccl_self=True, halo_mode=halo_mode)
+    for s in (one, nc):
+        init_sim(s, case)
+        s.step(case.steps)
+    np.testing.assert_array_equal(one.populations(raw=True), nc.populations(raw=True))
+    nc2 = make_sim(case, nccl_self=True, halo_mode=halo_mode)
+    init_sim(nc2, case, use_random_kernel=False)  # host arrays + exchange of the initial ghosts
+    nc2.step(case.steps)
+    np.testing.assert_array_equal(one.populations(raw=True), nc2.populations(raw=True))
+
+
 # -----------------------------------------------------------------------------------------
 # Full BASELINE sizes (the launch configuration bench.py times): sampled cells vs the oracle
 # evaluated on the (2k+1)^3 neighbourhood each sample depends on after k steps.
