@@ -62,8 +62,8 @@ def lib():
             ("ora_step_push", [P, P, P, P], C.c_int),
             ("ora_stream", [P, P, P, P], C.c_int),
             ("ora_collide_all", [P, P, P], C.c_int),
-            ("ora_aa_even", [P, P], C.c_int),
-            ("ora_aa_odd", [P, P], C.c_int),
+            ("ora_aa_even", [P, P, P], C.c_int),
+            ("ora_aa_odd", [P, P, P], C.c_int),
             ("ora_init_equilibrium", [P, P, P, P], C.c_int),
             ("ora_macroscopic", [P, P, C.c_double, P, P], C.c_int),
             ("ora_collide_cell", [P, P, P], None),
@@ -193,12 +193,12 @@ class Domain:
         lib().ora_collide_all(self._pc(), _p(a), self._fl())
 
     def aa_even(self, a: np.ndarray) -> None:
-        assert self.flags is None and not self.zghost
-        assert lib().ora_aa_even(self._pc(), _p(a)) == 0
+        assert not self.zghost
+        assert lib().ora_aa_even(self._pc(), _p(a), self._fl()) == 0
 
     def aa_odd(self, a: np.ndarray) -> None:
-        assert self.flags is None and not self.zghost
-        assert lib().ora_aa_odd(self._pc(), _p(a)) == 0
+        assert not self.zghost
+        assert lib().ora_aa_odd(self._pc(), _p(a), self._fl()) == 0
 
     def run_pull(self, f0: np.ndarray, n: int) -> np.ndarray:
         """P(n) = (C o S)^n P(0) with two arrays (G11). Wall cells keep their initial values."""

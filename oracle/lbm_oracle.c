@@ -483,9 +483,11 @@ int ora_step_push(const ora_cfg *cfg, double *f, double *tmp, const uint8_t *fla
     return ora_stream(cfg, tmp, f, flags);
 }
 
-/* AA pattern (Fig. 3), single array, periodic (no flags), no ghost planes.
- * Even step: in-place collision with reversed storage: read a[x](q), write a[x](qbar). */
-int ora_aa_even(const ora_cfg *cfg, double *a) {
+/* AA pattern (Fig. 3), single array, no ghost planes, optional flag field.
+ * Even step: in-place collision with reversed storage: read a[x](q), write a[x](qbar). Wall cells
+ * are skipped; boundary conditions act in the odd step (the boundary handling follows
+ * the pattern's even/odd access scheme). */
+int ora_aa_even(const ora_cfg *cfg, double *a, const uint8_t *flags) {
     if (cfg->zghost) return -1;
     ora_stencil_t s;
     build_stencil(cfg->Q, &s);
@@ -496,6 +498,7 @@ int ora_aa_even(const ora_cfg *cfg, double *a) {
         for (int64_t y = 0; y < cfg->ny; ++y)
             for (int64_t x = 0; x < cfg->nx; ++x) {
                 int64_t self = cell(cfg, x, y, z);
+                if (flags && flags[self] != FLAG_FLUID) continue;
                 double f[27], out[27];
                 for (int q = 0; q < s.Q; ++q) f[q] = a[q * Sq + self];
                 collide(cfg, &s, f, out);
@@ -504,9 +507,20 @@ int ora_aa_even(const ora_cfg *cfg, double *a) {
     return 0;
 }
 
+/* UBB term 6 w_q rho_w c_q.u_w of direction q (G8). */
+static double ubb_term(const ora_cfg *cfg, const ora_stencil_t *s, int q) {
+    double cu = s->c[q][0] * cfg->ubb_u[0] + s->c[q][1] * cfg->ubb_u[1] + s->c[q][2] * cfg->ubb_u[2];
+    return 6.0 * s->w[q] * cfg->ubb_rho * cu;
+}
+
 /* Odd step: stream-pull, collide, stream-push: read a[x - c_q](qbar), write a[x + c_q](q).
- * Each cell reads and writes the same set of slots, so cells are independent. */
-int ora_aa_odd(const ora_cfg *cfg, double *a) {
+ * With walls (same rules as the pull streaming O6, expressed in the AA slots):
+ *   read : x - c_q a wall -> the bounced population C_qbar(x), stored by the even step in a[x](q),
+ *          plus the UBB term of q;
+ *   write: x + c_q a wall -> the population returns to x as qbar next step: a[x](qbar) = out_q plus
+ *          the UBB term of qbar.
+ * Each fluid cell reads and writes the same set of slots, so cells are independent. */
+int ora_aa_odd(const ora_cfg *cfg, double *a, const uint8_t *flags) {
     if (cfg->zghost) return -1;
     ora_stencil_t s;
     build_stencil(cfg->Q, &s);
@@ -516,12 +530,32 @@ int ora_aa_odd(const ora_cfg *cfg, double *a) {
     for (int64_t z = 0; z < cfg->nz; ++z)
         for (int64_t y = 0; y < cfg->ny; ++y)
             for (int64_t x = 0; x < cfg->nx; ++x) {
+                int64_t self = cell(cfg, x, y, z);
+                if (flags && flags[self] != FLAG_FLUID) continue;
                 double f[27], out[27];
-                for (int q = 0; q < s.Q; ++q)
-                    f[q] = a[s.opp[q] * Sq + cell(cfg, x - s.c[q][0], y - s.c[q][1], z - s.c[q][2])];
+                for (int q = 0; q < s.Q; ++q) {
+                    int64_t nb = cell(cfg, x - s.c[q][0], y - s.c[q][1], z - s.c[q][2]);
+                    uint8_t fl = flags ? flags[nb] : FLAG_FLUID;
+                    if (fl == FLAG_FLUID) {
+                        f[q] = a[s.opp[q] * Sq + nb];
+                    } else {
+                        double v = a[q * Sq + self];
+                        if (fl == FLAG_UBB) v += ubb_term(cfg, &s, q);
+                        f[q] = v;
+                    }
+                }
                 collide(cfg, &s, f, out);
-                for (int q = 0; q < s.Q; ++q)
-                    a[q * Sq + cell(cfg, x + s.c[q][0], y + s.c[q][1], z + s.c[q][2])] = out[q];
+                for (int q = 0; q < s.Q; ++q) {
+                    int64_t tg = cell(cfg, x + s.c[q][0], y + s.c[q][1], z + s.c[q][2]);
+                    uint8_t fl = flags ? flags[tg] : FLAG_FLUID;
+                    if (fl == FLAG_FLUID) {
+                        a[q * Sq + tg] = out[q];
+                    } else {
+                        double v = out[q];
+                        if (fl == FLAG_UBB) v += ubb_term(cfg, &s, s.opp[q]);
+                        a[s.opp[q] * Sq + self] = v;
+                    }
+                }
             }
     return 0;
 }

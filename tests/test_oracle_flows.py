@@ -69,6 +69,30 @@ def test_pattern_identities(op, Q, rates):
     np.testing.assert_array_equal(Pn, CF)
 
 
+@pytest.mark.parametrize("op,Q,rates", [("trt", 19, (1.6, 0.5)), ("cumulant", 27, (1.95,)), ("identity", 27, ())])
+def test_aa_with_walls_equals_push(op, Q, rates):
+    """AA with NoSlip/UBB walls (odd-step slot rules) reproduces the push pattern F(2N) bit-exactly,
+    and after an odd number of steps the reversed-slot layout plus the wall rule gives F(2N+1)."""
+    n = 7
+    fl = LI.random_obstacles(4, n, n, n, frac=0.2, ubb_frac=0.5)
+    m = O.Method(Q=Q, op=op, rates=rates, ubb_u=(0.03, -0.02, 0.01), nthreads=1)
+    d = O.Domain(m, n, n, n, flags=fl)
+    f0 = _rand_f0(d, u_amp=0.03) * (1 + 0.01 * np.random.default_rng(9).uniform(-1, 1, d.shape))
+    fluid = np.broadcast_to(fl == 0, d.shape)
+    for N in (2, 4):
+        np.testing.assert_array_equal(d.run_aa(f0, N)[fluid], d.run_push(f0, N)[fluid])
+    a = d.run_aa(f0, 3)
+    F3 = d.run_push(f0, 3)
+    c, w, opp = O.stencil_arrays(Q)
+    for q in range(Q):
+        gathered = np.roll(a[opp[q]], shift=(c[q, 2], c[q, 1], c[q, 0]), axis=(0, 1, 2))
+        nbw = np.roll(fl, shift=(c[q, 2], c[q, 1], c[q, 0]), axis=(0, 1, 2))  # flag of x - c_q
+        cu = c[q] @ np.array(m.ubb_u)
+        bounced = a[q] + np.where(nbw == LI.UBB, 6.0 * w[q] * 1.0 * cu, 0.0)
+        can = np.where(nbw == 0, gathered, bounced)
+        np.testing.assert_array_equal(can[fl == 0], F3[q][fl == 0])
+
+
 def test_aa_odd_parity_layout():
     """After an odd number of AA steps the array holds C(F(n-1)) with reversed slots:
     F(n)_q(y) = a[y - c_q](qbar) (P:864-869)."""
