@@ -14,10 +14,10 @@ PullLaunch select_pull_trt(int Q, int dtype, bool flags, bool force);
 PullLaunch select_pull_mrt(int Q, int dtype, bool flags, bool force);
 PullLaunch select_pull_cumulant(int Q, int dtype, bool flags, bool force);
 PullLaunch select_pull_identity(int Q, int dtype, bool flags, bool force);
-AALaunch select_aa_trt(int Q, int dtype, bool force);
-AALaunch select_aa_mrt(int Q, int dtype, bool force);
-AALaunch select_aa_cumulant(int Q, int dtype, bool force);
-AALaunch select_aa_identity(int Q, int dtype, bool force);
+AALaunch select_aa_trt(int Q, int dtype, bool flags, bool force);
+AALaunch select_aa_mrt(int Q, int dtype, bool flags, bool force);
+AALaunch select_aa_cumulant(int Q, int dtype, bool flags, bool force);
+AALaunch select_aa_identity(int Q, int dtype, bool flags, bool force);
 
 // Auxiliary kernels (k_misc.cu), dispatched on (Q, dtype).
 void launch_init(int Q, int dtype, const InitArgs &a, void *f0, void *f1, dim3 grid, dim3 block, cudaStream_t s);

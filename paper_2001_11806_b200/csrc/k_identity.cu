@@ -6,18 +6,12 @@ namespace lbm {
 
 PullLaunch select_pull_identity(int Q, int dtype, bool flags, bool force) {
     (void)force;
-    if (Q == 19) return dtype == 0 ? pick_pull_noforce<19, OP_IDENTITY, double>(flags, false)
-                                   : pick_pull_noforce<19, OP_IDENTITY, float>(flags, false);
-    if (Q == 27) return dtype == 0 ? pick_pull_noforce<27, OP_IDENTITY, double>(flags, false)
-                                   : pick_pull_noforce<27, OP_IDENTITY, float>(flags, false);
-    return nullptr;
+    return select_pull_op<OP_IDENTITY, false, true, true>(Q, dtype, flags, false);
 }
 
-AALaunch select_aa_identity(int Q, int dtype, bool force) {
+AALaunch select_aa_identity(int Q, int dtype, bool flags, bool force) {
     (void)force;
-    if (Q == 19) return dtype == 0 ? &aa_launcher<19, OP_IDENTITY, double, false> : &aa_launcher<19, OP_IDENTITY, float, false>;
-    if (Q == 27) return dtype == 0 ? &aa_launcher<27, OP_IDENTITY, double, false> : &aa_launcher<27, OP_IDENTITY, float, false>;
-    return nullptr;
+    return select_aa_op<OP_IDENTITY, false, true, true>(Q, dtype, flags, false);
 }
 
 }  // namespace lbm

@@ -154,7 +154,15 @@ __global__ void __launch_bounds__(256, (MinBlocks<Q, OP, T>::pull)) k_pull(const
 // even: read a[x](q), collide, write a[x](qbar)   (in-place, reversed storage)
 // odd : read a[x - c_q](qbar), collide, write a[x + c_q](q)
 // =======================================================================================
-template <int Q, int OP, typename T, bool FORCE>
+// UBB term 6 w_q rho_w c_q.u_w (rho_w = 1, G8) in the storage precision
+template <int Q, typename T>
+__device__ __forceinline__ T ubb_term(const StepArgs &a, int q) {
+    using S = Stencil<Q>;
+    const double cu = S::cx(q) * a.uw[0] + S::cy(q) * a.uw[1] + S::cz(q) * a.uw[2];
+    return T(6.0 * S::w(q) * cu);
+}
+
+template <int Q, int OP, typename T, bool FLAGS, bool FORCE>
 __global__ void __launch_bounds__(256, (MinBlocks<Q, OP, T>::aa)) k_aa_even(const StepArgs a, T *__restrict__ f) {
     using S = Stencil<Q>;
     const int x = blockIdx.x * blockDim.x + threadIdx.x;
@@ -163,6 +171,7 @@ __global__ void __launch_bounds__(256, (MinBlocks<Q, OP, T>::aa)) k_aa_even(cons
     const int zs = a.z_begin + (int)blockIdx.z * a.z_step + a.geo.g;
     const uint32_t self = ((uint32_t)zs * (uint32_t)a.geo.ny + (uint32_t)y) * (uint32_t)a.geo.nx + (uint32_t)x;
     const int64_t Sq = a.geo.Sq;
+    if (FLAGS && (a.flags[self] & 3)) return;  // wall cells are not updated
     T g[Q];
 #pragma unroll
     for (int q = 0; q < Q; ++q) g[q] = f[q * Sq + self];
@@ -172,7 +181,11 @@ __global__ void __launch_bounds__(256, (MinBlocks<Q, OP, T>::aa)) k_aa_even(cons
     for (int q = 0; q < Q; ++q) f[S::opp(q) * Sq + self] = g[q];
 }
 
-template <int Q, int OP, typename T, bool FORCE>
+// Walls in the odd step (the pull rules of a3 expressed in AA slots): a population that
+// would come from a wall cell x - c_q is the cell's own bounced C_qbar(x), which the even step left
+// in a[x](q) (+ UBB term of q); a population leaving toward a wall x + c_q returns next step as qbar
+// and is stored directly in a[x](qbar) (+ UBB term of qbar). Only near-wall cells check flags.
+template <int Q, int OP, typename T, bool FLAGS, bool FORCE>
 __global__ void __launch_bounds__(256, (MinBlocks<Q, OP, T>::aa)) k_aa_odd(const StepArgs a, T *__restrict__ f) {
     using S = Stencil<Q>;
     const int x = blockIdx.x * blockDim.x + threadIdx.x;
@@ -181,13 +194,49 @@ __global__ void __launch_bounds__(256, (MinBlocks<Q, OP, T>::aa)) k_aa_odd(const
     const int zs = a.z_begin + (int)blockIdx.z * a.z_step + a.geo.g;
     const Nbr n = neighbours(a.geo, x, y, zs);
     const int64_t Sq = a.geo.Sq;
+    bool edge = false;
+    uint32_t self = 0;
+    if (FLAGS) {
+        self = nb_off(a.geo, n, 0, 0, 0);
+        const uint8_t own = a.flags[self];
+        if (own & 3) return;
+        edge = (own & 0x80) != 0;
+    }
     T g[Q];
 #pragma unroll
-    for (int q = 0; q < Q; ++q) g[q] = f[S::opp(q) * Sq + nb_off(a.geo, n, -S::cx(q), -S::cy(q), -S::cz(q))];
+    for (int q = 0; q < Q; ++q) {
+        const uint32_t o = nb_off(a.geo, n, -S::cx(q), -S::cy(q), -S::cz(q));
+        if (FLAGS && edge) {
+            const uint8_t fl = a.flags[o] & 3;
+            if (fl == 0) {
+                g[q] = f[S::opp(q) * Sq + o];
+            } else {
+                T v = f[q * Sq + self];
+                if (fl == 2) v += ubb_term<Q, T>(a, q);
+                g[q] = v;
+            }
+        } else {
+            g[q] = f[S::opp(q) * Sq + o];
+        }
+    }
     const Rates<T> r = load_rates<T>(a);
     collide<Q, OP, T, FORCE>(g, r);
 #pragma unroll
-    for (int q = 0; q < Q; ++q) f[q * Sq + nb_off(a.geo, n, S::cx(q), S::cy(q), S::cz(q))] = g[q];
+    for (int q = 0; q < Q; ++q) {
+        const uint32_t o = nb_off(a.geo, n, S::cx(q), S::cy(q), S::cz(q));
+        if (FLAGS && edge) {
+            const uint8_t fl = a.flags[o] & 3;
+            if (fl == 0) {
+                f[q * Sq + o] = g[q];
+            } else {
+                T v = g[q];
+                if (fl == 2) v += ubb_term<Q, T>(a, S::opp(q));
+                f[S::opp(q) * Sq + self] = v;
+            }
+        } else {
+            f[q * Sq + o] = g[q];
+        }
+    }
 }
 
 // =======================================================================================
@@ -284,16 +333,26 @@ struct ReadArgs {
     int raw;         // 1: stored values, no +w, no gather
     double fsign;    // +1 pre-collision state, -1 post-collision (pull)
     double F[3];
+    const uint8_t *flags;  // AA odd gather with walls (same rule as k_aa_odd's reads)
+    double uw[3];
 };
 
 template <int Q, typename T>
 __device__ __forceinline__ T read_canonical(const ReadArgs &a, const T *f, int x, int y, int zs, int q) {
     using S = Stencil<Q>;
+    const uint32_t self = ((uint32_t)zs * (uint32_t)a.geo.ny + (uint32_t)y) * (uint32_t)a.geo.nx + (uint32_t)x;
     if (a.aa_odd && !a.raw) {
         const Nbr n = neighbours(a.geo, x, y, zs);
-        return f[S::opp(q) * a.geo.Sq + nb_off(a.geo, n, -S::cx(q), -S::cy(q), -S::cz(q))];
+        const uint32_t o = nb_off(a.geo, n, -S::cx(q), -S::cy(q), -S::cz(q));
+        if (a.flags && (a.flags[self] & 0x80)) {
+            const uint8_t fl = a.flags[o] & 3;
+            if (fl != 0) {
+                const double cu = S::cx(q) * a.uw[0] + S::cy(q) * a.uw[1] + S::cz(q) * a.uw[2];
+                return f[q * a.geo.Sq + self] + (fl == 2 ? T(6.0 * S::w(q) * cu) : T(0));
+            }
+        }
+        return f[S::opp(q) * a.geo.Sq + o];
     }
-    const uint32_t self = ((uint32_t)zs * (uint32_t)a.geo.ny + (uint32_t)y) * (uint32_t)a.geo.nx + (uint32_t)x;
     return f[q * a.geo.Sq + self];
 }
 

@@ -146,6 +146,7 @@ void launch_aa(lbm_handle_s *h, Slab &s, int odd, cudaStream_t st) {
     a.geo = geo_of(h, s);
     a.z_begin = 0;
     a.z_step = 1;
+    a.flags = s.flags;
     tbegin(h, st);
     h->aa(a, s.pdf[0], odd, grid_for(h, s.nz), h->block, st);
     tend(h, st);
@@ -357,7 +358,6 @@ int validate(const lbm_config *c) {
     if (c->collision == LBM_CUMULANT && c->stencil != 27) return fail(nullptr, LBM_EUNSUPPORTED, "cumulant is implemented for D3Q27");
     if (force && (c->collision == LBM_MRT || c->collision == LBM_CUMULANT))
         return fail(nullptr, LBM_EUNSUPPORTED, "forcing is implemented for SRT/TRT");
-    if (c->pattern == LBM_AA && c->flags) return fail(nullptr, LBM_EUNSUPPORTED, "AA with boundary flags is not implemented yet");
     if (c->pattern == LBM_AA && P > 1) return fail(nullptr, LBM_EUNSUPPORTED, "AA with slab decomposition is not implemented yet");
     // a non-periodic axis must carry wall cells on both faces
     for (int d = 0; d < 3; ++d) {
@@ -523,10 +523,10 @@ int lbm_create(const lbm_config *cfg, lbm_handle *out) {
     } else {
         switch (cfg->collision) {
             case LBM_SRT:
-            case LBM_TRT: h->aa = select_aa_trt(h->Q, h->dtype, force); break;
-            case LBM_MRT: h->aa = select_aa_mrt(h->Q, h->dtype, force); break;
-            case LBM_CUMULANT: h->aa = select_aa_cumulant(h->Q, h->dtype, force); break;
-            default: h->aa = select_aa_identity(h->Q, h->dtype, force); break;
+            case LBM_TRT: h->aa = select_aa_trt(h->Q, h->dtype, h->have_flags, force); break;
+            case LBM_MRT: h->aa = select_aa_mrt(h->Q, h->dtype, h->have_flags, force); break;
+            case LBM_CUMULANT: h->aa = select_aa_cumulant(h->Q, h->dtype, h->have_flags, force); break;
+            default: h->aa = select_aa_identity(h->Q, h->dtype, h->have_flags, force); break;
         }
         if (!h->aa) return fail(nullptr, LBM_EUNSUPPORTED, "no kernel instantiated for this combination");
     }
@@ -838,11 +838,16 @@ int lbm_kernel_time_ms(lbm_handle h, double *ms, int64_t *launches) {
     return LBM_OK;
 }
 
-static int read_common(lbm_handle h, ReadArgs &r, int raw) {
+static int read_common(lbm_handle h, ReadArgs &r, int raw, const Slab &s) {
     r.raw = raw;
     r.aa_odd = (h->cfg.pattern == LBM_AA) && h->aa_parity;
     r.fsign = h->cfg.pattern == LBM_PULL ? -1.0 : 1.0;
-    for (int d = 0; d < 3; ++d) r.F[d] = h->cfg.force[d];
+    for (int d = 0; d < 3; ++d) {
+        r.F[d] = h->cfg.force[d];
+        r.uw[d] = h->cfg.ubb_velocity[d];
+    }
+    r.geo = geo_of(h, s);
+    r.flags = s.flags;
     return LBM_OK;
 }
 
@@ -859,7 +864,7 @@ int lbm_get_populations(lbm_handle h, double *out, int32_t where, int32_t raw) {
     for (Slab &s : h->slabs) {
         ReadArgs r;
         std::memset(&r, 0, sizeof(r));
-        read_common(h, r, raw);
+        read_common(h, r, raw, s);
         r.geo = geo_of(h, s);
         const int64_t sc = (int64_t)h->nx * h->ny * s.nz;
         const void *f = s.pdf[h->cfg.pattern == LBM_PULL ? s.cur : 0];
@@ -900,7 +905,7 @@ int lbm_get_populations_at(lbm_handle h, const int64_t *cells, int64_t n, double
     for (Slab &s : h->slabs) {
         ReadArgs r;
         std::memset(&r, 0, sizeof(r));
-        read_common(h, r, 0);
+        read_common(h, r, 0, s);
         r.geo = geo_of(h, s);
         const int64_t sc = (int64_t)h->nx * h->ny * s.nz;
         launch_get_at(h->Q, h->dtype, r, s.pdf[h->cfg.pattern == LBM_PULL ? s.cur : 0], didx, n, first, first + sc, dout, h->stream);
@@ -926,7 +931,7 @@ int lbm_set_populations(lbm_handle h, const double *in, int32_t where, int32_t r
     for (Slab &s : h->slabs) {
         ReadArgs r;
         std::memset(&r, 0, sizeof(r));
-        read_common(h, r, raw);
+        read_common(h, r, raw, s);
         r.aa_odd = 0;
         r.geo = geo_of(h, s);
         const int64_t sc = (int64_t)h->nx * h->ny * s.nz;
@@ -963,7 +968,7 @@ int lbm_get_macroscopic(lbm_handle h, double *rho, double *u, int32_t where) {
     for (Slab &s : h->slabs) {
         ReadArgs r;
         std::memset(&r, 0, sizeof(r));
-        read_common(h, r, 0);
+        read_common(h, r, 0, s);
         r.geo = geo_of(h, s);
         const int64_t sc = (int64_t)h->nx * h->ny * s.nz;
         const void *f = s.pdf[h->cfg.pattern == LBM_PULL ? s.cur : 0];
