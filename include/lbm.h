@@ -184,6 +184,38 @@ int lbm_halo_schedule(int32_t stencil, int64_t nz_local, int32_t rank, int32_t n
 /* Direction table of a stencil in ABI order: c_out[3*q + d], w_out[q]. Returns Q or LBM_EINVAL. */
 int lbm_stencil_table(int32_t stencil, int32_t *c_out, double *w_out);
 
+/* ---- Low-level kernel ABI ("raw pointer, together with shape and stride
+ * information ... relaxation rates or constant external forces become parameters") -------------
+ * One launch of one fused kernel on caller-owned device memory, asynchronous on `stream`.
+ * Layout: contiguous SoA, element (q, zs, y, x) at q*Sq + (zs*ny + y)*nx + x with
+ * Sq = nx*ny*(nz + 2*ghost); zs = z + ghost; populations stored zero-centred (g = f - w_q) in the
+ * dtype's precision. `flags` (device, one byte per storage cell, or NULL) must have been prepared
+ * by lbm_prepare_flags. The kernel updates interior planes z in [z_begin, z_end). Returns LBM_OK
+ * once the launch is enqueued; LBM_EINVAL / LBM_EUNSUPPORTED for bad arguments; LBM_ECUDA if the
+ * launch failed. */
+typedef struct lbm_kernel_args {
+    int32_t stencil, collision, dtype;
+    const void *src;      /* pull: read array; AA: unused */
+    void *dst;            /* pull: write array; AA: the single array (read and written) */
+    const uint8_t *flags; /* prepared flags or NULL (all fluid) */
+    int64_t shape[3];     /* nx, ny, nz (interior planes) */
+    int32_t ghost;        /* 0: z wraps within the array; 1: one ghost plane per z side */
+    int64_t z_begin, z_end;
+    double rates[8];      /* as lbm_config.rates (SRT: [omega]) */
+    double force[3];
+    double ubb_velocity[3];
+    void *stream;         /* cudaStream_t */
+} lbm_kernel_args;
+
+/* Fused stream-pull-collide: dst = C(S(src)) on the fluid cells of planes [z_begin, z_end). */
+int lbm_kernel_pull(const lbm_kernel_args *a);
+/* AA even (odd = 0) or odd (odd = 1) step on dst in place (ghost must be 0). */
+int lbm_kernel_aa(const lbm_kernel_args *a, int32_t odd);
+/* Device flag bytes for the kernels: copies host flags (nx*ny*nplanes, values 0/1/2) and marks
+ * fluid cells that have a non-fluid neighbour (bit 7). nplanes includes ghost planes. */
+int lbm_prepare_flags(const uint8_t *host_flags, int64_t nx, int64_t ny, int64_t nplanes, int32_t ghost,
+                      uint8_t *device_out, void *stream);
+
 const char *lbm_strerror(int status);
 const char *lbm_last_error(lbm_handle h);
 /* Library version string. */

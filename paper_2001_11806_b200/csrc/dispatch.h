@@ -28,6 +28,8 @@ void launch_set_pops(int Q, int dtype, const ReadArgs &a, void *f, const double 
 void launch_macro(int Q, int dtype, const ReadArgs &a, const void *f, double *rho, double *u, dim3 grid, dim3 block, cudaStream_t s);
 void launch_pack(int Q, int dtype, const Geo &geo, const void *f, int zs, int dir, void *out, bool out_f64, cudaStream_t s);
 void launch_unpack(int Q, int dtype, const Geo &geo, void *f, int zs, int dir, const void *in, cudaStream_t s);
+void launch_unpack_masked(int Q, int dtype, const Geo &geo, void *f, int zs, int dir, const void *in, const uint8_t *flags,
+                          cudaStream_t s);
 void launch_mark_near_wall(const Geo &geo, int nplanes, const uint8_t *in, uint8_t *out, cudaStream_t s);
 void launch_nan_check(int dtype, const void *f, int64_t n, int *flag, cudaStream_t s);
 

@@ -53,6 +53,13 @@ void launch_unpack(int Q, int dtype, const Geo &geo, void *f, int zs, int dir, c
     LBM_DISPATCH(Q, dtype, (k_unpack<QQ, T><<<blocks_for(n), 256, 0, s>>>(geo, static_cast<T *>(f), zs, dir, static_cast<const T *>(in))));
 }
 
+void launch_unpack_masked(int Q, int dtype, const Geo &geo, void *f, int zs, int dir, const void *in, const uint8_t *flags,
+                          cudaStream_t s) {
+    const int64_t n = (int64_t)geo.nx * geo.ny * (Q == 19 ? 5 : 9);
+    LBM_DISPATCH(Q, dtype, (k_unpack_masked<QQ, T><<<blocks_for(n), 256, 0, s>>>(geo, static_cast<T *>(f), zs, dir,
+                                                                                static_cast<const T *>(in), flags)));
+}
+
 __global__ void k_mark_near_wall(const Geo geo, int nplanes, const uint8_t *__restrict__ in, uint8_t *__restrict__ out) {
     const int64_t plane = (int64_t)geo.nx * geo.ny;
     const int64_t n = plane * nplanes;

@@ -463,6 +463,26 @@ __global__ void k_unpack(const Geo geo, T *__restrict__ f, int zs, int dir, cons
     }
 }
 
+// AA return of ghost-plane writes with walls: population q arriving in storage plane zs was
+// produced by the cell one step against c_q (in the neighbour's slab). If that cell is a wall the
+// value is not in the buffer (the receiving cell bounced it locally), so it is skipped.
+template <int Q, typename T>
+__global__ void k_unpack_masked(const Geo geo, T *__restrict__ f, int zs, int dir, const T *__restrict__ in,
+                                const uint8_t *__restrict__ flags) {
+    using S = Stencil<Q>;
+    const int64_t plane = (int64_t)geo.nx * geo.ny;
+    const int64_t n = plane * S::kCross;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int k = (int)(i / plane);
+        const int64_t r = i - k * plane;
+        const int q = crossing_dir<Q>(dir, k);
+        const int x = (int)(r % geo.nx), y = (int)(r / geo.nx);
+        const int xs = (x - S::cx(q) + geo.nx) % geo.nx, ys = (y - S::cy(q) + geo.ny) % geo.ny;
+        const int64_t src = (int64_t)(zs - S::cz(q)) * plane + (int64_t)ys * geo.nx + xs;
+        if ((flags[src] & 3) == 0) f[q * geo.Sq + zs * plane + r] = in[i];
+    }
+}
+
 // =======================================================================================
 // Flag preprocessing and diagnostics
 // =======================================================================================

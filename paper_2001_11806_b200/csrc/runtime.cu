@@ -141,66 +141,86 @@ void launch_pull_range(lbm_handle_s *h, Slab &s, int z_begin, int nplanes, int z
     h->launches++;
 }
 
-void launch_aa(lbm_handle_s *h, Slab &s, int odd, cudaStream_t st) {
+void launch_aa_range(lbm_handle_s *h, Slab &s, int odd, int z_begin, int nplanes, int z_step, cudaStream_t st) {
+    if (nplanes <= 0) return;
     StepArgs a = h->base;
     a.geo = geo_of(h, s);
-    a.z_begin = 0;
-    a.z_step = 1;
+    a.z_begin = z_begin;
+    a.z_step = z_step;
     a.flags = s.flags;
     tbegin(h, st);
-    h->aa(a, s.pdf[0], odd, grid_for(h, s.nz), h->block, st);
+    h->aa(a, s.pdf[0], odd, grid_for(h, nplanes), h->block, st);
     tend(h, st);
     h->launches++;
 }
 
-// Zero-copy halo schedule (posting order inside one NCCL group). Per peer pair the sends of one
-// side and the receives of the other are posted in the same order, so NCCL matches them even when
-// the up and down neighbours are the same rank (P = 2).
+// Halo exchange phases. Each phase moves, per slab, one set of crossing slots through face A
+// (sent up, received from below) and one through face B (sent down, received from above):
+//   pull           : A = c_z=+1 slots of the top plane   -> lower ghost;  B = c_z=-1 of plane 1 -> upper ghost
+//   AA ghost fill  : A = c_z=-1 slots of the top plane   -> lower ghost;  B = c_z=+1 of plane 1 -> upper ghost
+//                    (after the even step: the odd step pulls a[x - c_q](qbar) across the face)
+//   AA return      : A = c_z=+1 slots of the upper ghost -> plane 1;      B = c_z=-1 of the lower ghost -> plane nz
+//                    (after the odd step: its pushes a[x + c_q](q) that landed in ghost planes go home;
+//                    with walls only where the producing cell is fluid)
+struct Phase {
+    int dirA, sendA, recvA, dirB, sendB, recvB;
+    bool masked;
+};
+Phase phase_pull(int nz) { return {+1, nz, 0, -1, 1, nz + 1, false}; }
+Phase phase_aa_fill(int nz) { return {-1, nz, 0, +1, 1, nz + 1, false}; }
+Phase phase_aa_return(int nz, bool masked) { return {+1, nz + 1, 1, -1, 0, nz, masked}; }
+
+// Zero-copy schedule of a phase (posting order inside one NCCL group). Per peer pair the sends of
+// one side and the receives of the other are posted in the same order, so NCCL matches them even
+// when the up and down neighbours are the same rank (P = 2).
 struct HaloOp {
     int kind, peer, q, zs;  // kind 0 = send, 1 = recv
 };
 
-std::vector<HaloOp> halo_schedule(int Q, int nz, int up, int down) {
-    int qu[9], qd[9];
-    const int nu = crossing(Q, +1, qu), nd = crossing(Q, -1, qd);
+std::vector<HaloOp> phase_schedule(int Q, const Phase &ph, int up, int down) {
+    int qa[9], qb[9];
+    const int na = crossing(Q, ph.dirA, qa), nb = crossing(Q, ph.dirB, qb);
     std::vector<HaloOp> ops;
-    for (int k = 0; k < nu; ++k) ops.push_back({0, up, qu[k], nz});       // c_z = +1 leaves the top plane
-    for (int k = 0; k < nu; ++k) ops.push_back({1, down, qu[k], 0});      // ... and arrives in the lower ghost
-    for (int k = 0; k < nd; ++k) ops.push_back({0, down, qd[k], 1});      // c_z = -1 leaves the bottom plane
-    for (int k = 0; k < nd; ++k) ops.push_back({1, up, qd[k], nz + 1});   // ... and arrives in the upper ghost
+    for (int k = 0; k < na; ++k) ops.push_back({0, up, qa[k], ph.sendA});
+    for (int k = 0; k < na; ++k) ops.push_back({1, down, qa[k], ph.recvA});
+    for (int k = 0; k < nb; ++k) ops.push_back({0, down, qb[k], ph.sendB});
+    for (int k = 0; k < nb; ++k) ops.push_back({1, up, qb[k], ph.recvB});
     return ops;
 }
 
+std::vector<HaloOp> halo_schedule(int Q, int nz, int up, int down) { return phase_schedule(Q, phase_pull(nz), up, down); }
+
+void unpack_face(lbm_handle_s *h, const Slab &d, int arr, int zs, int dir, const void *buf, bool masked, cudaStream_t st) {
+    const Geo g = geo_of(h, d);
+    if (masked) launch_unpack_masked(h->Q, h->dtype, g, d.pdf[arr], zs, dir, buf, d.flags, st);
+    else launch_unpack(h->Q, h->dtype, g, d.pdf[arr], zs, dir, buf, st);
+    h->launches++;
+}
+
 // ---- halo exchange ------------------------------------------------------------------
-// After an update that wrote array `arr` of every slab: the crossing populations of the
-// boundary planes go into the neighbours' ghost planes of the same array.
-int exchange_loopback(lbm_handle_s *h, int arr_sel_cur, cudaStream_t st) {
+// arr(slab) selects the array of each slab the phase works on (pull: the freshly written one).
+template <typename ArrSel>
+int exchange_loopback(lbm_handle_s *h, const Phase &ph0, ArrSel arr, cudaStream_t st) {
     const int P = (int)h->slabs.size();
-    int up[9], dn[9];
-    const int nu = crossing(h->Q, +1, up), nd = crossing(h->Q, -1, dn);
-    for (int r = 0; r < P; ++r) {
-        Slab &s = h->slabs[r];
-        Slab &su = h->slabs[(r + 1) % P];
-        Slab &sd = h->slabs[(r - 1 + P) % P];
-        const int arr = arr_sel_cur ? s.cur : 1 - s.cur;
-        const int arru = arr_sel_cur ? su.cur : 1 - su.cur;
-        const int arrd = arr_sel_cur ? sd.cur : 1 - sd.cur;
-        if (h->cfg.halo_mode == LBM_HALO_PACKED) {
-            Geo g = geo_of(h, s), gu = geo_of(h, su), gd = geo_of(h, sd);
-            launch_pack(h->Q, h->dtype, g, s.pdf[arr], s.nz, +1, s.halo[0], false, st);
-            launch_unpack(h->Q, h->dtype, gu, su.pdf[arru], 0, +1, s.halo[0], st);
-            launch_pack(h->Q, h->dtype, g, s.pdf[arr], 1, -1, s.halo[1], false, st);
-            launch_unpack(h->Q, h->dtype, gd, sd.pdf[arrd], sd.nz + 1, -1, s.halo[1], st);
-            h->launches += 4;
+    const bool packed = h->cfg.halo_mode == LBM_HALO_PACKED || ph0.masked;
+    if (packed) {
+        for (int r = 0; r < P; ++r) {
+            Slab &s = h->slabs[r];
+            Slab &su = h->slabs[(r + 1) % P];
+            Slab &sd = h->slabs[(r - 1 + P) % P];
+            const Phase ph = ph0;
+            launch_pack(h->Q, h->dtype, geo_of(h, s), s.pdf[arr(s)], ph.sendA, ph.dirA, s.halo[0], false, st);
+            unpack_face(h, su, arr(su), ph.recvA, ph.dirA, s.halo[0], ph.masked, st);
+            launch_pack(h->Q, h->dtype, geo_of(h, s), s.pdf[arr(s)], ph.sendB, ph.dirB, s.halo[1], false, st);
+            unpack_face(h, sd, arr(sd), ph.recvB, ph.dirB, s.halo[1], ph.masked, st);
+            h->launches += 2;
         }
+        return LBM_OK;
     }
-    if (h->cfg.halo_mode == LBM_HALO_PACKED) return LBM_OK;
-    (void)nu;
-    (void)nd;
     // zero-copy: execute the same per-rank schedule NCCL uses; the k-th send of slab r to peer p
     // is matched with the k-th receive of p from r (NCCL's in-order matching per peer pair)
     std::vector<std::vector<HaloOp>> sched(P);
-    for (int r = 0; r < P; ++r) sched[r] = halo_schedule(h->Q, h->slabs[r].nz, (r + 1) % P, (r - 1 + P) % P);
+    for (int r = 0; r < P; ++r) sched[r] = phase_schedule(h->Q, ph0, (r + 1) % P, (r - 1 + P) % P);
     for (int r = 0; r < P; ++r) {
         for (int p = 0; p < P; ++p) {
             std::vector<const HaloOp *> sends, recvs;
@@ -211,43 +231,37 @@ int exchange_loopback(lbm_handle_s *h, int arr_sel_cur, cudaStream_t st) {
             if (sends.size() != recvs.size()) return fail(h, LBM_EINVAL, "halo schedule mismatch");
             Slab &s = h->slabs[r];
             Slab &d = h->slabs[p];
-            const int as = arr_sel_cur ? s.cur : 1 - s.cur;
-            const int ad = arr_sel_cur ? d.cur : 1 - d.cur;
             for (size_t k = 0; k < sends.size(); ++k)
-                CUDA_TRY(h, cudaMemcpyAsync(qplane(h, d, ad, recvs[k]->q, recvs[k]->zs), qplane(h, s, as, sends[k]->q, sends[k]->zs),
-                                            plane_bytes(h), cudaMemcpyDeviceToDevice, st));
+                CUDA_TRY(h, cudaMemcpyAsync(qplane(h, d, arr(d), recvs[k]->q, recvs[k]->zs),
+                                            qplane(h, s, arr(s), sends[k]->q, sends[k]->zs), plane_bytes(h),
+                                            cudaMemcpyDeviceToDevice, st));
         }
     }
     return LBM_OK;
 }
 
-int exchange_nccl(lbm_handle_s *h, int arr_sel_cur, cudaStream_t st) {
+int exchange_nccl(lbm_handle_s *h, const Phase &ph, int arr, cudaStream_t st) {
     Slab &s = h->slabs[0];
-    const int arr = arr_sel_cur ? s.cur : 1 - s.cur;
     const ncclDataType_t dt = h->dtype == 0 ? ncclDouble : ncclFloat;
     const size_t plane = (size_t)h->nx * h->ny;
-    int up[9], dn[9];
-    const int nu = crossing(h->Q, +1, up), nd = crossing(h->Q, -1, dn);
+    const size_t ncross = h->Q == 19 ? 5 : 9;
     const Geo g = geo_of(h, s);
-    if (h->cfg.halo_mode == LBM_HALO_PACKED) {
-        launch_pack(h->Q, h->dtype, g, s.pdf[arr], s.nz, +1, s.halo[0], false, st);
-        launch_pack(h->Q, h->dtype, g, s.pdf[arr], 1, -1, s.halo[1], false, st);
+    if (h->cfg.halo_mode == LBM_HALO_PACKED || ph.masked) {
+        launch_pack(h->Q, h->dtype, g, s.pdf[arr], ph.sendA, ph.dirA, s.halo[0], false, st);
+        launch_pack(h->Q, h->dtype, g, s.pdf[arr], ph.sendB, ph.dirB, s.halo[1], false, st);
         h->launches += 2;
         NCCL_TRY(h, ncclGroupStart());
-        NCCL_TRY(h, ncclSend(s.halo[0], plane * nu, dt, h->up, h->comm, st));
-        NCCL_TRY(h, ncclRecv(s.halo[2], plane * nu, dt, h->down, h->comm, st));
-        NCCL_TRY(h, ncclSend(s.halo[1], plane * nd, dt, h->down, h->comm, st));
-        NCCL_TRY(h, ncclRecv(s.halo[3], plane * nd, dt, h->up, h->comm, st));
+        NCCL_TRY(h, ncclSend(s.halo[0], plane * ncross, dt, h->up, h->comm, st));
+        NCCL_TRY(h, ncclRecv(s.halo[2], plane * ncross, dt, h->down, h->comm, st));
+        NCCL_TRY(h, ncclSend(s.halo[1], plane * ncross, dt, h->down, h->comm, st));
+        NCCL_TRY(h, ncclRecv(s.halo[3], plane * ncross, dt, h->up, h->comm, st));
         NCCL_TRY(h, ncclGroupEnd());
-        launch_unpack(h->Q, h->dtype, g, s.pdf[arr], 0, +1, s.halo[2], st);
-        launch_unpack(h->Q, h->dtype, g, s.pdf[arr], s.nz + 1, -1, s.halo[3], st);
-        h->launches += 2;
+        unpack_face(h, s, arr, ph.recvA, ph.dirA, s.halo[2], ph.masked, st);
+        unpack_face(h, s, arr, ph.recvB, ph.dirB, s.halo[3], ph.masked, st);
     } else {
-        // zero-copy: each crossing population's boundary plane is one contiguous nx*ny run
-        (void)nu;
-        (void)nd;
+        // zero-copy: each crossing population's plane is one contiguous nx*ny run
         NCCL_TRY(h, ncclGroupStart());
-        for (const HaloOp &op : halo_schedule(h->Q, s.nz, h->up, h->down)) {
+        for (const HaloOp &op : phase_schedule(h->Q, ph, h->up, h->down)) {
             if (op.kind == 0) NCCL_TRY(h, ncclSend(qplane(h, s, arr, op.q, op.zs), plane, dt, op.peer, h->comm, st));
             else NCCL_TRY(h, ncclRecv(qplane(h, s, arr, op.q, op.zs), plane, dt, op.peer, h->comm, st));
         }
@@ -256,48 +270,64 @@ int exchange_nccl(lbm_handle_s *h, int arr_sel_cur, cudaStream_t st) {
     return LBM_OK;
 }
 
-// exchange the CURRENT state's ghost planes (after init / set_populations), synchronously ordered on stream
+// exchange the CURRENT pull state's ghost planes (after init / set_populations), ordered on stream
 int exchange_current(lbm_handle_s *h) {
-    if (h->g == 0) return LBM_OK;
-    if (h->use_nccl) return exchange_nccl(h, 1, h->stream);
-    return exchange_loopback(h, 1, h->stream);
+    if (h->g == 0 || h->cfg.pattern == LBM_AA) return LBM_OK;  // AA needs ghosts only before odd steps
+    const Phase ph = phase_pull(h->slabs[0].nz);
+    if (h->use_nccl) return exchange_nccl(h, ph, h->slabs[0].cur, h->stream);
+    return exchange_loopback(h, ph, [](const Slab &s) { return s.cur; }, h->stream);
 }
 
 // ---- one time step ------------------------------------------------------------------
+// Decomposed steps run the boundary planes first, then (NCCL) exchange on the comm stream while
+// the interior planes update on the compute stream; the next step waits for the exchange.
 int step_once(lbm_handle_s *h) {
     cudaStream_t st = h->stream;
-    if (h->cfg.pattern == LBM_AA) {
-        Slab &s = h->slabs[0];
-        launch_aa(h, s, h->aa_parity, st);
-        h->aa_parity ^= 1;
-        return LBM_OK;
-    }
     if (h->g == 0) {
         Slab &s = h->slabs[0];
-        launch_pull_range(h, s, 0, s.nz, 1, st);
-        s.cur ^= 1;
+        if (h->cfg.pattern == LBM_AA) {
+            launch_aa_range(h, s, h->aa_parity, 0, s.nz, 1, st);
+            h->aa_parity ^= 1;
+        } else {
+            launch_pull_range(h, s, 0, s.nz, 1, st);
+            s.cur ^= 1;
+        }
         return LBM_OK;
     }
+    const bool aa = h->cfg.pattern == LBM_AA;
+    const int odd = h->aa_parity;
+    auto bnd = [&](Slab &s) {
+        if (aa) launch_aa_range(h, s, odd, 0, 2, s.nz - 1, st);
+        else launch_pull_range(h, s, 0, 2, s.nz - 1, st);
+    };
+    auto inner = [&](Slab &s) {
+        if (aa) launch_aa_range(h, s, odd, 1, s.nz - 2, 1, st);
+        else launch_pull_range(h, s, 1, s.nz - 2, 1, st);
+    };
+    const int nz = h->slabs[0].nz;
+    const Phase ph = !aa ? phase_pull(nz) : (odd ? phase_aa_return(nz, h->have_flags) : phase_aa_fill(nz));
     if (!h->use_nccl) {
         // loopback slabs on one GPU, one stream: boundary planes, exchange, interior
-        for (Slab &s : h->slabs) launch_pull_range(h, s, 0, 2, s.nz - 1, st);
-        int rc = exchange_loopback(h, 0, st);
+        for (Slab &s : h->slabs) bnd(s);
+        int rc = aa ? exchange_loopback(h, ph, [](const Slab &) { return 0; }, st)
+                    : exchange_loopback(h, ph, [](const Slab &s) { return 1 - s.cur; }, st);
         if (rc) return rc;
-        for (Slab &s : h->slabs) launch_pull_range(h, s, 1, s.nz - 2, 1, st);
-        for (Slab &s : h->slabs) s.cur ^= 1;
+        for (Slab &s : h->slabs) inner(s);
+        if (aa) h->aa_parity ^= 1;
+        else for (Slab &s : h->slabs) s.cur ^= 1;
         return LBM_OK;
     }
-    // NCCL: boundary planes -> event -> (comm stream) exchange || (compute stream) interior
     Slab &s = h->slabs[0];
-    launch_pull_range(h, s, 0, 2, s.nz - 1, st);
+    bnd(s);
     CUDA_TRY(h, cudaEventRecord(h->ev_bnd, st));
     CUDA_TRY(h, cudaStreamWaitEvent(h->comm_stream, h->ev_bnd, 0));
-    int rc = exchange_nccl(h, 0, h->comm_stream);
+    int rc = exchange_nccl(h, ph, aa ? 0 : 1 - s.cur, h->comm_stream);
     if (rc) return rc;
     CUDA_TRY(h, cudaEventRecord(h->ev_x, h->comm_stream));
-    launch_pull_range(h, s, 1, s.nz - 2, 1, st);
-    CUDA_TRY(h, cudaStreamWaitEvent(st, h->ev_x, 0));  // next step's boundary planes need the ghosts
-    s.cur ^= 1;
+    inner(s);
+    CUDA_TRY(h, cudaStreamWaitEvent(st, h->ev_x, 0));  // the next step's boundary planes need the exchange
+    if (aa) h->aa_parity ^= 1;
+    else s.cur ^= 1;
     return LBM_OK;
 }
 
@@ -349,7 +379,6 @@ int validate(const lbm_config *c) {
     if (c->nranks > 1 && !c->nccl_id) return fail(nullptr, LBM_EINVAL, "nranks > 1 needs an nccl_id");
     if (c->nccl_self && (c->nranks != 1 || c->n_local_slabs > 1 || c->global[2] < 2))
         return fail(nullptr, LBM_EINVAL, "nccl_self needs nranks == 1, one slab and nz >= 2");
-    if (c->nccl_self && c->pattern == LBM_AA) return fail(nullptr, LBM_EUNSUPPORTED, "AA with slab decomposition is not implemented yet");
     const int64_t planes = c->global[2] / P + (P > 1 ? 2 : 0);
     if ((double)c->global[0] * c->global[1] * planes >= 2147483647.0)
         return fail(nullptr, LBM_EINVAL, "slab too large for 32-bit in-plane offsets (split it over more slabs)");
@@ -358,7 +387,6 @@ int validate(const lbm_config *c) {
     if (c->collision == LBM_CUMULANT && c->stencil != 27) return fail(nullptr, LBM_EUNSUPPORTED, "cumulant is implemented for D3Q27");
     if (force && (c->collision == LBM_MRT || c->collision == LBM_CUMULANT))
         return fail(nullptr, LBM_EUNSUPPORTED, "forcing is implemented for SRT/TRT");
-    if (c->pattern == LBM_AA && P > 1) return fail(nullptr, LBM_EUNSUPPORTED, "AA with slab decomposition is not implemented yet");
     // a non-periodic axis must carry wall cells on both faces
     for (int d = 0; d < 3; ++d) {
         if (c->periodic[d]) continue;
@@ -434,6 +462,116 @@ const char *lbm_strerror(int s) {
 }
 
 const char *lbm_last_error(lbm_handle h) { return h ? h->err.c_str() : g_create_error.c_str(); }
+
+static int kernel_args_common(const lbm_kernel_args *k, StepArgs &a, bool aa) {
+    if (!k || (k->stencil != 19 && k->stencil != 27) || k->collision < 0 || k->collision > 4 ||
+        (k->dtype != LBM_F64 && k->dtype != LBM_F32) || !k->dst || (!aa && !k->src) || k->ghost < 0 || k->ghost > 1)
+        return LBM_EINVAL;
+    if (k->shape[0] < 1 || k->shape[1] < 1 || k->shape[2] < 1 || k->z_begin < 0 || k->z_end > k->shape[2] ||
+        k->z_begin > k->z_end)
+        return LBM_EINVAL;
+    if ((double)k->shape[0] * k->shape[1] * (k->shape[2] + 2 * k->ghost) >= 2147483647.0) return LBM_EINVAL;
+    if (aa && k->ghost) return LBM_EUNSUPPORTED;
+    std::memset(&a, 0, sizeof(a));
+    a.geo.nx = (int)k->shape[0];
+    a.geo.ny = (int)k->shape[1];
+    a.geo.nz = (int)k->shape[2];
+    a.geo.g = k->ghost;
+    a.geo.Sq = k->shape[0] * k->shape[1] * (k->shape[2] + 2 * k->ghost);
+    a.z_begin = (int)k->z_begin;
+    a.z_step = 1;
+    for (int i = 0; i < 8; ++i) a.rates[i] = k->rates[i];
+    if (k->collision == LBM_SRT) a.rates[1] = a.rates[0];
+    if (k->collision == LBM_MRT)
+        for (int i = 0; i < 4; ++i)
+            if (a.rates[i] == 0.0) a.rates[i] = 1.0;
+    if (k->collision == LBM_CUMULANT)
+        for (int i = 1; i < 6; ++i)
+            if (a.rates[i] == 0.0) a.rates[i] = 1.0;
+    for (int d = 0; d < 3; ++d) {
+        a.F[d] = k->force[d];
+        a.uw[d] = k->ubb_velocity[d];
+    }
+    a.flags = k->flags;
+    return LBM_OK;
+}
+
+static dim3 kernel_block(int64_t nx, int64_t ny) {
+    int bx = 256;
+    if (bx > nx) bx = (int)((nx + 31) / 32 * 32);
+    int by = 256 / bx;
+    if (by > ny) by = (int)ny;
+    return dim3(bx, by < 1 ? 1 : by, 1);
+}
+
+int lbm_kernel_pull(const lbm_kernel_args *k) {
+    StepArgs a;
+    int rc = kernel_args_common(k, a, false);
+    if (rc) return rc;
+    const bool flags = k->flags != nullptr;
+    const bool force = k->force[0] != 0 || k->force[1] != 0 || k->force[2] != 0;
+    PullLaunch fn = nullptr;
+    switch (k->collision) {
+        case LBM_SRT:
+        case LBM_TRT: fn = select_pull_trt(k->stencil, k->dtype, flags, force); break;
+        case LBM_MRT: fn = select_pull_mrt(k->stencil, k->dtype, flags, force); break;
+        case LBM_CUMULANT: fn = select_pull_cumulant(k->stencil, k->dtype, flags, force); break;
+        default: fn = select_pull_identity(k->stencil, k->dtype, flags, force); break;
+    }
+    if (!fn) return LBM_EUNSUPPORTED;
+    if (k->z_end == k->z_begin) return LBM_OK;
+    const dim3 b = kernel_block(k->shape[0], k->shape[1]);
+    const dim3 grid((unsigned)((k->shape[0] + b.x - 1) / b.x), (unsigned)((k->shape[1] + b.y - 1) / b.y),
+                    (unsigned)(k->z_end - k->z_begin));
+    fn(a, k->src, k->dst, grid, b, static_cast<cudaStream_t>(k->stream));
+    return cudaGetLastError() == cudaSuccess ? LBM_OK : LBM_ECUDA;
+}
+
+int lbm_kernel_aa(const lbm_kernel_args *k, int32_t odd) {
+    StepArgs a;
+    int rc = kernel_args_common(k, a, true);
+    if (rc) return rc;
+    const bool flags = k->flags != nullptr;
+    const bool force = k->force[0] != 0 || k->force[1] != 0 || k->force[2] != 0;
+    AALaunch fn = nullptr;
+    switch (k->collision) {
+        case LBM_SRT:
+        case LBM_TRT: fn = select_aa_trt(k->stencil, k->dtype, flags, force); break;
+        case LBM_MRT: fn = select_aa_mrt(k->stencil, k->dtype, flags, force); break;
+        case LBM_CUMULANT: fn = select_aa_cumulant(k->stencil, k->dtype, flags, force); break;
+        default: fn = select_aa_identity(k->stencil, k->dtype, flags, force); break;
+    }
+    if (!fn) return LBM_EUNSUPPORTED;
+    if (k->z_end == k->z_begin) return LBM_OK;
+    const dim3 b = kernel_block(k->shape[0], k->shape[1]);
+    const dim3 grid((unsigned)((k->shape[0] + b.x - 1) / b.x), (unsigned)((k->shape[1] + b.y - 1) / b.y),
+                    (unsigned)(k->z_end - k->z_begin));
+    fn(a, k->dst, odd ? 1 : 0, grid, b, static_cast<cudaStream_t>(k->stream));
+    return cudaGetLastError() == cudaSuccess ? LBM_OK : LBM_ECUDA;
+}
+
+int lbm_prepare_flags(const uint8_t *host_flags, int64_t nx, int64_t ny, int64_t nplanes, int32_t ghost,
+                      uint8_t *device_out, void *stream) {
+    if (!host_flags || !device_out || nx < 1 || ny < 1 || nplanes < 1 || ghost < 0 || ghost > 1) return LBM_EINVAL;
+    const size_t cells = (size_t)nx * ny * nplanes;
+    uint8_t *tmp = nullptr;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (cudaMalloc(&tmp, cells) != cudaSuccess) return LBM_EOOM;
+    Geo g;
+    g.nx = (int)nx;
+    g.ny = (int)ny;
+    g.nz = (int)(nplanes - 2 * ghost);
+    g.g = ghost;
+    g.Sq = (int64_t)cells;
+    if (cudaMemcpyAsync(tmp, host_flags, cells, cudaMemcpyHostToDevice, st) != cudaSuccess) {
+        cudaFree(tmp);
+        return LBM_ECUDA;
+    }
+    launch_mark_near_wall(g, (int)nplanes, tmp, device_out, st);
+    const cudaError_t e = cudaStreamSynchronize(st);
+    cudaFree(tmp);
+    return e == cudaSuccess ? LBM_OK : LBM_ECUDA;
+}
 
 int lbm_slab_plan(int64_t nz, int32_t nranks, int32_t rank, int64_t out[4]) {
     if (nranks < 1 || rank < 0 || rank >= nranks || nz % nranks != 0 || (nranks > 1 && nz / nranks < 2)) return LBM_EINVAL;

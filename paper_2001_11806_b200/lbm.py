@@ -45,6 +45,16 @@ class lbm_config(C.Structure):
     ]
 
 
+class lbm_kernel_args(C.Structure):
+    _fields_ = [
+        ("stencil", C.c_int32), ("collision", C.c_int32), ("dtype", C.c_int32),
+        ("src", C.c_void_p), ("dst", C.c_void_p), ("flags", C.c_void_p),
+        ("shape", C.c_int64 * 3), ("ghost", C.c_int32), ("z_begin", C.c_int64), ("z_end", C.c_int64),
+        ("rates", C.c_double * 8), ("force", C.c_double * 3), ("ubb_velocity", C.c_double * 3),
+        ("stream", C.c_void_p),
+    ]
+
+
 class LBMError(RuntimeError):
     def __init__(self, status: int, msg: str):
         super().__init__(f"{msg} (status {status})")
@@ -79,6 +89,9 @@ _SIGS = {
     "lbm_crossing_directions": ([_I32, _I32, _P], C.c_int),
     "lbm_stencil_table": ([_I32, _P, _P], C.c_int),
     "lbm_halo_schedule": ([_I32, _I64, _I32, _I32, _P, _I32], C.c_int),
+    "lbm_kernel_pull": ([C.POINTER(lbm_kernel_args)], C.c_int),
+    "lbm_kernel_aa": ([C.POINTER(lbm_kernel_args), _I32], C.c_int),
+    "lbm_prepare_flags": ([_P, _I64, _I64, _I64, _I32, _P, _P], C.c_int),
     "lbm_strerror": ([C.c_int], C.c_char_p),
     "lbm_last_error": ([_P], C.c_char_p),
     "lbm_version": ([], C.c_char_p),

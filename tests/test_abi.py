@@ -81,7 +81,7 @@ def test_slab_plan(L):
     (dict(collision="mrt", rates=(1.9,), force=(1e-5, 0, 0)), -2),
     (dict(n_local_slabs=3), -1),                                # nz % slabs != 0
     (dict(periodic=(1, 0, 1)), -1),                             # non-periodic axis without walls
-    (dict(pattern="aa", n_local_slabs=2), -2),
+    (dict(nccl_self=True, n_local_slabs=2), -1),                # self-exchange is single-slab
 ])
 def test_create_validation_errors(L, kw, code):
     """Validation happens before any CUDA call, so these run on a CPU-only host."""

@@ -221,12 +221,36 @@ def test_slab_decomposition_other_ops(Q, op, rates, dtype):
     np.testing.assert_array_equal(one.populations(raw=True), many.populations(raw=True))
 
 
+@pytest.mark.parametrize("P", [2, 4])
 @pytest.mark.parametrize("halo_mode", [0, 1])
-@pytest.mark.parametrize("Q,op,rates,geometry", [(19, "trt", (1.6, 0.5), "channel"), (27, "cumulant", (1.95,), "periodic")])
-def test_nccl_self_exchange_bit_identical(halo_mode, Q, op, rates, geometry):
+@pytest.mark.parametrize("Q,op,rates,geometry,force", [(19, "trt", (1.6, 0.5), "channel", (1e-5, 0, 0)),
+                                                       (19, "srt", (1.7,), "obstacles", (0, 0, 0)),
+                                                       (27, "cumulant", (1.95,), "periodic", (0, 0, 0))])
+def test_aa_slab_decomposition_bit_identical(P, halo_mode, Q, op, rates, geometry, force):
+    """AA with slabs: ghost fill after even steps, return of ghost-plane writes after odd steps
+    (masked by the producing cell's flag with walls). Odd and even step counts."""
+    case = Case("aadec", (14, 12, 16), Q, op, rates, "f64", pattern="aa", force=force, geometry=geometry,
+                ubb=(0.02, -0.01, 0.03))
+    for steps in (7, 10):
+        one = make_sim(case)
+        many = make_sim(case, n_local_slabs=P, halo_mode=halo_mode)
+        for s in (one, many):
+            init_sim(s, case)
+            s.step(steps)
+        mask = fluid_mask(case, Q)
+        np.testing.assert_array_equal(one.populations(raw=True)[mask], many.populations(raw=True)[mask])
+        np.testing.assert_array_equal(one.populations()[mask], many.populations()[mask])
+
+
+@pytest.mark.parametrize("halo_mode", [0, 1])
+@pytest.mark.parametrize("Q,op,rates,geometry,pattern", [(19, "trt", (1.6, 0.5), "channel", "pull"),
+                                                         (27, "cumulant", (1.95,), "periodic", "pull"),
+                                                         (19, "trt", (1.6, 0.5), "obstacles", "aa")])
+def test_nccl_self_exchange_bit_identical(halo_mode, Q, op, rates, geometry, pattern):
     """The NCCL exchange path (ghost planes, schedule, comm stream overlapped with the interior
     launch, event ordering) on one GPU through a 1-rank communicator: bit-identical to local z wrap."""
-    case = Case("self", (16, 12, 10), Q, op, rates, "f64", geometry=geometry, steps=13)
+    case = Case("self", (16, 12, 10), Q, op, rates, "f64", geometry=geometry, steps=13, pattern=pattern,
+                ubb=(0.02, -0.01, 0.03))
     one = make_sim(case)
     nc = make_sim(case, nccl_self=True, halo_mode=halo_mode)
     for s in (one, nc):
@@ -295,3 +319,49 @@ def test_full_size_sampled_parity(name):
     err = float(np.max(np.abs(got - ref) / np.abs(ref)))
     assert err <= TOL[case.dtype], err
     sim.close()
+
+
+# -----------------------------------------------------------------------------------------
+# Low-level kernel ABI on caller-owned (torch) device memory
+# -----------------------------------------------------------------------------------------
+@pytest.mark.parametrize("pattern", ["pull", "aa"])
+def test_low_level_kernel_abi(pattern):
+    import ctypes as C
+    import torch
+    from paper_2001_11806_b200 import lbm as L
+    case = Case("ll", (19, 14, 9), 19, "trt", (1.6, 0.5), "f64", pattern=pattern, force=(1e-5, 0, 0),
+                geometry="obstacles", ubb=(0.02, 0.0, -0.01), steps=6)
+    nx, ny, nz = case.shape
+    d = O.Domain(case.method(), nx, ny, nz, flags=case.flags())
+    rho, u = case.fields()
+    f0 = d.init_equilibrium(rho, u)
+    _, w, _ = O.stencil_arrays(19)
+    g0 = torch.from_numpy(f0 - w[:, None, None, None]).cuda()
+    g1 = g0.clone()
+    fl = torch.empty(nx * ny * nz, dtype=torch.uint8, device="cuda")
+    stream = torch.cuda.Stream()
+    hf = np.ascontiguousarray(case.flags())
+    assert L.lbm_prepare_flags(hf.ctypes.data, nx, ny, nz, 0, fl.data_ptr(), stream.cuda_stream) == 0
+    k = L.lbm_kernel_args()
+    k.stencil, k.collision, k.dtype = 19, L.TRT, L.F64
+    k.flags = fl.data_ptr()
+    k.shape[0], k.shape[1], k.shape[2] = nx, ny, nz
+    k.ghost, k.z_begin, k.z_end = 0, 0, nz
+    k.rates[0], k.rates[1] = case.rates
+    for i in range(3):
+        k.force[i] = case.force[i]
+        k.ubb_velocity[i] = case.ubb[i]
+    k.stream = stream.cuda_stream
+    a, b = g0, g1
+    for t in range(case.steps):
+        if pattern == "pull":
+            k.src, k.dst = a.data_ptr(), b.data_ptr()
+            assert L.lbm_kernel_pull(C.byref(k)) == 0
+            a, b = b, a
+        else:
+            k.dst = a.data_ptr()
+            assert L.lbm_kernel_aa(C.byref(k), t % 2) == 0
+    stream.synchronize()
+    got = a.cpu().numpy() + w[:, None, None, None]
+    ref = d.run_pull(f0, case.steps) if pattern == "pull" else d.run_push(f0, case.steps)
+    assert max_rel_err(got, ref, fluid_mask(case, 19)) <= 1e-12
