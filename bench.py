@@ -181,7 +181,9 @@ def run_reference(args, cfg):
     threads = os.cpu_count() or 1
     m = O.Method(Q=cfg["Q"], op=cfg["op"], rates=cfg["rates"], force=cfg["force"], ubb_u=cfg.get("ubb", (0, 0, 0)),
                  nthreads=threads)
-    planes = 2  # each reference step = one pull step of a 2-plane sub-slab (bounded sample)
+    # each reference step = one pull step of a sub-slab with one z plane per host thread (the
+    # oracle parallelises over z), a bounded sample of the workload
+    planes = max(2, min(nz, threads))
     d = O.Domain(m, nx, ny, planes)
     f = np.empty(d.shape)
     _, w, _ = O.stencil_arrays(cfg["Q"])
@@ -219,7 +221,7 @@ def main():
     ap.add_argument("--e2e-reps", type=int, default=2)
     ap.add_argument("--e2e-steps", type=int, default=0, help="LB steps per e2e job (0 = the config's step count)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--halo-mode", type=int, default=0)
+    ap.add_argument("--halo-mode", type=int, default=-1, help="0 zero-copy NCCL, 1 packed NCCL, 2 fused NVLink peer stores; default: 2 when exchanging (pull), else 0")
     ap.add_argument("--nccl-self", type=int, default=0,
                     help="N=1 only: ghost planes exchanged through a 1-rank NCCL communicator (times the multi-GPU path)")
     ap.add_argument("--block-x", type=int, default=0)
@@ -266,11 +268,43 @@ def main():
     use_graph = bool(small) if args.graph < 0 else bool(args.graph)
     nccl_self = bool(args.nccl_self) and world == 1
     use_graph = use_graph and not nccl_self
-    sim = L.Simulation(gshape, stencil=cfg["Q"], collision=cfg["op"], rates=cfg["rates"], dtype=cfg["dtype"],
-                       pattern=cfg["pattern"], force=cfg["force"], flags=flags, ubb_velocity=cfg.get("ubb", (0, 0, 0)),
-                       periodic=periodic, rank=rank, nranks=world, nccl_id=nccl_id, device=local,
-                       stream=stream.cuda_stream, halo_mode=args.halo_mode, use_graph=use_graph, block_x=args.block_x,
-                       nccl_self=nccl_self)
+    exchanging = world > 1 or nccl_self
+    halo_mode = args.halo_mode
+    if halo_mode < 0:  # default: fused NVLink peer-store halo for the pull pattern, else zero-copy NCCL
+        halo_mode = L.HALO_FUSED if (exchanging and cfg["pattern"] == "pull") else L.HALO_ZEROCOPY
+
+    def make(mode):
+        return L.Simulation(gshape, stencil=cfg["Q"], collision=cfg["op"], rates=cfg["rates"], dtype=cfg["dtype"],
+                            pattern=cfg["pattern"], force=cfg["force"], flags=flags,
+                            ubb_velocity=cfg.get("ubb", (0, 0, 0)), periodic=periodic, rank=rank, nranks=world,
+                            nccl_id=nccl_id, device=local, stream=stream.cuda_stream, halo_mode=mode,
+                            use_graph=use_graph, block_x=args.block_x, nccl_self=nccl_self)
+
+    sim, err = None, None
+    try:
+        sim = make(halo_mode)
+    except L.LBMError as e:
+        err = str(e)
+    if world > 1:  # every rank must agree before falling back (creation is collective)
+        ok = torch.tensor([0 if sim is None else 1], dtype=torch.int32, device="cuda")
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+        if int(ok) == 0 and sim is not None:
+            sim.close()
+            sim = None
+    if sim is None:
+        if halo_mode != L.HALO_FUSED:
+            raise RuntimeError(err or "lbm_create failed on another rank")
+        if rank == 0:
+            print(f"# fused halo unavailable ({err}); falling back to zero-copy NCCL", file=sys.stderr)
+        halo_mode = L.HALO_ZEROCOPY
+        if world > 1:  # fresh NCCL id for the second communicator
+            buf = torch.zeros(128, dtype=torch.uint8, device="cuda")
+            if rank == 0:
+                buf.copy_(torch.frombuffer(bytearray(L.nccl_unique_id()), dtype=torch.uint8))
+            dist.broadcast(buf, 0)
+            nccl_id = bytes(buf.cpu().numpy().tobytes())
+        sim = make(halo_mode)
+    args.halo_mode = halo_mode
     kind = cfg["init"][0]
     if kind == "rest":
         sim.init_equilibrium(torch.ones(sim.cells, dtype=torch.float64, device="cuda"),
@@ -371,7 +405,7 @@ def main():
                        "parallelism": f"z-slab x{world}" if world > 1 else
                        ("single GPU, NCCL self-exchange of ghost planes" if nccl_self else "single GPU"),
                        "l2": "inputs larger than L2 (no flush)" if not small else "L2-resident (launch-bound config)",
-                       "halo_mode": "zerocopy" if args.halo_mode == 0 else "packed", "cuda_graph": use_graph},
+                       "halo_mode": {0: "zerocopy NCCL send/recv", 1: "packed NCCL send/recv", 2: "fused NVLink peer stores (NCCL LSA windows)"}[args.halo_mode] if (world > 1 or nccl_self) else "none (single slab, z wraps in-kernel)", "cuda_graph": use_graph},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                          "traffic": load_traffic(args.config), "peak_source": peak_src,
                          "algorithmic_bytes_per_cell": bpc, "cells_per_launch": nf_local,

@@ -75,6 +75,10 @@ extern "C" {
 
 #define LBM_HALO_ZEROCOPY 0 /* one NCCL message per crossing population plane */
 #define LBM_HALO_PACKED 1   /* pack kernel + one message per face            */
+#define LBM_HALO_FUSED 2    /* pull + NCCL ranks: the boundary-plane kernel stores crossing
+                               populations straight into the neighbours' ghost planes through
+                               NCCL symmetric-window (LSA) pointers over NVLink; an LSA barrier
+                               kernel orders the steps. Arrays live in ncclMemAlloc memory. */
 
 typedef struct lbm_config {
     int32_t stencil;   /* LBM_D3Q19 | LBM_D3Q27 */
@@ -95,7 +99,7 @@ typedef struct lbm_config {
                                with device copies (loopback; tests the multi-GPU path on one GPU) */
     int32_t device;         /* CUDA device ordinal */
     void *stream;           /* cudaStream_t for compute; NULL = library-created stream */
-    int32_t halo_mode;      /* LBM_HALO_ZEROCOPY | LBM_HALO_PACKED */
+    int32_t halo_mode;      /* LBM_HALO_ZEROCOPY | LBM_HALO_PACKED | LBM_HALO_FUSED */
     int32_t use_graph;      /* 1 = capture a two-step cycle in a CUDA graph (single slab only) */
     int32_t block_x;        /* threads per block along x (0 = default) */
     int32_t check_nan_every;/* >0: check for NaN every k steps inside lbm_step (LBM_ENAN) */

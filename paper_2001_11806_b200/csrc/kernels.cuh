@@ -56,6 +56,8 @@ struct StepArgs {
     const uint8_t *flags;          // storage-indexed (with ghost planes) or nullptr; bits 0-1 = type
                                    // (0 fluid, 1 no-slip, 2 UBB), bit 7 = fluid cell with a non-fluid
                                    // neighbour (only such cells read neighbour flags)
+    void *peer_up;                 // fused halo (boundary launch only): base of the up neighbour's
+    void *peer_down;               // dst array / down neighbour's dst array (NVLink LSA pointers)
 };
 
 template <typename T>
@@ -147,6 +149,24 @@ __global__ void __launch_bounds__(256, (MinBlocks<Q, OP, T>::pull)) k_pull(const
     collide<Q, OP, T, FORCE>(g, r);
 #pragma unroll
     for (int q = 0; q < Q; ++q) dst[q * Sq + self] = g[q];
+    if (a.peer_up != nullptr) {
+        // fused halo: the crossing populations of the boundary planes also go straight into the
+        // neighbours' ghost planes (top plane, c_z = +1 -> up's plane 0; bottom, c_z = -1 -> down's nz+1)
+        const uint32_t inplane = (uint32_t)y * (uint32_t)a.geo.nx + (uint32_t)x;
+        const int64_t plane = (int64_t)a.geo.nx * a.geo.ny;
+        if (zs == a.geo.nz) {
+            T *up = static_cast<T *>(a.peer_up);
+#pragma unroll
+            for (int q = 0; q < Q; ++q)
+                if (S::cz(q) == 1) up[q * Sq + inplane] = g[q];
+        }
+        if (zs == 1) {
+            T *dn = static_cast<T *>(a.peer_down);
+#pragma unroll
+            for (int q = 0; q < Q; ++q)
+                if (S::cz(q) == -1) dn[q * Sq + (a.geo.nz + 1) * plane + inplane] = g[q];
+        }
+    }
 }
 
 // =======================================================================================

@@ -15,6 +15,7 @@
 
 #include "../../include/lbm.h"
 #include "dispatch.h"
+#include "fused.h"
 
 using namespace lbm;
 
@@ -61,6 +62,8 @@ struct lbm_handle_s {
     double *scratch = nullptr;
     size_t scratch_bytes = 0;
     Timing timing;
+    bool fused = false;       // halo through NVLink peer stores (LBM_HALO_FUSED)
+    FusedState fst;
     std::string err;
     dim3 block;
 };
@@ -128,13 +131,18 @@ void tbegin(lbm_handle_s *h, cudaStream_t s) {
 }
 void tend(lbm_handle_s *h, cudaStream_t s) { tbegin(h, s); }
 
-void launch_pull_range(lbm_handle_s *h, Slab &s, int z_begin, int nplanes, int z_step, cudaStream_t st) {
+void launch_pull_range(lbm_handle_s *h, Slab &s, int z_begin, int nplanes, int z_step, cudaStream_t st,
+                       bool peer_stores = false) {
     if (nplanes <= 0) return;
     StepArgs a = h->base;
     a.geo = geo_of(h, s);
     a.z_begin = z_begin;
     a.z_step = z_step;
     a.flags = s.flags;
+    if (peer_stores) {  // fused halo: LSA bases of the neighbours' dst array (1 - cur)
+        a.peer_up = h->fst.bases[2 * (1 - s.cur) + 0];
+        a.peer_down = h->fst.bases[2 * (1 - s.cur) + 1];
+    }
     tbegin(h, st);
     h->pull(a, s.pdf[s.cur], s.pdf[1 - s.cur], grid_for(h, nplanes), h->block, st);
     tend(h, st);
@@ -318,6 +326,16 @@ int step_once(lbm_handle_s *h) {
         return LBM_OK;
     }
     Slab &s = h->slabs[0];
+    if (h->fused) {
+        // gate (LSA barrier: all ranks finished the previous step) -> boundary planes with peer
+        // stores into the neighbours' ghost planes -> interior planes; one stream, no send/recv
+        fused_gate(h->fst, st);
+        h->launches++;
+        launch_pull_range(h, s, 0, 2, s.nz - 1, st, true);
+        launch_pull_range(h, s, 1, s.nz - 2, 1, st);
+        s.cur ^= 1;
+        return LBM_OK;
+    }
     bnd(s);
     CUDA_TRY(h, cudaEventRecord(h->ev_bnd, st));
     CUDA_TRY(h, cudaStreamWaitEvent(h->comm_stream, h->ev_bnd, 0));
@@ -377,6 +395,9 @@ int validate(const lbm_config *c) {
     if (c->global[2] % P != 0) return fail(nullptr, LBM_EINVAL, "nz % nranks != 0");
     if (P > 1 && c->global[2] / P < 2) return fail(nullptr, LBM_EINVAL, "slabs need at least 2 planes");
     if (c->nranks > 1 && !c->nccl_id) return fail(nullptr, LBM_EINVAL, "nranks > 1 needs an nccl_id");
+    if (c->halo_mode == LBM_HALO_FUSED && ((c->nranks == 1 && !c->nccl_self) || c->pattern != LBM_PULL))
+        return fail(nullptr, LBM_EUNSUPPORTED, "fused halo needs NCCL ranks (or nccl_self) and the pull pattern");
+    if (c->halo_mode < 0 || c->halo_mode > 2) return fail(nullptr, LBM_EINVAL, "bad halo_mode");
     if (c->nccl_self && (c->nranks != 1 || c->n_local_slabs > 1 || c->global[2] < 2))
         return fail(nullptr, LBM_EINVAL, "nccl_self needs nranks == 1, one slab and nz >= 2");
     const int64_t planes = c->global[2] / P + (P > 1 ? 2 : 0);
@@ -643,6 +664,7 @@ int lbm_create(const lbm_config *cfg, lbm_handle *out) {
     h->nranks = cfg->nranks;
     const int P = cfg->nranks > 1 ? cfg->nranks : (cfg->n_local_slabs > 1 ? cfg->n_local_slabs : 1);
     h->use_nccl = cfg->nranks > 1 || cfg->nccl_self;
+    h->fused = h->use_nccl && cfg->halo_mode == LBM_HALO_FUSED;
     h->g = (P > 1 || h->use_nccl) ? 1 : 0;
     h->have_flags = cfg->flags != nullptr;
     h->have_force = cfg->force[0] != 0 || cfg->force[1] != 0 || cfg->force[2] != 0;
@@ -726,6 +748,7 @@ int lbm_create(const lbm_config *cfg, lbm_handle *out) {
         const Geo g = geo_of(h, s);
         const size_t bytes = (size_t)g.Sq * h->Q * h->esize;
         for (int a = 0; a < (cfg->pattern == LBM_PULL ? 2 : 1); ++a) {
+            if (h->fused) break;  // allocated in NCCL symmetric memory below
             if (cudaMalloc(&s.pdf[a], bytes) != cudaSuccess) {
                 h->err = "cudaMalloc populations (" + std::to_string(bytes) + " B)";
                 return bail(LBM_EOOM);
@@ -777,6 +800,22 @@ int lbm_create(const lbm_config *cfg, lbm_handle *out) {
             h->err = std::string("ncclCommInitRank: ") + ncclGetErrorString(r);
             return bail(LBM_ENCCL);
         }
+        if (h->fused) {
+            Slab &s = h->slabs[0];
+            const size_t bytes = (size_t)geo_of(h, s).Sq * h->Q * h->esize;
+            for (int a = 0; a < 2; ++a) {
+                if ((r = ncclMemAlloc(&s.pdf[a], bytes)) != ncclSuccess) {
+                    h->err = std::string("ncclMemAlloc populations: ") + ncclGetErrorString(r);
+                    return bail(LBM_EOOM);
+                }
+                cudaMemsetAsync(s.pdf[a], 0, bytes, h->stream);
+            }
+            std::string err;
+            if (fused_setup(h->comm, s.pdf[0], s.pdf[1], bytes, h->up, h->down, &h->fst, h->stream, err)) {
+                h->err = "fused halo: " + err;
+                return bail(LBM_ENCCL);
+            }
+        }
     }
     cudaError_t e = cudaStreamSynchronize(h->stream);
     if (e != cudaSuccess) {
@@ -792,8 +831,13 @@ int lbm_destroy(lbm_handle h) {
     if (h->stream) cudaStreamSynchronize(h->stream);
     if (h->comm_stream) cudaStreamSynchronize(h->comm_stream);
     if (h->graph) cudaGraphExecDestroy(h->graph);
+    if (h->fused && h->comm) fused_teardown(h->comm, &h->fst);
     for (Slab &s : h->slabs) {
-        for (void *p : s.pdf) if (p) cudaFree(p);
+        for (void *p : s.pdf)
+            if (p) {
+                if (h->fused) ncclMemFree(p);
+                else cudaFree(p);
+            }
         for (void *p : s.halo) if (p) cudaFree(p);
         if (s.flags) cudaFree(s.flags);
     }

@@ -26,7 +26,7 @@ F64, F32 = 0, 1
 PULL, AA = 0, 1
 FLUID, NOSLIP, UBB = 0, 1, 2
 HOST, DEVICE = 0, 1
-HALO_ZEROCOPY, HALO_PACKED = 0, 1
+HALO_ZEROCOPY, HALO_PACKED, HALO_FUSED = 0, 1, 2
 
 COLLISIONS = {"srt": SRT, "trt": TRT, "mrt": MRT, "cumulant": CUMULANT, "identity": IDENTITY}
 DTYPES = {"f64": F64, "float64": F64, "fp64": F64, "f32": F32, "float32": F32, "fp32": F32}
