@@ -14,8 +14,10 @@
  *     pattern.
  *   - Boundaries from a uint8 flag field, compiled into the kernel:
  *     0 = fluid, 1 = no-slip bounce-back, 2 = velocity bounce-back UBB (G8).
- *   - Multi-GPU: z-slab decomposition, one ghost plane per side, NCCL send/recv of the
- *     populations crossing each z face, overlapped with the interior update.
+ *   - Multi-GPU: z-slab decomposition, one ghost plane per side; the populations crossing each z
+ *     face move by NCCL send/recv overlapped with the interior update, or (LBM_HALO_FUSED) are
+ *     stored by the boundary-plane kernel straight into the neighbour's ghost plane over NVLink
+ *     (P:1056-1071). AA slabs: ghost fill after even steps, return of ghost writes after odd steps.
  *
  * Layout (part of the ABI): populations are SoA  f[q][z][y][x], x fastest. Host-visible arrays
  * passed to this API always use the canonical layout of the *local* slab (no ghost planes):
@@ -114,10 +116,10 @@ typedef struct lbm_handle_s *lbm_handle;
 void lbm_config_default(lbm_config *cfg);
 
 /* Create a simulation. Validates cfg (LBM_EINVAL: bad enum, rate outside (0,2), nz % nranks != 0,
- * non-periodic axis without walls on its faces; LBM_EUNSUPPORTED: AA with flags or with
- * decomposition, MRT other than D3Q19, cumulant other than D3Q27, force with MRT/cumulant),
- * allocates device memory and, for nranks > 1, creates the NCCL communicator (collective: every
- * rank must call it). The state is zero until an init call. */
+ * slabs thinner than 2 planes, non-periodic axis without walls on its faces; LBM_EUNSUPPORTED:
+ * MRT other than D3Q19, cumulant other than D3Q27, force with MRT/cumulant, fused halo with the AA
+ * pattern), allocates device memory and, for nranks > 1 (or nccl_self), creates the NCCL
+ * communicator (collective: every rank must call it). The state is zero until an init call. */
 int lbm_create(const lbm_config *cfg, lbm_handle *out);
 int lbm_destroy(lbm_handle h);
 
