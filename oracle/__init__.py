@@ -24,8 +24,9 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 SRC = os.path.join(HERE, "lbm_oracle.c")
 LIB = os.path.join(HERE, "liblbm_oracle.so")
 
-SRT, TRT, MRT, CUMULANT, IDENTITY = 0, 1, 2, 3, 4
-OPS = {"srt": SRT, "trt": TRT, "mrt": MRT, "cumulant": CUMULANT, "identity": IDENTITY}
+SRT, TRT, MRT, CUMULANT, IDENTITY, SMAGORINSKY, KBC = 0, 1, 2, 3, 4, 5, 6
+OPS = {"srt": SRT, "trt": TRT, "mrt": MRT, "cumulant": CUMULANT, "identity": IDENTITY,
+       "smagorinsky": SMAGORINSKY, "kbc": KBC}
 FLUID, NOSLIP, UBB = 0, 1, 2
 
 
@@ -67,6 +68,7 @@ def lib():
             ("ora_init_equilibrium", [P, P, P, P], C.c_int),
             ("ora_macroscopic", [P, P, C.c_double, P, P], C.c_int),
             ("ora_collide_cell", [P, P, P], None),
+            ("ora_smagorinsky_omega_cell", [P, P], C.c_double),
             ("ora_equilibrium_cell", [C.c_int, C.c_double, P, P], None),
             ("ora_product_equilibrium_cell", [C.c_int, C.c_double, P, P], None),
             ("ora_cumulants_cell", [C.c_int, P, P], C.c_double),
@@ -117,8 +119,11 @@ class Method:
             dirs = methods.stencil(name)
             Mr = methods.moment_matrix(polys, dirs)
             Minv = methods.mat_inverse(Mr)
-            r = list(self.rates) + [1.0] * 4
-            S = methods.mrt_rates_per_row(groups, r[0], r[1], r[2], r[3])
+            if self.op == "kbc":  # row parts: 0 conserved, 1 shear (s), 2 higher order (h)
+                S = [0.0 if g == "conserved" else 1.0 if g == "shear" else 2.0 for g in groups]
+            else:
+                r = list(self.rates) + [1.0] * 4
+                S = methods.mrt_rates_per_row(groups, r[0], r[1], r[2], r[3])
             self._mats = (np.array([[float(v) for v in row] for row in Mr]),
                           np.array([[float(v) for v in row] for row in Minv]),
                           np.array(S, dtype=np.float64))
@@ -153,7 +158,7 @@ class Domain:
         cfg.ubb_u = (C.c_double * 3)(*method.ubb_u)
         cfg.ubb_rho = method.ubb_rho
         self._keep = []
-        if method.op == "mrt":
+        if method.op in ("mrt", "kbc"):
             M, Minv, S = method.mrt_matrices()
             self._keep = [np.ascontiguousarray(M), np.ascontiguousarray(Minv), np.ascontiguousarray(S)]
             cfg.M, cfg.Minv, cfg.S = (_p(a) for a in self._keep)
@@ -282,3 +287,9 @@ def from_cumulants_cell(rho: float, kappa: np.ndarray) -> np.ndarray:
     out = np.zeros(27)
     lib().ora_from_cumulants_cell(27, rho, _p(k), _p(out))
     return out
+
+
+def smagorinsky_omega_cell(method: Method, f: np.ndarray) -> float:
+    d = Domain(method, 1, 1, 1)
+    f = np.ascontiguousarray(f, np.float64)
+    return lib().ora_smagorinsky_omega_cell(d._pc(), _p(f))

@@ -35,6 +35,8 @@
 #define ORA_MRT 2
 #define ORA_CUMULANT 3
 #define ORA_IDENTITY 4
+#define ORA_SMAGORINSKY 5
+#define ORA_KBC 6
 
 #define FLAG_FLUID 0
 #define FLAG_NOSLIP 1
@@ -52,7 +54,8 @@ typedef struct {
     double ubb_rho;     /* UBB reference density rho_w (G8: 1) */
     const double *M;    /* MRT: Q x Q moment matrix, row-major (M_kq = P_k(c_q)) */
     const double *Minv; /* MRT: its inverse */
-    const double *S;    /* MRT: Q relaxation rates (diagonal of S) */
+    const double *S;    /* MRT: Q relaxation rates (diagonal of S); KBC: per-row part, 0 conserved,
+                           1 = shear (s), 2 = higher order (h) */
 } ora_cfg;
 
 /* ------------------------------------------------------------------------------------ */
@@ -362,8 +365,75 @@ static void collide_cumulant(const ora_cfg *cfg, const ora_stencil_t *s, const d
     from_cumulants(s, rho, kap, out);
 }
 
+/* Smagorinsky SRT (Eqs. 11-14): nu_t = (C_S Delta)^2 |S|, Delta = 1,
+ * |S| = sqrt(2 S_ij S_ij), S_ij = -(3 omega / (2 rho)) Pi^neq_ij, Pi^neq = sum_q c c (f - f_eq),
+ * omega = 2 / (6 C_S^2 |S| + 6 nu_0 + 1). Solving the two equations for omega (the step the paper
+ * leaves to sympy): with tau_0 = 1/omega_0 = 3 nu_0 + 1/2 and P = sqrt(2 Pi:Pi),
+ * (9 C^2 P / rho) omega^2 + 2 tau_0 omega - 2 = 0, whose positive root is
+ * omega = 2 / (tau_0 + sqrt(tau_0^2 + 18 C^2 P / rho)). rates = [omega_0, C_S]. */
+static double smagorinsky_omega(const ora_stencil_t *s, const double *f, double rho, const double *feq,
+                                double omega0, double cs) {
+    double Pi[3][3];
+    for (int a = 0; a < 3; ++a)
+        for (int b = 0; b < 3; ++b) {
+            double v = 0.0;
+            for (int q = 0; q < s->Q; ++q) v += s->c[q][a] * s->c[q][b] * (f[q] - feq[q]);
+            Pi[a][b] = v;
+        }
+    double pp = 0.0;
+    for (int a = 0; a < 3; ++a)
+        for (int b = 0; b < 3; ++b) pp += Pi[a][b] * Pi[a][b];
+    double P = sqrt(2.0 * pp);
+    double tau0 = 1.0 / omega0;
+    return 2.0 / (tau0 + sqrt(tau0 * tau0 + 18.0 * cs * cs * P / rho));
+}
+
+static void collide_smagorinsky(const ora_cfg *cfg, const ora_stencil_t *s, const double *f, double *out) {
+    double rho, u[3], feq[27];
+    macroscopic(s, f, cfg->force, +1.0, &rho, u);
+    equilibrium(s, rho, u, feq);
+    double w = smagorinsky_omega(s, f, rho, feq, cfg->rates[0], cfg->rates[1]);
+    for (int q = 0; q < s->Q; ++q) out[q] = w * feq[q] + (1.0 - w) * f[q]; /* Eq. (1) with the local omega */
+}
+
+/* KBC entropic operator: with an MRT basis split into shear moments (s) and the other
+ * non-conserved moments (h), f = f_eq + Delta_s + Delta_h and (Eq. 16) f' = f - w_s Delta_s - w_h Delta_h;
+ * w_h from the linearised entropy condition (Eq. 19): w_h = 1 + (1 - w_s) <Ds,Dh>_E / <Dh,Dh>_E with
+ * <a,b>_E = sum_q a_q b_q / f_eq,q. Delta_s = M^-1 [s rows of M(f - f_eq)], Delta_h likewise.
+ * rates = [w_s]. */
+static void collide_kbc(const ora_cfg *cfg, const ora_stencil_t *s, const double *f, double *out) {
+    int Q = s->Q;
+    double rho, u[3], feq[27], dm[27], ms[27], mh[27], ds[27], dh[27];
+    macroscopic(s, f, cfg->force, +1.0, &rho, u);
+    equilibrium(s, rho, u, feq);
+    for (int k = 0; k < Q; ++k) {
+        dm[k] = 0.0;
+        for (int q = 0; q < Q; ++q) dm[k] += cfg->M[k * Q + q] * (f[q] - feq[q]);
+        ms[k] = (cfg->S[k] == 1.0) ? dm[k] : 0.0;
+        mh[k] = (cfg->S[k] == 2.0) ? dm[k] : 0.0;
+    }
+    for (int q = 0; q < Q; ++q) {
+        ds[q] = 0.0;
+        dh[q] = 0.0;
+        for (int k = 0; k < Q; ++k) {
+            ds[q] += cfg->Minv[q * Q + k] * ms[k];
+            dh[q] += cfg->Minv[q * Q + k] * mh[k];
+        }
+    }
+    double sh = 0.0, hh = 0.0;
+    for (int q = 0; q < Q; ++q) {
+        sh += ds[q] * dh[q] / feq[q];
+        hh += dh[q] * dh[q] / feq[q];
+    }
+    double ws = cfg->rates[0];
+    double wh = (hh > 0.0) ? 1.0 + (1.0 - ws) * sh / hh : 1.0;
+    for (int q = 0; q < Q; ++q) out[q] = f[q] - ws * ds[q] - wh * dh[q];
+}
+
 static void collide(const ora_cfg *cfg, const ora_stencil_t *s, const double *f, double *out) {
     switch (cfg->op) {
+        case ORA_SMAGORINSKY: collide_smagorinsky(cfg, s, f, out); break;
+        case ORA_KBC: collide_kbc(cfg, s, f, out); break;
         case ORA_SRT: collide_srt(cfg, s, f, out); break;
         case ORA_TRT: collide_trt(cfg, s, f, out); break;
         case ORA_MRT: collide_mrt(cfg, s, f, out); break;
@@ -604,6 +674,16 @@ int ora_macroscopic(const ora_cfg *cfg, const double *f, double fsign, double *r
 }
 
 /* Single-cell helpers for tests and sampled full-size parity. */
+/* The local Smagorinsky omega of a pre-collision cell state (for the Eq. (14) pins). */
+double ora_smagorinsky_omega_cell(const ora_cfg *cfg, const double *f) {
+    ora_stencil_t s;
+    build_stencil(cfg->Q, &s);
+    double rho, u[3], feq[27];
+    macroscopic(&s, f, cfg->force, +1.0, &rho, u);
+    equilibrium(&s, rho, u, feq);
+    return smagorinsky_omega(&s, f, rho, feq, cfg->rates[0], cfg->rates[1]);
+}
+
 void ora_collide_cell(const ora_cfg *cfg, const double *f, double *out) {
     ora_stencil_t s;
     build_stencil(cfg->Q, &s);

@@ -35,13 +35,14 @@ class Exact:
         self.rates = [to_fr(r) for r in rates]
         self.F = [to_fr(v) for v in force]
         self.uw = [to_fr(v) for v in ubb_u]
-        if op == "mrt":
+        if op in ("mrt", "kbc"):
             polys, groups = methods.mrt_method(self.name, weighted=True)
             self.M = methods.moment_matrix(polys, self.dirs)
             self.Minv = methods.mat_inverse(self.M)
             r = list(self.rates) + [Fr(1)] * 4
             tab = {"conserved": Fr(0), "shear": r[0], "bulk": r[1], "order3": r[2], "order4+": r[3]}
             self.S = [tab[g] for g in groups]
+            self.groups = groups
         if op == "cumulant":
             self.rates = list(self.rates) + [Fr(1)] * (6 - len(self.rates))
 
@@ -93,6 +94,18 @@ class Exact:
             me = [sum((self.M[k][q] * fe[q] for q in range(Q)), Fr(0)) for k in range(Q)]
             mp = [self.S[k] * me[k] + (1 - self.S[k]) * m[k] for k in range(Q)]
             return [sum((self.Minv[q][k] * mp[k] for k in range(Q)), Fr(0)) for q in range(Q)]
+        if self.op == "kbc":  # Eqs. (16), (19): s = shear rows, h = the other non-conserved rows
+            Q = self.Q
+            dm = [sum((self.M[k][q] * (f[q] - fe[q]) for q in range(Q)), Fr(0)) for k in range(Q)]
+            ms = [dm[k] if self.groups[k] == "shear" else Fr(0) for k in range(Q)]
+            mh = [dm[k] if self.groups[k] not in ("shear", "conserved") else Fr(0) for k in range(Q)]
+            ds = [sum((self.Minv[q][k] * ms[k] for k in range(Q)), Fr(0)) for q in range(Q)]
+            dh = [sum((self.Minv[q][k] * mh[k] for k in range(Q)), Fr(0)) for q in range(Q)]
+            sh = sum((ds[q] * dh[q] / fe[q] for q in range(Q)), Fr(0))
+            hh = sum((dh[q] * dh[q] / fe[q] for q in range(Q)), Fr(0))
+            ws = self.rates[0]
+            wh = 1 + (1 - ws) * sh / hh if hh != 0 else Fr(1)
+            return [f[q] - ws * ds[q] - wh * dh[q] for q in range(Q)]
         raise ValueError(self.op)
 
     # truncated series in xi with exponents <= 2 per axis: dict (a,b,c) -> Fr
