@@ -61,6 +61,10 @@ extern "C" {
 #define LBM_MRT 2      /* rates = [omega_shear, omega_bulk, omega_3, omega_4] (D3Q19)  */
 #define LBM_CUMULANT 3 /* rates = [omega_shear, omega_bulk, omega_3..omega_6] (D3Q27); missing = 1 */
 #define LBM_IDENTITY 4 /* debug: no collision (pure data movement, bit-exact tests)    */
+#define LBM_SMAGORINSKY 5 /* SRT with the local Smagorinsky omega (Eqs. 11-14):
+                             rates = [omega_0, C_S]                                    */
+#define LBM_KBC 6      /* entropic KBC (Eqs. 15-19), D3Q19: rates = [omega_s];
+                          s = shear moments, h = the other non-conserved moments        */
 
 #define LBM_F64 0
 #define LBM_F32 1

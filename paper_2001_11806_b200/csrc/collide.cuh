@@ -224,6 +224,171 @@ __device__ __forceinline__ void collide_mrt19(T (&g)[19], const Rates<T> &p) {
 }
 
 // ---------------------------------------------------------------------------------------
+// Smagorinsky SRT (Eqs. 11-14), rates = [omega_0, C_S]. The local omega solves
+// Eq. (14) with |S| of Eq. (12): omega = 2 / (tau_0 + sqrt(tau_0^2 + 18 C_S^2 P / rho)),
+// P = sqrt(2 Pi^neq : Pi^neq), tau_0 = 1/omega_0; then Eq. (1) with that omega.
+// ---------------------------------------------------------------------------------------
+template <int Q, typename T>
+__device__ __forceinline__ void collide_smagorinsky(T (&g)[Q], const Rates<T> &p) {
+    using S = Stencil<Q>;
+    T drho, jx, jy, jz;
+    moments0<Q, T>(g, drho, jx, jy, jz);
+    const T rho = T(1) + drho;
+    const T inv = T(1) / rho;
+    const T ux = jx * inv, uy = jy * inv, uz = jz * inv;
+    const T uu15 = T(1.5) * (ux * ux + uy * uy + uz * uz);
+    T d[Q];  // non-equilibrium part g - g_eq
+    {
+        const T w0 = T(S::w(0));
+        d[0] = g[0] - (w0 * drho - w0 * rho * uu15);
+    }
+#pragma unroll
+    for (int q = 1; q < Q; ++q) {
+        if (q < S::opp(q)) {
+            const int b = S::opp(q);
+            const T w = T(S::w(q));
+            const T cu = T(S::cx(q)) * ux + T(S::cy(q)) * uy + T(S::cz(q)) * uz;
+            const T wr = w * rho;
+            const T eqs = w * drho + wr * (T(4.5) * cu * cu - uu15);
+            const T eqa = wr * T(3) * cu;
+            d[q] = g[q] - (eqs + eqa);
+            d[b] = g[b] - (eqs - eqa);
+        }
+    }
+    // Pi^neq_ab = sum_q c_a c_b d_q (only the non-zero products of the stencil)
+    T pxx = T(0), pyy = T(0), pzz = T(0), pxy = T(0), pxz = T(0), pyz = T(0);
+#pragma unroll
+    for (int q = 1; q < Q; ++q) {
+        if (S::cx(q) != 0) pxx += d[q];
+        if (S::cy(q) != 0) pyy += d[q];
+        if (S::cz(q) != 0) pzz += d[q];
+        if (S::cx(q) * S::cy(q) > 0) pxy += d[q];
+        if (S::cx(q) * S::cy(q) < 0) pxy -= d[q];
+        if (S::cx(q) * S::cz(q) > 0) pxz += d[q];
+        if (S::cx(q) * S::cz(q) < 0) pxz -= d[q];
+        if (S::cy(q) * S::cz(q) > 0) pyz += d[q];
+        if (S::cy(q) * S::cz(q) < 0) pyz -= d[q];
+    }
+    const T pp = pxx * pxx + pyy * pyy + pzz * pzz + T(2) * (pxy * pxy + pxz * pxz + pyz * pyz);
+    const T P = sqrt(T(2) * pp);
+    const T tau0 = T(1) / p.r[0];
+    const T cs = p.r[1];
+    const T omega = T(2) / (tau0 + sqrt(tau0 * tau0 + T(18) * cs * cs * P * inv));
+#pragma unroll
+    for (int q = 0; q < Q; ++q) g[q] -= omega * d[q];
+}
+
+// ---------------------------------------------------------------------------------------
+// KBC entropic operator, D3Q19 (Eqs. 15-19), rates = [omega_s]. Delta_s = shear-group
+// projection, Delta_h = bulk + order 3 + order 4 projections of g - g_eq (the weighted basis of
+// collide_mrt19); omega_h = 1 + (1 - omega_s) <Ds,Dh>_E / <Dh,Dh>_E, <a,b>_E = sum a b / f_eq.
+// ---------------------------------------------------------------------------------------
+template <typename T>
+__device__ __forceinline__ void collide_kbc19(T (&g)[19], const Rates<T> &p) {
+    using S = Stencil<19>;
+    T drho, jx, jy, jz;
+    moments0<19, T>(g, drho, jx, jy, jz);
+    const T rho = T(1) + drho;
+    const T inv = T(1) / rho;
+    const T ux = jx * inv, uy = jy * inv, uz = jz * inv;
+    const T uu15 = T(1.5) * (ux * ux + uy * uy + uz * uz);
+    const T w0 = T(S::w(0));
+    const T eq0 = w0 * drho - w0 * rho * uu15;
+    const T d0 = g[0] - eq0;
+    T dp[19], dm[19], es[19], ea[19];
+#pragma unroll
+    for (int q = 1; q < 19; ++q) {
+        if (q < S::opp(q)) {
+            const int b = S::opp(q);
+            const T w = T(S::w(q));
+            const T cu = T(S::cx(q)) * ux + T(S::cy(q)) * uy + T(S::cz(q)) * uz;
+            const T wr = w * rho;
+            es[q] = w * drho + wr * (T(4.5) * cu * cu - uu15);
+            ea[q] = wr * T(3) * cu;
+            dp[q] = (g[q] + g[b]) - T(2) * es[q];
+            dm[q] = (g[q] - g[b]) - T(2) * ea[q];
+        }
+    }
+    T a[15];  // <P_k, g - g_eq> / N_k
+#pragma unroll
+    for (int k = 0; k < 15; ++k) {
+        const bool odd = (k >= 6 && k <= 11);
+        T m = T(0);
+        if (!odd) {
+            const int c0 = mrt_poly(k, 0, 0, 0);
+            if (c0 != 0) m = T(c0) * d0;
+        }
+#pragma unroll
+        for (int q = 1; q < 19; ++q) {
+            if (q < S::opp(q)) {
+                const int c = mrt_poly(k, S::cx(q), S::cy(q), S::cz(q));
+                const T v = odd ? dm[q] : dp[q];
+                if (c == 1) m += v;
+                else if (c == -1) m -= v;
+                else if (c != 0) m += T(c) * v;
+            }
+        }
+        a[k] = T(mrt_inv_norm(k)) * m;
+    }
+    // Delta_s (shear, even) and Delta_h (even part: bulk + order 4, odd part: order 3) per pair
+    T s0 = T(0), h0 = T(0);
+#pragma unroll
+    for (int k = 0; k < 15; ++k) {
+        const int c = mrt_poly(k, 0, 0, 0);
+        if (c != 0) {
+            if (mrt_group(k) == 0) s0 += T(c) * a[k];
+            else h0 += T(c) * a[k];
+        }
+    }
+    T se[19], he[19], ho[19];
+#pragma unroll
+    for (int q = 1; q < 19; ++q) {
+        if (q < S::opp(q)) {
+            T s = T(0), he_ = T(0), ho_ = T(0);
+#pragma unroll
+            for (int k = 0; k < 15; ++k) {
+                const int c = mrt_poly(k, S::cx(q), S::cy(q), S::cz(q));
+                if (c == 0) continue;
+                T &acc = mrt_group(k) == 0 ? s : ((k >= 6 && k <= 11) ? ho_ : he_);
+                if (c == 1) acc += a[k];
+                else if (c == -1) acc -= a[k];
+                else acc += T(c) * a[k];
+            }
+            const T w = T(S::w(q));
+            se[q] = w * s;
+            he[q] = w * he_;
+            ho[q] = w * ho_;
+        }
+    }
+    // entropic products with 1/f_eq (f_eq = w + g_eq)
+    const T ds0 = w0 * s0, dh0 = w0 * h0;
+    const T ief0 = T(1) / (w0 + eq0);
+    T sh = ds0 * dh0 * ief0, hh = dh0 * dh0 * ief0;
+#pragma unroll
+    for (int q = 1; q < 19; ++q) {
+        if (q < S::opp(q)) {
+            const T w = T(S::w(q));
+            const T iq = T(1) / (w + es[q] + ea[q]);
+            const T ib = T(1) / (w + es[q] - ea[q]);
+            const T hq = he[q] + ho[q], hb = he[q] - ho[q];
+            sh += se[q] * (hq * iq + hb * ib);
+            hh += hq * hq * iq + hb * hb * ib;
+        }
+    }
+    const T ws = p.r[0];
+    const T wh = hh > T(0) ? T(1) + (T(1) - ws) * sh / hh : T(1);
+    g[0] -= ws * ds0 + wh * dh0;
+#pragma unroll
+    for (int q = 1; q < 19; ++q) {
+        if (q < S::opp(q)) {
+            const int b = S::opp(q);
+            g[q] -= ws * se[q] + wh * (he[q] + ho[q]);
+            g[b] -= ws * se[q] + wh * (he[q] - ho[q]);
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------------------
 // Cumulant, D3Q27.
 // Tensor index of a direction: t = (cx+1)*9 + (cy+1)*3 + (cz+1); after the forward transform
 // slot (a,b,c) holds the central moment K_abc = sum_q (cx-ux)^a (cy-uy)^b (cz-uz)^c f_q.
@@ -388,7 +553,7 @@ __device__ __forceinline__ void collide_cumulant27(T (&g)[27], const Rates<T> &p
 // ---------------------------------------------------------------------------------------
 // Dispatch
 // ---------------------------------------------------------------------------------------
-enum Op { OP_SRT = 0, OP_TRT = 1, OP_MRT = 2, OP_CUMULANT = 3, OP_IDENTITY = 4 };
+enum Op { OP_SRT = 0, OP_TRT = 1, OP_MRT = 2, OP_CUMULANT = 3, OP_IDENTITY = 4, OP_SMAGORINSKY = 5, OP_KBC = 6 };
 
 template <int Q, int OP, typename T, bool FORCE>
 __device__ __forceinline__ void collide(T (&g)[Q], const Rates<T> &p) {
@@ -400,6 +565,11 @@ __device__ __forceinline__ void collide(T (&g)[Q], const Rates<T> &p) {
     } else if constexpr (OP == OP_CUMULANT) {
         static_assert(Q == 27, "cumulant is implemented for D3Q27");
         collide_cumulant27<T>(g, p);
+    } else if constexpr (OP == OP_SMAGORINSKY) {
+        collide_smagorinsky<Q, T>(g, p);
+    } else if constexpr (OP == OP_KBC) {
+        static_assert(Q == 19, "KBC is implemented for D3Q19");
+        collide_kbc19<T>(g, p);
     }
 }
 

@@ -14,6 +14,15 @@ PullLaunch select_pull_trt(int Q, int dtype, bool flags, bool force);
 PullLaunch select_pull_mrt(int Q, int dtype, bool flags, bool force);
 PullLaunch select_pull_cumulant(int Q, int dtype, bool flags, bool force);
 PullLaunch select_pull_identity(int Q, int dtype, bool flags, bool force);
+PullLaunch select_pull_smagorinsky(int Q, int dtype, bool flags, bool force);
+PullLaunch select_pull_kbc(int Q, int dtype, bool flags, bool force);
+AALaunch select_aa_smagorinsky(int Q, int dtype, bool flags, bool force);
+AALaunch select_aa_kbc(int Q, int dtype, bool flags, bool force);
+
+// Operator dispatch used by the handle API and the low-level kernel ABI (runtime.cu); SRT runs the
+// TRT kernel with equal rates. nullptr = combination not instantiated.
+PullLaunch select_pull(int collision, int Q, int dtype, bool flags, bool force);
+AALaunch select_aa(int collision, int Q, int dtype, bool flags, bool force);
 AALaunch select_aa_trt(int Q, int dtype, bool flags, bool force);
 AALaunch select_aa_mrt(int Q, int dtype, bool flags, bool force);
 AALaunch select_aa_cumulant(int Q, int dtype, bool flags, bool force);

@@ -24,10 +24,11 @@ namespace lbm {
 template <int Q, int OP, typename T>
 struct MinBlocks {
     static constexpr bool f64 = sizeof(T) == 8;
+    // OP: 0 SRT, 1 TRT, 2 MRT, 3 cumulant, 4 identity, 5 Smagorinsky, 6 KBC
     static constexpr int pull_default =
-        f64 ? ((OP == 2 || (Q == 27 && OP <= 1)) ? 2 : 3)
-            : ((OP <= 1 || OP == 4) ? (Q == 19 ? 6 : 4) : 3);
-    static constexpr int aa_default = f64 ? 2 : ((OP == 2 || (Q == 19 && OP <= 1)) ? 3 : 2);
+        f64 ? ((OP == 2 || OP == 5 || OP == 6 || (Q == 27 && OP <= 1)) ? 2 : 3)
+            : ((OP <= 1 || OP == 4 || OP == 5) ? (Q == 19 ? 6 : 4) : 3);
+    static constexpr int aa_default = f64 ? 2 : ((OP == 2 || OP == 6 || (Q == 19 && (OP <= 1 || OP == 5))) ? 3 : 2);
 #ifdef LBM_MINB_OVERRIDE_PULL
     static constexpr int pull = LBM_MINB_OVERRIDE_PULL;
 #else

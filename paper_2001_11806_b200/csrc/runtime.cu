@@ -379,10 +379,10 @@ int run_graph_cycle(lbm_handle_s *h) {
 int validate(const lbm_config *c) {
     if (!c) return fail(nullptr, LBM_EINVAL, "null config");
     if (c->stencil != 19 && c->stencil != 27) return fail(nullptr, LBM_EINVAL, "stencil must be 19 or 27");
-    if (c->collision < 0 || c->collision > 4) return fail(nullptr, LBM_EINVAL, "bad collision");
+    if (c->collision < 0 || c->collision > 6) return fail(nullptr, LBM_EINVAL, "bad collision");
     if (c->dtype != LBM_F64 && c->dtype != LBM_F32) return fail(nullptr, LBM_EINVAL, "bad dtype");
     if (c->pattern != LBM_PULL && c->pattern != LBM_AA) return fail(nullptr, LBM_EINVAL, "bad pattern");
-    const int need[] = {1, 2, 1, 1, 0};
+    const int need[] = {1, 2, 1, 1, 0, 2, 1};
     if (c->n_rates < need[c->collision] || c->n_rates > 8) return fail(nullptr, LBM_EINVAL, "wrong number of rates");
     for (int i = 0; i < c->n_rates; ++i)
         if (!(c->rates[i] > 0.0 && c->rates[i] < 2.0)) return fail(nullptr, LBM_EINVAL, "relaxation rate outside (0, 2)");
@@ -406,7 +406,8 @@ int validate(const lbm_config *c) {
     const bool force = c->force[0] != 0 || c->force[1] != 0 || c->force[2] != 0;
     if (c->collision == LBM_MRT && c->stencil != 19) return fail(nullptr, LBM_EUNSUPPORTED, "MRT is implemented for D3Q19");
     if (c->collision == LBM_CUMULANT && c->stencil != 27) return fail(nullptr, LBM_EUNSUPPORTED, "cumulant is implemented for D3Q27");
-    if (force && (c->collision == LBM_MRT || c->collision == LBM_CUMULANT))
+    if (c->collision == LBM_KBC && c->stencil != 19) return fail(nullptr, LBM_EUNSUPPORTED, "KBC is implemented for D3Q19");
+    if (force && c->collision != LBM_SRT && c->collision != LBM_TRT)
         return fail(nullptr, LBM_EUNSUPPORTED, "forcing is implemented for SRT/TRT");
     // a non-periodic axis must carry wall cells on both faces
     for (int d = 0; d < 3; ++d) {
@@ -451,6 +452,31 @@ int64_t local_cells(const lbm_handle_s *h) {
 // =========================================================================================
 // C ABI
 // =========================================================================================
+namespace lbm {
+PullLaunch select_pull(int collision, int Q, int dtype, bool flags, bool force) {
+    switch (collision) {
+        case LBM_SRT:
+        case LBM_TRT: return select_pull_trt(Q, dtype, flags, force);
+        case LBM_MRT: return select_pull_mrt(Q, dtype, flags, force);
+        case LBM_CUMULANT: return select_pull_cumulant(Q, dtype, flags, force);
+        case LBM_SMAGORINSKY: return select_pull_smagorinsky(Q, dtype, flags, force);
+        case LBM_KBC: return select_pull_kbc(Q, dtype, flags, force);
+        default: return select_pull_identity(Q, dtype, flags, force);
+    }
+}
+AALaunch select_aa(int collision, int Q, int dtype, bool flags, bool force) {
+    switch (collision) {
+        case LBM_SRT:
+        case LBM_TRT: return select_aa_trt(Q, dtype, flags, force);
+        case LBM_MRT: return select_aa_mrt(Q, dtype, flags, force);
+        case LBM_CUMULANT: return select_aa_cumulant(Q, dtype, flags, force);
+        case LBM_SMAGORINSKY: return select_aa_smagorinsky(Q, dtype, flags, force);
+        case LBM_KBC: return select_aa_kbc(Q, dtype, flags, force);
+        default: return select_aa_identity(Q, dtype, flags, force);
+    }
+}
+}  // namespace lbm
+
 extern "C" {
 
 void lbm_config_default(lbm_config *c) {
@@ -484,8 +510,9 @@ const char *lbm_strerror(int s) {
 
 const char *lbm_last_error(lbm_handle h) { return h ? h->err.c_str() : g_create_error.c_str(); }
 
+
 static int kernel_args_common(const lbm_kernel_args *k, StepArgs &a, bool aa) {
-    if (!k || (k->stencil != 19 && k->stencil != 27) || k->collision < 0 || k->collision > 4 ||
+    if (!k || (k->stencil != 19 && k->stencil != 27) || k->collision < 0 || k->collision > 6 ||
         (k->dtype != LBM_F64 && k->dtype != LBM_F32) || !k->dst || (!aa && !k->src) || k->ghost < 0 || k->ghost > 1)
         return LBM_EINVAL;
     if (k->shape[0] < 1 || k->shape[1] < 1 || k->shape[2] < 1 || k->z_begin < 0 || k->z_end > k->shape[2] ||
@@ -531,14 +558,7 @@ int lbm_kernel_pull(const lbm_kernel_args *k) {
     if (rc) return rc;
     const bool flags = k->flags != nullptr;
     const bool force = k->force[0] != 0 || k->force[1] != 0 || k->force[2] != 0;
-    PullLaunch fn = nullptr;
-    switch (k->collision) {
-        case LBM_SRT:
-        case LBM_TRT: fn = select_pull_trt(k->stencil, k->dtype, flags, force); break;
-        case LBM_MRT: fn = select_pull_mrt(k->stencil, k->dtype, flags, force); break;
-        case LBM_CUMULANT: fn = select_pull_cumulant(k->stencil, k->dtype, flags, force); break;
-        default: fn = select_pull_identity(k->stencil, k->dtype, flags, force); break;
-    }
+    const PullLaunch fn = select_pull(k->collision, k->stencil, k->dtype, flags, force);
     if (!fn) return LBM_EUNSUPPORTED;
     if (k->z_end == k->z_begin) return LBM_OK;
     const dim3 b = kernel_block(k->shape[0], k->shape[1]);
@@ -554,14 +574,7 @@ int lbm_kernel_aa(const lbm_kernel_args *k, int32_t odd) {
     if (rc) return rc;
     const bool flags = k->flags != nullptr;
     const bool force = k->force[0] != 0 || k->force[1] != 0 || k->force[2] != 0;
-    AALaunch fn = nullptr;
-    switch (k->collision) {
-        case LBM_SRT:
-        case LBM_TRT: fn = select_aa_trt(k->stencil, k->dtype, flags, force); break;
-        case LBM_MRT: fn = select_aa_mrt(k->stencil, k->dtype, flags, force); break;
-        case LBM_CUMULANT: fn = select_aa_cumulant(k->stencil, k->dtype, flags, force); break;
-        default: fn = select_aa_identity(k->stencil, k->dtype, flags, force); break;
-    }
+    const AALaunch fn = select_aa(k->collision, k->stencil, k->dtype, flags, force);
     if (!fn) return LBM_EUNSUPPORTED;
     if (k->z_end == k->z_begin) return LBM_OK;
     const dim3 b = kernel_block(k->shape[0], k->shape[1]);
@@ -672,22 +685,10 @@ int lbm_create(const lbm_config *cfg, lbm_handle *out) {
     // kernel selection (SRT = TRT with equal rates)
     const bool force = h->have_force;
     if (cfg->pattern == LBM_PULL) {
-        switch (cfg->collision) {
-            case LBM_SRT:
-            case LBM_TRT: h->pull = select_pull_trt(h->Q, h->dtype, h->have_flags, force); break;
-            case LBM_MRT: h->pull = select_pull_mrt(h->Q, h->dtype, h->have_flags, force); break;
-            case LBM_CUMULANT: h->pull = select_pull_cumulant(h->Q, h->dtype, h->have_flags, force); break;
-            default: h->pull = select_pull_identity(h->Q, h->dtype, h->have_flags, force); break;
-        }
+        h->pull = select_pull(cfg->collision, h->Q, h->dtype, h->have_flags, force);
         if (!h->pull) return fail(nullptr, LBM_EUNSUPPORTED, "no kernel instantiated for this combination");
     } else {
-        switch (cfg->collision) {
-            case LBM_SRT:
-            case LBM_TRT: h->aa = select_aa_trt(h->Q, h->dtype, h->have_flags, force); break;
-            case LBM_MRT: h->aa = select_aa_mrt(h->Q, h->dtype, h->have_flags, force); break;
-            case LBM_CUMULANT: h->aa = select_aa_cumulant(h->Q, h->dtype, h->have_flags, force); break;
-            default: h->aa = select_aa_identity(h->Q, h->dtype, h->have_flags, force); break;
-        }
+        h->aa = select_aa(cfg->collision, h->Q, h->dtype, h->have_flags, force);
         if (!h->aa) return fail(nullptr, LBM_EUNSUPPORTED, "no kernel instantiated for this combination");
     }
     // rates into the kernel argument block

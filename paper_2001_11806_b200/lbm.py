@@ -21,14 +21,15 @@ LIBPATH = os.environ.get("LBM_B200_LIB") or os.path.join(HERE, "liblbm_b200.so")
 
 LBM_OK, LBM_EINVAL, LBM_EUNSUPPORTED, LBM_ECUDA, LBM_ENCCL, LBM_ENAN, LBM_EOOM = 0, -1, -2, -3, -4, -5, -6
 D3Q19, D3Q27 = 19, 27
-SRT, TRT, MRT, CUMULANT, IDENTITY = 0, 1, 2, 3, 4
+SRT, TRT, MRT, CUMULANT, IDENTITY, SMAGORINSKY, KBC = 0, 1, 2, 3, 4, 5, 6
 F64, F32 = 0, 1
 PULL, AA = 0, 1
 FLUID, NOSLIP, UBB = 0, 1, 2
 HOST, DEVICE = 0, 1
 HALO_ZEROCOPY, HALO_PACKED, HALO_FUSED = 0, 1, 2
 
-COLLISIONS = {"srt": SRT, "trt": TRT, "mrt": MRT, "cumulant": CUMULANT, "identity": IDENTITY}
+COLLISIONS = {"srt": SRT, "trt": TRT, "mrt": MRT, "cumulant": CUMULANT, "identity": IDENTITY,
+              "smagorinsky": SMAGORINSKY, "kbc": KBC}
 DTYPES = {"f64": F64, "float64": F64, "fp64": F64, "f32": F32, "float32": F32, "fp32": F32}
 PATTERNS = {"pull": PULL, "aa": AA}
 

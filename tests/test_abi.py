@@ -79,6 +79,8 @@ def test_slab_plan(L):
     (dict(stencil=27, collision="mrt", rates=(1.9,)), -2),      # MRT is D3Q19 only
     (dict(stencil=19, collision="cumulant", rates=(1.9,)), -2),  # cumulant is D3Q27 only
     (dict(collision="mrt", rates=(1.9,), force=(1e-5, 0, 0)), -2),
+    (dict(stencil=27, collision="kbc", rates=(1.9,)), -2),        # KBC is D3Q19 only
+    (dict(collision="smagorinsky", rates=(1.9,)), -1),             # needs [omega_0, C_S]
     (dict(n_local_slabs=3), -1),                                # nz % slabs != 0
     (dict(periodic=(1, 0, 1)), -1),                             # non-periodic axis without walls
     (dict(nccl_self=True, n_local_slabs=2), -1),                # self-exchange is single-slab

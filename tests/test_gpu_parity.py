@@ -153,6 +153,17 @@ PARITY = [
     Case("aa_mrt_f32_channel", (16, 20, 12), 19, "mrt", (1.9, 1.0, 1.0, 1.0), "f32", pattern="aa",
          geometry="channel", steps=24),
     Case("tiny_1x1x4", (1, 1, 4), 19, "srt", (1.5,), "f64", steps=7),
+    Case("smagorinsky_q19_f64_channel", (16, 20, 10), 19, "smagorinsky", (1.95, 0.17), "f64", geometry="channel",
+         u_amp=0.05, steps=30),
+    Case("smagorinsky_q27_f32_obst", (17, 13, 11), 27, "smagorinsky", (1.9, 0.12), "f32", geometry="obstacles",
+         ubb=(0.02, -0.01, 0.03), u_amp=0.05, steps=20),
+    Case("smagorinsky_aa_q19_f64", (18, 14, 10), 19, "smagorinsky", (1.95, 0.2), "f64", pattern="aa", u_amp=0.05,
+         steps=13),
+    Case("kbc_q19_f64_cavity", (14, 14, 14), 19, "kbc", (1.99,), "f64", geometry="cavity", ubb=(0.05, 0, 0),
+         steps=30),
+    Case("kbc_q19_f32", (16, 12, 10), 19, "kbc", (1.9,), "f32", u_amp=0.05, steps=20),
+    Case("kbc_aa_q19_f64_obst", (17, 13, 11), 19, "kbc", (1.95,), "f64", pattern="aa", geometry="obstacles",
+         ubb=(0.02, -0.01, 0.03), u_amp=0.05, steps=15),
 ]
 
 
