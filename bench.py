@@ -52,6 +52,18 @@ CONFIGS = {
                weak=False, Q=27, op="cumulant", rates=(1.95,), dtype="f64", pattern="pull", force=(0, 0, 0),
                geometry="cavity", init=("rest",), job_steps=1000, ubb=(0.05, 0, 0)),
 }
+CONFIGS["c3_aa"] = dict(CONFIGS["c3"], pattern="aa", desc="D3Q27 cumulant fp64 384^3 lid-driven cavity, AA pattern")
+CONFIGS["c3_periodic"] = dict(CONFIGS["c3"], geometry="periodic", init=("random", 1e-3, 0.01),
+                              desc="D3Q27 cumulant fp64 384^3 periodic pull (C3 without walls, diagnostic)")
+# Operator comparison in the spirit of Fig. 9: the same D3Q19 AA fp64 periodic
+# domain (512^3 instead of the paper's 300x100x100 so the B200 is HBM-bound) for each operator.
+for _name, _op, _q, _rates in [("trt", "trt", 19, (1.6, 0.5)), ("smagorinsky", "smagorinsky", 19, (1.95, 0.17)),
+                               ("mrt", "mrt", 19, (1.9, 1.0, 1.0, 1.0)), ("kbc", "kbc", 19, (1.95,)),
+                               ("cumulant27", "cumulant", 27, (1.95,))]:
+    CONFIGS[f"op_{_name}"] = dict(desc=f"D3Q{_q} {_op} fp64 AA 512^3 periodic (Fig. 9-style operator comparison)",
+                                  shape=(512, 512, 512), weak=False, Q=_q, op=_op, rates=_rates, dtype="f64",
+                                  pattern="aa", force=(0, 0, 0), geometry="periodic", init=("random", 1e-3, 0.01),
+                                  job_steps=200)
 
 
 def flags_for(cfg, shape):

@@ -8,25 +8,27 @@ namespace lbm {
 
 using PullLaunch = void (*)(const StepArgs &, const void *src, void *dst, dim3 grid, dim3 block, cudaStream_t);
 using AALaunch = void (*)(const StepArgs &, void *f, int odd, dim3 grid, dim3 block, cudaStream_t);
+// near-wall cell list launch (split wall mode): pull edge kernel, or the AA odd edge kernel (src unused)
+using EdgeLaunch = void (*)(const StepArgs &, const void *src, void *dst, const uint32_t *cells, uint32_t n, cudaStream_t);
 
-// Per-operator selection (nullptr = combination not instantiated). dtype: 0 = f64, 1 = f32.
-PullLaunch select_pull_trt(int Q, int dtype, bool flags, bool force);
-PullLaunch select_pull_mrt(int Q, int dtype, bool flags, bool force);
-PullLaunch select_pull_cumulant(int Q, int dtype, bool flags, bool force);
-PullLaunch select_pull_identity(int Q, int dtype, bool flags, bool force);
-PullLaunch select_pull_smagorinsky(int Q, int dtype, bool flags, bool force);
-PullLaunch select_pull_kbc(int Q, int dtype, bool flags, bool force);
-AALaunch select_aa_smagorinsky(int Q, int dtype, bool flags, bool force);
-AALaunch select_aa_kbc(int Q, int dtype, bool flags, bool force);
+// The kernels of one (operator, stencil, dtype, wall mode, force) combination; null members = not
+// instantiated. fm: FM_NONE, FM_INLINE or FM_BULK (kernels.cuh); the edge launchers go with FM_BULK.
+struct Kernels {
+    PullLaunch pull = nullptr;
+    AALaunch aa = nullptr;
+    EdgeLaunch pull_edges = nullptr;
+    EdgeLaunch aa_edges = nullptr;
+};
 
+Kernels select_trt(int Q, int dtype, int fm, bool force);
+Kernels select_mrt(int Q, int dtype, int fm, bool force);
+Kernels select_cumulant(int Q, int dtype, int fm, bool force);
+Kernels select_identity(int Q, int dtype, int fm, bool force);
+Kernels select_smagorinsky(int Q, int dtype, int fm, bool force);
+Kernels select_kbc(int Q, int dtype, int fm, bool force);
 // Operator dispatch used by the handle API and the low-level kernel ABI (runtime.cu); SRT runs the
-// TRT kernel with equal rates. nullptr = combination not instantiated.
-PullLaunch select_pull(int collision, int Q, int dtype, bool flags, bool force);
-AALaunch select_aa(int collision, int Q, int dtype, bool flags, bool force);
-AALaunch select_aa_trt(int Q, int dtype, bool flags, bool force);
-AALaunch select_aa_mrt(int Q, int dtype, bool flags, bool force);
-AALaunch select_aa_cumulant(int Q, int dtype, bool flags, bool force);
-AALaunch select_aa_identity(int Q, int dtype, bool flags, bool force);
+// TRT kernel with equal rates.
+Kernels select_kernels(int collision, int Q, int dtype, int fm, bool force);
 
 // Auxiliary kernels (k_misc.cu), dispatched on (Q, dtype).
 void launch_init(int Q, int dtype, const InitArgs &a, void *f0, void *f1, dim3 grid, dim3 block, cudaStream_t s);

@@ -3,12 +3,5 @@
 
 namespace lbm {
 
-PullLaunch select_pull_cumulant(int Q, int dtype, bool flags, bool force) {
-    return select_pull_op<OP_CUMULANT, false, false, true>(Q, dtype, flags, force);
-}
-
-AALaunch select_aa_cumulant(int Q, int dtype, bool flags, bool force) {
-    return select_aa_op<OP_CUMULANT, false, false, true>(Q, dtype, flags, force);
-}
-
+Kernels select_cumulant(int Q, int dtype, int fm, bool force) { return select_op<OP_CUMULANT, false, false, true>(Q, dtype, fm, force); }
 }  // namespace lbm

@@ -4,14 +4,8 @@
 
 namespace lbm {
 
-PullLaunch select_pull_identity(int Q, int dtype, bool flags, bool force) {
+Kernels select_identity(int Q, int dtype, int fm, bool force) {
     (void)force;
-    return select_pull_op<OP_IDENTITY, false, true, true>(Q, dtype, flags, false);
+    return select_op<OP_IDENTITY, false, true, true>(Q, dtype, fm, false);
 }
-
-AALaunch select_aa_identity(int Q, int dtype, bool flags, bool force) {
-    (void)force;
-    return select_aa_op<OP_IDENTITY, false, true, true>(Q, dtype, flags, false);
-}
-
 }  // namespace lbm

@@ -4,17 +4,8 @@
 
 namespace lbm {
 
-PullLaunch select_pull_smagorinsky(int Q, int dtype, bool flags, bool force) {
-    return select_pull_op<OP_SMAGORINSKY, false, true, true>(Q, dtype, flags, force);
+Kernels select_smagorinsky(int Q, int dtype, int fm, bool force) {
+    return select_op<OP_SMAGORINSKY, false, true, true>(Q, dtype, fm, force);
 }
-AALaunch select_aa_smagorinsky(int Q, int dtype, bool flags, bool force) {
-    return select_aa_op<OP_SMAGORINSKY, false, true, true>(Q, dtype, flags, force);
-}
-PullLaunch select_pull_kbc(int Q, int dtype, bool flags, bool force) {
-    return select_pull_op<OP_KBC, false, true, false>(Q, dtype, flags, force);
-}
-AALaunch select_aa_kbc(int Q, int dtype, bool flags, bool force) {
-    return select_aa_op<OP_KBC, false, true, false>(Q, dtype, flags, force);
-}
-
+Kernels select_kbc(int Q, int dtype, int fm, bool force) { return select_op<OP_KBC, false, true, false>(Q, dtype, fm, force); }
 }  // namespace lbm

@@ -3,12 +3,5 @@
 
 namespace lbm {
 
-PullLaunch select_pull_mrt(int Q, int dtype, bool flags, bool force) {
-    return select_pull_op<OP_MRT, false, true, false>(Q, dtype, flags, force);
-}
-
-AALaunch select_aa_mrt(int Q, int dtype, bool flags, bool force) {
-    return select_aa_op<OP_MRT, false, true, false>(Q, dtype, flags, force);
-}
-
+Kernels select_mrt(int Q, int dtype, int fm, bool force) { return select_op<OP_MRT, false, true, false>(Q, dtype, fm, force); }
 }  // namespace lbm

@@ -4,57 +4,89 @@
 
 namespace lbm {
 
-template <int Q, int OP, typename T, bool FLAGS, bool FORCE>
+template <int Q, int OP, typename T, int FM, bool FORCE>
 void pull_launcher(const StepArgs &a, const void *src, void *dst, dim3 grid, dim3 block, cudaStream_t s) {
-    k_pull<Q, OP, T, FLAGS, FORCE><<<grid, block, 0, s>>>(a, static_cast<const T *>(src), static_cast<T *>(dst));
+    // peer stores (fused halo, boundary-plane launches only) are a separate instantiation so the
+    // interior kernel carries no extra live registers
+    if (a.peer_up != nullptr)
+        k_pull<Q, OP, T, FM, FORCE, true><<<grid, block, 0, s>>>(a, static_cast<const T *>(src), static_cast<T *>(dst));
+    else
+        k_pull<Q, OP, T, FM, FORCE, false><<<grid, block, 0, s>>>(a, static_cast<const T *>(src), static_cast<T *>(dst));
 }
 
-template <int Q, int OP, typename T, bool FLAGS, bool FORCE>
+template <int Q, int OP, typename T, bool FORCE>
+void pull_edge_launcher(const StepArgs &a, const void *src, void *dst, const uint32_t *cells, uint32_t n, cudaStream_t s) {
+    if (n == 0) return;
+    const unsigned blocks = (n + 127) / 128;
+    if (a.peer_up != nullptr)
+        k_pull_edges<Q, OP, T, FORCE, true><<<blocks, 128, 0, s>>>(a, static_cast<const T *>(src), static_cast<T *>(dst), cells, n);
+    else
+        k_pull_edges<Q, OP, T, FORCE, false><<<blocks, 128, 0, s>>>(a, static_cast<const T *>(src), static_cast<T *>(dst), cells, n);
+}
+
+template <int Q, int OP, typename T, int FM, bool FORCE>
 void aa_launcher(const StepArgs &a, void *f, int odd, dim3 grid, dim3 block, cudaStream_t s) {
     if (odd)
-        k_aa_odd<Q, OP, T, FLAGS, FORCE><<<grid, block, 0, s>>>(a, static_cast<T *>(f));
-    else
-        k_aa_even<Q, OP, T, FLAGS, FORCE><<<grid, block, 0, s>>>(a, static_cast<T *>(f));
+        k_aa_odd<Q, OP, T, FM, FORCE><<<grid, block, 0, s>>>(a, static_cast<T *>(f));
+    else  // the even step is in place: walls are skipped, near-wall cells need nothing special
+        k_aa_even<Q, OP, T, (FM != FM_NONE), FORCE><<<grid, block, 0, s>>>(a, static_cast<T *>(f));
+}
+
+template <int Q, int OP, typename T, bool FORCE>
+void aa_edge_launcher(const StepArgs &a, const void *src, void *f, const uint32_t *cells, uint32_t n, cudaStream_t s) {
+    (void)src;
+    if (n == 0) return;
+    k_aa_odd_edges<Q, OP, T, FORCE><<<(n + 127) / 128, 128, 0, s>>>(a, static_cast<T *>(f), cells, n);
+}
+
+template <int Q, int OP, typename T, bool FORCE>
+PullLaunch pick_pull_fm(int fm) {
+    switch (fm) {
+        case FM_INLINE: return &pull_launcher<Q, OP, T, FM_INLINE, FORCE>;
+        case FM_BULK: return &pull_launcher<Q, OP, T, FM_BULK, FORCE>;
+        default: return &pull_launcher<Q, OP, T, FM_NONE, FORCE>;
+    }
+}
+
+template <int Q, int OP, typename T, bool FORCE>
+AALaunch pick_aa_fm(int fm) {
+    switch (fm) {
+        case FM_INLINE: return &aa_launcher<Q, OP, T, FM_INLINE, FORCE>;
+        case FM_BULK: return &aa_launcher<Q, OP, T, FM_BULK, FORCE>;
+        default: return &aa_launcher<Q, OP, T, FM_NONE, FORCE>;
+    }
 }
 
 // FORCE variants are instantiated only for operators with a forcing term (SRT/TRT).
 template <int Q, int OP, typename T, bool WITH_FORCE>
-PullLaunch pick_pull(bool flags, bool force) {
+Kernels pick(int fm, bool force) {
+    Kernels k;
     if constexpr (WITH_FORCE) {
-        if (force) return flags ? &pull_launcher<Q, OP, T, true, true> : &pull_launcher<Q, OP, T, false, true>;
+        if (force) {
+            k.pull = pick_pull_fm<Q, OP, T, true>(fm);
+            k.aa = pick_aa_fm<Q, OP, T, true>(fm);
+            k.pull_edges = &pull_edge_launcher<Q, OP, T, true>;
+            k.aa_edges = &aa_edge_launcher<Q, OP, T, true>;
+            return k;
+        }
     } else {
-        if (force) return nullptr;
+        if (force) return k;  // not instantiated
     }
-    return flags ? &pull_launcher<Q, OP, T, true, false> : &pull_launcher<Q, OP, T, false, false>;
+    k.pull = pick_pull_fm<Q, OP, T, false>(fm);
+    k.aa = pick_aa_fm<Q, OP, T, false>(fm);
+    k.pull_edges = &pull_edge_launcher<Q, OP, T, false>;
+    k.aa_edges = &aa_edge_launcher<Q, OP, T, false>;
+    return k;
 }
 
-template <int Q, int OP, typename T, bool WITH_FORCE>
-AALaunch pick_aa(bool flags, bool force) {
-    if constexpr (WITH_FORCE) {
-        if (force) return flags ? &aa_launcher<Q, OP, T, true, true> : &aa_launcher<Q, OP, T, false, true>;
-    } else {
-        if (force) return nullptr;
-    }
-    return flags ? &aa_launcher<Q, OP, T, true, false> : &aa_launcher<Q, OP, T, false, false>;
-}
-
-// (Q, dtype) dispatch of one operator; Qs lists the stencils it is instantiated for
+// (Q, dtype) dispatch of one operator over the stencils it is instantiated for
 template <int OP, bool WITH_FORCE, bool Q19, bool Q27>
-PullLaunch select_pull_op(int Q, int dtype, bool flags, bool force) {
+Kernels select_op(int Q, int dtype, int fm, bool force) {
     if constexpr (Q19)
-        if (Q == 19) return dtype == 0 ? pick_pull<19, OP, double, WITH_FORCE>(flags, force) : pick_pull<19, OP, float, WITH_FORCE>(flags, force);
+        if (Q == 19) return dtype == 0 ? pick<19, OP, double, WITH_FORCE>(fm, force) : pick<19, OP, float, WITH_FORCE>(fm, force);
     if constexpr (Q27)
-        if (Q == 27) return dtype == 0 ? pick_pull<27, OP, double, WITH_FORCE>(flags, force) : pick_pull<27, OP, float, WITH_FORCE>(flags, force);
-    return nullptr;
-}
-
-template <int OP, bool WITH_FORCE, bool Q19, bool Q27>
-AALaunch select_aa_op(int Q, int dtype, bool flags, bool force) {
-    if constexpr (Q19)
-        if (Q == 19) return dtype == 0 ? pick_aa<19, OP, double, WITH_FORCE>(flags, force) : pick_aa<19, OP, float, WITH_FORCE>(flags, force);
-    if constexpr (Q27)
-        if (Q == 27) return dtype == 0 ? pick_aa<27, OP, double, WITH_FORCE>(flags, force) : pick_aa<27, OP, float, WITH_FORCE>(flags, force);
-    return nullptr;
+        if (Q == 27) return dtype == 0 ? pick<27, OP, double, WITH_FORCE>(fm, force) : pick<27, OP, float, WITH_FORCE>(fm, force);
+    return Kernels{};
 }
 
 }  // namespace lbm

@@ -106,35 +106,72 @@ __device__ __forceinline__ uint32_t nb_off(const Geo &g, const Nbr &n, int dx, i
 }
 
 // =======================================================================================
-// Fused stream-pull-collide, two arrays. dst = C(S(src)) on fluid cells of planes
-// z = z_begin + blockIdx.z * z_step. Wall cells are not written.
+// Wall handling modes of the update kernels (flags = storage-indexed flag bytes):
+//   FM_NONE   no flag field (periodic / walls absent);
+//   FM_INLINE every cell reads its flag, wall cells return, near-wall cells (bit 7) resolve the
+//             directions that come from a wall in the same kernel (low-level ABI);
+//   FM_BULK   the bulk kernel of the split: cells with any flag bit (walls and near-wall cells)
+//             return after one 1-byte read, so the kernel runs the periodic fast path;
+//   FM_EDGE   the boundary kernel of the split: processes only the near-wall fluid cells given by
+//             an index list (the GPU form of the paper's separate boundary kernels).
 // =======================================================================================
-template <int Q, int OP, typename T, bool FLAGS, bool FORCE>
-__global__ void __launch_bounds__(256, (MinBlocks<Q, OP, T>::pull)) k_pull(const StepArgs a, const T *__restrict__ src, T *__restrict__ dst) {
+enum FMode { FM_NONE = 0, FM_INLINE = 1, FM_BULK = 2, FM_EDGE = 3 };
+
+// =======================================================================================
+// Fused stream-pull-collide, two arrays: dst = C(S(src)) at one fluid cell.
+// =======================================================================================
+template <int Q, int OP, typename T, int FM, bool FORCE, bool PEER>
+__device__ __forceinline__ void pull_cell(const StepArgs &a, const T *__restrict__ src, T *__restrict__ dst, int x, int y,
+                                          int zs) {
     using S = Stencil<Q>;
-    const int x = blockIdx.x * blockDim.x + threadIdx.x;
-    const int y = blockIdx.y * blockDim.y + threadIdx.y;
-    if (x >= a.geo.nx || y >= a.geo.ny) return;
-    const int zs = a.z_begin + (int)blockIdx.z * a.z_step + a.geo.g;
     const Nbr n = neighbours(a.geo, x, y, zs);
     const uint32_t self = nb_off(a.geo, n, 0, 0, 0);
     const int64_t Sq = a.geo.Sq;
-    bool edge = false;
-    if (FLAGS) {
+    bool edge = FM == FM_EDGE;
+    if (FM == FM_INLINE) {
         const uint8_t own = a.flags[self];
         if (own & 3) return;  // wall cells are not updated
         edge = (own & 0x80) != 0;
+    } else if (FM == FM_BULK) {
+        if (a.flags[self] != 0) return;  // walls, and near-wall cells (done by the edge kernel)
     }
+    // Two strategies for near-wall cells in the inline mode, chosen per kernel family from B200
+    // measurements: gather-then-fix-up (fp64 and the cumulant: all Q loads
+    // issue back to back — the neighbour's storage always exists, wall or not — and the wall
+    // directions are replaced afterwards) and branch-per-direction (fp32 TRT at 40 registers).
+    constexpr bool kWalls = FM == FM_INLINE || FM == FM_EDGE;
+    constexpr bool kFixup = kWalls && (sizeof(T) == 8 || OP == OP_CUMULANT) && FM == FM_INLINE;
     T g[Q];
+    if constexpr (kWalls && !kFixup) {
 #pragma unroll
-    for (int q = 0; q < Q; ++q) {
-        // pull from x - c_q
-        const uint32_t o = nb_off(a.geo, n, -S::cx(q), -S::cy(q), -S::cz(q));
-        if (FLAGS && edge) {
-            const uint8_t fl = a.flags[o] & 3;
-            if (fl == 0) {
-                g[q] = ldg_stream(src + q * Sq + o);
+        for (int q = 0; q < Q; ++q) {
+            const uint32_t o = nb_off(a.geo, n, -S::cx(q), -S::cy(q), -S::cz(q));
+            if (edge) {
+                const uint8_t fl = a.flags[o] & 3;
+                if (fl == 0) {
+                    g[q] = ldg_stream(src + q * Sq + o);
+                } else {
+                    T v = ldg_stream(src + S::opp(q) * Sq + self);
+                    if (fl == 2) {
+                        const double cu = S::cx(q) * a.uw[0] + S::cy(q) * a.uw[1] + S::cz(q) * a.uw[2];
+                        v += T(6.0 * S::w(q) * cu);
+                    }
+                    g[q] = v;
+                }
             } else {
+                g[q] = ldg_stream(src + q * Sq + o);
+            }
+        }
+    } else {
+#pragma unroll
+        for (int q = 0; q < Q; ++q)
+            g[q] = ldg_stream(src + q * Sq + nb_off(a.geo, n, -S::cx(q), -S::cy(q), -S::cz(q)));
+    }
+    if (kFixup && edge) {
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+            const uint8_t fl = a.flags[nb_off(a.geo, n, -S::cx(q), -S::cy(q), -S::cz(q))] & 3;
+            if (fl != 0) {
                 T v = ldg_stream(src + S::opp(q) * Sq + self);
                 if (fl == 2) {
                     const double cu = S::cx(q) * a.uw[0] + S::cy(q) * a.uw[1] + S::cz(q) * a.uw[2];
@@ -142,15 +179,13 @@ __global__ void __launch_bounds__(256, (MinBlocks<Q, OP, T>::pull)) k_pull(const
                 }
                 g[q] = v;
             }
-        } else {
-            g[q] = ldg_stream(src + q * Sq + o);
         }
     }
     const Rates<T> r = load_rates<T>(a);
     collide<Q, OP, T, FORCE>(g, r);
 #pragma unroll
     for (int q = 0; q < Q; ++q) dst[q * Sq + self] = g[q];
-    if (a.peer_up != nullptr) {
+    if (PEER) {
         // fused halo: the crossing populations of the boundary planes also go straight into the
         // neighbours' ghost planes (top plane, c_z = +1 -> up's plane 0; bottom, c_z = -1 -> down's nz+1)
         const uint32_t inplane = (uint32_t)y * (uint32_t)a.geo.nx + (uint32_t)x;
@@ -168,6 +203,29 @@ __global__ void __launch_bounds__(256, (MinBlocks<Q, OP, T>::pull)) k_pull(const
                 if (S::cz(q) == -1) dn[q * Sq + (a.geo.nz + 1) * plane + inplane] = g[q];
         }
     }
+}
+
+// One thread per cell along x; planes z = z_begin + blockIdx.z * z_step (interior indices).
+template <int Q, int OP, typename T, int FM, bool FORCE, bool PEER = false>
+__global__ void __launch_bounds__(256, (MinBlocks<Q, OP, T>::pull)) k_pull(const StepArgs a, const T *__restrict__ src, T *__restrict__ dst) {
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    const int y = blockIdx.y * blockDim.y + threadIdx.y;
+    if (x >= a.geo.nx || y >= a.geo.ny) return;
+    const int zs = a.z_begin + (int)blockIdx.z * a.z_step + a.geo.g;
+    pull_cell<Q, OP, T, FM, FORCE, PEER>(a, src, dst, x, y, zs);
+}
+
+// Near-wall fluid cells from a list of storage cell indices (one thread per listed cell).
+template <int Q, int OP, typename T, bool FORCE, bool PEER = false>
+__global__ void __launch_bounds__(128) k_pull_edges(const StepArgs a, const T *__restrict__ src, T *__restrict__ dst,
+                                                   const uint32_t *__restrict__ cells, uint32_t n) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint32_t c = cells[i];
+    const uint32_t plane = (uint32_t)a.geo.nx * (uint32_t)a.geo.ny;
+    const int zs = (int)(c / plane);
+    const uint32_t r = c - (uint32_t)zs * plane;
+    pull_cell<Q, OP, T, FM_EDGE, FORCE, PEER>(a, src, dst, (int)(r % (uint32_t)a.geo.nx), (int)(r / (uint32_t)a.geo.nx), zs);
 }
 
 // =======================================================================================
@@ -202,62 +260,81 @@ __global__ void __launch_bounds__(256, (MinBlocks<Q, OP, T>::aa)) k_aa_even(cons
     for (int q = 0; q < Q; ++q) f[S::opp(q) * Sq + self] = g[q];
 }
 
-// Walls in the odd step (the pull rules of a3 expressed in AA slots, P:870-872): a population that
-// would come from a wall cell x - c_q is the cell's own bounced C_qbar(x), which the even step left
-// in a[x](q) (+ UBB term of q); a population leaving toward a wall x + c_q returns next step as qbar
-// and is stored directly in a[x](qbar) (+ UBB term of qbar). Only near-wall cells check flags.
-template <int Q, int OP, typename T, bool FLAGS, bool FORCE>
-__global__ void __launch_bounds__(256, (MinBlocks<Q, OP, T>::aa)) k_aa_odd(const StepArgs a, T *__restrict__ f) {
+template <int Q, int OP, typename T, int FM, bool FORCE>
+__device__ __forceinline__ void aa_odd_cell(const StepArgs &a, T *__restrict__ f, int x, int y, int zs) {
     using S = Stencil<Q>;
-    const int x = blockIdx.x * blockDim.x + threadIdx.x;
-    const int y = blockIdx.y * blockDim.y + threadIdx.y;
-    if (x >= a.geo.nx || y >= a.geo.ny) return;
-    const int zs = a.z_begin + (int)blockIdx.z * a.z_step + a.geo.g;
     const Nbr n = neighbours(a.geo, x, y, zs);
     const int64_t Sq = a.geo.Sq;
-    bool edge = false;
-    uint32_t self = 0;
-    if (FLAGS) {
-        self = nb_off(a.geo, n, 0, 0, 0);
+    bool edge = FM == FM_EDGE;
+    const uint32_t self = nb_off(a.geo, n, 0, 0, 0);
+    if (FM == FM_INLINE) {
         const uint8_t own = a.flags[self];
         if (own & 3) return;
         edge = (own & 0x80) != 0;
+    } else if (FM == FM_BULK) {
+        if (a.flags[self] != 0) return;
     }
+    // unconditional gather (loads issue back to back), wall directions fixed up in near-wall cells
     T g[Q];
 #pragma unroll
-    for (int q = 0; q < Q; ++q) {
-        const uint32_t o = nb_off(a.geo, n, -S::cx(q), -S::cy(q), -S::cz(q));
-        if (FLAGS && edge) {
-            const uint8_t fl = a.flags[o] & 3;
-            if (fl == 0) {
-                g[q] = f[S::opp(q) * Sq + o];
-            } else {
+    for (int q = 0; q < Q; ++q) g[q] = f[S::opp(q) * Sq + nb_off(a.geo, n, -S::cx(q), -S::cy(q), -S::cz(q))];
+    uint32_t wallmask = 0;  // bit q: x - c_q is a wall (x + c_q for the opposite direction)
+    if (edge) {
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+            const uint8_t fl = a.flags[nb_off(a.geo, n, -S::cx(q), -S::cy(q), -S::cz(q))] & 3;
+            if (fl != 0) {
+                wallmask |= 1u << q;
                 T v = f[q * Sq + self];
                 if (fl == 2) v += ubb_term<Q, T>(a, q);
                 g[q] = v;
             }
-        } else {
-            g[q] = f[S::opp(q) * Sq + o];
         }
     }
     const Rates<T> r = load_rates<T>(a);
     collide<Q, OP, T, FORCE>(g, r);
+    if (!edge) {
 #pragma unroll
-    for (int q = 0; q < Q; ++q) {
-        const uint32_t o = nb_off(a.geo, n, S::cx(q), S::cy(q), S::cz(q));
-        if (FLAGS && edge) {
-            const uint8_t fl = a.flags[o] & 3;
-            if (fl == 0) {
-                f[q * Sq + o] = g[q];
-            } else {
+        for (int q = 0; q < Q; ++q) f[q * Sq + nb_off(a.geo, n, S::cx(q), S::cy(q), S::cz(q))] = g[q];
+    } else {
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+            const uint32_t o = nb_off(a.geo, n, S::cx(q), S::cy(q), S::cz(q));
+            if (wallmask & (1u << S::opp(q))) {  // x + c_q is a wall: returns next step as qbar
+                const uint8_t fl = a.flags[o] & 3;
                 T v = g[q];
                 if (fl == 2) v += ubb_term<Q, T>(a, S::opp(q));
                 f[S::opp(q) * Sq + self] = v;
+            } else {
+                f[q * Sq + o] = g[q];
             }
-        } else {
-            f[q * Sq + o] = g[q];
         }
     }
+}
+
+// Walls in the odd step (the pull rules of a3 expressed in AA slots, P:870-872): a population that
+// would come from a wall cell x - c_q is the cell's own bounced C_qbar(x), which the even step left
+// in a[x](q) (+ UBB term of q); a population leaving toward a wall x + c_q returns next step as qbar
+// and is stored directly in a[x](qbar) (+ UBB term of qbar).
+template <int Q, int OP, typename T, int FM, bool FORCE>
+__global__ void __launch_bounds__(256, (MinBlocks<Q, OP, T>::aa)) k_aa_odd(const StepArgs a, T *__restrict__ f) {
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    const int y = blockIdx.y * blockDim.y + threadIdx.y;
+    if (x >= a.geo.nx || y >= a.geo.ny) return;
+    const int zs = a.z_begin + (int)blockIdx.z * a.z_step + a.geo.g;
+    aa_odd_cell<Q, OP, T, FM, FORCE>(a, f, x, y, zs);
+}
+
+template <int Q, int OP, typename T, bool FORCE>
+__global__ void __launch_bounds__(128) k_aa_odd_edges(const StepArgs a, T *__restrict__ f, const uint32_t *__restrict__ cells,
+                                                     uint32_t n) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint32_t c = cells[i];
+    const uint32_t plane = (uint32_t)a.geo.nx * (uint32_t)a.geo.ny;
+    const int zs = (int)(c / plane);
+    const uint32_t r = c - (uint32_t)zs * plane;
+    aa_odd_cell<Q, OP, T, FM_EDGE, FORCE>(a, f, (int)(r % (uint32_t)a.geo.nx), (int)(r / (uint32_t)a.geo.nx), zs);
 }
 
 // =======================================================================================

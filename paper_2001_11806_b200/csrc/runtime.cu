@@ -26,6 +26,8 @@ struct Slab {
     int nz = 0;           // interior planes
     void *pdf[2] = {nullptr, nullptr};
     uint8_t *flags = nullptr;    // storage-indexed, with ghost planes
+    uint32_t *edges = nullptr;   // storage indices of near-wall fluid cells (split wall mode)
+    std::vector<int64_t> edge_off;  // edges of storage plane zs: [edge_off[zs], edge_off[zs+1])
     void *halo[4] = {nullptr, nullptr, nullptr, nullptr};  // packed mode: send up, send down, recv below, recv above
     int cur = 0;          // index of the array holding the current state (pull)
 };
@@ -50,8 +52,7 @@ struct lbm_handle_s {
     int rank = 0, nranks = 1, up = 0, down = 0;
     bool use_nccl = false;  // nranks > 1, or the 1-rank self-exchange variant
     bool have_flags = false, have_force = false;
-    PullLaunch pull = nullptr;
-    AALaunch aa = nullptr;
+    Kernels kern;  // kernels of the configured operator and wall mode
     StepArgs base{};
     int64_t steps = 0;
     int aa_parity = 0;
@@ -131,6 +132,24 @@ void tbegin(lbm_handle_s *h, cudaStream_t s) {
 }
 void tend(lbm_handle_s *h, cudaStream_t s) { tbegin(h, s); }
 
+// Split wall mode: the near-wall cells of the planes a bulk launch covered (interior indices
+// z_begin + k * z_step, k < nplanes), one edge-list launch per contiguous run of planes.
+void launch_edges(lbm_handle_s *h, Slab &s, const StepArgs &a, EdgeLaunch fn, const void *src, void *dst, int z_begin,
+                  int nplanes, int z_step, cudaStream_t st) {
+    if (!s.edges || !fn) return;
+    auto run = [&](int zlo, int zhi) {  // interior planes [zlo, zhi)
+        const int64_t b = s.edge_off[zlo + h->g], e = s.edge_off[zhi + h->g];
+        if (e <= b) return;
+        tbegin(h, st);
+        fn(a, src, dst, s.edges + b, (uint32_t)(e - b), st);
+        tend(h, st);
+        h->launches++;
+    };
+    if (z_step == 1) run(z_begin, z_begin + nplanes);
+    else
+        for (int k = 0; k < nplanes; ++k) run(z_begin + k * z_step, z_begin + k * z_step + 1);
+}
+
 void launch_pull_range(lbm_handle_s *h, Slab &s, int z_begin, int nplanes, int z_step, cudaStream_t st,
                        bool peer_stores = false) {
     if (nplanes <= 0) return;
@@ -144,9 +163,10 @@ void launch_pull_range(lbm_handle_s *h, Slab &s, int z_begin, int nplanes, int z
         a.peer_down = h->fst.bases[2 * (1 - s.cur) + 1];
     }
     tbegin(h, st);
-    h->pull(a, s.pdf[s.cur], s.pdf[1 - s.cur], grid_for(h, nplanes), h->block, st);
+    h->kern.pull(a, s.pdf[s.cur], s.pdf[1 - s.cur], grid_for(h, nplanes), h->block, st);
     tend(h, st);
     h->launches++;
+    launch_edges(h, s, a, h->kern.pull_edges, s.pdf[s.cur], s.pdf[1 - s.cur], z_begin, nplanes, z_step, st);
 }
 
 void launch_aa_range(lbm_handle_s *h, Slab &s, int odd, int z_begin, int nplanes, int z_step, cudaStream_t st) {
@@ -157,9 +177,10 @@ void launch_aa_range(lbm_handle_s *h, Slab &s, int odd, int z_begin, int nplanes
     a.z_step = z_step;
     a.flags = s.flags;
     tbegin(h, st);
-    h->aa(a, s.pdf[0], odd, grid_for(h, nplanes), h->block, st);
+    h->kern.aa(a, s.pdf[0], odd, grid_for(h, nplanes), h->block, st);
     tend(h, st);
     h->launches++;
+    if (odd) launch_edges(h, s, a, h->kern.aa_edges, nullptr, s.pdf[0], z_begin, nplanes, z_step, st);
 }
 
 // Halo exchange phases. Each phase moves, per slab, one set of crossing slots through face A
@@ -453,26 +474,15 @@ int64_t local_cells(const lbm_handle_s *h) {
 // C ABI
 // =========================================================================================
 namespace lbm {
-PullLaunch select_pull(int collision, int Q, int dtype, bool flags, bool force) {
+Kernels select_kernels(int collision, int Q, int dtype, int fm, bool force) {
     switch (collision) {
         case LBM_SRT:
-        case LBM_TRT: return select_pull_trt(Q, dtype, flags, force);
-        case LBM_MRT: return select_pull_mrt(Q, dtype, flags, force);
-        case LBM_CUMULANT: return select_pull_cumulant(Q, dtype, flags, force);
-        case LBM_SMAGORINSKY: return select_pull_smagorinsky(Q, dtype, flags, force);
-        case LBM_KBC: return select_pull_kbc(Q, dtype, flags, force);
-        default: return select_pull_identity(Q, dtype, flags, force);
-    }
-}
-AALaunch select_aa(int collision, int Q, int dtype, bool flags, bool force) {
-    switch (collision) {
-        case LBM_SRT:
-        case LBM_TRT: return select_aa_trt(Q, dtype, flags, force);
-        case LBM_MRT: return select_aa_mrt(Q, dtype, flags, force);
-        case LBM_CUMULANT: return select_aa_cumulant(Q, dtype, flags, force);
-        case LBM_SMAGORINSKY: return select_aa_smagorinsky(Q, dtype, flags, force);
-        case LBM_KBC: return select_aa_kbc(Q, dtype, flags, force);
-        default: return select_aa_identity(Q, dtype, flags, force);
+        case LBM_TRT: return select_trt(Q, dtype, fm, force);
+        case LBM_MRT: return select_mrt(Q, dtype, fm, force);
+        case LBM_CUMULANT: return select_cumulant(Q, dtype, fm, force);
+        case LBM_SMAGORINSKY: return select_smagorinsky(Q, dtype, fm, force);
+        case LBM_KBC: return select_kbc(Q, dtype, fm, force);
+        default: return select_identity(Q, dtype, fm, force);
     }
 }
 }  // namespace lbm
@@ -558,7 +568,7 @@ int lbm_kernel_pull(const lbm_kernel_args *k) {
     if (rc) return rc;
     const bool flags = k->flags != nullptr;
     const bool force = k->force[0] != 0 || k->force[1] != 0 || k->force[2] != 0;
-    const PullLaunch fn = select_pull(k->collision, k->stencil, k->dtype, flags, force);
+    const PullLaunch fn = select_kernels(k->collision, k->stencil, k->dtype, flags ? FM_INLINE : FM_NONE, force).pull;
     if (!fn) return LBM_EUNSUPPORTED;
     if (k->z_end == k->z_begin) return LBM_OK;
     const dim3 b = kernel_block(k->shape[0], k->shape[1]);
@@ -574,7 +584,7 @@ int lbm_kernel_aa(const lbm_kernel_args *k, int32_t odd) {
     if (rc) return rc;
     const bool flags = k->flags != nullptr;
     const bool force = k->force[0] != 0 || k->force[1] != 0 || k->force[2] != 0;
-    const AALaunch fn = select_aa(k->collision, k->stencil, k->dtype, flags, force);
+    const AALaunch fn = select_kernels(k->collision, k->stencil, k->dtype, flags ? FM_INLINE : FM_NONE, force).aa;
     if (!fn) return LBM_EUNSUPPORTED;
     if (k->z_end == k->z_begin) return LBM_OK;
     const dim3 b = kernel_block(k->shape[0], k->shape[1]);
@@ -685,11 +695,11 @@ int lbm_create(const lbm_config *cfg, lbm_handle *out) {
     // kernel selection (SRT = TRT with equal rates)
     const bool force = h->have_force;
     if (cfg->pattern == LBM_PULL) {
-        h->pull = select_pull(cfg->collision, h->Q, h->dtype, h->have_flags, force);
-        if (!h->pull) return fail(nullptr, LBM_EUNSUPPORTED, "no kernel instantiated for this combination");
+        h->kern = select_kernels(cfg->collision, h->Q, h->dtype, h->have_flags ? FM_BULK : FM_NONE, force);
+        if (!h->kern.pull) return fail(nullptr, LBM_EUNSUPPORTED, "no kernel instantiated for this combination");
     } else {
-        h->aa = select_aa(cfg->collision, h->Q, h->dtype, h->have_flags, force);
-        if (!h->aa) return fail(nullptr, LBM_EUNSUPPORTED, "no kernel instantiated for this combination");
+        h->kern = select_kernels(cfg->collision, h->Q, h->dtype, h->have_flags ? FM_BULK : FM_NONE, force);
+        if (!h->kern.aa) return fail(nullptr, LBM_EUNSUPPORTED, "no kernel instantiated for this combination");
     }
     // rates into the kernel argument block
     StepArgs &b = h->base;
@@ -782,6 +792,25 @@ int lbm_create(const lbm_config *cfg, lbm_handle *out) {
             launch_mark_near_wall(g, nplanes, tmp, s.flags, h->stream);
             cudaStreamSynchronize(h->stream);
             cudaFree(tmp);
+            // near-wall fluid cells of the interior planes, in storage order, for the edge kernels
+            cudaMemcpy(hf.data(), s.flags, cells, cudaMemcpyDeviceToHost);
+            std::vector<uint32_t> list;
+            s.edge_off.assign(nplanes + 1, 0);
+            const size_t plane = (size_t)h->nx * h->ny;
+            for (int zs = 0; zs < nplanes; ++zs) {
+                s.edge_off[zs] = (int64_t)list.size();
+                if (zs >= h->g && zs < h->g + s.nz)
+                    for (size_t i = 0; i < plane; ++i)
+                        if (hf[zs * plane + i] == 0x80) list.push_back((uint32_t)(zs * plane + i));
+            }
+            s.edge_off[nplanes] = (int64_t)list.size();
+            if (!list.empty()) {
+                if (cudaMalloc(&s.edges, list.size() * sizeof(uint32_t)) != cudaSuccess) {
+                    h->err = "cudaMalloc edge list";
+                    return bail(LBM_EOOM);
+                }
+                cudaMemcpy(s.edges, list.data(), list.size() * sizeof(uint32_t), cudaMemcpyHostToDevice);
+            }
         }
     }
     if (h->use_nccl) {
@@ -841,6 +870,7 @@ int lbm_destroy(lbm_handle h) {
             }
         for (void *p : s.halo) if (p) cudaFree(p);
         if (s.flags) cudaFree(s.flags);
+        if (s.edges) cudaFree(s.edges);
     }
     if (h->comm) ncclCommDestroy(h->comm);
     for (cudaEvent_t e : h->timing.ev) cudaEventDestroy(e);
