@@ -52,6 +52,9 @@ CONFIGS = {
                weak=False, Q=27, op="cumulant", rates=(1.95,), dtype="f64", pattern="pull", force=(0, 0, 0),
                geometry="cavity", init=("rest",), job_steps=1000, ubb=(0.05, 0, 0)),
 }
+CONFIGS["c4_strong"] = dict(CONFIGS["c4"], shape=(1024, 1024, 1024), weak=False, dtype="f32",
+                           desc="D3Q19 TRT fp32 1024^3 strong scaling (BASELINE config 4, second part); needs >= 2 GPUs "
+                                "for the 32-bit slab offsets (81.6 GB/GPU at P = 2)")
 CONFIGS["c3_aa"] = dict(CONFIGS["c3"], pattern="aa", desc="D3Q27 cumulant fp64 384^3 lid-driven cavity, AA pattern")
 CONFIGS["c3_periodic"] = dict(CONFIGS["c3"], geometry="periodic", init=("random", 1e-3, 0.01),
                               desc="D3Q27 cumulant fp64 384^3 periodic pull (C3 without walls, diagnostic)")

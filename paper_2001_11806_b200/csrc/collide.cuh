@@ -283,6 +283,24 @@ __device__ __forceinline__ void collide_smagorinsky(T (&g)[Q], const Rates<T> &p
 // projection, Delta_h = bulk + order 3 + order 4 projections of g - g_eq (the weighted basis of
 // collide_mrt19); omega_h = 1 + (1 - omega_s) <Ds,Dh>_E / <Dh,Dh>_E, <a,b>_E = sum a b / f_eq.
 // ---------------------------------------------------------------------------------------
+// per-pair reconstruction of the KBC parts from the group coefficients a_k: shear (even), the
+// even part of h (bulk + order 4) and the odd part of h (order 3), each without the factor w_q
+template <typename T>
+__device__ __forceinline__ void kbc_pair_parts(const T (&a)[15], int cx, int cy, int cz, T &s, T &he, T &ho) {
+    s = T(0);
+    he = T(0);
+    ho = T(0);
+#pragma unroll
+    for (int k = 0; k < 15; ++k) {
+        const int c = mrt_poly(k, cx, cy, cz);
+        if (c == 0) continue;
+        T &acc = mrt_group(k) == 0 ? s : ((k >= 6 && k <= 11) ? ho : he);
+        if (c == 1) acc += a[k];
+        else if (c == -1) acc -= a[k];
+        else acc += T(c) * a[k];
+    }
+}
+
 template <typename T>
 __device__ __forceinline__ void collide_kbc19(T (&g)[19], const Rates<T> &p) {
     using S = Stencil<19>;
@@ -294,8 +312,18 @@ __device__ __forceinline__ void collide_kbc19(T (&g)[19], const Rates<T> &p) {
     const T uu15 = T(1.5) * (ux * ux + uy * uy + uz * uz);
     const T w0 = T(S::w(0));
     const T eq0 = w0 * drho - w0 * rho * uu15;
-    const T d0 = g[0] - eq0;
-    T dp[19], dm[19], es[19], ea[19];
+    // <P_k, g - g_eq> / N_k for the 15 non-conserved weighted-orthogonal polynomials, accumulated
+    // pair by pair so that only a[] stays live (the KBC needs g_eq and the parts twice; both are
+    // recomputed per pair below instead of being kept in registers)
+    T a[15];
+    {
+        const T d0 = g[0] - eq0;
+#pragma unroll
+        for (int k = 0; k < 15; ++k) {
+            const int c0 = mrt_poly(k, 0, 0, 0);
+            a[k] = (k >= 6 && k <= 11) || c0 == 0 ? T(0) : T(c0) * d0;
+        }
+    }
 #pragma unroll
     for (int q = 1; q < 19; ++q) {
         if (q < S::opp(q)) {
@@ -303,87 +331,62 @@ __device__ __forceinline__ void collide_kbc19(T (&g)[19], const Rates<T> &p) {
             const T w = T(S::w(q));
             const T cu = T(S::cx(q)) * ux + T(S::cy(q)) * uy + T(S::cz(q)) * uz;
             const T wr = w * rho;
-            es[q] = w * drho + wr * (T(4.5) * cu * cu - uu15);
-            ea[q] = wr * T(3) * cu;
-            dp[q] = (g[q] + g[b]) - T(2) * es[q];
-            dm[q] = (g[q] - g[b]) - T(2) * ea[q];
-        }
-    }
-    T a[15];  // <P_k, g - g_eq> / N_k
-#pragma unroll
-    for (int k = 0; k < 15; ++k) {
-        const bool odd = (k >= 6 && k <= 11);
-        T m = T(0);
-        if (!odd) {
-            const int c0 = mrt_poly(k, 0, 0, 0);
-            if (c0 != 0) m = T(c0) * d0;
-        }
-#pragma unroll
-        for (int q = 1; q < 19; ++q) {
-            if (q < S::opp(q)) {
-                const int c = mrt_poly(k, S::cx(q), S::cy(q), S::cz(q));
-                const T v = odd ? dm[q] : dp[q];
-                if (c == 1) m += v;
-                else if (c == -1) m -= v;
-                else if (c != 0) m += T(c) * v;
-            }
-        }
-        a[k] = T(mrt_inv_norm(k)) * m;
-    }
-    // Delta_s (shear, even) and Delta_h (even part: bulk + order 4, odd part: order 3) per pair
-    T s0 = T(0), h0 = T(0);
-#pragma unroll
-    for (int k = 0; k < 15; ++k) {
-        const int c = mrt_poly(k, 0, 0, 0);
-        if (c != 0) {
-            if (mrt_group(k) == 0) s0 += T(c) * a[k];
-            else h0 += T(c) * a[k];
-        }
-    }
-    T se[19], he[19], ho[19];
-#pragma unroll
-    for (int q = 1; q < 19; ++q) {
-        if (q < S::opp(q)) {
-            T s = T(0), he_ = T(0), ho_ = T(0);
+            const T es = w * drho + wr * (T(4.5) * cu * cu - uu15);
+            const T ea = wr * T(3) * cu;
+            const T dp = (g[q] + g[b]) - T(2) * es;
+            const T dm = (g[q] - g[b]) - T(2) * ea;
 #pragma unroll
             for (int k = 0; k < 15; ++k) {
                 const int c = mrt_poly(k, S::cx(q), S::cy(q), S::cz(q));
-                if (c == 0) continue;
-                T &acc = mrt_group(k) == 0 ? s : ((k >= 6 && k <= 11) ? ho_ : he_);
-                if (c == 1) acc += a[k];
-                else if (c == -1) acc -= a[k];
-                else acc += T(c) * a[k];
+                const T v = (k >= 6 && k <= 11) ? dm : dp;
+                if (c == 1) a[k] += v;
+                else if (c == -1) a[k] -= v;
+                else if (c != 0) a[k] += T(c) * v;
             }
-            const T w = T(S::w(q));
-            se[q] = w * s;
-            he[q] = w * he_;
-            ho[q] = w * ho_;
         }
     }
-    // entropic products with 1/f_eq (f_eq = w + g_eq)
-    const T ds0 = w0 * s0, dh0 = w0 * h0;
-    const T ief0 = T(1) / (w0 + eq0);
-    T sh = ds0 * dh0 * ief0, hh = dh0 * dh0 * ief0;
+#pragma unroll
+    for (int k = 0; k < 15; ++k) a[k] *= T(mrt_inv_norm(k));
+    // pass 1: entropic products <Ds,Dh>_E and <Dh,Dh>_E (f_eq = w + g_eq)
+    T s0, he0, ho0;
+    kbc_pair_parts<T>(a, 0, 0, 0, s0, he0, ho0);
+    const T ds0 = w0 * s0, dh0 = w0 * he0;
+    T sh, hh;
+    {
+        const T ief0 = T(1) / (w0 + eq0);
+        sh = ds0 * dh0 * ief0;
+        hh = dh0 * dh0 * ief0;
+    }
 #pragma unroll
     for (int q = 1; q < 19; ++q) {
         if (q < S::opp(q)) {
             const T w = T(S::w(q));
-            const T iq = T(1) / (w + es[q] + ea[q]);
-            const T ib = T(1) / (w + es[q] - ea[q]);
-            const T hq = he[q] + ho[q], hb = he[q] - ho[q];
-            sh += se[q] * (hq * iq + hb * ib);
+            const T cu = T(S::cx(q)) * ux + T(S::cy(q)) * uy + T(S::cz(q)) * uz;
+            const T wr = w * rho;
+            const T es = w * drho + wr * (T(4.5) * cu * cu - uu15);
+            const T ea = wr * T(3) * cu;
+            T s, he, ho;
+            kbc_pair_parts<T>(a, S::cx(q), S::cy(q), S::cz(q), s, he, ho);
+            const T iq = T(1) / (w + es + ea);
+            const T ib = T(1) / (w + es - ea);
+            const T hq = w * (he + ho), hb = w * (he - ho);
+            sh += w * s * (hq * iq + hb * ib);
             hh += hq * hq * iq + hb * hb * ib;
         }
     }
     const T ws = p.r[0];
     const T wh = hh > T(0) ? T(1) + (T(1) - ws) * sh / hh : T(1);
+    // pass 2: f' = f - w_s Ds - w_h Dh
     g[0] -= ws * ds0 + wh * dh0;
 #pragma unroll
     for (int q = 1; q < 19; ++q) {
         if (q < S::opp(q)) {
             const int b = S::opp(q);
-            g[q] -= ws * se[q] + wh * (he[q] + ho[q]);
-            g[b] -= ws * se[q] + wh * (he[q] - ho[q]);
+            const T w = T(S::w(q));
+            T s, he, ho;
+            kbc_pair_parts<T>(a, S::cx(q), S::cy(q), S::cz(q), s, he, ho);
+            g[q] -= w * (ws * s + wh * (he + ho));
+            g[b] -= w * (ws * s + wh * (he - ho));
         }
     }
 }
