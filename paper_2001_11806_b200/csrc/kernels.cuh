@@ -7,6 +7,7 @@
 // grid covers (x-blocks, y-blocks, z planes). Every population is read once and written once
 // per step: 2*q*sizeof(T) bytes per fluid cell, + 1 B of flag near walls.
 #pragma once
+#include <cassert>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -81,7 +82,18 @@ struct Nbr {
     int xs[3], ys[3], zs[3];
 };
 
+// Debug builds (-DLBM_BOUNDS_CHECK, `build.build(defines=["LBM_BOUNDS_CHECK"])`) assert that every
+// cell an update kernel touches lies inside the storage of its slab (compute-sanitizer is not
+// available on the GPU pool; the GPU tests run once against this variant).
+#ifdef LBM_BOUNDS_CHECK
+#define LBM_ASSERT(c) assert(c)
+#else
+#define LBM_ASSERT(c) ((void)0)
+#endif
+
 __device__ __forceinline__ Nbr neighbours(const Geo &g, int x, int y, int zs) {
+    LBM_ASSERT(x >= 0 && x < g.nx && y >= 0 && y < g.ny);
+    LBM_ASSERT(g.g ? (zs >= 1 && zs <= g.nz) : (zs >= 0 && zs < g.nz));  // only interior planes update
     Nbr n;
     n.xs[1] = x;
     n.xs[0] = (x == 0) ? g.nx - 1 : x - 1;
@@ -222,6 +234,7 @@ __global__ void __launch_bounds__(128) k_pull_edges(const StepArgs a, const T *_
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const uint32_t c = cells[i];
+    LBM_ASSERT((int64_t)c < a.geo.Sq);
     const uint32_t plane = (uint32_t)a.geo.nx * (uint32_t)a.geo.ny;
     const int zs = (int)(c / plane);
     const uint32_t r = c - (uint32_t)zs * plane;
@@ -331,6 +344,7 @@ __global__ void __launch_bounds__(128) k_aa_odd_edges(const StepArgs a, T *__res
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const uint32_t c = cells[i];
+    LBM_ASSERT((int64_t)c < a.geo.Sq);
     const uint32_t plane = (uint32_t)a.geo.nx * (uint32_t)a.geo.ny;
     const int zs = (int)(c / plane);
     const uint32_t r = c - (uint32_t)zs * plane;
@@ -545,6 +559,7 @@ __global__ void k_pack(const Geo geo, const T *__restrict__ f, int zs, int dir, 
         const int k = (int)(i / plane);
         const int64_t r = i - k * plane;
         const int q = crossing_dir<Q>(dir, k);
+        LBM_ASSERT(q >= 0 && zs >= 0 && zs < geo.nz + 2 * geo.g);
         out[i] = OutT(f[q * geo.Sq + zs * plane + r]);
     }
 }
@@ -557,6 +572,7 @@ __global__ void k_unpack(const Geo geo, T *__restrict__ f, int zs, int dir, cons
         const int k = (int)(i / plane);
         const int64_t r = i - k * plane;
         const int q = crossing_dir<Q>(dir, k);
+        LBM_ASSERT(q >= 0 && zs >= 0 && zs < geo.nz + 2 * geo.g);
         f[q * geo.Sq + zs * plane + r] = in[i];
     }
 }
@@ -577,6 +593,7 @@ __global__ void k_unpack_masked(const Geo geo, T *__restrict__ f, int zs, int di
         const int x = (int)(r % geo.nx), y = (int)(r / geo.nx);
         const int xs = (x - S::cx(q) + geo.nx) % geo.nx, ys = (y - S::cy(q) + geo.ny) % geo.ny;
         const int64_t src = (int64_t)(zs - S::cz(q)) * plane + (int64_t)ys * geo.nx + xs;
+        LBM_ASSERT(q >= 0 && zs >= 0 && zs < geo.nz + 2 * geo.g && zs - S::cz(q) >= 0 && zs - S::cz(q) < geo.nz + 2 * geo.g);
         if ((flags[src] & 3) == 0) f[q * geo.Sq + zs * plane + r] = in[i];
     }
 }
