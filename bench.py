@@ -240,7 +240,9 @@ def main():
     ap.add_argument("--nccl-self", type=int, default=0,
                     help="N=1 only: ghost planes exchanged through a 1-rank NCCL communicator (times the multi-GPU path)")
     ap.add_argument("--block-x", type=int, default=0)
-    ap.add_argument("--graph", type=int, default=-1, help="CUDA-graph capture (default: on for small domains)")
+    ap.add_argument("--graph", type=int, default=-1,
+                    help="small-domain launch mode: 0 plain launches, 1 CUDA graph, 2 persistent cooperative kernel "
+                         "(default: 2 for domains of <= 2^21 cells per GPU, else 0)")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     if args.impl == "reference":
@@ -280,9 +282,9 @@ def main():
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
     small = np.prod(gshape) / P <= 2 ** 21
-    use_graph = bool(small) if args.graph < 0 else bool(args.graph)
+    use_graph = (2 if small else 0) if args.graph < 0 else args.graph
     nccl_self = bool(args.nccl_self) and world == 1
-    use_graph = use_graph and not nccl_self
+    use_graph = 0 if nccl_self else use_graph
     exchanging = world > 1 or nccl_self
     halo_mode = args.halo_mode
     if halo_mode < 0:  # default: fused NVLink peer-store halo for the pull pattern, else zero-copy NCCL
@@ -333,7 +335,7 @@ def main():
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    sim.enable_kernel_timing() if not use_graph else None
+    sim.enable_kernel_timing() if use_graph != 1 else None
     l0 = sim.launches
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
@@ -345,7 +347,7 @@ def main():
         dist.barrier()
     t_ms = ev0.elapsed_time(ev1)
     launches = sim.launches - l0
-    if not use_graph:
+    if use_graph != 1:
         kms, klaunch = sim.kernel_time_ms()
     else:
         kms, klaunch = t_ms, launches
@@ -420,7 +422,7 @@ def main():
                        "parallelism": f"z-slab x{world}" if world > 1 else
                        ("single GPU, NCCL self-exchange of ghost planes" if nccl_self else "single GPU"),
                        "l2": "inputs larger than L2 (no flush)" if not small else "L2-resident (launch-bound config)",
-                       "halo_mode": {0: "zerocopy NCCL send/recv", 1: "packed NCCL send/recv", 2: "fused NVLink peer stores (NCCL LSA windows)"}[args.halo_mode] if (world > 1 or nccl_self) else "none (single slab, z wraps in-kernel)", "cuda_graph": use_graph},
+                       "halo_mode": {0: "zerocopy NCCL send/recv", 1: "packed NCCL send/recv", 2: "fused NVLink peer stores (NCCL LSA windows)"}[args.halo_mode] if (world > 1 or nccl_self) else "none (single slab, z wraps in-kernel)", "small_domain_mode": {0: "plain launches", 1: "CUDA graph (2-step cycle)", 2: "persistent cooperative kernel"}[use_graph]},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                          "traffic": load_traffic(args.config), "peak_source": peak_src,
                          "algorithmic_bytes_per_cell": bpc, "cells_per_launch": nf_local,

@@ -106,7 +106,9 @@ typedef struct lbm_config {
     int32_t device;         /* CUDA device ordinal */
     void *stream;           /* cudaStream_t for compute; NULL = library-created stream */
     int32_t halo_mode;      /* LBM_HALO_ZEROCOPY | LBM_HALO_PACKED | LBM_HALO_FUSED */
-    int32_t use_graph;      /* 1 = capture a two-step cycle in a CUDA graph (single slab only) */
+    int32_t use_graph;      /* small single-slab domains (launch-bound): 1 = replay a captured two-step
+                               CUDA graph; 2 = one persistent cooperative kernel per lbm_step call with a
+                               grid-wide barrier between steps (walls inline) */
     int32_t block_x;        /* threads per block along x (0 = default) */
     int32_t check_nan_every;/* >0: check for NaN every k steps inside lbm_step (LBM_ENAN) */
     int32_t nccl_self;      /* nranks == 1 only: keep ghost planes and exchange them through a

@@ -13,11 +13,16 @@ using EdgeLaunch = void (*)(const StepArgs &, const void *src, void *dst, const 
 
 // The kernels of one (operator, stencil, dtype, wall mode, force) combination; null members = not
 // instantiated. fm: FM_NONE, FM_INLINE or FM_BULK (kernels.cuh); the edge launchers go with FM_BULK.
+// persistent multi-step launch (cooperative); returns 0, or -1 if the launch failed
+using PersistLaunch = int (*)(const StepArgs &, void *A, void *B, int phase, int nsteps, cudaStream_t);
+
 struct Kernels {
     PullLaunch pull = nullptr;
     AALaunch aa = nullptr;
     EdgeLaunch pull_edges = nullptr;
     EdgeLaunch aa_edges = nullptr;
+    PersistLaunch persist_pull = nullptr;  // walls inline (FM_INLINE) when a flag field exists
+    PersistLaunch persist_aa = nullptr;
 };
 
 Kernels select_trt(int Q, int dtype, int fm, bool force);

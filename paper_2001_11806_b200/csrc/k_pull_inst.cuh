@@ -1,5 +1,7 @@
 // k_pull_inst.cuh — helpers to instantiate pull/AA launchers for one collision operator.
 #pragma once
+#include <cstdlib>
+
 #include "dispatch.h"
 
 namespace lbm {
@@ -39,6 +41,42 @@ void aa_edge_launcher(const StepArgs &a, const void *src, void *f, const uint32_
     k_aa_odd_edges<Q, OP, T, FORCE><<<(n + 127) / 128, 128, 0, s>>>(a, static_cast<T *>(f), cells, n);
 }
 
+template <int Q, int OP, typename T, int FM, bool FORCE, bool AA>
+int persistent_launcher(const StepArgs &a, void *A, void *B, int phase, int nsteps, cudaStream_t s) {
+    auto kern = k_persistent<Q, OP, T, FM, FORCE, AA>;
+    static int coresident = 0;
+    if (coresident == 0) {
+        int per_sm = 0, sms = 0, dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, 0);
+        coresident = per_sm * sms;
+    }
+    const int64_t ncell = (int64_t)a.geo.nx * a.geo.ny * a.geo.nz;
+    // cells per thread: a few cells per thread keeps the grid (and so the grid barrier) small
+    static const int cpt = [] {
+        const char *e = getenv("LBM_PERSIST_CELLS_PER_THREAD");
+        return e ? atoi(e) : 1;
+    }();
+    int64_t grid = (ncell + 256 * (int64_t)cpt - 1) / (256 * (int64_t)cpt);
+    if (grid > coresident) grid = coresident;
+    if (grid < 1) return -1;
+    T *pa = static_cast<T *>(A), *pb = static_cast<T *>(B);
+    void *args[] = {const_cast<StepArgs *>(&a), &pa, &pb, &phase, &nsteps};
+    return cudaLaunchCooperativeKernel((const void *)kern, dim3((unsigned)grid), dim3(256), args, 0, s) == cudaSuccess ? 0 : -1;
+}
+
+template <int Q, int OP, typename T, bool FORCE>
+void pick_persistent(int fm, Kernels &k) {
+    if (fm == FM_NONE) {
+        k.persist_pull = &persistent_launcher<Q, OP, T, FM_NONE, FORCE, false>;
+        k.persist_aa = &persistent_launcher<Q, OP, T, FM_NONE, FORCE, true>;
+    } else {
+        k.persist_pull = &persistent_launcher<Q, OP, T, FM_INLINE, FORCE, false>;
+        k.persist_aa = &persistent_launcher<Q, OP, T, FM_INLINE, FORCE, true>;
+    }
+}
+
 template <int Q, int OP, typename T, bool FORCE>
 PullLaunch pick_pull_fm(int fm) {
     switch (fm) {
@@ -67,6 +105,7 @@ Kernels pick(int fm, bool force) {
             k.aa = pick_aa_fm<Q, OP, T, true>(fm);
             k.pull_edges = &pull_edge_launcher<Q, OP, T, true>;
             k.aa_edges = &aa_edge_launcher<Q, OP, T, true>;
+            pick_persistent<Q, OP, T, true>(fm, k);
             return k;
         }
     } else {
@@ -76,6 +115,7 @@ Kernels pick(int fm, bool force) {
     k.aa = pick_aa_fm<Q, OP, T, false>(fm);
     k.pull_edges = &pull_edge_launcher<Q, OP, T, false>;
     k.aa_edges = &aa_edge_launcher<Q, OP, T, false>;
+    pick_persistent<Q, OP, T, false>(fm, k);
     return k;
 }
 

@@ -9,6 +9,7 @@
 #pragma once
 #include <cassert>
 #include <cstdint>
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include "collide.cuh"
@@ -255,12 +256,8 @@ __device__ __forceinline__ T ubb_term(const StepArgs &a, int q) {
 }
 
 template <int Q, int OP, typename T, bool FLAGS, bool FORCE>
-__global__ void __launch_bounds__(256, (MinBlocks<Q, OP, T>::aa)) k_aa_even(const StepArgs a, T *__restrict__ f) {
+__device__ __forceinline__ void aa_even_cell(const StepArgs &a, T *__restrict__ f, int x, int y, int zs) {
     using S = Stencil<Q>;
-    const int x = blockIdx.x * blockDim.x + threadIdx.x;
-    const int y = blockIdx.y * blockDim.y + threadIdx.y;
-    if (x >= a.geo.nx || y >= a.geo.ny) return;
-    const int zs = a.z_begin + (int)blockIdx.z * a.z_step + a.geo.g;
     const uint32_t self = ((uint32_t)zs * (uint32_t)a.geo.ny + (uint32_t)y) * (uint32_t)a.geo.nx + (uint32_t)x;
     const int64_t Sq = a.geo.Sq;
     if (FLAGS && (a.flags[self] & 3)) return;  // wall cells are not updated
@@ -271,6 +268,14 @@ __global__ void __launch_bounds__(256, (MinBlocks<Q, OP, T>::aa)) k_aa_even(cons
     collide<Q, OP, T, FORCE>(g, r);
 #pragma unroll
     for (int q = 0; q < Q; ++q) f[S::opp(q) * Sq + self] = g[q];
+}
+
+template <int Q, int OP, typename T, bool FLAGS, bool FORCE>
+__global__ void __launch_bounds__(256, (MinBlocks<Q, OP, T>::aa)) k_aa_even(const StepArgs a, T *__restrict__ f) {
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    const int y = blockIdx.y * blockDim.y + threadIdx.y;
+    if (x >= a.geo.nx || y >= a.geo.ny) return;
+    aa_even_cell<Q, OP, T, FLAGS, FORCE>(a, f, x, y, a.z_begin + (int)blockIdx.z * a.z_step + a.geo.g);
 }
 
 template <int Q, int OP, typename T, int FM, bool FORCE>
@@ -349,6 +354,33 @@ __global__ void __launch_bounds__(128) k_aa_odd_edges(const StepArgs a, T *__res
     const int zs = (int)(c / plane);
     const uint32_t r = c - (uint32_t)zs * plane;
     aa_odd_cell<Q, OP, T, FM_EDGE, FORCE>(a, f, (int)(r % (uint32_t)a.geo.nx), (int)(r / (uint32_t)a.geo.nx), zs);
+}
+
+// =======================================================================================
+// Persistent multi-step kernel for small single-slab domains (launch-bound otherwise, e.g. the
+// 32^3 config 0): one cooperative launch runs all n steps of an lbm_step call, cells grid-strided,
+// with a grid-wide barrier between steps instead of a kernel boundary. Walls are handled inline.
+// =======================================================================================
+template <int Q, int OP, typename T, int FM, bool FORCE, bool AA>
+__global__ void __launch_bounds__(256) k_persistent(const StepArgs a, T *A, T *B, int phase, int nsteps) {
+    cooperative_groups::grid_group grid = cooperative_groups::this_grid();
+    const int64_t ncell = (int64_t)a.geo.nx * a.geo.ny * a.geo.nz;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int t = 0; t < nsteps; ++t) {
+        const int p = (phase + t) & 1;
+        for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < ncell; i += stride) {
+            const int x = (int)(i % a.geo.nx);
+            const int y = (int)((i / a.geo.nx) % a.geo.ny);
+            const int zs = (int)(i / ((int64_t)a.geo.nx * a.geo.ny));
+            if constexpr (AA) {
+                if (p == 0) aa_even_cell<Q, OP, T, (FM != FM_NONE), FORCE>(a, A, x, y, zs);
+                else aa_odd_cell<Q, OP, T, FM, FORCE>(a, A, x, y, zs);
+            } else {
+                pull_cell<Q, OP, T, FM, FORCE, false>(a, p ? B : A, p ? A : B, x, y, zs);
+            }
+        }
+        grid.sync();
+    }
 }
 
 // =======================================================================================

@@ -370,7 +370,10 @@ int step_once(lbm_handle_s *h) {
     return LBM_OK;
 }
 
-bool graph_ok(const lbm_handle_s *h) { return h->cfg.use_graph && h->g == 0 && h->slabs.size() == 1 && !h->timing.on; }
+bool graph_ok(const lbm_handle_s *h) { return h->cfg.use_graph == 1 && h->g == 0 && h->slabs.size() == 1 && !h->timing.on; }
+bool persistent_ok(const lbm_handle_s *h) {
+    return h->cfg.use_graph == 2 && h->g == 0 && h->slabs.size() == 1 && h->kern.persist_pull && h->kern.persist_aa;
+}
 
 int run_graph_cycle(lbm_handle_s *h) {
     // one cycle = two steps (pull: src->dst->src; AA: even+odd), replayed; state returns to the same slots
@@ -988,13 +991,32 @@ int lbm_step(lbm_handle h, int64_t n) {
             if (chunk > to_check) chunk = to_check;
         }
         int64_t i = 0;
+        if (persistent_ok(h) && chunk > 0) {
+            // one cooperative launch runs the whole chunk (grid-wide barrier between steps)
+            Slab &s = h->slabs[0];
+            StepArgs a = h->base;
+            a.geo = geo_of(h, s);
+            a.z_begin = 0;
+            a.z_step = 1;
+            a.flags = s.flags;
+            const bool aa = h->cfg.pattern == LBM_AA;
+            const int phase = aa ? h->aa_parity : s.cur;
+            tbegin(h, h->stream);
+            const int rc = (aa ? h->kern.persist_aa : h->kern.persist_pull)(a, s.pdf[0], aa ? nullptr : s.pdf[1], phase,
+                                                                          (int)chunk, h->stream);
+            tend(h, h->stream);
+            if (rc) return fail(h, LBM_ECUDA, "persistent cooperative launch failed");
+            h->launches++;
+            if (chunk & 1) {
+                if (aa) h->aa_parity ^= 1;
+                else s.cur ^= 1;
+            }
+            i = chunk;
+        }
         if (graph_ok(h)) {
-            for (; i + 2 <= chunk; i += 2) {
+            for (; i + 2 <= chunk; i += 2) {  // a two-step cycle returns the state to the same slots
                 int rc = run_graph_cycle(h);
                 if (rc) return rc;
-                if (h->cfg.pattern == LBM_PULL) {
-                    // a two-step cycle returns the state to the same array
-                }
             }
         }
         for (; i < chunk; ++i) {

@@ -188,6 +188,31 @@ def test_cuda_graph_path_bit_identical():
     np.testing.assert_array_equal(a.populations(raw=True), b.populations(raw=True))
 
 
+PERSISTENT = [
+    Case("p_c0", (32, 32, 32), 19, "srt", (1.8,), "f64", steps=37),
+    Case("p_walls_force", (17, 13, 11), 19, "trt", (1.6, 0.5), "f64", force=(1e-5, 0, 0), geometry="obstacles",
+         ubb=(0.02, -0.01, 0.03), steps=15),
+    Case("p_aa_cumulant_cavity", (12, 12, 12), 27, "cumulant", (1.95,), "f64", pattern="aa", geometry="cavity",
+         ubb=(0.05, 0, 0), steps=13),
+    Case("p_aa_mrt_f32", (20, 16, 12), 19, "mrt", (1.9, 1.0, 1.0, 1.0), "f32", pattern="aa", init="shear",
+         rho_amp=0.0, u_amp=1e-4, steps=12),
+]
+
+
+@pytest.mark.parametrize("case", PERSISTENT, ids=lambda c: c.name)
+def test_persistent_multistep_kernel(case):
+    """use_graph = 2: one cooperative launch per lbm_step call (grid barrier between steps); split
+    into uneven calls and NaN-check chunks to exercise the phase bookkeeping."""
+    sim = make_sim(case, use_graph=2, check_nan_every=4)
+    init_sim(sim, case)
+    l0 = sim.launches
+    sim.step(case.steps // 2)
+    sim.step(case.steps - case.steps // 2)
+    assert sim.launches - l0 <= 2 + case.steps // 4 + 2  # one launch per chunk, not per step
+    err = max_rel_err(sim.populations(), oracle_run(case), fluid_mask(case, case.Q))
+    assert err <= TOL[case.dtype], err
+
+
 def test_nan_detection():
     from paper_2001_11806_b200 import lbm as L
     case = Case("nan", (8, 8, 8), 19, "srt", (1.8,), "f64")
