@@ -228,6 +228,22 @@ int lbm_kernel_aa(const lbm_kernel_args *a, int32_t odd);
 int lbm_prepare_flags(const uint8_t *host_flags, int64_t nx, int64_t ny, int64_t nplanes, int32_t ghost,
                       uint8_t *device_out, void *stream);
 
+/* ---- Kernel path of the bulk update kernels (process-wide; affects launches issued afterwards) ----
+ * LBM_PATH_PLAIN : one thread per cell gathers its q populations straight into registers (ld.global.nc).
+ * LBM_PATH_STAGED: persistent CTAs; a producer warp moves the source rows of each direction into a
+ *                  shared-memory ring with 1-D bulk copies (cp.async.bulk, the TMA engine, mbarrier
+ *                  completion) and consumer warps gather from shared memory. Needs nx * sizeof(real)
+ *                  % 16 == 0 (and nx % 16 == 0 with walls); otherwise the plain kernel runs.
+ * LBM_PATH_AUTO  : the measured per-operator choice. Default; the environment
+ *                  variable LBM_KERNEL_PATH=auto|plain|staged sets the initial value.
+ * Both paths compute the same update (same arithmetic in the same order). Returns LBM_EINVAL for an
+ * unknown path. */
+#define LBM_PATH_AUTO 0
+#define LBM_PATH_PLAIN 1
+#define LBM_PATH_STAGED 2
+int lbm_set_kernel_path(int32_t path);
+int32_t lbm_get_kernel_path(void);
+
 const char *lbm_strerror(int status);
 const char *lbm_last_error(lbm_handle h);
 /* Library version string. */

@@ -1,5 +1,9 @@
 // k_misc.cu — auxiliary kernels: initialisation, readout, halo pack/unpack, flag row mask and
 // NaN check, dispatched on (stencil, dtype).
+#include <atomic>
+#include <cstdlib>
+#include <cstring>
+
 #include "dispatch.h"
 
 namespace lbm {
@@ -103,4 +107,30 @@ void launch_nan_check(int dtype, const void *f, int64_t n, int *flag, cudaStream
         k_nan_check<float><<<blocks_for(n), 256, 0, s>>>(static_cast<const float *>(f), n, flag);
 }
 
+}  // namespace lbm
+
+namespace lbm {
+// Kernel path of the bulk update kernels (staged.cuh): LBM_PATH_AUTO (measured per-family policy),
+// LBM_PATH_PLAIN (register-gather kernels everywhere) or LBM_PATH_STAGED (TMA-staged wherever the
+// layout allows). Initial value from LBM_KERNEL_PATH=auto|plain|staged; lbm_set_kernel_path changes
+// it process-wide. LBM_STAGES sets the pipeline depth (tiles in flight per CTA, 2..6).
+static std::atomic<int> g_kernel_path{-1};
+int staged_path() {
+    int v = g_kernel_path.load(std::memory_order_relaxed);
+    if (v < 0) {
+        const char *e = getenv("LBM_KERNEL_PATH");
+        v = !e ? 0 : (!strcmp(e, "plain") ? 1 : (!strcmp(e, "staged") ? 2 : 0));
+        g_kernel_path.store(v, std::memory_order_relaxed);
+    }
+    return v;
+}
+void set_staged_path(int v) { g_kernel_path.store(v, std::memory_order_relaxed); }
+int staged_nstages() {
+    static const int n = [] {
+        const char *e = getenv("LBM_STAGES");
+        const int v = e ? atoi(e) : 2;
+        return v < 2 ? 2 : (v > 6 ? 6 : v);
+    }();
+    return n;
+}
 }  // namespace lbm

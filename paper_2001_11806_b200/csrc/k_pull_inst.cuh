@@ -3,6 +3,7 @@
 #include <cstdlib>
 
 #include "dispatch.h"
+#include "staged.cuh"
 
 namespace lbm {
 
@@ -10,6 +11,7 @@ template <int Q, int OP, typename T, int FM, bool FORCE>
 void pull_launcher(const StepArgs &a, const void *src, void *dst, dim3 grid, dim3 block, cudaStream_t s) {
     // peer stores (fused halo, boundary-plane launches only) are a separate instantiation so the
     // interior kernel carries no extra live registers
+    if (a.peer_up == nullptr && staged_launch<Q, OP, T, FM, FORCE, SM_PULL>(a, src, dst, (int)grid.z, s)) return;
     if (a.peer_up != nullptr)
         k_pull<Q, OP, T, FM, FORCE, true><<<grid, block, 0, s>>>(a, static_cast<const T *>(src), static_cast<T *>(dst));
     else
@@ -28,6 +30,11 @@ void pull_edge_launcher(const StepArgs &a, const void *src, void *dst, const uin
 
 template <int Q, int OP, typename T, int FM, bool FORCE>
 void aa_launcher(const StepArgs &a, void *f, int odd, dim3 grid, dim3 block, cudaStream_t s) {
+    if (odd) {
+        if (staged_launch<Q, OP, T, FM, FORCE, SM_AA_ODD>(a, f, f, (int)grid.z, s)) return;
+    } else {
+        if (staged_launch<Q, OP, T, (FM == FM_NONE ? FM_NONE : FM_BULK), FORCE, SM_AA_EVEN>(a, f, f, (int)grid.z, s)) return;
+    }
     if (odd)
         k_aa_odd<Q, OP, T, FM, FORCE><<<grid, block, 0, s>>>(a, static_cast<T *>(f));
     else  // the even step is in place: walls are skipped, near-wall cells need nothing special

@@ -506,7 +506,14 @@ void lbm_config_default(lbm_config *c) {
     c->n_local_slabs = 1;
 }
 
-const char *lbm_version(void) { return "b200-lbm 0.1 (sm_100a)"; }
+const char *lbm_version(void) { return "b200-lbm 0.2 (sm_100a)"; }
+
+int lbm_set_kernel_path(int32_t path) {
+    if (path < LBM_PATH_AUTO || path > LBM_PATH_STAGED) return LBM_EINVAL;
+    lbm::set_staged_path(path);
+    return LBM_OK;
+}
+int32_t lbm_get_kernel_path(void) { return lbm::staged_path(); }
 
 const char *lbm_strerror(int s) {
     switch (s) {

@@ -27,6 +27,8 @@ PULL, AA = 0, 1
 FLUID, NOSLIP, UBB = 0, 1, 2
 HOST, DEVICE = 0, 1
 HALO_ZEROCOPY, HALO_PACKED, HALO_FUSED = 0, 1, 2
+PATH_AUTO, PATH_PLAIN, PATH_STAGED = 0, 1, 2
+KERNEL_PATHS = {"auto": PATH_AUTO, "plain": PATH_PLAIN, "staged": PATH_STAGED}
 
 COLLISIONS = {"srt": SRT, "trt": TRT, "mrt": MRT, "cumulant": CUMULANT, "identity": IDENTITY,
               "smagorinsky": SMAGORINSKY, "kbc": KBC}
@@ -96,6 +98,8 @@ _SIGS = {
     "lbm_strerror": ([C.c_int], C.c_char_p),
     "lbm_last_error": ([_P], C.c_char_p),
     "lbm_version": ([], C.c_char_p),
+    "lbm_set_kernel_path": ([_I32], C.c_int),
+    "lbm_get_kernel_path": ([], _I32),
 }
 for _name, (_args, _res) in _SIGS.items():
     _fn = getattr(_lib, _name)
@@ -121,6 +125,16 @@ def _ptr(a) -> int:
         return a.ctypes.data
     assert a.is_contiguous()
     return a.data_ptr()
+
+
+def set_kernel_path(path) -> None:
+    """Bulk kernel path, process-wide: "auto" | "plain" | "staged" (include/lbm.h)."""
+    _check(lbm_set_kernel_path(KERNEL_PATHS[path] if isinstance(path, str) else int(path)), what="lbm_set_kernel_path")
+
+
+def kernel_path() -> str:
+    v = int(lbm_get_kernel_path())
+    return {b: a for a, b in KERNEL_PATHS.items()}[v]
 
 
 def slab_plan(nz: int, nranks: int, rank: int):

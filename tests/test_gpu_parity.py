@@ -167,8 +167,17 @@ PARITY = [
 ]
 
 
+@pytest.fixture(params=["plain", "staged"])
+def kernel_path(request):
+    """Run the test with the bulk kernels forced to one path (include/lbm.h lbm_set_kernel_path)."""
+    from paper_2001_11806_b200 import lbm as L
+    L.set_kernel_path(request.param)
+    yield request.param
+    L.set_kernel_path("auto")
+
+
 @pytest.mark.parametrize("case", PARITY, ids=lambda c: c.name)
-def test_parity_vs_oracle(case):
+def test_parity_vs_oracle(case, kernel_path):
     sim = make_sim(case)
     init_sim(sim, case)
     sim.step(case.steps)
@@ -176,6 +185,41 @@ def test_parity_vs_oracle(case):
     ref = oracle_run(case)
     err = max_rel_err(got, ref, fluid_mask(case, case.Q))
     assert err <= TOL[case.dtype], err
+
+
+STAGED_CASES = [
+    Case("st_trt_f64_ragged_rows", (32, 13, 9), 19, "trt", (1.6, 0.5), "f64", force=(1e-5, 0, 0), steps=9),
+    Case("st_mrt_f32_aa_walls16", (32, 20, 12), 19, "mrt", (1.9, 1.3, 1.1, 0.8), "f32", pattern="aa",
+         geometry="channel", steps=11),
+    Case("st_cumulant_pull_cavity16", (16, 16, 16), 27, "cumulant", (1.95,), "f64", geometry="cavity",
+         ubb=(0.05, 0, 0), steps=9),
+    Case("st_kbc_aa_obst", (48, 10, 8), 19, "kbc", (1.95,), "f64", pattern="aa", geometry="obstacles",
+         ubb=(0.02, -0.01, 0.03), u_amp=0.05, steps=9),
+    Case("st_smag_q27_f32", (64, 6, 5), 27, "smagorinsky", (1.9, 0.12), "f32", u_amp=0.05, steps=8),
+]
+
+
+@pytest.mark.parametrize("case", STAGED_CASES, ids=lambda c: c.name)
+def test_staged_and_plain_paths_agree(case):
+    """Shapes the TMA-staged kernels accept (nx * sizeof(real) % 16 == 0; staged flag rows at nx % 16 == 0;
+    several rows per tile and a ragged last tile): both paths against the oracle, and against each other."""
+    from paper_2001_11806_b200 import lbm as L
+    out = {}
+    try:
+        for path in ("plain", "staged"):
+            L.set_kernel_path(path)
+            sim = make_sim(case)
+            init_sim(sim, case)
+            sim.step(case.steps)
+            out[path] = sim.populations(raw=True)
+            err = max_rel_err(sim.populations(), oracle_run(case), fluid_mask(case, case.Q))
+            assert err <= TOL[case.dtype], (path, err)
+            sim.close()
+    finally:
+        L.set_kernel_path("auto")
+    mask = fluid_mask(case, case.Q)
+    d = np.abs(out["plain"][mask] - out["staged"][mask])
+    assert float(d.max()) <= (1e-14 if case.dtype == "f64" else 1e-6)
 
 
 def test_cuda_graph_path_bit_identical():
