@@ -144,7 +144,14 @@ __host__ __device__ constexpr double mrt_inv_norm(int k) {
          : k == 12 ? 0.5 : k == 13 ? 2.25 : 0.75;
 }
 __host__ __device__ constexpr int mrt_group(int k) { return k <= 4 ? 0 : k == 5 ? 1 : k <= 11 ? 2 : 3; }
+// index of polynomial k inside its group (0..5)
+__host__ __device__ constexpr int mrt_slot(int k) { return k <= 4 ? k : k == 5 ? 0 : k <= 11 ? k - 6 : k - 12; }
 
+// Eq. (4) with per-group rates, written as f* = f_eq + sum_g (1 - omega_g) P_g (f - f_eq): the
+// projectors of the four non-conserved groups plus the conserved one sum to the identity and
+// d = f - f_eq has no conserved part, so f - sum_g omega_g P_g d = f_eq + sum_g (1 - omega_g) P_g d.
+// A group relaxed with omega_g = 1 contributes nothing and is skipped by a uniform branch — the
+// run-time counterpart of the paper's pre-evaluation of constant relaxation rates.
 template <typename T>
 __device__ __forceinline__ void collide_mrt19(T (&g)[19], const Rates<T> &p) {
     using S = Stencil<19>;
@@ -156,9 +163,10 @@ __device__ __forceinline__ void collide_mrt19(T (&g)[19], const Rates<T> &p) {
     const T uu15 = T(1.5) * (ux * ux + uy * uy + uz * uz);
     // Non-equilibrium part d = g - g_eq, split over the direction pairs (q, qbar): even moment
     // polynomials (shear, bulk, order 4) see only dp = d_q + d_qbar, odd ones (order 3) only
-    // dm = d_q - d_qbar — half the work of the plain 15 x 19 transform.
+    // dm = d_q - d_qbar — half the work of the plain 15 x 19 transform. g is overwritten with g_eq.
     const T w0 = T(S::w(0));
     const T d0 = g[0] - (w0 * drho - w0 * rho * uu15);
+    g[0] -= d0;
     T dp[19], dm[19];
 #pragma unroll
     for (int q = 1; q < 19; ++q) {
@@ -171,54 +179,63 @@ __device__ __forceinline__ void collide_mrt19(T (&g)[19], const Rates<T> &p) {
             const T eqa = wr * T(3) * cu;
             dp[q] = (g[q] + g[b]) - T(2) * eqs;
             dm[q] = (g[q] - g[b]) - T(2) * eqa;
+            g[q] = eqs + eqa;
+            g[b] = eqs - eqa;
         }
     }
-    T a[15];
 #pragma unroll
-    for (int k = 0; k < 15; ++k) {
-        const bool odd = (k >= 6 && k <= 11);
-        T m = T(0);
+    for (int grp = 0; grp < 4; ++grp) {
+        const T keep = T(1) - p.r[grp];
+        if (keep == T(0)) continue;  // uniform: omega_g = 1 relaxes the group to equilibrium
+        const bool odd = grp == 2;
+        T a[6];
+#pragma unroll
+        for (int k = 0; k < 15; ++k) {
+            if (mrt_group(k) != grp) continue;
+            T m = T(0);
+            if (!odd) {
+                const int c0 = mrt_poly(k, 0, 0, 0);
+                if (c0 != 0) m = T(c0) * d0;
+            }
+#pragma unroll
+            for (int q = 1; q < 19; ++q) {
+                if (q < S::opp(q)) {
+                    const int c = mrt_poly(k, S::cx(q), S::cy(q), S::cz(q));
+                    const T v = odd ? dm[q] : dp[q];
+                    if (c == 1) m += v;
+                    else if (c == -1) m -= v;
+                    else if (c != 0) m += T(c) * v;
+                }
+            }
+            a[mrt_slot(k)] = keep * T(mrt_inv_norm(k)) * m;
+        }
         if (!odd) {
-            const int c0 = mrt_poly(k, 0, 0, 0);
-            if (c0 != 0) m = T(c0) * d0;
+            T s = T(0);
+#pragma unroll
+            for (int k = 0; k < 15; ++k) {
+                if (mrt_group(k) != grp) continue;
+                const int c = mrt_poly(k, 0, 0, 0);
+                if (c != 0) s += T(c) * a[mrt_slot(k)];
+            }
+            g[0] += w0 * s;
         }
 #pragma unroll
         for (int q = 1; q < 19; ++q) {
             if (q < S::opp(q)) {
-                const int c = mrt_poly(k, S::cx(q), S::cy(q), S::cz(q));
-                const T v = odd ? dm[q] : dp[q];
-                if (c == 1) m += v;
-                else if (c == -1) m -= v;
-                else if (c != 0) m += T(c) * v;
+                const int b = S::opp(q);
+                T acc = T(0);
+#pragma unroll
+                for (int k = 0; k < 15; ++k) {
+                    if (mrt_group(k) != grp) continue;
+                    const int c = mrt_poly(k, S::cx(q), S::cy(q), S::cz(q));
+                    if (c == 1) acc += a[mrt_slot(k)];
+                    else if (c == -1) acc -= a[mrt_slot(k)];
+                    else if (c != 0) acc += T(c) * a[mrt_slot(k)];
+                }
+                const T w = T(S::w(q));
+                g[q] += w * acc;
+                g[b] += odd ? -w * acc : w * acc;
             }
-        }
-        a[k] = p.r[mrt_group(k)] * T(mrt_inv_norm(k)) * m;
-    }
-    {
-        T s = T(0);
-#pragma unroll
-        for (int k = 0; k < 15; ++k) {
-            const int c = mrt_poly(k, 0, 0, 0);
-            if (c != 0) s += T(c) * a[k];
-        }
-        g[0] -= w0 * s;
-    }
-#pragma unroll
-    for (int q = 1; q < 19; ++q) {
-        if (q < S::opp(q)) {
-            const int b = S::opp(q);
-            T se = T(0), so = T(0);
-#pragma unroll
-            for (int k = 0; k < 15; ++k) {
-                const int c = mrt_poly(k, S::cx(q), S::cy(q), S::cz(q));
-                T &acc = (k >= 6 && k <= 11) ? so : se;
-                if (c == 1) acc += a[k];
-                else if (c == -1) acc -= a[k];
-                else if (c != 0) acc += T(c) * a[k];
-            }
-            const T w = T(S::w(q));
-            g[q] -= w * (se + so);
-            g[b] -= w * (se - so);
         }
     }
 }
@@ -283,24 +300,10 @@ __device__ __forceinline__ void collide_smagorinsky(T (&g)[Q], const Rates<T> &p
 // projection, Delta_h = bulk + order 3 + order 4 projections of g - g_eq (the weighted basis of
 // collide_mrt19); omega_h = 1 + (1 - omega_s) <Ds,Dh>_E / <Dh,Dh>_E, <a,b>_E = sum a b / f_eq.
 // ---------------------------------------------------------------------------------------
-// per-pair reconstruction of the KBC parts from the group coefficients a_k: shear (even), the
-// even part of h (bulk + order 4) and the odd part of h (order 3), each without the factor w_q
-template <typename T>
-__device__ __forceinline__ void kbc_pair_parts(const T (&a)[15], int cx, int cy, int cz, T &s, T &he, T &ho) {
-    s = T(0);
-    he = T(0);
-    ho = T(0);
-#pragma unroll
-    for (int k = 0; k < 15; ++k) {
-        const int c = mrt_poly(k, cx, cy, cz);
-        if (c == 0) continue;
-        T &acc = mrt_group(k) == 0 ? s : ((k >= 6 && k <= 11) ? ho : he);
-        if (c == 1) acc += a[k];
-        else if (c == -1) acc -= a[k];
-        else acc += T(c) * a[k];
-    }
-}
-
+// Only the shear part is projected: d = g - g_eq has no conserved moments, so the higher-order part
+// is Delta_h = d - Delta_s exactly (f = f_eq + Delta_s + Delta_h, Eq. 15), and
+// f' = f - w_s Ds - w_h Dh = f_eq + (1 - w_h) d + (w_h - w_s) Ds. The shear polynomials are even
+// and vanish at c = 0, so Ds is the same for q and qbar and zero at the centre.
 template <typename T>
 __device__ __forceinline__ void collide_kbc19(T (&g)[19], const Rates<T> &p) {
     using S = Stencil<19>;
@@ -312,18 +315,9 @@ __device__ __forceinline__ void collide_kbc19(T (&g)[19], const Rates<T> &p) {
     const T uu15 = T(1.5) * (ux * ux + uy * uy + uz * uz);
     const T w0 = T(S::w(0));
     const T eq0 = w0 * drho - w0 * rho * uu15;
-    // <P_k, g - g_eq> / N_k for the 15 non-conserved weighted-orthogonal polynomials, accumulated
-    // pair by pair so that only a[] stays live (the KBC needs g_eq and the parts twice; both are
-    // recomputed per pair below instead of being kept in registers)
-    T a[15];
-    {
-        const T d0 = g[0] - eq0;
-#pragma unroll
-        for (int k = 0; k < 15; ++k) {
-            const int c0 = mrt_poly(k, 0, 0, 0);
-            a[k] = (k >= 6 && k <= 11) || c0 == 0 ? T(0) : T(c0) * d0;
-        }
-    }
+    // g <- d = g - g_eq; shear coefficients a_k = <P_k, d> / N_k from the pair sums
+    g[0] -= eq0;
+    T a[5] = {T(0), T(0), T(0), T(0), T(0)};
 #pragma unroll
     for (int q = 1; q < 19; ++q) {
         if (q < S::opp(q)) {
@@ -333,60 +327,66 @@ __device__ __forceinline__ void collide_kbc19(T (&g)[19], const Rates<T> &p) {
             const T wr = w * rho;
             const T es = w * drho + wr * (T(4.5) * cu * cu - uu15);
             const T ea = wr * T(3) * cu;
-            const T dp = (g[q] + g[b]) - T(2) * es;
-            const T dm = (g[q] - g[b]) - T(2) * ea;
+            g[q] -= es + ea;
+            g[b] -= es - ea;
+            const T dp = g[q] + g[b];
 #pragma unroll
-            for (int k = 0; k < 15; ++k) {
+            for (int k = 0; k < 5; ++k) {
                 const int c = mrt_poly(k, S::cx(q), S::cy(q), S::cz(q));
-                const T v = (k >= 6 && k <= 11) ? dm : dp;
-                if (c == 1) a[k] += v;
-                else if (c == -1) a[k] -= v;
-                else if (c != 0) a[k] += T(c) * v;
+                if (c == 1) a[k] += dp;
+                else if (c == -1) a[k] -= dp;
+                else if (c != 0) a[k] += T(c) * dp;
             }
         }
     }
 #pragma unroll
-    for (int k = 0; k < 15; ++k) a[k] *= T(mrt_inv_norm(k));
-    // pass 1: entropic products <Ds,Dh>_E and <Dh,Dh>_E (f_eq = w + g_eq)
-    T s0, he0, ho0;
-    kbc_pair_parts<T>(a, 0, 0, 0, s0, he0, ho0);
-    const T ds0 = w0 * s0, dh0 = w0 * he0;
-    T sh, hh;
-    {
-        const T ief0 = T(1) / (w0 + eq0);
-        sh = ds0 * dh0 * ief0;
-        hh = dh0 * dh0 * ief0;
-    }
+    for (int k = 0; k < 5; ++k) a[k] *= T(mrt_inv_norm(k));
+    // entropic products <Ds,Dh>_E, <Dh,Dh>_E with <x,y>_E = sum x y / f_eq, f_eq = w + g_eq (Eq. 19)
+    T sh = T(0), hh = g[0] * g[0] / (w0 + eq0);
+    T ds[19];
 #pragma unroll
     for (int q = 1; q < 19; ++q) {
         if (q < S::opp(q)) {
+            const int b = S::opp(q);
             const T w = T(S::w(q));
+            T acc = T(0);
+#pragma unroll
+            for (int k = 0; k < 5; ++k) {
+                const int c = mrt_poly(k, S::cx(q), S::cy(q), S::cz(q));
+                if (c == 1) acc += a[k];
+                else if (c == -1) acc -= a[k];
+                else if (c != 0) acc += T(c) * a[k];
+            }
+            const T s = w * acc;
+            ds[q] = s;
             const T cu = T(S::cx(q)) * ux + T(S::cy(q)) * uy + T(S::cz(q)) * uz;
             const T wr = w * rho;
             const T es = w * drho + wr * (T(4.5) * cu * cu - uu15);
             const T ea = wr * T(3) * cu;
-            T s, he, ho;
-            kbc_pair_parts<T>(a, S::cx(q), S::cy(q), S::cz(q), s, he, ho);
             const T iq = T(1) / (w + es + ea);
             const T ib = T(1) / (w + es - ea);
-            const T hq = w * (he + ho), hb = w * (he - ho);
-            sh += w * s * (hq * iq + hb * ib);
+            const T hq = g[q] - s, hb = g[b] - s;
+            sh += s * (hq * iq + hb * ib);
             hh += hq * hq * iq + hb * hb * ib;
         }
     }
     const T ws = p.r[0];
     const T wh = hh > T(0) ? T(1) + (T(1) - ws) * sh / hh : T(1);
-    // pass 2: f' = f - w_s Ds - w_h Dh
-    g[0] -= ws * ds0 + wh * dh0;
+    // f' = f_eq + (1 - w_h) d + (w_h - w_s) Ds
+    const T kd = T(1) - wh, ks = wh - ws;
+    g[0] = eq0 + kd * g[0];
 #pragma unroll
     for (int q = 1; q < 19; ++q) {
         if (q < S::opp(q)) {
             const int b = S::opp(q);
             const T w = T(S::w(q));
-            T s, he, ho;
-            kbc_pair_parts<T>(a, S::cx(q), S::cy(q), S::cz(q), s, he, ho);
-            g[q] -= w * (ws * s + wh * (he + ho));
-            g[b] -= w * (ws * s + wh * (he - ho));
+            const T cu = T(S::cx(q)) * ux + T(S::cy(q)) * uy + T(S::cz(q)) * uz;
+            const T wr = w * rho;
+            const T es = w * drho + wr * (T(4.5) * cu * cu - uu15);
+            const T ea = wr * T(3) * cu;
+            const T sk = ks * ds[q];
+            g[q] = (es + ea) + kd * g[q] + sk;
+            g[b] = (es - ea) + kd * g[b] + sk;
         }
     }
 }
