@@ -46,7 +46,11 @@ class _Cfg(C.Structure):
                 ("zghost", C.c_int32), ("nthreads", C.c_int32),
                 ("rates", C.c_double * 8), ("force", C.c_double * 3),
                 ("ubb_u", C.c_double * 3), ("ubb_rho", C.c_double),
-                ("M", C.c_void_p), ("Minv", C.c_void_p), ("S", C.c_void_p)]
+                ("M", C.c_void_p), ("Minv", C.c_void_p), ("S", C.c_void_p),
+                ("eq_kind", C.c_int32), ("mono_exp", C.c_void_p), ("Mmono_inv", C.c_void_p)]
+
+
+EQ_KINDS = {"compressible": 0, "incompressible": 1, "moment_matched": 2}
 
 
 _lib = None
@@ -71,6 +75,7 @@ def lib():
             ("ora_smagorinsky_omega_cell", [P, P], C.c_double),
             ("ora_equilibrium_cell", [C.c_int, C.c_double, P, P], None),
             ("ora_product_equilibrium_cell", [C.c_int, C.c_double, P, P], None),
+            ("ora_equilibrium_kind_cell", [P, C.c_double, P, P], None),
             ("ora_cumulants_cell", [C.c_int, P, P], C.c_double),
             ("ora_from_cumulants_cell", [C.c_int, C.c_double, P, P], None),
             ("ora_pull_cell", [P, P, P, C.c_int64, C.c_int64, C.c_int64, P], None),
@@ -109,7 +114,23 @@ class Method:
     ubb_rho: float = 1.0
     mrt_weighted: bool = True
     nthreads: int = 0
+    equilibrium: str = "compressible"  # | "incompressible" (rho0 = 1) | "moment_matched"
     _mats: tuple = field(default=None, repr=False)
+    _mono: tuple = field(default=None, repr=False)
+
+    def monomial_tables(self):
+        """Exponents of the monomial moment basis and the exact inverse of its moment
+        matrix, for the moment-matched equilibrium."""
+        if self._mono is None:
+            name = f"D3Q{self.Q}"
+            basis = methods.monomial_basis(name)
+            assert all(len(p) == 1 for p in basis), "D3Q19/D3Q27 monomial bases are single monomials"
+            exps = [next(iter(p)) for p in basis]
+            Mr = methods.moment_matrix(basis, methods.stencil(name))
+            Minv = methods.mat_inverse(Mr)
+            self._mono = (np.array(exps, dtype=np.int32),
+                          np.array([[float(v) for v in row] for row in Minv]))
+        return self._mono
 
     def mrt_matrices(self):
         """M (rows = weighted-orthogonal moment polynomials), M^-1 (exact) and S (Eq. 4)."""
@@ -162,6 +183,11 @@ class Domain:
             M, Minv, S = method.mrt_matrices()
             self._keep = [np.ascontiguousarray(M), np.ascontiguousarray(Minv), np.ascontiguousarray(S)]
             cfg.M, cfg.Minv, cfg.S = (_p(a) for a in self._keep)
+        cfg.eq_kind = EQ_KINDS[method.equilibrium]
+        if method.equilibrium == "moment_matched":
+            exps, minv = method.monomial_tables()
+            self._keep += [np.ascontiguousarray(exps), np.ascontiguousarray(minv)]
+            cfg.mono_exp, cfg.Mmono_inv = _p(self._keep[-2]), _p(self._keep[-1])
         self.cfg = cfg
 
     # -- allocation ------------------------------------------------------------------
@@ -264,6 +290,15 @@ def equilibrium_cell(Q: int, rho: float, u) -> np.ndarray:
     u = np.ascontiguousarray(u, np.float64)
     out = np.zeros(Q)
     lib().ora_equilibrium_cell(Q, rho, _p(u), _p(out))
+    return out
+
+
+def equilibrium_kind_cell(method: Method, rho: float, u) -> np.ndarray:
+    """Equilibrium of `method.equilibrium`'s kind at (rho, u)."""
+    d = Domain(method, 1, 1, 1)
+    u = np.ascontiguousarray(u, np.float64)
+    out = np.zeros(method.Q)
+    lib().ora_equilibrium_kind_cell(d._pc(), rho, _p(u), _p(out))
     return out
 
 

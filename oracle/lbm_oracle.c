@@ -56,7 +56,15 @@ typedef struct {
     const double *Minv; /* MRT: its inverse */
     const double *S;    /* MRT: Q relaxation rates (diagonal of S); KBC: per-row part, 0 conserved,
                            1 = shear (s), 2 = higher order (h) */
+    int32_t eq_kind;    /* ORA_EQ_*: which equilibrium SRT/TRT/MRT relax to */
+    const int32_t *mono_exp;  /* ORA_EQ_MOMENT_MATCHED: Q x 3 exponents of the monomial basis */
+    const double *Mmono_inv;  /* ... and the inverse of its moment matrix M_kq = c_q^e_k (row-major) */
 } ora_cfg;
+
+#define ORA_EQ_COMPRESSIBLE 0    /* Eq. (3) with rho0 = rho */
+#define ORA_EQ_INCOMPRESSIBLE 1  /* Eq. (3) with rho0 = 1 (He & Luo) */
+#define ORA_EQ_MOMENT_MATCHED 2  /* moments of the continuous Maxwellian Eq. (7)-(8), truncated at 2nd
+                                    order in u, mapped to populations with M^-1 */
 
 /* ------------------------------------------------------------------------------------ */
 /* Stencils (ordering G10: centre, then |c|_1, then lexicographic -1<0<1).     */
@@ -122,17 +130,23 @@ void ora_stencil(int Q, int *c_out, double *w_out, int *opp_out) {
 /* Macroscopic values Eq. (2) and equilibrium Eq. (3).                                     */
 /* ------------------------------------------------------------------------------------ */
 
-/* rho = sum_q f_q; u = (sum_q c_q f_q + fsign * F/2) / rho (compressible rho0 = rho).
- * fsign = +1 for a pre-collision state (Guo), -1 for a post-collision state (G11). */
-static void macroscopic(const ora_stencil_t *s, const double *f, const double *F, double fsign,
-                        double *rho, double u[3]) {
+/* Eq. (2): rho = sum_q f_q; u = (sum_q c_q f_q + fsign * F/2) / rho0 with rho0 = rho (compressible)
+ * or rho0 = 1 (incompressible). fsign = +1 for a pre-collision state (Guo), -1 for a
+ * post-collision state (G11). */
+static void macroscopic_eq(const ora_stencil_t *s, const double *f, const double *F, double fsign, int incompressible,
+                           double *rho, double u[3]) {
     double r = 0.0, j[3] = {0.0, 0.0, 0.0};
     for (int q = 0; q < s->Q; ++q) {
         r += f[q];
         for (int d = 0; d < 3; ++d) j[d] += s->c[q][d] * f[q];
     }
-    for (int d = 0; d < 3; ++d) u[d] = (j[d] + fsign * 0.5 * F[d]) / r;
+    double rho0 = incompressible ? 1.0 : r;
+    for (int d = 0; d < 3; ++d) u[d] = (j[d] + fsign * 0.5 * F[d]) / rho0;
     *rho = r;
+}
+static void macroscopic(const ora_stencil_t *s, const double *f, const double *F, double fsign,
+                        double *rho, double u[3]) {
+    macroscopic_eq(s, f, F, fsign, 0, rho, u);
 }
 
 /* Eq. (3), second order, compressible: f_eq = w rho [1 + c.u/cs2 + (c.u)^2/(2 cs4) - u.u/(2 cs2)]
@@ -151,6 +165,63 @@ static void equilibrium(const ora_stencil_t *s, double rho, const double u[3], d
     }
     (void)uu;
 }
+
+/* Eq. (3), second order, with reference density rho0: f_eq = w rho + w rho0 [c.u/cs2 +
+ * u_a u_b (c_a c_b - cs2 delta_ab) / (2 cs4)]. rho0 = rho gives equilibrium() above. */
+static void equilibrium_rho0(const ora_stencil_t *s, double rho, double rho0, const double u[3], double *feq) {
+    const double cs2 = 1.0 / 3.0;
+    for (int q = 0; q < s->Q; ++q) {
+        double cu = s->c[q][0] * u[0] + s->c[q][1] * u[1] + s->c[q][2] * u[2];
+        double second = 0.0;
+        for (int a = 0; a < 3; ++a)
+            for (int b = 0; b < 3; ++b)
+                second += u[a] * u[b] * (s->c[q][a] * s->c[q][b] - (a == b ? cs2 : 0.0));
+        second /= 2.0 * cs2 * cs2;
+        feq[q] = s->w[q] * rho + s->w[q] * rho0 * (cu / cs2 + second);
+    }
+}
+
+/* Moment-matched equilibrium: the raw moment of basis monomial x^a y^b z^c of the
+ * continuous Maxwellian Eq. (7) is rho prod_d mu_{e_d}(u_d) with mu_0 = 1, mu_1 = u, mu_2 = cs2 + u^2
+ * (the Gaussian factorises over the axes); the product is expanded in powers of u and truncated after
+ * 2nd order ("Optionally the moments can be truncated to a given order in u"); the
+ * populations are M^-1 m_eq. */
+static void equilibrium_moment_matched(const ora_cfg *cfg, const ora_stencil_t *s, double rho, const double u[3],
+                                       double *feq) {
+    const double cs2 = 1.0 / 3.0;
+    double m[27];
+    for (int k = 0; k < s->Q; ++k) {
+        /* factor d as coefficients of u_d^0, u_d^1, u_d^2 */
+        double fac[3][3];
+        for (int d = 0; d < 3; ++d) {
+            int e = cfg->mono_exp[3 * k + d];
+            fac[d][0] = (e == 0) ? 1.0 : (e == 2) ? cs2 : 0.0;
+            fac[d][1] = (e == 1) ? u[d] : 0.0;
+            fac[d][2] = (e == 2) ? u[d] * u[d] : 0.0;
+        }
+        double v = 0.0;
+        for (int i = 0; i < 3; ++i)
+            for (int j = 0; j < 3; ++j)
+                for (int l = 0; l < 3; ++l)
+                    if (i + j + l <= 2) v += fac[0][i] * fac[1][j] * fac[2][l];
+        m[k] = rho * v;
+    }
+    for (int q = 0; q < s->Q; ++q) {
+        double v = 0.0;
+        for (int k = 0; k < s->Q; ++k) v += cfg->Mmono_inv[q * s->Q + k] * m[k];
+        feq[q] = v;
+    }
+}
+
+/* The equilibrium of the configured kind (cfg->eq_kind). */
+static void equilibrium_cfg(const ora_cfg *cfg, const ora_stencil_t *s, double rho, const double u[3], double *feq) {
+    switch (cfg->eq_kind) {
+        case ORA_EQ_INCOMPRESSIBLE: equilibrium_rho0(s, rho, 1.0, u, feq); break;
+        case ORA_EQ_MOMENT_MATCHED: equilibrium_moment_matched(cfg, s, rho, u, feq); break;
+        default: equilibrium(s, rho, u, feq); break;
+    }
+}
+static int incompressible(const ora_cfg *cfg) { return cfg->eq_kind == ORA_EQ_INCOMPRESSIBLE; }
 
 /* Product equilibrium (G2): the fixed point of the cumulant collision for D3Q27,
  * prod_axes p(c_i; u_i), p(+-1) = (1/3 + u^2 +- u)/2, p(0) = 2/3 - u^2. */
@@ -188,8 +259,8 @@ static int has_force(const ora_cfg *cfg) {
 static void collide_srt(const ora_cfg *cfg, const ora_stencil_t *s, const double *f, double *out) {
     double rho, u[3], feq[27];
     double w = cfg->rates[0];
-    macroscopic(s, f, cfg->force, +1.0, &rho, u);
-    equilibrium(s, rho, u, feq);
+    macroscopic_eq(s, f, cfg->force, +1.0, incompressible(cfg), &rho, u);
+    equilibrium_cfg(cfg, s, rho, u, feq);
     for (int q = 0; q < s->Q; ++q) {
         out[q] = w * feq[q] + (1.0 - w) * f[q];
         if (has_force(cfg)) out[q] += guo_source(s, q, u, cfg->force, w, w);
@@ -200,8 +271,8 @@ static void collide_srt(const ora_cfg *cfg, const ora_stencil_t *s, const double
 static void collide_trt(const ora_cfg *cfg, const ora_stencil_t *s, const double *f, double *out) {
     double rho, u[3], feq[27];
     double we = cfg->rates[0], wo = cfg->rates[1];
-    macroscopic(s, f, cfg->force, +1.0, &rho, u);
-    equilibrium(s, rho, u, feq);
+    macroscopic_eq(s, f, cfg->force, +1.0, incompressible(cfg), &rho, u);
+    equilibrium_cfg(cfg, s, rho, u, feq);
     for (int q = 0; q < s->Q; ++q) {
         int qb = s->opp[q];
         double fp = 0.5 * (f[q] + f[qb]), fm = 0.5 * (f[q] - f[qb]);
@@ -215,8 +286,8 @@ static void collide_trt(const ora_cfg *cfg, const ora_stencil_t *s, const double
 static void collide_mrt(const ora_cfg *cfg, const ora_stencil_t *s, const double *f, double *out) {
     int Q = s->Q;
     double rho, u[3], feq[27], m[27], meq[27], mp[27];
-    macroscopic(s, f, cfg->force, +1.0, &rho, u);
-    equilibrium(s, rho, u, feq);
+    macroscopic_eq(s, f, cfg->force, +1.0, incompressible(cfg), &rho, u);
+    equilibrium_cfg(cfg, s, rho, u, feq);
     for (int k = 0; k < Q; ++k) {
         m[k] = 0.0;
         meq[k] = 0.0;
@@ -647,7 +718,7 @@ int ora_init_equilibrium(const ora_cfg *cfg, const double *rho, const double *u,
                 int64_t i = (z * cfg->ny + y) * cfg->nx + x;
                 double uu[3] = {u[i], u[n + i], u[2 * n + i]}, feq[27];
                 if (cfg->op == ORA_CUMULANT) product_equilibrium(&s, rho[i], uu, feq);
-                else equilibrium(&s, rho[i], uu, feq);
+                else equilibrium_cfg(cfg, &s, rho[i], uu, feq);
                 int64_t self = cell(cfg, x, y, z);
                 for (int q = 0; q < s.Q; ++q) f[q * Sq + self] = feq[q];
             }
@@ -666,7 +737,7 @@ int ora_macroscopic(const ora_cfg *cfg, const double *f, double fsign, double *r
                 int64_t i = (z * cfg->ny + y) * cfg->nx + x, self = cell(cfg, x, y, z);
                 double fc[27], r, uu[3];
                 for (int q = 0; q < s.Q; ++q) fc[q] = f[q * Sq + self];
-                macroscopic(&s, fc, cfg->force, fsign, &r, uu);
+                macroscopic_eq(&s, fc, cfg->force, fsign, incompressible(cfg), &r, uu);
                 rho[i] = r;
                 u[i] = uu[0]; u[n + i] = uu[1]; u[2 * n + i] = uu[2];
             }
@@ -693,6 +764,12 @@ void ora_equilibrium_cell(int Q, double rho, const double *u, double *feq) {
     ora_stencil_t s;
     build_stencil(Q, &s);
     equilibrium(&s, rho, u, feq);
+}
+/* The equilibrium of cfg's kind (Eq. 3 compressible / incompressible, or moment-matched). */
+void ora_equilibrium_kind_cell(const ora_cfg *cfg, double rho, const double *u, double *feq) {
+    ora_stencil_t s;
+    build_stencil(cfg->Q, &s);
+    equilibrium_cfg(cfg, &s, rho, u, feq);
 }
 void ora_product_equilibrium_cell(int Q, double rho, const double *u, double *feq) {
     ora_stencil_t s;

@@ -25,7 +25,8 @@ def to_fr(x: float) -> Fr:
 
 
 class Exact:
-    def __init__(self, Q: int, op: str, rates: Sequence, force=(0, 0, 0), ubb_u=(0, 0, 0)):
+    def __init__(self, Q: int, op: str, rates: Sequence, force=(0, 0, 0), ubb_u=(0, 0, 0), equilibrium="compressible"):
+        self.equilibrium = equilibrium
         self.name = f"D3Q{Q}"
         self.dirs = methods.stencil(self.name)
         self.w = methods.weights(self.name)
@@ -50,15 +51,31 @@ class Exact:
     def macro(self, f):
         rho = sum(f, Fr(0))
         j = [sum((c[d] * fq for c, fq in zip(self.dirs, f)), Fr(0)) for d in range(3)]
-        u = [(j[d] + self.F[d] / 2) / rho for d in range(3)]
+        rho0 = Fr(1) if self.equilibrium == "incompressible" else rho  # Eq. (2)
+        u = [(j[d] + self.F[d] / 2) / rho0 for d in range(3)]
         return rho, u
 
     def feq(self, rho, u):
         out = []
         uu = sum(v * v for v in u)
+        rho0 = Fr(1) if self.equilibrium == "incompressible" else rho
         for c, w in zip(self.dirs, self.w):
             cu = sum(c[d] * u[d] for d in range(3))
-            out.append(w * rho * (1 + 3 * cu + Fr(9, 2) * cu * cu - Fr(3, 2) * uu))
+            out.append(w * rho + w * rho0 * (3 * cu + Fr(9, 2) * cu * cu - Fr(3, 2) * uu))
+        if self.equilibrium == "moment_matched" and self.Q == 19:
+            # hand-derived correction (independent of the oracle's M^-1 route): the Maxwellian x^2 y^2
+            # moment truncated at 2nd order is rho (cs^4 + cs^2 (ux^2 + uy^2)), Eq. (3) gives
+            # rho/9 + rho (ux^2 + uy^2)/3 - rho uz^2/6; the 4 xy-edges carry +rho uz^2/24 each (and
+            # cyclically), the faces -2 (a + b) so that orders 0-3 are unchanged, the centre 4 (a + b + c).
+            a = {2: rho * u[2] ** 2 / 24, 1: rho * u[1] ** 2 / 24, 0: rho * u[0] ** 2 / 24}  # keyed by the zero axis
+            for q, c in enumerate(self.dirs):
+                nz = [d for d in range(3) if c[d] != 0]
+                if len(nz) == 2:
+                    out[q] += a[3 - nz[0] - nz[1]]
+                elif len(nz) == 1:
+                    out[q] += -2 * sum(a[k] for k in range(3) if k != nz[0])
+                else:
+                    out[q] += 4 * (a[0] + a[1] + a[2])
         return out
 
     def guo(self, q, u, we, wo):
