@@ -69,6 +69,16 @@ for _name, _op, _q, _rates in [("trt", "trt", 19, (1.6, 0.5)), ("smagorinsky", "
                                   job_steps=200)
 
 
+# Equilibrium variants: C4's D3Q19 TRT fp64 512^3 pull with the incompressible
+# and the moment-matched equilibria; C2's MRT fp32 AA with the incompressible one.
+CONFIGS["eq_inc_c4"] = dict(CONFIGS["c4"], equilibrium="incompressible",
+                            desc="D3Q19 TRT fp64 512^3 periodic, incompressible Eq. (3) (rho0 = 1)")
+CONFIGS["eq_mm_c4"] = dict(CONFIGS["c4"], equilibrium="moment_matched",
+                           desc="D3Q19 TRT fp64 512^3 periodic, moment-matched equilibrium")
+CONFIGS["eq_inc_c2"] = dict(CONFIGS["c2"], equilibrium="incompressible",
+                            desc="D3Q19 weighted MRT fp32 AA 512^3 shear wave, incompressible Eq. (3)")
+
+
 def flags_for(cfg, shape):
     import lbminputs as LI
     nx, ny, nz = shape
@@ -164,6 +174,7 @@ def oracle_sample(cfg, target_s=15.0, max_steps=None):
     nx, ny, nz = cfg["shape"]
     threads = os.cpu_count() or 1
     m = O.Method(Q=cfg["Q"], op=cfg["op"], rates=cfg["rates"], force=cfg["force"], ubb_u=cfg.get("ubb", (0, 0, 0)),
+                 equilibrium=cfg.get("equilibrium", "compressible"),
                  nthreads=threads)
     per_cell = 1.0 / (2.0e6 if cfg["op"] in ("srt", "trt") else 0.6e6 if cfg["op"] == "mrt" else 0.17e6)
     planes = max(2, min(nz, int(target_s / (per_cell * nx * ny * 2))))
@@ -195,6 +206,7 @@ def run_reference(args, cfg):
     nx, ny, nz = cfg["shape"]
     threads = os.cpu_count() or 1
     m = O.Method(Q=cfg["Q"], op=cfg["op"], rates=cfg["rates"], force=cfg["force"], ubb_u=cfg.get("ubb", (0, 0, 0)),
+                 equilibrium=cfg.get("equilibrium", "compressible"),
                  nthreads=threads)
     # each reference step = one pull step of a sub-slab with one z plane per host thread (the
     # oracle parallelises over z), a bounded sample of the workload
@@ -295,7 +307,8 @@ def main():
                             pattern=cfg["pattern"], force=cfg["force"], flags=flags,
                             ubb_velocity=cfg.get("ubb", (0, 0, 0)), periodic=periodic, rank=rank, nranks=world,
                             nccl_id=nccl_id, device=local, stream=stream.cuda_stream, halo_mode=mode,
-                            use_graph=use_graph, block_x=args.block_x, nccl_self=nccl_self)
+                            use_graph=use_graph, block_x=args.block_x, nccl_self=nccl_self,
+                            equilibrium=cfg.get("equilibrium", "compressible"))
 
     sim, err = None, None
     try:

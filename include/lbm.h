@@ -79,6 +79,17 @@ extern "C" {
 #define LBM_HOST 0   /* pointer argument is host memory   */
 #define LBM_DEVICE 1 /* pointer argument is device memory */
 
+/* Equilibrium of SRT/TRT/MRT:
+ * COMPRESSIBLE   Eq. (3), 2nd order, rho0 = rho; u = j / rho (G1; default)
+ * INCOMPRESSIBLE Eq. (3) with rho0 = 1 (He & Luo): u = j (Eq. 2), f_eq = w rho + w [3 c.u + ...];
+ *                macroscopic readout then reports u = j +- F/2
+ * MOMENT_MATCHED the raw moments of the basis monomials are those of the continuous Maxwellian
+ *                Eq. (7)-(8) truncated at 2nd order in u: differs from Eq. (3) for D3Q19 in
+ *                the three x^2 y^2-type moments (by rho u_k^2 / 6), identical for D3Q27 */
+#define LBM_EQ_COMPRESSIBLE 0
+#define LBM_EQ_INCOMPRESSIBLE 1
+#define LBM_EQ_MOMENT_MATCHED 2
+
 #define LBM_HALO_ZEROCOPY 0 /* one NCCL message per crossing population plane */
 #define LBM_HALO_PACKED 1   /* pack kernel + one message per face            */
 #define LBM_HALO_FUSED 2    /* pull + NCCL ranks: the boundary-plane kernel stores crossing
@@ -114,6 +125,8 @@ typedef struct lbm_config {
     int32_t nccl_self;      /* nranks == 1 only: keep ghost planes and exchange them through a
                                1-rank NCCL communicator (self send/recv) instead of wrapping z
                                locally — exercises and times the multi-GPU exchange path on 1 GPU */
+    int32_t equilibrium;    /* LBM_EQ_*: what SRT/TRT/MRT relax to (and what lbm_init_equilibrium writes);
+                               other operators require LBM_EQ_COMPRESSIBLE (LBM_EUNSUPPORTED) */
 } lbm_config;
 
 typedef struct lbm_handle_s *lbm_handle;
@@ -217,6 +230,7 @@ typedef struct lbm_kernel_args {
     double force[3];
     double ubb_velocity[3];
     void *stream;         /* cudaStream_t */
+    int32_t equilibrium;  /* LBM_EQ_* (SRT/TRT/MRT) */
 } lbm_kernel_args;
 
 /* Fused stream-pull-collide: dst = C(S(src)) on the fluid cells of planes [z_begin, z_end). */

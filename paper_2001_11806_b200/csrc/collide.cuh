@@ -18,6 +18,31 @@
 
 namespace lbm {
 
+// Operator template parameter: low 4 bits = collision (enum Op below), bits 4-5 = equilibrium
+// variant (EQ_*): Eq. (3) compressible (rho0 = rho), incompressible (rho0 = 1), or the
+// moment-matched D3Q19 equilibrium (identical to Eq. (3) for D3Q27).
+enum EqKind { EQ_COMPRESSIBLE = 0, EQ_INCOMPRESSIBLE = 1, EQ_MOMENT_MATCHED = 2 };
+__host__ __device__ constexpr int op_base(int op) { return op & 15; }
+__host__ __device__ constexpr int op_eq(int op) { return op >> 4; }
+__host__ __device__ constexpr int op_with_eq(int op, int eq) { return op | (eq << 4); }
+
+// Moment-matched correction of the symmetric equilibrium part of direction q (D3Q19; zero for
+// D3Q27): the 2nd-order-truncated Maxwellian x^2 y^2 moment exceeds Eq. (3)'s by rho u_z^2 / 6
+// (and cyclically); the correction that fixes the three order-4 moments and leaves orders 0-3
+// unchanged puts rho u_k^2 / 24 on each edge in the plane normal to axis k, -rho (u^2 - u_k^2) / 12
+// on the two faces along axis k and rho u^2 / 6 on the centre (derivation; pinned by the
+// oracle's M^-1 route in tests/test_bruteforce.py).
+template <int Q, typename T>
+__device__ __forceinline__ T mm_delta(int q, T rho, T ux, T uy, T uz) {
+    if (Q != 19) return T(0);
+    const int cx = kC27[q][0], cy = kC27[q][1], cz = kC27[q][2];
+    const int n = cx * cx + cy * cy + cz * cz;
+    const T r24 = rho * T(1.0 / 24.0);
+    if (n == 2) return r24 * (cx == 0 ? ux * ux : cy == 0 ? uy * uy : uz * uz);
+    if (n == 1) return T(-2) * r24 * (cx != 0 ? uy * uy + uz * uz : cy != 0 ? ux * ux + uz * uz : ux * ux + uy * uy);
+    return T(4) * r24 * (ux * ux + uy * uy + uz * uz);
+}
+
 template <typename T>
 struct Rates {
     T r[8];
@@ -49,14 +74,15 @@ __device__ __forceinline__ void moments0(const T (&g)[Q], T &drho, T &jx, T &jy,
 // ---------------------------------------------------------------------------------------
 // TRT (+ Guo). SRT passes we == wo.
 // ---------------------------------------------------------------------------------------
-template <int Q, typename T, bool FORCE>
+template <int Q, typename T, bool FORCE, int EQ = EQ_COMPRESSIBLE>
 __device__ __forceinline__ void collide_trt(T (&g)[Q], const Rates<T> &p) {
     using S = Stencil<Q>;
     const T we = p.r[0], wo = p.r[1];
     T drho, jx, jy, jz;
     moments0<Q, T>(g, drho, jx, jy, jz);
     const T rho = T(1) + drho;
-    const T inv = T(1) / rho;
+    const T rho0 = EQ == EQ_INCOMPRESSIBLE ? T(1) : rho;  // reference density of Eq. (2)/(3)
+    const T inv = EQ == EQ_INCOMPRESSIBLE ? T(1) : T(1) / rho;
     T ux, uy, uz;
     if (FORCE) {
         ux = (jx + T(0.5) * p.F[0]) * inv;
@@ -73,7 +99,8 @@ __device__ __forceinline__ void collide_trt(T (&g)[Q], const Rates<T> &p) {
     if (FORCE) uF3 = T(3) * (ux * p.F[0] + uy * p.F[1] + uz * p.F[2]);
     {  // centre
         const T w0 = T(S::w(0));
-        const T eq = w0 * drho - w0 * rho * uu15;
+        T eq = w0 * drho - w0 * rho0 * uu15;
+        if (EQ == EQ_MOMENT_MATCHED) eq += mm_delta<Q, T>(0, rho, ux, uy, uz);
         g[0] = g[0] - we * (g[0] - eq);
         if (FORCE) g[0] -= se * w0 * uF3;
     }
@@ -85,8 +112,9 @@ __device__ __forceinline__ void collide_trt(T (&g)[Q], const Rates<T> &p) {
             const int b = S::opp(q);
             const T w = T(S::w(q));
             const T cu = T(S::cx(q)) * ux + T(S::cy(q)) * uy + T(S::cz(q)) * uz;
-            const T wr = w * rho;
-            const T eqs = w * drho + wr * (T(4.5) * cu * cu - uu15);
+            const T wr = w * rho0;
+            T eqs = w * drho + wr * (T(4.5) * cu * cu - uu15);
+            if (EQ == EQ_MOMENT_MATCHED) eqs += mm_delta<Q, T>(q, rho, ux, uy, uz);
             const T eqa = wr * T(3) * cu;
             const T fp = T(0.5) * (g[q] + g[b]);
             const T fm = T(0.5) * (g[q] - g[b]);
@@ -152,20 +180,23 @@ __host__ __device__ constexpr int mrt_slot(int k) { return k <= 4 ? k : k == 5 ?
 // d = f - f_eq has no conserved part, so f - sum_g omega_g P_g d = f_eq + sum_g (1 - omega_g) P_g d.
 // A group relaxed with omega_g = 1 contributes nothing and is skipped by a uniform branch — the
 // run-time counterpart of the paper's pre-evaluation of constant relaxation rates.
-template <typename T>
+template <typename T, int EQ = EQ_COMPRESSIBLE>
 __device__ __forceinline__ void collide_mrt19(T (&g)[19], const Rates<T> &p) {
     using S = Stencil<19>;
     T drho, jx, jy, jz;
     moments0<19, T>(g, drho, jx, jy, jz);
     const T rho = T(1) + drho;
-    const T inv = T(1) / rho;
+    const T rho0 = EQ == EQ_INCOMPRESSIBLE ? T(1) : rho;
+    const T inv = EQ == EQ_INCOMPRESSIBLE ? T(1) : T(1) / rho;
     const T ux = jx * inv, uy = jy * inv, uz = jz * inv;
     const T uu15 = T(1.5) * (ux * ux + uy * uy + uz * uz);
     // Non-equilibrium part d = g - g_eq, split over the direction pairs (q, qbar): even moment
     // polynomials (shear, bulk, order 4) see only dp = d_q + d_qbar, odd ones (order 3) only
     // dm = d_q - d_qbar — half the work of the plain 15 x 19 transform. g is overwritten with g_eq.
     const T w0 = T(S::w(0));
-    const T d0 = g[0] - (w0 * drho - w0 * rho * uu15);
+    T eq0 = w0 * drho - w0 * rho0 * uu15;
+    if (EQ == EQ_MOMENT_MATCHED) eq0 += mm_delta<19, T>(0, rho, ux, uy, uz);
+    const T d0 = g[0] - eq0;
     g[0] -= d0;
     T dp[19], dm[19];
 #pragma unroll
@@ -174,8 +205,9 @@ __device__ __forceinline__ void collide_mrt19(T (&g)[19], const Rates<T> &p) {
             const int b = S::opp(q);
             const T w = T(S::w(q));
             const T cu = T(S::cx(q)) * ux + T(S::cy(q)) * uy + T(S::cz(q)) * uz;
-            const T wr = w * rho;
-            const T eqs = w * drho + wr * (T(4.5) * cu * cu - uu15);
+            const T wr = w * rho0;
+            T eqs = w * drho + wr * (T(4.5) * cu * cu - uu15);
+            if (EQ == EQ_MOMENT_MATCHED) eqs += mm_delta<19, T>(q, rho, ux, uy, uz);
             const T eqa = wr * T(3) * cu;
             dp[q] = (g[q] + g[b]) - T(2) * eqs;
             dm[q] = (g[q] - g[b]) - T(2) * eqa;
@@ -558,13 +590,16 @@ __device__ __forceinline__ void collide_cumulant27(T (&g)[27], const Rates<T> &p
 // ---------------------------------------------------------------------------------------
 enum Op { OP_SRT = 0, OP_TRT = 1, OP_MRT = 2, OP_CUMULANT = 3, OP_IDENTITY = 4, OP_SMAGORINSKY = 5, OP_KBC = 6 };
 
-template <int Q, int OP, typename T, bool FORCE>
+template <int Q, int OPX, typename T, bool FORCE>
 __device__ __forceinline__ void collide(T (&g)[Q], const Rates<T> &p) {
+    constexpr int OP = op_base(OPX), EQ = op_eq(OPX);
+    static_assert(EQ == EQ_COMPRESSIBLE || OP == OP_SRT || OP == OP_TRT || OP == OP_MRT,
+                  "equilibrium variants exist for SRT/TRT/MRT");
     if constexpr (OP == OP_SRT || OP == OP_TRT) {
-        collide_trt<Q, T, FORCE>(g, p);
+        collide_trt<Q, T, FORCE, EQ>(g, p);
     } else if constexpr (OP == OP_MRT) {
         static_assert(Q == 19, "MRT is implemented for D3Q19");
-        collide_mrt19<T>(g, p);
+        collide_mrt19<T, EQ>(g, p);
     } else if constexpr (OP == OP_CUMULANT) {
         static_assert(Q == 27, "cumulant is implemented for D3Q27");
         collide_cumulant27<T>(g, p);

@@ -31,9 +31,14 @@ Kernels select_cumulant(int Q, int dtype, int fm, bool force);
 Kernels select_identity(int Q, int dtype, int fm, bool force);
 Kernels select_smagorinsky(int Q, int dtype, int fm, bool force);
 Kernels select_kbc(int Q, int dtype, int fm, bool force);
+// equilibrium variants (EQ_INCOMPRESSIBLE / EQ_MOMENT_MATCHED of collide.cuh), k_eq_*.cu
+Kernels select_trt_eq(int Q, int dtype, int fm, bool force, int eq);
+Kernels select_mrt_eq(int Q, int dtype, int fm, bool force, int eq);
+Kernels select_trt_mm(int Q, int dtype, int fm, bool force);
+Kernels select_mrt_mm(int Q, int dtype, int fm, bool force);
 // Operator dispatch used by the handle API and the low-level kernel ABI (runtime.cu); SRT runs the
 // TRT kernel with equal rates.
-Kernels select_kernels(int collision, int Q, int dtype, int fm, bool force);
+Kernels select_kernels(int collision, int Q, int dtype, int fm, bool force, int eq = 0);
 
 // Auxiliary kernels (k_misc.cu), dispatched on (Q, dtype).
 void launch_init(int Q, int dtype, const InitArgs &a, void *f0, void *f1, dim3 grid, dim3 block, cudaStream_t s);

@@ -23,8 +23,9 @@
 // for sweeps only.
 namespace lbm {
 
-template <int Q, int OP, typename T>
+template <int Q, int OPX, typename T>
 struct MinBlocks {
+    static constexpr int OP = op_base(OPX);  // the equilibrium variant bits do not change the cap
     static constexpr bool f64 = sizeof(T) == 8;
     // OP: 0 SRT, 1 TRT, 2 MRT, 3 cumulant, 4 identity, 5 Smagorinsky, 6 KBC
     static constexpr int pull_default =
@@ -153,7 +154,7 @@ __device__ __forceinline__ void pull_cell(const StepArgs &a, const T *__restrict
     // issue back to back — the neighbour's storage always exists, wall or not — and the wall
     // directions are replaced afterwards) and branch-per-direction (fp32 TRT at 40 registers).
     constexpr bool kWalls = FM == FM_INLINE || FM == FM_EDGE;
-    constexpr bool kFixup = kWalls && (sizeof(T) == 8 || OP == OP_CUMULANT) && FM == FM_INLINE;
+    constexpr bool kFixup = kWalls && (sizeof(T) == 8 || op_base(OP) == OP_CUMULANT) && FM == FM_INLINE;
     T g[Q];
     if constexpr (kWalls && !kFixup) {
 #pragma unroll
@@ -400,6 +401,7 @@ struct InitArgs {
     double rho_amp, u_amp, profile_amp;
     int profile;
     int product_eq;            // cumulant: product equilibrium (G2)
+    int eq_kind;               // EQ_* of collide.cuh (SRT/TRT/MRT): Eq. (3) rho0 = rho / rho0 = 1 / moment-matched
 };
 
 __device__ __forceinline__ uint64_t splitmix64(uint64_t k) {
@@ -460,7 +462,9 @@ __global__ void k_init(const InitArgs a, T *__restrict__ f0, T *__restrict__ f1)
             gq = v - S::w(q);
         } else {
             const double cu = S::cx(q) * ux + S::cy(q) * uy + S::cz(q) * uz;
-            gq = S::w(q) * drho + S::w(q) * rho * (3.0 * cu + 4.5 * cu * cu - uu15);
+            const double rho0 = a.eq_kind == EQ_INCOMPRESSIBLE ? 1.0 : rho;
+            gq = S::w(q) * drho + S::w(q) * rho0 * (3.0 * cu + 4.5 * cu * cu - uu15);
+            if (a.eq_kind == EQ_MOMENT_MATCHED) gq += mm_delta<Q, double>(q, rho, ux, uy, uz);
         }
         f0[q * a.geo.Sq + self] = T(gq);
         if (f1) f1[q * a.geo.Sq + self] = T(gq);
@@ -479,6 +483,7 @@ struct ReadArgs {
     double F[3];
     const uint8_t *flags;  // AA odd gather with walls (same rule as k_aa_odd's reads)
     double uw[3];
+    int incompressible;    // u = (j +- F/2) / rho0 with rho0 = 1 instead of rho
 };
 
 template <int Q, typename T>
@@ -571,12 +576,13 @@ __global__ void k_macro(const ReadArgs a, const T *__restrict__ f, double *__res
         jz += S::cz(q) * v;
     }
     const double rho = 1.0 + drho;
+    const double rho0 = a.incompressible ? 1.0 : rho;
     const int64_t nc = (int64_t)a.geo.nx * a.geo.ny * a.geo.nz;
     const int64_t i = ((int64_t)zl * a.geo.ny + y) * a.geo.nx + x;
     rho_out[i] = rho;
-    u_out[i] = (jx + a.fsign * 0.5 * a.F[0]) / rho;
-    u_out[nc + i] = (jy + a.fsign * 0.5 * a.F[1]) / rho;
-    u_out[2 * nc + i] = (jz + a.fsign * 0.5 * a.F[2]) / rho;
+    u_out[i] = (jx + a.fsign * 0.5 * a.F[0]) / rho0;
+    u_out[nc + i] = (jy + a.fsign * 0.5 * a.F[1]) / rho0;
+    u_out[2 * nc + i] = (jz + a.fsign * 0.5 * a.F[2]) / rho0;
 }
 
 // =======================================================================================

@@ -433,6 +433,11 @@ int validate(const lbm_config *c) {
     if (c->collision == LBM_KBC && c->stencil != 19) return fail(nullptr, LBM_EUNSUPPORTED, "KBC is implemented for D3Q19");
     if (force && c->collision != LBM_SRT && c->collision != LBM_TRT)
         return fail(nullptr, LBM_EUNSUPPORTED, "forcing is implemented for SRT/TRT");
+    if (c->equilibrium < LBM_EQ_COMPRESSIBLE || c->equilibrium > LBM_EQ_MOMENT_MATCHED)
+        return fail(nullptr, LBM_EINVAL, "bad equilibrium");
+    if (c->equilibrium != LBM_EQ_COMPRESSIBLE && c->collision != LBM_SRT && c->collision != LBM_TRT &&
+        c->collision != LBM_MRT && c->collision != LBM_IDENTITY)
+        return fail(nullptr, LBM_EUNSUPPORTED, "equilibrium variants are implemented for SRT/TRT/MRT");
     // a non-periodic axis must carry wall cells on both faces
     for (int d = 0; d < 3; ++d) {
         if (c->periodic[d]) continue;
@@ -477,7 +482,13 @@ int64_t local_cells(const lbm_handle_s *h) {
 // C ABI
 // =========================================================================================
 namespace lbm {
-Kernels select_kernels(int collision, int Q, int dtype, int fm, bool force) {
+Kernels select_kernels(int collision, int Q, int dtype, int fm, bool force, int eq) {
+    if (eq == EQ_MOMENT_MATCHED && Q == 27) eq = EQ_COMPRESSIBLE;  // identical for D3Q27
+    if (eq != EQ_COMPRESSIBLE) {
+        if (collision == LBM_SRT || collision == LBM_TRT) return select_trt_eq(Q, dtype, fm, force, eq);
+        if (collision == LBM_MRT) return select_mrt_eq(Q, dtype, fm, force, eq);
+        if (collision != LBM_IDENTITY) return Kernels{};
+    }
     switch (collision) {
         case LBM_SRT:
         case LBM_TRT: return select_trt(Q, dtype, fm, force);
@@ -533,7 +544,8 @@ const char *lbm_last_error(lbm_handle h) { return h ? h->err.c_str() : g_create_
 
 static int kernel_args_common(const lbm_kernel_args *k, StepArgs &a, bool aa) {
     if (!k || (k->stencil != 19 && k->stencil != 27) || k->collision < 0 || k->collision > 6 ||
-        (k->dtype != LBM_F64 && k->dtype != LBM_F32) || !k->dst || (!aa && !k->src) || k->ghost < 0 || k->ghost > 1)
+        (k->dtype != LBM_F64 && k->dtype != LBM_F32) || !k->dst || (!aa && !k->src) || k->ghost < 0 || k->ghost > 1 ||
+        k->equilibrium < LBM_EQ_COMPRESSIBLE || k->equilibrium > LBM_EQ_MOMENT_MATCHED)
         return LBM_EINVAL;
     if (k->shape[0] < 1 || k->shape[1] < 1 || k->shape[2] < 1 || k->z_begin < 0 || k->z_end > k->shape[2] ||
         k->z_begin > k->z_end)
@@ -578,7 +590,7 @@ int lbm_kernel_pull(const lbm_kernel_args *k) {
     if (rc) return rc;
     const bool flags = k->flags != nullptr;
     const bool force = k->force[0] != 0 || k->force[1] != 0 || k->force[2] != 0;
-    const PullLaunch fn = select_kernels(k->collision, k->stencil, k->dtype, flags ? FM_INLINE : FM_NONE, force).pull;
+    const PullLaunch fn = select_kernels(k->collision, k->stencil, k->dtype, flags ? FM_INLINE : FM_NONE, force, k->equilibrium).pull;
     if (!fn) return LBM_EUNSUPPORTED;
     if (k->z_end == k->z_begin) return LBM_OK;
     const dim3 b = kernel_block(k->shape[0], k->shape[1]);
@@ -594,7 +606,7 @@ int lbm_kernel_aa(const lbm_kernel_args *k, int32_t odd) {
     if (rc) return rc;
     const bool flags = k->flags != nullptr;
     const bool force = k->force[0] != 0 || k->force[1] != 0 || k->force[2] != 0;
-    const AALaunch fn = select_kernels(k->collision, k->stencil, k->dtype, flags ? FM_INLINE : FM_NONE, force).aa;
+    const AALaunch fn = select_kernels(k->collision, k->stencil, k->dtype, flags ? FM_INLINE : FM_NONE, force, k->equilibrium).aa;
     if (!fn) return LBM_EUNSUPPORTED;
     if (k->z_end == k->z_begin) return LBM_OK;
     const dim3 b = kernel_block(k->shape[0], k->shape[1]);
@@ -705,10 +717,10 @@ int lbm_create(const lbm_config *cfg, lbm_handle *out) {
     // kernel selection (SRT = TRT with equal rates)
     const bool force = h->have_force;
     if (cfg->pattern == LBM_PULL) {
-        h->kern = select_kernels(cfg->collision, h->Q, h->dtype, h->have_flags ? FM_BULK : FM_NONE, force);
+        h->kern = select_kernels(cfg->collision, h->Q, h->dtype, h->have_flags ? FM_BULK : FM_NONE, force, cfg->equilibrium);
         if (!h->kern.pull) return fail(nullptr, LBM_EUNSUPPORTED, "no kernel instantiated for this combination");
     } else {
-        h->kern = select_kernels(cfg->collision, h->Q, h->dtype, h->have_flags ? FM_BULK : FM_NONE, force);
+        h->kern = select_kernels(cfg->collision, h->Q, h->dtype, h->have_flags ? FM_BULK : FM_NONE, force, cfg->equilibrium);
         if (!h->kern.aa) return fail(nullptr, LBM_EUNSUPPORTED, "no kernel instantiated for this combination");
     }
     // rates into the kernel argument block
@@ -928,6 +940,7 @@ static int init_common(lbm_handle h, InitArgs &a, const double *rho, const doubl
         b.ny_g = h->ny;
         b.nz_g = h->nzg;
         b.product_eq = h->op == LBM_CUMULANT;
+        b.eq_kind = h->cfg.equilibrium;
         if (a.mode == 0) {
             // the arrays cover the concatenated local slabs; ghost planes are filled by exchange
             b.rho = drho + off;
@@ -1084,6 +1097,7 @@ static int read_common(lbm_handle h, ReadArgs &r, int raw, const Slab &s) {
     r.raw = raw;
     r.aa_odd = (h->cfg.pattern == LBM_AA) && h->aa_parity;
     r.fsign = h->cfg.pattern == LBM_PULL ? -1.0 : 1.0;
+    r.incompressible = h->cfg.equilibrium == LBM_EQ_INCOMPRESSIBLE;
     for (int d = 0; d < 3; ++d) {
         r.F[d] = h->cfg.force[d];
         r.uw[d] = h->cfg.ubb_velocity[d];

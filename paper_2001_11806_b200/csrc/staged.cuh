@@ -40,8 +40,9 @@ __host__ __device__ constexpr bool sh_of(int mode) { return mode != SM_AA_EVEN; 
 constexpr int kStagedBT = LBM_STAGED_BT;
 
 // registers: 65536 / (BT * minBlocks); the heavy fp64 operators get more room
-template <int Q, int OP, typename T>
+template <int Q, int OPX, typename T>
 struct StagedMinBlocks {
+    static constexpr int OP = op_base(OPX);
     static constexpr bool heavy = sizeof(T) == 8 && (OP == OP_MRT || OP == OP_CUMULANT || OP == OP_KBC || OP == OP_SMAGORINSKY || Q == 27);
 #ifdef LBM_STAGED_MINB
     static constexpr int value = LBM_STAGED_MINB;
@@ -226,8 +227,9 @@ int staged_path();     // 0 auto, 1 plain, 2 staged (lbm_set_kernel_path / LBM_K
 // Auto policy, from B200 sweeps: the staged kernels win for the register-heavy
 // operators (MRT, KBC, Smagorinsky; the cumulant in the AA pattern), the plain kernels for TRT/SRT
 // (already at copy bandwidth) and the cumulant pull kernel.
-template <int Q, int OP, int MODE>
+template <int Q, int OPX, int MODE>
 constexpr bool staged_auto() {
+    constexpr int OP = op_base(OPX);
     return OP == OP_MRT || OP == OP_KBC || OP == OP_SMAGORINSKY || (OP == OP_CUMULANT && MODE != SM_PULL);
 }
 

@@ -28,6 +28,8 @@ FLUID, NOSLIP, UBB = 0, 1, 2
 HOST, DEVICE = 0, 1
 HALO_ZEROCOPY, HALO_PACKED, HALO_FUSED = 0, 1, 2
 PATH_AUTO, PATH_PLAIN, PATH_STAGED = 0, 1, 2
+EQ_COMPRESSIBLE, EQ_INCOMPRESSIBLE, EQ_MOMENT_MATCHED = 0, 1, 2
+EQUILIBRIA = {"compressible": EQ_COMPRESSIBLE, "incompressible": EQ_INCOMPRESSIBLE, "moment_matched": EQ_MOMENT_MATCHED}
 KERNEL_PATHS = {"auto": PATH_AUTO, "plain": PATH_PLAIN, "staged": PATH_STAGED}
 
 COLLISIONS = {"srt": SRT, "trt": TRT, "mrt": MRT, "cumulant": CUMULANT, "identity": IDENTITY,
@@ -45,6 +47,7 @@ class lbm_config(C.Structure):
         ("nccl_id", C.c_void_p), ("n_local_slabs", C.c_int32), ("device", C.c_int32),
         ("stream", C.c_void_p), ("halo_mode", C.c_int32), ("use_graph", C.c_int32),
         ("block_x", C.c_int32), ("check_nan_every", C.c_int32), ("nccl_self", C.c_int32),
+        ("equilibrium", C.c_int32),
     ]
 
 
@@ -54,7 +57,7 @@ class lbm_kernel_args(C.Structure):
         ("src", C.c_void_p), ("dst", C.c_void_p), ("flags", C.c_void_p),
         ("shape", C.c_int64 * 3), ("ghost", C.c_int32), ("z_begin", C.c_int64), ("z_end", C.c_int64),
         ("rates", C.c_double * 8), ("force", C.c_double * 3), ("ubb_velocity", C.c_double * 3),
-        ("stream", C.c_void_p),
+        ("stream", C.c_void_p), ("equilibrium", C.c_int32),
     ]
 
 
@@ -183,7 +186,7 @@ class Simulation:
                  rank: int = 0, nranks: int = 1, nccl_id: Optional[bytes] = None,
                  n_local_slabs: int = 1, device: int = 0, stream: Optional[int] = None,
                  halo_mode: int = HALO_ZEROCOPY, use_graph: bool = False, block_x: int = 0,
-                 check_nan_every: int = 0, nccl_self: bool = False):
+                 check_nan_every: int = 0, nccl_self: bool = False, equilibrium: str = "compressible"):
         cfg = lbm_config()
         lbm_config_default(C.byref(cfg))
         nx, ny, nz = shape
@@ -217,6 +220,7 @@ class Simulation:
         cfg.block_x = block_x
         cfg.check_nan_every = check_nan_every
         cfg.nccl_self = int(nccl_self)
+        cfg.equilibrium = EQUILIBRIA[equilibrium] if isinstance(equilibrium, str) else int(equilibrium)
         self.cfg = cfg
         self.Q = stencil
         h = C.c_void_p()

@@ -30,6 +30,7 @@ class Case:
     u_amp: float = 0.01
     steps: int = 10
     seed: int = 0
+    equilibrium: str = "compressible"  # | incompressible | moment_matched (SRT/TRT/MRT)
     extra: dict = field(default_factory=dict)
 
     def flags(self) -> Optional[np.ndarray]:
@@ -58,14 +59,15 @@ class Case:
         return (LI.PROFILE_SHEAR_WAVE, 0.01) if self.init == "shear" else (LI.PROFILE_NONE, 0.0)
 
     def method(self, nthreads=0) -> O.Method:
-        return O.Method(Q=self.Q, op=self.op, rates=self.rates, force=self.force, ubb_u=self.ubb, nthreads=nthreads)
+        return O.Method(Q=self.Q, op=self.op, rates=self.rates, force=self.force, ubb_u=self.ubb, nthreads=nthreads,
+                        equilibrium=self.equilibrium)
 
 
 def make_sim(case: Case, **kw):
     from paper_2001_11806_b200 import lbm as L
     args = dict(shape=case.shape, stencil=case.Q, collision=case.op, rates=case.rates, dtype=case.dtype,
                 pattern=case.pattern, force=case.force, flags=case.flags(), ubb_velocity=case.ubb,
-                periodic=case.periodic())
+                periodic=case.periodic(), equilibrium=case.equilibrium)
     args.update(case.extra)
     args.update(kw)
     return L.Simulation(**args)

@@ -84,6 +84,9 @@ def test_slab_plan(L):
     (dict(n_local_slabs=3), -1),                                # nz % slabs != 0
     (dict(periodic=(1, 0, 1)), -1),                             # non-periodic axis without walls
     (dict(nccl_self=True, n_local_slabs=2), -1),                # self-exchange is single-slab
+    (dict(equilibrium=3), -1),                                  # unknown equilibrium kind
+    (dict(stencil=27, collision="cumulant", rates=(1.9,), equilibrium="incompressible"), -2),
+    (dict(collision="kbc", rates=(1.9,), equilibrium="moment_matched"), -2),
 ])
 def test_create_validation_errors(L, kw, code):
     """Validation happens before any CUDA call, so these run on a CPU-only host."""

@@ -97,6 +97,22 @@ def test_init_random_matches_seeded_inputs(Q, op, rates):
     assert max_rel_err(sim.populations(), ref) < 1e-14
 
 
+@pytest.mark.parametrize("equilibrium", ["compressible", "incompressible"])
+def test_macroscopic_readout_equilibrium_kinds(equilibrium):
+    """u = (j -+ F/2) / rho0 with rho0 = rho (compressible) or 1 (incompressible, P:285)."""
+    case = Case("mro", (12, 16, 8), 19, "trt", (1.6, 0.5), "f64", force=(1e-5, 0, 0), geometry="channel",
+                steps=9, equilibrium=equilibrium)
+    sim = make_sim(case)
+    init_sim(sim, case)
+    sim.step(case.steps)
+    d = O.Domain(case.method(), *case.shape, flags=case.flags())
+    rho_o, u_o = d.macroscopic(oracle_run(case), post_collision=True)
+    rho, u = sim.macroscopic()
+    fl = case.flags() == 0
+    np.testing.assert_allclose(rho[fl], rho_o[fl], rtol=1e-13)
+    np.testing.assert_allclose(u[:, fl], u_o[:, fl], rtol=0, atol=1e-15)
+
+
 def test_macroscopic_readout():
     case = FULL["c1_f64"]
     case = Case("c1s", (12, 16, 8), **{k: getattr(case, k) for k in ("Q", "op", "rates", "dtype", "force", "geometry")},
@@ -164,6 +180,23 @@ PARITY = [
     Case("kbc_q19_f32", (16, 12, 10), 19, "kbc", (1.9,), "f32", u_amp=0.05, steps=20),
     Case("kbc_aa_q19_f64_obst", (17, 13, 11), 19, "kbc", (1.95,), "f64", pattern="aa", geometry="obstacles",
          ubb=(0.02, -0.01, 0.03), u_amp=0.05, steps=15),
+    # equilibrium variants: incompressible Eq. (3), moment-matched
+    Case("inc_trt_force_channel_f64", (16, 20, 8), 19, "trt", (1.6, 0.5), "f64", force=(1e-5, 0, 0), geometry="channel",
+         steps=40, equilibrium="incompressible"),
+    Case("inc_trt_q27_f32_aa", (18, 14, 10), 27, "trt", (1.5, 1.2), "f32", pattern="aa", steps=12,
+         equilibrium="incompressible"),
+    Case("inc_mrt_f64_obst", (17, 13, 11), 19, "mrt", (1.9, 1.3, 1.1, 0.8), "f64", geometry="obstacles",
+         ubb=(0.02, -0.01, 0.03), steps=20, equilibrium="incompressible"),
+    Case("inc_srt_f32_aa_mrt_rates", (32, 16, 8), 19, "mrt", (1.9, 1.0, 1.0, 1.0), "f32", pattern="aa", init="shear",
+         rho_amp=0.0, u_amp=1e-4, steps=16, equilibrium="incompressible"),
+    Case("mm_trt_q19_f64_walls", (17, 13, 11), 19, "trt", (1.6, 0.5), "f64", force=(1e-5, 2e-5, 0), geometry="obstacles",
+         ubb=(0.02, -0.01, 0.03), u_amp=0.05, steps=20, equilibrium="moment_matched"),
+    Case("mm_srt_q19_f32_aa", (18, 14, 10), 19, "srt", (1.7,), "f32", pattern="aa", u_amp=0.05, steps=13,
+         equilibrium="moment_matched"),
+    Case("mm_mrt_q19_f64_aa_channel", (16, 20, 12), 19, "mrt", (1.9, 1.3, 1.1, 0.8), "f64", pattern="aa",
+         geometry="channel", u_amp=0.05, steps=14, equilibrium="moment_matched"),
+    Case("mm_trt_q27_is_eq3", (14, 12, 10), 27, "trt", (1.3, 0.9), "f64", u_amp=0.05, steps=10,
+         equilibrium="moment_matched"),
 ]
 
 
