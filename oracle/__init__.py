@@ -11,6 +11,7 @@ numpy arrays. Arrays use the canonical layout ``f[q, z(+ghosts), y, x]`` (x fast
 from __future__ import annotations
 
 import ctypes as C
+import functools
 import os
 import subprocess
 from dataclasses import dataclass, field
@@ -28,6 +29,21 @@ SRT, TRT, MRT, CUMULANT, IDENTITY, SMAGORINSKY, KBC = 0, 1, 2, 3, 4, 5, 6
 OPS = {"srt": SRT, "trt": TRT, "mrt": MRT, "cumulant": CUMULANT, "identity": IDENTITY,
        "smagorinsky": SMAGORINSKY, "kbc": KBC}
 FLUID, NOSLIP, UBB = 0, 1, 2
+
+
+@functools.lru_cache(maxsize=None)
+def _monomial_tables(Q: int):
+    name = f"D3Q{Q}"
+    basis = methods.monomial_basis(name)
+    assert all(len(p) == 1 for p in basis), "D3Q19/D3Q27 monomial bases are single monomials"
+    exps = [next(iter(p)) for p in basis]
+    Mr = methods.moment_matrix(basis, methods.stencil(name))
+    Minv = methods.mat_inverse(Mr)
+    exps = np.array(exps, dtype=np.int32)
+    minv = np.array([[float(v) for v in row] for row in Minv])
+    exps.setflags(write=False)
+    minv.setflags(write=False)
+    return exps, minv
 
 
 def build(force: bool = False) -> str:
@@ -76,6 +92,8 @@ def lib():
             ("ora_equilibrium_cell", [C.c_int, C.c_double, P, P], None),
             ("ora_product_equilibrium_cell", [C.c_int, C.c_double, P, P], None),
             ("ora_equilibrium_kind_cell", [P, C.c_double, P, P], None),
+            ("ora_maxwellian_equilibrium_cell", [P, C.c_double, P, P], None),
+            ("ora_from_cumulants_cfg_cell", [P, C.c_double, P, P], None),
             ("ora_cumulants_cell", [C.c_int, P, P], C.c_double),
             ("ora_from_cumulants_cell", [C.c_int, C.c_double, P, P], None),
             ("ora_pull_cell", [P, P, P, C.c_int64, C.c_int64, C.c_int64, P], None),
@@ -120,17 +138,8 @@ class Method:
 
     def monomial_tables(self):
         """Exponents of the monomial moment basis and the exact inverse of its moment
-        matrix, for the moment-matched equilibrium."""
-        if self._mono is None:
-            name = f"D3Q{self.Q}"
-            basis = methods.monomial_basis(name)
-            assert all(len(p) == 1 for p in basis), "D3Q19/D3Q27 monomial bases are single monomials"
-            exps = [next(iter(p)) for p in basis]
-            Mr = methods.moment_matrix(basis, methods.stencil(name))
-            Minv = methods.mat_inverse(Mr)
-            self._mono = (np.array(exps, dtype=np.int32),
-                          np.array([[float(v) for v in row] for row in Minv]))
-        return self._mono
+        matrix (moment-matched equilibrium; D3Q19 cumulant)."""
+        return _monomial_tables(self.Q)
 
     def mrt_matrices(self):
         """M (rows = weighted-orthogonal moment polynomials), M^-1 (exact) and S (Eq. 4)."""
@@ -184,7 +193,7 @@ class Domain:
             self._keep = [np.ascontiguousarray(M), np.ascontiguousarray(Minv), np.ascontiguousarray(S)]
             cfg.M, cfg.Minv, cfg.S = (_p(a) for a in self._keep)
         cfg.eq_kind = EQ_KINDS[method.equilibrium]
-        if method.equilibrium == "moment_matched":
+        if method.equilibrium == "moment_matched" or method.op == "cumulant":
             exps, minv = method.monomial_tables()
             self._keep += [np.ascontiguousarray(exps), np.ascontiguousarray(minv)]
             cfg.mono_exp, cfg.Mmono_inv = _p(self._keep[-2]), _p(self._keep[-1])
@@ -300,6 +309,32 @@ def equilibrium_kind_cell(method: Method, rho: float, u) -> np.ndarray:
     out = np.zeros(method.Q)
     lib().ora_equilibrium_kind_cell(d._pc(), rho, _p(u), _p(out))
     return out
+
+
+def maxwellian_equilibrium_cell(Q: int, rho: float, u) -> np.ndarray:
+    """Populations with the untruncated Maxwellian basis moments (the cumulant fixed point; D3Q27:
+    the product equilibrium)."""
+    d = Domain(Method(Q=Q, op="cumulant", rates=(1.0,)), 1, 1, 1)
+    u = np.ascontiguousarray(u, np.float64)
+    out = np.zeros(Q)
+    lib().ora_maxwellian_equilibrium_cell(d._pc(), rho, _p(u), _p(out))
+    return out
+
+
+def from_cumulants_any(Q: int, rho: float, kappa: np.ndarray) -> np.ndarray:
+    """Inverse cumulant transform on D3Q19 or D3Q27 (basis-moment route)."""
+    d = Domain(Method(Q=Q, op="cumulant", rates=(1.0,)), 1, 1, 1)
+    k = np.ascontiguousarray(kappa, np.float64).reshape(27)
+    out = np.zeros(Q)
+    lib().ora_from_cumulants_cfg_cell(d._pc(), rho, _p(k), _p(out))
+    return out
+
+
+def cumulants_any(Q: int, f: np.ndarray):
+    f = np.ascontiguousarray(f, np.float64)
+    k = np.zeros(27)
+    rho = lib().ora_cumulants_cell(Q, _p(f), _p(k))
+    return rho, k.reshape(3, 3, 3)
 
 
 def product_equilibrium_cell(Q: int, rho: float, u) -> np.ndarray:

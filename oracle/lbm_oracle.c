@@ -410,6 +410,81 @@ static void from_cumulants(const ora_stencil_t *s, double rho, const double *kap
     }
 }
 
+/* The populations whose raw moments of the monomial basis are m[a*9 + b*3 + c]:
+ * D3Q27 per axis (V x V x V)^-1 as in from_cumulants(); other stencils (D3Q19) f = M^-1 m over the
+ * basis exponents (cfg->mono_exp, cfg->Mmono_inv). Moments of the dropped monomials are ignored: for
+ * D3Q19 they vanish identically. */
+static void populations_from_moments(const ora_cfg *cfg, const ora_stencil_t *s, const double *m, double *f) {
+    if (s->Q == 27) {
+        for (int q = 0; q < 27; ++q) {
+            double v = 0.0;
+            for (int a = 0; a < 3; ++a)
+                for (int b = 0; b < 3; ++b)
+                    for (int c = 0; c < 3; ++c) {
+                        int e[3] = {a, b, c};
+                        double coef = 1.0;
+                        for (int d = 0; d < 3; ++d) {
+                            int cd = s->c[q][d];
+                            double k;
+                            if (cd == 0) k = (e[d] == 0) ? 1.0 : (e[d] == 2) ? -1.0 : 0.0;
+                            else if (cd == 1) k = (e[d] == 0) ? 0.0 : 0.5;
+                            else k = (e[d] == 0) ? 0.0 : (e[d] == 1) ? -0.5 : 0.5;
+                            coef *= k;
+                        }
+                        v += coef * m[a * 9 + b * 3 + c];
+                    }
+            f[q] = v;
+        }
+        return;
+    }
+    for (int q = 0; q < s->Q; ++q) {
+        double v = 0.0;
+        for (int k = 0; k < s->Q; ++k) {
+            const int32_t *e = cfg->mono_exp + 3 * k;
+            v += cfg->Mmono_inv[q * s->Q + k] * m[e[0] * 9 + e[1] * 3 + e[2]];
+        }
+        f[q] = v;
+    }
+}
+
+/* Inverse of cumulants() on any stencil: moments from exp(K) (O5 step 6), populations from the
+ * moments of the basis monomials. */
+static void from_cumulants_cfg(const ora_cfg *cfg, const ora_stencil_t *s, double rho, const double *kappa, double *f) {
+    double K[27], E[27], m[27];
+    for (int a = 0; a < 3; ++a)
+        for (int b = 0; b < 3; ++b)
+            for (int c = 0; c < 3; ++c)
+                K[a * 9 + b * 3 + c] = kappa[a * 9 + b * 3 + c] / (fact3[a] * fact3[b] * fact3[c]);
+    K[0] = 0.0;
+    ser_exp(K, E);
+    for (int a = 0; a < 3; ++a)
+        for (int b = 0; b < 3; ++b)
+            for (int c = 0; c < 3; ++c)
+                m[a * 9 + b * 3 + c] = rho * fact3[a] * fact3[b] * fact3[c] * E[a * 9 + b * 3 + c];
+    populations_from_moments(cfg, s, m, f);
+}
+
+/* Maxwellian-moment equilibrium (G2 generalised): the populations whose basis moments are the raw
+ * moments of the continuous Maxwellian Eq. (7)-(8), rho prod_d mu_{e_d}(u_d) (NOT truncated). For
+ * D3Q27 this is the product equilibrium; it is the fixed point of the cumulant collision on any
+ * stencil (kappa_eq = (ln rho, u, cs2 delta, 0, ...)). */
+static void maxwellian_equilibrium(const ora_cfg *cfg, const ora_stencil_t *s, double rho, const double u[3], double *feq) {
+    if (s->Q == 27) {
+        product_equilibrium(s, rho, u, feq);
+        return;
+    }
+    double m[27];
+    for (int a = 0; a < 3; ++a)
+        for (int b = 0; b < 3; ++b)
+            for (int c = 0; c < 3; ++c) {
+                int e[3] = {a, b, c};
+                double v = rho;
+                for (int d = 0; d < 3; ++d) v *= (e[d] == 0) ? 1.0 : (e[d] == 1) ? u[d] : (1.0 / 3.0 + u[d] * u[d]);
+                m[a * 9 + b * 3 + c] = v;
+            }
+    populations_from_moments(cfg, s, m, feq);
+}
+
 /* Cumulant collision (O5 step 5, G7 rates): order 1 unchanged; 2nd-order trace
  * T -> T + wb (3 cs2 - T); deviator and off-diagonals -> (1 - ws); order n >= 3 -> (1 - w_n). */
 static void collide_cumulant(const ora_cfg *cfg, const ora_stencil_t *s, const double *f, double *out) {
@@ -433,7 +508,7 @@ static void collide_cumulant(const ora_cfg *cfg, const ora_stencil_t *s, const d
                 int n = a + b + c;
                 if (n >= 3) kap[a * 9 + b * 3 + c] *= (1.0 - cfg->rates[n - 1]); /* w3..w6 = rates[2..5] */
             }
-    from_cumulants(s, rho, kap, out);
+    from_cumulants_cfg(cfg, s, rho, kap, out);
 }
 
 /* Smagorinsky SRT (Eqs. 11-14): nu_t = (C_S Delta)^2 |S|, Delta = 1,
@@ -717,7 +792,7 @@ int ora_init_equilibrium(const ora_cfg *cfg, const double *rho, const double *u,
             for (int64_t x = 0; x < cfg->nx; ++x) {
                 int64_t i = (z * cfg->ny + y) * cfg->nx + x;
                 double uu[3] = {u[i], u[n + i], u[2 * n + i]}, feq[27];
-                if (cfg->op == ORA_CUMULANT) product_equilibrium(&s, rho[i], uu, feq);
+                if (cfg->op == ORA_CUMULANT) maxwellian_equilibrium(cfg, &s, rho[i], uu, feq);
                 else equilibrium_cfg(cfg, &s, rho[i], uu, feq);
                 int64_t self = cell(cfg, x, y, z);
                 for (int q = 0; q < s.Q; ++q) f[q * Sq + self] = feq[q];
@@ -770,6 +845,16 @@ void ora_equilibrium_kind_cell(const ora_cfg *cfg, double rho, const double *u, 
     ora_stencil_t s;
     build_stencil(cfg->Q, &s);
     equilibrium_cfg(cfg, &s, rho, u, feq);
+}
+void ora_maxwellian_equilibrium_cell(const ora_cfg *cfg, double rho, const double *u, double *feq) {
+    ora_stencil_t s;
+    build_stencil(cfg->Q, &s);
+    maxwellian_equilibrium(cfg, &s, rho, u, feq);
+}
+void ora_from_cumulants_cfg_cell(const ora_cfg *cfg, double rho, const double *kappa, double *f) {
+    ora_stencil_t s;
+    build_stencil(cfg->Q, &s);
+    from_cumulants_cfg(cfg, &s, rho, kappa, f);
 }
 void ora_product_equilibrium_cell(int Q, double rho, const double *u, double *feq) {
     ora_stencil_t s;

@@ -214,3 +214,73 @@ def test_cumulant_config3_isserlis_closed_form():
         mom = np.array([rho * _gaussian_raw_moment(e, u, Sp) for e in product(range(3), repeat=3)])
         ref = np.linalg.solve(A, mom)
         np.testing.assert_allclose(O.collide_cell(m, f), ref, rtol=0, atol=2e-15)
+
+
+# ---------------------------------------------------------------------------------------
+# D3Q19 cumulant ("cumulant methods not only for D3Q27 ... but also for D3Q19"): the
+# cumulants of the 19 basis monomials are relaxed as in G7 and mapped back through the
+# basis moments. Pins: Eq. (9) by the Cauchy/FFT route, round trip, fixed point, conservation, the
+# Maxwellian (all rates 1) and Gaussian/Isserlis (C3-like rates) closed forms on the basis moments.
+# ---------------------------------------------------------------------------------------
+def _basis19():
+    c, _, _ = O.stencil_arrays(19)
+    es = [e for e in product(range(3), repeat=3) if min(e) == 0]  # the 19 non-zero-row monomials
+    A = np.array([[np.prod(np.asarray(cq, float) ** np.array(e)) for cq in c] for e in es])
+    return c, es, A
+
+
+def test_d3q19_cumulants_match_generating_function_eq9():
+    c, es, _ = _basis19()
+    fact = np.array([1.0, 1.0, 2.0])
+    for _ in range(3):
+        f = _random_state(19, amp=0.2)
+        rho, kap = O.cumulants_any(19, f)
+        ref = _taylor_coeffs_of_K(f, c) * fact[:, None, None] * fact[None, :, None] * fact[None, None, :]
+        assert abs(rho - f.sum()) < 1e-15
+        for e in es[1:]:
+            assert abs(kap[e] - ref[e]) < 1e-12, e
+
+
+def test_d3q19_cumulant_round_trip_and_fixed_point():
+    m = O.Method(Q=19, op="cumulant", rates=(1.8, 1.3, 1.1, 0.9))
+    c, _, _ = O.stencil_arrays(19)
+    for _ in range(5):
+        f = _random_state(19, amp=0.3)
+        rho, kap = O.cumulants_any(19, f)
+        np.testing.assert_allclose(O.from_cumulants_any(19, rho, kap), f, rtol=0, atol=1e-15)
+        u = c.T @ f / rho
+        feq = O.maxwellian_equilibrium_cell(19, rho, u)
+        np.testing.assert_allclose(O.collide_cell(m, feq), feq, rtol=0, atol=2e-16)
+        out = O.collide_cell(m, f)
+        assert abs(out.sum() - f.sum()) < 1e-15
+        np.testing.assert_allclose(c.T @ out, c.T @ f, rtol=0, atol=1e-16)
+
+
+def test_d3q19_cumulant_all_rates_one_gives_maxwellian_moments():
+    """kappa' = kappa_eq -> the basis moments of f* are the untruncated Maxwellian moments
+    rho prod_d mu_{e_d}(u_d) (Gaussian factorisation of Eq. 7)."""
+    c, es, A = _basis19()
+    m = O.Method(Q=19, op="cumulant", rates=(1, 1, 1, 1))
+    for _ in range(3):
+        f = _random_state(19, amp=0.3)
+        rho = f.sum()
+        u = c.T @ f / rho
+        mu = lambda k, v: 1.0 if k == 0 else v if k == 1 else 1 / 3 + v * v
+        ref = np.array([rho * mu(e[0], u[0]) * mu(e[1], u[1]) * mu(e[2], u[2]) for e in es])
+        np.testing.assert_allclose(A @ O.collide_cell(m, f), ref, rtol=0, atol=5e-16)
+
+
+def test_d3q19_cumulant_isserlis_closed_form():
+    """C3-like rates (ws = 1.95, others 1): the basis moments of f* are rho E_{N(u, S')}[X^a Y^b Z^c]
+    with S' = cs2 I + (1 - ws) dev(S), S the central second moments / rho (Isserlis, brute-force pairings)."""
+    c, es, A = _basis19()
+    m = O.Method(Q=19, op="cumulant", rates=(1.95,))
+    for _ in range(3):
+        f = _random_state(19, amp=0.2)
+        rho = f.sum()
+        u = c.T @ f / rho
+        d = c - u
+        Sig = np.einsum("qa,qb,q->ab", d, d, f) / rho
+        Sp = np.eye(3) / 3 + (1 - 1.95) * (Sig - np.trace(Sig) / 3 * np.eye(3))
+        mom = np.array([rho * _gaussian_raw_moment(e, u, Sp) for e in es])
+        np.testing.assert_allclose(O.collide_cell(m, f), np.linalg.solve(A, mom), rtol=0, atol=2e-15)
