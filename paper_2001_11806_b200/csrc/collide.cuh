@@ -586,6 +586,127 @@ __device__ __forceinline__ void collide_cumulant27(T (&g)[27], const Rates<T> &p
 }
 
 // ---------------------------------------------------------------------------------------
+// Cumulant, D3Q19 (cumulant methods "also for D3Q19"): the 19 populations are embedded in
+// the 3x3x3 tensor with zero corners, transformed to central moments by the same per-axis chimera
+// transform, the cumulants of the 19 basis monomials (at least one exponent 0; the set is
+// closed under taking sub-indices, so none of them needs a dropped monomial) are relaxed as in G7
+// (orders 2, 3, 4), shifted back to raw moments per axis and mapped to populations with the
+// closed-form inverse of the D3Q19 monomial moment matrix (d3q19_from_raw).
+// ---------------------------------------------------------------------------------------
+// raw moment tensor M[a*9 + b*3 + c] (basis entries only are read) -> the 19 populations
+template <typename T>
+__device__ __forceinline__ void d3q19_from_raw(const T (&M)[27], T (&f)[19]) {
+#define MI(a, b, c) M[(a) * 9 + (b) * 3 + (c)]
+    // faces: f(+-e_x) = ((M200 - M220 - M202) +- (M100 - M120 - M102)) / 2, and cyclically
+    const T sx = MI(2, 0, 0) - MI(2, 2, 0) - MI(2, 0, 2), dx = MI(1, 0, 0) - MI(1, 2, 0) - MI(1, 0, 2);
+    const T sy = MI(0, 2, 0) - MI(2, 2, 0) - MI(0, 2, 2), dy = MI(0, 1, 0) - MI(2, 1, 0) - MI(0, 1, 2);
+    const T sz = MI(0, 0, 2) - MI(2, 0, 2) - MI(0, 2, 2), dz = MI(0, 0, 1) - MI(2, 0, 1) - MI(0, 2, 1);
+#pragma unroll
+    for (int q = 0; q < 19; ++q) {
+        const int cx = kC27[q][0], cy = kC27[q][1], cz = kC27[q][2];
+        const int n = cx * cx + cy * cy + cz * cz;
+        T v;
+        if (n == 0) {
+            v = MI(0, 0, 0) - MI(2, 0, 0) - MI(0, 2, 0) - MI(0, 0, 2) + MI(2, 2, 0) + MI(2, 0, 2) + MI(0, 2, 2);
+        } else if (n == 1) {
+            const T sgn = T(cx + cy + cz);
+            v = cx ? T(0.5) * (sx + sgn * dx) : cy ? T(0.5) * (sy + sgn * dy) : T(0.5) * (sz + sgn * dz);
+        } else if (cz == 0) {  // xy edge: (M220 + sx M120 + sy M210 + sx sy M110) / 4
+            v = T(0.25) * (MI(2, 2, 0) + T(cx) * MI(1, 2, 0) + T(cy) * MI(2, 1, 0) + T(cx * cy) * MI(1, 1, 0));
+        } else if (cy == 0) {  // xz edge
+            v = T(0.25) * (MI(2, 0, 2) + T(cx) * MI(1, 0, 2) + T(cz) * MI(2, 0, 1) + T(cx * cz) * MI(1, 0, 1));
+        } else {  // yz edge
+            v = T(0.25) * (MI(0, 2, 2) + T(cy) * MI(0, 1, 2) + T(cz) * MI(0, 2, 1) + T(cy * cz) * MI(0, 1, 1));
+        }
+        f[q] = v;
+    }
+#undef MI
+}
+
+// central -> raw moments along one line (K0, K1, K2) about velocity u
+template <typename T>
+__device__ __forceinline__ void shift_raw(T &m, T &z, T &p, T u) {
+    const T k0 = m, k1 = z, k2 = p;
+    z = k1 + u * k0;
+    p = k2 + T(2) * u * k1 + u * u * k0;
+}
+
+template <typename T>
+__device__ __forceinline__ void collide_cumulant19(T (&g)[19], const Rates<T> &p) {
+    using S = Stencil<19>;
+    T K[27];
+#pragma unroll
+    for (int t = 0; t < 27; ++t) K[t] = T(0);
+#pragma unroll
+    for (int q = 0; q < 19; ++q) K[tidx(q)] = g[q] + T(S::w(q));
+    T drho, jx, jy, jz;
+    moments0<19, T>(g, drho, jx, jy, jz);
+    const T rho = T(1) + drho;
+    const T inv = T(1) / rho;
+    const T ux = jx * inv, uy = jy * inv, uz = jz * inv;
+#define KI(a, b, c) K[(a) * 9 + (b) * 3 + (c)]
+#pragma unroll
+    for (int b = 0; b < 3; ++b)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) chim_fwd(KI(0, b, c), KI(1, b, c), KI(2, b, c), ux);
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) chim_fwd(KI(a, 0, c), KI(a, 1, c), KI(a, 2, c), uy);
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int b = 0; b < 3; ++b) chim_fwd(KI(a, b, 0), KI(a, b, 1), KI(a, b, 2), uz);
+    const T c200 = KI(2, 0, 0) * inv, c020 = KI(0, 2, 0) * inv, c002 = KI(0, 0, 2) * inv;
+    const T c110 = KI(1, 1, 0) * inv, c101 = KI(1, 0, 1) * inv, c011 = KI(0, 1, 1) * inv;
+    // order 4 of the basis: kappa_220 = c220 - c200 c020 - 2 c110^2 (and cyclically)
+    const T k220 = KI(2, 2, 0) * inv - c200 * c020 - T(2) * c110 * c110;
+    const T k202 = KI(2, 0, 2) * inv - c200 * c002 - T(2) * c101 * c101;
+    const T k022 = KI(0, 2, 2) * inv - c020 * c002 - T(2) * c011 * c011;
+    const T ws = p.r[0], wb = p.r[1], r3 = T(1) - p.r[2], r4 = T(1) - p.r[3];
+    const T tr = c200 + c020 + c002;
+    const T trn = tr + wb * (T(1) - tr);
+    const T rs = T(1) - ws;
+    const T third = T(1) / T(3);
+    const T n200 = third * trn + rs * (c200 - third * tr);
+    const T n020 = third * trn + rs * (c020 - third * tr);
+    const T n002 = third * trn + rs * (c002 - third * tr);
+    const T n110 = rs * c110, n101 = rs * c101, n011 = rs * c011;
+    // relaxed central moments (times rho) of the basis; the dropped entries are never read
+    KI(0, 0, 0) = rho;
+    KI(1, 0, 0) = T(0);
+    KI(0, 1, 0) = T(0);
+    KI(0, 0, 1) = T(0);
+    KI(2, 0, 0) = rho * n200; KI(0, 2, 0) = rho * n020; KI(0, 0, 2) = rho * n002;
+    KI(1, 1, 0) = rho * n110; KI(1, 0, 1) = rho * n101; KI(0, 1, 1) = rho * n011;
+    KI(2, 1, 0) *= r3; KI(2, 0, 1) *= r3; KI(1, 2, 0) *= r3;
+    KI(0, 2, 1) *= r3; KI(1, 0, 2) *= r3; KI(0, 1, 2) *= r3;
+    KI(2, 2, 0) = rho * (r4 * k220 + n200 * n020 + T(2) * n110 * n110);
+    KI(2, 0, 2) = rho * (r4 * k202 + n200 * n002 + T(2) * n101 * n101);
+    KI(0, 2, 2) = rho * (r4 * k022 + n020 * n002 + T(2) * n011 * n011);
+    KI(1, 1, 1) = T(0); KI(2, 1, 1) = T(0); KI(1, 2, 1) = T(0); KI(1, 1, 2) = T(0);
+    KI(2, 2, 1) = T(0); KI(2, 1, 2) = T(0); KI(1, 2, 2) = T(0); KI(2, 2, 2) = T(0);
+    // central -> raw moments per axis
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int b = 0; b < 3; ++b) shift_raw(KI(a, b, 0), KI(a, b, 1), KI(a, b, 2), uz);
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) shift_raw(KI(a, 0, c), KI(a, 1, c), KI(a, 2, c), uy);
+#pragma unroll
+    for (int b = 0; b < 3; ++b)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) shift_raw(KI(0, b, c), KI(1, b, c), KI(2, b, c), ux);
+#undef KI
+    T f[19];
+    d3q19_from_raw<T>(K, f);
+#pragma unroll
+    for (int q = 0; q < 19; ++q) g[q] = f[q] - T(S::w(q));
+}
+
+// ---------------------------------------------------------------------------------------
 // Dispatch
 // ---------------------------------------------------------------------------------------
 enum Op { OP_SRT = 0, OP_TRT = 1, OP_MRT = 2, OP_CUMULANT = 3, OP_IDENTITY = 4, OP_SMAGORINSKY = 5, OP_KBC = 6 };
@@ -601,8 +722,8 @@ __device__ __forceinline__ void collide(T (&g)[Q], const Rates<T> &p) {
         static_assert(Q == 19, "MRT is implemented for D3Q19");
         collide_mrt19<T, EQ>(g, p);
     } else if constexpr (OP == OP_CUMULANT) {
-        static_assert(Q == 27, "cumulant is implemented for D3Q27");
-        collide_cumulant27<T>(g, p);
+        if constexpr (Q == 27) collide_cumulant27<T>(g, p);
+        else collide_cumulant19<T>(g, p);
     } else if constexpr (OP == OP_SMAGORINSKY) {
         collide_smagorinsky<Q, T>(g, p);
     } else if constexpr (OP == OP_KBC) {

@@ -28,6 +28,7 @@ struct Kernels {
 Kernels select_trt(int Q, int dtype, int fm, bool force);
 Kernels select_mrt(int Q, int dtype, int fm, bool force);
 Kernels select_cumulant(int Q, int dtype, int fm, bool force);
+Kernels select_cumulant19(int Q, int dtype, int fm, bool force);
 Kernels select_identity(int Q, int dtype, int fm, bool force);
 Kernels select_smagorinsky(int Q, int dtype, int fm, bool force);
 Kernels select_kbc(int Q, int dtype, int fm, bool force);

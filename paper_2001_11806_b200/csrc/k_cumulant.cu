@@ -3,5 +3,8 @@
 
 namespace lbm {
 
-Kernels select_cumulant(int Q, int dtype, int fm, bool force) { return select_op<OP_CUMULANT, false, false, true>(Q, dtype, fm, force); }
+Kernels select_cumulant(int Q, int dtype, int fm, bool force) {
+    if (Q == 19) return select_cumulant19(Q, dtype, fm, force);
+    return select_op<OP_CUMULANT, false, false, true>(Q, dtype, fm, force);
+}
 }  // namespace lbm

@@ -452,7 +452,9 @@ __global__ void k_init(const InitArgs a, T *__restrict__ f0, T *__restrict__ f1)
 #pragma unroll
     for (int q = 0; q < Q; ++q) {
         double gq;
-        if (a.product_eq) {
+        if (a.product_eq && Q == 19) {
+            gq = 0.0;  // written below from the Maxwellian basis moments
+        } else if (a.product_eq) {
             double v = rho;
             const double uc[3] = {ux, uy, uz};
             const int c[3] = {S::cx(q), S::cy(q), S::cz(q)};
@@ -466,8 +468,29 @@ __global__ void k_init(const InitArgs a, T *__restrict__ f0, T *__restrict__ f1)
             gq = S::w(q) * drho + S::w(q) * rho0 * (3.0 * cu + 4.5 * cu * cu - uu15);
             if (a.eq_kind == EQ_MOMENT_MATCHED) gq += mm_delta<Q, double>(q, rho, ux, uy, uz);
         }
+        if (a.product_eq && Q == 19) continue;
         f0[q * a.geo.Sq + self] = T(gq);
         if (f1) f1[q * a.geo.Sq + self] = T(gq);
+    }
+    if (Q == 19 && a.product_eq) {
+        // D3Q19 cumulant fixed point: basis moments = untruncated Maxwellian moments rho prod mu_e(u)
+        double M[27], f[19];
+        const double uc[3] = {ux, uy, uz};
+#pragma unroll
+        for (int t = 0; t < 27; ++t) {
+            const int e[3] = {t / 9, (t / 3) % 3, t % 3};
+            double v = rho;
+#pragma unroll
+            for (int d = 0; d < 3; ++d) v *= e[d] == 0 ? 1.0 : e[d] == 1 ? uc[d] : (1.0 / 3.0 + uc[d] * uc[d]);
+            M[t] = v;
+        }
+        d3q19_from_raw<double>(M, f);
+#pragma unroll
+        for (int q = 0; q < 19; ++q) {
+            const double gq = f[q] - Stencil<19>::w(q);
+            f0[q * a.geo.Sq + self] = T(gq);
+            if (f1) f1[q * a.geo.Sq + self] = T(gq);
+        }
     }
 }
 

@@ -77,7 +77,6 @@ def test_slab_plan(L):
     (dict(rates=(2.5,)), -1),                                   # rate outside (0, 2)
     (dict(collision="trt", rates=(1.6,)), -1),                  # TRT needs two rates
     (dict(stencil=27, collision="mrt", rates=(1.9,)), -2),      # MRT is D3Q19 only
-    (dict(stencil=19, collision="cumulant", rates=(1.9,)), -2),  # cumulant is D3Q27 only
     (dict(collision="mrt", rates=(1.9,), force=(1e-5, 0, 0)), -2),
     (dict(stencil=27, collision="kbc", rates=(1.9,)), -2),        # KBC is D3Q19 only
     (dict(collision="smagorinsky", rates=(1.9,)), -1),             # needs [omega_0, C_S]
