@@ -174,6 +174,8 @@ class Exact:
             for e, v in P.items():
                 E[e] = E.get(e, Fr(0)) + v / nf
         mp = {e: rho * fac[e[0]] * fac[e[1]] * fac[e[2]] * E.get(e, Fr(0)) for e in idx}
+        if self.Q == 19:
+            return self._d3q19_from_moments(mp)
         out = []
         for c in self.dirs:
             v = Fr(0)
@@ -188,6 +190,31 @@ class Exact:
                         k = {0: Fr(0), 1: Fr(-1, 2), 2: Fr(1, 2)}[e[d]]
                     coef *= k
                 v += coef * mp[e]
+            out.append(v)
+        return out
+
+    def _d3q19_from_moments(self, M):
+        """Hand-derived inverse of the D3Q19 monomial moment map (edges from their 4 plane moments,
+        faces from the axis moments minus the edges, centre from the mass) — independent of the
+        oracle's M^-1 route."""
+        out = []
+        for c in self.dirs:
+            nz = [d for d in range(3) if c[d] != 0]
+            if not nz:
+                v = (M[(0, 0, 0)] - M[(2, 0, 0)] - M[(0, 2, 0)] - M[(0, 0, 2)]
+                     + M[(2, 2, 0)] + M[(2, 0, 2)] + M[(0, 2, 2)])
+            elif len(nz) == 1:
+                a = nz[0]
+                o = [d for d in range(3) if d != a]
+                e2 = tuple(2 if d == a else 0 for d in range(3))
+                e1 = tuple(1 if d == a else 0 for d in range(3))
+                s_ = M[e2] - sum(M[tuple(2 if d in (a, b) else 0 for d in range(3))] for b in o)
+                d_ = M[e1] - sum(M[tuple(1 if d == a else 2 if d == b else 0 for d in range(3))] for b in o)
+                v = (s_ + c[a] * d_) / 2
+            else:
+                a, b = nz
+                e = lambda ka, kb: tuple(ka if d == a else kb if d == b else 0 for d in range(3))
+                v = (M[e(2, 2)] + c[a] * M[e(1, 2)] + c[b] * M[e(2, 1)] + c[a] * c[b] * M[e(1, 1)]) / 4
             out.append(v)
         return out
 

@@ -30,6 +30,8 @@ CASES = [
     ("trt", 27, (1.3, 0.9), (0, 0, 0), "walls", 1),
     ("mrt", 19, (1.9, 1.3, 1.1, 0.8), (0, 0, 0), "walls", 1),
     ("kbc", 19, (1.9,), (0, 0, 0), "walls", 1),
+    ("kbc", 27, (1.8,), (0, 0, 0), "walls", 1),
+    ("cumulant", 19, (1.9, 1.2, 1.1, 0.8), (0, 0, 0), "walls", 1),
     ("cumulant", 27, (1.95, 1.2, 1.1, 0.9, 1.3, 0.7), (0, 0, 0), "periodic", 1),
     ("cumulant", 27, (1.95,), (0, 0, 0), "walls", 1),
     ("trt", 19, (1.6, 0.5), (1e-3, 0, -5e-4), "walls", 2, "incompressible"),

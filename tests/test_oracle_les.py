@@ -59,9 +59,9 @@ def test_smagorinsky_limits():
     np.testing.assert_allclose(O.collide_cell(m, feq), feq, rtol=0, atol=1e-15)
 
 
-def _kbc_reference(f, ws):
-    c, w, _ = O.stencil_arrays(19)
-    rho, feq, Pi = _pi_neq(19, f)
+def _kbc_reference(f, ws, Q=19):
+    c, w, _ = O.stencil_arrays(Q)
+    rho, feq, Pi = _pi_neq(Q, f)
     dev = Pi - np.trace(Pi) / 3 * np.eye(3)
     ds = 4.5 * w * np.einsum("qa,qb,ab->q", c, c, dev)   # weighted shear projection (G6)
     dh = (f - feq) - ds
@@ -69,13 +69,16 @@ def _kbc_reference(f, ws):
     return feq, ds, dh, wh
 
 
+@pytest.mark.parametrize("Q", [19, 27])
 @pytest.mark.parametrize("ws", [1.99, 1.7, 1.2])
-def test_kbc_matches_eq19_and_entropy_condition(ws):
-    m = O.Method(Q=19, op="kbc", rates=(ws,))
-    c, _, _ = O.stencil_arrays(19)
+def test_kbc_matches_eq19_and_entropy_condition(ws, Q):
+    """D3Q27: the same reading G17 on the D3Q27 weighted basis; the shear
+    projector (9/2) w c c : dev(Pi) holds there too (4th-order isotropy of both weight sets)."""
+    m = O.Method(Q=Q, op="kbc", rates=(ws,))
+    c, _, _ = O.stencil_arrays(Q)
     for amp in (1e-3, 0.05, 0.2):
-        f = _state(19, amp)
-        feq, ds, dh, wh = _kbc_reference(f, ws)
+        f = _state(Q, amp)
+        feq, ds, dh, wh = _kbc_reference(f, ws, Q)
         out = O.collide_cell(m, f)
         np.testing.assert_allclose(out, f - ws * ds - wh * dh, rtol=0, atol=1e-15)
         # linearised optimum (exact up to the rounding of sum(f - f_eq), ~1e-16)
@@ -84,12 +87,13 @@ def test_kbc_matches_eq19_and_entropy_condition(ws):
         np.testing.assert_allclose(c.T @ out, c.T @ f, atol=1e-16)
 
 
-def test_kbc_limits():
-    f = _state(19, 0.1)
-    feq, _, _, _ = _kbc_reference(f, 1.0)
-    np.testing.assert_allclose(O.collide_cell(O.Method(Q=19, op="kbc", rates=(1.0,)), f), feq, rtol=0, atol=1e-15)
-    e = O.equilibrium_cell(19, 0.99, np.array([0.01, 0.02, -0.03]))
-    np.testing.assert_allclose(O.collide_cell(O.Method(Q=19, op="kbc", rates=(1.8,)), e), e, rtol=0, atol=1e-15)
+@pytest.mark.parametrize("Q", [19, 27])
+def test_kbc_limits(Q):
+    f = _state(Q, 0.1)
+    feq, _, _, _ = _kbc_reference(f, 1.0, Q)
+    np.testing.assert_allclose(O.collide_cell(O.Method(Q=Q, op="kbc", rates=(1.0,)), f), feq, rtol=0, atol=1e-15)
+    e = O.equilibrium_cell(Q, 0.99, np.array([0.01, 0.02, -0.03]))
+    np.testing.assert_allclose(O.collide_cell(O.Method(Q=Q, op="kbc", rates=(1.8,)), e), e, rtol=0, atol=1e-15)
 
 
 def test_kbc_entropy_not_below_linearised_neighbours():
