@@ -9,7 +9,7 @@
  *     then lexicographic on (cx, cy, cz) with -1 < 0 < 1.
  *   - Collision: SRT/BGK Eq. (1); TRT with Guo forcing split by moment
  *     parity (G4); weighted-orthogonal MRT Eq. (4) (G5/G6; D3Q19); cumulant
- *     (G7; D3Q27 and D3Q19); Smagorinsky SRT and KBC (D3Q19).
+ *     (G7; D3Q27 and D3Q19); Smagorinsky SRT and KBC.
  *     Equilibrium Eq. (3), 2nd order, compressible (G1), or its incompressible and
  *     moment-matched variants (LBM_EQ_*).
  *   - Storage patterns: two-array stream-pull-collide and the single-array AA
@@ -67,7 +67,7 @@ extern "C" {
 #define LBM_IDENTITY 4 /* debug: no collision (pure data movement, bit-exact tests)    */
 #define LBM_SMAGORINSKY 5 /* SRT with the local Smagorinsky omega (Eqs. 11-14):
                              rates = [omega_0, C_S]                                    */
-#define LBM_KBC 6      /* entropic KBC (Eqs. 15-19), D3Q19: rates = [omega_s];
+#define LBM_KBC 6      /* entropic KBC (Eqs. 15-19), D3Q19 and D3Q27: rates = [omega_s];
                           s = shear moments, h = the other non-conserved moments        */
 
 #define LBM_F64 0
@@ -140,7 +140,7 @@ void lbm_config_default(lbm_config *cfg);
 
 /* Create a simulation. Validates cfg (LBM_EINVAL: bad enum, rate outside (0,2), nz % nranks != 0,
  * slabs thinner than 2 planes, non-periodic axis without walls on its faces; LBM_EUNSUPPORTED:
- * MRT or KBC other than D3Q19, force with operators other than SRT/TRT, fused halo with the AA
+ * MRT other than D3Q19, force with operators other than SRT/TRT, fused halo with the AA
  * pattern), allocates device memory and, for nranks > 1 (or nccl_self), creates the NCCL
  * communicator (collective: every rank must call it). The state is zero until an init call. */
 int lbm_create(const lbm_config *cfg, lbm_handle *out);

@@ -328,7 +328,7 @@ __device__ __forceinline__ void collide_smagorinsky(T (&g)[Q], const Rates<T> &p
 }
 
 // ---------------------------------------------------------------------------------------
-// KBC entropic operator, D3Q19 (Eqs. 15-19), rates = [omega_s]. Delta_s = shear-group
+// KBC entropic operator, D3Q19 and D3Q27 (Eqs. 15-19), rates = [omega_s]. Delta_s = shear-group
 // projection, Delta_h = bulk + order 3 + order 4 projections of g - g_eq (the weighted basis of
 // collide_mrt19); omega_h = 1 + (1 - omega_s) <Ds,Dh>_E / <Dh,Dh>_E, <a,b>_E = sum a b / f_eq.
 // ---------------------------------------------------------------------------------------
@@ -336,11 +336,11 @@ __device__ __forceinline__ void collide_smagorinsky(T (&g)[Q], const Rates<T> &p
 // is Delta_h = d - Delta_s exactly (f = f_eq + Delta_s + Delta_h, Eq. 15), and
 // f' = f - w_s Ds - w_h Dh = f_eq + (1 - w_h) d + (w_h - w_s) Ds. The shear polynomials are even
 // and vanish at c = 0, so Ds is the same for q and qbar and zero at the centre.
-template <typename T>
-__device__ __forceinline__ void collide_kbc19(T (&g)[19], const Rates<T> &p) {
-    using S = Stencil<19>;
+template <int Q, typename T>
+__device__ __forceinline__ void collide_kbc(T (&g)[Q], const Rates<T> &p) {
+    using S = Stencil<Q>;
     T drho, jx, jy, jz;
-    moments0<19, T>(g, drho, jx, jy, jz);
+    moments0<Q, T>(g, drho, jx, jy, jz);
     const T rho = T(1) + drho;
     const T inv = T(1) / rho;
     const T ux = jx * inv, uy = jy * inv, uz = jz * inv;
@@ -351,7 +351,7 @@ __device__ __forceinline__ void collide_kbc19(T (&g)[19], const Rates<T> &p) {
     g[0] -= eq0;
     T a[5] = {T(0), T(0), T(0), T(0), T(0)};
 #pragma unroll
-    for (int q = 1; q < 19; ++q) {
+    for (int q = 1; q < Q; ++q) {
         if (q < S::opp(q)) {
             const int b = S::opp(q);
             const T w = T(S::w(q));
@@ -375,9 +375,9 @@ __device__ __forceinline__ void collide_kbc19(T (&g)[19], const Rates<T> &p) {
     for (int k = 0; k < 5; ++k) a[k] *= T(mrt_inv_norm(k));
     // entropic products <Ds,Dh>_E, <Dh,Dh>_E with <x,y>_E = sum x y / f_eq, f_eq = w + g_eq (Eq. 19)
     T sh = T(0), hh = g[0] * g[0] / (w0 + eq0);
-    T ds[19];
+    T ds[Q];
 #pragma unroll
-    for (int q = 1; q < 19; ++q) {
+    for (int q = 1; q < Q; ++q) {
         if (q < S::opp(q)) {
             const int b = S::opp(q);
             const T w = T(S::w(q));
@@ -408,7 +408,7 @@ __device__ __forceinline__ void collide_kbc19(T (&g)[19], const Rates<T> &p) {
     const T kd = T(1) - wh, ks = wh - ws;
     g[0] = eq0 + kd * g[0];
 #pragma unroll
-    for (int q = 1; q < 19; ++q) {
+    for (int q = 1; q < Q; ++q) {
         if (q < S::opp(q)) {
             const int b = S::opp(q);
             const T w = T(S::w(q));
@@ -727,8 +727,7 @@ __device__ __forceinline__ void collide(T (&g)[Q], const Rates<T> &p) {
     } else if constexpr (OP == OP_SMAGORINSKY) {
         collide_smagorinsky<Q, T>(g, p);
     } else if constexpr (OP == OP_KBC) {
-        static_assert(Q == 19, "KBC is implemented for D3Q19");
-        collide_kbc19<T>(g, p);
+        collide_kbc<Q, T>(g, p);
     }
 }
 

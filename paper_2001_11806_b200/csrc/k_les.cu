@@ -7,5 +7,8 @@ namespace lbm {
 Kernels select_smagorinsky(int Q, int dtype, int fm, bool force) {
     return select_op<OP_SMAGORINSKY, false, true, true>(Q, dtype, fm, force);
 }
-Kernels select_kbc(int Q, int dtype, int fm, bool force) { return select_op<OP_KBC, false, true, false>(Q, dtype, fm, force); }
+Kernels select_kbc(int Q, int dtype, int fm, bool force) {
+    if (Q == 27) return select_kbc27(Q, dtype, fm, force);
+    return select_op<OP_KBC, false, true, false>(Q, dtype, fm, force);
+}
 }  // namespace lbm

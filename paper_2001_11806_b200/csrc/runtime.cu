@@ -429,7 +429,6 @@ int validate(const lbm_config *c) {
         return fail(nullptr, LBM_EINVAL, "slab too large for 32-bit in-plane offsets (split it over more slabs)");
     const bool force = c->force[0] != 0 || c->force[1] != 0 || c->force[2] != 0;
     if (c->collision == LBM_MRT && c->stencil != 19) return fail(nullptr, LBM_EUNSUPPORTED, "MRT is implemented for D3Q19");
-    if (c->collision == LBM_KBC && c->stencil != 19) return fail(nullptr, LBM_EUNSUPPORTED, "KBC is implemented for D3Q19");
     if (force && c->collision != LBM_SRT && c->collision != LBM_TRT)
         return fail(nullptr, LBM_EUNSUPPORTED, "forcing is implemented for SRT/TRT");
     if (c->equilibrium < LBM_EQ_COMPRESSIBLE || c->equilibrium > LBM_EQ_MOMENT_MATCHED)

@@ -78,7 +78,6 @@ def test_slab_plan(L):
     (dict(collision="trt", rates=(1.6,)), -1),                  # TRT needs two rates
     (dict(stencil=27, collision="mrt", rates=(1.9,)), -2),      # MRT is D3Q19 only
     (dict(collision="mrt", rates=(1.9,), force=(1e-5, 0, 0)), -2),
-    (dict(stencil=27, collision="kbc", rates=(1.9,)), -2),        # KBC is D3Q19 only
     (dict(collision="smagorinsky", rates=(1.9,)), -1),             # needs [omega_0, C_S]
     (dict(n_local_slabs=3), -1),                                # nz % slabs != 0
     (dict(periodic=(1, 0, 1)), -1),                             # non-periodic axis without walls

@@ -197,6 +197,10 @@ PARITY = [
          geometry="channel", u_amp=0.05, steps=14, equilibrium="moment_matched"),
     Case("mm_trt_q27_is_eq3", (14, 12, 10), 27, "trt", (1.3, 0.9), "f64", u_amp=0.05, steps=10,
          equilibrium="moment_matched"),
+    # KBC on D3Q27
+    Case("kbc_q27_f64_cavity", (14, 14, 14), 27, "kbc", (1.99,), "f64", geometry="cavity", ubb=(0.05, 0, 0), steps=25),
+    Case("kbc_q27_f32_aa_obst", (17, 13, 11), 27, "kbc", (1.9,), "f32", pattern="aa", geometry="obstacles",
+         ubb=(0.02, -0.01, 0.03), u_amp=0.05, steps=14),
     # D3Q19 cumulant
     Case("cum19_f64_periodic", (16, 14, 12), 19, "cumulant", (1.95,), "f64", u_amp=0.05, steps=20),
     Case("cum19_general_rates_cavity", (14, 14, 14), 19, "cumulant", (1.8, 1.3, 1.2, 0.9), "f64", geometry="cavity",
@@ -236,6 +240,7 @@ STAGED_CASES = [
     Case("st_kbc_aa_obst", (48, 10, 8), 19, "kbc", (1.95,), "f64", pattern="aa", geometry="obstacles",
          ubb=(0.02, -0.01, 0.03), u_amp=0.05, steps=9),
     Case("st_smag_q27_f32", (64, 6, 5), 27, "smagorinsky", (1.9, 0.12), "f32", u_amp=0.05, steps=8),
+    Case("st_kbc27_pull_f64", (32, 9, 7), 27, "kbc", (1.95,), "f64", u_amp=0.05, steps=7),
     Case("st_cum19_aa_f32_walls16", (32, 12, 10), 19, "cumulant", (1.95,), "f32", pattern="aa", geometry="channel",
          u_amp=0.03, steps=9),
 ]
