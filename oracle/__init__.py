@@ -63,7 +63,8 @@ class _Cfg(C.Structure):
                 ("rates", C.c_double * 8), ("force", C.c_double * 3),
                 ("ubb_u", C.c_double * 3), ("ubb_rho", C.c_double),
                 ("M", C.c_void_p), ("Minv", C.c_void_p), ("S", C.c_void_p),
-                ("eq_kind", C.c_int32), ("mono_exp", C.c_void_p), ("Mmono_inv", C.c_void_p)]
+                ("eq_kind", C.c_int32), ("mono_exp", C.c_void_p), ("Mmono_inv", C.c_void_p),
+                ("wall_u", C.c_void_p)]
 
 
 EQ_KINDS = {"compressible": 0, "incompressible": 1, "moment_matched": 2}
@@ -164,7 +165,9 @@ class Domain:
     """Local lattice of nx*ny*nz cells; zghost=1 adds ghost planes z=-1 and z=nz (slab mode)."""
 
     def __init__(self, method: Method, nx: int, ny: int, nz: int, zghost: int = 0,
-                 flags: Optional[np.ndarray] = None):
+                 flags: Optional[np.ndarray] = None, wall_u: Optional[np.ndarray] = None):
+        """wall_u: optional per-cell wall velocity (3, nz+2*zghost, ny, nx) used by UBB cells instead
+        of method.ubb_u (per-link boundary data)."""
         self.m = method
         self.nx, self.ny, self.nz, self.zghost = nx, ny, nz, zghost
         self.Q = method.Q
@@ -192,6 +195,11 @@ class Domain:
             M, Minv, S = method.mrt_matrices()
             self._keep = [np.ascontiguousarray(M), np.ascontiguousarray(Minv), np.ascontiguousarray(S)]
             cfg.M, cfg.Minv, cfg.S = (_p(a) for a in self._keep)
+        if wall_u is not None:
+            wall_u = np.ascontiguousarray(wall_u, np.float64)
+            assert wall_u.shape == (3,) + self.shape[1:], wall_u.shape
+            self._wall_u = wall_u
+            cfg.wall_u = _p(wall_u)
         cfg.eq_kind = EQ_KINDS[method.equilibrium]
         if method.equilibrium == "moment_matched" or method.op == "cumulant":
             exps, minv = method.monomial_tables()

@@ -59,6 +59,9 @@ typedef struct {
     int32_t eq_kind;    /* ORA_EQ_*: which equilibrium SRT/TRT/MRT relax to */
     const int32_t *mono_exp;  /* ORA_EQ_MOMENT_MATCHED: Q x 3 exponents of the monomial basis */
     const double *Mmono_inv;  /* ... and the inverse of its moment matrix M_kq = c_q^e_k (row-major) */
+    const double *wall_u;     /* NULL, or the wall velocity of every storage cell, [3][storage cells]:
+                                 a UBB cell uses its own entry instead of ubb_u ("custom boundary data
+                                 ... e.g. the wall velocity", per boundary link) */
 } ora_cfg;
 
 #define ORA_EQ_COMPRESSIBLE 0    /* Eq. (3) with rho0 = rho */
@@ -603,6 +606,18 @@ static inline int64_t cell(const ora_cfg *cfg, int64_t x, int64_t y, int64_t z) 
     return ((z + cfg->zghost) * cfg->ny + y) * cfg->nx + x;
 }
 
+/* UBB term 6 w_q rho_w c_q.u_w of direction q for the wall cell `wall` (G8); u_w = ubb_u, or the
+ * wall cell's own velocity when a wall velocity field is given. */
+static double ubb_term_at(const ora_cfg *cfg, const ora_stencil_t *s, int q, int64_t wall) {
+    double uw[3] = {cfg->ubb_u[0], cfg->ubb_u[1], cfg->ubb_u[2]};
+    if (cfg->wall_u) {
+        int64_t n = plane_cells(cfg);
+        for (int d = 0; d < 3; ++d) uw[d] = cfg->wall_u[d * n + wall];
+    }
+    double cu = s->c[q][0] * uw[0] + s->c[q][1] * uw[1] + s->c[q][2] * uw[2];
+    return 6.0 * s->w[q] * cfg->ubb_rho * cu;
+}
+
 /* Pull-streaming value of direction q at fluid cell (x,y,z) from array `a` (O6):
  * neighbour n = x - c_q; fluid -> a_q(n); NOSLIP -> a_qbar(x); UBB -> a_qbar(x) + 6 w rho_w c.u_w */
 static double pull_value(const ora_cfg *cfg, const ora_stencil_t *s, const double *a, const uint8_t *flags,
@@ -613,10 +628,7 @@ static double pull_value(const ora_cfg *cfg, const ora_stencil_t *s, const doubl
     uint8_t fl = flags ? flags[nb] : FLAG_FLUID;
     if (fl == FLAG_FLUID) return a[q * Sq + nb];
     double v = a[s->opp[q] * Sq + self];
-    if (fl == FLAG_UBB) {
-        double cu = s->c[q][0] * cfg->ubb_u[0] + s->c[q][1] * cfg->ubb_u[1] + s->c[q][2] * cfg->ubb_u[2];
-        v += 6.0 * s->w[q] * cfg->ubb_rho * cu;
-    }
+    if (fl == FLAG_UBB) v += ubb_term_at(cfg, s, q, nb);
     return v;
 }
 
@@ -723,12 +735,6 @@ int ora_aa_even(const ora_cfg *cfg, double *a, const uint8_t *flags) {
     return 0;
 }
 
-/* UBB term 6 w_q rho_w c_q.u_w of direction q (G8). */
-static double ubb_term(const ora_cfg *cfg, const ora_stencil_t *s, int q) {
-    double cu = s->c[q][0] * cfg->ubb_u[0] + s->c[q][1] * cfg->ubb_u[1] + s->c[q][2] * cfg->ubb_u[2];
-    return 6.0 * s->w[q] * cfg->ubb_rho * cu;
-}
-
 /* Odd step: stream-pull, collide, stream-push: read a[x - c_q](qbar), write a[x + c_q](q).
  * With walls (same rules as the pull streaming O6, expressed in the AA slots):
  *   read : x - c_q a wall -> the bounced population C_qbar(x), stored by the even step in a[x](q),
@@ -756,7 +762,7 @@ int ora_aa_odd(const ora_cfg *cfg, double *a, const uint8_t *flags) {
                         f[q] = a[s.opp[q] * Sq + nb];
                     } else {
                         double v = a[q * Sq + self];
-                        if (fl == FLAG_UBB) v += ubb_term(cfg, &s, q);
+                        if (fl == FLAG_UBB) v += ubb_term_at(cfg, &s, q, nb);
                         f[q] = v;
                     }
                 }
@@ -768,7 +774,7 @@ int ora_aa_odd(const ora_cfg *cfg, double *a, const uint8_t *flags) {
                         a[q * Sq + tg] = out[q];
                     } else {
                         double v = out[q];
-                        if (fl == FLAG_UBB) v += ubb_term(cfg, &s, s.opp[q]);
+                        if (fl == FLAG_UBB) v += ubb_term_at(cfg, &s, s.opp[q], tg);
                         a[s.opp[q] * Sq + self] = v;
                     }
                 }

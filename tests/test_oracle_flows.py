@@ -289,3 +289,33 @@ def test_slab_decomposition_bit_identical():
     got = np.concatenate([a[:, 1:-1] for _, a, _ in slabs], axis=1)
     fluid = np.broadcast_to(fl == 0, ref.shape)
     np.testing.assert_array_equal(got[fluid], ref[fluid])
+
+
+@pytest.mark.parametrize("omega,tol,steps", [(1.0, 2e-12, 6000), (1.8, 1e-11, 60000)])
+def test_couette_two_moving_walls_wall_velocity_field(omega, tol, steps):
+    """Per-link wall data: both walls UBB, bottom u1 = (0.02, 0, 0), top u2 = (-0.03, 0, 0),
+    given as a per-cell wall-velocity field. The steady profile is exactly linear between the half-way
+    walls, u_x = u1 + (u2 - u1) (y - 1/2) / H; a uniform field equals the global ubb_u bit-exactly."""
+    H, u1, u2 = 16, 0.02, -0.03
+    fl = np.zeros((1, H + 2, 1), np.uint8)
+    fl[:, 0, :] = LI.UBB
+    fl[:, H + 1, :] = LI.UBB
+    wall = np.zeros((3, 1, H + 2, 1))
+    wall[0, :, 0, :] = u1
+    wall[0, :, H + 1, :] = u2
+    m = O.Method(Q=19, op="srt", rates=(omega,), nthreads=1)
+    d = O.Domain(m, 1, H + 2, 1, flags=fl, wall_u=wall)
+    f0 = d.init_equilibrium(np.ones((1, H + 2, 1)), np.zeros((3, 1, H + 2, 1)))
+    f = d.run_pull(f0, steps)
+    _, u = d.macroscopic(f, post_collision=True)
+    y = np.arange(1, H + 1)
+    np.testing.assert_allclose(u[0, 0, 1:H + 1, 0], u1 + (u2 - u1) * (y - 0.5) / H, rtol=0, atol=tol)
+    # uniform field == global velocity
+    uw = (0.05, -0.01, 0.02)
+    fl2 = LI.couette_flags(3, H, 2)
+    wall2 = np.broadcast_to(np.array(uw)[:, None, None, None], (3,) + fl2.shape).copy()
+    a = O.Domain(O.Method(Q=19, op="trt", rates=(1.6, 0.5), ubb_u=uw, nthreads=1), 3, H + 2, 2, flags=fl2)
+    b = O.Domain(O.Method(Q=19, op="trt", rates=(1.6, 0.5), nthreads=1), 3, H + 2, 2, flags=fl2, wall_u=wall2)
+    g0 = a.init_equilibrium(np.ones((2, H + 2, 3)), np.zeros((3, 2, H + 2, 3)))
+    np.testing.assert_array_equal(a.run_pull(g0, 7), b.run_pull(g0, 7))
+    np.testing.assert_array_equal(a.run_aa(g0, 7), b.run_aa(g0, 7))
