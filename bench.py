@@ -76,6 +76,11 @@ CONFIGS["eq_inc_c4"] = dict(CONFIGS["c4"], equilibrium="incompressible",
                             desc="D3Q19 TRT fp64 512^3 periodic, incompressible Eq. (3) (rho0 = 1)")
 CONFIGS["eq_mm_c4"] = dict(CONFIGS["c4"], equilibrium="moment_matched",
                            desc="D3Q19 TRT fp64 512^3 periodic, moment-matched equilibrium")
+# Index-list boundaries (Fig. 8 analog: separate boundary kernel vs compiled-in handling)
+CONFIGS["c3_links"] = dict(CONFIGS["c3"], boundary_mode="links",
+                           desc="D3Q27 cumulant fp64 384^3 lid-driven cavity, index-list boundaries (flag-free update + link kernel)")
+CONFIGS["c1_f64_links"] = dict(CONFIGS["c1_f64"], boundary_mode="links",
+                               desc="D3Q19 TRT+Guo fp64 256^3 channel, index-list boundaries")
 CONFIGS["eq_inc_c2"] = dict(CONFIGS["c2"], equilibrium="incompressible",
                             desc="D3Q19 weighted MRT fp32 AA 512^3 shear wave, incompressible Eq. (3)")
 
@@ -309,7 +314,8 @@ def main():
                             ubb_velocity=cfg.get("ubb", (0, 0, 0)), periodic=periodic, rank=rank, nranks=world,
                             nccl_id=nccl_id, device=local, stream=stream.cuda_stream, halo_mode=mode,
                             use_graph=use_graph, block_x=args.block_x, nccl_self=nccl_self,
-                            equilibrium=cfg.get("equilibrium", "compressible"))
+                            equilibrium=cfg.get("equilibrium", "compressible"),
+                            boundary_mode=cfg.get("boundary_mode", "flags"))
 
     sim, err = None, None
     try:

@@ -94,6 +94,19 @@ extern "C" {
 #define LBM_EQ_INCOMPRESSIBLE 1
 #define LBM_EQ_MOMENT_MATCHED 2
 
+/* Boundary handling:
+ * FLAGS: compiled into the update: the bulk kernel skips walls and near-wall fluid cells (one flag
+ *        byte), an edge kernel updates the near-wall cells from an index list with the bounce-back /
+ *        UBB substitution inline (default).
+ * LINKS: index-list boundaries: the flag field only seeds one list entry per boundary link (wall cell
+ *        b, direction q from b to the fluid cell b + c_q, per-link UBB term); the update kernels are
+ *        flag-free and a separate boundary kernel writes, before each pull step (AA: after each step),
+ *        the values the fluid cells stream from the wall cells. Per-link wall
+ *        velocities: lbm_boundary_links / lbm_set_link_velocities. Wall cells are updated like fluid
+ *        cells and hold meaningless values. Single slab only (LBM_EUNSUPPORTED otherwise). */
+#define LBM_BOUNDARY_FLAGS 0
+#define LBM_BOUNDARY_LINKS 1
+
 #define LBM_HALO_ZEROCOPY 0 /* one NCCL message per crossing population plane */
 #define LBM_HALO_PACKED 1   /* pack kernel + one message per face            */
 #define LBM_HALO_FUSED 2    /* pull + NCCL ranks: the boundary-plane kernel stores crossing
@@ -131,6 +144,7 @@ typedef struct lbm_config {
                                locally — exercises and times the multi-GPU exchange path on 1 GPU */
     int32_t equilibrium;    /* LBM_EQ_*: what SRT/TRT/MRT relax to (and what lbm_init_equilibrium writes);
                                other operators require LBM_EQ_COMPRESSIBLE (LBM_EUNSUPPORTED) */
+    int32_t boundary_mode;  /* LBM_BOUNDARY_FLAGS | LBM_BOUNDARY_LINKS (see below) */
 } lbm_config;
 
 typedef struct lbm_handle_s *lbm_handle;
@@ -245,6 +259,16 @@ int lbm_kernel_aa(const lbm_kernel_args *a, int32_t odd);
  * fluid cells that have a non-fluid neighbour (bit 7). nplanes includes ghost planes. */
 int lbm_prepare_flags(const uint8_t *host_flags, int64_t nx, int64_t ny, int64_t nplanes, int32_t ghost,
                       uint8_t *device_out, void *stream);
+
+/* Index-list boundaries (boundary_mode == LBM_BOUNDARY_LINKS). lbm_boundary_links returns the number
+ * of links n and, if the arrays are non-NULL (cap >= n, else LBM_EINVAL), per link i: cells[i] = global
+ * linear index x + nx (y + ny z) of the wall cell, dirs[i] = q (the fluid cell is at cells[i] + c_q,
+ * periodic wrap), types[i] = LBM_FLAG_NOSLIP | LBM_FLAG_UBB. Returns 0 in flag mode.
+ * lbm_set_link_velocities sets the wall velocity of every link (host uw[3*i + d], n == link count);
+ * UBB links then use 6 w_q rho_w c_q.u_w(i) (G8, rho_w = 1), no-slip links ignore it. Synchronises the
+ * handle's stream. The initial velocities are cfg.ubb_velocity. */
+int64_t lbm_boundary_links(lbm_handle h, int64_t *cells, int32_t *dirs, int32_t *types, int64_t cap);
+int lbm_set_link_velocities(lbm_handle h, const double *uw, int64_t n);
 
 /* ---- Kernel path of the bulk update kernels (process-wide; affects launches issued afterwards) ----
  * LBM_PATH_PLAIN : one thread per cell gathers its q populations straight into registers (ld.global.nc).

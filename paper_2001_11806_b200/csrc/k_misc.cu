@@ -34,6 +34,12 @@ void launch_set_pops(int Q, int dtype, const ReadArgs &a, void *f, const double 
     LBM_DISPATCH(Q, dtype, (k_set_pops<QQ, T><<<grid, block, 0, s>>>(a, static_cast<T *>(f), in)));
 }
 
+void launch_links(int Q, int dtype, const LinkArgs &a, void *f, cudaStream_t s) {
+    if (a.n == 0) return;
+    const unsigned blocks = (a.n + 255) / 256;
+    LBM_DISPATCH(Q, dtype, (k_links<QQ, T><<<blocks, 256, 0, s>>>(a, static_cast<T *>(f))));
+}
+
 void launch_macro(int Q, int dtype, const ReadArgs &a, const void *f, double *rho, double *u, dim3 grid, dim3 block, cudaStream_t s) {
     LBM_DISPATCH(Q, dtype, (k_macro<QQ, T><<<grid, block, 0, s>>>(a, static_cast<const T *>(f), rho, u)));
 }

@@ -660,6 +660,40 @@ __global__ void k_unpack_masked(const Geo geo, T *__restrict__ f, int zs, int di
 }
 
 // =======================================================================================
+// Index-list boundary handling: one entry per boundary link (wall cell b, direction q
+// pointing from b to the fluid cell x = b + c_q, per-link UBB term 6 w_q rho_w c_q.u_w, 0 for
+// no-slip). The separate boundary kernel prepares the wall cell's slot that the flag-free update
+// kernel streams from:
+//   mode 0, pull, before the step:    src[b](q)    = src[x](qbar) + term
+//   mode 1, AA, after the even step:  a[b](qbar)   = a[x](q) + term     (read by x in the odd step)
+//   mode 2, AA, after the odd step:   a[x](q)      = a[b](qbar) + term  (x's push toward b, bounced)
+// Every slot is written by one link and read by no other link of the same launch.
+// =======================================================================================
+struct LinkArgs {
+    int64_t Sq;
+    const uint32_t *wall, *fluid;  // storage cell indices
+    const uint8_t *dir;            // q
+    const double *term;            // per-link UBB term
+    uint32_t n;
+    int mode;
+};
+
+template <int Q, typename T>
+__global__ void k_links(const LinkArgs a, T *__restrict__ f) {
+    using S = Stencil<Q>;
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= a.n) return;
+    const int q = a.dir[i];
+    const int qb = S::opp(q);
+    const int64_t b = a.wall[i], x = a.fluid[i];
+    LBM_ASSERT(b < a.Sq && x < a.Sq && q > 0 && q < Q);
+    const T t = T(a.term[i]);
+    if (a.mode == 0) f[q * a.Sq + b] = f[qb * a.Sq + x] + t;
+    else if (a.mode == 1) f[qb * a.Sq + b] = f[q * a.Sq + x] + t;
+    else f[q * a.Sq + x] = f[qb * a.Sq + b] + t;
+}
+
+// =======================================================================================
 // Flag preprocessing and diagnostics
 // =======================================================================================
 // out = in | 0x80 for fluid cells with a non-fluid cell among their 26 neighbours (x, y wrap; z wraps

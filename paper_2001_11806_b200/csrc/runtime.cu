@@ -28,6 +28,12 @@ struct Slab {
     uint8_t *flags = nullptr;    // storage-indexed, with ghost planes
     uint32_t *edges = nullptr;   // storage indices of near-wall fluid cells (split wall mode)
     std::vector<int64_t> edge_off;  // edges of storage plane zs: [edge_off[zs], edge_off[zs+1])
+    // index-list boundaries (LBM_BOUNDARY_LINKS): device arrays + host copies for queries
+    uint32_t *link_wall = nullptr, *link_fluid = nullptr;
+    uint8_t *link_dir = nullptr;
+    double *link_term = nullptr;
+    std::vector<uint32_t> h_link_wall;
+    std::vector<uint8_t> h_link_dir, h_link_type;
     void *halo[4] = {nullptr, nullptr, nullptr, nullptr};  // packed mode: send up, send down, recv below, recv above
     int cur = 0;          // index of the array holding the current state (pull)
 };
@@ -64,6 +70,7 @@ struct lbm_handle_s {
     size_t scratch_bytes = 0;
     Timing timing;
     bool fused = false;       // halo through NVLink peer stores (LBM_HALO_FUSED)
+    bool links = false;       // index-list boundaries: flag-free update kernels + link kernel
     FusedState fst;
     std::string err;
     dim3 block;
@@ -136,7 +143,7 @@ void tend(lbm_handle_s *h, cudaStream_t s) { tbegin(h, s); }
 // z_begin + k * z_step, k < nplanes), one edge-list launch per contiguous run of planes.
 void launch_edges(lbm_handle_s *h, Slab &s, const StepArgs &a, EdgeLaunch fn, const void *src, void *dst, int z_begin,
                   int nplanes, int z_step, cudaStream_t st) {
-    if (!s.edges || !fn) return;
+    if (!s.edges || !fn || h->links) return;  // index-list boundaries: the update kernels are flag-free
     auto run = [&](int zlo, int zhi) {  // interior planes [zlo, zhi)
         const int64_t b = s.edge_off[zlo + h->g], e = s.edge_off[zhi + h->g];
         if (e <= b) return;
@@ -148,6 +155,23 @@ void launch_edges(lbm_handle_s *h, Slab &s, const StepArgs &a, EdgeLaunch fn, co
     if (z_step == 1) run(z_begin, z_begin + nplanes);
     else
         for (int k = 0; k < nplanes; ++k) run(z_begin + k * z_step, z_begin + k * z_step + 1);
+}
+
+// index-list boundary kernel (mode 0: pull, before the step; 1: AA after even; 2: AA after odd)
+void launch_links_fix(lbm_handle_s *h, Slab &s, void *f, int mode, cudaStream_t st) {
+    if (!h->links || s.h_link_wall.empty()) return;
+    LinkArgs a;
+    a.Sq = geo_of(h, s).Sq;
+    a.wall = s.link_wall;
+    a.fluid = s.link_fluid;
+    a.dir = s.link_dir;
+    a.term = s.link_term;
+    a.n = (uint32_t)s.h_link_wall.size();
+    a.mode = mode;
+    tbegin(h, st);
+    launch_links(h->Q, h->dtype, a, f, st);
+    tend(h, st);
+    h->launches++;
 }
 
 void launch_pull_range(lbm_handle_s *h, Slab &s, int z_begin, int nplanes, int z_step, cudaStream_t st,
@@ -316,8 +340,10 @@ int step_once(lbm_handle_s *h) {
         Slab &s = h->slabs[0];
         if (h->cfg.pattern == LBM_AA) {
             launch_aa_range(h, s, h->aa_parity, 0, s.nz, 1, st);
+            launch_links_fix(h, s, s.pdf[0], h->aa_parity ? 2 : 1, st);
             h->aa_parity ^= 1;
         } else {
+            launch_links_fix(h, s, s.pdf[s.cur], 0, st);
             launch_pull_range(h, s, 0, s.nz, 1, st);
             s.cur ^= 1;
         }
@@ -372,7 +398,7 @@ int step_once(lbm_handle_s *h) {
 
 bool graph_ok(const lbm_handle_s *h) { return h->cfg.use_graph == 1 && h->g == 0 && h->slabs.size() == 1 && !h->timing.on; }
 bool persistent_ok(const lbm_handle_s *h) {
-    return h->cfg.use_graph == 2 && h->g == 0 && h->slabs.size() == 1 && h->kern.persist_pull && h->kern.persist_aa;
+    return h->cfg.use_graph == 2 && !h->links && h->g == 0 && h->slabs.size() == 1 && h->kern.persist_pull && h->kern.persist_aa;
 }
 
 int run_graph_cycle(lbm_handle_s *h) {
@@ -431,6 +457,10 @@ int validate(const lbm_config *c) {
     if (c->collision == LBM_MRT && c->stencil != 19) return fail(nullptr, LBM_EUNSUPPORTED, "MRT is implemented for D3Q19");
     if (force && c->collision != LBM_SRT && c->collision != LBM_TRT)
         return fail(nullptr, LBM_EUNSUPPORTED, "forcing is implemented for SRT/TRT");
+    if (c->boundary_mode != LBM_BOUNDARY_FLAGS && c->boundary_mode != LBM_BOUNDARY_LINKS)
+        return fail(nullptr, LBM_EINVAL, "bad boundary_mode");
+    if (c->boundary_mode == LBM_BOUNDARY_LINKS && (c->nranks > 1 || c->n_local_slabs > 1 || c->nccl_self))
+        return fail(nullptr, LBM_EUNSUPPORTED, "index-list boundaries are implemented for a single slab");
     if (c->equilibrium < LBM_EQ_COMPRESSIBLE || c->equilibrium > LBM_EQ_MOMENT_MATCHED)
         return fail(nullptr, LBM_EINVAL, "bad equilibrium");
     if (c->equilibrium != LBM_EQ_COMPRESSIBLE && c->collision != LBM_SRT && c->collision != LBM_TRT &&
@@ -455,6 +485,22 @@ int validate(const lbm_config *c) {
                 }
         }
     }
+    return LBM_OK;
+}
+
+// per-link UBB terms 6 w_q rho_w c_q.u_w (rho_w = 1, G8) from per-link wall velocities uw[3*i+d];
+// no-slip links get 0
+int upload_link_terms(lbm_handle h, Slab &s, const double *uw) {
+    const size_t n = s.h_link_wall.size();
+    std::vector<double> term(n, 0.0);
+    for (size_t i = 0; i < n; ++i) {
+        if (s.h_link_type[i] != LBM_FLAG_UBB) continue;
+        const int q = s.h_link_dir[i];
+        const double w = h->Q == 19 ? Stencil<19>::w(q) : Stencil<27>::w(q);
+        const double cu = kC27[q][0] * uw[3 * i] + kC27[q][1] * uw[3 * i + 1] + kC27[q][2] * uw[3 * i + 2];
+        term[i] = 6.0 * w * cu;
+    }
+    if (n) CUDA_TRY(h, cudaMemcpy(s.link_term, term.data(), n * sizeof(double), cudaMemcpyHostToDevice));
     return LBM_OK;
 }
 
@@ -516,6 +562,29 @@ void lbm_config_default(lbm_config *c) {
 }
 
 const char *lbm_version(void) { return "b200-lbm 0.2 (sm_100a)"; }
+
+int64_t lbm_boundary_links(lbm_handle h, int64_t *cells, int32_t *dirs, int32_t *types, int64_t cap) {
+    if (!h) return LBM_EINVAL;
+    if (!h->links) return 0;
+    const Slab &s = h->slabs[0];
+    const int64_t n = (int64_t)s.h_link_wall.size();
+    if (cap < n && (cells || dirs || types)) return fail(h, LBM_EINVAL, "link buffer too small");
+    for (int64_t i = 0; i < n; ++i) {
+        if (cells) cells[i] = (int64_t)s.h_link_wall[i];  // single slab: storage index == global index
+        if (dirs) dirs[i] = s.h_link_dir[i];
+        if (types) types[i] = s.h_link_type[i];
+    }
+    return n;
+}
+
+int lbm_set_link_velocities(lbm_handle h, const double *uw, int64_t n) {
+    if (!h || !uw) return LBM_EINVAL;
+    if (!h->links) return fail(h, LBM_EINVAL, "no index-list boundaries (boundary_mode != LBM_BOUNDARY_LINKS)");
+    Slab &s = h->slabs[0];
+    if (n != (int64_t)s.h_link_wall.size()) return fail(h, LBM_EINVAL, "link count mismatch");
+    CUDA_TRY(h, cudaStreamSynchronize(h->stream));  // the terms may be in use by queued link kernels
+    return upload_link_terms(h, s, uw);
+}
 
 int lbm_set_kernel_path(int32_t path) {
     if (path < LBM_PATH_AUTO || path > LBM_PATH_STAGED) return LBM_EINVAL;
@@ -711,14 +780,16 @@ int lbm_create(const lbm_config *cfg, lbm_handle *out) {
     h->g = (P > 1 || h->use_nccl) ? 1 : 0;
     h->have_flags = cfg->flags != nullptr;
     h->have_force = cfg->force[0] != 0 || cfg->force[1] != 0 || cfg->force[2] != 0;
+    h->links = cfg->boundary_mode == LBM_BOUNDARY_LINKS && h->have_flags;
 
-    // kernel selection (SRT = TRT with equal rates)
+    // kernel selection (SRT = TRT with equal rates); index-list boundaries run the flag-free kernels
+    const int fm_bulk = h->have_flags && !h->links ? FM_BULK : FM_NONE;
     const bool force = h->have_force;
     if (cfg->pattern == LBM_PULL) {
-        h->kern = select_kernels(cfg->collision, h->Q, h->dtype, h->have_flags ? FM_BULK : FM_NONE, force, cfg->equilibrium);
+        h->kern = select_kernels(cfg->collision, h->Q, h->dtype, fm_bulk, force, cfg->equilibrium);
         if (!h->kern.pull) return fail(nullptr, LBM_EUNSUPPORTED, "no kernel instantiated for this combination");
     } else {
-        h->kern = select_kernels(cfg->collision, h->Q, h->dtype, h->have_flags ? FM_BULK : FM_NONE, force, cfg->equilibrium);
+        h->kern = select_kernels(cfg->collision, h->Q, h->dtype, fm_bulk, force, cfg->equilibrium);
         if (!h->kern.aa) return fail(nullptr, LBM_EUNSUPPORTED, "no kernel instantiated for this combination");
     }
     // rates into the kernel argument block
@@ -831,6 +902,43 @@ int lbm_create(const lbm_config *cfg, lbm_handle *out) {
                 }
                 cudaMemcpy(s.edges, list.data(), list.size() * sizeof(uint32_t), cudaMemcpyHostToDevice);
             }
+            if (h->links) {
+                // one entry per boundary link: wall cell b, direction q with b + c_q fluid (single slab:
+                // x, y, z all wrap), in storage order of b then q
+                std::vector<uint32_t> lf;
+                for (int zs = 0; zs < s.nz; ++zs)
+                    for (int64_t y = 0; y < h->ny; ++y)
+                        for (int64_t x = 0; x < h->nx; ++x) {
+                            const size_t b = ((size_t)zs * h->ny + y) * h->nx + x;
+                            const uint8_t t = hf[b] & 3;
+                            if (!t) continue;
+                            for (int q = 1; q < h->Q; ++q) {
+                                const int64_t xx = (x + kC27[q][0] + h->nx) % h->nx, yy = (y + kC27[q][1] + h->ny) % h->ny;
+                                const int64_t zz = (zs + kC27[q][2] + s.nz) % s.nz;
+                                const size_t nb = ((size_t)zz * h->ny + yy) * h->nx + xx;
+                                if (hf[nb] & 3) continue;
+                                s.h_link_wall.push_back((uint32_t)b);
+                                lf.push_back((uint32_t)nb);
+                                s.h_link_dir.push_back((uint8_t)q);
+                                s.h_link_type.push_back(t);
+                            }
+                        }
+                const size_t n = s.h_link_wall.size();
+                if (n) {
+                    if (cudaMalloc(&s.link_wall, n * 4) != cudaSuccess || cudaMalloc(&s.link_fluid, n * 4) != cudaSuccess ||
+                        cudaMalloc(&s.link_dir, n) != cudaSuccess || cudaMalloc(&s.link_term, n * 8) != cudaSuccess) {
+                        h->err = "cudaMalloc link list";
+                        return bail(LBM_EOOM);
+                    }
+                    cudaMemcpy(s.link_wall, s.h_link_wall.data(), n * 4, cudaMemcpyHostToDevice);
+                    cudaMemcpy(s.link_fluid, lf.data(), n * 4, cudaMemcpyHostToDevice);
+                    cudaMemcpy(s.link_dir, s.h_link_dir.data(), n, cudaMemcpyHostToDevice);
+                    std::vector<double> uw(3 * n);
+                    for (size_t i = 0; i < n; ++i)
+                        for (int d = 0; d < 3; ++d) uw[3 * i + d] = cfg->ubb_velocity[d];
+                    upload_link_terms(h, s, uw.data());
+                }
+            }
         }
     }
     if (h->use_nccl) {
@@ -891,6 +999,8 @@ int lbm_destroy(lbm_handle h) {
         for (void *p : s.halo) if (p) cudaFree(p);
         if (s.flags) cudaFree(s.flags);
         if (s.edges) cudaFree(s.edges);
+        for (void *p : {(void *)s.link_wall, (void *)s.link_fluid, (void *)s.link_dir, (void *)s.link_term})
+            if (p) cudaFree(p);
     }
     if (h->comm) ncclCommDestroy(h->comm);
     for (cudaEvent_t e : h->timing.ev) cudaEventDestroy(e);
@@ -1101,7 +1211,7 @@ static int read_common(lbm_handle h, ReadArgs &r, int raw, const Slab &s) {
         r.uw[d] = h->cfg.ubb_velocity[d];
     }
     r.geo = geo_of(h, s);
-    r.flags = s.flags;
+    r.flags = h->links ? nullptr : s.flags;  // link mode: the wall slots hold the bounced values
     return LBM_OK;
 }
 

@@ -29,6 +29,8 @@ HOST, DEVICE = 0, 1
 HALO_ZEROCOPY, HALO_PACKED, HALO_FUSED = 0, 1, 2
 PATH_AUTO, PATH_PLAIN, PATH_STAGED = 0, 1, 2
 EQ_COMPRESSIBLE, EQ_INCOMPRESSIBLE, EQ_MOMENT_MATCHED = 0, 1, 2
+BOUNDARY_FLAGS, BOUNDARY_LINKS = 0, 1
+BOUNDARY_MODES = {"flags": BOUNDARY_FLAGS, "links": BOUNDARY_LINKS}
 EQUILIBRIA = {"compressible": EQ_COMPRESSIBLE, "incompressible": EQ_INCOMPRESSIBLE, "moment_matched": EQ_MOMENT_MATCHED}
 KERNEL_PATHS = {"auto": PATH_AUTO, "plain": PATH_PLAIN, "staged": PATH_STAGED}
 
@@ -47,7 +49,7 @@ class lbm_config(C.Structure):
         ("nccl_id", C.c_void_p), ("n_local_slabs", C.c_int32), ("device", C.c_int32),
         ("stream", C.c_void_p), ("halo_mode", C.c_int32), ("use_graph", C.c_int32),
         ("block_x", C.c_int32), ("check_nan_every", C.c_int32), ("nccl_self", C.c_int32),
-        ("equilibrium", C.c_int32),
+        ("equilibrium", C.c_int32), ("boundary_mode", C.c_int32),
     ]
 
 
@@ -102,6 +104,8 @@ _SIGS = {
     "lbm_last_error": ([_P], C.c_char_p),
     "lbm_version": ([], C.c_char_p),
     "lbm_set_kernel_path": ([_I32], C.c_int),
+    "lbm_boundary_links": ([_P, _P, _P, _P, _I64], _I64),
+    "lbm_set_link_velocities": ([_P, _P, _I64], C.c_int),
     "lbm_get_kernel_path": ([], _I32),
 }
 for _name, (_args, _res) in _SIGS.items():
@@ -186,7 +190,8 @@ class Simulation:
                  rank: int = 0, nranks: int = 1, nccl_id: Optional[bytes] = None,
                  n_local_slabs: int = 1, device: int = 0, stream: Optional[int] = None,
                  halo_mode: int = HALO_ZEROCOPY, use_graph: bool = False, block_x: int = 0,
-                 check_nan_every: int = 0, nccl_self: bool = False, equilibrium: str = "compressible"):
+                 check_nan_every: int = 0, nccl_self: bool = False, equilibrium: str = "compressible",
+                 boundary_mode: str = "flags"):
         cfg = lbm_config()
         lbm_config_default(C.byref(cfg))
         nx, ny, nz = shape
@@ -221,6 +226,7 @@ class Simulation:
         cfg.check_nan_every = check_nan_every
         cfg.nccl_self = int(nccl_self)
         cfg.equilibrium = EQUILIBRIA[equilibrium] if isinstance(equilibrium, str) else int(equilibrium)
+        cfg.boundary_mode = BOUNDARY_MODES[boundary_mode] if isinstance(boundary_mode, str) else int(boundary_mode)
         self.cfg = cfg
         self.Q = stencil
         h = C.c_void_p()
@@ -231,6 +237,22 @@ class Simulation:
         _check(lbm_local_extent(self.h, ext.ctypes.data), self.h, "lbm_local_extent")
         self.z0, self.nz_local, self.nx, self.ny = (int(v) for v in ext)
         self.cells = self.nx * self.ny * self.nz_local
+
+    # -- index-list boundaries -------------------------------------------------------
+    def boundary_links(self):
+        """(cells, dirs, types) of the boundary links (empty in flag mode)."""
+        n = int(lbm_boundary_links(self.h, None, None, None, 0))
+        _check(n, self.h, "lbm_boundary_links")
+        cells, dirs, types = np.zeros(n, np.int64), np.zeros(n, np.int32), np.zeros(n, np.int32)
+        if n:
+            _check(int(lbm_boundary_links(self.h, cells.ctypes.data, dirs.ctypes.data, types.ctypes.data, n)), self.h,
+                   "lbm_boundary_links")
+        return cells, dirs, types
+
+    def set_link_velocities(self, uw: np.ndarray) -> None:
+        uw = np.ascontiguousarray(uw, np.float64)
+        assert uw.ndim == 2 and uw.shape[1] == 3
+        _check(lbm_set_link_velocities(self.h, uw.ctypes.data, uw.shape[0]), self.h, "lbm_set_link_velocities")
 
     # -- lifecycle ------------------------------------------------------------------
     def close(self):

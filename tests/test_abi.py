@@ -83,6 +83,8 @@ def test_slab_plan(L):
     (dict(periodic=(1, 0, 1)), -1),                             # non-periodic axis without walls
     (dict(nccl_self=True, n_local_slabs=2), -1),                # self-exchange is single-slab
     (dict(equilibrium=3), -1),                                  # unknown equilibrium kind
+    (dict(boundary_mode=2), -1),                                # unknown boundary mode
+    (dict(boundary_mode="links", n_local_slabs=2), -2),         # index-list boundaries: single slab
     (dict(stencil=27, collision="cumulant", rates=(1.9,), equilibrium="incompressible"), -2),
     (dict(collision="kbc", rates=(1.9,), equilibrium="moment_matched"), -2),
 ])
