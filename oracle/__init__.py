@@ -86,6 +86,9 @@ def lib():
             ("ora_collide_all", [P, P, P], C.c_int),
             ("ora_aa_even", [P, P, P], C.c_int),
             ("ora_aa_odd", [P, P, P], C.c_int),
+            ("ora_eso_even", [P, P, P], C.c_int),
+            ("ora_eso_odd", [P, P, P], C.c_int),
+            ("ora_eso_layout", [P, P, P, C.c_int, C.c_int], C.c_int),
             ("ora_init_equilibrium", [P, P, P, P], C.c_int),
             ("ora_macroscopic", [P, P, C.c_double, P, P], C.c_int),
             ("ora_collide_cell", [P, P, P], None),
@@ -269,6 +272,27 @@ class Domain:
         a = f0.copy()
         for t in range(n):
             (self.aa_even if t % 2 == 0 else self.aa_odd)(a)
+        return a
+
+    def eso_from_canonical(self, f: np.ndarray, parity: int = 0) -> np.ndarray:
+        """EsoTwist storage holding the canonical (pre-collision) state f."""
+        assert not self.zghost
+        f = np.ascontiguousarray(f, np.float64)
+        a = self.zeros()
+        assert lib().ora_eso_layout(self._pc(), _p(f), _p(a), parity, 1) == 0
+        return a
+
+    def eso_to_canonical(self, a: np.ndarray, parity: int) -> np.ndarray:
+        f = self.zeros()
+        assert lib().ora_eso_layout(self._pc(), _p(f), _p(np.ascontiguousarray(a)), parity, 0) == 0
+        return f
+
+    def run_eso(self, f0: np.ndarray, n: int) -> np.ndarray:
+        """EsoTwist even/odd steps on one array starting from the canonical state f0; returns the raw
+        array after n steps (slot layout of parity n % 2)."""
+        a = self.eso_from_canonical(f0, 0)
+        for t in range(n):
+            assert (lib().ora_eso_even if t % 2 == 0 else lib().ora_eso_odd)(self._pc(), _p(a), self._fl()) == 0
         return a
 
     # -- readout ---------------------------------------------------------------------

@@ -782,6 +782,88 @@ int ora_aa_odd(const ora_cfg *cfg, double *a, const uint8_t *flags) {
     return 0;
 }
 
+/* EsoTwist (Fig. 4), single array, no ghost planes, optional flag field. Every
+ * population is stored "on its link": the population travelling from cell y to y + c_q lives at
+ * location y + min(c_q, 0) (componentwise); seen from the arriving cell x that is x - max(c_q, 0).
+ * Both time steps touch the same locations of each cell (x and its neighbours in negative
+ * directions); they differ only in the slot ("twist" = the pointer swap q <-> qbar the paper replaces
+ * by an even and an odd kernel):
+ *   even: read arriving q at (x - c_q^+, q),    write departing q at (x + c_q^-, qbar)
+ *   odd : read arriving q at (x - c_q^+, qbar), write departing q at (x + c_q^-, q)
+ * (c^+ = max(c, 0), c^- = min(c, 0)); the departing slot of y is the next step's arriving slot of
+ * y + c_q. Walls (pull rule O6 / G8): a departing population q whose target x + c_q is a wall comes
+ * back as qbar next step; it is written, plus the UBB term of qbar, into the slot the next step reads
+ * arriving qbar from: the other slot of the same location. Reads need no wall rule.
+ * The canonical pre-collision state after n steps (= push F(n), G11) is a(x - c_q^+)(q) for even n,
+ * a(x - c_q^+)(qbar) for odd n. */
+static int64_t eso_loc(const ora_cfg *cfg, const ora_stencil_t *s, int64_t x, int64_t y, int64_t z, int q, int plus) {
+    int64_t d[3];
+    for (int k = 0; k < 3; ++k) {
+        int c = s->c[q][k];
+        d[k] = plus ? -(c > 0 ? c : 0) : (c < 0 ? c : 0); /* x - c^+  or  x + c^- */
+    }
+    return cell(cfg, x + d[0], y + d[1], z + d[2]);
+}
+
+static int ora_eso_step(const ora_cfg *cfg, double *a, const uint8_t *flags, int odd) {
+    if (cfg->zghost) return -1;
+    ora_stencil_t s;
+    build_stencil(cfg->Q, &s);
+    int64_t Sq = plane_cells(cfg);
+    set_threads(cfg);
+#pragma omp parallel for schedule(static)
+    for (int64_t z = 0; z < cfg->nz; ++z)
+        for (int64_t y = 0; y < cfg->ny; ++y)
+            for (int64_t x = 0; x < cfg->nx; ++x) {
+                int64_t self = cell(cfg, x, y, z);
+                if (flags && flags[self] != FLAG_FLUID) continue;
+                double f[27], out[27];
+                for (int q = 0; q < s.Q; ++q) {
+                    int slot = odd ? s.opp[q] : q;
+                    f[q] = a[slot * Sq + eso_loc(cfg, &s, x, y, z, q, 1)];
+                }
+                collide(cfg, &s, f, out);
+                for (int q = 0; q < s.Q; ++q) {
+                    int64_t loc = eso_loc(cfg, &s, x, y, z, q, 0);
+                    int64_t tg = cell(cfg, x + s.c[q][0], y + s.c[q][1], z + s.c[q][2]);
+                    uint8_t fl = flags ? flags[tg] : FLAG_FLUID;
+                    if (fl == FLAG_FLUID) {
+                        int slot = odd ? q : s.opp[q];
+                        a[slot * Sq + loc] = out[q];
+                    } else { /* bounced: comes back as qbar, read next step from the other slot */
+                        int slot = odd ? s.opp[q] : q;
+                        double v = out[q];
+                        if (fl == FLAG_UBB) v += ubb_term_at(cfg, &s, s.opp[q], tg);
+                        a[slot * Sq + loc] = v;
+                    }
+                }
+            }
+    return 0;
+}
+int ora_eso_even(const ora_cfg *cfg, double *a, const uint8_t *flags) { return ora_eso_step(cfg, a, flags, 0); }
+int ora_eso_odd(const ora_cfg *cfg, double *a, const uint8_t *flags) { return ora_eso_step(cfg, a, flags, 1); }
+
+/* Canonical state <-> EsoTwist storage after `parity` (0: even number of steps done, 1: odd).
+ * to_eso = 1: a(x - c_q^+)(slot) = f_q(x); to_eso = 0: f_q(x) = a(x - c_q^+)(slot). */
+int ora_eso_layout(const ora_cfg *cfg, double *canon, double *a, int parity, int to_eso) {
+    if (cfg->zghost) return -1;
+    ora_stencil_t s;
+    build_stencil(cfg->Q, &s);
+    int64_t Sq = plane_cells(cfg);
+    for (int64_t z = 0; z < cfg->nz; ++z)
+        for (int64_t y = 0; y < cfg->ny; ++y)
+            for (int64_t x = 0; x < cfg->nx; ++x) {
+                int64_t self = cell(cfg, x, y, z);
+                for (int q = 0; q < s.Q; ++q) {
+                    int slot = parity ? s.opp[q] : q;
+                    int64_t loc = eso_loc(cfg, &s, x, y, z, q, 1);
+                    if (to_eso) a[slot * Sq + loc] = canon[q * Sq + self];
+                    else canon[q * Sq + self] = a[slot * Sq + loc];
+                }
+            }
+    return 0;
+}
+
 /* ------------------------------------------------------------------------------------ */
 /* Initialisation and readout                                                              */
 /* ------------------------------------------------------------------------------------ */

@@ -93,6 +93,31 @@ def test_aa_with_walls_equals_push(op, Q, rates):
         np.testing.assert_array_equal(can[fl == 0], F3[q][fl == 0])
 
 
+@pytest.mark.parametrize("op,Q,rates", [("identity", 19, ()), ("srt", 19, (1.8,)), ("trt", 27, (1.6, 0.5)),
+                                         ("mrt", 19, (1.9, 1.3, 1.1, 0.8)), ("cumulant", 27, (1.95, 1.1))])
+@pytest.mark.parametrize("walls", [False, True])
+def test_esotwist_equals_push(op, Q, rates, walls):
+    """EsoTwist reproduces the push pattern F(n) bit-exactly for even and odd n, with and
+    without NoSlip/UBB walls; the canonical state is gathered here with np.roll (independent of the
+    oracle's layout routine): F_q(x) = a(x - c_q^+)(q) after even n, a(x - c_q^+)(qbar) after odd n."""
+    n = 7
+    fl = LI.random_obstacles(5, n, n, n, frac=0.2, ubb_frac=0.5) if walls else None
+    m = O.Method(Q=Q, op=op, rates=rates, ubb_u=(0.03, -0.02, 0.01), nthreads=1)
+    d = O.Domain(m, n, n, n, flags=fl)
+    f0 = _rand_f0(d, u_amp=0.03) * (1 + 0.01 * np.random.default_rng(9).uniform(-1, 1, d.shape))
+    fluid = np.ones((n, n, n), bool) if fl is None else fl == 0
+    c, _, opp = O.stencil_arrays(Q)
+    cp = np.maximum(c, 0)
+    for N in (1, 2, 5, 6):
+        a = d.run_eso(f0, N)
+        F = d.run_push(f0, N)
+        for q in range(Q):
+            slot = opp[q] if N % 2 else q
+            can = np.roll(a[slot], shift=(cp[q, 2], cp[q, 1], cp[q, 0]), axis=(0, 1, 2))
+            np.testing.assert_array_equal(can[fluid], F[q][fluid])
+        np.testing.assert_array_equal(d.eso_to_canonical(a, N % 2)[:, fluid], F[:, fluid])
+
+
 def test_aa_odd_parity_layout():
     """After an odd number of AA steps the array holds C(F(n-1)) with reversed slots:
     F(n)_q(y) = a[y - c_q](qbar) (P:864-869)."""
