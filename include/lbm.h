@@ -13,7 +13,7 @@
  *     Equilibrium Eq. (3), 2nd order, compressible (G1), or its incompressible and
  *     moment-matched variants (LBM_EQ_*).
  *   - Storage patterns: two-array stream-pull-collide and the single-array AA
- *     pattern.
+ *      and EsoTwist patterns.
  *   - Boundaries from a uint8 flag field, compiled into the kernel:
  *     0 = fluid, 1 = no-slip bounce-back, 2 = velocity bounce-back UBB (G8).
  *   - Multi-GPU: z-slab decomposition, one ghost plane per side; the populations crossing each z
@@ -75,6 +75,9 @@ extern "C" {
 
 #define LBM_PULL 0 /* two arrays, fused stream-pull-collide: state P(n) = (C o S)^n P(0) */
 #define LBM_AA 1   /* one array, AA pattern: state F(n) = (S o C)^n f0 (G11)            */
+#define LBM_ESOTWIST 2 /* one array, EsoTwist as even/odd kernels: populations stored on
+                          their links at x - c_q^+, slot q or qbar by parity; state F(n) as AA.
+                          Single slab, flag boundaries (LBM_EUNSUPPORTED otherwise) */
 
 #define LBM_FLAG_FLUID 0
 #define LBM_FLAG_NOSLIP 1
@@ -119,7 +122,7 @@ typedef struct lbm_config {
     int32_t collision; /* LBM_SRT .. LBM_IDENTITY */
     int32_t dtype;     /* LBM_F64 | LBM_F32: storage and arithmetic precision. Populations are
                           stored zero-centred, g_q = f_q - w_q (G12), in both precisions. */
-    int32_t pattern;   /* LBM_PULL | LBM_AA */
+    int32_t pattern;   /* LBM_PULL | LBM_AA | LBM_ESOTWIST */
     int32_t n_rates;
     double rates[8];      /* see the collision enum; every rate must lie in (0, 2) */
     double force[3];      /* Guo body force per cell (SRT/TRT only); all zero = force-free kernel */

@@ -23,6 +23,8 @@ struct Kernels {
     EdgeLaunch aa_edges = nullptr;
     PersistLaunch persist_pull = nullptr;  // walls inline (FM_INLINE) when a flag field exists
     PersistLaunch persist_aa = nullptr;
+    AALaunch eso = nullptr;          // EsoTwist even/odd (odd flag)
+    EdgeLaunch eso_edges = nullptr;  // near-wall cells; src != nullptr marks the odd step
 };
 
 Kernels select_trt(int Q, int dtype, int fm, bool force);

@@ -48,6 +48,22 @@ void aa_edge_launcher(const StepArgs &a, const void *src, void *f, const uint32_
     k_aa_odd_edges<Q, OP, T, FORCE><<<(n + 127) / 128, 128, 0, s>>>(a, static_cast<T *>(f), cells, n);
 }
 
+template <int Q, int OP, typename T, int FM, bool FORCE>
+void eso_launcher(const StepArgs &a, void *f, int odd, dim3 grid, dim3 block, cudaStream_t s) {
+    if (odd) k_eso<Q, OP, T, FM, FORCE, true><<<grid, block, 0, s>>>(a, static_cast<T *>(f));
+    else k_eso<Q, OP, T, FM, FORCE, false><<<grid, block, 0, s>>>(a, static_cast<T *>(f));
+}
+
+// EdgeLaunch has no parity argument; for EsoTwist the caller (runtime.cu) marks the odd step by a
+// non-null `src` (the kernel itself only uses `f`).
+template <int Q, int OP, typename T, bool FORCE>
+void eso_edge_launcher(const StepArgs &a, const void *src, void *f, const uint32_t *cells, uint32_t n, cudaStream_t s) {
+    if (n == 0) return;
+    const bool odd = src != nullptr;  // runtime passes a non-null marker for odd steps
+    if (odd) k_eso_edges<Q, OP, T, FORCE, true><<<(n + 127) / 128, 128, 0, s>>>(a, static_cast<T *>(f), cells, n);
+    else k_eso_edges<Q, OP, T, FORCE, false><<<(n + 127) / 128, 128, 0, s>>>(a, static_cast<T *>(f), cells, n);
+}
+
 template <int Q, int OP, typename T, int FM, bool FORCE, bool AA>
 int persistent_launcher(const StepArgs &a, void *A, void *B, int phase, int nsteps, cudaStream_t s) {
     auto kern = k_persistent<Q, OP, T, FM, FORCE, AA>;
@@ -94,6 +110,15 @@ PullLaunch pick_pull_fm(int fm) {
 }
 
 template <int Q, int OP, typename T, bool FORCE>
+AALaunch pick_eso_fm(int fm) {
+    switch (fm) {
+        case FM_INLINE: return &eso_launcher<Q, OP, T, FM_INLINE, FORCE>;
+        case FM_BULK: return &eso_launcher<Q, OP, T, FM_BULK, FORCE>;
+        default: return &eso_launcher<Q, OP, T, FM_NONE, FORCE>;
+    }
+}
+
+template <int Q, int OP, typename T, bool FORCE>
 AALaunch pick_aa_fm(int fm) {
     switch (fm) {
         case FM_INLINE: return &aa_launcher<Q, OP, T, FM_INLINE, FORCE>;
@@ -112,6 +137,8 @@ Kernels pick(int fm, bool force) {
             k.aa = pick_aa_fm<Q, OP, T, true>(fm);
             k.pull_edges = &pull_edge_launcher<Q, OP, T, true>;
             k.aa_edges = &aa_edge_launcher<Q, OP, T, true>;
+            k.eso = pick_eso_fm<Q, OP, T, true>(fm);
+            k.eso_edges = &eso_edge_launcher<Q, OP, T, true>;
             pick_persistent<Q, OP, T, true>(fm, k);
             return k;
         }
@@ -122,6 +149,8 @@ Kernels pick(int fm, bool force) {
     k.aa = pick_aa_fm<Q, OP, T, false>(fm);
     k.pull_edges = &pull_edge_launcher<Q, OP, T, false>;
     k.aa_edges = &aa_edge_launcher<Q, OP, T, false>;
+    k.eso = pick_eso_fm<Q, OP, T, false>(fm);
+    k.eso_edges = &eso_edge_launcher<Q, OP, T, false>;
     pick_persistent<Q, OP, T, false>(fm, k);
     return k;
 }

@@ -358,6 +358,77 @@ __global__ void __launch_bounds__(128) k_aa_odd_edges(const StepArgs a, T *__res
 }
 
 // =======================================================================================
+// EsoTwist (Fig. 4), one array. Populations live on their links: the one travelling from
+// y to y + c_q at location y + c_q^- (componentwise min(c, 0)), i.e. x - c_q^+ seen from the
+// arriving cell x. Both parities touch the same locations of a cell (itself and its neighbours in
+// negative directions) and differ only in the slot, the "twist" that replaces EsoTwist's pointer
+// swap by an even and an odd kernel:
+//   even: read arriving q at (x - c_q^+, q),    write departing q at (x + c_q^-, qbar)
+//   odd : read arriving q at (x - c_q^+, qbar), write departing q at (x + c_q^-, q)
+// Walls: a departing population toward a wall returns as qbar next step; it goes, plus the UBB term of
+// qbar, into the other slot of the same location (the one the next step reads). Reads need no rule.
+// Every slot a cell touches belongs to one of its links, so cells are independent (in place).
+// =======================================================================================
+__host__ __device__ constexpr int cpos(int c) { return c > 0 ? c : 0; }
+__host__ __device__ constexpr int cneg(int c) { return c < 0 ? c : 0; }
+
+template <int Q, int OP, typename T, int FM, bool FORCE, bool ODD>
+__device__ __forceinline__ void eso_cell(const StepArgs &a, T *__restrict__ f, int x, int y, int zs) {
+    using S = Stencil<Q>;
+    const Nbr n = neighbours(a.geo, x, y, zs);
+    const int64_t Sq = a.geo.Sq;
+    bool edge = FM == FM_EDGE;
+    const uint32_t self = nb_off(a.geo, n, 0, 0, 0);
+    if (FM == FM_INLINE) {
+        const uint8_t own = a.flags[self];
+        if (own & 3) return;
+        edge = (own & 0x80) != 0;
+    } else if (FM == FM_BULK) {
+        if (a.flags[self] != 0) return;
+    }
+    T g[Q];
+#pragma unroll
+    for (int q = 0; q < Q; ++q)
+        g[q] = f[(ODD ? S::opp(q) : q) * Sq + nb_off(a.geo, n, -cpos(S::cx(q)), -cpos(S::cy(q)), -cpos(S::cz(q)))];
+    const Rates<T> r = load_rates<T>(a);
+    collide<Q, OP, T, FORCE>(g, r);
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+        const uint32_t loc = nb_off(a.geo, n, cneg(S::cx(q)), cneg(S::cy(q)), cneg(S::cz(q)));
+        if (edge) {
+            const uint8_t fl = a.flags[nb_off(a.geo, n, S::cx(q), S::cy(q), S::cz(q))] & 3;
+            if (fl != 0) {  // toward a wall: back as qbar next step, into the other slot
+                T v = g[q];
+                if (fl == 2) v += ubb_term<Q, T>(a, S::opp(q));
+                f[(ODD ? S::opp(q) : q) * Sq + loc] = v;
+                continue;
+            }
+        }
+        f[(ODD ? q : S::opp(q)) * Sq + loc] = g[q];
+    }
+}
+
+template <int Q, int OP, typename T, int FM, bool FORCE, bool ODD>
+__global__ void __launch_bounds__(256, (MinBlocks<Q, OP, T>::aa)) k_eso(const StepArgs a, T *f) {
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    const int y = blockIdx.y * blockDim.y + threadIdx.y;
+    if (x >= a.geo.nx || y >= a.geo.ny) return;
+    eso_cell<Q, OP, T, FM, FORCE, ODD>(a, f, x, y, a.z_begin + (int)blockIdx.z * a.z_step + a.geo.g);
+}
+
+template <int Q, int OP, typename T, bool FORCE, bool ODD>
+__global__ void __launch_bounds__(128) k_eso_edges(const StepArgs a, T *f, const uint32_t *__restrict__ cells, uint32_t n) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint32_t c = cells[i];
+    LBM_ASSERT((int64_t)c < a.geo.Sq);
+    const uint32_t plane = (uint32_t)a.geo.nx * (uint32_t)a.geo.ny;
+    const int zs = (int)(c / plane);
+    const uint32_t r = c - (uint32_t)zs * plane;
+    eso_cell<Q, OP, T, FM_EDGE, FORCE, ODD>(a, f, (int)(r % (uint32_t)a.geo.nx), (int)(r / (uint32_t)a.geo.nx), zs);
+}
+
+// =======================================================================================
 // Persistent multi-step kernel for small single-slab domains (launch-bound otherwise, e.g. the
 // 32^3 config 0): one cooperative launch runs all n steps of an lbm_step call, cells grid-strided,
 // with a grid-wide barrier between steps instead of a kernel boundary. Walls are handled inline.
@@ -402,6 +473,7 @@ struct InitArgs {
     int profile;
     int product_eq;            // cumulant: product equilibrium (G2)
     int eq_kind;               // EQ_* of collide.cuh (SRT/TRT/MRT): Eq. (3) rho0 = rho / rho0 = 1 / moment-matched
+    int eso;                   // EsoTwist storage: f_q(x) goes to location x - c_q^+ (slot q)
 };
 
 __device__ __forceinline__ uint64_t splitmix64(uint64_t k) {
@@ -446,7 +518,12 @@ __global__ void k_init(const InitArgs a, T *__restrict__ f0, T *__restrict__ f1)
             ux = __dadd_rn(__dmul_rn(a.profile_amp, s), ux);
         }
     }
-    const uint32_t self = ((uint32_t)zs * (uint32_t)a.geo.ny + (uint32_t)y) * (uint32_t)a.geo.nx + (uint32_t)x;
+    const uint32_t self0 = ((uint32_t)zs * (uint32_t)a.geo.ny + (uint32_t)y) * (uint32_t)a.geo.nx + (uint32_t)x;
+    Nbr nb;
+    if (a.eso) nb = neighbours(a.geo, x, y, zs);
+    auto addr = [&](int q) -> uint32_t {
+        return a.eso ? nb_off(a.geo, nb, -cpos(S::cx(q)), -cpos(S::cy(q)), -cpos(S::cz(q))) : self0;
+    };
     const double drho = rho - 1.0;
     const double uu15 = 1.5 * (ux * ux + uy * uy + uz * uz);
 #pragma unroll
@@ -469,8 +546,8 @@ __global__ void k_init(const InitArgs a, T *__restrict__ f0, T *__restrict__ f1)
             if (a.eq_kind == EQ_MOMENT_MATCHED) gq += mm_delta<Q, double>(q, rho, ux, uy, uz);
         }
         if (a.product_eq && Q == 19) continue;
-        f0[q * a.geo.Sq + self] = T(gq);
-        if (f1) f1[q * a.geo.Sq + self] = T(gq);
+        f0[q * a.geo.Sq + addr(q)] = T(gq);
+        if (f1) f1[q * a.geo.Sq + addr(q)] = T(gq);
     }
     if (Q == 19 && a.product_eq) {
         // D3Q19 cumulant fixed point: basis moments = untruncated Maxwellian moments rho prod mu_e(u)
@@ -488,8 +565,8 @@ __global__ void k_init(const InitArgs a, T *__restrict__ f0, T *__restrict__ f1)
 #pragma unroll
         for (int q = 0; q < 19; ++q) {
             const double gq = f[q] - Stencil<19>::w(q);
-            f0[q * a.geo.Sq + self] = T(gq);
-            if (f1) f1[q * a.geo.Sq + self] = T(gq);
+            f0[q * a.geo.Sq + addr(q)] = T(gq);
+            if (f1) f1[q * a.geo.Sq + addr(q)] = T(gq);
         }
     }
 }
@@ -507,12 +584,18 @@ struct ReadArgs {
     const uint8_t *flags;  // AA odd gather with walls (same rule as k_aa_odd's reads)
     double uw[3];
     int incompressible;    // u = (j +- F/2) / rho0 with rho0 = 1 instead of rho
+    int eso;               // EsoTwist storage: F_q(x) = f(x - c_q^+)(eso_odd ? qbar : q)
+    int eso_odd;
 };
 
 template <int Q, typename T>
 __device__ __forceinline__ T read_canonical(const ReadArgs &a, const T *f, int x, int y, int zs, int q) {
     using S = Stencil<Q>;
     const uint32_t self = ((uint32_t)zs * (uint32_t)a.geo.ny + (uint32_t)y) * (uint32_t)a.geo.nx + (uint32_t)x;
+    if (a.eso && !a.raw) {
+        const Nbr n = neighbours(a.geo, x, y, zs);
+        return f[(a.eso_odd ? S::opp(q) : q) * a.geo.Sq + nb_off(a.geo, n, -cpos(S::cx(q)), -cpos(S::cy(q)), -cpos(S::cz(q)))];
+    }
     if (a.aa_odd && !a.raw) {
         const Nbr n = neighbours(a.geo, x, y, zs);
         const uint32_t o = nb_off(a.geo, n, -S::cx(q), -S::cy(q), -S::cz(q));
@@ -574,10 +657,16 @@ __global__ void k_set_pops(const ReadArgs a, T *__restrict__ f, const double *__
     const uint32_t self = ((uint32_t)(zl + a.geo.g) * (uint32_t)a.geo.ny + (uint32_t)y) * (uint32_t)a.geo.nx + (uint32_t)x;
     const int64_t nc = (int64_t)a.geo.nx * a.geo.ny * a.geo.nz;
     const int64_t i = ((int64_t)zl * a.geo.ny + y) * a.geo.nx + x;
+    const bool eso = a.eso && !a.raw;
+    Nbr n;
+    if (eso) n = neighbours(a.geo, x, y, zl + a.geo.g);
 #pragma unroll
     for (int q = 0; q < Q; ++q) {
         const double v = in[q * nc + i];
-        f[q * a.geo.Sq + self] = a.raw ? T(v) : T(v - S::w(q));
+        const int64_t addr = eso ? (int64_t)(a.eso_odd ? S::opp(q) : q) * a.geo.Sq +
+                                       nb_off(a.geo, n, -cpos(S::cx(q)), -cpos(S::cy(q)), -cpos(S::cz(q)))
+                                 : (int64_t)q * a.geo.Sq + self;
+        f[addr] = a.raw ? T(v) : T(v - S::w(q));
     }
 }
 

@@ -193,6 +193,21 @@ void launch_pull_range(lbm_handle_s *h, Slab &s, int z_begin, int nplanes, int z
     launch_edges(h, s, a, h->kern.pull_edges, s.pdf[s.cur], s.pdf[1 - s.cur], z_begin, nplanes, z_step, st);
 }
 
+void launch_eso_range(lbm_handle_s *h, Slab &s, int odd, int z_begin, int nplanes, int z_step, cudaStream_t st) {
+    if (nplanes <= 0) return;
+    StepArgs a = h->base;
+    a.geo = geo_of(h, s);
+    a.z_begin = z_begin;
+    a.z_step = z_step;
+    a.flags = s.flags;
+    tbegin(h, st);
+    h->kern.eso(a, s.pdf[0], odd, grid_for(h, nplanes), h->block, st);
+    tend(h, st);
+    h->launches++;
+    // near-wall cells (split wall mode); a non-null src marks the odd parity for the edge launcher
+    launch_edges(h, s, a, h->kern.eso_edges, odd ? s.pdf[0] : nullptr, s.pdf[0], z_begin, nplanes, z_step, st);
+}
+
 void launch_aa_range(lbm_handle_s *h, Slab &s, int odd, int z_begin, int nplanes, int z_step, cudaStream_t st) {
     if (nplanes <= 0) return;
     StepArgs a = h->base;
@@ -338,7 +353,10 @@ int step_once(lbm_handle_s *h) {
     cudaStream_t st = h->stream;
     if (h->g == 0) {
         Slab &s = h->slabs[0];
-        if (h->cfg.pattern == LBM_AA) {
+        if (h->cfg.pattern == LBM_ESOTWIST) {
+            launch_eso_range(h, s, h->aa_parity, 0, s.nz, 1, st);
+            h->aa_parity ^= 1;
+        } else if (h->cfg.pattern == LBM_AA) {
             launch_aa_range(h, s, h->aa_parity, 0, s.nz, 1, st);
             launch_links_fix(h, s, s.pdf[0], h->aa_parity ? 2 : 1, st);
             h->aa_parity ^= 1;
@@ -398,18 +416,18 @@ int step_once(lbm_handle_s *h) {
 
 bool graph_ok(const lbm_handle_s *h) { return h->cfg.use_graph == 1 && h->g == 0 && h->slabs.size() == 1 && !h->timing.on; }
 bool persistent_ok(const lbm_handle_s *h) {
-    return h->cfg.use_graph == 2 && !h->links && h->g == 0 && h->slabs.size() == 1 && h->kern.persist_pull && h->kern.persist_aa;
+    return h->cfg.use_graph == 2 && !h->links && h->cfg.pattern != LBM_ESOTWIST && h->g == 0 && h->slabs.size() == 1 && h->kern.persist_pull && h->kern.persist_aa;
 }
 
 int run_graph_cycle(lbm_handle_s *h) {
     // one cycle = two steps (pull: src->dst->src; AA: even+odd), replayed; state returns to the same slots
-    if (!h->graph || h->graph_parity != (h->cfg.pattern == LBM_AA ? h->aa_parity : h->slabs[0].cur)) {
+    if (!h->graph || h->graph_parity != (h->cfg.pattern != LBM_PULL ? h->aa_parity : h->slabs[0].cur)) {
         if (h->graph) {
             cudaGraphExecDestroy(h->graph);
             h->graph = nullptr;
         }
         cudaGraph_t gr;
-        const int par = h->cfg.pattern == LBM_AA ? h->aa_parity : h->slabs[0].cur;
+        const int par = h->cfg.pattern != LBM_PULL ? h->aa_parity : h->slabs[0].cur;
         CUDA_TRY(h, cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
         const int64_t l0 = h->launches;
         step_once(h);
@@ -431,7 +449,11 @@ int validate(const lbm_config *c) {
     if (c->stencil != 19 && c->stencil != 27) return fail(nullptr, LBM_EINVAL, "stencil must be 19 or 27");
     if (c->collision < 0 || c->collision > 6) return fail(nullptr, LBM_EINVAL, "bad collision");
     if (c->dtype != LBM_F64 && c->dtype != LBM_F32) return fail(nullptr, LBM_EINVAL, "bad dtype");
-    if (c->pattern != LBM_PULL && c->pattern != LBM_AA) return fail(nullptr, LBM_EINVAL, "bad pattern");
+    if (c->pattern != LBM_PULL && c->pattern != LBM_AA && c->pattern != LBM_ESOTWIST) return fail(nullptr, LBM_EINVAL, "bad pattern");
+    if (c->pattern == LBM_ESOTWIST && (c->nranks > 1 || c->n_local_slabs > 1 || c->nccl_self))
+        return fail(nullptr, LBM_EUNSUPPORTED, "EsoTwist is implemented for a single slab");
+    if (c->pattern == LBM_ESOTWIST && c->boundary_mode == LBM_BOUNDARY_LINKS)
+        return fail(nullptr, LBM_EUNSUPPORTED, "index-list boundaries are implemented for the pull and AA patterns");
     const int need[] = {1, 2, 1, 1, 0, 2, 1};
     if (c->n_rates < need[c->collision] || c->n_rates > 8) return fail(nullptr, LBM_EINVAL, "wrong number of rates");
     for (int i = 0; i < c->n_rates; ++i)
@@ -790,7 +812,8 @@ int lbm_create(const lbm_config *cfg, lbm_handle *out) {
         if (!h->kern.pull) return fail(nullptr, LBM_EUNSUPPORTED, "no kernel instantiated for this combination");
     } else {
         h->kern = select_kernels(cfg->collision, h->Q, h->dtype, fm_bulk, force, cfg->equilibrium);
-        if (!h->kern.aa) return fail(nullptr, LBM_EUNSUPPORTED, "no kernel instantiated for this combination");
+        if (!(cfg->pattern == LBM_ESOTWIST ? (void *)h->kern.eso : (void *)h->kern.aa))
+            return fail(nullptr, LBM_EUNSUPPORTED, "no kernel instantiated for this combination");
     }
     // rates into the kernel argument block
     StepArgs &b = h->base;
@@ -1049,6 +1072,7 @@ static int init_common(lbm_handle h, InitArgs &a, const double *rho, const doubl
         b.nz_g = h->nzg;
         b.product_eq = h->op == LBM_CUMULANT;
         b.eq_kind = h->cfg.equilibrium;
+        b.eso = h->cfg.pattern == LBM_ESOTWIST;
         if (a.mode == 0) {
             // the arrays cover the concatenated local slabs; ghost planes are filled by exchange
             b.rho = drho + off;
@@ -1204,6 +1228,8 @@ int lbm_kernel_time_ms(lbm_handle h, double *ms, int64_t *launches) {
 static int read_common(lbm_handle h, ReadArgs &r, int raw, const Slab &s) {
     r.raw = raw;
     r.aa_odd = (h->cfg.pattern == LBM_AA) && h->aa_parity;
+    r.eso = h->cfg.pattern == LBM_ESOTWIST;
+    r.eso_odd = h->aa_parity;
     r.fsign = h->cfg.pattern == LBM_PULL ? -1.0 : 1.0;
     r.incompressible = h->cfg.equilibrium == LBM_EQ_INCOMPRESSIBLE;
     for (int d = 0; d < 3; ++d) {
@@ -1373,6 +1399,7 @@ int lbm_pack_face(lbm_handle h, int64_t z, int32_t dir, double *out, int32_t whe
     }
     if (!sp || zz < 0) return fail(h, LBM_EINVAL, "plane out of range");
     if (h->cfg.pattern == LBM_AA && h->aa_parity) return fail(h, LBM_EUNSUPPORTED, "pack_face on an odd AA state");
+    if (h->cfg.pattern == LBM_ESOTWIST) return fail(h, LBM_EUNSUPPORTED, "pack_face on an EsoTwist state");
     const size_t n = (size_t)h->nx * h->ny * (h->Q == 19 ? 5 : 9);
     double *dst = out;
     if (where == LBM_HOST) {

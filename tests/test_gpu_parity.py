@@ -64,6 +64,25 @@ def test_aa_slots_bit_exact(Q, geometry):
                                       _centre_free(d.run_push(m, n), Q, True)[mask])
 
 
+@pytest.mark.parametrize("Q", [19, 27])
+@pytest.mark.parametrize("geometry", ["periodic", "obstacles"])
+def test_esotwist_slots_bit_exact(Q, geometry):
+    """EsoTwist storage (identity collision, dyadic markers): raw array == oracle's EsoTwist array after
+    every step, and the canonical gather == the push pattern; both parities."""
+    case = Case("emark", (9, 7, 6), Q, "identity", (), "f64", pattern="esotwist", geometry=geometry)
+    sim = make_sim(case)
+    m = _markers(Q, case.shape, 3)
+    d = O.Domain(O.Method(Q=Q, op="identity", rates=()), *case.shape, flags=case.flags())
+    sim.set_populations(d.eso_from_canonical(m, 0), raw=True)  # storage layout written directly
+    _, w, _ = O.stencil_arrays(Q)
+    mask = fluid_mask(case, Q)
+    for n in (1, 2, 3):
+        sim.step(1)
+        raw_ref = d.run_eso(m, n)  # identity: the stored values are the markers (no w offset)
+        np.testing.assert_array_equal(sim.populations(raw=True)[mask], raw_ref[mask])
+        np.testing.assert_array_equal(sim.populations(raw=False)[mask], (d.run_push(m, n) + w[:, None, None, None])[mask])
+
+
 def _centre_free(f_raw_stream, Q, add_w):
     # identity collision: canonical value = raw marker + w_q (the library adds w back)
     _, w, _ = O.stencil_arrays(Q)
@@ -208,6 +227,18 @@ PARITY = [
     Case("cum19_f32_channel", (16, 20, 12), 19, "cumulant", (1.9,), "f32", geometry="channel", u_amp=0.03, steps=20),
     Case("cum19_aa_f64_obst", (17, 13, 11), 19, "cumulant", (1.95, 1.1, 1.0, 1.2), "f64", pattern="aa",
          geometry="obstacles", ubb=(0.02, -0.01, 0.03), u_amp=0.05, steps=15),
+    # EsoTwist
+    Case("eso_trt_force_f64_odd", (18, 14, 10), 19, "trt", (1.6, 0.5), "f64", pattern="esotwist", force=(1e-5, 2e-5, 0),
+         steps=21),
+    Case("eso_srt_q27_f32_even", (18, 14, 10), 27, "srt", (1.7,), "f32", pattern="esotwist", steps=12),
+    Case("eso_trt_obstacles_odd", (17, 13, 11), 19, "trt", (1.6, 0.5), "f64", pattern="esotwist", force=(1e-5, 0, 0),
+         geometry="obstacles", ubb=(0.02, -0.01, 0.03), steps=15),
+    Case("eso_cumulant_cavity", (14, 14, 14), 27, "cumulant", (1.95,), "f64", pattern="esotwist", geometry="cavity",
+         ubb=(0.05, 0, 0), steps=20),
+    Case("eso_mrt_f32_channel", (16, 20, 12), 19, "mrt", (1.9, 1.3, 1.1, 0.8), "f32", pattern="esotwist",
+         geometry="channel", steps=13),
+    Case("eso_kbc_obst_f64", (17, 13, 11), 19, "kbc", (1.95,), "f64", pattern="esotwist", geometry="obstacles",
+         ubb=(0.02, -0.01, 0.03), u_amp=0.05, steps=14),
 ]
 
 
