@@ -56,6 +56,14 @@ CONFIGS["c4_strong"] = dict(CONFIGS["c4"], shape=(1024, 1024, 1024), weak=False,
                            desc="D3Q19 TRT fp32 1024^3 strong scaling (BASELINE config 4, second part); needs >= 2 GPUs "
                                 "for the 32-bit slab offsets (81.6 GB/GPU at P = 2)")
 CONFIGS["c3_aa"] = dict(CONFIGS["c3"], pattern="aa", desc="D3Q27 cumulant fp64 384^3 lid-driven cavity, AA pattern")
+# C1/C3 run with index-list boundaries (the faster of the two boundary implementations on the B200,
+# DESIGN.md section 6); the *_flags lines keep the compiled-in flag handling for comparison.
+CONFIGS["c3_flags"] = dict(CONFIGS["c3"], desc=CONFIGS["c3"]["desc"] + ", compiled-in flag boundaries")
+CONFIGS["c3"] = dict(CONFIGS["c3"], boundary_mode="links", desc=CONFIGS["c3"]["desc"] + ", index-list boundaries")
+CONFIGS["c1_f64_flags"] = dict(CONFIGS["c1_f64"], desc=CONFIGS["c1_f64"]["desc"] + ", compiled-in flag boundaries")
+CONFIGS["c1_f32_flags"] = dict(CONFIGS["c1_f32"], desc=CONFIGS["c1_f32"]["desc"] + ", compiled-in flag boundaries")
+CONFIGS["c1_f64"] = dict(CONFIGS["c1_f64"], boundary_mode="links", desc=CONFIGS["c1_f64"]["desc"] + ", index-list boundaries")
+CONFIGS["c1_f32"] = dict(CONFIGS["c1_f32"], boundary_mode="links", desc=CONFIGS["c1_f32"]["desc"] + ", index-list boundaries")
 CONFIGS["c3_periodic"] = dict(CONFIGS["c3"], geometry="periodic", init=("random", 1e-3, 0.01),
                               desc="D3Q27 cumulant fp64 384^3 periodic pull (C3 without walls, diagnostic)")
 # Operator comparison in the spirit of Fig. 9: the same D3Q19 AA fp64 periodic
@@ -77,10 +85,6 @@ CONFIGS["eq_inc_c4"] = dict(CONFIGS["c4"], equilibrium="incompressible",
 CONFIGS["eq_mm_c4"] = dict(CONFIGS["c4"], equilibrium="moment_matched",
                            desc="D3Q19 TRT fp64 512^3 periodic, moment-matched equilibrium")
 # Index-list boundaries (Fig. 8 analog: separate boundary kernel vs compiled-in handling)
-CONFIGS["c3_links"] = dict(CONFIGS["c3"], boundary_mode="links",
-                           desc="D3Q27 cumulant fp64 384^3 lid-driven cavity, index-list boundaries (flag-free update + link kernel)")
-CONFIGS["c1_f64_links"] = dict(CONFIGS["c1_f64"], boundary_mode="links",
-                               desc="D3Q19 TRT+Guo fp64 256^3 channel, index-list boundaries")
 # EsoTwist (Fig. 7 analog with the other single-array pattern)
 CONFIGS["eso_c4"] = dict(CONFIGS["c4"], pattern="esotwist", desc="D3Q19 TRT fp64 512^3 periodic, EsoTwist single array")
 CONFIGS["eso_c3"] = dict(CONFIGS["c3"], pattern="esotwist", desc="D3Q27 cumulant fp64 384^3 cavity, EsoTwist single array")

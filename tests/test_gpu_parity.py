@@ -460,15 +460,17 @@ def _oracle_at(case, pts, k):
     return np.array(out).T
 
 
-@pytest.mark.parametrize("name", ["c0", "c1_f64", "c1_f32", "c2", "c3", "c4"])
-def test_full_size_sampled_parity(name):
+@pytest.mark.parametrize("name,boundary_mode", [("c0", "flags"), ("c1_f64", "flags"), ("c1_f32", "flags"), ("c2", "flags"),
+                                                ("c3", "flags"), ("c4", "flags"), ("c1_f64", "links"),
+                                                ("c1_f32", "links"), ("c3", "links")])
+def test_full_size_sampled_parity(name, boundary_mode):
     base = FULL[name]
     # random near-equilibrium start (instead of rest) so every sampled cell does non-trivial work
     case = Case(base.name, base.shape, base.Q, base.op, base.rates, base.dtype, base.pattern, base.force,
                 base.geometry, base.ubb, init="shear" if base.init == "shear" else "random",
                 rho_amp=base.rho_amp if base.init == "shear" else 1e-3, u_amp=base.u_amp if base.init == "shear" else 0.01)
     k = 2 if case.pattern == "aa" else 3
-    sim = make_sim(case)
+    sim = make_sim(case, boundary_mode=boundary_mode)
     init_sim(sim, case)
     sim.step(k)
     pts = _sample_cells(case)
