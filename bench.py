@@ -108,8 +108,11 @@ def fluid_cells(cfg, shape, flags):
 
 
 def bytes_per_cell(cfg, flags):
+    """2 q s, + 1 B flag where the update kernel reads a flag field (not with index-list
+    boundaries, whose update kernels are flag-free)."""
     s = 8 if cfg["dtype"] == "f64" else 4
-    return 2 * cfg["Q"] * s + (1 if flags is not None else 0)
+    reads_flags = flags is not None and cfg.get("boundary_mode", "flags") == "flags"
+    return 2 * cfg["Q"] * s + (1 if reads_flags else 0)
 
 
 def load_peaks():
