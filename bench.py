@@ -87,7 +87,7 @@ CONFIGS["eq_mm_c4"] = dict(CONFIGS["c4"], equilibrium="moment_matched",
 # Index-list boundaries (Fig. 8 analog: separate boundary kernel vs compiled-in handling)
 # EsoTwist (Fig. 7 analog with the other single-array pattern)
 CONFIGS["eso_c4"] = dict(CONFIGS["c4"], pattern="esotwist", desc="D3Q19 TRT fp64 512^3 periodic, EsoTwist single array")
-CONFIGS["eso_c3"] = dict(CONFIGS["c3"], pattern="esotwist", desc="D3Q27 cumulant fp64 384^3 cavity, EsoTwist single array")
+CONFIGS["eso_c3"] = dict(CONFIGS["c3_flags"], pattern="esotwist", desc="D3Q27 cumulant fp64 384^3 cavity, EsoTwist single array")
 CONFIGS["eso_c2"] = dict(CONFIGS["c2"], pattern="esotwist", desc="D3Q19 weighted MRT fp32 512^3 shear wave, EsoTwist")
 CONFIGS["eq_inc_c2"] = dict(CONFIGS["c2"], equilibrium="incompressible",
                             desc="D3Q19 weighted MRT fp32 AA 512^3 shear wave, incompressible Eq. (3)")

@@ -60,7 +60,8 @@ extern "C" {
 
 #define LBM_SRT 0      /* rates = [omega]                                              */
 #define LBM_TRT 1      /* rates = [omega_even, omega_odd]                              */
-#define LBM_MRT 2      /* rates = [omega_shear, omega_bulk, omega_3, omega_4] (D3Q19)  */
+#define LBM_MRT 2      /* rates = [omega_shear, omega_bulk, omega_3, omega_4] (D3Q19), or one rate per
+                          moment via lbm_config.n_row_rates / row_rates                  */
 #define LBM_CUMULANT 3 /* rates = [omega_shear, omega_bulk, omega_3..omega_6]; missing = 1. D3Q27, and
                           D3Q19 (the cumulants of the 19 basis monomials, orders 2-4;
                           omega_5, omega_6 unused) */
@@ -106,7 +107,8 @@ extern "C" {
  *        flag-free and a separate boundary kernel writes, before each pull step (AA: after each step),
  *        the values the fluid cells stream from the wall cells. Per-link wall
  *        velocities: lbm_boundary_links / lbm_set_link_velocities. Wall cells are updated like fluid
- *        cells and hold meaningless values. Single slab only (LBM_EUNSUPPORTED otherwise). */
+ *        cells and hold meaningless values. Pull: any slab decomposition (the link kernel also fills
+ *        the wall slots of ghost planes, after the exchange); AA: single slab (LBM_EUNSUPPORTED). */
 #define LBM_BOUNDARY_FLAGS 0
 #define LBM_BOUNDARY_LINKS 1
 
@@ -148,6 +150,13 @@ typedef struct lbm_config {
     int32_t equilibrium;    /* LBM_EQ_*: what SRT/TRT/MRT relax to (and what lbm_init_equilibrium writes);
                                other operators require LBM_EQ_COMPRESSIBLE (LBM_EUNSUPPORTED) */
     int32_t boundary_mode;  /* LBM_BOUNDARY_FLAGS | LBM_BOUNDARY_LINKS (see below) */
+    int32_t n_row_rates;    /* 0, or 15 with LBM_MRT: one relaxation rate per non-conserved moment,
+                               row_rates[k] for the rows of the weighted Gram-Schmidt basis in the paper's
+                               order: x^2-y^2, xy, xz, y^2-z^2, yz (orthogonalised), bulk,
+                               x^2y, x^2z, xy^2, xz^2, y^2z, yz^2, x^2y^2, x^2z^2, y^2z^2 (orthogonalised);
+                               rates[] is then ignored (D3Q19, compressible equilibrium, not in the
+                               low-level kernel ABI) */
+    double row_rates[15];
 } lbm_config;
 
 typedef struct lbm_handle_s *lbm_handle;

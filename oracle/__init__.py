@@ -155,6 +155,9 @@ class Method:
             Minv = methods.mat_inverse(Mr)
             if self.op == "kbc":  # row parts: 0 conserved, 1 shear (s), 2 higher order (h)
                 S = [0.0 if g == "conserved" else 1.0 if g == "shear" else 2.0 for g in groups]
+            elif len(self.rates) == 15:  # one rate per non-conserved row, in the basis order
+                assert groups[:4] == ["conserved"] * 4
+                S = [0.0] * 4 + [float(v) for v in self.rates]
             else:
                 r = list(self.rates) + [1.0] * 4
                 S = methods.mrt_rates_per_row(groups, r[0], r[1], r[2], r[3])

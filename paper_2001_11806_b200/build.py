@@ -15,7 +15,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "liblbm_b200.so")
 OBJ = os.path.join(HERE, "build_obj")
-SOURCES = ["runtime.cu", "k_misc.cu", "k_trt.cu", "k_mrt.cu", "k_cumulant.cu", "k_identity.cu", "k_fused.cu", "k_les.cu", "k_eq_inc.cu", "k_eq_mm.cu", "k_cumulant19.cu", "k_kbc27.cu"]
+SOURCES = ["runtime.cu", "k_misc.cu", "k_trt.cu", "k_mrt.cu", "k_cumulant.cu", "k_identity.cu", "k_fused.cu", "k_les.cu", "k_eq_inc.cu", "k_eq_mm.cu", "k_cumulant19.cu", "k_kbc27.cu", "k_mrt_rows.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 

@@ -45,7 +45,7 @@ __device__ __forceinline__ T mm_delta(int q, T rho, T ux, T uy, T uz) {
 
 template <typename T>
 struct Rates {
-    T r[8];
+    T r[16];
     T F[3];
 };
 
@@ -271,6 +271,72 @@ __device__ __forceinline__ void collide_mrt19(T (&g)[19], const Rates<T> &p) {
         }
     }
 }
+
+// ---------------------------------------------------------------------------------------
+// MRT with one relaxation rate per moment ("a relaxation rate separately for each of the
+// previously selected moments"), D3Q19. Here the rows themselves matter (G6), so the basis is the
+// paper's: the weighted Gram-Schmidt of the monomial sequence sorted by order, then
+// lexicographically with the highest power of x first, the second-order moments split into shear
+// and bulk parts with shear first:
+//   1 | x y z | x^2-y^2, xy, xz, y^2-z^2, yz, x^2+y^2+z^2 | x^2y x^2z xy^2 xz^2 y^2z yz^2 | x^2y^2 x^2z^2 y^2z^2
+// (the 8 monomials with every exponent >= 1 have zero rows on D3Q19 and are dropped).
+// The orthogonalisation runs at compile time on the value vectors P(c_q); rows are used only through
+// the projector w P <P, .> / <P, P>_w, so their normalisation is irrelevant. rates r[0..14] belong to
+// the 15 non-conserved rows in this order.
+// ---------------------------------------------------------------------------------------
+__host__ __device__ constexpr int mrt_input19(int r, int x, int y, int z) {
+    const int xx = x * x, yy = y * y, zz = z * z;
+    switch (r) {
+        case 0: return 1;
+        case 1: return x;
+        case 2: return y;
+        case 3: return z;
+        case 4: return xx - yy;
+        case 5: return x * y;
+        case 6: return x * z;
+        case 7: return yy - zz;
+        case 8: return y * z;
+        case 9: return xx + yy + zz;
+        case 10: return xx * y;
+        case 11: return xx * z;
+        case 12: return x * yy;
+        case 13: return x * zz;
+        case 14: return yy * z;
+        case 15: return y * zz;
+        case 16: return xx * yy;
+        case 17: return xx * zz;
+        default: return yy * zz;
+    }
+}
+
+struct MrtRows19 {
+    double v[19][19];     // v[k][q] = P_k(c_q), rows 0..3 conserved
+    double inv_norm[19];  // 1 / sum_q w_q P_k(c_q)^2
+};
+
+__host__ __device__ constexpr MrtRows19 make_mrt_rows19() {
+    MrtRows19 b{};
+    for (int k = 0; k < 19; ++k) {
+        for (int q = 0; q < 19; ++q) b.v[k][q] = mrt_input19(k, kC27[q][0], kC27[q][1], kC27[q][2]);
+        for (int j = 0; j < k; ++j) {  // classical Gram-Schmidt, weighted inner product
+            double num = 0.0, den = 0.0;
+            for (int q = 0; q < 19; ++q) {
+                const double w = Stencil<19>::w(q);
+                num += w * mrt_input19(k, kC27[q][0], kC27[q][1], kC27[q][2]) * b.v[j][q];
+                den += w * b.v[j][q] * b.v[j][q];
+            }
+            for (int q = 0; q < 19; ++q) b.v[k][q] -= num / den * b.v[j][q];
+        }
+        double nn = 0.0;
+        for (int q = 0; q < 19; ++q) nn += Stencil<19>::w(q) * b.v[k][q] * b.v[k][q];
+        b.inv_norm[k] = 1.0 / nn;
+    }
+    return b;
+}
+// The rows live in __constant__ memory of k_mrt_rows.cu (filled once from make_mrt_rows19() on the host);
+// the unrolled loops read them as constant-bank operands. Defined only in that translation unit.
+template <typename T>
+__device__ void collide_mrt19_rows(T (&g)[19], const Rates<T> &p);
 
 // ---------------------------------------------------------------------------------------
 // Smagorinsky SRT (Eqs. 11-14), rates = [omega_0, C_S]. The local omega solves
@@ -709,7 +775,8 @@ __device__ __forceinline__ void collide_cumulant19(T (&g)[19], const Rates<T> &p
 // ---------------------------------------------------------------------------------------
 // Dispatch
 // ---------------------------------------------------------------------------------------
-enum Op { OP_SRT = 0, OP_TRT = 1, OP_MRT = 2, OP_CUMULANT = 3, OP_IDENTITY = 4, OP_SMAGORINSKY = 5, OP_KBC = 6 };
+enum Op { OP_SRT = 0, OP_TRT = 1, OP_MRT = 2, OP_CUMULANT = 3, OP_IDENTITY = 4, OP_SMAGORINSKY = 5, OP_KBC = 6,
+          OP_MRT_ROWS = 7 /* MRT with one rate per moment (internal id; ABI: LBM_MRT + n_row_rates = 15) */ };
 
 template <int Q, int OPX, typename T, bool FORCE>
 __device__ __forceinline__ void collide(T (&g)[Q], const Rates<T> &p) {
@@ -728,6 +795,9 @@ __device__ __forceinline__ void collide(T (&g)[Q], const Rates<T> &p) {
         collide_smagorinsky<Q, T>(g, p);
     } else if constexpr (OP == OP_KBC) {
         collide_kbc<Q, T>(g, p);
+    } else if constexpr (OP == OP_MRT_ROWS) {
+        static_assert(Q == 19, "per-moment MRT is implemented for D3Q19");
+        collide_mrt19_rows<T>(g, p);
     }
 }
 

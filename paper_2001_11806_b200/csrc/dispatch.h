@@ -29,6 +29,8 @@ struct Kernels {
 
 Kernels select_trt(int Q, int dtype, int fm, bool force);
 Kernels select_mrt(int Q, int dtype, int fm, bool force);
+Kernels select_mrt_rows(int Q, int dtype, int fm, bool force);
+int mrt_rows_upload();  // per-moment MRT rows -> __constant__ memory of the current device
 Kernels select_cumulant(int Q, int dtype, int fm, bool force);
 Kernels select_cumulant19(int Q, int dtype, int fm, bool force);
 Kernels select_identity(int Q, int dtype, int fm, bool force);

@@ -54,7 +54,7 @@ struct StepArgs {
     Geo geo;
     int z_begin;  // first local plane (interior index) of this launch
     int z_step;   // plane stride between blockIdx.z values (boundary-plane launches use nz-1)
-    double rates[8];
+    double rates[16];              // per operator (include/lbm.h); 15 per-moment MRT rates
     double F[3];
     double uw[3];                  // UBB wall velocity; rho_w = 1 (G8)
     const uint8_t *flags;          // storage-indexed (with ghost planes) or nullptr; bits 0-1 = type
@@ -68,7 +68,7 @@ template <typename T>
 __device__ __forceinline__ Rates<T> load_rates(const StepArgs &a) {
     Rates<T> r;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) r.r[i] = T(a.rates[i]);
+    for (int i = 0; i < 16; ++i) r.r[i] = T(a.rates[i]);
 #pragma unroll
     for (int i = 0; i < 3; ++i) r.F[i] = T(a.F[i]);
     return r;

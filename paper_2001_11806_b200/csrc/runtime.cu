@@ -379,6 +379,9 @@ int step_once(lbm_handle_s *h) {
     };
     const int nz = h->slabs[0].nz;
     const Phase ph = !aa ? phase_pull(nz) : (odd ? phase_aa_return(nz, h->have_flags) : phase_aa_fill(nz));
+    if (!aa)  // index-list boundaries: wall slots (ghost planes included) before the boundary planes read them
+        for (Slab &s : h->slabs)
+            if (!h->fused) launch_links_fix(h, s, s.pdf[s.cur], 0, st);
     if (!h->use_nccl) {
         // loopback slabs on one GPU, one stream: boundary planes, exchange, interior
         for (Slab &s : h->slabs) bnd(s);
@@ -396,6 +399,7 @@ int step_once(lbm_handle_s *h) {
         // stores into the neighbours' ghost planes -> interior planes; one stream, no send/recv
         fused_gate(h->fst, st);
         h->launches++;
+        launch_links_fix(h, s, s.pdf[s.cur], 0, st);  // after the gate: the peers' stores into our ghosts are done
         launch_pull_range(h, s, 0, 2, s.nz - 1, st, true);
         launch_pull_range(h, s, 1, s.nz - 2, 1, st);
         s.cur ^= 1;
@@ -455,7 +459,8 @@ int validate(const lbm_config *c) {
     if (c->pattern == LBM_ESOTWIST && c->boundary_mode == LBM_BOUNDARY_LINKS)
         return fail(nullptr, LBM_EUNSUPPORTED, "index-list boundaries are implemented for the pull and AA patterns");
     const int need[] = {1, 2, 1, 1, 0, 2, 1};
-    if (c->n_rates < need[c->collision] || c->n_rates > 8) return fail(nullptr, LBM_EINVAL, "wrong number of rates");
+    const int need_n = (c->collision == LBM_MRT && c->n_row_rates == 15) ? 0 : need[c->collision];
+    if (c->n_rates < need_n || c->n_rates > 8) return fail(nullptr, LBM_EINVAL, "wrong number of rates");
     for (int i = 0; i < c->n_rates; ++i)
         if (!(c->rates[i] > 0.0 && c->rates[i] < 2.0)) return fail(nullptr, LBM_EINVAL, "relaxation rate outside (0, 2)");
     for (int d = 0; d < 3; ++d)
@@ -479,10 +484,19 @@ int validate(const lbm_config *c) {
     if (c->collision == LBM_MRT && c->stencil != 19) return fail(nullptr, LBM_EUNSUPPORTED, "MRT is implemented for D3Q19");
     if (force && c->collision != LBM_SRT && c->collision != LBM_TRT)
         return fail(nullptr, LBM_EUNSUPPORTED, "forcing is implemented for SRT/TRT");
+    if (c->n_row_rates != 0 && c->n_row_rates != 15) return fail(nullptr, LBM_EINVAL, "n_row_rates must be 0 or 15");
+    if (c->n_row_rates == 15) {
+        if (c->collision != LBM_MRT) return fail(nullptr, LBM_EINVAL, "per-moment rates are for LBM_MRT");
+        for (int i = 0; i < 15; ++i)
+            if (!(c->row_rates[i] > 0.0 && c->row_rates[i] < 2.0))
+                return fail(nullptr, LBM_EINVAL, "relaxation rate outside (0, 2)");
+        if (c->equilibrium != LBM_EQ_COMPRESSIBLE)
+            return fail(nullptr, LBM_EUNSUPPORTED, "per-moment MRT rates use the compressible equilibrium");
+    }
     if (c->boundary_mode != LBM_BOUNDARY_FLAGS && c->boundary_mode != LBM_BOUNDARY_LINKS)
         return fail(nullptr, LBM_EINVAL, "bad boundary_mode");
-    if (c->boundary_mode == LBM_BOUNDARY_LINKS && (c->nranks > 1 || c->n_local_slabs > 1 || c->nccl_self))
-        return fail(nullptr, LBM_EUNSUPPORTED, "index-list boundaries are implemented for a single slab");
+    if (c->boundary_mode == LBM_BOUNDARY_LINKS && c->pattern == LBM_AA && (c->nranks > 1 || c->n_local_slabs > 1 || c->nccl_self))
+        return fail(nullptr, LBM_EUNSUPPORTED, "index-list boundaries with the AA pattern are implemented for a single slab");
     if (c->equilibrium < LBM_EQ_COMPRESSIBLE || c->equilibrium > LBM_EQ_MOMENT_MATCHED)
         return fail(nullptr, LBM_EINVAL, "bad equilibrium");
     if (c->equilibrium != LBM_EQ_COMPRESSIBLE && c->collision != LBM_SRT && c->collision != LBM_TRT &&
@@ -556,6 +570,7 @@ Kernels select_kernels(int collision, int Q, int dtype, int fm, bool force, int 
         if (collision != LBM_IDENTITY) return Kernels{};
     }
     switch (collision) {
+        case OP_MRT_ROWS: return eq == EQ_COMPRESSIBLE ? select_mrt_rows(Q, dtype, fm, force) : Kernels{};
         case LBM_SRT:
         case LBM_TRT: return select_trt(Q, dtype, fm, force);
         case LBM_MRT: return select_mrt(Q, dtype, fm, force);
@@ -588,24 +603,38 @@ const char *lbm_version(void) { return "b200-lbm 0.2 (sm_100a)"; }
 int64_t lbm_boundary_links(lbm_handle h, int64_t *cells, int32_t *dirs, int32_t *types, int64_t cap) {
     if (!h) return LBM_EINVAL;
     if (!h->links) return 0;
-    const Slab &s = h->slabs[0];
-    const int64_t n = (int64_t)s.h_link_wall.size();
+    int64_t n = 0;
+    for (const Slab &s : h->slabs) n += (int64_t)s.h_link_wall.size();
     if (cap < n && (cells || dirs || types)) return fail(h, LBM_EINVAL, "link buffer too small");
-    for (int64_t i = 0; i < n; ++i) {
-        if (cells) cells[i] = (int64_t)s.h_link_wall[i];  // single slab: storage index == global index
-        if (dirs) dirs[i] = s.h_link_dir[i];
-        if (types) types[i] = s.h_link_type[i];
-    }
+    int64_t i = 0;
+    const int64_t plane = h->nx * h->ny;
+    for (const Slab &s : h->slabs)
+        for (size_t k = 0; k < s.h_link_wall.size(); ++k, ++i) {
+            if (cells) {  // storage index -> global linear index (ghost planes map to the neighbour's planes)
+                const int64_t b = s.h_link_wall[k], zs = b / plane;
+                const int64_t zg = ((s.z0 + zs - h->g) % h->nzg + h->nzg) % h->nzg;
+                cells[i] = zg * plane + (b - zs * plane);
+            }
+            if (dirs) dirs[i] = s.h_link_dir[k];
+            if (types) types[i] = s.h_link_type[k];
+        }
     return n;
 }
 
 int lbm_set_link_velocities(lbm_handle h, const double *uw, int64_t n) {
     if (!h || !uw) return LBM_EINVAL;
     if (!h->links) return fail(h, LBM_EINVAL, "no index-list boundaries (boundary_mode != LBM_BOUNDARY_LINKS)");
-    Slab &s = h->slabs[0];
-    if (n != (int64_t)s.h_link_wall.size()) return fail(h, LBM_EINVAL, "link count mismatch");
+    int64_t total = 0;
+    for (const Slab &s : h->slabs) total += (int64_t)s.h_link_wall.size();
+    if (n != total) return fail(h, LBM_EINVAL, "link count mismatch");
     CUDA_TRY(h, cudaStreamSynchronize(h->stream));  // the terms may be in use by queued link kernels
-    return upload_link_terms(h, s, uw);
+    int64_t off = 0;
+    for (Slab &s : h->slabs) {
+        const int rc = upload_link_terms(h, s, uw + 3 * off);
+        if (rc) return rc;
+        off += (int64_t)s.h_link_wall.size();
+    }
+    return LBM_OK;
 }
 
 int lbm_set_kernel_path(int32_t path) {
@@ -806,12 +835,14 @@ int lbm_create(const lbm_config *cfg, lbm_handle *out) {
 
     // kernel selection (SRT = TRT with equal rates); index-list boundaries run the flag-free kernels
     const int fm_bulk = h->have_flags && !h->links ? FM_BULK : FM_NONE;
+    const bool per_row = cfg->collision == LBM_MRT && cfg->n_row_rates == 15;
+    const int kcoll = per_row ? (int)OP_MRT_ROWS : cfg->collision;
     const bool force = h->have_force;
     if (cfg->pattern == LBM_PULL) {
-        h->kern = select_kernels(cfg->collision, h->Q, h->dtype, fm_bulk, force, cfg->equilibrium);
+        h->kern = select_kernels(kcoll, h->Q, h->dtype, fm_bulk, force, cfg->equilibrium);
         if (!h->kern.pull) return fail(nullptr, LBM_EUNSUPPORTED, "no kernel instantiated for this combination");
     } else {
-        h->kern = select_kernels(cfg->collision, h->Q, h->dtype, fm_bulk, force, cfg->equilibrium);
+        h->kern = select_kernels(kcoll, h->Q, h->dtype, fm_bulk, force, cfg->equilibrium);
         if (!(cfg->pattern == LBM_ESOTWIST ? (void *)h->kern.eso : (void *)h->kern.aa))
             return fail(nullptr, LBM_EUNSUPPORTED, "no kernel instantiated for this combination");
     }
@@ -819,8 +850,10 @@ int lbm_create(const lbm_config *cfg, lbm_handle *out) {
     StepArgs &b = h->base;
     std::memset(&b, 0, sizeof(b));
     for (int i = 0; i < 8; ++i) b.rates[i] = cfg->rates[i];
+    if (per_row)
+        for (int i = 0; i < 15; ++i) b.rates[i] = cfg->row_rates[i];
     if (cfg->collision == LBM_SRT) b.rates[1] = b.rates[0];
-    if (cfg->collision == LBM_MRT)
+    if (cfg->collision == LBM_MRT && !per_row)
         for (int i = cfg->n_rates; i < 4; ++i) b.rates[i] = 1.0;
     if (cfg->collision == LBM_CUMULANT)
         for (int i = cfg->n_rates; i < 6; ++i) b.rates[i] = 1.0;  // higher orders default to 1 (G7)
@@ -854,6 +887,10 @@ int lbm_create(const lbm_config *cfg, lbm_handle *out) {
         cudaEventCreateWithFlags(&h->ev_bnd, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&h->ev_x, cudaEventDisableTiming) != cudaSuccess) {
         h->err = "stream/event creation failed";
+        return bail(LBM_ECUDA);
+    }
+    if (per_row && mrt_rows_upload() != 0) {
+        h->err = "per-moment MRT rows: constant upload failed";
         return bail(LBM_ECUDA);
     }
     if (cudaMalloc(&h->d_nanflag, sizeof(int)) != cudaSuccess) {
@@ -926,18 +963,21 @@ int lbm_create(const lbm_config *cfg, lbm_handle *out) {
                 cudaMemcpy(s.edges, list.data(), list.size() * sizeof(uint32_t), cudaMemcpyHostToDevice);
             }
             if (h->links) {
-                // one entry per boundary link: wall cell b, direction q with b + c_q fluid (single slab:
-                // x, y, z all wrap), in storage order of b then q
+                // one entry per boundary link: wall cell b (any storage plane, ghosts included), direction q
+                // with b + c_q a fluid cell of this slab's interior (x, y wrap; z wraps without ghost planes),
+                // in storage order of b then q. A link is listed by the slab owning its fluid cell.
                 std::vector<uint32_t> lf;
-                for (int zs = 0; zs < s.nz; ++zs)
+                for (int zs = 0; zs < nplanes; ++zs)
                     for (int64_t y = 0; y < h->ny; ++y)
                         for (int64_t x = 0; x < h->nx; ++x) {
                             const size_t b = ((size_t)zs * h->ny + y) * h->nx + x;
                             const uint8_t t = hf[b] & 3;
                             if (!t) continue;
                             for (int q = 1; q < h->Q; ++q) {
+                                int64_t zz = zs + kC27[q][2];
+                                if (h->g == 0) zz = (zz + s.nz) % s.nz;
+                                else if (zz < h->g || zz >= h->g + s.nz) continue;  // fluid cell not in this slab
                                 const int64_t xx = (x + kC27[q][0] + h->nx) % h->nx, yy = (y + kC27[q][1] + h->ny) % h->ny;
-                                const int64_t zz = (zs + kC27[q][2] + s.nz) % s.nz;
                                 const size_t nb = ((size_t)zz * h->ny + yy) * h->nx + xx;
                                 if (hf[nb] & 3) continue;
                                 s.h_link_wall.push_back((uint32_t)b);

@@ -50,6 +50,7 @@ class lbm_config(C.Structure):
         ("stream", C.c_void_p), ("halo_mode", C.c_int32), ("use_graph", C.c_int32),
         ("block_x", C.c_int32), ("check_nan_every", C.c_int32), ("nccl_self", C.c_int32),
         ("equilibrium", C.c_int32), ("boundary_mode", C.c_int32),
+        ("n_row_rates", C.c_int32), ("row_rates", C.c_double * 15),
     ]
 
 
@@ -199,9 +200,15 @@ class Simulation:
         cfg.collision = COLLISIONS[collision] if isinstance(collision, str) else collision
         cfg.dtype = DTYPES[dtype] if isinstance(dtype, str) else dtype
         cfg.pattern = PATTERNS[pattern] if isinstance(pattern, str) else pattern
-        cfg.n_rates = len(rates)
-        for i, r in enumerate(rates):
-            cfg.rates[i] = r
+        if len(rates) == 15:  # MRT with one rate per moment
+            cfg.n_rates = 0
+            cfg.n_row_rates = 15
+            for i, r in enumerate(rates):
+                cfg.row_rates[i] = r
+        else:
+            cfg.n_rates = len(rates)
+            for i, r in enumerate(rates):
+                cfg.rates[i] = r
         for d in range(3):
             cfg.force[d] = force[d]
             cfg.ubb_velocity[d] = ubb_velocity[d]

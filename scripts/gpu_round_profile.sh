@@ -4,6 +4,7 @@
 # Each ncu command runs only after the same command exited 0 without ncu.
 set -u
 O=gpurun_out; mkdir -p $O
+timeout 900 python -m pytest tests -m gpu -x -q > $O/gpu_tests.log 2>&1; echo "tests=$?" >> $O/status.txt
 timeout 900 python bench.py > $O/bench_default.log 2>&1; echo "default=$?" >> $O/status.txt
 timeout 600 python bench.py --impl reference > $O/bench_reference.log 2>&1; echo "reference=$?" >> $O/status.txt
 for c in c0 c1_f64 c1_f32 c2 c3 c1_f64_flags c1_f32_flags c3_flags c3_aa eso_c4 eso_c2 eso_c3 eq_inc_c4 eq_mm_c4 eq_inc_c2 \
@@ -20,6 +21,10 @@ prof() {  # config kernel-regex skip count
   timeout 300 $C > $O/plain_$1.log 2>&1 && \
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:$2 -s $3 -c $4 -o $O/prof_$1 $C > $O/ncu_$1.log 2>&1
   echo "prof_$1=$?" >> $O/status.txt
+  # gpurun copies back at most 64 MiB: keep the raw metric pages (CSV), drop the report
+  ncu -i $O/prof_$1.ncu-rep --page raw --csv > $O/prof_$1_raw.csv 2>/dev/null
+  ncu -i $O/prof_$1.ncu-rep --page details --csv > $O/prof_$1_details.csv 2>/dev/null
+  rm -f $O/prof_$1.ncu-rep
 }
 prof c4 k_pull 3 1
 prof c2 k_staged 4 2

@@ -23,7 +23,11 @@ def main(rnd, configs):
     traffic = json.load(open(tr_path)) if os.path.exists(tr_path) else {}
     for c in configs:
         rep = os.path.join(ROOT, "gpurun_out", f"prof_{c}.ncu-rep")
-        out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+        raw_csv = os.path.join(ROOT, "gpurun_out", f"prof_{c}_raw.csv")
+        if os.path.exists(raw_csv):  # exported on the GPU box (reports exceed gpurun's copy-back limit)
+            out = open(raw_csv).read()
+        else:
+            out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
         rows = list(csv.reader(io.StringIO(out)))
         hdr, units = rows[0], rows[1]
         kernels = []
@@ -39,7 +43,13 @@ def main(rnd, configs):
         if not kernels:
             print(c, "no kernels in report (graph-launched?)")
             continue
-        traffic[c] = sum(k["dram_bytes"] for k in kernels) / len(kernels)
+        # dominant kernel(s): those within 2x of the longest launch (AA/EsoTwist: the even and odd kernels)
+        def dur(k):
+            v, u = k["metrics"]["gpu__time_duration.sum"].split()
+            return float(v) * {"ns": 1e-9, "us": 1e-6, "usecond": 1e-6, "ms": 1e-3, "msecond": 1e-3}.get(u, 1.0)
+        tmax = max(dur(k) for k in kernels)
+        dom = [k for k in kernels if dur(k) >= 0.5 * tmax]
+        traffic[c] = sum(k["dram_bytes"] for k in dom) / len(dom)
         print(c, [(k["kernel"][:40], k["dram_bytes"]) for k in kernels])
     json.dump(traffic, open(tr_path, "w"), indent=1)
 

@@ -84,7 +84,11 @@ def test_slab_plan(L):
     (dict(nccl_self=True, n_local_slabs=2), -1),                # self-exchange is single-slab
     (dict(equilibrium=3), -1),                                  # unknown equilibrium kind
     (dict(boundary_mode=2), -1),                                # unknown boundary mode
-    (dict(boundary_mode="links", n_local_slabs=2), -2),         # index-list boundaries: single slab
+    (dict(collision="trt", rates=(1.0,) * 15), -1),             # per-moment rates are for MRT
+    (dict(collision="mrt", rates=(1.0,) * 14 + (2.0,)), -1),    # per-moment rate outside (0, 2)
+    (dict(collision="mrt", rates=(1.0,) * 15, equilibrium="incompressible"), -2),
+    (dict(boundary_mode="links", n_local_slabs=2, pattern="aa"), -2),  # AA + index-list: single slab
+    (dict(pattern="esotwist", n_local_slabs=2), -2),            # EsoTwist: single slab
     (dict(stencil=27, collision="cumulant", rates=(1.9,), equilibrium="incompressible"), -2),
     (dict(collision="kbc", rates=(1.9,), equilibrium="moment_matched"), -2),
 ])

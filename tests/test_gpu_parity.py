@@ -13,6 +13,8 @@ from tests.gpu_common import FULL, TOL, Case, fluid_mask, init_sim, make_sim, ma
 
 pytestmark = pytest.mark.gpu
 
+ROW_RATES = (1.9, 1.7, 1.5, 1.3, 1.1, 1.05, 0.9, 1.2, 1.4, 0.8, 1.6, 1.0, 1.25, 0.7, 1.35)  # per-moment MRT
+
 
 @pytest.fixture(scope="module", autouse=True)
 def _lib():
@@ -227,6 +229,12 @@ PARITY = [
     Case("cum19_f32_channel", (16, 20, 12), 19, "cumulant", (1.9,), "f32", geometry="channel", u_amp=0.03, steps=20),
     Case("cum19_aa_f64_obst", (17, 13, 11), 19, "cumulant", (1.95, 1.1, 1.0, 1.2), "f64", pattern="aa",
          geometry="obstacles", ubb=(0.02, -0.01, 0.03), u_amp=0.05, steps=15),
+    # MRT with one rate per moment
+    Case("mrt_rows_f64_walls", (17, 13, 11), 19, "mrt", ROW_RATES, "f64", geometry="obstacles", ubb=(0.02, -0.01, 0.03),
+         u_amp=0.05, steps=15),
+    Case("mrt_rows_f32_aa", (32, 16, 8), 19, "mrt", ROW_RATES, "f32", pattern="aa", u_amp=0.03, steps=12),
+    Case("mrt_rows_f64_eso_channel", (16, 20, 12), 19, "mrt", ROW_RATES, "f64", pattern="esotwist", geometry="channel",
+         steps=11),
     # EsoTwist
     Case("eso_trt_force_f64_odd", (18, 14, 10), 19, "trt", (1.6, 0.5), "f64", pattern="esotwist", force=(1e-5, 2e-5, 0),
          steps=21),
@@ -601,3 +609,21 @@ def test_index_list_per_link_wall_velocities(pattern, steps):
     rho_g, u_g = sim.macroscopic()
     rho_o, u_o = d.macroscopic(ref, post_collision=pattern == "pull")
     np.testing.assert_allclose(u_g[:, fl == 0], u_o[:, fl == 0], rtol=0, atol=1e-15)
+
+
+@pytest.mark.parametrize("P,halo_mode,nccl_self", [(2, 0, False), (4, 1, False), (1, 0, True), (1, 1, True), (1, 2, True)])
+def test_index_list_boundaries_slabs_bit_identical(P, halo_mode, nccl_self):
+    """Index-list boundaries with slab decomposition (pull): the link kernel also fills the wall slots of
+    ghost planes after the exchange; loopback slabs, NCCL self-exchange and the fused NVLink halo are
+    bit-identical to the single slab, and the concatenated link lists are the global list."""
+    case = Case("lkdec", (16, 12, 16), 19, "trt", (1.6, 0.5), "f64", force=(1e-5, 0, 0), geometry="obstacles",
+                ubb=(0.02, -0.01, 0.03), steps=13)
+    one = make_sim(case, boundary_mode="links")
+    many = make_sim(case, boundary_mode="links", n_local_slabs=P, halo_mode=halo_mode, nccl_self=nccl_self)
+    a, b = one.boundary_links(), many.boundary_links()
+    assert sorted(zip(*[v.tolist() for v in a])) == sorted(zip(*[v.tolist() for v in b]))
+    for s in (one, many):
+        init_sim(s, case)
+        s.step(case.steps)
+    mask = fluid_mask(case, case.Q)
+    np.testing.assert_array_equal(one.populations(raw=True)[mask], many.populations(raw=True)[mask])

@@ -284,3 +284,39 @@ def test_d3q19_cumulant_isserlis_closed_form():
         Sp = np.eye(3) / 3 + (1 - 1.95) * (Sig - np.trace(Sig) / 3 * np.eye(3))
         mom = np.array([rho * _gaussian_raw_moment(e, u, Sp) for e in es])
         np.testing.assert_allclose(O.collide_cell(m, f), np.linalg.solve(A, mom), rtol=0, atol=2e-15)
+
+
+# ---------------------------------------------------------------------------------------
+# MRT with one rate per moment: the rows are the paper's weighted
+# Gram-Schmidt basis in its order (pinned by the D2Q9 tableau, tests/golden/d2q9_mrt_weighted.txt).
+# ---------------------------------------------------------------------------------------
+ROW_RATES = (1.9, 1.7, 1.5, 1.3, 1.1, 1.05, 0.9, 1.2, 1.4, 0.8, 1.6, 1.0, 1.25, 0.7, 1.35)
+
+
+def test_mrt_per_row_rates_reduce_to_group_rates():
+    groups = (1.9, 1.3, 1.1, 0.8)
+    per_row = (groups[0],) * 5 + (groups[1],) + (groups[2],) * 6 + (groups[3],) * 3
+    a = O.Method(Q=19, op="mrt", rates=per_row)
+    b = O.Method(Q=19, op="mrt", rates=groups)
+    for _ in range(5):
+        f = _random_state(19, amp=0.1)
+        np.testing.assert_allclose(O.collide_cell(a, f), O.collide_cell(b, f), rtol=0, atol=1e-16)
+
+
+def test_mrt_per_row_rates_conservation_fixed_point_and_row_relaxation():
+    """Each non-conserved moment m_k = <P_k, f> relaxes by its own rate: m_k' - m_k,eq = (1 - w_k)(m_k - m_k,eq)."""
+    from oracle import methods
+    m = O.Method(Q=19, op="mrt", rates=ROW_RATES)
+    M, _, S = m.mrt_matrices()
+    c, _, _ = O.stencil_arrays(19)
+    for _ in range(5):
+        f = _random_state(19, amp=0.1)
+        out = O.collide_cell(m, f)
+        assert abs(out.sum() - f.sum()) < 1e-15
+        np.testing.assert_allclose(c.T @ out, c.T @ f, atol=1e-16)
+        rho = f.sum()
+        feq = O.equilibrium_cell(19, rho, c.T @ f / rho)
+        np.testing.assert_allclose(M @ (out - feq), (1 - S) * (M @ (f - feq)) * (S > 0) + (M @ (out - feq)) * (S == 0),
+                                   rtol=0, atol=2e-16)
+        np.testing.assert_allclose(O.collide_cell(m, feq), feq, rtol=0, atol=2e-16)
+    assert list(S[4:]) == list(ROW_RATES)
