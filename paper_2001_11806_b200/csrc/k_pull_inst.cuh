@@ -50,6 +50,9 @@ void aa_edge_launcher(const StepArgs &a, const void *src, void *f, const uint32_
 
 template <int Q, int OP, typename T, int FM, bool FORCE>
 void eso_launcher(const StepArgs &a, void *f, int odd, dim3 grid, dim3 block, cudaStream_t s) {
+    if (odd ? staged_launch<Q, OP, T, FM, FORCE, SM_ESO_ODD>(a, f, f, (int)grid.z, s)
+            : staged_launch<Q, OP, T, FM, FORCE, SM_ESO_EVEN>(a, f, f, (int)grid.z, s))
+        return;
     if (odd) k_eso<Q, OP, T, FM, FORCE, true><<<grid, block, 0, s>>>(a, static_cast<T *>(f));
     else k_eso<Q, OP, T, FM, FORCE, false><<<grid, block, 0, s>>>(a, static_cast<T *>(f));
 }

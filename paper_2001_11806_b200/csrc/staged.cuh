@@ -30,9 +30,16 @@
 
 namespace lbm {
 
-enum SMode { SM_PULL = 0, SM_AA_EVEN = 1, SM_AA_ODD = 2 };
-// modes whose gather is shifted by -c_q
-__host__ __device__ constexpr bool sh_of(int mode) { return mode != SM_AA_EVEN; }
+enum SMode { SM_PULL = 0, SM_AA_EVEN = 1, SM_AA_ODD = 2, SM_ESO_EVEN = 3, SM_ESO_ODD = 4 };
+// arriving population q of cell x is read from location x - rshift(c_q) (componentwise) ...
+__host__ __device__ constexpr int rshift(int mode, int c) {
+    return mode == SM_AA_EVEN ? 0 : (mode == SM_ESO_EVEN || mode == SM_ESO_ODD) ? (c > 0 ? c : 0) : c;
+}
+// ... in slot src_slot (EsoTwist: P:875-891, kernels.cuh eso_cell)
+template <int Q>
+__host__ __device__ constexpr int src_slot(int mode, int q) {
+    return (mode == SM_AA_ODD || mode == SM_ESO_ODD) ? Stencil<Q>::opp(q) : q;
+}
 
 #ifndef LBM_STAGED_BT
 #define LBM_STAGED_BT 256
@@ -106,7 +113,6 @@ template <int Q, typename T, int FM, int MODE>
 __device__ __forceinline__ void stage_issue(const StepArgs &a, const T *f, const Tile &tl, int H, T *buf, uint64_t *bar,
                                             int lane) {
     using S = Stencil<Q>;
-    constexpr bool sh = MODE != SM_AA_EVEN;
     const int nx = a.geo.nx, ny = a.geo.ny;
     const uint32_t row_bytes = (uint32_t)nx * sizeof(T);
     const uint32_t per_q = (uint32_t)tl.hl * row_bytes;
@@ -115,14 +121,11 @@ __device__ __forceinline__ void stage_issue(const StepArgs &a, const T *f, const
     if (lane == 0) mbar_expect_tx(bar, per_q * Q + flag_bytes);
     __syncwarp();
     for (int q = lane; q < Q; q += 32) {
-        const int P = MODE == SM_AA_ODD ? S::opp(q) : q;
-        int ys = tl.y0, zz = tl.zs;
-        if (sh) {
-            ys = tl.y0 - S::cy(q);
-            ys = ys < 0 ? ys + ny : (ys >= ny ? ys - ny : ys);
-            zz = tl.zs - S::cz(q);
-            if (!a.geo.g) zz = zz < 0 ? zz + a.geo.nz : (zz >= a.geo.nz ? zz - a.geo.nz : zz);
-        }
+        const int P = src_slot<Q>(MODE, q);
+        int ys = tl.y0 - rshift(MODE, S::cy(q));
+        ys = ys < 0 ? ys + ny : (ys >= ny ? ys - ny : ys);
+        int zz = tl.zs - rshift(MODE, S::cz(q));
+        if (!a.geo.g) zz = zz < 0 ? zz + a.geo.nz : (zz >= a.geo.nz ? zz - a.geo.nz : zz);
         const T *plane = f + (int64_t)P * a.geo.Sq + (int64_t)zz * ny * nx;
         T *dst = buf + (int64_t)q * H * nx;
         const int n1 = min(tl.hl, ny - ys);  // rows before the y-wrap
@@ -196,7 +199,8 @@ __global__ void __launch_bounds__(kStagedBT + 32, (StagedMinBlocks<Q, OP, T>::va
             T g[Q];
 #pragma unroll
             for (int q = 0; q < Q; ++q) {
-                const int xs = (!sh_of(MODE) || S::cx(q) == 0) ? xc : (S::cx(q) > 0 ? xm : xp);
+                const int sx = rshift(MODE, S::cx(q));
+                const int xs = sx == 0 ? xc : (sx > 0 ? xm : xp);
                 g[q] = buf[q * rowlen + hc * nx + xs];
             }
             collide<Q, OP, T, FORCE>(g, r);
@@ -208,6 +212,13 @@ __global__ void __launch_bounds__(kStagedBT + 32, (StagedMinBlocks<Q, OP, T>::va
             } else if constexpr (MODE == SM_AA_EVEN) {
 #pragma unroll
                 for (int q = 0; q < Q; ++q) dst[S::opp(q) * Sq + self] = g[q];
+            } else if constexpr (MODE == SM_ESO_EVEN || MODE == SM_ESO_ODD) {
+                // departing q at x + c_q^- (slot qbar after the even step, q after the odd one)
+                const Nbr n = neighbours(a.geo, xc, y, tl.zs);
+#pragma unroll
+                for (int q = 0; q < Q; ++q)
+                    dst[(MODE == SM_ESO_ODD ? q : S::opp(q)) * Sq + nb_off(a.geo, n, cneg(S::cx(q)), cneg(S::cy(q)), cneg(S::cz(q)))] =
+                        g[q];
             } else {
                 const Nbr n = neighbours(a.geo, xc, y, tl.zs);
 #pragma unroll
@@ -230,7 +241,7 @@ int staged_path();     // 0 auto, 1 plain, 2 staged (lbm_set_kernel_path / LBM_K
 template <int Q, int OPX, int MODE>
 constexpr bool staged_auto() {
     constexpr int OP = op_base(OPX);
-    return OP == OP_MRT || OP == OP_KBC || OP == OP_SMAGORINSKY || (OP == OP_CUMULANT && MODE != SM_PULL);
+    return OP == OP_MRT || OP == OP_MRT_ROWS || OP == OP_KBC || OP == OP_SMAGORINSKY || (OP == OP_CUMULANT && MODE != SM_PULL);
 }
 
 template <int Q, int OP, typename T, int FM, bool FORCE, int MODE>

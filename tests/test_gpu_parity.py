@@ -280,6 +280,10 @@ STAGED_CASES = [
          ubb=(0.02, -0.01, 0.03), u_amp=0.05, steps=9),
     Case("st_smag_q27_f32", (64, 6, 5), 27, "smagorinsky", (1.9, 0.12), "f32", u_amp=0.05, steps=8),
     Case("st_kbc27_pull_f64", (32, 9, 7), 27, "kbc", (1.95,), "f64", u_amp=0.05, steps=7),
+    Case("st_eso_mrt_f32_walls16", (32, 14, 10), 19, "mrt", (1.9, 1.3, 1.1, 0.8), "f32", pattern="esotwist",
+         geometry="channel", steps=9),
+    Case("st_eso_cum27_f64_odd", (16, 9, 7), 27, "cumulant", (1.95,), "f64", pattern="esotwist", u_amp=0.03, steps=7),
+    Case("st_mrt_rows_aa_f64", (32, 9, 7), 19, "mrt", ROW_RATES, "f64", pattern="aa", u_amp=0.03, steps=8),
     Case("st_cum19_aa_f32_walls16", (32, 12, 10), 19, "cumulant", (1.95,), "f32", pattern="aa", geometry="channel",
          u_amp=0.03, steps=9),
 ]
