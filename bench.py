@@ -316,8 +316,8 @@ def main():
     use_graph = 0 if nccl_self else use_graph
     exchanging = world > 1 or nccl_self
     halo_mode = args.halo_mode
-    if halo_mode < 0:  # default: fused NVLink peer-store halo for the pull pattern, else zero-copy NCCL
-        halo_mode = L.HALO_FUSED if (exchanging and cfg["pattern"] == "pull") else L.HALO_ZEROCOPY
+    if halo_mode < 0:  # default: fused NVLink peer-store halo for pull and AA, else zero-copy NCCL
+        halo_mode = L.HALO_FUSED if (exchanging and cfg["pattern"] in ("pull", "aa")) else L.HALO_ZEROCOPY
 
     def make(mode):
         return L.Simulation(gshape, stencil=cfg["Q"], collision=cfg["op"], rates=cfg["rates"], dtype=cfg["dtype"],

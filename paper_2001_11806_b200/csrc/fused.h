@@ -12,8 +12,8 @@ struct FusedState {
     void *bases[4] = {nullptr, nullptr, nullptr, nullptr};  // LSA base of array 0 up/down, array 1 up/down
 };
 
-// Registers both population arrays (allocated with ncclMemAlloc, `bytes` each, same size on every
-// rank) as symmetric windows, creates a device communicator with one LSA barrier and resolves the
+// Registers the population arrays (allocated with ncclMemAlloc, `bytes` each, same size on every
+// rank; pdf1 = nullptr for the single-array AA pattern) as symmetric windows, creates a device communicator with one LSA barrier and resolves the
 // neighbours' window base pointers. Collective over the communicator. Returns 0 or -1 (err set).
 int fused_setup(ncclComm_t comm, void *pdf0, void *pdf1, size_t bytes, int up_world, int down_world, FusedState *st,
                 cudaStream_t s, std::string &err);

@@ -1,7 +1,7 @@
 // k_fused.cu — fused halo exchange over NVLink peer memory (NCCL 2.28 device API).
 //
 // The population arrays live in NCCL symmetric memory windows. The boundary-plane launch of
-// k_pull stores the populations that cross a z face both into its own array and, through LSA
+// k_pull (AA: k_aa_even / k_aa_odd, kernels.cuh) stores the populations that cross a z face both into its own array and, through LSA
 // (load/store accessible) pointers, straight into the neighbour's ghost plane of the same array
 // — no pack kernel, no send/recv, the transfer overlaps the collision math thread by thread
 // (P:1067-1071 for the exchange it replaces). A one-CTA gate kernel at the
@@ -21,8 +21,8 @@ namespace lbm {
 __global__ void k_lsa_peer_bases(ncclWindow_t w0, ncclWindow_t w1, int up, int down, void **out) {
     out[0] = ncclGetLsaPointer(w0, 0, up);
     out[1] = ncclGetLsaPointer(w0, 0, down);
-    out[2] = ncclGetLsaPointer(w1, 0, up);
-    out[3] = ncclGetLsaPointer(w1, 0, down);
+    out[2] = w1 ? ncclGetLsaPointer(w1, 0, up) : nullptr;  // single-array patterns register one window
+    out[3] = w1 ? ncclGetLsaPointer(w1, 0, down) : nullptr;
 }
 
 __global__ void k_lsa_gate(ncclDevComm comm) {
@@ -50,7 +50,7 @@ int fused_setup(ncclComm_t comm, void *pdf0, void *pdf1, size_t bytes, int up_wo
     }
     ncclResult_t r;
     if ((r = ncclCommWindowRegister(comm, pdf0, bytes, &im->win[0], NCCL_WIN_COLL_SYMMETRIC)) != ncclSuccess ||
-        (r = ncclCommWindowRegister(comm, pdf1, bytes, &im->win[1], NCCL_WIN_COLL_SYMMETRIC)) != ncclSuccess) {
+        (pdf1 && (r = ncclCommWindowRegister(comm, pdf1, bytes, &im->win[1], NCCL_WIN_COLL_SYMMETRIC)) != ncclSuccess)) {
         err = std::string("ncclCommWindowRegister: ") + ncclGetErrorString(r);
         return -1;
     }

@@ -30,6 +30,11 @@ void pull_edge_launcher(const StepArgs &a, const void *src, void *dst, const uin
 
 template <int Q, int OP, typename T, int FM, bool FORCE>
 void aa_launcher(const StepArgs &a, void *f, int odd, dim3 grid, dim3 block, cudaStream_t s) {
+    if (a.peer_up != nullptr) {  // fused halo: boundary-plane launch with peer stores (plain kernels)
+        if (odd) k_aa_odd<Q, OP, T, FM, FORCE, true><<<grid, block, 0, s>>>(a, static_cast<T *>(f));
+        else k_aa_even<Q, OP, T, (FM != FM_NONE), FORCE, true><<<grid, block, 0, s>>>(a, static_cast<T *>(f));
+        return;
+    }
     if (odd) {
         if (staged_launch<Q, OP, T, FM, FORCE, SM_AA_ODD>(a, f, f, (int)grid.z, s)) return;
     } else {
@@ -45,7 +50,10 @@ template <int Q, int OP, typename T, bool FORCE>
 void aa_edge_launcher(const StepArgs &a, const void *src, void *f, const uint32_t *cells, uint32_t n, cudaStream_t s) {
     (void)src;
     if (n == 0) return;
-    k_aa_odd_edges<Q, OP, T, FORCE><<<(n + 127) / 128, 128, 0, s>>>(a, static_cast<T *>(f), cells, n);
+    if (a.peer_up != nullptr)
+        k_aa_odd_edges<Q, OP, T, FORCE, true><<<(n + 127) / 128, 128, 0, s>>>(a, static_cast<T *>(f), cells, n);
+    else
+        k_aa_odd_edges<Q, OP, T, FORCE, false><<<(n + 127) / 128, 128, 0, s>>>(a, static_cast<T *>(f), cells, n);
 }
 
 template <int Q, int OP, typename T, int FM, bool FORCE>

@@ -256,7 +256,14 @@ __device__ __forceinline__ T ubb_term(const StepArgs &a, int q) {
     return T(6.0 * S::w(q) * cu);
 }
 
-template <int Q, int OP, typename T, bool FLAGS, bool FORCE>
+// Fused AA halo (PEER): the boundary planes' even step also stores the slots the neighbours' odd step
+// pulls across the face into their ghost planes (top plane, slots with c_z = -1 -> up's plane 0;
+// bottom plane, slots with c_z = +1 -> down's plane nz+1), and the odd step stores its pushes across
+// the face straight into the neighbours' interior planes (top plane, c_z = +1 -> up's plane 1; bottom
+// plane, c_z = -1 -> down's plane nz), through NCCL LSA pointers of the single array. These are the
+// fill and return phases of the NCCL path without a pack, a send/recv or a masked unpack (a wall
+// target never receives a push: the odd step's wall rule keeps that value in the cell's own slot).
+template <int Q, int OP, typename T, bool FLAGS, bool FORCE, bool PEER = false>
 __device__ __forceinline__ void aa_even_cell(const StepArgs &a, T *__restrict__ f, int x, int y, int zs) {
     using S = Stencil<Q>;
     const uint32_t self = ((uint32_t)zs * (uint32_t)a.geo.ny + (uint32_t)y) * (uint32_t)a.geo.nx + (uint32_t)x;
@@ -269,17 +276,33 @@ __device__ __forceinline__ void aa_even_cell(const StepArgs &a, T *__restrict__ 
     collide<Q, OP, T, FORCE>(g, r);
 #pragma unroll
     for (int q = 0; q < Q; ++q) f[S::opp(q) * Sq + self] = g[q];
+    if (PEER) {
+        const uint32_t inplane = (uint32_t)y * (uint32_t)a.geo.nx + (uint32_t)x;
+        const int64_t plane = (int64_t)a.geo.nx * a.geo.ny;
+        if (zs == a.geo.nz) {  // slot qbar with c_qbar,z = -1, i.e. c_q,z = +1
+            T *up = static_cast<T *>(a.peer_up);
+#pragma unroll
+            for (int q = 0; q < Q; ++q)
+                if (S::cz(q) == 1) up[S::opp(q) * Sq + inplane] = g[q];
+        }
+        if (zs == 1) {
+            T *dn = static_cast<T *>(a.peer_down);
+#pragma unroll
+            for (int q = 0; q < Q; ++q)
+                if (S::cz(q) == -1) dn[S::opp(q) * Sq + (a.geo.nz + 1) * plane + inplane] = g[q];
+        }
+    }
 }
 
-template <int Q, int OP, typename T, bool FLAGS, bool FORCE>
+template <int Q, int OP, typename T, bool FLAGS, bool FORCE, bool PEER = false>
 __global__ void __launch_bounds__(256, (MinBlocks<Q, OP, T>::aa)) k_aa_even(const StepArgs a, T *__restrict__ f) {
     const int x = blockIdx.x * blockDim.x + threadIdx.x;
     const int y = blockIdx.y * blockDim.y + threadIdx.y;
     if (x >= a.geo.nx || y >= a.geo.ny) return;
-    aa_even_cell<Q, OP, T, FLAGS, FORCE>(a, f, x, y, a.z_begin + (int)blockIdx.z * a.z_step + a.geo.g);
+    aa_even_cell<Q, OP, T, FLAGS, FORCE, PEER>(a, f, x, y, a.z_begin + (int)blockIdx.z * a.z_step + a.geo.g);
 }
 
-template <int Q, int OP, typename T, int FM, bool FORCE>
+template <int Q, int OP, typename T, int FM, bool FORCE, bool PEER = false>
 __device__ __forceinline__ void aa_odd_cell(const StepArgs &a, T *__restrict__ f, int x, int y, int zs) {
     using S = Stencil<Q>;
     const Nbr n = neighbours(a.geo, x, y, zs);
@@ -312,6 +335,19 @@ __device__ __forceinline__ void aa_odd_cell(const StepArgs &a, T *__restrict__ f
     }
     const Rates<T> r = load_rates<T>(a);
     collide<Q, OP, T, FORCE>(g, r);
+    if (PEER && (zs == a.geo.nz || zs == 1)) {
+        // pushes across the face go straight to the neighbour's interior plane (in-plane target wraps)
+        const int64_t plane = (int64_t)a.geo.nx * a.geo.ny;
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+            const int dz = S::cz(q);
+            if (dz == 0 || (dz == 1) != (zs == a.geo.nz)) continue;
+            if (edge && (wallmask & (1u << S::opp(q)))) continue;  // toward a wall: kept locally below
+            const uint32_t inplane = (uint32_t)n.ys[S::cy(q) + 1] * (uint32_t)a.geo.nx + (uint32_t)n.xs[S::cx(q) + 1];
+            if (dz == 1) static_cast<T *>(a.peer_up)[q * Sq + plane + inplane] = g[q];
+            else static_cast<T *>(a.peer_down)[q * Sq + a.geo.nz * plane + inplane] = g[q];
+        }
+    }
     if (!edge) {
 #pragma unroll
         for (int q = 0; q < Q; ++q) f[q * Sq + nb_off(a.geo, n, S::cx(q), S::cy(q), S::cz(q))] = g[q];
@@ -335,16 +371,16 @@ __device__ __forceinline__ void aa_odd_cell(const StepArgs &a, T *__restrict__ f
 // would come from a wall cell x - c_q is the cell's own bounced C_qbar(x), which the even step left
 // in a[x](q) (+ UBB term of q); a population leaving toward a wall x + c_q returns next step as qbar
 // and is stored directly in a[x](qbar) (+ UBB term of qbar).
-template <int Q, int OP, typename T, int FM, bool FORCE>
+template <int Q, int OP, typename T, int FM, bool FORCE, bool PEER = false>
 __global__ void __launch_bounds__(256, (MinBlocks<Q, OP, T>::aa)) k_aa_odd(const StepArgs a, T *__restrict__ f) {
     const int x = blockIdx.x * blockDim.x + threadIdx.x;
     const int y = blockIdx.y * blockDim.y + threadIdx.y;
     if (x >= a.geo.nx || y >= a.geo.ny) return;
     const int zs = a.z_begin + (int)blockIdx.z * a.z_step + a.geo.g;
-    aa_odd_cell<Q, OP, T, FM, FORCE>(a, f, x, y, zs);
+    aa_odd_cell<Q, OP, T, FM, FORCE, PEER>(a, f, x, y, zs);
 }
 
-template <int Q, int OP, typename T, bool FORCE>
+template <int Q, int OP, typename T, bool FORCE, bool PEER = false>
 __global__ void __launch_bounds__(128) k_aa_odd_edges(const StepArgs a, T *__restrict__ f, const uint32_t *__restrict__ cells,
                                                      uint32_t n) {
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -354,7 +390,7 @@ __global__ void __launch_bounds__(128) k_aa_odd_edges(const StepArgs a, T *__res
     const uint32_t plane = (uint32_t)a.geo.nx * (uint32_t)a.geo.ny;
     const int zs = (int)(c / plane);
     const uint32_t r = c - (uint32_t)zs * plane;
-    aa_odd_cell<Q, OP, T, FM_EDGE, FORCE>(a, f, (int)(r % (uint32_t)a.geo.nx), (int)(r / (uint32_t)a.geo.nx), zs);
+    aa_odd_cell<Q, OP, T, FM_EDGE, FORCE, PEER>(a, f, (int)(r % (uint32_t)a.geo.nx), (int)(r / (uint32_t)a.geo.nx), zs);
 }
 
 // =======================================================================================

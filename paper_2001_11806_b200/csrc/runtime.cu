@@ -208,13 +208,18 @@ void launch_eso_range(lbm_handle_s *h, Slab &s, int odd, int z_begin, int nplane
     launch_edges(h, s, a, h->kern.eso_edges, odd ? s.pdf[0] : nullptr, s.pdf[0], z_begin, nplanes, z_step, st);
 }
 
-void launch_aa_range(lbm_handle_s *h, Slab &s, int odd, int z_begin, int nplanes, int z_step, cudaStream_t st) {
+void launch_aa_range(lbm_handle_s *h, Slab &s, int odd, int z_begin, int nplanes, int z_step, cudaStream_t st,
+                     bool peer_stores = false) {
     if (nplanes <= 0) return;
     StepArgs a = h->base;
     a.geo = geo_of(h, s);
     a.z_begin = z_begin;
     a.z_step = z_step;
     a.flags = s.flags;
+    if (peer_stores) {  // fused halo: LSA bases of the neighbours' single array
+        a.peer_up = h->fst.bases[0];
+        a.peer_down = h->fst.bases[1];
+    }
     tbegin(h, st);
     h->kern.aa(a, s.pdf[0], odd, grid_for(h, nplanes), h->block, st);
     tend(h, st);
@@ -394,6 +399,16 @@ int step_once(lbm_handle_s *h) {
         return LBM_OK;
     }
     Slab &s = h->slabs[0];
+    if (h->fused && aa) {
+        // gate -> boundary planes (even: fill slots into the neighbours' ghost planes; odd: pushes across
+        // the face into the neighbours' interior planes) -> interior planes; no send/recv, no unpack
+        fused_gate(h->fst, st);
+        h->launches++;
+        launch_aa_range(h, s, odd, 0, 2, s.nz - 1, st, true);
+        launch_aa_range(h, s, odd, 1, s.nz - 2, 1, st);
+        h->aa_parity ^= 1;
+        return LBM_OK;
+    }
     if (h->fused) {
         // gate (LSA barrier: all ranks finished the previous step) -> boundary planes with peer
         // stores into the neighbours' ghost planes -> interior planes; one stream, no send/recv
@@ -472,8 +487,8 @@ int validate(const lbm_config *c) {
     if (c->global[2] % P != 0) return fail(nullptr, LBM_EINVAL, "nz % nranks != 0");
     if (P > 1 && c->global[2] / P < 2) return fail(nullptr, LBM_EINVAL, "slabs need at least 2 planes");
     if (c->nranks > 1 && !c->nccl_id) return fail(nullptr, LBM_EINVAL, "nranks > 1 needs an nccl_id");
-    if (c->halo_mode == LBM_HALO_FUSED && ((c->nranks == 1 && !c->nccl_self) || c->pattern != LBM_PULL))
-        return fail(nullptr, LBM_EUNSUPPORTED, "fused halo needs NCCL ranks (or nccl_self) and the pull pattern");
+    if (c->halo_mode == LBM_HALO_FUSED && ((c->nranks == 1 && !c->nccl_self) || c->pattern == LBM_ESOTWIST))
+        return fail(nullptr, LBM_EUNSUPPORTED, "fused halo needs NCCL ranks (or nccl_self) and the pull or AA pattern");
     if (c->halo_mode < 0 || c->halo_mode > 2) return fail(nullptr, LBM_EINVAL, "bad halo_mode");
     if (c->nccl_self && (c->nranks != 1 || c->n_local_slabs > 1 || c->global[2] < 2))
         return fail(nullptr, LBM_EINVAL, "nccl_self needs nranks == 1, one slab and nz >= 2");
@@ -1024,7 +1039,7 @@ int lbm_create(const lbm_config *cfg, lbm_handle *out) {
         if (h->fused) {
             Slab &s = h->slabs[0];
             const size_t bytes = (size_t)geo_of(h, s).Sq * h->Q * h->esize;
-            for (int a = 0; a < 2; ++a) {
+            for (int a = 0; a < (cfg->pattern == LBM_PULL ? 2 : 1); ++a) {
                 if ((r = ncclMemAlloc(&s.pdf[a], bytes)) != ncclSuccess) {
                     h->err = std::string("ncclMemAlloc populations: ") + ncclGetErrorString(r);
                     return bail(LBM_EOOM);

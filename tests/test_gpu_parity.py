@@ -415,14 +415,14 @@ def test_aa_slab_decomposition_bit_identical(P, halo_mode, Q, op, rates, geometr
 @pytest.mark.parametrize("halo_mode", [0, 1, 2])
 @pytest.mark.parametrize("Q,op,rates,geometry,pattern", [(19, "trt", (1.6, 0.5), "channel", "pull"),
                                                          (27, "cumulant", (1.95,), "periodic", "pull"),
-                                                         (19, "trt", (1.6, 0.5), "obstacles", "aa")])
+                                                         (19, "trt", (1.6, 0.5), "obstacles", "aa"),
+                                                         (27, "cumulant", (1.95,), "cavity", "aa"),
+                                                         (19, "mrt", (1.9, 1.3, 1.1, 0.8), "channel", "aa")])
 def test_nccl_self_exchange_bit_identical(halo_mode, Q, op, rates, geometry, pattern):
-    if halo_mode == 2 and pattern == "aa":
-        pytest.skip("fused (NVLink peer-store) halo is implemented for the pull pattern")
     """The NCCL exchange path (ghost planes, schedule, comm stream overlapped with the interior
     launch, event ordering) on one GPU through a 1-rank communicator: bit-identical to local z wrap."""
-    case = Case("self", (16, 12, 10), Q, op, rates, "f64", geometry=geometry, steps=13, pattern=pattern,
-                ubb=(0.02, -0.01, 0.03))
+    case = Case("self", (16, 16, 16) if geometry == "cavity" else (16, 12, 10), Q, op, rates, "f64", geometry=geometry,
+                steps=13, pattern=pattern, ubb=(0.02, -0.01, 0.03))
     one = make_sim(case)
     nc = make_sim(case, nccl_self=True, halo_mode=halo_mode)
     for s in (one, nc):
