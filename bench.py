@@ -265,7 +265,7 @@ def main():
     ap.add_argument("--e2e-reps", type=int, default=2)
     ap.add_argument("--e2e-steps", type=int, default=0, help="LB steps per e2e job (0 = the config's step count)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--halo-mode", type=int, default=-1, help="0 zero-copy NCCL, 1 packed NCCL, 2 fused NVLink peer stores; default: 2 when exchanging (pull), else 0")
+    ap.add_argument("--halo-mode", type=int, default=-1, help="0 zero-copy NCCL, 1 packed NCCL, 2 fused NVLink peer stores; default: 2 when exchanging (pull, AA), else 0")
     ap.add_argument("--nccl-self", type=int, default=0,
                     help="N=1 only: ghost planes exchanged through a 1-rank NCCL communicator (times the multi-GPU path)")
     ap.add_argument("--block-x", type=int, default=0)

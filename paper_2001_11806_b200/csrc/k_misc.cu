@@ -63,6 +63,14 @@ void launch_unpack(int Q, int dtype, const Geo &geo, void *f, int zs, int dir, c
     LBM_DISPATCH(Q, dtype, (k_unpack<QQ, T><<<blocks_for(n), 256, 0, s>>>(geo, static_cast<T *>(f), zs, dir, static_cast<const T *>(in))));
 }
 
+void launch_unpack_masked_eso(int Q, int dtype, const Geo &geo, void *f, int zs, int dir, const void *in, const uint8_t *flags,
+                              int parity_done, cudaStream_t s) {
+    const int64_t n = (int64_t)geo.nx * geo.ny * (Q == 19 ? 5 : 9);
+    LBM_DISPATCH(Q, dtype, (k_unpack_masked_eso<QQ, T><<<blocks_for(n), 256, 0, s>>>(geo, static_cast<T *>(f), zs, dir,
+                                                                                    static_cast<const T *>(in), flags,
+                                                                                    parity_done)));
+}
+
 void launch_unpack_masked(int Q, int dtype, const Geo &geo, void *f, int zs, int dir, const void *in, const uint8_t *flags,
                           cudaStream_t s) {
     const int64_t n = (int64_t)geo.nx * geo.ny * (Q == 19 ? 5 : 9);

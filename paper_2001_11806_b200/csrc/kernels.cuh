@@ -818,6 +818,31 @@ __global__ void k_links(const LinkArgs a, T *__restrict__ f) {
     else f[q * a.Sq + x] = f[qb * a.Sq + b] + t;
 }
 
+// EsoTwist exchange with walls: slot r of location L (storage plane zs) was written by the cell that
+// produced the population stored there — L + c_r^+ after an even step (departing rbar, slot r), L - c_r^-
+// after an odd one (departing r). If that cell is a wall, nothing was produced (the receiving side keeps
+// its own bounced value in that slot), so the entry is skipped.
+template <int Q, typename T>
+__global__ void k_unpack_masked_eso(const Geo geo, T *__restrict__ f, int zs, int dir, const T *__restrict__ in,
+                                    const uint8_t *__restrict__ flags, int parity_done) {
+    using S = Stencil<Q>;
+    const int64_t plane = (int64_t)geo.nx * geo.ny;
+    const int64_t n = plane * S::kCross;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int k = (int)(i / plane);
+        const int64_t r = i - k * plane;
+        const int q = crossing_dir<Q>(dir, k);
+        const int x = (int)(r % geo.nx), y = (int)(r / geo.nx);
+        const int ox = parity_done ? -cneg(S::cx(q)) : cpos(S::cx(q));
+        const int oy = parity_done ? -cneg(S::cy(q)) : cpos(S::cy(q));
+        const int oz = parity_done ? -cneg(S::cz(q)) : cpos(S::cz(q));
+        const int xs = (x + ox + geo.nx) % geo.nx, ys = (y + oy + geo.ny) % geo.ny;
+        const int64_t src = (int64_t)(zs + oz) * plane + (int64_t)ys * geo.nx + xs;
+        LBM_ASSERT(q >= 0 && zs + oz >= 0 && zs + oz < geo.nz + 2 * geo.g);
+        if ((flags[src] & 3) == 0) f[q * geo.Sq + zs * plane + r] = in[i];
+    }
+}
+
 // =======================================================================================
 // Flag preprocessing and diagnostics
 // =======================================================================================

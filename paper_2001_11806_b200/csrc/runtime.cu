@@ -235,13 +235,23 @@ void launch_aa_range(lbm_handle_s *h, Slab &s, int odd, int z_begin, int nplanes
 //   AA return      : A = c_z=+1 slots of the upper ghost -> plane 1;      B = c_z=-1 of the lower ghost -> plane nz
 //                    (after the odd step: its pushes a[x + c_q](q) that landed in ghost planes go home;
 //                    with walls only where the producing cell is fluid)
+//   EsoTwist       : after every step, A = the slots the next step's plane-1 cells read from below, of the
+//                    top plane -> lower ghost (slot set c_z(slot) = -1 after even steps, +1 after odd),
+//                    B = the slots the plane-1 cells wrote into the lower ghost -> the down neighbour's top
+//                    plane (c_z(slot) = +1 after even, -1 after odd). With walls both are masked by the
+//                    cell that produced the slot (EsoTwist rule: L + c^+ after even, L - c^- after odd).
 struct Phase {
     int dirA, sendA, recvA, dirB, sendB, recvB;
     bool masked;
+    int eso_parity = -1;  // EsoTwist exchange: parity of the step just done (selects the producer rule)
 };
 Phase phase_pull(int nz) { return {+1, nz, 0, -1, 1, nz + 1, false}; }
 Phase phase_aa_fill(int nz) { return {-1, nz, 0, +1, 1, nz + 1, false}; }
 Phase phase_aa_return(int nz, bool masked) { return {+1, nz + 1, 1, -1, 0, nz, masked}; }
+Phase phase_eso(int nz, int parity_done, bool masked) {
+    const int d = parity_done ? 1 : -1;
+    return {d, nz, 0, -d, 0, nz, masked, parity_done};
+}
 
 // Zero-copy schedule of a phase (posting order inside one NCCL group). Per peer pair the sends of
 // one side and the receives of the other are posted in the same order, so NCCL matches them even
@@ -263,9 +273,11 @@ std::vector<HaloOp> phase_schedule(int Q, const Phase &ph, int up, int down) {
 
 std::vector<HaloOp> halo_schedule(int Q, int nz, int up, int down) { return phase_schedule(Q, phase_pull(nz), up, down); }
 
-void unpack_face(lbm_handle_s *h, const Slab &d, int arr, int zs, int dir, const void *buf, bool masked, cudaStream_t st) {
+void unpack_face(lbm_handle_s *h, const Slab &d, int arr, int zs, int dir, const void *buf, bool masked, cudaStream_t st,
+                 int eso_parity = -1) {
     const Geo g = geo_of(h, d);
-    if (masked) launch_unpack_masked(h->Q, h->dtype, g, d.pdf[arr], zs, dir, buf, d.flags, st);
+    if (masked && eso_parity >= 0) launch_unpack_masked_eso(h->Q, h->dtype, g, d.pdf[arr], zs, dir, buf, d.flags, eso_parity, st);
+    else if (masked) launch_unpack_masked(h->Q, h->dtype, g, d.pdf[arr], zs, dir, buf, d.flags, st);
     else launch_unpack(h->Q, h->dtype, g, d.pdf[arr], zs, dir, buf, st);
     h->launches++;
 }
@@ -283,9 +295,9 @@ int exchange_loopback(lbm_handle_s *h, const Phase &ph0, ArrSel arr, cudaStream_
             Slab &sd = h->slabs[(r - 1 + P) % P];
             const Phase ph = ph0;
             launch_pack(h->Q, h->dtype, geo_of(h, s), s.pdf[arr(s)], ph.sendA, ph.dirA, s.halo[0], false, st);
-            unpack_face(h, su, arr(su), ph.recvA, ph.dirA, s.halo[0], ph.masked, st);
+            unpack_face(h, su, arr(su), ph.recvA, ph.dirA, s.halo[0], ph.masked, st, ph.eso_parity);
             launch_pack(h->Q, h->dtype, geo_of(h, s), s.pdf[arr(s)], ph.sendB, ph.dirB, s.halo[1], false, st);
-            unpack_face(h, sd, arr(sd), ph.recvB, ph.dirB, s.halo[1], ph.masked, st);
+            unpack_face(h, sd, arr(sd), ph.recvB, ph.dirB, s.halo[1], ph.masked, st, ph.eso_parity);
             h->launches += 2;
         }
         return LBM_OK;
@@ -329,8 +341,8 @@ int exchange_nccl(lbm_handle_s *h, const Phase &ph, int arr, cudaStream_t st) {
         NCCL_TRY(h, ncclSend(s.halo[1], plane * ncross, dt, h->down, h->comm, st));
         NCCL_TRY(h, ncclRecv(s.halo[3], plane * ncross, dt, h->up, h->comm, st));
         NCCL_TRY(h, ncclGroupEnd());
-        unpack_face(h, s, arr, ph.recvA, ph.dirA, s.halo[2], ph.masked, st);
-        unpack_face(h, s, arr, ph.recvB, ph.dirB, s.halo[3], ph.masked, st);
+        unpack_face(h, s, arr, ph.recvA, ph.dirA, s.halo[2], ph.masked, st, ph.eso_parity);
+        unpack_face(h, s, arr, ph.recvB, ph.dirB, s.halo[3], ph.masked, st, ph.eso_parity);
     } else {
         // zero-copy: each crossing population's plane is one contiguous nx*ny run
         NCCL_TRY(h, ncclGroupStart());
@@ -345,7 +357,8 @@ int exchange_nccl(lbm_handle_s *h, const Phase &ph, int arr, cudaStream_t st) {
 
 // exchange the CURRENT pull state's ghost planes (after init / set_populations), ordered on stream
 int exchange_current(lbm_handle_s *h) {
-    if (h->g == 0 || h->cfg.pattern == LBM_AA) return LBM_OK;  // AA needs ghosts only before odd steps
+    // AA needs ghosts only before odd steps; EsoTwist initialises its lower ghost slots itself
+    if (h->g == 0 || h->cfg.pattern != LBM_PULL) return LBM_OK;
     const Phase ph = phase_pull(h->slabs[0].nz);
     if (h->use_nccl) return exchange_nccl(h, ph, h->slabs[0].cur, h->stream);
     return exchange_loopback(h, ph, [](const Slab &s) { return s.cur; }, h->stream);
@@ -372,18 +385,22 @@ int step_once(lbm_handle_s *h) {
         }
         return LBM_OK;
     }
-    const bool aa = h->cfg.pattern == LBM_AA;
+    const bool eso = h->cfg.pattern == LBM_ESOTWIST;
+    const bool aa = h->cfg.pattern == LBM_AA || eso;  // single array, parity-toggled
     const int odd = h->aa_parity;
     auto bnd = [&](Slab &s) {
-        if (aa) launch_aa_range(h, s, odd, 0, 2, s.nz - 1, st);
+        if (eso) launch_eso_range(h, s, odd, 0, 2, s.nz - 1, st);
+        else if (aa) launch_aa_range(h, s, odd, 0, 2, s.nz - 1, st);
         else launch_pull_range(h, s, 0, 2, s.nz - 1, st);
     };
     auto inner = [&](Slab &s) {
-        if (aa) launch_aa_range(h, s, odd, 1, s.nz - 2, 1, st);
+        if (eso) launch_eso_range(h, s, odd, 1, s.nz - 2, 1, st);
+        else if (aa) launch_aa_range(h, s, odd, 1, s.nz - 2, 1, st);
         else launch_pull_range(h, s, 1, s.nz - 2, 1, st);
     };
     const int nz = h->slabs[0].nz;
-    const Phase ph = !aa ? phase_pull(nz) : (odd ? phase_aa_return(nz, h->have_flags) : phase_aa_fill(nz));
+    const Phase ph = eso ? phase_eso(nz, odd, h->have_flags)
+                         : !aa ? phase_pull(nz) : (odd ? phase_aa_return(nz, h->have_flags) : phase_aa_fill(nz));
     if (!aa)  // index-list boundaries: wall slots (ghost planes included) before the boundary planes read them
         for (Slab &s : h->slabs)
             if (!h->fused) launch_links_fix(h, s, s.pdf[s.cur], 0, st);
@@ -469,8 +486,6 @@ int validate(const lbm_config *c) {
     if (c->collision < 0 || c->collision > 6) return fail(nullptr, LBM_EINVAL, "bad collision");
     if (c->dtype != LBM_F64 && c->dtype != LBM_F32) return fail(nullptr, LBM_EINVAL, "bad dtype");
     if (c->pattern != LBM_PULL && c->pattern != LBM_AA && c->pattern != LBM_ESOTWIST) return fail(nullptr, LBM_EINVAL, "bad pattern");
-    if (c->pattern == LBM_ESOTWIST && (c->nranks > 1 || c->n_local_slabs > 1 || c->nccl_self))
-        return fail(nullptr, LBM_EUNSUPPORTED, "EsoTwist is implemented for a single slab");
     if (c->pattern == LBM_ESOTWIST && c->boundary_mode == LBM_BOUNDARY_LINKS)
         return fail(nullptr, LBM_EUNSUPPORTED, "index-list boundaries are implemented for the pull and AA patterns");
     const int need[] = {1, 2, 1, 1, 0, 2, 1};
@@ -1134,6 +1149,9 @@ static int init_common(lbm_handle h, InitArgs &a, const double *rho, const doubl
             b.u = du + off;
             b.ustride = cells;
             b.zlo = h->g;
+            b.zhi = h->g + s.nz;
+        } else if (b.eso) {
+            b.zlo = h->g;  // EsoTwist: each interior cell writes its arriving populations (lower ghost included)
             b.zhi = h->g + s.nz;
         } else {
             b.zlo = 0;  // random init is keyed by the global index: ghost planes computed directly
