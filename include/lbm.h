@@ -236,6 +236,18 @@ int lbm_crossing_directions(int32_t stencil, int32_t dir, int32_t *q_out);
  * ghost plane; each message is the contiguous nx*ny run of population q in that plane. Returns the
  * number of operations (4 * n_cross) or LBM_EINVAL (also if cap is too small). */
 int lbm_halo_schedule(int32_t stencil, int64_t nz_local, int32_t rank, int32_t nranks, int32_t *out, int32_t cap);
+/* The same for every exchange phase (crossing slot set c_z(slot) = +-1 of one storage plane per face):
+ * LBM_PHASE_PULL (after every pull step), LBM_PHASE_AA_FILL (after AA even steps), LBM_PHASE_AA_RETURN
+ * (after AA odd steps; with walls the library unpacks it masked), LBM_PHASE_ESO_AFTER_EVEN /
+ * LBM_PHASE_ESO_AFTER_ODD (EsoTwist: lower-ghost fill from the down neighbour's top plane and return
+ * of the bottom plane's writes; masked with walls). lbm_halo_schedule == phase LBM_PHASE_PULL. */
+#define LBM_PHASE_PULL 0
+#define LBM_PHASE_AA_FILL 1
+#define LBM_PHASE_AA_RETURN 2
+#define LBM_PHASE_ESO_AFTER_EVEN 3
+#define LBM_PHASE_ESO_AFTER_ODD 4
+int lbm_halo_schedule_phase(int32_t stencil, int32_t phase, int64_t nz_local, int32_t rank, int32_t nranks, int32_t *out,
+                            int32_t cap);
 /* Direction table of a stencil in ABI order: c_out[3*q + d], w_out[q]. Returns Q or LBM_EINVAL. */
 int lbm_stencil_table(int32_t stencil, int32_t *c_out, double *w_out);
 

@@ -247,12 +247,14 @@ class Domain:
         lib().ora_collide_all(self._pc(), _p(a), self._fl())
 
     def aa_even(self, a: np.ndarray) -> None:
-        assert not self.zghost
         assert lib().ora_aa_even(self._pc(), _p(a), self._fl()) == 0
 
     def aa_odd(self, a: np.ndarray) -> None:
-        assert not self.zghost
         assert lib().ora_aa_odd(self._pc(), _p(a), self._fl()) == 0
+
+    def eso_step(self, a: np.ndarray, odd: int) -> None:
+        """One EsoTwist step on the raw array (ghost planes included in slab mode)."""
+        assert (lib().ora_eso_odd if odd else lib().ora_eso_even)(self._pc(), _p(a), self._fl()) == 0
 
     def run_pull(self, f0: np.ndarray, n: int) -> np.ndarray:
         """P(n) = (C o S)^n P(0) with two arrays (G11). Wall cells keep their initial values."""

@@ -711,12 +711,12 @@ int ora_step_push(const ora_cfg *cfg, double *f, double *tmp, const uint8_t *fla
     return ora_stream(cfg, tmp, f, flags);
 }
 
-/* AA pattern (Fig. 3), single array, no ghost planes, optional flag field.
+/* AA pattern (Fig. 3), single array, optional flag field; with ghost planes (slab mode) the
+ * caller exchanges them between steps (the ghost planes are read and written like any storage).
  * Even step: in-place collision with reversed storage: read a[x](q), write a[x](qbar). Wall cells
  * are skipped; boundary conditions act in the odd step (the boundary handling follows
  * the pattern's even/odd access scheme). */
 int ora_aa_even(const ora_cfg *cfg, double *a, const uint8_t *flags) {
-    if (cfg->zghost) return -1;
     ora_stencil_t s;
     build_stencil(cfg->Q, &s);
     int64_t Sq = plane_cells(cfg);
@@ -743,7 +743,6 @@ int ora_aa_even(const ora_cfg *cfg, double *a, const uint8_t *flags) {
  *          the UBB term of qbar.
  * Each fluid cell reads and writes the same set of slots, so cells are independent. */
 int ora_aa_odd(const ora_cfg *cfg, double *a, const uint8_t *flags) {
-    if (cfg->zghost) return -1;
     ora_stencil_t s;
     build_stencil(cfg->Q, &s);
     int64_t Sq = plane_cells(cfg);
@@ -806,7 +805,6 @@ static int64_t eso_loc(const ora_cfg *cfg, const ora_stencil_t *s, int64_t x, in
 }
 
 static int ora_eso_step(const ora_cfg *cfg, double *a, const uint8_t *flags, int odd) {
-    if (cfg->zghost) return -1;
     ora_stencil_t s;
     build_stencil(cfg->Q, &s);
     int64_t Sq = plane_cells(cfg);

@@ -806,8 +806,20 @@ int lbm_crossing_directions(int32_t stencil, int32_t dir, int32_t *q_out) {
 }
 
 int lbm_halo_schedule(int32_t stencil, int64_t nz_local, int32_t rank, int32_t nranks, int32_t *out, int32_t cap) {
-    if ((stencil != 19 && stencil != 27) || nranks < 1 || rank < 0 || rank >= nranks || nz_local < 2 || !out) return LBM_EINVAL;
-    const auto ops = halo_schedule(stencil, (int)nz_local, (rank + 1) % nranks, (rank - 1 + nranks) % nranks);
+    return lbm_halo_schedule_phase(stencil, LBM_PHASE_PULL, nz_local, rank, nranks, out, cap);
+}
+
+int lbm_halo_schedule_phase(int32_t stencil, int32_t phase, int64_t nz_local, int32_t rank, int32_t nranks, int32_t *out,
+                            int32_t cap) {
+    if ((stencil != 19 && stencil != 27) || nranks < 1 || rank < 0 || rank >= nranks || nz_local < 2 || !out ||
+        phase < LBM_PHASE_PULL || phase > LBM_PHASE_ESO_AFTER_ODD)
+        return LBM_EINVAL;
+    const int nz = (int)nz_local;
+    const Phase ph = phase == LBM_PHASE_PULL ? phase_pull(nz)
+                   : phase == LBM_PHASE_AA_FILL ? phase_aa_fill(nz)
+                   : phase == LBM_PHASE_AA_RETURN ? phase_aa_return(nz, false)
+                   : phase_eso(nz, phase == LBM_PHASE_ESO_AFTER_ODD, false);
+    const auto ops = phase_schedule(stencil, ph, (rank + 1) % nranks, (rank - 1 + nranks) % nranks);
     if ((int)ops.size() > cap) return LBM_EINVAL;
     for (size_t i = 0; i < ops.size(); ++i) {
         out[4 * i + 0] = ops[i].kind;

@@ -98,6 +98,7 @@ _SIGS = {
     "lbm_crossing_directions": ([_I32, _I32, _P], C.c_int),
     "lbm_stencil_table": ([_I32, _P, _P], C.c_int),
     "lbm_halo_schedule": ([_I32, _I64, _I32, _I32, _P, _I32], C.c_int),
+    "lbm_halo_schedule_phase": ([_I32, _I32, _I64, _I32, _I32, _P, _I32], C.c_int),
     "lbm_kernel_pull": ([C.POINTER(lbm_kernel_args)], C.c_int),
     "lbm_kernel_aa": ([C.POINTER(lbm_kernel_args), _I32], C.c_int),
     "lbm_prepare_flags": ([_P, _I64, _I64, _I64, _I32, _P, _P], C.c_int),
@@ -165,12 +166,16 @@ def stencil_table(stencil: int):
     return c.reshape(stencil, 3), w
 
 
-def halo_schedule(stencil: int, nz_local: int, rank: int, nranks: int):
-    """Zero-copy halo operations of one step in NCCL posting order: (kind, peer, q, plane) with
-    kind 0 = send, 1 = recv; plane 0 / nz_local+1 are the ghost planes."""
+PHASE_PULL, PHASE_AA_FILL, PHASE_AA_RETURN, PHASE_ESO_AFTER_EVEN, PHASE_ESO_AFTER_ODD = 0, 1, 2, 3, 4
+
+
+def halo_schedule(stencil: int, nz_local: int, rank: int, nranks: int, phase: int = PHASE_PULL):
+    """Zero-copy halo operations of one exchange phase in NCCL posting order: (kind, peer, q, plane)
+    with kind 0 = send, 1 = recv, q the slot (plane of the q-th population array); plane 0 /
+    nz_local+1 are the ghost planes."""
     out = np.zeros((64, 4), np.int32)
-    n = lbm_halo_schedule(stencil, nz_local, rank, nranks, out.ctypes.data, 64)
-    _check(n, what="lbm_halo_schedule")
+    n = lbm_halo_schedule_phase(stencil, phase, nz_local, rank, nranks, out.ctypes.data, 64)
+    _check(n, what="lbm_halo_schedule_phase")
     return [tuple(int(v) for v in r) for r in out[:n]]
 
 

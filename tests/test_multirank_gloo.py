@@ -24,8 +24,13 @@ def _free_port():
 
 
 CASES = {
-    "trt_channel_force": dict(Q=19, op="trt", rates=(1.6, 0.5), force=(1e-4, 0, 0), geom="channel"),
-    "cumulant_periodic": dict(Q=27, op="cumulant", rates=(1.95,), force=(0, 0, 0), geom="periodic"),
+    "trt_channel_force": dict(Q=19, op="trt", rates=(1.6, 0.5), force=(1e-4, 0, 0), geom="channel", pattern="pull"),
+    "cumulant_periodic": dict(Q=27, op="cumulant", rates=(1.95,), force=(0, 0, 0), geom="periodic", pattern="pull"),
+    "aa_trt_periodic": dict(Q=19, op="trt", rates=(1.6, 0.5), force=(1e-4, 0, 0), geom="periodic", pattern="aa"),
+    "aa_cumulant_periodic": dict(Q=27, op="cumulant", rates=(1.95,), force=(0, 0, 0), geom="periodic", pattern="aa"),
+    "eso_trt_periodic": dict(Q=19, op="trt", rates=(1.6, 0.5), force=(1e-4, 0, 0), geom="periodic", pattern="esotwist"),
+    "eso_mrt_periodic": dict(Q=19, op="mrt", rates=(1.9, 1.3, 1.1, 0.8), force=(0, 0, 0), geom="periodic",
+                             pattern="esotwist"),
 }
 NX, NY, NZ, STEPS = 6, 5, 8, 3
 
@@ -52,14 +57,13 @@ def _worker(rank, world, port, case, out_path):
     full = O.Domain(m, NX, NY, nzl + 2)  # equilibrium of every storage plane
     a = np.ascontiguousarray(full.init_equilibrium(rho, u))
     b = a.copy()
-    sched = L.halo_schedule(c["Q"], nzl, rank, world)
-    for _ in range(STEPS):
-        d.step_pull(a, b)
-        # post the schedule: gloo isend/irecv in the same order NCCL would see them
+
+    def exchange(arr, phase):
+        # post the product's schedule: gloo isend/irecv in the same order NCCL would see them
         reqs, bufs = [], []
-        for kind, peer, q, plane in sched:
+        for kind, peer, q, plane in L.halo_schedule(c["Q"], nzl, rank, world, phase):
             if kind == 0:
-                t = torch.from_numpy(np.ascontiguousarray(b[q, plane]))
+                t = torch.from_numpy(np.ascontiguousarray(arr[q, plane]))
                 bufs.append(t)
                 reqs.append(dist.isend(t, peer))
             else:
@@ -71,9 +75,44 @@ def _worker(rank, world, port, case, out_path):
         for item in bufs:
             if isinstance(item, tuple):
                 t, q, plane = item
-                b[q, plane] = t.numpy()
-        a, b = b, a
-    np.save(os.path.join(out_path, f"rank{rank}.npy"), a[:, 1:-1])
+                arr[q, plane] = t.numpy()
+
+    if c["pattern"] == "pull":
+        for _ in range(STEPS):
+            d.step_pull(a, b)
+            exchange(b, L.PHASE_PULL)
+            a, b = b, a
+        out = a[:, 1:-1]
+    elif c["pattern"] == "aa":
+        # AA: even step (local), ghost fill, odd step, return of the ghost-plane pushes
+        for t in range(STEPS):
+            if t % 2 == 0:
+                d.aa_even(a)
+                exchange(a, L.PHASE_AA_FILL)
+            else:
+                d.aa_odd(a)
+                exchange(a, L.PHASE_AA_RETURN)
+        out = a[:, 1:-1]
+    else:
+        # EsoTwist: the slab's own cells write the arriving populations of the first step, lower ghost included
+        e = np.zeros_like(a)
+        canon = a[:, 1:-1]
+        _, _, _ = O.stencil_arrays(c["Q"])
+        cq, _, _ = O.stencil_arrays(c["Q"])
+        opp = O.stencil_arrays(c["Q"])[2]
+        cp = np.maximum(cq, 0)
+        for q in range(c["Q"]):  # a(x - c_q^+)(q) = f_q(x) for interior x (storage plane z + 1)
+            for z in range(nzl):
+                e[q, z + 1 - cp[q, 2]] = np.roll(canon[q, z], shift=(-cp[q, 1], -cp[q, 0]), axis=(0, 1))
+        for t in range(STEPS):
+            d.eso_step(e, t % 2)
+            exchange(e, L.PHASE_ESO_AFTER_ODD if t % 2 else L.PHASE_ESO_AFTER_EVEN)
+        out = np.zeros_like(canon)
+        for q in range(c["Q"]):  # canonical F_q(x) = a(x - c_q^+)(q or qbar)
+            slot = opp[q] if STEPS % 2 else q
+            for z in range(nzl):
+                out[q, z] = np.roll(e[slot, z + 1 - cp[q, 2]], shift=(cp[q, 1], cp[q, 0]), axis=(0, 1))
+    np.save(os.path.join(out_path, f"rank{rank}.npy"), out)
     dist.barrier()
     dist.destroy_process_group()
 
@@ -87,7 +126,15 @@ def test_decomposed_oracle_with_product_schedule_bit_identical(tmp_path, world, 
     c, fl, m = _setup(case)
     ref_d = O.Domain(m, NX, NY, NZ, flags=fl)
     rho, u = LI.random_fields(0, NX, NY, NZ, 1e-3, 0.01)
-    ref = ref_d.run_pull(ref_d.init_equilibrium(rho, u), STEPS)
+    f0 = ref_d.init_equilibrium(rho, u)
+    ref = ref_d.run_pull(f0, STEPS) if c["pattern"] == "pull" else ref_d.run_push(f0, STEPS)
+    if c["pattern"] == "aa" and STEPS % 2:  # raw AA array after an odd step count: gather
+        got_raw = np.concatenate([np.load(tmp_path / f"rank{r}.npy") for r in range(world)], axis=1)
+        cq, _, opp = O.stencil_arrays(c["Q"])
+        got = np.stack([np.roll(got_raw[opp[q]], shift=(cq[q, 2], cq[q, 1], cq[q, 0]), axis=(0, 1, 2))
+                        for q in range(c["Q"])])
+        np.testing.assert_array_equal(got, ref)
+        return
     got = np.concatenate([np.load(tmp_path / f"rank{r}.npy") for r in range(world)], axis=1)
     mask = np.ones(ref.shape, bool) if fl is None else np.broadcast_to(fl == 0, ref.shape)
     np.testing.assert_array_equal(got[mask], ref[mask])
