@@ -43,6 +43,18 @@ __device__ __forceinline__ T mm_delta(int q, T rho, T ux, T uy, T uz) {
     return T(4) * r24 * (ux * ux + uy * uy + uz * uz);
 }
 
+// Reciprocal for weights (the KBC entropic scalar product): fp64 = hardware approximation
+// (rcp.approx.ftz.f64, ~20 bits) refined by two Newton steps (~1 ulp, no division slow path);
+// fp32 = IEEE division.
+__device__ __forceinline__ double fast_rcp(double x) {
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+    r = r * (2.0 - x * r);
+    r = r * (2.0 - x * r);
+    return r;
+}
+__device__ __forceinline__ float fast_rcp(float x) { return 1.0f / x; }
+
 template <typename T>
 struct Rates {
     T r[16];
@@ -461,8 +473,11 @@ __device__ __forceinline__ void collide_kbc(T (&g)[Q], const Rates<T> &p) {
             const T wr = w * rho;
             const T es = w * drho + wr * (T(4.5) * cu * cu - uu15);
             const T ea = wr * T(3) * cu;
-            const T iq = T(1) / (w + es + ea);
-            const T ib = T(1) / (w + es - ea);
+            // 1/f_eq of the pair from one reciprocal: 1/(A +- B) = (A -+ B) / (A^2 - B^2)
+            const T A = w + es;
+            const T rr = fast_rcp(A * A - ea * ea);
+            const T iq = (A - ea) * rr;
+            const T ib = (A + ea) * rr;
             const T hq = g[q] - s, hb = g[b] - s;
             sh += s * (hq * iq + hb * ib);
             hh += hq * hq * iq + hb * hb * ib;
