@@ -58,6 +58,8 @@ CONFIGS["c4_strong"] = dict(CONFIGS["c4"], shape=(1024, 1024, 1024), weak=False,
 CONFIGS["c3_aa"] = dict(CONFIGS["c3"], pattern="aa", desc="D3Q27 cumulant fp64 384^3 lid-driven cavity, AA pattern")
 # C1/C3 run with index-list boundaries (the faster of the two boundary implementations on the B200,
 # DESIGN.md section 6); the *_flags lines keep the compiled-in flag handling for comparison.
+CONFIGS["c3_aa_links"] = dict(CONFIGS["c3_aa"], boundary_mode="links",
+                              desc="D3Q27 cumulant fp64 384^3 lid-driven cavity, AA pattern, index-list boundaries")
 CONFIGS["c3_flags"] = dict(CONFIGS["c3"], desc=CONFIGS["c3"]["desc"] + ", compiled-in flag boundaries")
 CONFIGS["c3"] = dict(CONFIGS["c3"], boundary_mode="links", desc=CONFIGS["c3"]["desc"] + ", index-list boundaries")
 CONFIGS["c1_f64_flags"] = dict(CONFIGS["c1_f64"], desc=CONFIGS["c1_f64"]["desc"] + ", compiled-in flag boundaries")

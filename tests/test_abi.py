@@ -83,6 +83,8 @@ def test_slab_plan(L):
     (dict(periodic=(1, 0, 1)), -1),                             # non-periodic axis without walls
     (dict(nccl_self=True, n_local_slabs=2), -1),                # self-exchange is single-slab
     (dict(equilibrium=3), -1),                                  # unknown equilibrium kind
+    (dict(shape=(0, 8, 8)), -1),                                # empty lattice
+    (dict(shape=(8, 8, 0)), -1),
     (dict(boundary_mode=2), -1),                                # unknown boundary mode
     (dict(collision="trt", rates=(1.0,) * 15), -1),             # per-moment rates are for MRT
     (dict(collision="mrt", rates=(1.0,) * 14 + (2.0,)), -1),    # per-moment rate outside (0, 2)

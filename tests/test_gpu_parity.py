@@ -347,6 +347,18 @@ def test_persistent_multistep_kernel(case):
     assert err <= TOL[case.dtype], err
 
 
+@pytest.mark.parametrize("pattern", ["pull", "aa", "esotwist"])
+def test_zero_steps_is_identity_and_counters(pattern):
+    """lbm_step(0) launches nothing and leaves the state bit-identical (degenerate call)."""
+    case = Case("zero", (16, 8, 6), 19, "trt", (1.6, 0.5), "f64", pattern=pattern, steps=0)
+    sim = make_sim(case)
+    init_sim(sim, case)
+    before, l0 = sim.populations(raw=True), sim.launches
+    sim.step(0)
+    assert sim.launches == l0
+    np.testing.assert_array_equal(sim.populations(raw=True), before)
+
+
 def test_nan_detection():
     from paper_2001_11806_b200 import lbm as L
     case = Case("nan", (8, 8, 8), 19, "srt", (1.8,), "f64")
