@@ -107,8 +107,9 @@ extern "C" {
  *        flag-free and a separate boundary kernel writes, before each pull step (AA: after each step),
  *        the values the fluid cells stream from the wall cells. Per-link wall
  *        velocities: lbm_boundary_links / lbm_set_link_velocities. Wall cells are updated like fluid
- *        cells and hold meaningless values. Pull: any slab decomposition (the link kernel also fills
- *        the wall slots of ghost planes, after the exchange); AA: single slab (LBM_EUNSUPPORTED). */
+ *        cells and hold meaningless values. Any slab decomposition (the link kernel also fills the wall
+ *        slots of ghost planes, after the exchange); not with the fused halo for AA, not with
+ *        EsoTwist (LBM_EUNSUPPORTED). */
 #define LBM_BOUNDARY_FLAGS 0
 #define LBM_BOUNDARY_LINKS 1
 

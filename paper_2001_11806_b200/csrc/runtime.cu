@@ -411,6 +411,8 @@ int step_once(lbm_handle_s *h) {
                     : exchange_loopback(h, ph, [](const Slab &s) { return 1 - s.cur; }, st);
         if (rc) return rc;
         for (Slab &s : h->slabs) inner(s);
+        if (aa && !eso)  // index-list boundaries (AA): after the exchange, over ghost planes too
+            for (Slab &s : h->slabs) launch_links_fix(h, s, s.pdf[0], odd ? 2 : 1, st);
         if (aa) h->aa_parity ^= 1;
         else for (Slab &s : h->slabs) s.cur ^= 1;
         return LBM_OK;
@@ -445,6 +447,7 @@ int step_once(lbm_handle_s *h) {
     CUDA_TRY(h, cudaEventRecord(h->ev_x, h->comm_stream));
     inner(s);
     CUDA_TRY(h, cudaStreamWaitEvent(st, h->ev_x, 0));  // the next step's boundary planes need the exchange
+    if (aa && !eso) launch_links_fix(h, s, s.pdf[0], odd ? 2 : 1, st);  // index-list boundaries (AA)
     if (aa) h->aa_parity ^= 1;
     else s.cur ^= 1;
     return LBM_OK;
@@ -525,8 +528,8 @@ int validate(const lbm_config *c) {
     }
     if (c->boundary_mode != LBM_BOUNDARY_FLAGS && c->boundary_mode != LBM_BOUNDARY_LINKS)
         return fail(nullptr, LBM_EINVAL, "bad boundary_mode");
-    if (c->boundary_mode == LBM_BOUNDARY_LINKS && c->pattern == LBM_AA && (c->nranks > 1 || c->n_local_slabs > 1 || c->nccl_self))
-        return fail(nullptr, LBM_EUNSUPPORTED, "index-list boundaries with the AA pattern are implemented for a single slab");
+    if (c->boundary_mode == LBM_BOUNDARY_LINKS && c->pattern == LBM_AA && c->halo_mode == LBM_HALO_FUSED)
+        return fail(nullptr, LBM_EUNSUPPORTED, "index-list boundaries with the AA pattern use the NCCL or loopback halo");
     if (c->equilibrium < LBM_EQ_COMPRESSIBLE || c->equilibrium > LBM_EQ_MOMENT_MATCHED)
         return fail(nullptr, LBM_EINVAL, "bad equilibrium");
     if (c->equilibrium != LBM_EQ_COMPRESSIBLE && c->collision != LBM_SRT && c->collision != LBM_TRT &&

@@ -89,7 +89,7 @@ def test_slab_plan(L):
     (dict(collision="trt", rates=(1.0,) * 15), -1),             # per-moment rates are for MRT
     (dict(collision="mrt", rates=(1.0,) * 14 + (2.0,)), -1),    # per-moment rate outside (0, 2)
     (dict(collision="mrt", rates=(1.0,) * 15, equilibrium="incompressible"), -2),
-    (dict(boundary_mode="links", n_local_slabs=2, pattern="aa"), -2),  # AA + index-list: single slab
+    (dict(boundary_mode="links", nccl_self=True, halo_mode=2, pattern="aa"), -2),  # AA + links: no fused halo
     (dict(pattern="esotwist", nccl_self=True, halo_mode=2), -2),  # no fused halo for EsoTwist
     (dict(stencil=27, collision="cumulant", rates=(1.9,), equilibrium="incompressible"), -2),
     (dict(collision="kbc", rates=(1.9,), equilibrium="moment_matched"), -2),
