@@ -267,7 +267,7 @@ def main():
     ap.add_argument("--e2e-reps", type=int, default=2)
     ap.add_argument("--e2e-steps", type=int, default=0, help="LB steps per e2e job (0 = the config's step count)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--halo-mode", type=int, default=-1, help="0 zero-copy NCCL, 1 packed NCCL, 2 fused NVLink peer stores; default: 2 when exchanging (pull, AA), else 0")
+    ap.add_argument("--halo-mode", type=int, default=-1, help="0 zero-copy NCCL, 1 packed NCCL, 2 fused NVLink peer stores; default: 2 when exchanging, else 0")
     ap.add_argument("--nccl-self", type=int, default=0,
                     help="N=1 only: ghost planes exchanged through a 1-rank NCCL communicator (times the multi-GPU path)")
     ap.add_argument("--block-x", type=int, default=0)
@@ -318,8 +318,8 @@ def main():
     use_graph = 0 if nccl_self else use_graph
     exchanging = world > 1 or nccl_self
     halo_mode = args.halo_mode
-    if halo_mode < 0:  # default: fused NVLink peer-store halo for pull and AA, else zero-copy NCCL
-        halo_mode = L.HALO_FUSED if (exchanging and cfg["pattern"] in ("pull", "aa")) else L.HALO_ZEROCOPY
+    if halo_mode < 0:  # default: fused NVLink peer-store halo when exchanging
+        halo_mode = L.HALO_FUSED if exchanging else L.HALO_ZEROCOPY
 
     def make(mode):
         return L.Simulation(gshape, stencil=cfg["Q"], collision=cfg["op"], rates=cfg["rates"], dtype=cfg["dtype"],

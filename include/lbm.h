@@ -78,7 +78,7 @@ extern "C" {
 #define LBM_AA 1   /* one array, AA pattern: state F(n) = (S o C)^n f0 (G11)            */
 #define LBM_ESOTWIST 2 /* one array, EsoTwist as even/odd kernels: populations stored on
                           their links at x - c_q^+, slot q or qbar by parity; state F(n) as AA.
-                          Single slab, flag boundaries (LBM_EUNSUPPORTED otherwise) */
+                          Flag boundaries; any slab decomposition and halo mode */
 
 #define LBM_FLAG_FLUID 0
 #define LBM_FLAG_NOSLIP 1

@@ -58,6 +58,11 @@ void aa_edge_launcher(const StepArgs &a, const void *src, void *f, const uint32_
 
 template <int Q, int OP, typename T, int FM, bool FORCE>
 void eso_launcher(const StepArgs &a, void *f, int odd, dim3 grid, dim3 block, cudaStream_t s) {
+    if (a.peer_up != nullptr) {  // fused halo: boundary-plane launch with peer stores (plain kernels)
+        if (odd) k_eso<Q, OP, T, FM, FORCE, true, true><<<grid, block, 0, s>>>(a, static_cast<T *>(f));
+        else k_eso<Q, OP, T, FM, FORCE, false, true><<<grid, block, 0, s>>>(a, static_cast<T *>(f));
+        return;
+    }
     if (odd ? staged_launch<Q, OP, T, FM, FORCE, SM_ESO_ODD>(a, f, f, (int)grid.z, s)
             : staged_launch<Q, OP, T, FM, FORCE, SM_ESO_EVEN>(a, f, f, (int)grid.z, s))
         return;
@@ -71,8 +76,15 @@ template <int Q, int OP, typename T, bool FORCE>
 void eso_edge_launcher(const StepArgs &a, const void *src, void *f, const uint32_t *cells, uint32_t n, cudaStream_t s) {
     if (n == 0) return;
     const bool odd = src != nullptr;  // runtime passes a non-null marker for odd steps
-    if (odd) k_eso_edges<Q, OP, T, FORCE, true><<<(n + 127) / 128, 128, 0, s>>>(a, static_cast<T *>(f), cells, n);
-    else k_eso_edges<Q, OP, T, FORCE, false><<<(n + 127) / 128, 128, 0, s>>>(a, static_cast<T *>(f), cells, n);
+    const unsigned b = (n + 127) / 128;
+    T *ff = static_cast<T *>(f);
+    if (a.peer_up != nullptr) {
+        if (odd) k_eso_edges<Q, OP, T, FORCE, true, true><<<b, 128, 0, s>>>(a, ff, cells, n);
+        else k_eso_edges<Q, OP, T, FORCE, false, true><<<b, 128, 0, s>>>(a, ff, cells, n);
+    } else {
+        if (odd) k_eso_edges<Q, OP, T, FORCE, true, false><<<b, 128, 0, s>>>(a, ff, cells, n);
+        else k_eso_edges<Q, OP, T, FORCE, false, false><<<b, 128, 0, s>>>(a, ff, cells, n);
+    }
 }
 
 template <int Q, int OP, typename T, int FM, bool FORCE, bool AA>

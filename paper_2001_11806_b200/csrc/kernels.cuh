@@ -408,7 +408,12 @@ __global__ void __launch_bounds__(128) k_aa_odd_edges(const StepArgs a, T *__res
 __host__ __device__ constexpr int cpos(int c) { return c > 0 ? c : 0; }
 __host__ __device__ constexpr int cneg(int c) { return c < 0 ? c : 0; }
 
-template <int Q, int OP, typename T, int FM, bool FORCE, bool ODD>
+// Fused EsoTwist halo (PEER, boundary planes): the regular departing writes that the neighbours read
+// next step are also stored into their copy of the location — top plane, c_z = +1 -> up's lower ghost;
+// bottom plane, c_z = -1 (written into our lower ghost) -> down's top plane. Bounce writes stay local.
+// Within a step the neighbour touches the other slot of those locations (the twist), so only the
+// per-step LSA barrier is needed.
+template <int Q, int OP, typename T, int FM, bool FORCE, bool ODD, bool PEER = false>
 __device__ __forceinline__ void eso_cell(const StepArgs &a, T *__restrict__ f, int x, int y, int zs) {
     using S = Stencil<Q>;
     const Nbr n = neighbours(a.geo, x, y, zs);
@@ -441,18 +446,25 @@ __device__ __forceinline__ void eso_cell(const StepArgs &a, T *__restrict__ f, i
             }
         }
         f[(ODD ? q : S::opp(q)) * Sq + loc] = g[q];
+        if (PEER && S::cz(q) != 0 && (S::cz(q) == 1) == (zs == a.geo.nz) && (zs == a.geo.nz || zs == 1)) {
+            const uint32_t inplane =
+                (uint32_t)n.ys[cneg(S::cy(q)) + 1] * (uint32_t)a.geo.nx + (uint32_t)n.xs[cneg(S::cx(q)) + 1];
+            const int64_t slot = (int64_t)(ODD ? q : S::opp(q)) * Sq;
+            if (S::cz(q) == 1) static_cast<T *>(a.peer_up)[slot + inplane] = g[q];  // up's plane 0
+            else static_cast<T *>(a.peer_down)[slot + (int64_t)a.geo.nz * a.geo.nx * a.geo.ny + inplane] = g[q];
+        }
     }
 }
 
-template <int Q, int OP, typename T, int FM, bool FORCE, bool ODD>
+template <int Q, int OP, typename T, int FM, bool FORCE, bool ODD, bool PEER = false>
 __global__ void __launch_bounds__(256, (MinBlocks<Q, OP, T>::aa)) k_eso(const StepArgs a, T *f) {
     const int x = blockIdx.x * blockDim.x + threadIdx.x;
     const int y = blockIdx.y * blockDim.y + threadIdx.y;
     if (x >= a.geo.nx || y >= a.geo.ny) return;
-    eso_cell<Q, OP, T, FM, FORCE, ODD>(a, f, x, y, a.z_begin + (int)blockIdx.z * a.z_step + a.geo.g);
+    eso_cell<Q, OP, T, FM, FORCE, ODD, PEER>(a, f, x, y, a.z_begin + (int)blockIdx.z * a.z_step + a.geo.g);
 }
 
-template <int Q, int OP, typename T, bool FORCE, bool ODD>
+template <int Q, int OP, typename T, bool FORCE, bool ODD, bool PEER = false>
 __global__ void __launch_bounds__(128) k_eso_edges(const StepArgs a, T *f, const uint32_t *__restrict__ cells, uint32_t n) {
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
@@ -461,7 +473,7 @@ __global__ void __launch_bounds__(128) k_eso_edges(const StepArgs a, T *f, const
     const uint32_t plane = (uint32_t)a.geo.nx * (uint32_t)a.geo.ny;
     const int zs = (int)(c / plane);
     const uint32_t r = c - (uint32_t)zs * plane;
-    eso_cell<Q, OP, T, FM_EDGE, FORCE, ODD>(a, f, (int)(r % (uint32_t)a.geo.nx), (int)(r / (uint32_t)a.geo.nx), zs);
+    eso_cell<Q, OP, T, FM_EDGE, FORCE, ODD, PEER>(a, f, (int)(r % (uint32_t)a.geo.nx), (int)(r / (uint32_t)a.geo.nx), zs);
 }
 
 // =======================================================================================

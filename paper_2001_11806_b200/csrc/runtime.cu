@@ -193,13 +193,18 @@ void launch_pull_range(lbm_handle_s *h, Slab &s, int z_begin, int nplanes, int z
     launch_edges(h, s, a, h->kern.pull_edges, s.pdf[s.cur], s.pdf[1 - s.cur], z_begin, nplanes, z_step, st);
 }
 
-void launch_eso_range(lbm_handle_s *h, Slab &s, int odd, int z_begin, int nplanes, int z_step, cudaStream_t st) {
+void launch_eso_range(lbm_handle_s *h, Slab &s, int odd, int z_begin, int nplanes, int z_step, cudaStream_t st,
+                      bool peer_stores = false) {
     if (nplanes <= 0) return;
     StepArgs a = h->base;
     a.geo = geo_of(h, s);
     a.z_begin = z_begin;
     a.z_step = z_step;
     a.flags = s.flags;
+    if (peer_stores) {
+        a.peer_up = h->fst.bases[0];
+        a.peer_down = h->fst.bases[1];
+    }
     tbegin(h, st);
     h->kern.eso(a, s.pdf[0], odd, grid_for(h, nplanes), h->block, st);
     tend(h, st);
@@ -418,6 +423,15 @@ int step_once(lbm_handle_s *h) {
         return LBM_OK;
     }
     Slab &s = h->slabs[0];
+    if (h->fused && eso) {
+        // gate -> boundary planes with peer stores of the link slots the neighbours read next -> interior
+        fused_gate(h->fst, st);
+        h->launches++;
+        launch_eso_range(h, s, odd, 0, 2, s.nz - 1, st, true);
+        launch_eso_range(h, s, odd, 1, s.nz - 2, 1, st);
+        h->aa_parity ^= 1;
+        return LBM_OK;
+    }
     if (h->fused && aa) {
         // gate -> boundary planes (even: fill slots into the neighbours' ghost planes; odd: pushes across
         // the face into the neighbours' interior planes) -> interior planes; no send/recv, no unpack
@@ -505,8 +519,8 @@ int validate(const lbm_config *c) {
     if (c->global[2] % P != 0) return fail(nullptr, LBM_EINVAL, "nz % nranks != 0");
     if (P > 1 && c->global[2] / P < 2) return fail(nullptr, LBM_EINVAL, "slabs need at least 2 planes");
     if (c->nranks > 1 && !c->nccl_id) return fail(nullptr, LBM_EINVAL, "nranks > 1 needs an nccl_id");
-    if (c->halo_mode == LBM_HALO_FUSED && ((c->nranks == 1 && !c->nccl_self) || c->pattern == LBM_ESOTWIST))
-        return fail(nullptr, LBM_EUNSUPPORTED, "fused halo needs NCCL ranks (or nccl_self) and the pull or AA pattern");
+    if (c->halo_mode == LBM_HALO_FUSED && c->nranks == 1 && !c->nccl_self)
+        return fail(nullptr, LBM_EUNSUPPORTED, "fused halo needs NCCL ranks (or nccl_self)");
     if (c->halo_mode < 0 || c->halo_mode > 2) return fail(nullptr, LBM_EINVAL, "bad halo_mode");
     if (c->nccl_self && (c->nranks != 1 || c->n_local_slabs > 1 || c->global[2] < 2))
         return fail(nullptr, LBM_EINVAL, "nccl_self needs nranks == 1, one slab and nz >= 2");

@@ -90,7 +90,6 @@ def test_slab_plan(L):
     (dict(collision="mrt", rates=(1.0,) * 14 + (2.0,)), -1),    # per-moment rate outside (0, 2)
     (dict(collision="mrt", rates=(1.0,) * 15, equilibrium="incompressible"), -2),
     (dict(boundary_mode="links", nccl_self=True, halo_mode=2, pattern="aa"), -2),  # AA + links: no fused halo
-    (dict(pattern="esotwist", nccl_self=True, halo_mode=2), -2),  # no fused halo for EsoTwist
     (dict(stencil=27, collision="cumulant", rates=(1.9,), equilibrium="incompressible"), -2),
     (dict(collision="kbc", rates=(1.9,), equilibrium="moment_matched"), -2),
 ])

@@ -648,7 +648,7 @@ def test_index_list_boundaries_slabs_bit_identical(P, halo_mode, nccl_self, patt
     np.testing.assert_array_equal(one.populations()[mask], many.populations()[mask])
 
 
-@pytest.mark.parametrize("P,halo_mode,nccl_self", [(2, 0, False), (4, 1, False), (1, 0, True), (1, 1, True)])
+@pytest.mark.parametrize("P,halo_mode,nccl_self", [(2, 0, False), (4, 1, False), (1, 0, True), (1, 1, True), (1, 2, True)])
 @pytest.mark.parametrize("Q,op,rates,geometry", [(19, "trt", (1.6, 0.5), "obstacles"), (27, "cumulant", (1.95,), "periodic"),
                                                  (19, "mrt", (1.9, 1.3, 1.1, 0.8), "channel")])
 def test_esotwist_slab_decomposition_bit_identical(P, halo_mode, nccl_self, Q, op, rates, geometry):
