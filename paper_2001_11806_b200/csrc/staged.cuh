@@ -1,30 +1,31 @@
-// staged.cuh — TMA-staged persistent update kernels (bulk kernels of the pull and AA patterns).
+// staged.cuh — TMA-staged persistent update kernels (bulk kernels of the pull, AA and EsoTwist
+// patterns).
 //
 // The plain kernels (kernels.cuh) keep every population load of a cell in registers until it
 // arrives, so the bytes a SM has in flight are bounded by registers x occupancy; the heavy
 // operators (MRT, cumulant, KBC) need 80-170 registers per thread and fall short of the ~50 KB per
 // SM that Little's law asks for at HBM3e bandwidth. Here the loads are
-// decoupled from registers: a persistent CTA walks x-row segments ("tiles", BT cells of one row
-// y of one plane z); for every direction q one warp-0 lane issues a 1-D bulk copy
-// (cp.async.bulk, the TMA engine) of the source row segment of that direction into a shared-
-// memory stage, completion is signalled on the stage's mbarrier (complete_tx), and NSTAGE tiles
-// are in flight while the CTA computes the current one. Each thread then gathers its Q values
-// from shared memory (x-shift of the direction applied there), collides in registers and stores
-// straight to global memory (the stores are fire-and-forget).
+// decoupled from registers. A persistent CTA = BT consumer threads + one producer warp walks tiles
+// of H full x-rows of one plane. Full rows are contiguous in the [q][z][y][x] layout, so for every
+// direction q the producer issues ONE 1-D bulk copy (cp.async.bulk, the TMA engine; two when the
+// y-shift wraps) of the shifted source rows into a shared-memory ring of nstages stages, arming the
+// stage's "full" mbarrier with expect_tx; consumer warps wait on it, gather their Q values from
+// shared memory (the x-shift and the periodic x-wrap are index arithmetic inside the staged row),
+// release the stage on its "empty" mbarrier, collide in registers and store straight to global
+// memory. Warp specialisation keeps the copy issue off the consumers' critical path: one warp
+// issues about one bulk copy per ~125 cycles, so copies are kept >= 2 KB (scripts/tma_probe.cu).
 //
 //   pull: plane q of src, row (y - cy, z - cz), element x - cx; store dst[x](q)
 //   AA even: plane q of f, row (y, z), element x; store f[x](qbar)
 //   AA odd             : plane qbar of f, row (y - cy, z - cz), element x - cx; store f[x + c](q)
+//   EsoTwist: slot q (even) / qbar (odd) of location x - c^+; store at x + c^- (slot
+//                        qbar / q)
 //
-// In-place safety (AA): every slot a cell reads in a step is written in that step by the same cell
-// only (even: (x, q) -> (x, qbar); odd: reads (x - c_q, qbar) = (x + c_qbar, qbar), which it writes
-// for direction qbar), and a CTA only prefetches rows of its own future tiles, so the early reads
-// of the prefetch never see another cell's write of this step.
-//
-// A row segment [x0, x0 + W) is copied with a pad of A = 16 B / sizeof(T) elements on each side
-// (the x-shifted directions read x0 - 1 and x0 + W); at the row ends the pad is filled from the
-// other end of the row (periodic x). Bulk copies need 16-byte aligned addresses and sizes: the
-// launcher only uses this path when nx * sizeof(T) % 16 == 0 (then every row start is aligned).
+// In-place safety (AA, EsoTwist): every slot a cell reads in a step is written in that step by the
+// same cell only, and a CTA prefetches only rows of its own future tiles, so the early reads of the
+// prefetch never see another cell's write of this step. Bulk copies need 16-byte aligned addresses
+// and sizes: the launcher uses this path only when nx * sizeof(T) % 16 == 0 (then every row start
+// is aligned); flag rows are staged too when nx % 16 == 0.
 #pragma once
 #include "kernels.cuh"
 
@@ -87,7 +88,6 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
 __device__ __forceinline__ void mbar_arrive(uint64_t *b) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
 }
-__device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
 // Tile = hl (<= H) consecutive full x-rows y0 .. y0+hl-1 of one storage plane zs. Full rows are
 // contiguous in the [q][z][y][x] layout, so the source rows of a direction are one bulk copy (two
