@@ -459,7 +459,10 @@ def main():
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                          "traffic": load_traffic(args.config), "peak_source": peak_src,
                          "algorithmic_bytes_per_cell": bpc, "cells_per_launch": nf_local,
-                         "kernel_ms_per_step": kernel_ms_per_step, "kernel_launches_timed": klaunch},
+                         "kernel_ms_per_step": kernel_ms_per_step, "kernel_launches_timed": klaunch,
+                         "frac_of_nominal_8tbs": achieved / 8000.0,
+                         "boundary_mode": cfg.get("boundary_mode", "flags") if flags is not None else "none",
+                         "kernel_path": L.kernel_path()},
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches,
