@@ -15,7 +15,13 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "liblbm_b200.so")
 OBJ = os.path.join(HERE, "build_obj")
-SOURCES = ["runtime.cu", "k_misc.cu", "k_trt.cu", "k_mrt.cu", "k_cumulant.cu", "k_identity.cu", "k_fused.cu", "k_les.cu", "k_eq_inc.cu", "k_eq_mm.cu", "k_cumulant19.cu", "k_kbc27.cu", "k_mrt_rows.cu"]
+SOURCES = ["runtime.cu", "k_misc.cu", "k_fused.cu", "k_select.cu", "k_mrt_rows.cu"]
+# k_inst.cu is compiled once per kernel family: (function, op | eq << 4, Q, dtype, Guo-forced variants too)
+_OPS = [("trt", 1, 1, (19, 27)), ("mrt", 2, 0, (19,)), ("cum", 3, 0, (19, 27)), ("ident", 4, 0, (19, 27)),
+        ("smag", 5, 0, (19, 27)), ("kbc", 6, 0, (19, 27)),
+        ("trt_inc", 1 | 16, 1, (19, 27)), ("mrt_inc", 2 | 16, 0, (19,)),  # incompressible Eq. (3)
+        ("trt_mm", 1 | 32, 1, (19,)), ("mrt_mm", 2 | 32, 0, (19,))]        # moment-matched D3Q19
+INSTANCES = [(f"inst_{n}{q}{t[0]}", op, q, t, force) for n, op, force, qs in _OPS for q in qs for t in ("double", "float")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
@@ -56,9 +62,10 @@ def build(force: bool = False, verbose: bool = False, defines=(), out: str = OUT
     os.makedirs(obj_dir, exist_ok=True)
     flags = _flags() + [f"-D{d}" for d in defines]
 
-    def compile_one(src):
-        obj = os.path.join(obj_dir, src.replace(".cu", ".o"))
-        cmd = [NVCC, "-c", os.path.join(CSRC, src), "-o", obj] + flags
+    def compile_one(job):
+        src, extra, name = job
+        obj = os.path.join(obj_dir, name + ".o")
+        cmd = [NVCC, "-c", os.path.join(CSRC, src), "-o", obj] + flags + extra
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"nvcc failed for {src}:\n{r.stderr[-8000:]}")
@@ -66,8 +73,12 @@ def build(force: bool = False, verbose: bool = False, defines=(), out: str = OUT
             fh.write(r.stderr)
         return obj
 
-    with cf.ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
-        objs = list(ex.map(compile_one, SOURCES))
+    jobs = [(src, [], src[:-3]) for src in SOURCES]
+    jobs += [("k_inst.cu", [f"-DLBM_INST_NAME={n}", f"-DLBM_INST_OP={op}", f"-DLBM_INST_Q={q}", f"-DLBM_INST_T={t}",
+                            f"-DLBM_INST_FORCE={force}"], n) for n, op, q, t, force in INSTANCES]
+    jobs.sort(key=lambda j: j[0] != "k_inst.cu")  # the long ones first
+    with cf.ThreadPoolExecutor(max_workers=min(len(jobs), os.cpu_count() or 8)) as ex:
+        objs = list(ex.map(compile_one, jobs))
     _, libdir = nccl_dirs()
     cmd = [NVCC, "-shared", "-o", out + ".tmp"] + objs + ARCH + [
         "-L", libdir, "-l:libnccl.so.2", "-Xlinker", f"-rpath,{libdir}", "-Xcompiler", "-fPIC"]

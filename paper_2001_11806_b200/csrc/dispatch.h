@@ -32,16 +32,12 @@ Kernels select_mrt(int Q, int dtype, int fm, bool force);
 Kernels select_mrt_rows(int Q, int dtype, int fm, bool force);
 int mrt_rows_upload();  // per-moment MRT rows -> __constant__ memory of the current device
 Kernels select_cumulant(int Q, int dtype, int fm, bool force);
-Kernels select_cumulant19(int Q, int dtype, int fm, bool force);
 Kernels select_identity(int Q, int dtype, int fm, bool force);
 Kernels select_smagorinsky(int Q, int dtype, int fm, bool force);
 Kernels select_kbc(int Q, int dtype, int fm, bool force);
-Kernels select_kbc27(int Q, int dtype, int fm, bool force);
-// equilibrium variants (EQ_INCOMPRESSIBLE / EQ_MOMENT_MATCHED of collide.cuh), k_eq_*.cu
+// equilibrium variants (EQ_INCOMPRESSIBLE / EQ_MOMENT_MATCHED of collide.cuh); all in k_select.cu
 Kernels select_trt_eq(int Q, int dtype, int fm, bool force, int eq);
 Kernels select_mrt_eq(int Q, int dtype, int fm, bool force, int eq);
-Kernels select_trt_mm(int Q, int dtype, int fm, bool force);
-Kernels select_mrt_mm(int Q, int dtype, int fm, bool force);
 // Operator dispatch used by the handle API and the low-level kernel ABI (runtime.cu); SRT runs the
 // TRT kernel with equal rates.
 Kernels select_kernels(int collision, int Q, int dtype, int fm, bool force, int eq = 0);

@@ -12,10 +12,12 @@ void pull_launcher(const StepArgs &a, const void *src, void *dst, dim3 grid, dim
     // peer stores (fused halo, boundary-plane launches only) are a separate instantiation so the
     // interior kernel carries no extra live registers
     if (a.peer_up == nullptr && staged_launch<Q, OP, T, FM, FORCE, SM_PULL>(a, src, dst, (int)grid.z, s)) return;
-    if (a.peer_up != nullptr)
-        k_pull<Q, OP, T, FM, FORCE, true><<<grid, block, 0, s>>>(a, static_cast<const T *>(src), static_cast<T *>(dst));
-    else
-        k_pull<Q, OP, T, FM, FORCE, false><<<grid, block, 0, s>>>(a, static_cast<const T *>(src), static_cast<T *>(dst));
+    if constexpr (FM != FM_INLINE)  // the low-level ABI (inline walls) never stores to peers
+        if (a.peer_up != nullptr) {
+            k_pull<Q, OP, T, FM, FORCE, true><<<grid, block, 0, s>>>(a, static_cast<const T *>(src), static_cast<T *>(dst));
+            return;
+        }
+    k_pull<Q, OP, T, FM, FORCE, false><<<grid, block, 0, s>>>(a, static_cast<const T *>(src), static_cast<T *>(dst));
 }
 
 template <int Q, int OP, typename T, bool FORCE>
@@ -30,11 +32,12 @@ void pull_edge_launcher(const StepArgs &a, const void *src, void *dst, const uin
 
 template <int Q, int OP, typename T, int FM, bool FORCE>
 void aa_launcher(const StepArgs &a, void *f, int odd, dim3 grid, dim3 block, cudaStream_t s) {
-    if (a.peer_up != nullptr) {  // fused halo: boundary-plane launch with peer stores (plain kernels)
-        if (odd) k_aa_odd<Q, OP, T, FM, FORCE, true><<<grid, block, 0, s>>>(a, static_cast<T *>(f));
-        else k_aa_even<Q, OP, T, (FM != FM_NONE), FORCE, true><<<grid, block, 0, s>>>(a, static_cast<T *>(f));
-        return;
-    }
+    if constexpr (FM != FM_INLINE)
+        if (a.peer_up != nullptr) {  // fused halo: boundary-plane launch with peer stores (plain kernels)
+            if (odd) k_aa_odd<Q, OP, T, FM, FORCE, true><<<grid, block, 0, s>>>(a, static_cast<T *>(f));
+            else k_aa_even<Q, OP, T, (FM != FM_NONE), FORCE, true><<<grid, block, 0, s>>>(a, static_cast<T *>(f));
+            return;
+        }
     if (odd) {
         if (staged_launch<Q, OP, T, FM, FORCE, SM_AA_ODD>(a, f, f, (int)grid.z, s)) return;
     } else {
@@ -58,11 +61,12 @@ void aa_edge_launcher(const StepArgs &a, const void *src, void *f, const uint32_
 
 template <int Q, int OP, typename T, int FM, bool FORCE>
 void eso_launcher(const StepArgs &a, void *f, int odd, dim3 grid, dim3 block, cudaStream_t s) {
-    if (a.peer_up != nullptr) {  // fused halo: boundary-plane launch with peer stores (plain kernels)
-        if (odd) k_eso<Q, OP, T, FM, FORCE, true, true><<<grid, block, 0, s>>>(a, static_cast<T *>(f));
-        else k_eso<Q, OP, T, FM, FORCE, false, true><<<grid, block, 0, s>>>(a, static_cast<T *>(f));
-        return;
-    }
+    if constexpr (FM != FM_INLINE)
+        if (a.peer_up != nullptr) {  // fused halo: boundary-plane launch with peer stores (plain kernels)
+            if (odd) k_eso<Q, OP, T, FM, FORCE, true, true><<<grid, block, 0, s>>>(a, static_cast<T *>(f));
+            else k_eso<Q, OP, T, FM, FORCE, false, true><<<grid, block, 0, s>>>(a, static_cast<T *>(f));
+            return;
+        }
     if (odd ? staged_launch<Q, OP, T, FM, FORCE, SM_ESO_ODD>(a, f, f, (int)grid.z, s)
             : staged_launch<Q, OP, T, FM, FORCE, SM_ESO_EVEN>(a, f, f, (int)grid.z, s))
         return;
@@ -114,12 +118,17 @@ int persistent_launcher(const StepArgs &a, void *A, void *B, int phase, int nste
 
 template <int Q, int OP, typename T, bool FORCE>
 void pick_persistent(int fm, Kernels &k) {
+    if constexpr (op_eq(OP) != EQ_COMPRESSIBLE) {  // small-domain persistent kernels: base equilibrium only
+        (void)fm, (void)k;
+        return;
+    } else {
     if (fm == FM_NONE) {
         k.persist_pull = &persistent_launcher<Q, OP, T, FM_NONE, FORCE, false>;
         k.persist_aa = &persistent_launcher<Q, OP, T, FM_NONE, FORCE, true>;
     } else {
         k.persist_pull = &persistent_launcher<Q, OP, T, FM_INLINE, FORCE, false>;
         k.persist_aa = &persistent_launcher<Q, OP, T, FM_INLINE, FORCE, true>;
+    }
     }
 }
 

@@ -1,0 +1,88 @@
+// k_select.cu — run-time selection of the kernel families compiled from k_inst.cu (one object per
+// (operator, equilibrium, stencil, dtype), see build.py INSTANCES).
+#include "dispatch.h"
+
+namespace lbm {
+
+Kernels inst_trt19d(int fm, bool force);
+Kernels inst_trt19f(int fm, bool force);
+Kernels inst_trt27d(int fm, bool force);
+Kernels inst_trt27f(int fm, bool force);
+Kernels inst_mrt19d(int fm, bool force);
+Kernels inst_mrt19f(int fm, bool force);
+Kernels inst_cum19d(int fm, bool force);
+Kernels inst_cum19f(int fm, bool force);
+Kernels inst_cum27d(int fm, bool force);
+Kernels inst_cum27f(int fm, bool force);
+Kernels inst_ident19d(int fm, bool force);
+Kernels inst_ident19f(int fm, bool force);
+Kernels inst_ident27d(int fm, bool force);
+Kernels inst_ident27f(int fm, bool force);
+Kernels inst_smag19d(int fm, bool force);
+Kernels inst_smag19f(int fm, bool force);
+Kernels inst_smag27d(int fm, bool force);
+Kernels inst_smag27f(int fm, bool force);
+Kernels inst_kbc19d(int fm, bool force);
+Kernels inst_kbc19f(int fm, bool force);
+Kernels inst_kbc27d(int fm, bool force);
+Kernels inst_kbc27f(int fm, bool force);
+Kernels inst_trt_inc19d(int fm, bool force);
+Kernels inst_trt_inc19f(int fm, bool force);
+Kernels inst_trt_inc27d(int fm, bool force);
+Kernels inst_trt_inc27f(int fm, bool force);
+Kernels inst_mrt_inc19d(int fm, bool force);
+Kernels inst_mrt_inc19f(int fm, bool force);
+Kernels inst_trt_mm19d(int fm, bool force);
+Kernels inst_trt_mm19f(int fm, bool force);
+Kernels inst_mrt_mm19d(int fm, bool force);
+Kernels inst_mrt_mm19f(int fm, bool force);
+
+Kernels select_trt(int Q, int dtype, int fm, bool force) {
+    if (Q == 19) return dtype == 0 ? inst_trt19d(fm, force) : inst_trt19f(fm, force);
+    if (Q == 27) return dtype == 0 ? inst_trt27d(fm, force) : inst_trt27f(fm, force);
+    return Kernels{};
+}
+Kernels select_mrt(int Q, int dtype, int fm, bool force) {
+    if (Q == 19) return dtype == 0 ? inst_mrt19d(fm, force) : inst_mrt19f(fm, force);
+    return Kernels{};
+}
+Kernels select_cumulant(int Q, int dtype, int fm, bool force) {
+    if (Q == 19) return dtype == 0 ? inst_cum19d(fm, force) : inst_cum19f(fm, force);
+    if (Q == 27) return dtype == 0 ? inst_cum27d(fm, force) : inst_cum27f(fm, force);
+    return Kernels{};
+}
+Kernels select_identity(int Q, int dtype, int fm, bool force) {
+    force = false;
+    if (Q == 19) return dtype == 0 ? inst_ident19d(fm, force) : inst_ident19f(fm, force);
+    if (Q == 27) return dtype == 0 ? inst_ident27d(fm, force) : inst_ident27f(fm, force);
+    return Kernels{};
+}
+Kernels select_smagorinsky(int Q, int dtype, int fm, bool force) {
+    if (Q == 19) return dtype == 0 ? inst_smag19d(fm, force) : inst_smag19f(fm, force);
+    if (Q == 27) return dtype == 0 ? inst_smag27d(fm, force) : inst_smag27f(fm, force);
+    return Kernels{};
+}
+Kernels select_kbc(int Q, int dtype, int fm, bool force) {
+    if (Q == 19) return dtype == 0 ? inst_kbc19d(fm, force) : inst_kbc19f(fm, force);
+    if (Q == 27) return dtype == 0 ? inst_kbc27d(fm, force) : inst_kbc27f(fm, force);
+    return Kernels{};
+}
+Kernels select_trt_eq(int Q, int dtype, int fm, bool force, int eq) {
+    if (eq == EQ_INCOMPRESSIBLE) {
+        if (Q == 19) return dtype == 0 ? inst_trt_inc19d(fm, force) : inst_trt_inc19f(fm, force);
+        if (Q == 27) return dtype == 0 ? inst_trt_inc27d(fm, force) : inst_trt_inc27f(fm, force);
+    } else if (eq == EQ_MOMENT_MATCHED) {
+        if (Q == 19) return dtype == 0 ? inst_trt_mm19d(fm, force) : inst_trt_mm19f(fm, force);
+    }
+    return Kernels{};
+}
+Kernels select_mrt_eq(int Q, int dtype, int fm, bool force, int eq) {
+    if (eq == EQ_INCOMPRESSIBLE) {
+        if (Q == 19) return dtype == 0 ? inst_mrt_inc19d(fm, force) : inst_mrt_inc19f(fm, force);
+    } else if (eq == EQ_MOMENT_MATCHED) {
+        if (Q == 19) return dtype == 0 ? inst_mrt_mm19d(fm, force) : inst_mrt_mm19f(fm, force);
+    }
+    return Kernels{};
+}
+
+}  // namespace lbm

@@ -246,9 +246,13 @@ constexpr bool staged_auto() {
 
 template <int Q, int OP, typename T, int FM, bool FORCE, int MODE>
 bool staged_launch(const StepArgs &a, const void *src, void *dst, int nplanes, cudaStream_t s) {
+    if constexpr (FM != FM_NONE && FM != FM_BULK) {  // inline walls (low-level ABI): plain kernels only
+        (void)a, (void)src, (void)dst, (void)nplanes, (void)s;
+        return false;
+    } else {
     constexpr int BT = kStagedBT;
     const int path = staged_path();
-    if (path == 1 || (path == 0 && !staged_auto<Q, OP, MODE>()) || (FM != FM_NONE && FM != FM_BULK)) return false;
+    if (path == 1 || (path == 0 && !staged_auto<Q, OP, MODE>())) return false;
     const int64_t row_bytes = (int64_t)a.geo.nx * (int64_t)sizeof(T);
     if (row_bytes % 16 != 0) return false;
     if ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) % 16 != 0) return false;
@@ -277,6 +281,7 @@ bool staged_launch(const StepArgs &a, const void *src, void *dst, int nplanes, c
     kern<<<grid, BT + 32, smem, s>>>(a, static_cast<const T *>(src), static_cast<T *>(dst), nplanes, H, nst,
                                      (int)(stage_bytes / (int64_t)sizeof(T)));
     return true;
+    }
 }
 
 }  // namespace lbm
