@@ -91,6 +91,10 @@ CONFIGS["eq_mm_c4"] = dict(CONFIGS["c4"], equilibrium="moment_matched",
 CONFIGS["eso_c4"] = dict(CONFIGS["c4"], pattern="esotwist", desc="D3Q19 TRT fp64 512^3 periodic, EsoTwist single array")
 CONFIGS["eso_c3"] = dict(CONFIGS["c3_flags"], pattern="esotwist", desc="D3Q27 cumulant fp64 384^3 cavity, EsoTwist single array")
 CONFIGS["eso_c2"] = dict(CONFIGS["c2"], pattern="esotwist", desc="D3Q19 weighted MRT fp32 512^3 shear wave, EsoTwist")
+# collide-stream-push, two arrays
+CONFIGS["push_c4"] = dict(CONFIGS["c4"], pattern="push", desc="D3Q19 TRT fp64 512^3 periodic, collide-stream-push")
+CONFIGS["push_c3"] = dict(CONFIGS["c3"], pattern="push",
+                          desc="D3Q27 cumulant fp64 384^3 cavity, collide-stream-push, index-list boundaries")
 CONFIGS["eq_inc_c2"] = dict(CONFIGS["c2"], equilibrium="incompressible",
                             desc="D3Q19 weighted MRT fp32 AA 512^3 shear wave, incompressible Eq. (3)")
 

@@ -12,8 +12,8 @@
  *     (G7; D3Q27 and D3Q19); Smagorinsky SRT and KBC.
  *     Equilibrium Eq. (3), 2nd order, compressible (G1), or its incompressible and
  *     moment-matched variants (LBM_EQ_*).
- *   - Storage patterns: two-array stream-pull-collide and the single-array AA
- *      and EsoTwist patterns.
+ *   - Storage patterns: two-array stream-pull-collide and collide-stream-push, the
+ *     single-array AA and EsoTwist patterns; collision-only kernel.
  *   - Boundaries from a uint8 flag field, compiled into the kernel:
  *     0 = fluid, 1 = no-slip bounce-back, 2 = velocity bounce-back UBB (G8).
  *   - Multi-GPU: z-slab decomposition, one ghost plane per side; the populations crossing each z
@@ -76,6 +76,7 @@ extern "C" {
 
 #define LBM_PULL 0 /* two arrays, fused stream-pull-collide: state P(n) = (C o S)^n P(0) */
 #define LBM_AA 1   /* one array, AA pattern: state F(n) = (S o C)^n f0 (G11)            */
+#define LBM_PUSH 3  /* two arrays, fused collide-stream-push: state F(n) as AA */
 #define LBM_ESOTWIST 2 /* one array, EsoTwist as even/odd kernels: populations stored on
                           their links at x - c_q^+, slot q or qbar by parity; state F(n) as AA.
                           Flag boundaries; any slab decomposition and halo mode */
@@ -108,8 +109,8 @@ extern "C" {
  *        the values the fluid cells stream from the wall cells. Per-link wall
  *        velocities: lbm_boundary_links / lbm_set_link_velocities. Wall cells are updated like fluid
  *        cells and hold meaningless values. Any slab decomposition (the link kernel also fills the wall
- *        slots of ghost planes, after the exchange); not with the fused halo for AA, not with
- *        EsoTwist (LBM_EUNSUPPORTED). */
+ *        slots of ghost planes, after the exchange); not with the fused halo for AA and push, not
+ *        with EsoTwist (LBM_EUNSUPPORTED). */
 #define LBM_BOUNDARY_FLAGS 0
 #define LBM_BOUNDARY_LINKS 1
 
@@ -125,7 +126,7 @@ typedef struct lbm_config {
     int32_t collision; /* LBM_SRT .. LBM_IDENTITY */
     int32_t dtype;     /* LBM_F64 | LBM_F32: storage and arithmetic precision. Populations are
                           stored zero-centred, g_q = f_q - w_q (G12), in both precisions. */
-    int32_t pattern;   /* LBM_PULL | LBM_AA | LBM_ESOTWIST */
+    int32_t pattern;   /* LBM_PULL | LBM_AA | LBM_ESOTWIST | LBM_PUSH */
     int32_t n_rates;
     double rates[8];      /* see the collision enum; every rate must lie in (0, 2) */
     double force[3];      /* Guo body force per cell (SRT/TRT only); all zero = force-free kernel */
@@ -280,6 +281,11 @@ typedef struct lbm_kernel_args {
 int lbm_kernel_pull(const lbm_kernel_args *a);
 /* AA even (odd = 0) or odd (odd = 1) step on dst in place (ghost must be 0). */
 int lbm_kernel_aa(const lbm_kernel_args *a, int32_t odd);
+/* Fused collide-stream-push: dst(x + c_q)(q) = C(src(x))_q on the fluid cells of [z_begin, z_end);
+ * a population pushed toward a wall is bounced into dst(x)(qbar) (+ UBB term). */
+int lbm_kernel_push(const lbm_kernel_args *a);
+/* Collision only, in place on dst, fluid cells of [z_begin, z_end). */
+int lbm_kernel_collide(const lbm_kernel_args *a);
 /* Device flag bytes for the kernels: copies host flags (nx*ny*nplanes, values 0/1/2) and marks
  * fluid cells that have a non-fluid neighbour (bit 7). nplanes includes ghost planes. */
 int lbm_prepare_flags(const uint8_t *host_flags, int64_t nx, int64_t ny, int64_t nplanes, int32_t ghost,

@@ -25,6 +25,9 @@ struct Kernels {
     PersistLaunch persist_aa = nullptr;
     AALaunch eso = nullptr;          // EsoTwist even/odd (odd flag)
     EdgeLaunch eso_edges = nullptr;  // near-wall cells; src != nullptr marks the odd step
+    PullLaunch push = nullptr;       // collide-stream-push, two arrays
+    EdgeLaunch push_edges = nullptr;
+    AALaunch collide = nullptr;      // collision only, in place (odd argument unused)
 };
 
 Kernels select_trt(int Q, int dtype, int fm, bool force);

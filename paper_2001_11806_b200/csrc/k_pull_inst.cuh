@@ -60,6 +60,32 @@ void aa_edge_launcher(const StepArgs &a, const void *src, void *f, const uint32_
 }
 
 template <int Q, int OP, typename T, int FM, bool FORCE>
+void push_launcher(const StepArgs &a, const void *src, void *dst, dim3 grid, dim3 block, cudaStream_t s) {
+    if constexpr (FM != FM_INLINE)
+        if (a.peer_up != nullptr) {  // fused halo: boundary-plane launch with peer stores (plain kernels)
+            k_push<Q, OP, T, FM, FORCE, true><<<grid, block, 0, s>>>(a, static_cast<const T *>(src), static_cast<T *>(dst));
+            return;
+        }
+    if (staged_launch<Q, OP, T, FM, FORCE, SM_PUSH>(a, src, dst, (int)grid.z, s)) return;
+    k_push<Q, OP, T, FM, FORCE, false><<<grid, block, 0, s>>>(a, static_cast<const T *>(src), static_cast<T *>(dst));
+}
+
+template <int Q, int OP, typename T, bool FORCE>
+void push_edge_launcher(const StepArgs &a, const void *src, void *dst, const uint32_t *cells, uint32_t n, cudaStream_t s) {
+    if (n == 0) return;
+    const unsigned b = (n + 127) / 128;
+    if (a.peer_up != nullptr)
+        k_push_edges<Q, OP, T, FORCE, true><<<b, 128, 0, s>>>(a, static_cast<const T *>(src), static_cast<T *>(dst), cells, n);
+    else
+        k_push_edges<Q, OP, T, FORCE, false><<<b, 128, 0, s>>>(a, static_cast<const T *>(src), static_cast<T *>(dst), cells, n);
+}
+
+template <int Q, int OP, typename T, bool FLAGS, bool FORCE>
+void collide_launcher(const StepArgs &a, void *f, int, dim3 grid, dim3 block, cudaStream_t s) {
+    k_collide<Q, OP, T, FLAGS, FORCE><<<grid, block, 0, s>>>(a, static_cast<T *>(f));
+}
+
+template <int Q, int OP, typename T, int FM, bool FORCE>
 void eso_launcher(const StepArgs &a, void *f, int odd, dim3 grid, dim3 block, cudaStream_t s) {
     if constexpr (FM != FM_INLINE)
         if (a.peer_up != nullptr) {  // fused halo: boundary-plane launch with peer stores (plain kernels)
@@ -142,6 +168,15 @@ PullLaunch pick_pull_fm(int fm) {
 }
 
 template <int Q, int OP, typename T, bool FORCE>
+PullLaunch pick_push_fm(int fm) {
+    switch (fm) {
+        case FM_INLINE: return &push_launcher<Q, OP, T, FM_INLINE, FORCE>;
+        case FM_BULK: return &push_launcher<Q, OP, T, FM_BULK, FORCE>;
+        default: return &push_launcher<Q, OP, T, FM_NONE, FORCE>;
+    }
+}
+
+template <int Q, int OP, typename T, bool FORCE>
 AALaunch pick_eso_fm(int fm) {
     switch (fm) {
         case FM_INLINE: return &eso_launcher<Q, OP, T, FM_INLINE, FORCE>;
@@ -171,6 +206,9 @@ Kernels pick(int fm, bool force) {
             k.aa_edges = &aa_edge_launcher<Q, OP, T, true>;
             k.eso = pick_eso_fm<Q, OP, T, true>(fm);
             k.eso_edges = &eso_edge_launcher<Q, OP, T, true>;
+            k.push = pick_push_fm<Q, OP, T, true>(fm);
+            k.push_edges = &push_edge_launcher<Q, OP, T, true>;
+            k.collide = fm == FM_NONE ? &collide_launcher<Q, OP, T, false, true> : &collide_launcher<Q, OP, T, true, true>;
             pick_persistent<Q, OP, T, true>(fm, k);
             return k;
         }
@@ -183,6 +221,9 @@ Kernels pick(int fm, bool force) {
     k.aa_edges = &aa_edge_launcher<Q, OP, T, false>;
     k.eso = pick_eso_fm<Q, OP, T, false>(fm);
     k.eso_edges = &eso_edge_launcher<Q, OP, T, false>;
+    k.push = pick_push_fm<Q, OP, T, false>(fm);
+    k.push_edges = &push_edge_launcher<Q, OP, T, false>;
+    k.collide = fm == FM_NONE ? &collide_launcher<Q, OP, T, false, false> : &collide_launcher<Q, OP, T, true, false>;
     pick_persistent<Q, OP, T, false>(fm, k);
     return k;
 }

@@ -477,6 +477,99 @@ __global__ void __launch_bounds__(128) k_eso_edges(const StepArgs a, T *f, const
 }
 
 // =======================================================================================
+// Fused collide-stream-push, two arrays: dst[x + c_q](q) = C(src[x])_q, the push state
+// F(n) = (S o C)^n f0 (G11). Reads are aligned (own cell), stores shifted. Walls (pull rule O6 in push
+// form): a population leaving toward a wall x + c_q comes back as qbar: dst[x](qbar) = C_q + UBB term
+// of qbar. Fused halo (PEER, boundary planes): pushes across the face also go straight into the
+// neighbour's interior plane of its dst array. Collide-only: the same cell update without
+// streaming, in place (k_collide).
+// =======================================================================================
+template <int Q, int OP, typename T, int FM, bool FORCE, bool PEER = false>
+__device__ __forceinline__ void push_cell(const StepArgs &a, const T *__restrict__ src, T *__restrict__ dst, int x, int y,
+                                          int zs) {
+    using S = Stencil<Q>;
+    const Nbr n = neighbours(a.geo, x, y, zs);
+    const int64_t Sq = a.geo.Sq;
+    bool edge = FM == FM_EDGE;
+    const uint32_t self = nb_off(a.geo, n, 0, 0, 0);
+    if (FM == FM_INLINE) {
+        const uint8_t own = a.flags[self];
+        if (own & 3) return;
+        edge = (own & 0x80) != 0;
+    } else if (FM == FM_BULK) {
+        if (a.flags[self] != 0) return;
+    }
+    T g[Q];
+#pragma unroll
+    for (int q = 0; q < Q; ++q) g[q] = ldg_stream(src + q * Sq + self);
+    const Rates<T> r = load_rates<T>(a);
+    collide<Q, OP, T, FORCE>(g, r);
+    const int64_t plane = (int64_t)a.geo.nx * a.geo.ny;
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+        const uint32_t o = nb_off(a.geo, n, S::cx(q), S::cy(q), S::cz(q));
+        if (edge) {
+            const uint8_t fl = a.flags[o] & 3;
+            if (fl != 0) {  // toward a wall: bounced into the cell's own slot qbar
+                T v = g[q];
+                if (fl == 2) v += ubb_term<Q, T>(a, S::opp(q));
+                dst[S::opp(q) * Sq + self] = v;
+                continue;
+            }
+        }
+        dst[q * Sq + o] = g[q];
+        if (PEER && S::cz(q) != 0 && (S::cz(q) == 1) == (zs == a.geo.nz) && (zs == a.geo.nz || zs == 1)) {
+            const uint32_t inplane = (uint32_t)n.ys[S::cy(q) + 1] * (uint32_t)a.geo.nx + (uint32_t)n.xs[S::cx(q) + 1];
+            if (S::cz(q) == 1) static_cast<T *>(a.peer_up)[q * Sq + plane + inplane] = g[q];
+            else static_cast<T *>(a.peer_down)[q * Sq + a.geo.nz * plane + inplane] = g[q];
+        }
+    }
+}
+
+template <int Q, int OP, typename T, int FM, bool FORCE, bool PEER = false>
+__global__ void __launch_bounds__(256, (MinBlocks<Q, OP, T>::aa)) k_push(const StepArgs a, const T *__restrict__ src,
+                                                                          T *__restrict__ dst) {
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    const int y = blockIdx.y * blockDim.y + threadIdx.y;
+    if (x >= a.geo.nx || y >= a.geo.ny) return;
+    push_cell<Q, OP, T, FM, FORCE, PEER>(a, src, dst, x, y, a.z_begin + (int)blockIdx.z * a.z_step + a.geo.g);
+}
+
+template <int Q, int OP, typename T, bool FORCE, bool PEER = false>
+__global__ void __launch_bounds__(128) k_push_edges(const StepArgs a, const T *__restrict__ src, T *__restrict__ dst,
+                                                   const uint32_t *__restrict__ cells, uint32_t n) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint32_t c = cells[i];
+    LBM_ASSERT((int64_t)c < a.geo.Sq);
+    const uint32_t plane = (uint32_t)a.geo.nx * (uint32_t)a.geo.ny;
+    const int zs = (int)(c / plane);
+    const uint32_t r = c - (uint32_t)zs * plane;
+    push_cell<Q, OP, T, FM_EDGE, FORCE, PEER>(a, src, dst, (int)(r % (uint32_t)a.geo.nx), (int)(r / (uint32_t)a.geo.nx), zs);
+}
+
+// collision only, in place (same slot), fluid cells of the launched planes
+template <int Q, int OP, typename T, bool FLAGS, bool FORCE>
+__global__ void __launch_bounds__(256, (MinBlocks<Q, OP, T>::aa)) k_collide(const StepArgs a, T *__restrict__ f) {
+    using S = Stencil<Q>;
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    const int y = blockIdx.y * blockDim.y + threadIdx.y;
+    if (x >= a.geo.nx || y >= a.geo.ny) return;
+    const int zs = a.z_begin + (int)blockIdx.z * a.z_step + a.geo.g;
+    const uint32_t self = ((uint32_t)zs * (uint32_t)a.geo.ny + (uint32_t)y) * (uint32_t)a.geo.nx + (uint32_t)x;
+    const int64_t Sq = a.geo.Sq;
+    if (FLAGS && (a.flags[self] & 3)) return;
+    T g[Q];
+#pragma unroll
+    for (int q = 0; q < Q; ++q) g[q] = f[q * Sq + self];
+    const Rates<T> r = load_rates<T>(a);
+    collide<Q, OP, T, FORCE>(g, r);
+#pragma unroll
+    for (int q = 0; q < Q; ++q) f[q * Sq + self] = g[q];
+    (void)sizeof(S);
+}
+
+// =======================================================================================
 // Persistent multi-step kernel for small single-slab domains (launch-bound otherwise, e.g. the
 // 32^3 config 0): one cooperative launch runs all n steps of an lbm_step call, cells grid-strided,
 // with a grid-wide barrier between steps instead of a kernel boundary. Walls are handled inline.

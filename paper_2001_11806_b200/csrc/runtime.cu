@@ -107,6 +107,9 @@ int crossing(int Q, int dir, int *out) {
     return n;
 }
 
+bool two_arrays(const lbm_handle_s *h) { return h->cfg.pattern == LBM_PULL || h->cfg.pattern == LBM_PUSH; }
+int cur_array(const lbm_handle_s *h, const Slab &s) { return two_arrays(h) ? s.cur : 0; }
+
 Geo geo_of(const lbm_handle_s *h, const Slab &s) {
     Geo g;
     g.nx = (int)h->nx;
@@ -191,6 +194,25 @@ void launch_pull_range(lbm_handle_s *h, Slab &s, int z_begin, int nplanes, int z
     tend(h, st);
     h->launches++;
     launch_edges(h, s, a, h->kern.pull_edges, s.pdf[s.cur], s.pdf[1 - s.cur], z_begin, nplanes, z_step, st);
+}
+
+void launch_push_range(lbm_handle_s *h, Slab &s, int z_begin, int nplanes, int z_step, cudaStream_t st,
+                       bool peer_stores = false) {
+    if (nplanes <= 0) return;
+    StepArgs a = h->base;
+    a.geo = geo_of(h, s);
+    a.z_begin = z_begin;
+    a.z_step = z_step;
+    a.flags = s.flags;
+    if (peer_stores) {  // LSA bases of the neighbours' dst array (1 - cur)
+        a.peer_up = h->fst.bases[2 * (1 - s.cur) + 0];
+        a.peer_down = h->fst.bases[2 * (1 - s.cur) + 1];
+    }
+    tbegin(h, st);
+    h->kern.push(a, s.pdf[s.cur], s.pdf[1 - s.cur], grid_for(h, nplanes), h->block, st);
+    tend(h, st);
+    h->launches++;
+    launch_edges(h, s, a, h->kern.push_edges, s.pdf[s.cur], s.pdf[1 - s.cur], z_begin, nplanes, z_step, st);
 }
 
 void launch_eso_range(lbm_handle_s *h, Slab &s, int odd, int z_begin, int nplanes, int z_step, cudaStream_t st,
@@ -376,7 +398,11 @@ int step_once(lbm_handle_s *h) {
     cudaStream_t st = h->stream;
     if (h->g == 0) {
         Slab &s = h->slabs[0];
-        if (h->cfg.pattern == LBM_ESOTWIST) {
+        if (h->cfg.pattern == LBM_PUSH) {
+            launch_push_range(h, s, 0, s.nz, 1, st);
+            launch_links_fix(h, s, s.pdf[1 - s.cur], 2, st);  // pushes toward walls come back (index lists)
+            s.cur ^= 1;
+        } else if (h->cfg.pattern == LBM_ESOTWIST) {
             launch_eso_range(h, s, h->aa_parity, 0, s.nz, 1, st);
             h->aa_parity ^= 1;
         } else if (h->cfg.pattern == LBM_AA) {
@@ -391,22 +417,27 @@ int step_once(lbm_handle_s *h) {
         return LBM_OK;
     }
     const bool eso = h->cfg.pattern == LBM_ESOTWIST;
+    const bool push = h->cfg.pattern == LBM_PUSH;
     const bool aa = h->cfg.pattern == LBM_AA || eso;  // single array, parity-toggled
     const int odd = h->aa_parity;
     auto bnd = [&](Slab &s) {
-        if (eso) launch_eso_range(h, s, odd, 0, 2, s.nz - 1, st);
+        if (push) launch_push_range(h, s, 0, 2, s.nz - 1, st);
+        else if (eso) launch_eso_range(h, s, odd, 0, 2, s.nz - 1, st);
         else if (aa) launch_aa_range(h, s, odd, 0, 2, s.nz - 1, st);
         else launch_pull_range(h, s, 0, 2, s.nz - 1, st);
     };
     auto inner = [&](Slab &s) {
-        if (eso) launch_eso_range(h, s, odd, 1, s.nz - 2, 1, st);
+        if (push) launch_push_range(h, s, 1, s.nz - 2, 1, st);
+        else if (eso) launch_eso_range(h, s, odd, 1, s.nz - 2, 1, st);
         else if (aa) launch_aa_range(h, s, odd, 1, s.nz - 2, 1, st);
         else launch_pull_range(h, s, 1, s.nz - 2, 1, st);
     };
     const int nz = h->slabs[0].nz;
-    const Phase ph = eso ? phase_eso(nz, odd, h->have_flags)
+    // push: the pushes that landed in ghost planes go home after every step (the AA return phase)
+    const Phase ph = push ? phase_aa_return(nz, h->have_flags)
+                   : eso ? phase_eso(nz, odd, h->have_flags)
                          : !aa ? phase_pull(nz) : (odd ? phase_aa_return(nz, h->have_flags) : phase_aa_fill(nz));
-    if (!aa)  // index-list boundaries: wall slots (ghost planes included) before the boundary planes read them
+    if (!aa && !push)  // index-list boundaries: wall slots (ghost planes included) before the boundary planes read them
         for (Slab &s : h->slabs)
             if (!h->fused) launch_links_fix(h, s, s.pdf[s.cur], 0, st);
     if (!h->use_nccl) {
@@ -418,11 +449,21 @@ int step_once(lbm_handle_s *h) {
         for (Slab &s : h->slabs) inner(s);
         if (aa && !eso)  // index-list boundaries (AA): after the exchange, over ghost planes too
             for (Slab &s : h->slabs) launch_links_fix(h, s, s.pdf[0], odd ? 2 : 1, st);
+        if (push)
+            for (Slab &s : h->slabs) launch_links_fix(h, s, s.pdf[1 - s.cur], 2, st);
         if (aa) h->aa_parity ^= 1;
         else for (Slab &s : h->slabs) s.cur ^= 1;
         return LBM_OK;
     }
     Slab &s = h->slabs[0];
+    if (h->fused && push) {
+        fused_gate(h->fst, st);
+        h->launches++;
+        launch_push_range(h, s, 0, 2, s.nz - 1, st, true);
+        launch_push_range(h, s, 1, s.nz - 2, 1, st);
+        s.cur ^= 1;
+        return LBM_OK;
+    }
     if (h->fused && eso) {
         // gate -> boundary planes with peer stores of the link slots the neighbours read next -> interior
         fused_gate(h->fst, st);
@@ -462,6 +503,7 @@ int step_once(lbm_handle_s *h) {
     inner(s);
     CUDA_TRY(h, cudaStreamWaitEvent(st, h->ev_x, 0));  // the next step's boundary planes need the exchange
     if (aa && !eso) launch_links_fix(h, s, s.pdf[0], odd ? 2 : 1, st);  // index-list boundaries (AA)
+    if (push) launch_links_fix(h, s, s.pdf[1 - s.cur], 2, st);
     if (aa) h->aa_parity ^= 1;
     else s.cur ^= 1;
     return LBM_OK;
@@ -469,18 +511,18 @@ int step_once(lbm_handle_s *h) {
 
 bool graph_ok(const lbm_handle_s *h) { return h->cfg.use_graph == 1 && h->g == 0 && h->slabs.size() == 1 && !h->timing.on; }
 bool persistent_ok(const lbm_handle_s *h) {
-    return h->cfg.use_graph == 2 && !h->links && h->cfg.pattern != LBM_ESOTWIST && h->g == 0 && h->slabs.size() == 1 && h->kern.persist_pull && h->kern.persist_aa;
+    return h->cfg.use_graph == 2 && !h->links && (h->cfg.pattern == LBM_PULL || h->cfg.pattern == LBM_AA) && h->g == 0 && h->slabs.size() == 1 && h->kern.persist_pull && h->kern.persist_aa;
 }
 
 int run_graph_cycle(lbm_handle_s *h) {
     // one cycle = two steps (pull: src->dst->src; AA: even+odd), replayed; state returns to the same slots
-    if (!h->graph || h->graph_parity != (h->cfg.pattern != LBM_PULL ? h->aa_parity : h->slabs[0].cur)) {
+    if (!h->graph || h->graph_parity != (!two_arrays(h) ? h->aa_parity : h->slabs[0].cur)) {
         if (h->graph) {
             cudaGraphExecDestroy(h->graph);
             h->graph = nullptr;
         }
         cudaGraph_t gr;
-        const int par = h->cfg.pattern != LBM_PULL ? h->aa_parity : h->slabs[0].cur;
+        const int par = !two_arrays(h) ? h->aa_parity : h->slabs[0].cur;
         CUDA_TRY(h, cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
         const int64_t l0 = h->launches;
         step_once(h);
@@ -502,7 +544,7 @@ int validate(const lbm_config *c) {
     if (c->stencil != 19 && c->stencil != 27) return fail(nullptr, LBM_EINVAL, "stencil must be 19 or 27");
     if (c->collision < 0 || c->collision > 6) return fail(nullptr, LBM_EINVAL, "bad collision");
     if (c->dtype != LBM_F64 && c->dtype != LBM_F32) return fail(nullptr, LBM_EINVAL, "bad dtype");
-    if (c->pattern != LBM_PULL && c->pattern != LBM_AA && c->pattern != LBM_ESOTWIST) return fail(nullptr, LBM_EINVAL, "bad pattern");
+    if (c->pattern < LBM_PULL || c->pattern > LBM_PUSH) return fail(nullptr, LBM_EINVAL, "bad pattern");
     if (c->pattern == LBM_ESOTWIST && c->boundary_mode == LBM_BOUNDARY_LINKS)
         return fail(nullptr, LBM_EUNSUPPORTED, "index-list boundaries are implemented for the pull and AA patterns");
     const int need[] = {1, 2, 1, 1, 0, 2, 1};
@@ -542,8 +584,9 @@ int validate(const lbm_config *c) {
     }
     if (c->boundary_mode != LBM_BOUNDARY_FLAGS && c->boundary_mode != LBM_BOUNDARY_LINKS)
         return fail(nullptr, LBM_EINVAL, "bad boundary_mode");
-    if (c->boundary_mode == LBM_BOUNDARY_LINKS && c->pattern == LBM_AA && c->halo_mode == LBM_HALO_FUSED)
-        return fail(nullptr, LBM_EUNSUPPORTED, "index-list boundaries with the AA pattern use the NCCL or loopback halo");
+    if (c->boundary_mode == LBM_BOUNDARY_LINKS && (c->pattern == LBM_AA || c->pattern == LBM_PUSH) &&
+        c->halo_mode == LBM_HALO_FUSED)
+        return fail(nullptr, LBM_EUNSUPPORTED, "index-list boundaries with the AA / push patterns use the NCCL or loopback halo");
     if (c->equilibrium < LBM_EQ_COMPRESSIBLE || c->equilibrium > LBM_EQ_MOMENT_MATCHED)
         return fail(nullptr, LBM_EINVAL, "bad equilibrium");
     if (c->equilibrium != LBM_EQ_COMPRESSIBLE && c->collision != LBM_SRT && c->collision != LBM_TRT &&
@@ -781,6 +824,38 @@ int lbm_kernel_aa(const lbm_kernel_args *k, int32_t odd) {
     return cudaGetLastError() == cudaSuccess ? LBM_OK : LBM_ECUDA;
 }
 
+int lbm_kernel_push(const lbm_kernel_args *k) {
+    StepArgs a;
+    int rc = kernel_args_common(k, a, false);
+    if (rc) return rc;
+    const bool flags = k->flags != nullptr;
+    const bool force = k->force[0] != 0 || k->force[1] != 0 || k->force[2] != 0;
+    const PullLaunch fn = select_kernels(k->collision, k->stencil, k->dtype, flags ? FM_INLINE : FM_NONE, force, k->equilibrium).push;
+    if (!fn) return LBM_EUNSUPPORTED;
+    if (k->z_end == k->z_begin) return LBM_OK;
+    const dim3 b = kernel_block(k->shape[0], k->shape[1]);
+    const dim3 grid((unsigned)((k->shape[0] + b.x - 1) / b.x), (unsigned)((k->shape[1] + b.y - 1) / b.y),
+                    (unsigned)(k->z_end - k->z_begin));
+    fn(a, k->src, k->dst, grid, b, static_cast<cudaStream_t>(k->stream));
+    return cudaGetLastError() == cudaSuccess ? LBM_OK : LBM_ECUDA;
+}
+
+int lbm_kernel_collide(const lbm_kernel_args *k) {
+    StepArgs a;
+    int rc = kernel_args_common(k, a, true);
+    if (rc) return rc;
+    const bool flags = k->flags != nullptr;
+    const bool force = k->force[0] != 0 || k->force[1] != 0 || k->force[2] != 0;
+    const AALaunch fn = select_kernels(k->collision, k->stencil, k->dtype, flags ? FM_INLINE : FM_NONE, force, k->equilibrium).collide;
+    if (!fn) return LBM_EUNSUPPORTED;
+    if (k->z_end == k->z_begin) return LBM_OK;
+    const dim3 b = kernel_block(k->shape[0], k->shape[1]);
+    const dim3 grid((unsigned)((k->shape[0] + b.x - 1) / b.x), (unsigned)((k->shape[1] + b.y - 1) / b.y),
+                    (unsigned)(k->z_end - k->z_begin));
+    fn(a, k->dst, 0, grid, b, static_cast<cudaStream_t>(k->stream));
+    return cudaGetLastError() == cudaSuccess ? LBM_OK : LBM_ECUDA;
+}
+
 int lbm_prepare_flags(const uint8_t *host_flags, int64_t nx, int64_t ny, int64_t nplanes, int32_t ghost,
                       uint8_t *device_out, void *stream) {
     if (!host_flags || !device_out || nx < 1 || ny < 1 || nplanes < 1 || ghost < 0 || ghost > 1) return LBM_EINVAL;
@@ -897,9 +972,9 @@ int lbm_create(const lbm_config *cfg, lbm_handle *out) {
     const bool per_row = cfg->collision == LBM_MRT && cfg->n_row_rates == 15;
     const int kcoll = per_row ? (int)OP_MRT_ROWS : cfg->collision;
     const bool force = h->have_force;
-    if (cfg->pattern == LBM_PULL) {
+    if (cfg->pattern == LBM_PULL || cfg->pattern == LBM_PUSH) {
         h->kern = select_kernels(kcoll, h->Q, h->dtype, fm_bulk, force, cfg->equilibrium);
-        if (!h->kern.pull) return fail(nullptr, LBM_EUNSUPPORTED, "no kernel instantiated for this combination");
+        if (!(cfg->pattern == LBM_PUSH ? (void *)h->kern.push : (void *)h->kern.pull)) return fail(nullptr, LBM_EUNSUPPORTED, "no kernel instantiated for this combination");
     } else {
         h->kern = select_kernels(kcoll, h->Q, h->dtype, fm_bulk, force, cfg->equilibrium);
         if (!(cfg->pattern == LBM_ESOTWIST ? (void *)h->kern.eso : (void *)h->kern.aa))
@@ -968,7 +1043,7 @@ int lbm_create(const lbm_config *cfg, lbm_handle *out) {
         s.nz = (int)nzl;
         const Geo g = geo_of(h, s);
         const size_t bytes = (size_t)g.Sq * h->Q * h->esize;
-        for (int a = 0; a < (cfg->pattern == LBM_PULL ? 2 : 1); ++a) {
+        for (int a = 0; a < (two_arrays(h) ? 2 : 1); ++a) {
             if (h->fused) break;  // allocated in NCCL symmetric memory below
             if (cudaMalloc(&s.pdf[a], bytes) != cudaSuccess) {
                 h->err = "cudaMalloc populations (" + std::to_string(bytes) + " B)";
@@ -1083,7 +1158,7 @@ int lbm_create(const lbm_config *cfg, lbm_handle *out) {
         if (h->fused) {
             Slab &s = h->slabs[0];
             const size_t bytes = (size_t)geo_of(h, s).Sq * h->Q * h->esize;
-            for (int a = 0; a < (cfg->pattern == LBM_PULL ? 2 : 1); ++a) {
+            for (int a = 0; a < (two_arrays(h) ? 2 : 1); ++a) {
                 if ((r = ncclMemAlloc(&s.pdf[a], bytes)) != ncclSuccess) {
                     h->err = std::string("ncclMemAlloc populations: ") + ncclGetErrorString(r);
                     return bail(LBM_EOOM);
@@ -1283,7 +1358,7 @@ int lbm_step(lbm_handle h, int64_t n) {
             CUDA_TRY(h, cudaMemsetAsync(h->d_nanflag, 0, sizeof(int), h->stream));
             for (Slab &s : h->slabs) {
                 const Geo g = geo_of(h, s);
-                launch_nan_check(h->dtype, s.pdf[h->cfg.pattern == LBM_PULL ? s.cur : 0], g.Sq * h->Q, h->d_nanflag, h->stream);
+                launch_nan_check(h->dtype, s.pdf[cur_array(h, s)], g.Sq * h->Q, h->d_nanflag, h->stream);
             }
             int flag = 0;
             CUDA_TRY(h, cudaMemcpyAsync(&flag, h->d_nanflag, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
@@ -1332,7 +1407,7 @@ static int read_common(lbm_handle h, ReadArgs &r, int raw, const Slab &s) {
     r.aa_odd = (h->cfg.pattern == LBM_AA) && h->aa_parity;
     r.eso = h->cfg.pattern == LBM_ESOTWIST;
     r.eso_odd = h->aa_parity;
-    r.fsign = h->cfg.pattern == LBM_PULL ? -1.0 : 1.0;
+    r.fsign = h->cfg.pattern == LBM_PULL ? -1.0 : 1.0;  // push / AA / EsoTwist hold pre-collision states
     r.incompressible = h->cfg.equilibrium == LBM_EQ_INCOMPRESSIBLE;
     for (int d = 0; d < 3; ++d) {
         r.F[d] = h->cfg.force[d];
@@ -1359,7 +1434,7 @@ int lbm_get_populations(lbm_handle h, double *out, int32_t where, int32_t raw) {
         read_common(h, r, raw, s);
         r.geo = geo_of(h, s);
         const int64_t sc = (int64_t)h->nx * h->ny * s.nz;
-        const void *f = s.pdf[h->cfg.pattern == LBM_PULL ? s.cur : 0];
+        const void *f = s.pdf[cur_array(h, s)];
         double *tmp = dst;
         if (h->slabs.size() > 1) {  // per-slab block then scatter into [q][cells]
             int rc = ensure_scratch(h, (size_t)cells * h->Q * sizeof(double) * 2);
@@ -1400,7 +1475,7 @@ int lbm_get_populations_at(lbm_handle h, const int64_t *cells, int64_t n, double
         read_common(h, r, 0, s);
         r.geo = geo_of(h, s);
         const int64_t sc = (int64_t)h->nx * h->ny * s.nz;
-        launch_get_at(h->Q, h->dtype, r, s.pdf[h->cfg.pattern == LBM_PULL ? s.cur : 0], didx, n, first, first + sc, dout, h->stream);
+        launch_get_at(h->Q, h->dtype, r, s.pdf[cur_array(h, s)], didx, n, first, first + sc, dout, h->stream);
         first += sc;
     }
     CUDA_TRY(h, cudaMemcpyAsync(out, dout, (size_t)n * h->Q * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
@@ -1463,7 +1538,7 @@ int lbm_get_macroscopic(lbm_handle h, double *rho, double *u, int32_t where) {
         read_common(h, r, 0, s);
         r.geo = geo_of(h, s);
         const int64_t sc = (int64_t)h->nx * h->ny * s.nz;
-        const void *f = s.pdf[h->cfg.pattern == LBM_PULL ? s.cur : 0];
+        const void *f = s.pdf[cur_array(h, s)];
         double *tr = h->slabs.size() > 1 ? h->scratch + 4 * cells : drho;
         double *tu = h->slabs.size() > 1 ? h->scratch + 5 * cells : du;
         launch_macro(h->Q, h->dtype, r, f, tr, tu, dim3((unsigned)((h->nx + 31) / 32), (unsigned)((h->ny + 7) / 8), (unsigned)s.nz),
@@ -1509,7 +1584,7 @@ int lbm_pack_face(lbm_handle h, int64_t z, int32_t dir, double *out, int32_t whe
         if (rc) return rc;
         dst = h->scratch;
     }
-    launch_pack(h->Q, h->dtype, geo_of(h, *sp), sp->pdf[h->cfg.pattern == LBM_PULL ? sp->cur : 0], (int)zz + h->g, dir, dst, true,
+    launch_pack(h->Q, h->dtype, geo_of(h, *sp), sp->pdf[cur_array(h, *sp)], (int)zz + h->g, dir, dst, true,
                 h->stream);
     if (where == LBM_HOST) CUDA_TRY(h, cudaMemcpyAsync(out, dst, n * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
     CUDA_TRY(h, cudaStreamSynchronize(h->stream));

@@ -31,10 +31,10 @@
 
 namespace lbm {
 
-enum SMode { SM_PULL = 0, SM_AA_EVEN = 1, SM_AA_ODD = 2, SM_ESO_EVEN = 3, SM_ESO_ODD = 4 };
+enum SMode { SM_PULL = 0, SM_AA_EVEN = 1, SM_AA_ODD = 2, SM_ESO_EVEN = 3, SM_ESO_ODD = 4, SM_PUSH = 5 };
 // arriving population q of cell x is read from location x - rshift(c_q) (componentwise) ...
 __host__ __device__ constexpr int rshift(int mode, int c) {
-    return mode == SM_AA_EVEN ? 0 : (mode == SM_ESO_EVEN || mode == SM_ESO_ODD) ? (c > 0 ? c : 0) : c;
+    return (mode == SM_AA_EVEN || mode == SM_PUSH) ? 0 : (mode == SM_ESO_EVEN || mode == SM_ESO_ODD) ? (c > 0 ? c : 0) : c;
 }
 // ... in slot src_slot (EsoTwist: P:875-891, kernels.cuh eso_cell)
 template <int Q>
@@ -212,6 +212,10 @@ __global__ void __launch_bounds__(kStagedBT + 32, (StagedMinBlocks<Q, OP, T>::va
             } else if constexpr (MODE == SM_AA_EVEN) {
 #pragma unroll
                 for (int q = 0; q < Q; ++q) dst[S::opp(q) * Sq + self] = g[q];
+            } else if constexpr (MODE == SM_PUSH) {  // collide-stream-push into the second array
+                const Nbr n = neighbours(a.geo, xc, y, tl.zs);
+#pragma unroll
+                for (int q = 0; q < Q; ++q) dst[q * Sq + nb_off(a.geo, n, S::cx(q), S::cy(q), S::cz(q))] = g[q];
             } else if constexpr (MODE == SM_ESO_EVEN || MODE == SM_ESO_ODD) {
                 // departing q at x + c_q^- (slot qbar after the even step, q after the odd one)
                 const Nbr n = neighbours(a.geo, xc, y, tl.zs);

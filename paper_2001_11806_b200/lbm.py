@@ -23,7 +23,7 @@ LBM_OK, LBM_EINVAL, LBM_EUNSUPPORTED, LBM_ECUDA, LBM_ENCCL, LBM_ENAN, LBM_EOOM =
 D3Q19, D3Q27 = 19, 27
 SRT, TRT, MRT, CUMULANT, IDENTITY, SMAGORINSKY, KBC = 0, 1, 2, 3, 4, 5, 6
 F64, F32 = 0, 1
-PULL, AA, ESOTWIST = 0, 1, 2
+PULL, AA, ESOTWIST, PUSH = 0, 1, 2, 3
 FLUID, NOSLIP, UBB = 0, 1, 2
 HOST, DEVICE = 0, 1
 HALO_ZEROCOPY, HALO_PACKED, HALO_FUSED = 0, 1, 2
@@ -37,7 +37,7 @@ KERNEL_PATHS = {"auto": PATH_AUTO, "plain": PATH_PLAIN, "staged": PATH_STAGED}
 COLLISIONS = {"srt": SRT, "trt": TRT, "mrt": MRT, "cumulant": CUMULANT, "identity": IDENTITY,
               "smagorinsky": SMAGORINSKY, "kbc": KBC}
 DTYPES = {"f64": F64, "float64": F64, "fp64": F64, "f32": F32, "float32": F32, "fp32": F32}
-PATTERNS = {"pull": PULL, "aa": AA, "esotwist": ESOTWIST}
+PATTERNS = {"pull": PULL, "aa": AA, "esotwist": ESOTWIST, "push": PUSH}
 
 
 class lbm_config(C.Structure):
@@ -101,6 +101,8 @@ _SIGS = {
     "lbm_halo_schedule_phase": ([_I32, _I32, _I64, _I32, _I32, _P, _I32], C.c_int),
     "lbm_kernel_pull": ([C.POINTER(lbm_kernel_args)], C.c_int),
     "lbm_kernel_aa": ([C.POINTER(lbm_kernel_args), _I32], C.c_int),
+    "lbm_kernel_push": ([C.POINTER(lbm_kernel_args)], C.c_int),
+    "lbm_kernel_collide": ([C.POINTER(lbm_kernel_args)], C.c_int),
     "lbm_prepare_flags": ([_P, _I64, _I64, _I64, _I32, _P, _P], C.c_int),
     "lbm_strerror": ([C.c_int], C.c_char_p),
     "lbm_last_error": ([_P], C.c_char_p),

@@ -90,7 +90,7 @@ def oracle_run(case: Case, steps: Optional[int] = None) -> np.ndarray:
     rho, u = case.fields()
     f0 = d.init_equilibrium(rho, u)
     n = case.steps if steps is None else steps
-    if case.pattern in ("aa", "esotwist"):  # both hold the push state F(n) (G11)
+    if case.pattern in ("aa", "esotwist", "push"):  # all hold the push state F(n) (G11)
         return d.run_push(f0, n)
     return d.run_pull(f0, n)
 

@@ -235,6 +235,14 @@ PARITY = [
     Case("mrt_rows_f32_aa", (32, 16, 8), 19, "mrt", ROW_RATES, "f32", pattern="aa", u_amp=0.03, steps=12),
     Case("mrt_rows_f64_eso_channel", (16, 20, 12), 19, "mrt", ROW_RATES, "f64", pattern="esotwist", geometry="channel",
          steps=11),
+    # collide-stream-push, two arrays
+    Case("push_trt_force_obst_f64", (17, 13, 11), 19, "trt", (1.6, 0.5), "f64", pattern="push", force=(1e-5, 2e-5, 0),
+         geometry="obstacles", ubb=(0.02, -0.01, 0.03), steps=15),
+    Case("push_cumulant_cavity", (14, 14, 14), 27, "cumulant", (1.95,), "f64", pattern="push", geometry="cavity",
+         ubb=(0.05, 0, 0), steps=12),
+    Case("push_mrt_f32_channel32", (32, 20, 12), 19, "mrt", (1.9, 1.3, 1.1, 0.8), "f32", pattern="push",
+         geometry="channel", steps=13),
+    Case("push_kbc27_periodic", (16, 12, 10), 27, "kbc", (1.95,), "f64", pattern="push", u_amp=0.05, steps=9),
     # EsoTwist
     Case("eso_trt_force_f64_odd", (18, 14, 10), 19, "trt", (1.6, 0.5), "f64", pattern="esotwist", force=(1e-5, 2e-5, 0),
          steps=21),
@@ -347,7 +355,7 @@ def test_persistent_multistep_kernel(case):
     assert err <= TOL[case.dtype], err
 
 
-@pytest.mark.parametrize("pattern", ["pull", "aa", "esotwist"])
+@pytest.mark.parametrize("pattern", ["pull", "aa", "esotwist", "push"])
 def test_zero_steps_is_identity_and_counters(pattern):
     """lbm_step(0) launches nothing and leaves the state bit-identical (degenerate call)."""
     case = Case("zero", (16, 8, 6), 19, "trt", (1.6, 0.5), "f64", pattern=pattern, steps=0)
@@ -628,13 +636,13 @@ def test_index_list_per_link_wall_velocities(pattern, steps):
 
 
 @pytest.mark.parametrize("P,halo_mode,nccl_self", [(2, 0, False), (4, 1, False), (1, 0, True), (1, 1, True), (1, 2, True)])
-@pytest.mark.parametrize("pattern", ["pull", "aa"])
+@pytest.mark.parametrize("pattern", ["pull", "aa", "push"])
 def test_index_list_boundaries_slabs_bit_identical(P, halo_mode, nccl_self, pattern):
     """Index-list boundaries with slab decomposition (pull): the link kernel also fills the wall slots of
     ghost planes after the exchange; loopback slabs, NCCL self-exchange and the fused NVLink halo are
     bit-identical to the single slab, and the concatenated link lists are the global list."""
-    if pattern == "aa" and halo_mode == 2:
-        pytest.skip("AA + index-list boundaries use the NCCL or loopback halo")
+    if pattern in ("aa", "push") and halo_mode == 2:
+        pytest.skip("AA / push + index-list boundaries use the NCCL or loopback halo")
     case = Case("lkdec", (16, 12, 16), 19, "trt", (1.6, 0.5), "f64", force=(1e-5, 0, 0), geometry="obstacles",
                 ubb=(0.02, -0.01, 0.03), steps=13, pattern=pattern)
     one = make_sim(case, boundary_mode="links")
@@ -669,3 +677,64 @@ def test_esotwist_slab_decomposition_bit_identical(P, halo_mode, nccl_self, Q, o
     init_sim(many2, case, use_random_kernel=False)
     many2.step(5)
     np.testing.assert_allclose(many2.populations()[mask], oracle_run(case, 5)[mask], rtol=1e-12, atol=0)
+
+
+@pytest.mark.parametrize("P,halo_mode,nccl_self", [(2, 0, False), (4, 1, False), (1, 0, True), (1, 1, True), (1, 2, True)])
+@pytest.mark.parametrize("Q,op,rates,geometry", [(19, "trt", (1.6, 0.5), "obstacles"), (27, "cumulant", (1.95,), "cavity")])
+def test_push_slab_decomposition_bit_identical(P, halo_mode, nccl_self, Q, op, rates, geometry):
+    """Collide-stream-push across slabs: the pushes that land in ghost planes go home after every step
+    (masked by the producing cell with walls), or go straight to the neighbour's plane (fused)."""
+    case = Case("pushdec", (16, 16, 16), Q, op, rates, "f64", pattern="push", geometry=geometry, ubb=(0.02, -0.01, 0.03),
+                steps=11)
+    one = make_sim(case)
+    many = make_sim(case, n_local_slabs=P, halo_mode=halo_mode, nccl_self=nccl_self)
+    for s in (one, many):
+        init_sim(s, case)
+        s.step(case.steps)
+    mask = fluid_mask(case, Q)
+    np.testing.assert_array_equal(one.populations(raw=True)[mask], many.populations(raw=True)[mask])
+
+
+@pytest.mark.parametrize("kind", ["push", "collide"])
+def test_low_level_push_and_collide_kernels(kind):
+    """lbm_kernel_push (walls inline) and lbm_kernel_collide on caller-owned torch memory vs the oracle."""
+    import ctypes as C
+    import torch
+    from paper_2001_11806_b200 import lbm as L
+    case = Case("llp", (19, 14, 9), 19, "trt", (1.6, 0.5), "f64", force=(1e-5, 0, 0), geometry="obstacles",
+                ubb=(0.02, 0.0, -0.01), steps=5)
+    nx, ny, nz = case.shape
+    d = O.Domain(case.method(), nx, ny, nz, flags=case.flags())
+    rho, u = case.fields()
+    f0 = d.init_equilibrium(rho, u)
+    _, w, _ = O.stencil_arrays(19)
+    a = torch.from_numpy(f0 - w[:, None, None, None]).cuda()
+    b = a.clone()
+    fl = torch.empty(nx * ny * nz, dtype=torch.uint8, device="cuda")
+    stream = torch.cuda.Stream()
+    hf = np.ascontiguousarray(case.flags())
+    assert L.lbm_prepare_flags(hf.ctypes.data, nx, ny, nz, 0, fl.data_ptr(), stream.cuda_stream) == 0
+    k = L.lbm_kernel_args()
+    k.stencil, k.collision, k.dtype = 19, L.TRT, L.F64
+    k.flags = fl.data_ptr()
+    k.shape[0], k.shape[1], k.shape[2] = nx, ny, nz
+    k.ghost, k.z_begin, k.z_end = 0, 0, nz
+    k.rates[0], k.rates[1] = case.rates
+    for i in range(3):
+        k.force[i] = case.force[i]
+        k.ubb_velocity[i] = case.ubb[i]
+    k.stream = stream.cuda_stream
+    if kind == "push":
+        for _ in range(case.steps):
+            k.src, k.dst = a.data_ptr(), b.data_ptr()
+            assert L.lbm_kernel_push(C.byref(k)) == 0
+            a, b = b, a
+        ref = d.run_push(f0, case.steps)
+    else:
+        k.dst = a.data_ptr()
+        assert L.lbm_kernel_collide(C.byref(k)) == 0
+        ref = f0.copy()
+        d.collide_all(ref)
+    stream.synchronize()
+    got = a.cpu().numpy() + w[:, None, None, None]
+    assert max_rel_err(got, ref, fluid_mask(case, 19)) <= 1e-12
