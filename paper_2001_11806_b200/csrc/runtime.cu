@@ -391,121 +391,100 @@ int exchange_current(lbm_handle_s *h) {
     return exchange_loopback(h, ph, [](const Slab &s) { return s.cur; }, h->stream);
 }
 
+// the bulk update of planes z_begin + k * z_step (k < nplanes) in the configured pattern
+void launch_update(lbm_handle_s *h, Slab &s, int odd, int z_begin, int nplanes, int z_step, cudaStream_t st, bool peer) {
+    switch (h->cfg.pattern) {
+        case LBM_PUSH: launch_push_range(h, s, z_begin, nplanes, z_step, st, peer); break;
+        case LBM_ESOTWIST: launch_eso_range(h, s, odd, z_begin, nplanes, z_step, st, peer); break;
+        case LBM_AA: launch_aa_range(h, s, odd, z_begin, nplanes, z_step, st, peer); break;
+        default: launch_pull_range(h, s, z_begin, nplanes, z_step, st, peer); break;
+    }
+}
+
+// index-list boundaries: pull fixes the wall slots it is about to stream from (before the step, after
+// the previous exchange); AA (after even: pre-odd, after odd: post-odd) and push fix after the step's
+// exchange. EsoTwist has no link mode.
+void links_before_step(lbm_handle_s *h, Slab &s, cudaStream_t st) {
+    if (h->cfg.pattern == LBM_PULL) launch_links_fix(h, s, s.pdf[s.cur], 0, st);
+}
+void links_after_step(lbm_handle_s *h, Slab &s, int odd, cudaStream_t st) {
+    if (h->cfg.pattern == LBM_AA) launch_links_fix(h, s, s.pdf[0], odd ? 2 : 1, st);
+    else if (h->cfg.pattern == LBM_PUSH) launch_links_fix(h, s, s.pdf[1 - s.cur], 2, st);
+}
+
+void toggle_state(lbm_handle_s *h) {
+    if (two_arrays(h))
+        for (Slab &s : h->slabs) s.cur ^= 1;
+    else
+        h->aa_parity ^= 1;
+}
+
+// the exchange phase that follows a step of the configured pattern (odd = parity of that step)
+Phase step_phase(const lbm_handle_s *h, int odd) {
+    const int nz = h->slabs[0].nz;
+    switch (h->cfg.pattern) {
+        case LBM_PUSH: return phase_aa_return(nz, h->have_flags);  // pushes that landed in ghost planes go home
+        case LBM_ESOTWIST: return phase_eso(nz, odd, h->have_flags);
+        case LBM_AA: return odd ? phase_aa_return(nz, h->have_flags) : phase_aa_fill(nz);
+        default: return phase_pull(nz);
+    }
+}
+
 // ---- one time step ------------------------------------------------------------------
-// Decomposed steps run the boundary planes first, then (NCCL) exchange on the comm stream while
-// the interior planes update on the compute stream; the next step waits for the exchange.
+// Decomposed steps run the boundary planes first, then exchange (NCCL: on the comm stream while the
+// interior planes update on the compute stream; loopback: device copies; fused: the boundary-plane
+// kernels store into the neighbours' planes after an LSA barrier); the next step waits for it.
 int step_once(lbm_handle_s *h) {
     cudaStream_t st = h->stream;
+    const int odd = h->aa_parity;
     if (h->g == 0) {
         Slab &s = h->slabs[0];
-        if (h->cfg.pattern == LBM_PUSH) {
-            launch_push_range(h, s, 0, s.nz, 1, st);
-            launch_links_fix(h, s, s.pdf[1 - s.cur], 2, st);  // pushes toward walls come back (index lists)
-            s.cur ^= 1;
-        } else if (h->cfg.pattern == LBM_ESOTWIST) {
-            launch_eso_range(h, s, h->aa_parity, 0, s.nz, 1, st);
-            h->aa_parity ^= 1;
-        } else if (h->cfg.pattern == LBM_AA) {
-            launch_aa_range(h, s, h->aa_parity, 0, s.nz, 1, st);
-            launch_links_fix(h, s, s.pdf[0], h->aa_parity ? 2 : 1, st);
-            h->aa_parity ^= 1;
-        } else {
-            launch_links_fix(h, s, s.pdf[s.cur], 0, st);
-            launch_pull_range(h, s, 0, s.nz, 1, st);
-            s.cur ^= 1;
-        }
+        links_before_step(h, s, st);
+        launch_update(h, s, odd, 0, s.nz, 1, st, false);
+        links_after_step(h, s, odd, st);
+        toggle_state(h);
         return LBM_OK;
     }
-    const bool eso = h->cfg.pattern == LBM_ESOTWIST;
-    const bool push = h->cfg.pattern == LBM_PUSH;
-    const bool aa = h->cfg.pattern == LBM_AA || eso;  // single array, parity-toggled
-    const int odd = h->aa_parity;
-    auto bnd = [&](Slab &s) {
-        if (push) launch_push_range(h, s, 0, 2, s.nz - 1, st);
-        else if (eso) launch_eso_range(h, s, odd, 0, 2, s.nz - 1, st);
-        else if (aa) launch_aa_range(h, s, odd, 0, 2, s.nz - 1, st);
-        else launch_pull_range(h, s, 0, 2, s.nz - 1, st);
-    };
-    auto inner = [&](Slab &s) {
-        if (push) launch_push_range(h, s, 1, s.nz - 2, 1, st);
-        else if (eso) launch_eso_range(h, s, odd, 1, s.nz - 2, 1, st);
-        else if (aa) launch_aa_range(h, s, odd, 1, s.nz - 2, 1, st);
-        else launch_pull_range(h, s, 1, s.nz - 2, 1, st);
-    };
-    const int nz = h->slabs[0].nz;
-    // push: the pushes that landed in ghost planes go home after every step (the AA return phase)
-    const Phase ph = push ? phase_aa_return(nz, h->have_flags)
-                   : eso ? phase_eso(nz, odd, h->have_flags)
-                         : !aa ? phase_pull(nz) : (odd ? phase_aa_return(nz, h->have_flags) : phase_aa_fill(nz));
-    if (!aa && !push)  // index-list boundaries: wall slots (ghost planes included) before the boundary planes read them
-        for (Slab &s : h->slabs)
-            if (!h->fused) launch_links_fix(h, s, s.pdf[s.cur], 0, st);
+    const bool single = !two_arrays(h);  // the exchanged array: the single one, or the freshly written one
+    const Phase ph = step_phase(h, odd);
+    auto bnd = [&](Slab &s, bool peer) { launch_update(h, s, odd, 0, 2, s.nz - 1, st, peer); };
+    auto inner = [&](Slab &s) { launch_update(h, s, odd, 1, s.nz - 2, 1, st, false); };
     if (!h->use_nccl) {
         // loopback slabs on one GPU, one stream: boundary planes, exchange, interior
-        for (Slab &s : h->slabs) bnd(s);
-        int rc = aa ? exchange_loopback(h, ph, [](const Slab &) { return 0; }, st)
-                    : exchange_loopback(h, ph, [](const Slab &s) { return 1 - s.cur; }, st);
+        for (Slab &s : h->slabs) links_before_step(h, s, st);
+        for (Slab &s : h->slabs) bnd(s, false);
+        int rc = single ? exchange_loopback(h, ph, [](const Slab &) { return 0; }, st)
+                        : exchange_loopback(h, ph, [](const Slab &s) { return 1 - s.cur; }, st);
         if (rc) return rc;
         for (Slab &s : h->slabs) inner(s);
-        if (aa && !eso)  // index-list boundaries (AA): after the exchange, over ghost planes too
-            for (Slab &s : h->slabs) launch_links_fix(h, s, s.pdf[0], odd ? 2 : 1, st);
-        if (push)
-            for (Slab &s : h->slabs) launch_links_fix(h, s, s.pdf[1 - s.cur], 2, st);
-        if (aa) h->aa_parity ^= 1;
-        else for (Slab &s : h->slabs) s.cur ^= 1;
+        for (Slab &s : h->slabs) links_after_step(h, s, odd, st);
+        toggle_state(h);
         return LBM_OK;
     }
     Slab &s = h->slabs[0];
-    if (h->fused && push) {
-        fused_gate(h->fst, st);
-        h->launches++;
-        launch_push_range(h, s, 0, 2, s.nz - 1, st, true);
-        launch_push_range(h, s, 1, s.nz - 2, 1, st);
-        s.cur ^= 1;
-        return LBM_OK;
-    }
-    if (h->fused && eso) {
-        // gate -> boundary planes with peer stores of the link slots the neighbours read next -> interior
-        fused_gate(h->fst, st);
-        h->launches++;
-        launch_eso_range(h, s, odd, 0, 2, s.nz - 1, st, true);
-        launch_eso_range(h, s, odd, 1, s.nz - 2, 1, st);
-        h->aa_parity ^= 1;
-        return LBM_OK;
-    }
-    if (h->fused && aa) {
-        // gate -> boundary planes (even: fill slots into the neighbours' ghost planes; odd: pushes across
-        // the face into the neighbours' interior planes) -> interior planes; no send/recv, no unpack
-        fused_gate(h->fst, st);
-        h->launches++;
-        launch_aa_range(h, s, odd, 0, 2, s.nz - 1, st, true);
-        launch_aa_range(h, s, odd, 1, s.nz - 2, 1, st);
-        h->aa_parity ^= 1;
-        return LBM_OK;
-    }
     if (h->fused) {
-        // gate (LSA barrier: all ranks finished the previous step) -> boundary planes with peer
-        // stores into the neighbours' ghost planes -> interior planes; one stream, no send/recv
+        // gate (LSA barrier: every rank finished the previous step, so the stores into our planes are
+        // done and the slots we overwrite are no longer read) -> boundary planes with peer stores ->
+        // interior planes; one stream, no send/recv (index lists with AA / push are rejected at create)
         fused_gate(h->fst, st);
         h->launches++;
-        launch_links_fix(h, s, s.pdf[s.cur], 0, st);  // after the gate: the peers' stores into our ghosts are done
-        launch_pull_range(h, s, 0, 2, s.nz - 1, st, true);
-        launch_pull_range(h, s, 1, s.nz - 2, 1, st);
-        s.cur ^= 1;
+        links_before_step(h, s, st);
+        bnd(s, true);
+        inner(s);
+        toggle_state(h);
         return LBM_OK;
     }
-    bnd(s);
+    links_before_step(h, s, st);
+    bnd(s, false);
     CUDA_TRY(h, cudaEventRecord(h->ev_bnd, st));
     CUDA_TRY(h, cudaStreamWaitEvent(h->comm_stream, h->ev_bnd, 0));
-    int rc = exchange_nccl(h, ph, aa ? 0 : 1 - s.cur, h->comm_stream);
+    int rc = exchange_nccl(h, ph, single ? 0 : 1 - s.cur, h->comm_stream);
     if (rc) return rc;
     CUDA_TRY(h, cudaEventRecord(h->ev_x, h->comm_stream));
     inner(s);
     CUDA_TRY(h, cudaStreamWaitEvent(st, h->ev_x, 0));  // the next step's boundary planes need the exchange
-    if (aa && !eso) launch_links_fix(h, s, s.pdf[0], odd ? 2 : 1, st);  // index-list boundaries (AA)
-    if (push) launch_links_fix(h, s, s.pdf[1 - s.cur], 2, st);
-    if (aa) h->aa_parity ^= 1;
-    else s.cur ^= 1;
+    links_after_step(h, s, odd, st);
+    toggle_state(h);
     return LBM_OK;
 }
 
