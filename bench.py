@@ -271,6 +271,7 @@ def main():
     ap.add_argument("--e2e-reps", type=int, default=2)
     ap.add_argument("--e2e-steps", type=int, default=0, help="LB steps per e2e job (0 = the config's step count)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-probe", action="store_true", help="skip the copy-q roofline probe")
     ap.add_argument("--halo-mode", type=int, default=-1, help="0 zero-copy NCCL, 1 packed NCCL, 2 fused NVLink peer stores; default: 2 when exchanging, else 0")
     ap.add_argument("--nccl-self", type=int, default=0,
                     help="N=1 only: ghost planes exchanged through a 1-rank NCCL communicator (times the multi-GPU path)")
@@ -448,6 +449,14 @@ def main():
         cpu = oracle_sample(cfg)
 
     if rank == 0:
+        # copy-q probe (paper Table III analogue): the LB gather streams without collision, same local
+        # shape; run after the timed region with the simulation's arrays still resident
+        copyq = None
+        if not args.no_probe:
+            try:
+                copyq = L.probe_copy(cfg["Q"], cfg["dtype"], True, (nx, ny, sim.nz_local), reps=5, device=local)
+            except L.LBMError:
+                copyq = None
         line = {
             "metric": "MLUPS (fluid-cell updates per second, whole job)",
             "value": mlups, "unit": "MLUPS", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -465,6 +474,7 @@ def main():
                          "algorithmic_bytes_per_cell": bpc, "cells_per_launch": nf_local,
                          "kernel_ms_per_step": kernel_ms_per_step, "kernel_launches_timed": klaunch,
                          "frac_of_nominal_8tbs": achieved / 8000.0,
+                         "copy_q_gbs": copyq, "frac_of_copy_q": (achieved / copyq) if copyq else None,
                          "boundary_mode": cfg.get("boundary_mode", "flags") if flags is not None else "none",
                          "kernel_path": L.kernel_path()},
             "cpu_baseline": cpu,

@@ -301,6 +301,14 @@ int lbm_prepare_flags(const uint8_t *host_flags, int64_t nx, int64_t ny, int64_t
 int64_t lbm_boundary_links(lbm_handle h, int64_t *cells, int32_t *dirs, int32_t *types, int64_t cap);
 int lbm_set_link_velocities(lbm_handle h, const double *uw, int64_t n);
 
+/* Roofline probe "copy-q" (the analogue of the paper's copy-19 / update-19 bandwidth probes, Table III,
+ * P:1083-1127): allocates two q x nx x ny x nz arrays of the dtype on `device`, copies every cell's q
+ * populations from one to the other `reps` times (gathered from x - c_q with periodic wrap when
+ * shifted != 0 — the pull access pattern — else aligned) and returns the achieved read + write
+ * bandwidth in GB/s (CUDA events). Frees everything before returning. LBM_EOOM if the arrays do not fit. */
+int lbm_probe_copy(int32_t stencil, int32_t dtype, int32_t shifted, int64_t nx, int64_t ny, int64_t nz, int32_t reps,
+                   int32_t device, double *gbs_out);
+
 /* ---- Kernel path of the bulk update kernels (process-wide; affects launches issued afterwards) ----
  * LBM_PATH_PLAIN : one thread per cell gathers its q populations straight into registers (ld.global.nc).
  * LBM_PATH_STAGED: persistent CTAs; a producer warp moves the source rows of each direction into a

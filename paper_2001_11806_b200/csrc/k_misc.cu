@@ -34,6 +34,15 @@ void launch_set_pops(int Q, int dtype, const ReadArgs &a, void *f, const double 
     LBM_DISPATCH(Q, dtype, (k_set_pops<QQ, T><<<grid, block, 0, s>>>(a, static_cast<T *>(f), in)));
 }
 
+void launch_copyq(int Q, int dtype, bool shifted, const Geo &g, const void *src, void *dst, cudaStream_t s) {
+    const dim3 block(256, 1, 1), grid((unsigned)((g.nx + 255) / 256), (unsigned)g.ny, (unsigned)g.nz);
+    if (shifted) {
+        LBM_DISPATCH(Q, dtype, (k_copyq<QQ, T, true><<<grid, block, 0, s>>>(g, static_cast<const T *>(src), static_cast<T *>(dst))));
+    } else {
+        LBM_DISPATCH(Q, dtype, (k_copyq<QQ, T, false><<<grid, block, 0, s>>>(g, static_cast<const T *>(src), static_cast<T *>(dst))));
+    }
+}
+
 void launch_links(int Q, int dtype, const LinkArgs &a, void *f, cudaStream_t s) {
     if (a.n == 0) return;
     const unsigned blocks = (a.n + 255) / 256;

@@ -949,6 +949,29 @@ __global__ void k_unpack_masked_eso(const Geo geo, T *__restrict__ f, int zs, in
 }
 
 // =======================================================================================
+// Roofline probe "copy-q" (the B200 analogue of the paper's copy-19 / update-19 probes, Table III,
+// P:1083-1127): every cell copies its q populations from src to dst with the LB access pattern but no
+// collision — gathered from x - c_q (periodic) when `shifted`, else from x — so its bandwidth is the
+// ceiling for the update kernels' memory streams.
+// =======================================================================================
+template <int Q, typename T, bool SHIFTED>
+__global__ void __launch_bounds__(256) k_copyq(const Geo g, const T *__restrict__ src, T *__restrict__ dst) {
+    using S = Stencil<Q>;
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    const int y = blockIdx.y * blockDim.y + threadIdx.y;
+    if (x >= g.nx || y >= g.ny) return;
+    const int zs = blockIdx.z;
+    const Nbr n = neighbours(g, x, y, zs);
+    const uint32_t self = nb_off(g, n, 0, 0, 0);
+    T v[Q];
+#pragma unroll
+    for (int q = 0; q < Q; ++q)
+        v[q] = __ldg(src + q * g.Sq + (SHIFTED ? nb_off(g, n, -S::cx(q), -S::cy(q), -S::cz(q)) : self));
+#pragma unroll
+    for (int q = 0; q < Q; ++q) dst[q * g.Sq + self] = v[q];
+}
+
+// =======================================================================================
 // Flag preprocessing and diagnostics
 // =======================================================================================
 // out = in | 0x80 for fluid cells with a non-fluid cell among their 26 neighbours (x, y wrap; z wraps

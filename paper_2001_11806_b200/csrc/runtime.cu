@@ -706,6 +706,50 @@ int lbm_set_link_velocities(lbm_handle h, const double *uw, int64_t n) {
     return LBM_OK;
 }
 
+int lbm_probe_copy(int32_t stencil, int32_t dtype, int32_t shifted, int64_t nx, int64_t ny, int64_t nz, int32_t reps,
+                   int32_t device, double *gbs_out) {
+    if ((stencil != 19 && stencil != 27) || (dtype != LBM_F64 && dtype != LBM_F32) || nx < 1 || ny < 1 || nz < 1 ||
+        reps < 1 || !gbs_out || (double)nx * ny * nz >= 2147483647.0 || nx > 2147483647 / 256)
+        return LBM_EINVAL;
+    if (cudaSetDevice(device) != cudaSuccess) return LBM_ECUDA;
+    Geo g;
+    g.nx = (int)nx;
+    g.ny = (int)ny;
+    g.nz = (int)nz;
+    g.g = 0;
+    g.Sq = nx * ny * nz;
+    const size_t es = dtype == LBM_F64 ? 8 : 4;
+    const size_t bytes = (size_t)g.Sq * stencil * es;
+    void *a = nullptr, *b = nullptr;
+    if (cudaMalloc(&a, bytes) != cudaSuccess) return LBM_EOOM;
+    if (cudaMalloc(&b, bytes) != cudaSuccess) {
+        cudaFree(a);
+        return LBM_EOOM;
+    }
+    cudaStream_t s;
+    cudaEvent_t e0, e1;
+    cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaMemsetAsync(a, 0, bytes, s);
+    cudaMemsetAsync(b, 0, bytes, s);
+    for (int w = 0; w < 2; ++w) launch_copyq(stencil, dtype, shifted != 0, g, w ? b : a, w ? a : b, s);  // warm-up
+    cudaEventRecord(e0, s);
+    for (int r = 0; r < reps; ++r) launch_copyq(stencil, dtype, shifted != 0, g, (r & 1) ? b : a, (r & 1) ? a : b, s);
+    cudaEventRecord(e1, s);
+    const cudaError_t err = cudaEventSynchronize(e1);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaStreamDestroy(s);
+    cudaFree(a);
+    cudaFree(b);
+    if (err != cudaSuccess || ms <= 0.f) return LBM_ECUDA;
+    *gbs_out = 2.0 * (double)bytes * reps / (ms * 1e-3) / 1e9;
+    return LBM_OK;
+}
+
 int lbm_set_kernel_path(int32_t path) {
     if (path < LBM_PATH_AUTO || path > LBM_PATH_STAGED) return LBM_EINVAL;
     lbm::set_staged_path(path);

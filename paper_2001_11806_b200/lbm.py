@@ -108,6 +108,7 @@ _SIGS = {
     "lbm_last_error": ([_P], C.c_char_p),
     "lbm_version": ([], C.c_char_p),
     "lbm_set_kernel_path": ([_I32], C.c_int),
+    "lbm_probe_copy": ([_I32, _I32, _I32, _I64, _I64, _I64, _I32, _I32, _P], C.c_int),
     "lbm_boundary_links": ([_P, _P, _P, _P, _I64], _I64),
     "lbm_set_link_velocities": ([_P, _P, _I64], C.c_int),
     "lbm_get_kernel_path": ([], _I32),
@@ -136,6 +137,15 @@ def _ptr(a) -> int:
         return a.ctypes.data
     assert a.is_contiguous()
     return a.data_ptr()
+
+
+def probe_copy(stencil: int, dtype: str, shifted: bool, shape, reps: int = 10, device: int = 0) -> float:
+    """Copy-q roofline probe (include/lbm.h lbm_probe_copy): GB/s of the LB memory streams without collision."""
+    out = C.c_double()
+    nx, ny, nz = shape
+    _check(lbm_probe_copy(stencil, DTYPES[dtype], int(shifted), nx, ny, nz, reps, device, C.byref(out)),
+           what="lbm_probe_copy")
+    return out.value
 
 
 def set_kernel_path(path) -> None:

@@ -738,3 +738,11 @@ def test_low_level_push_and_collide_kernels(kind):
     stream.synchronize()
     got = a.cpu().numpy() + w[:, None, None, None]
     assert max_rel_err(got, ref, fluid_mask(case, 19)) <= 1e-12
+
+
+def test_copy_q_probe():
+    """The copy-q roofline probe runs and reports a plausible HBM bandwidth (it is a measurement, not a
+    parity check: > 1 TB/s on a B200)."""
+    from paper_2001_11806_b200 import lbm as L
+    gbs = L.probe_copy(19, "f64", True, (256, 128, 64), reps=3)
+    assert 1000.0 < gbs < 20000.0, gbs
