@@ -91,6 +91,26 @@ CONFIGS["eq_mm_c4"] = dict(CONFIGS["c4"], equilibrium="moment_matched",
 CONFIGS["eso_c4"] = dict(CONFIGS["c4"], pattern="esotwist", desc="D3Q19 TRT fp64 512^3 periodic, EsoTwist single array")
 CONFIGS["eso_c3"] = dict(CONFIGS["c3_flags"], pattern="esotwist", desc="D3Q27 cumulant fp64 384^3 cavity, EsoTwist single array")
 CONFIGS["eso_c2"] = dict(CONFIGS["c2"], pattern="esotwist", desc="D3Q19 weighted MRT fp32 512^3 shear wave, EsoTwist")
+# Paper-shaped workloads (SURVEY §8(d) extras; reported, not gated): Fig. 5 / Fig. 7 domain 300x100x100
+# (P:1091), Fig. 8 walled channel (walls on all non-periodic sides) compiled-in vs separate boundary
+# kernels, Fig. 10 small per-GPU blocks of the weighted-MRT AA channel.
+_paper = dict(shape=(300, 100, 100), weak=False, Q=19, force=(0, 0, 0), geometry="periodic",
+              init=("random", 1e-3, 0.01), job_steps=500, dtype="f64")
+CONFIGS["fig5_srt_pull"] = dict(_paper, op="srt", rates=(1.8,), pattern="pull",
+                                desc="D3Q19 SRT fp64 two-array pull 300x100x100 (Fig. 5 analog)")
+CONFIGS["fig7_trt_aa"] = dict(_paper, op="trt", rates=(1.6, 0.5), pattern="aa",
+                              desc="D3Q19 TRT fp64 AA 300x100x100 (Fig. 7 analog)")
+CONFIGS["fig7_trt_aa_q27"] = dict(_paper, Q=27, op="trt", rates=(1.6, 0.5), pattern="aa",
+                                  desc="D3Q27 TRT fp64 AA 300x100x100 (Fig. 7 analog, D3Q27)")
+CONFIGS["fig8_channel_flags"] = dict(_paper, op="trt", rates=(1.6, 0.5), pattern="aa", geometry="box",
+                                     desc="D3Q19 TRT fp64 AA 300x100x100 channel, walls on the y and z faces, "
+                                          "compiled-in flag boundaries (Fig. 8 analog)")
+CONFIGS["fig8_channel_links"] = dict(CONFIGS["fig8_channel_flags"], boundary_mode="links",
+                                     desc="D3Q19 TRT fp64 AA 300x100x100 channel, walls on the y and z faces, "
+                                          "separate index-list boundary kernel (Fig. 8 analog)")
+CONFIGS["fig10_small"] = dict(_paper, shape=(128, 128, 128), weak=True, op="mrt", rates=(1.9, 1.0, 1.0, 1.0),
+                              pattern="aa", desc="D3Q19 weighted MRT fp64 AA 128^3 per GPU, weak scaling "
+                                                 "(Fig. 10 small-block analog; report ms_per_step)")
 # collide-stream-push, two arrays
 CONFIGS["push_c4"] = dict(CONFIGS["c4"], pattern="push", desc="D3Q19 TRT fp64 512^3 periodic, collide-stream-push")
 CONFIGS["push_c3"] = dict(CONFIGS["c3"], pattern="push",
@@ -106,6 +126,11 @@ def flags_for(cfg, shape):
         return LI.channel_flags(nx, ny, nz), (1, 0, 1)
     if cfg["geometry"] == "cavity":
         return LI.cavity_flags(nx), (0, 0, 0)
+    if cfg["geometry"] == "box":  # channel along x, NoSlip on the y and z faces (Fig. 8)
+        fl = np.zeros((nz, ny, nx), np.uint8)
+        fl[:, 0, :] = fl[:, -1, :] = LI.NOSLIP
+        fl[0, :, :] = fl[-1, :, :] = LI.NOSLIP
+        return fl, (1, 0, 0)
     return None, (1, 1, 1)
 
 

@@ -609,6 +609,30 @@ int upload_link_terms(lbm_handle h, Slab &s, const double *uw) {
     return LBM_OK;
 }
 
+// Thread block of the plain update kernels: 256 threads as bx x-cells times 256/bx rows, with bx the
+// largest of 256, 128, 64, 32 that wastes the fewest idle lanes at the row end (nx = 384 -> 128 x 2,
+// nx = 300 -> 64 x 4 instead of 256 + a mostly idle block); the register caps of the kernels assume
+// 256-thread blocks. bx_req > 0 forces the x extent.
+dim3 block_for(int64_t nx, int64_t ny, int bx_req) {
+    int bx = bx_req;
+    if (bx <= 0) {
+        int64_t best = -1;
+        for (int c = 256; c >= 32; c /= 2) {
+            const int64_t waste = (nx + c - 1) / c * c - nx;
+            if (best < 0 || waste < best) {
+                best = waste;
+                bx = c;
+            }
+        }
+    }
+    if (bx > nx) bx = (int)((nx + 31) / 32 * 32);
+    if (bx > 256) bx = 256;
+    int by = 256 / bx;
+    if (by > ny) by = (int)ny;
+    if (by < 1) by = 1;
+    return dim3(bx, by, 1);
+}
+
 int ensure_scratch(lbm_handle h, size_t bytes) {
     if (h->scratch_bytes >= bytes) return LBM_OK;
     if (h->scratch) cudaFree(h->scratch);
@@ -807,13 +831,7 @@ static int kernel_args_common(const lbm_kernel_args *k, StepArgs &a, bool aa) {
     return LBM_OK;
 }
 
-static dim3 kernel_block(int64_t nx, int64_t ny) {
-    int bx = 256;
-    if (bx > nx) bx = (int)((nx + 31) / 32 * 32);
-    int by = 256 / bx;
-    if (by > ny) by = (int)ny;
-    return dim3(bx, by < 1 ? 1 : by, 1);
-}
+static dim3 kernel_block(int64_t nx, int64_t ny) { return block_for(nx, ny, 0); }
 
 int lbm_kernel_pull(const lbm_kernel_args *k) {
     StepArgs a;
@@ -1018,13 +1036,7 @@ int lbm_create(const lbm_config *cfg, lbm_handle *out) {
         b.F[d] = cfg->force[d];
         b.uw[d] = cfg->ubb_velocity[d];
     }
-    int bx = cfg->block_x > 0 ? cfg->block_x : 256;
-    if (bx > h->nx) bx = (int)((h->nx + 31) / 32 * 32);
-    if (bx > 256) bx = 256;
-    int by = 256 / bx;
-    if (by > h->ny) by = (int)h->ny;
-    if (by < 1) by = 1;
-    h->block = dim3(bx, by, 1);
+    h->block = cfg->block_x > 0 ? block_for(h->nx, h->ny, cfg->block_x) : block_for(h->nx, h->ny, 0);
 
     CUDA_TRY(nullptr, cudaSetDevice(cfg->device));
     if (cfg->stream) {
