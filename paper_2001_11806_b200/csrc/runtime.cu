@@ -1134,27 +1134,26 @@ int lbm_create(const lbm_config *cfg, lbm_handle *out) {
             if (h->links) {
                 // one entry per boundary link: wall cell b (any storage plane, ghosts included), direction q
                 // with b + c_q a fluid cell of this slab's interior (x, y wrap; z wraps without ghost planes),
-                // in storage order of b then q. A link is listed by the slab owning its fluid cell.
-                std::vector<uint32_t> lf;
-                for (int zs = 0; zs < nplanes; ++zs)
-                    for (int64_t y = 0; y < h->ny; ++y)
-                        for (int64_t x = 0; x < h->nx; ++x) {
-                            const size_t b = ((size_t)zs * h->ny + y) * h->nx + x;
-                            const uint8_t t = hf[b] & 3;
-                            if (!t) continue;
-                            for (int q = 1; q < h->Q; ++q) {
-                                int64_t zz = zs + kC27[q][2];
-                                if (h->g == 0) zz = (zz + s.nz) % s.nz;
-                                else if (zz < h->g || zz >= h->g + s.nz) continue;  // fluid cell not in this slab
-                                const int64_t xx = (x + kC27[q][0] + h->nx) % h->nx, yy = (y + kC27[q][1] + h->ny) % h->ny;
-                                const size_t nb = ((size_t)zz * h->ny + yy) * h->nx + xx;
-                                if (hf[nb] & 3) continue;
-                                s.h_link_wall.push_back((uint32_t)b);
-                                lf.push_back((uint32_t)nb);
-                                s.h_link_dir.push_back((uint8_t)q);
-                                s.h_link_type.push_back(t);
-                            }
-                        }
+                // grouped by direction q, storage order of b within a direction, so that consecutive threads of
+                // the link kernel touch consecutive cells of one q-plane. A link is listed by the
+                // slab owning its fluid cell.
+                std::vector<uint32_t> lf, walls;
+                for (size_t b = 0; b < (size_t)nplanes * plane; ++b)
+                    if (hf[b] & 3) walls.push_back((uint32_t)b);
+                for (int q = 1; q < h->Q; ++q)
+                    for (const uint32_t b : walls) {
+                        const int64_t zs = b / plane, y = (b % plane) / h->nx, x = b % h->nx;
+                        int64_t zz = zs + kC27[q][2];
+                        if (h->g == 0) zz = (zz + s.nz) % s.nz;
+                        else if (zz < h->g || zz >= h->g + s.nz) continue;  // fluid cell not in this slab
+                        const int64_t xx = (x + kC27[q][0] + h->nx) % h->nx, yy = (y + kC27[q][1] + h->ny) % h->ny;
+                        const size_t nb = ((size_t)zz * h->ny + yy) * h->nx + xx;
+                        if (hf[nb] & 3) continue;
+                        s.h_link_wall.push_back(b);
+                        lf.push_back((uint32_t)nb);
+                        s.h_link_dir.push_back((uint8_t)q);
+                        s.h_link_type.push_back(hf[b] & 3);
+                    }
                 const size_t n = s.h_link_wall.size();
                 if (n) {
                     if (cudaMalloc(&s.link_wall, n * 4) != cudaSuccess || cudaMalloc(&s.link_fluid, n * 4) != cudaSuccess ||

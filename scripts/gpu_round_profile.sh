@@ -7,8 +7,9 @@ O=gpurun_out; mkdir -p $O
 timeout 900 python -m pytest tests -m gpu -x -q > $O/gpu_tests.log 2>&1; echo "tests=$?" >> $O/status.txt
 timeout 900 python bench.py > $O/bench_default.log 2>&1; echo "default=$?" >> $O/status.txt
 timeout 600 python bench.py --impl reference > $O/bench_reference.log 2>&1; echo "reference=$?" >> $O/status.txt
-for c in c0 c1_f64 c1_f32 c2 c3 c1_f64_flags c1_f32_flags c3_flags c3_aa eso_c4 eso_c2 eso_c3 eq_inc_c4 eq_mm_c4 eq_inc_c2 \
-         op_trt op_mrt op_smagorinsky op_kbc op_kbc27 op_cumulant19 op_cumulant27; do
+for c in c0 c1_f64 c1_f32 c2 c3 c1_f64_flags c1_f32_flags c3_flags c3_aa c3_aa_links eso_c4 eso_c2 eso_c3 push_c4 push_c3 \
+         eq_inc_c4 eq_mm_c4 eq_inc_c2 op_trt op_mrt op_smagorinsky op_kbc op_kbc27 op_cumulant19 op_cumulant27 \
+         fig5_srt_pull fig7_trt_aa fig7_trt_aa_q27 fig8_channel_flags fig8_channel_links fig10_small; do
   timeout 300 python bench.py --config $c --steps 50 --warmup 5 --e2e-reps 1 --no-cpu-baseline > $O/bench_$c.log 2>&1
   echo "$c=$?" >> $O/status.txt
 done
@@ -30,4 +31,14 @@ prof c4 k_pull 3 1
 prof c2 k_staged 4 2
 prof c3 "k_pull|k_links" 6 2
 prof op_kbc k_staged 4 2
+prof c1_f64 "k_pull|k_links" 6 2
+prof c1_f32 "k_pull|k_links" 6 2
+cat $O/status.txt
+# halo transports on one GPU through a 1-rank communicator (self exchange), C4 and C2
+for hm in 0 1 2; do
+  for c in c4 c2; do
+    timeout 300 python bench.py --config $c --nccl-self 1 --halo-mode $hm --steps 50 --warmup 5 --e2e-reps 0 --no-cpu-baseline > $O/bench_self_${c}_h$hm.log 2>&1
+    echo "self_${c}_h$hm=$?" >> $O/status.txt
+  done
+done
 cat $O/status.txt
