@@ -14,12 +14,15 @@
  *     moment-matched variants (LBM_EQ_*).
  *   - Storage patterns: two-array stream-pull-collide and collide-stream-push, the
  *     single-array AA and EsoTwist patterns; collision-only kernel.
- *   - Boundaries from a uint8 flag field, compiled into the kernel:
- *     0 = fluid, 1 = no-slip bounce-back, 2 = velocity bounce-back UBB (G8).
- *   - Multi-GPU: z-slab decomposition, one ghost plane per side; the populations crossing each z
- *     face move by NCCL send/recv overlapped with the interior update, or (LBM_HALO_FUSED) are
- *     stored by the boundary-plane kernel straight into the neighbour's ghost plane over NVLink
- *     (P:1056-1071). AA slabs: ghost fill after even steps, return of ghost writes after odd steps.
+ *   - Boundaries from a uint8 flag field: 0 = fluid, 1 = no-slip bounce-back,
+ *     2 = velocity bounce-back UBB (G8), compiled into the update or applied
+ *     by a separate kernel from per-link index lists with per-link wall velocities.
+ *   - Multi-GPU: z-slab decomposition, one ghost plane per side, for every pattern; the exchanged
+ *     populations move by NCCL send/recv overlapped with the interior update, or (LBM_HALO_FUSED)
+ *     are stored by the boundary-plane kernel straight into the neighbour's planes over NVLink
+ *     (P:1056-1071). AA slabs: ghost fill after even steps, return of ghost writes after odd steps;
+ *     push: return after every step; EsoTwist: lower-face fill and return after every step.
+ *   - Bulk kernels: plain register gathers or TMA-staged persistent kernels (lbm_set_kernel_path).
  *
  * Layout (part of the ABI): populations are SoA  f[q][z][y][x], x fastest. Host-visible arrays
  * passed to this API always use the canonical layout of the *local* slab (no ghost planes):
