@@ -108,8 +108,8 @@ extern "C" {
  *        UBB substitution inline (default).
  * LINKS: index-list boundaries: the flag field only seeds one list entry per boundary link (wall cell
  *        b, direction q from b to the fluid cell b + c_q, per-link UBB term); the update kernels are
- *        flag-free and a separate boundary kernel writes, before each pull step (AA: after each step),
- *        the values the fluid cells stream from the wall cells. Per-link wall
+ *        flag-free and a separate boundary kernel writes, before each pull step (AA and push: after
+ *        each step), the values the fluid cells stream from the wall cells. Per-link wall
  *        velocities: lbm_boundary_links / lbm_set_link_velocities. Wall cells are updated like fluid
  *        cells and hold meaningless values. Any slab decomposition (the link kernel also fills the wall
  *        slots of ghost planes, after the exchange); not with the fused halo for AA and push, not
@@ -119,14 +119,16 @@ extern "C" {
 
 #define LBM_HALO_ZEROCOPY 0 /* one NCCL message per crossing population plane */
 #define LBM_HALO_PACKED 1   /* pack kernel + one message per face            */
-#define LBM_HALO_FUSED 2    /* pull + NCCL ranks: the boundary-plane kernel stores crossing
-                               populations straight into the neighbours' ghost planes through
-                               NCCL symmetric-window (LSA) pointers over NVLink; an LSA barrier
-                               kernel orders the steps. Arrays live in ncclMemAlloc memory. */
+#define LBM_HALO_FUSED 2    /* NCCL ranks (or nccl_self): the boundary-plane kernel stores the
+                               exchanged populations straight into the neighbours' planes through
+                               NCCL symmetric-window (LSA) pointers over NVLink (pull: their ghost
+                               planes; AA/push/EsoTwist: the planes the exchange phases of
+                               lbm_halo_schedule_phase target); an LSA barrier kernel orders the
+                               steps. Arrays live in ncclMemAlloc memory. */
 
 typedef struct lbm_config {
     int32_t stencil;   /* LBM_D3Q19 | LBM_D3Q27 */
-    int32_t collision; /* LBM_SRT .. LBM_IDENTITY */
+    int32_t collision; /* LBM_SRT .. LBM_KBC */
     int32_t dtype;     /* LBM_F64 | LBM_F32: storage and arithmetic precision. Populations are
                           stored zero-centred, g_q = f_q - w_q (G12), in both precisions. */
     int32_t pattern;   /* LBM_PULL | LBM_AA | LBM_ESOTWIST | LBM_PUSH */
@@ -146,7 +148,8 @@ typedef struct lbm_config {
     int32_t halo_mode;      /* LBM_HALO_ZEROCOPY | LBM_HALO_PACKED | LBM_HALO_FUSED */
     int32_t use_graph;      /* small single-slab domains (launch-bound): 1 = replay a captured two-step
                                CUDA graph; 2 = one persistent cooperative kernel per lbm_step call with a
-                               grid-wide barrier between steps (walls inline) */
+                               grid-wide barrier between steps (walls inline; pull and AA, compressible
+                               equilibrium, flag boundaries; otherwise plain launches) */
     int32_t block_x;        /* threads per block along x (0 = default) */
     int32_t check_nan_every;/* >0: check for NaN every k steps inside lbm_step (LBM_ENAN) */
     int32_t nccl_self;      /* nranks == 1 only: keep ghost planes and exchange them through a
