@@ -499,6 +499,8 @@ def main():
                          "algorithmic_bytes_per_cell": bpc, "cells_per_launch": nf_local,
                          "kernel_ms_per_step": kernel_ms_per_step, "kernel_launches_timed": klaunch,
                          "frac_of_nominal_8tbs": achieved / 8000.0,
+                         "note": ("L2-resident launch/latency-bound domain: the HBM roofline does not bind "
+                                  "(one persistent kernel per lbm_step call)") if small and world == 1 else None,
                          "copy_q_gbs": copyq, "frac_of_copy_q": (achieved / copyq) if copyq else None,
                          "boundary_mode": cfg.get("boundary_mode", "flags") if flags is not None else "none",
                          "kernel_path": L.kernel_path()},
