@@ -500,7 +500,9 @@ def main():
                          "kernel_ms_per_step": kernel_ms_per_step, "kernel_launches_timed": klaunch,
                          "frac_of_nominal_8tbs": achieved / 8000.0,
                          "note": ("L2-resident launch/latency-bound domain: the HBM roofline does not bind "
-                                  "(one persistent kernel per lbm_step call)") if small and world == 1 else None,
+                                  "(one persistent kernel per lbm_step call)")
+                                 if (cfg["Q"] * np.prod(gshape) / P * (8 if cfg["dtype"] == "f64" else 4)
+                                     * (2 if cfg["pattern"] in ("pull", "push") else 1)) < 100e6 else None,
                          "copy_q_gbs": copyq, "frac_of_copy_q": (achieved / copyq) if copyq else None,
                          "boundary_mode": cfg.get("boundary_mode", "flags") if flags is not None else "none",
                          "kernel_path": L.kernel_path()},
