@@ -25,9 +25,9 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 SRC = os.path.join(HERE, "lbm_oracle.c")
 LIB = os.path.join(HERE, "liblbm_oracle.so")
 
-SRT, TRT, MRT, CUMULANT, IDENTITY, SMAGORINSKY, KBC = 0, 1, 2, 3, 4, 5, 6
+SRT, TRT, MRT, CUMULANT, IDENTITY, SMAGORINSKY, KBC, KBC_EXACT = 0, 1, 2, 3, 4, 5, 6, 7
 OPS = {"srt": SRT, "trt": TRT, "mrt": MRT, "cumulant": CUMULANT, "identity": IDENTITY,
-       "smagorinsky": SMAGORINSKY, "kbc": KBC}
+       "smagorinsky": SMAGORINSKY, "kbc": KBC, "kbc_exact": KBC_EXACT}
 FLUID, NOSLIP, UBB = 0, 1, 2
 
 
@@ -153,7 +153,7 @@ class Method:
             dirs = methods.stencil(name)
             Mr = methods.moment_matrix(polys, dirs)
             Minv = methods.mat_inverse(Mr)
-            if self.op == "kbc":  # row parts: 0 conserved, 1 shear (s), 2 higher order (h)
+            if self.op in ("kbc", "kbc_exact"):  # row parts: 0 conserved, 1 shear (s), 2 higher order (h)
                 S = [0.0 if g == "conserved" else 1.0 if g == "shear" else 2.0 for g in groups]
             elif len(self.rates) == 15:  # one rate per non-conserved row, in the basis order
                 assert groups[:4] == ["conserved"] * 4
@@ -197,7 +197,7 @@ class Domain:
         cfg.ubb_u = (C.c_double * 3)(*method.ubb_u)
         cfg.ubb_rho = method.ubb_rho
         self._keep = []
-        if method.op in ("mrt", "kbc"):
+        if method.op in ("mrt", "kbc", "kbc_exact"):
             M, Minv, S = method.mrt_matrices()
             self._keep = [np.ascontiguousarray(M), np.ascontiguousarray(Minv), np.ascontiguousarray(S)]
             cfg.M, cfg.Minv, cfg.S = (_p(a) for a in self._keep)

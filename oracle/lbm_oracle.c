@@ -37,6 +37,7 @@
 #define ORA_IDENTITY 4
 #define ORA_SMAGORINSKY 5
 #define ORA_KBC 6
+#define ORA_KBC_EXACT 7 /* KBC with the entropy maximised exactly by Newton's method */
 
 #define FLAG_FLUID 0
 #define FLAG_NOSLIP 1
@@ -579,10 +580,69 @@ static void collide_kbc(const ora_cfg *cfg, const ora_stencil_t *s, const double
     for (int q = 0; q < Q; ++q) out[q] = f[q] - ws * ds[q] - wh * dh[q];
 }
 
+/* KBC with exact entropy maximisation ("This condition could be solved numerically in
+ * every cell using Newton's method"; the "more costly but also more general numerical
+ * maximization procedure for the post-collision state entropy, which is based on Newton's method").
+ * f'(w_h) = f - w_s Ds - w_h Dh (Eq. 16); maximise S(w_h) = -sum f' ln(f'/f_eq) (Eq. 17): solve
+ * g(w) = sum_q Dh_q [ln(f'_q(w)/f_eq,q) + 1] = 0 with g'(w) = -sum_q Dh_q^2 / f'_q(w), starting from the
+ * linearised w_h of Eq. (19). Iterates until |dw| <= 1e-14 (at most 50 steps); if a step would make a
+ * population non-positive it is halved. Same parts Ds, Dh as collide_kbc (G17). */
+static void collide_kbc_exact(const ora_cfg *cfg, const ora_stencil_t *s, const double *f, double *out) {
+    int Q = s->Q;
+    double rho, u[3], feq[27], dm[27], ms[27], mh[27], ds[27], dh[27];
+    macroscopic(s, f, cfg->force, +1.0, &rho, u);
+    equilibrium(s, rho, u, feq);
+    for (int k = 0; k < Q; ++k) {
+        dm[k] = 0.0;
+        for (int q = 0; q < Q; ++q) dm[k] += cfg->M[k * Q + q] * (f[q] - feq[q]);
+        ms[k] = (cfg->S[k] == 1.0) ? dm[k] : 0.0;
+        mh[k] = (cfg->S[k] == 2.0) ? dm[k] : 0.0;
+    }
+    for (int q = 0; q < Q; ++q) {
+        ds[q] = 0.0;
+        dh[q] = 0.0;
+        for (int k = 0; k < Q; ++k) {
+            ds[q] += cfg->Minv[q * Q + k] * ms[k];
+            dh[q] += cfg->Minv[q * Q + k] * mh[k];
+        }
+    }
+    double sh = 0.0, hh = 0.0;
+    for (int q = 0; q < Q; ++q) {
+        sh += ds[q] * dh[q] / feq[q];
+        hh += dh[q] * dh[q] / feq[q];
+    }
+    double ws = cfg->rates[0];
+    double w = (hh > 0.0) ? 1.0 + (1.0 - ws) * sh / hh : 1.0;
+    if (hh > 0.0) {
+        for (int it = 0; it < 50; ++it) {
+            double g = 0.0, gp = 0.0;
+            for (int q = 0; q < Q; ++q) {
+                double fp = f[q] - ws * ds[q] - w * dh[q];
+                g += dh[q] * (log(fp / feq[q]) + 1.0);
+                gp -= dh[q] * dh[q] / fp;
+            }
+            double step = g / gp;
+            double wn = w - step;
+            for (int tries = 0; tries < 60; ++tries) { /* keep every population positive */
+                int ok = 1;
+                for (int q = 0; q < Q; ++q)
+                    if (f[q] - ws * ds[q] - wn * dh[q] <= 0.0) ok = 0;
+                if (ok) break;
+                step *= 0.5;
+                wn = w - step;
+            }
+            w = wn;
+            if (fabs(step) <= 1e-14) break;
+        }
+    }
+    for (int q = 0; q < Q; ++q) out[q] = f[q] - ws * ds[q] - w * dh[q];
+}
+
 static void collide(const ora_cfg *cfg, const ora_stencil_t *s, const double *f, double *out) {
     switch (cfg->op) {
         case ORA_SMAGORINSKY: collide_smagorinsky(cfg, s, f, out); break;
         case ORA_KBC: collide_kbc(cfg, s, f, out); break;
+        case ORA_KBC_EXACT: collide_kbc_exact(cfg, s, f, out); break;
         case ORA_SRT: collide_srt(cfg, s, f, out); break;
         case ORA_TRT: collide_trt(cfg, s, f, out); break;
         case ORA_MRT: collide_mrt(cfg, s, f, out); break;

@@ -109,3 +109,65 @@ def test_kbc_entropy_not_below_linearised_neighbours():
     ws_grid = wh + np.linspace(-0.5, 0.5, 2001)
     best = ws_grid[np.argmax([S(w) for w in ws_grid])]
     assert abs(best - wh) < 0.05
+
+
+# ---- KBC with the exact entropy maximum (Newton's method) ----
+
+def _exact_entropy_wh(f, ws, feq, ds, dh):
+    """Maximiser of S(w) = -sum f'(w) ln(f'(w)/f_eq) (Eq. 17) by bounded Brent search
+    (scipy), an iteration that shares nothing with the oracle's Newton loop."""
+    from scipy.optimize import minimize_scalar
+
+    def negS(w):
+        fp = f - ws * ds - w * dh
+        if np.any(fp <= 0):
+            return np.inf
+        return float(np.sum(fp * np.log(fp / feq)))
+    wh = 1 + (1 - ws) * np.sum(ds * dh / feq) / np.sum(dh * dh / feq)
+    r = minimize_scalar(negS, bounds=(wh - 1.5, wh + 1.5), method="bounded",
+                        options={"xatol": 1e-12, "maxiter": 2000})
+    return r.x
+
+
+@pytest.mark.parametrize("Q", [19, 27])
+@pytest.mark.parametrize("ws", [1.99, 1.6])
+def test_kbc_exact_maximises_entropy(ws, Q):
+    m = O.Method(Q=Q, op="kbc_exact", rates=(ws,))
+    c, _, _ = O.stencil_arrays(Q)
+    for amp in (1e-3, 0.05, 0.4):
+        f = _state(Q, amp)
+        feq, ds, dh, wh_lin = _kbc_reference(f, ws, Q)
+        out = O.collide_cell(m, f)
+        # the update is still of the form of Eq. (16) with the same Delta_s
+        w_star = np.dot(f - ws * ds - out, dh) / np.dot(dh, dh)
+        np.testing.assert_allclose(out, f - ws * ds - w_star * dh, rtol=0, atol=1e-15)
+        # optimality condition of P:620-623 holds to rounding
+        g = np.sum(dh * (np.log(out / feq) + 1))
+        assert abs(g) < 1e-13 * max(1.0, np.sum(np.abs(dh))), g
+        # and it is the maximum found by an unrelated search (S is too flat near equilibrium for a
+        # value-based search to locate w better than ~sqrt(eps / S''), so only the larger amplitudes)
+        if amp >= 0.05:
+            assert abs(w_star - _exact_entropy_wh(f, ws, feq, ds, dh)) < 1e-6
+        # near equilibrium the linearisation of P:627-629 is accurate
+        if amp <= 1e-3:
+            assert abs(w_star - wh_lin) < 5e-3
+        assert abs(out.sum() - f.sum()) < 1e-15
+        np.testing.assert_allclose(c.T @ out, c.T @ f, atol=1e-16)
+    # far from equilibrium the exact and linearised rates differ (the variant is not a relabel)
+    f = _state(Q, 0.4)
+    feq, ds, dh, wh_lin = _kbc_reference(f, ws, Q)
+    out = O.collide_cell(m, f)
+    assert abs(np.dot(f - ws * ds - out, dh) / np.dot(dh, dh) - wh_lin) > 1e-4
+
+
+@pytest.mark.parametrize("Q", [19, 27])
+def test_kbc_exact_limits(Q):
+    """w_s = 1: f' = f_eq + (1 - w) Dh, whose entropy is maximal at w = 1 (sum Dh = 0) -> f_eq;
+    equilibrium is a fixed point (Dh = 0)."""
+    f = _state(Q, 0.1)
+    feq, _, _, _ = _kbc_reference(f, 1.0, Q)
+    np.testing.assert_allclose(O.collide_cell(O.Method(Q=Q, op="kbc_exact", rates=(1.0,)), f), feq,
+                               rtol=0, atol=1e-15)
+    e = O.equilibrium_cell(Q, 0.99, np.array([0.01, 0.02, -0.03]))
+    np.testing.assert_allclose(O.collide_cell(O.Method(Q=Q, op="kbc_exact", rates=(1.8,)), e), e,
+                               rtol=0, atol=1e-15)
