@@ -73,7 +73,8 @@ CONFIGS["c3_periodic"] = dict(CONFIGS["c3"], geometry="periodic", init=("random"
 for _name, _op, _q, _rates in [("trt", "trt", 19, (1.6, 0.5)), ("smagorinsky", "smagorinsky", 19, (1.95, 0.17)),
                                ("mrt", "mrt", 19, (1.9, 1.0, 1.0, 1.0)), ("kbc", "kbc", 19, (1.95,)),
                                ("cumulant27", "cumulant", 27, (1.95,)), ("cumulant19", "cumulant", 19, (1.95,)),
-                               ("kbc27", "kbc", 27, (1.95,))]:
+                               ("kbc27", "kbc", 27, (1.95,)), ("kbc_exact", "kbc_exact", 19, (1.95,)),
+                               ("kbc27_exact", "kbc_exact", 27, (1.95,))]:
     CONFIGS[f"op_{_name}"] = dict(desc=f"D3Q{_q} {_op} fp64 AA 512^3 periodic (Fig. 9-style operator comparison)",
                                   shape=(512, 512, 512), weak=False, Q=_q, op=_op, rates=_rates, dtype="f64",
                                   pattern="aa", force=(0, 0, 0), geometry="periodic", init=("random", 1e-3, 0.01),

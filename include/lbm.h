@@ -73,6 +73,11 @@ extern "C" {
                              rates = [omega_0, C_S]                                    */
 #define LBM_KBC 6      /* entropic KBC (Eqs. 15-19), D3Q19 and D3Q27: rates = [omega_s];
                           s = shear moments, h = the other non-conserved moments        */
+#define LBM_KBC_EXACT 7 /* KBC with omega_h maximising the entropy of Eq. (17) exactly, per cell, by
+                           Newton's method started from Eq. (19); rates =
+                           [omega_s]. A step that would make a population <= 0 is halved; stops after a
+                           full step |d omega_h| <= 1e-8 (fp64) / 1e-4 (fp32) (quadratic convergence:
+                           remaining error ~1e-16 / 1e-8) or 30 / 8 steps. ALU-bound.             */
 
 #define LBM_F64 0
 #define LBM_F32 1
@@ -128,7 +133,7 @@ extern "C" {
 
 typedef struct lbm_config {
     int32_t stencil;   /* LBM_D3Q19 | LBM_D3Q27 */
-    int32_t collision; /* LBM_SRT .. LBM_KBC */
+    int32_t collision; /* LBM_SRT .. LBM_KBC_EXACT */
     int32_t dtype;     /* LBM_F64 | LBM_F32: storage and arithmetic precision. Populations are
                           stored zero-centred, g_q = f_q - w_q (G12), in both precisions. */
     int32_t pattern;   /* LBM_PULL | LBM_AA | LBM_ESOTWIST | LBM_PUSH */

@@ -414,7 +414,51 @@ __device__ __forceinline__ void collide_smagorinsky(T (&g)[Q], const Rates<T> &p
 // is Delta_h = d - Delta_s exactly (f = f_eq + Delta_s + Delta_h, Eq. 15), and
 // f' = f - w_s Ds - w_h Dh = f_eq + (1 - w_h) d + (w_h - w_s) Ds. The shear polynomials are even
 // and vanish at c = 0, so Ds is the same for q and qbar and zero at the centre.
+//
+// EXACT: omega_h maximises the entropy S of Eq. (17) itself ("solved numerically in every cell using
+// Newton's method"): Newton on G(w) = sum_q Dh_q ln(f'_q(w) / f_eq,q) = 0
+// (the "+1" term of the optimality condition sums to zero, sum Dh = 0) with
+// G'(w) = -sum_q Dh_q^2 / f'_q(w), started from the linearised omega_h above; with
+// x_q = ((1 - w_s) Ds_q + (1 - w) Dh_q) / f_eq,q, f'_q / f_eq,q = 1 + x_q and ln = log1p(x_q).
+// A step that would make some f'_q <= 0 is halved (as the oracle does). Newton converges
+// quadratically, so after a full step of size s the remaining error is ~K s^2 (K = G''/2G' = O(1)):
+// the loop stops after a full step with |s| <= 1e-8 (fp64) / 1e-4 (fp32), i.e. at an error the oracle's
+// 1e-14 criterion would only confirm with one more evaluation (G-reading G25), or after 30 / 8 steps.
+// 1/f_eq of a pair is recomputed per step (registers, not a stored array).
+// ln(1 + x): near 0 (|x| < 1/16, the usual case f' ~ f_eq) by the atanh series
+// 2 (s + s^3/3 + ... + s^13/13), s = x / (2 + x), |s| < 1/31 so the tail is below 1e-18 relative;
+// elsewhere the library log1p. fp32 uses log1pf throughout.
+__device__ __forceinline__ double ln1p_kbc(double x) {
+    if (fabs(x) < 0.0625) {
+        const double s = x * fast_rcp(2.0 + x), s2 = s * s;
+        double p = 1.0 / 13.0;
+        p = fma(p, s2, 1.0 / 11.0);
+        p = fma(p, s2, 1.0 / 9.0);
+        p = fma(p, s2, 1.0 / 7.0);
+        p = fma(p, s2, 1.0 / 5.0);
+        p = fma(p, s2, 1.0 / 3.0);
+        return 2.0 * fma(s * s2, p, s);
+    }
+    return log1p(x);
+}
+__device__ __forceinline__ float ln1p_kbc(float x) { return log1pf(x); }
+
 template <int Q, typename T>
+__device__ __forceinline__ void kbc_pair_feq(int q, T drho, T rho, T ux, T uy, T uz, T uu15, T &es, T &ea, T &iq, T &ib) {
+    using S = Stencil<Q>;
+    const T w = T(S::w(q));
+    const T cu = T(S::cx(q)) * ux + T(S::cy(q)) * uy + T(S::cz(q)) * uz;
+    const T wr = w * rho;
+    es = w * drho + wr * (T(4.5) * cu * cu - uu15);
+    ea = wr * T(3) * cu;
+    // 1/f_eq of the pair from one reciprocal: 1/(A +- B) = (A -+ B) / (A^2 - B^2)
+    const T A = w + es;
+    const T rr = fast_rcp(A * A - ea * ea);
+    iq = (A - ea) * rr;
+    ib = (A + ea) * rr;
+}
+
+template <int Q, typename T, bool EXACT = false>
 __device__ __forceinline__ void collide_kbc(T (&g)[Q], const Rates<T> &p) {
     using S = Stencil<Q>;
     T drho, jx, jy, jz;
@@ -484,7 +528,69 @@ __device__ __forceinline__ void collide_kbc(T (&g)[Q], const Rates<T> &p) {
         }
     }
     const T ws = p.r[0];
-    const T wh = hh > T(0) ? T(1) + (T(1) - ws) * sh / hh : T(1);
+    T wh = hh > T(0) ? T(1) + (T(1) - ws) * sh / hh : T(1);
+    if constexpr (EXACT) {
+        if (hh > T(0)) {
+            constexpr bool f64 = sizeof(T) == 8;
+            constexpr int kMaxIt = f64 ? 30 : 8;
+            const T tol = f64 ? T(1e-8) : T(1e-4);
+            const T i0 = T(1) / (w0 + eq0);
+            const T kw = T(1) - ws;
+            // x_q(w) and positivity at a trial w; G and G' at w
+            auto positive = [&](T w) {
+                bool ok = T(1) + (T(1) - w) * g[0] * i0 > T(0);
+#pragma unroll
+                for (int q = 1; q < Q; ++q) {
+                    if (q < S::opp(q)) {
+                        const int b = S::opp(q);
+                        T es, ea, iq, ib;
+                        kbc_pair_feq<Q, T>(q, drho, rho, ux, uy, uz, uu15, es, ea, iq, ib);
+                        ok = ok && (T(1) + (kw * ds[q] + (T(1) - w) * (g[q] - ds[q])) * iq > T(0)) &&
+                             (T(1) + (kw * ds[q] + (T(1) - w) * (g[b] - ds[q])) * ib > T(0));
+                    }
+                }
+                return ok;
+            };
+            for (int it = 0; it < kMaxIt; ++it) {
+                const T km = T(1) - wh;
+                T x0 = km * g[0] * i0;
+                T G = g[0] * ln1p_kbc(x0);
+                // G' only sets the convergence rate, not the root: approximate reciprocals suffice
+                T Gp = -g[0] * g[0] * i0 * fast_rcp(T(1) + x0);
+                // min_q f'/f_eq and max_q |Dh/f_eq| bound f' at the next iterate: f'(w - s)/f_eq =
+                // 1 + x + s Dh/f_eq stays positive when min(1 + x) > |s| max|Dh/f_eq|
+                T lo = T(1) + x0, hi = fabs(g[0] * i0);
+#pragma unroll
+                for (int q = 1; q < Q; ++q) {
+                    if (q < S::opp(q)) {
+                        const int b = S::opp(q);
+                        T es, ea, iq, ib;
+                        kbc_pair_feq<Q, T>(q, drho, rho, ux, uy, uz, uu15, es, ea, iq, ib);
+                        const T hq = g[q] - ds[q], hb = g[b] - ds[q];
+                        const T xq = (kw * ds[q] + km * hq) * iq, xb = (kw * ds[q] + km * hb) * ib;
+                        G += hq * ln1p_kbc(xq) + hb * ln1p_kbc(xb);
+                        Gp -= hq * hq * iq * fast_rcp(T(1) + xq) + hb * hb * ib * fast_rcp(T(1) + xb);
+                        lo = fmin(lo, fmin(T(1) + xq, T(1) + xb));
+                        hi = fmax(hi, fmax(fabs(hq * iq), fabs(hb * ib)));
+                    }
+                }
+                T step = G / Gp;
+                if (!(fabs(step) <= T(1e30))) {  // NaN state (a non-positive f' already): keep it NaN
+                    wh = step;
+                    break;
+                }
+                T wn = wh - step;
+                bool full = true;
+                for (int tries = 0; tries < 60 && !(lo > fabs(step) * hi) && !positive(wn); ++tries) {
+                    step *= T(0.5);
+                    wn = wh - step;
+                    full = false;
+                }
+                wh = wn;
+                if (full && fabs(step) <= tol) break;
+            }
+        }
+    }
     // f' = f_eq + (1 - w_h) d + (w_h - w_s) Ds
     const T kd = T(1) - wh, ks = wh - ws;
     g[0] = eq0 + kd * g[0];
@@ -791,7 +897,8 @@ __device__ __forceinline__ void collide_cumulant19(T (&g)[19], const Rates<T> &p
 // Dispatch
 // ---------------------------------------------------------------------------------------
 enum Op { OP_SRT = 0, OP_TRT = 1, OP_MRT = 2, OP_CUMULANT = 3, OP_IDENTITY = 4, OP_SMAGORINSKY = 5, OP_KBC = 6,
-          OP_MRT_ROWS = 7 /* MRT with one rate per moment (internal id; ABI: LBM_MRT + n_row_rates = 15) */ };
+          OP_KBC_EXACT = 7, /* KBC, omega_h by Newton maximisation of Eq. (17) (= LBM_KBC_EXACT) */
+          OP_MRT_ROWS = 8 /* MRT with one rate per moment (internal id; ABI: LBM_MRT + n_row_rates = 15) */ };
 
 template <int Q, int OPX, typename T, bool FORCE>
 __device__ __forceinline__ void collide(T (&g)[Q], const Rates<T> &p) {
@@ -810,6 +917,8 @@ __device__ __forceinline__ void collide(T (&g)[Q], const Rates<T> &p) {
         collide_smagorinsky<Q, T>(g, p);
     } else if constexpr (OP == OP_KBC) {
         collide_kbc<Q, T>(g, p);
+    } else if constexpr (OP == OP_KBC_EXACT) {
+        collide_kbc<Q, T, true>(g, p);
     } else if constexpr (OP == OP_MRT_ROWS) {
         static_assert(Q == 19, "per-moment MRT is implemented for D3Q19");
         collide_mrt19_rows<T>(g, p);

@@ -26,6 +26,10 @@ Kernels inst_kbc19d(int fm, bool force);
 Kernels inst_kbc19f(int fm, bool force);
 Kernels inst_kbc27d(int fm, bool force);
 Kernels inst_kbc27f(int fm, bool force);
+Kernels inst_kbcx19d(int fm, bool force);
+Kernels inst_kbcx19f(int fm, bool force);
+Kernels inst_kbcx27d(int fm, bool force);
+Kernels inst_kbcx27f(int fm, bool force);
 Kernels inst_trt_inc19d(int fm, bool force);
 Kernels inst_trt_inc19f(int fm, bool force);
 Kernels inst_trt_inc27d(int fm, bool force);
@@ -65,6 +69,11 @@ Kernels select_smagorinsky(int Q, int dtype, int fm, bool force) {
 Kernels select_kbc(int Q, int dtype, int fm, bool force) {
     if (Q == 19) return dtype == 0 ? inst_kbc19d(fm, force) : inst_kbc19f(fm, force);
     if (Q == 27) return dtype == 0 ? inst_kbc27d(fm, force) : inst_kbc27f(fm, force);
+    return Kernels{};
+}
+Kernels select_kbc_exact(int Q, int dtype, int fm, bool force) {
+    if (Q == 19) return dtype == 0 ? inst_kbcx19d(fm, force) : inst_kbcx19f(fm, force);
+    if (Q == 27) return dtype == 0 ? inst_kbcx27d(fm, force) : inst_kbcx27f(fm, force);
     return Kernels{};
 }
 Kernels select_trt_eq(int Q, int dtype, int fm, bool force, int eq) {

@@ -27,11 +27,11 @@ template <int Q, int OPX, typename T>
 struct MinBlocks {
     static constexpr int OP = op_base(OPX);  // the equilibrium variant bits do not change the cap
     static constexpr bool f64 = sizeof(T) == 8;
-    // OP: 0 SRT, 1 TRT, 2 MRT, 3 cumulant, 4 identity, 5 Smagorinsky, 6 KBC
+    // OP: 0 SRT, 1 TRT, 2 MRT, 3 cumulant, 4 identity, 5 Smagorinsky, 6 KBC, 7 KBC exact, 8 MRT rows
     static constexpr int pull_default =
-        f64 ? ((OP == 2 || OP == 5 || OP == 6 || (Q == 27 && OP <= 1)) ? 2 : 3)
+        f64 ? (OP == 7 ? 1 : (OP == 2 || OP == 5 || OP == 6 || (Q == 27 && OP <= 1)) ? 2 : 3)
             : ((OP <= 1 || OP == 4 || OP == 5) ? (Q == 19 ? 6 : 4) : 3);
-    static constexpr int aa_default = f64 ? 2 : ((OP == 2 || OP == 6 || (Q == 19 && (OP <= 1 || OP == 5))) ? 3 : 2);
+    static constexpr int aa_default = f64 ? (OP == 7 ? 1 : 2) : ((OP == 2 || OP == 6 || (Q == 19 && (OP <= 1 || OP == 5))) ? 3 : 2);
 #ifdef LBM_MINB_OVERRIDE_PULL
     static constexpr int pull = LBM_MINB_OVERRIDE_PULL;
 #else

@@ -521,12 +521,12 @@ int run_graph_cycle(lbm_handle_s *h) {
 int validate(const lbm_config *c) {
     if (!c) return fail(nullptr, LBM_EINVAL, "null config");
     if (c->stencil != 19 && c->stencil != 27) return fail(nullptr, LBM_EINVAL, "stencil must be 19 or 27");
-    if (c->collision < 0 || c->collision > 6) return fail(nullptr, LBM_EINVAL, "bad collision");
+    if (c->collision < 0 || c->collision > LBM_KBC_EXACT) return fail(nullptr, LBM_EINVAL, "bad collision");
     if (c->dtype != LBM_F64 && c->dtype != LBM_F32) return fail(nullptr, LBM_EINVAL, "bad dtype");
     if (c->pattern < LBM_PULL || c->pattern > LBM_PUSH) return fail(nullptr, LBM_EINVAL, "bad pattern");
     if (c->pattern == LBM_ESOTWIST && c->boundary_mode == LBM_BOUNDARY_LINKS)
         return fail(nullptr, LBM_EUNSUPPORTED, "index-list boundaries are implemented for the pull and AA patterns");
-    const int need[] = {1, 2, 1, 1, 0, 2, 1};
+    const int need[] = {1, 2, 1, 1, 0, 2, 1, 1};
     const int need_n = (c->collision == LBM_MRT && c->n_row_rates == 15) ? 0 : need[c->collision];
     if (c->n_rates < need_n || c->n_rates > 8) return fail(nullptr, LBM_EINVAL, "wrong number of rates");
     for (int i = 0; i < c->n_rates; ++i)
@@ -670,6 +670,7 @@ Kernels select_kernels(int collision, int Q, int dtype, int fm, bool force, int 
         case LBM_CUMULANT: return select_cumulant(Q, dtype, fm, force);
         case LBM_SMAGORINSKY: return select_smagorinsky(Q, dtype, fm, force);
         case LBM_KBC: return select_kbc(Q, dtype, fm, force);
+        case LBM_KBC_EXACT: return select_kbc_exact(Q, dtype, fm, force);
         default: return select_identity(Q, dtype, fm, force);
     }
 }
@@ -798,7 +799,7 @@ const char *lbm_last_error(lbm_handle h) { return h ? h->err.c_str() : g_create_
 
 
 static int kernel_args_common(const lbm_kernel_args *k, StepArgs &a, bool aa) {
-    if (!k || (k->stencil != 19 && k->stencil != 27) || k->collision < 0 || k->collision > 6 ||
+    if (!k || (k->stencil != 19 && k->stencil != 27) || k->collision < 0 || k->collision > LBM_KBC_EXACT ||
         (k->dtype != LBM_F64 && k->dtype != LBM_F32) || !k->dst || (!aa && !k->src) || k->ghost < 0 || k->ghost > 1 ||
         k->equilibrium < LBM_EQ_COMPRESSIBLE || k->equilibrium > LBM_EQ_MOMENT_MATCHED)
         return LBM_EINVAL;

@@ -51,7 +51,7 @@ constexpr int kStagedBT = LBM_STAGED_BT;
 template <int Q, int OPX, typename T>
 struct StagedMinBlocks {
     static constexpr int OP = op_base(OPX);
-    static constexpr bool heavy = sizeof(T) == 8 && (OP == OP_MRT || OP == OP_CUMULANT || OP == OP_KBC || OP == OP_SMAGORINSKY || Q == 27);
+    static constexpr bool heavy = sizeof(T) == 8 && (OP == OP_MRT || OP == OP_CUMULANT || OP == OP_KBC || OP == OP_KBC_EXACT || OP == OP_SMAGORINSKY || Q == 27);
 #ifdef LBM_STAGED_MINB
     static constexpr int value = LBM_STAGED_MINB;
 #else
@@ -241,7 +241,8 @@ int staged_path();     // 0 auto, 1 plain, 2 staged (lbm_set_kernel_path / LBM_K
 
 // Auto policy, from B200 sweeps: the staged kernels win for the register-heavy
 // operators (MRT, KBC, Smagorinsky; the cumulant in the AA pattern), the plain kernels for TRT/SRT
-// (already at copy bandwidth) and the cumulant pull kernel.
+// (already at copy bandwidth) and the cumulant pull kernel. The exact (Newton) KBC is FP64-ALU bound:
+// the plain kernel with the full register file wins (D3Q27 1.65 vs 0.94 GLUPS, staged spills).
 template <int Q, int OPX, int MODE>
 constexpr bool staged_auto() {
     constexpr int OP = op_base(OPX);

@@ -92,6 +92,8 @@ def test_slab_plan(L):
     (dict(boundary_mode="links", nccl_self=True, halo_mode=2, pattern="aa"), -2),  # AA + links: no fused halo
     (dict(stencil=27, collision="cumulant", rates=(1.9,), equilibrium="incompressible"), -2),
     (dict(collision="kbc", rates=(1.9,), equilibrium="moment_matched"), -2),
+    (dict(collision="kbc_exact", rates=(1.9,), force=(1e-5, 0, 0)), -2),   # forcing is SRT/TRT only
+    (dict(collision=8), -1),                                    # unknown collision id
 ])
 def test_create_validation_errors(L, kw, code):
     """Validation happens before any CUDA call, so these run on a CPU-only host."""

@@ -255,6 +255,15 @@ PARITY = [
          geometry="channel", steps=13),
     Case("eso_kbc_obst_f64", (17, 13, 11), 19, "kbc", (1.95,), "f64", pattern="esotwist", geometry="obstacles",
          ubb=(0.02, -0.01, 0.03), u_amp=0.05, steps=14),
+    # KBC with the exact entropy maximum by Newton's method
+    Case("kbcx_q19_f64_cavity", (14, 14, 14), 19, "kbc_exact", (1.99,), "f64", geometry="cavity", ubb=(0.08, 0, 0),
+         u_amp=0.1, steps=20),
+    Case("kbcx_q27_f64_aa_obst", (17, 13, 11), 27, "kbc_exact", (1.95,), "f64", pattern="aa", geometry="obstacles",
+         ubb=(0.02, -0.01, 0.03), u_amp=0.1, steps=12),
+    Case("kbcx_q19_f32", (16, 12, 10), 19, "kbc_exact", (1.9,), "f32", u_amp=0.08, steps=15),
+    Case("kbcx_q27_f32_push_channel", (16, 20, 12), 27, "kbc_exact", (1.97,), "f32", pattern="push", geometry="channel",
+         u_amp=0.08, steps=11),
+    Case("kbcx_q19_f64_eso_odd", (18, 14, 10), 19, "kbc_exact", (1.95,), "f64", pattern="esotwist", u_amp=0.1, steps=9),
 ]
 
 
@@ -288,6 +297,9 @@ STAGED_CASES = [
          ubb=(0.02, -0.01, 0.03), u_amp=0.05, steps=9),
     Case("st_smag_q27_f32", (64, 6, 5), 27, "smagorinsky", (1.9, 0.12), "f32", u_amp=0.05, steps=8),
     Case("st_kbc27_pull_f64", (32, 9, 7), 27, "kbc", (1.95,), "f64", u_amp=0.05, steps=7),
+    Case("st_kbcx27_pull_f64", (32, 9, 7), 27, "kbc_exact", (1.95,), "f64", u_amp=0.1, steps=7),
+    Case("st_kbcx19_aa_f32_walls16", (32, 12, 10), 19, "kbc_exact", (1.95,), "f32", pattern="aa", geometry="channel",
+         u_amp=0.08, steps=9),
     Case("st_eso_mrt_f32_walls16", (32, 14, 10), 19, "mrt", (1.9, 1.3, 1.1, 0.8), "f32", pattern="esotwist",
          geometry="channel", steps=9),
     Case("st_eso_cum27_f64_odd", (16, 9, 7), 27, "cumulant", (1.95,), "f64", pattern="esotwist", u_amp=0.03, steps=7),
@@ -400,7 +412,8 @@ def test_slab_decomposition_bit_identical(P, halo_mode):
     np.testing.assert_array_equal(one.populations(raw=True), many2.populations(raw=True))
 
 
-@pytest.mark.parametrize("Q,op,rates,dtype", [(27, "cumulant", (1.95,), "f64"), (19, "srt", (1.8,), "f32")])
+@pytest.mark.parametrize("Q,op,rates,dtype", [(27, "cumulant", (1.95,), "f64"), (19, "srt", (1.8,), "f32"),
+                                              (27, "kbc_exact", (1.95,), "f64")])
 def test_slab_decomposition_other_ops(Q, op, rates, dtype):
     case = Case("dec2", (12, 10, 12), Q, op, rates, dtype, steps=9)
     one = make_sim(case)
