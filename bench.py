@@ -74,12 +74,16 @@ for _name, _op, _q, _rates in [("trt", "trt", 19, (1.6, 0.5)), ("smagorinsky", "
                                ("mrt", "mrt", 19, (1.9, 1.0, 1.0, 1.0)), ("kbc", "kbc", 19, (1.95,)),
                                ("cumulant27", "cumulant", 27, (1.95,)), ("cumulant19", "cumulant", 19, (1.95,)),
                                ("kbc27", "kbc", 27, (1.95,)), ("kbc_exact", "kbc_exact", 19, (1.95,)),
-                               ("kbc27_exact", "kbc_exact", 27, (1.95,))]:
+                               ("kbc27_exact", "kbc_exact", 27, (1.95,)), ("gen_trt", "gen_trt", 19, (1.6, 0.5)),
+                               ("gen_mrt", "gen_mrt", 19, (1.9, 1.0, 1.0, 1.0)), ("gen_srt27", "gen_srt", 27, (1.8,))]:
     CONFIGS[f"op_{_name}"] = dict(desc=f"D3Q{_q} {_op} fp64 AA 512^3 periodic (Fig. 9-style operator comparison)",
                                   shape=(512, 512, 512), weak=False, Q=_q, op=_op, rates=_rates, dtype="f64",
                                   pattern="aa", force=(0, 0, 0), geometry="periodic", init=("random", 1e-3, 0.01),
                                   job_steps=200)
 
+# Generated operators (codegen/): C4 and C2 with the generated TRT / weighted MRT.
+CONFIGS["c4_gen"] = dict(CONFIGS["c4"], op="gen_trt", desc=CONFIGS["c4"]["desc"] + ", generated TRT operator")
+CONFIGS["c2_gen"] = dict(CONFIGS["c2"], op="gen_mrt", desc=CONFIGS["c2"]["desc"] + ", generated weighted MRT operator")
 
 # Equilibrium variants: C4's D3Q19 TRT fp64 512^3 pull with the incompressible
 # and the moment-matched equilibria; C2's MRT fp32 AA with the incompressible one.
@@ -222,7 +226,7 @@ def oracle_sample(cfg, target_s=15.0, max_steps=None):
     import oracle as O
     nx, ny, nz = cfg["shape"]
     threads = os.cpu_count() or 1
-    m = O.Method(Q=cfg["Q"], op=cfg["op"], rates=cfg["rates"], force=cfg["force"], ubb_u=cfg.get("ubb", (0, 0, 0)),
+    m = O.Method(Q=cfg["Q"], op=cfg["op"].removeprefix("gen_"), rates=cfg["rates"], force=cfg["force"], ubb_u=cfg.get("ubb", (0, 0, 0)),
                  equilibrium=cfg.get("equilibrium", "compressible"),
                  nthreads=threads)
     per_cell = 1.0 / (2.0e6 if cfg["op"] in ("srt", "trt") else 0.6e6 if cfg["op"] == "mrt" else 0.17e6)
@@ -254,7 +258,7 @@ def run_reference(args, cfg):
     import oracle as O
     nx, ny, nz = cfg["shape"]
     threads = os.cpu_count() or 1
-    m = O.Method(Q=cfg["Q"], op=cfg["op"], rates=cfg["rates"], force=cfg["force"], ubb_u=cfg.get("ubb", (0, 0, 0)),
+    m = O.Method(Q=cfg["Q"], op=cfg["op"].removeprefix("gen_"), rates=cfg["rates"], force=cfg["force"], ubb_u=cfg.get("ubb", (0, 0, 0)),
                  equilibrium=cfg.get("equilibrium", "compressible"),
                  nthreads=threads)
     # each reference step = one pull step of a sub-slab with one z plane per host thread (the

@@ -26,6 +26,16 @@ Kernels inst_kbc19d(int fm, bool force);
 Kernels inst_kbc19f(int fm, bool force);
 Kernels inst_kbc27d(int fm, bool force);
 Kernels inst_kbc27f(int fm, bool force);
+Kernels inst_gsrt19d(int fm, bool force);
+Kernels inst_gsrt19f(int fm, bool force);
+Kernels inst_gsrt27d(int fm, bool force);
+Kernels inst_gsrt27f(int fm, bool force);
+Kernels inst_gtrt19d(int fm, bool force);
+Kernels inst_gtrt19f(int fm, bool force);
+Kernels inst_gtrt27d(int fm, bool force);
+Kernels inst_gtrt27f(int fm, bool force);
+Kernels inst_gmrt19d(int fm, bool force);
+Kernels inst_gmrt19f(int fm, bool force);
 Kernels inst_kbcx19d(int fm, bool force);
 Kernels inst_kbcx19f(int fm, bool force);
 Kernels inst_kbcx27d(int fm, bool force);
@@ -69,6 +79,20 @@ Kernels select_smagorinsky(int Q, int dtype, int fm, bool force) {
 Kernels select_kbc(int Q, int dtype, int fm, bool force) {
     if (Q == 19) return dtype == 0 ? inst_kbc19d(fm, force) : inst_kbc19f(fm, force);
     if (Q == 27) return dtype == 0 ? inst_kbc27d(fm, force) : inst_kbc27f(fm, force);
+    return Kernels{};
+}
+Kernels select_generated(int op, int Q, int dtype, int fm, bool force) {
+    force = false;
+    const bool d = dtype == 0;
+    if (op == OP_GEN_SRT) {
+        if (Q == 19) return d ? inst_gsrt19d(fm, force) : inst_gsrt19f(fm, force);
+        if (Q == 27) return d ? inst_gsrt27d(fm, force) : inst_gsrt27f(fm, force);
+    } else if (op == OP_GEN_TRT) {
+        if (Q == 19) return d ? inst_gtrt19d(fm, force) : inst_gtrt19f(fm, force);
+        if (Q == 27) return d ? inst_gtrt27d(fm, force) : inst_gtrt27f(fm, force);
+    } else if (op == OP_GEN_MRT) {
+        if (Q == 19) return d ? inst_gmrt19d(fm, force) : inst_gmrt19f(fm, force);
+    }
     return Kernels{};
 }
 Kernels select_kbc_exact(int Q, int dtype, int fm, bool force) {

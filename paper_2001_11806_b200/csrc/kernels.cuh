@@ -25,7 +25,7 @@ namespace lbm {
 
 template <int Q, int OPX, typename T>
 struct MinBlocks {
-    static constexpr int OP = op_base(OPX);  // the equilibrium variant bits do not change the cap
+    static constexpr int OP = op_class(op_base(OPX));  // the equilibrium variant bits do not change the cap
     static constexpr bool f64 = sizeof(T) == 8;
     // OP: 0 SRT, 1 TRT, 2 MRT, 3 cumulant, 4 identity, 5 Smagorinsky, 6 KBC, 7 KBC exact, 8 MRT rows
     static constexpr int pull_default =

@@ -521,12 +521,12 @@ int run_graph_cycle(lbm_handle_s *h) {
 int validate(const lbm_config *c) {
     if (!c) return fail(nullptr, LBM_EINVAL, "null config");
     if (c->stencil != 19 && c->stencil != 27) return fail(nullptr, LBM_EINVAL, "stencil must be 19 or 27");
-    if (c->collision < 0 || c->collision > LBM_KBC_EXACT) return fail(nullptr, LBM_EINVAL, "bad collision");
+    if (c->collision < 0 || c->collision > LBM_GEN_MRT) return fail(nullptr, LBM_EINVAL, "bad collision");
     if (c->dtype != LBM_F64 && c->dtype != LBM_F32) return fail(nullptr, LBM_EINVAL, "bad dtype");
     if (c->pattern < LBM_PULL || c->pattern > LBM_PUSH) return fail(nullptr, LBM_EINVAL, "bad pattern");
     if (c->pattern == LBM_ESOTWIST && c->boundary_mode == LBM_BOUNDARY_LINKS)
         return fail(nullptr, LBM_EUNSUPPORTED, "index-list boundaries are implemented for the pull and AA patterns");
-    const int need[] = {1, 2, 1, 1, 0, 2, 1, 1};
+    const int need[] = {1, 2, 1, 1, 0, 2, 1, 1, 1, 2, 1};
     const int need_n = (c->collision == LBM_MRT && c->n_row_rates == 15) ? 0 : need[c->collision];
     if (c->n_rates < need_n || c->n_rates > 8) return fail(nullptr, LBM_EINVAL, "wrong number of rates");
     for (int i = 0; i < c->n_rates; ++i)
@@ -549,7 +549,8 @@ int validate(const lbm_config *c) {
     if ((double)c->global[0] * c->global[1] * planes >= 2147483647.0)
         return fail(nullptr, LBM_EINVAL, "slab too large for 32-bit in-plane offsets (split it over more slabs)");
     const bool force = c->force[0] != 0 || c->force[1] != 0 || c->force[2] != 0;
-    if (c->collision == LBM_MRT && c->stencil != 19) return fail(nullptr, LBM_EUNSUPPORTED, "MRT is implemented for D3Q19");
+    if ((c->collision == LBM_MRT || c->collision == LBM_GEN_MRT) && c->stencil != 19)
+        return fail(nullptr, LBM_EUNSUPPORTED, "MRT is implemented for D3Q19");
     if (force && c->collision != LBM_SRT && c->collision != LBM_TRT)
         return fail(nullptr, LBM_EUNSUPPORTED, "forcing is implemented for SRT/TRT");
     if (c->n_row_rates != 0 && c->n_row_rates != 15) return fail(nullptr, LBM_EINVAL, "n_row_rates must be 0 or 15");
@@ -671,6 +672,9 @@ Kernels select_kernels(int collision, int Q, int dtype, int fm, bool force, int 
         case LBM_SMAGORINSKY: return select_smagorinsky(Q, dtype, fm, force);
         case LBM_KBC: return select_kbc(Q, dtype, fm, force);
         case LBM_KBC_EXACT: return select_kbc_exact(Q, dtype, fm, force);
+        case LBM_GEN_SRT:
+        case LBM_GEN_TRT:
+        case LBM_GEN_MRT: return select_generated(collision, Q, dtype, fm, force);
         default: return select_identity(Q, dtype, fm, force);
     }
 }
@@ -799,7 +803,7 @@ const char *lbm_last_error(lbm_handle h) { return h ? h->err.c_str() : g_create_
 
 
 static int kernel_args_common(const lbm_kernel_args *k, StepArgs &a, bool aa) {
-    if (!k || (k->stencil != 19 && k->stencil != 27) || k->collision < 0 || k->collision > LBM_KBC_EXACT ||
+    if (!k || (k->stencil != 19 && k->stencil != 27) || k->collision < 0 || k->collision > LBM_GEN_MRT ||
         (k->dtype != LBM_F64 && k->dtype != LBM_F32) || !k->dst || (!aa && !k->src) || k->ghost < 0 || k->ghost > 1 ||
         k->equilibrium < LBM_EQ_COMPRESSIBLE || k->equilibrium > LBM_EQ_MOMENT_MATCHED)
         return LBM_EINVAL;
@@ -818,7 +822,7 @@ static int kernel_args_common(const lbm_kernel_args *k, StepArgs &a, bool aa) {
     a.z_step = 1;
     for (int i = 0; i < 8; ++i) a.rates[i] = k->rates[i];
     if (k->collision == LBM_SRT) a.rates[1] = a.rates[0];
-    if (k->collision == LBM_MRT)
+    if (k->collision == LBM_MRT || k->collision == LBM_GEN_MRT)
         for (int i = 0; i < 4; ++i)
             if (a.rates[i] == 0.0) a.rates[i] = 1.0;
     if (k->collision == LBM_CUMULANT)
@@ -1029,7 +1033,7 @@ int lbm_create(const lbm_config *cfg, lbm_handle *out) {
     if (per_row)
         for (int i = 0; i < 15; ++i) b.rates[i] = cfg->row_rates[i];
     if (cfg->collision == LBM_SRT) b.rates[1] = b.rates[0];
-    if (cfg->collision == LBM_MRT && !per_row)
+    if ((cfg->collision == LBM_MRT && !per_row) || cfg->collision == LBM_GEN_MRT)
         for (int i = cfg->n_rates; i < 4; ++i) b.rates[i] = 1.0;
     if (cfg->collision == LBM_CUMULANT)
         for (int i = cfg->n_rates; i < 6; ++i) b.rates[i] = 1.0;  // higher orders default to 1 (G7)

@@ -50,7 +50,7 @@ constexpr int kStagedBT = LBM_STAGED_BT;
 // registers: 65536 / (BT * minBlocks); the heavy fp64 operators get more room
 template <int Q, int OPX, typename T>
 struct StagedMinBlocks {
-    static constexpr int OP = op_base(OPX);
+    static constexpr int OP = op_class(op_base(OPX));
     static constexpr bool heavy = sizeof(T) == 8 && (OP == OP_MRT || OP == OP_CUMULANT || OP == OP_KBC || OP == OP_KBC_EXACT || OP == OP_SMAGORINSKY || Q == 27);
 #ifdef LBM_STAGED_MINB
     static constexpr int value = LBM_STAGED_MINB;
@@ -245,7 +245,7 @@ int staged_path();     // 0 auto, 1 plain, 2 staged (lbm_set_kernel_path / LBM_K
 // the plain kernel with the full register file wins (D3Q27 1.65 vs 0.94 GLUPS, staged spills).
 template <int Q, int OPX, int MODE>
 constexpr bool staged_auto() {
-    constexpr int OP = op_base(OPX);
+    constexpr int OP = op_class(op_base(OPX));
     return OP == OP_MRT || OP == OP_MRT_ROWS || OP == OP_KBC || OP == OP_SMAGORINSKY || (OP == OP_CUMULANT && MODE != SM_PULL);
 }
 

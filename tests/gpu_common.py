@@ -59,7 +59,8 @@ class Case:
         return (LI.PROFILE_SHEAR_WAVE, 0.01) if self.init == "shear" else (LI.PROFILE_NONE, 0.0)
 
     def method(self, nthreads=0) -> O.Method:
-        return O.Method(Q=self.Q, op=self.op, rates=self.rates, force=self.force, ubb_u=self.ubb, nthreads=nthreads,
+        # the generated operators (codegen/) compute the same operator as their hand-written kin
+        return O.Method(Q=self.Q, op=self.op.removeprefix("gen_"), rates=self.rates, force=self.force, ubb_u=self.ubb, nthreads=nthreads,
                         equilibrium=self.equilibrium)
 
 

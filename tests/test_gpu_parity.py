@@ -255,6 +255,22 @@ PARITY = [
          geometry="channel", steps=13),
     Case("eso_kbc_obst_f64", (17, 13, 11), 19, "kbc", (1.95,), "f64", pattern="esotwist", geometry="obstacles",
          ubb=(0.02, -0.01, 0.03), u_amp=0.05, steps=14),
+    # generated operators (codegen/)
+    Case("gen_srt_q19_f64_cavity", (14, 14, 14), 19, "gen_srt", (1.9,), "f64", geometry="cavity", ubb=(0.05, 0, 0),
+         steps=20),
+    Case("gen_trt_q19_f32_channel", (16, 20, 12), 19, "gen_trt", (1.6, 0.5), "f32", geometry="channel", u_amp=0.05,
+         steps=20),
+    Case("gen_trt_q19_f64_obst_aa", (17, 13, 11), 19, "gen_trt", (1.7, 1.1), "f64", pattern="aa", geometry="obstacles",
+         ubb=(0.02, -0.01, 0.03), u_amp=0.05, steps=13),
+    Case("gen_mrt_q19_f64_aa", (18, 14, 10), 19, "gen_mrt", (1.9, 1.3, 1.1, 0.8), "f64", pattern="aa", u_amp=0.05,
+         steps=12),
+    Case("gen_mrt_q19_f32_pull_walls", (32, 20, 12), 19, "gen_mrt", (1.9, 1.0, 1.0, 1.0), "f32", geometry="channel",
+         u_amp=0.03, steps=11),
+    Case("gen_srt_q27_f32_aa", (18, 14, 10), 27, "gen_srt", (1.7,), "f32", pattern="aa", u_amp=0.05, steps=12),
+    Case("gen_trt_q27_f64_push_obst", (17, 13, 11), 27, "gen_trt", (1.6, 0.5), "f64", pattern="push",
+         geometry="obstacles", ubb=(0.02, -0.01, 0.03), u_amp=0.05, steps=11),
+    Case("gen_trt_q19_f64_eso", (18, 14, 10), 19, "gen_trt", (1.6, 0.5), "f64", pattern="esotwist", u_amp=0.05,
+         steps=9),
     # KBC with the exact entropy maximum by Newton's method
     Case("kbcx_q19_f64_cavity", (14, 14, 14), 19, "kbc_exact", (1.99,), "f64", geometry="cavity", ubb=(0.08, 0, 0),
          u_amp=0.1, steps=20),
@@ -759,3 +775,22 @@ def test_copy_q_probe():
     from paper_2001_11806_b200 import lbm as L
     gbs = L.probe_copy(19, "f64", True, (256, 128, 64), reps=3)
     assert 1000.0 < gbs < 20000.0, gbs
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("gen,hand,Q,rates,dtype,pattern", [
+    ("gen_trt", "trt", 19, (1.6, 0.5), "f64", "pull"), ("gen_srt", "srt", 27, (1.8,), "f32", "aa"),
+    ("gen_mrt", "mrt", 19, (1.9, 1.0, 1.0, 1.0), "f32", "aa"), ("gen_mrt", "mrt", 19, (1.9, 1.3, 1.1, 0.8), "f64", "pull")])
+def test_generated_equals_hand_written(gen, hand, Q, rates, dtype, pattern):
+    """The generated operator (codegen/) and the hand-written kernel are the same operator: same
+    states after several steps up to FP reassociation."""
+    out = []
+    for op in (gen, hand):
+        case = Case(f"gh_{op}", (32, 12, 10), Q, op, rates, dtype, pattern=pattern, geometry="obstacles",
+                    ubb=(0.02, -0.01, 0.03), u_amp=0.05, steps=10)
+        sim = make_sim(case)
+        init_sim(sim, case)
+        sim.step(case.steps)
+        out.append(sim.populations())
+    tol = 1e-13 if dtype == "f64" else 1e-5
+    np.testing.assert_allclose(out[0], out[1], rtol=0, atol=tol)
