@@ -79,6 +79,8 @@ extern "C" {
 #define LBM_GEN_TRT 9   /* generated TRT, rates = [omega_e, omega_o], D3Q19/D3Q27 (no forcing)    */
 #define LBM_GEN_MRT 10  /* generated weighted MRT, rates = [omega_shear, omega_bulk, omega_3,
                            omega_4] (missing = 1), D3Q19                                        */
+#define LBM_GEN_SMAGORINSKY 11 /* generated Smagorinsky SRT, rates = [omega_0, C_S], D3Q19/D3Q27.
+                           LBM_GEN_SRT / LBM_GEN_TRT also take LBM_EQ_INCOMPRESSIBLE          */
 #define LBM_KBC_EXACT 7 /* KBC with omega_h maximising the entropy of Eq. (17) exactly, per cell, by
                            Newton's method started from Eq. (19); rates =
                            [omega_s]. A step that would make a population <= 0 is halved; stops after a
@@ -139,7 +141,7 @@ extern "C" {
 
 typedef struct lbm_config {
     int32_t stencil;   /* LBM_D3Q19 | LBM_D3Q27 */
-    int32_t collision; /* LBM_SRT .. LBM_GEN_MRT */
+    int32_t collision; /* LBM_SRT .. LBM_GEN_SMAGORINSKY */
     int32_t dtype;     /* LBM_F64 | LBM_F32: storage and arithmetic precision. Populations are
                           stored zero-centred, g_q = f_q - w_q (G12), in both precisions. */
     int32_t pattern;   /* LBM_PULL | LBM_AA | LBM_ESOTWIST | LBM_PUSH */

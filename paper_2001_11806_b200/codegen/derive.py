@@ -52,7 +52,7 @@ class Flops:
 
 def count_flops(e: sp.Expr) -> Flops:
     """Operations to evaluate `e` as written (no re-association)."""
-    if e.is_Atom:
+    if e.is_Atom or e.is_number:  # constants (e.g. sqrt(2)) fold at compile time
         return Flops()
     f = Flops()
     if e.is_Add:
@@ -108,6 +108,12 @@ class Operator:
     main: List[sp.Expr]
     macro: Tuple[sp.Symbol, ...]          # drho, ux, uy, uz
     history: List[Tuple[str, Flops]] = field(default_factory=list)
+    relax: Tuple[sp.Symbol, ...] = ()     # the relaxation-rate symbols the pipeline factors out
+    equilibrium: str = "compressible"
+
+    def __post_init__(self):
+        if not self.relax:
+            self.relax = self.rates
 
     def flops(self) -> Flops:
         return count_assignments(self.subs, self.main)
@@ -118,45 +124,73 @@ class Operator:
 
 
 def n_rates(op: str) -> int:
-    return {"srt": 1, "trt": 2, "mrt": 4}[op]
+    return {"srt": 1, "trt": 2, "mrt": 4, "smagorinsky": 2}[op]
 
 
-def derive(Q: int, op: str) -> Operator:
-    """The moment-space form of SRT / TRT / weighted MRT with the compressible Eq. (3).
+def derive(Q: int, op: str, equilibrium: str = "compressible") -> Operator:
+    """The moment-space form of SRT / TRT / weighted MRT / Smagorinsky-SRT with Eq. (3),
+    compressible (rho0 = rho) or incompressible (rho0 = 1 in Eqs. 2 and 3, DESIGN G19).
 
     Conserved rows: their relaxation rate "can be chosen arbitrarily" because
     m - m_eq vanishes there; SRT gives them omega, TRT omega_e / omega_o by parity (then
-    M^-1 S M is omega I, resp. the parity projectors), MRT 0."""
+    M^-1 S M is omega I, resp. the parity projectors), MRT 0.
+    Smagorinsky (Eqs. 11-14; DESIGN G18): SRT with the local rate
+    omega = 2 / (tau0 + sqrt(tau0^2 + 18 C_S^2 sqrt(2 Pi:Pi) / rho)), Pi = sum c c (g - g_eq);
+    rates = [omega_0, C_S]."""
+    incompressible = equilibrium == "incompressible"
     dirs = methods.stencil(Q)
     w = methods.weights(Q)
     g = sp.symbols(f"g0:{Q}")
     rates = sp.symbols(f"omega0:{n_rates(op)}")
     drho, rho, irho, jx, jy, jz, ux, uy, uz = sp.symbols("drho rho inv_rho j_x j_y j_z u_x u_y u_z")
-    subs: List[Assign] = [(drho, sp.Add(*g)), (rho, drho + 1), (irho, 1 / rho)]
+    subs: List[Assign] = [(drho, sp.Add(*g)), (rho, drho + 1)]
+    if not incompressible:
+        subs.append((irho, 1 / rho))
     for sym, a in ((jx, 0), (jy, 1), (jz, 2)):
         subs.append((sym, sp.Add(*[c[a] * gq for c, gq in zip(dirs, g) if c[a] != 0])))
     for sym, j in ((ux, jx), (uy, jy), (uz, jz)):
-        subs.append((sym, j * irho))  # one division by the density (P:739-741)
+        # one division by the density (P:739-741); none with rho0 = 1
+        subs.append((sym, j if incompressible else j * irho))
+    rho0 = 1 if incompressible else rho
     usq = ux ** 2 + uy ** 2 + uz ** 2
     geq = []
     for c, wq in zip(dirs, w):
         cu = c[0] * ux + c[1] * uy + c[2] * uz
-        geq.append(wq * drho + wq * rho * (3 * cu + sp.Rational(9, 2) * cu ** 2 - sp.Rational(3, 2) * usq))
+        geq.append(wq * drho + wq * rho0 * (3 * cu + sp.Rational(9, 2) * cu ** 2 - sp.Rational(3, 2) * usq))
+    relax = rates
+    kind = op
+    if op == "smagorinsky":
+        om = sp.Symbol("omega_eff")
+        tau0, P = sp.symbols("tau0 Pi_norm")
+        pis = []
+        for a, b in ((0, 0), (1, 1), (2, 2), (0, 1), (0, 2), (1, 2)):
+            s_ab = sp.Symbol(f"Pi_{'xyz'[a]}{'xyz'[b]}")
+            # non-equilibrium moment: population moment minus the (simplified) equilibrium moment
+            m_ab = sp.Add(*[c[a] * c[b] * gq for c, gq in zip(dirs, g) if c[a] * c[b] != 0])
+            meq_ab = sp.factor(sp.expand(sum(c[a] * c[b] * eq for c, eq in zip(dirs, geq))))
+            subs.append((s_ab, m_ab - meq_ab))
+            pis.append((s_ab, a == b))
+        subs.append((P, sp.sqrt(2 * sp.Add(*[(1 if diag else 2) * s_ab ** 2 for s_ab, diag in pis]))))
+        subs.append((tau0, 1 / rates[0]))
+        subs.append((om, 2 / (tau0 + sp.sqrt(tau0 ** 2 + 18 * rates[1] ** 2 * P / rho))))
+        relax = (om,)
+        kind = "srt"
     M = methods.moment_matrix(Q)
     Minv = M.inv()
-    S = methods.relaxation_rates(Q, op, rates)
+    S = methods.relaxation_rates(Q, kind, relax)
     basis = methods.moment_basis(Q)
     for k, (p, grp) in enumerate(basis):
-        if grp == "conserved" and op in ("srt", "trt"):
+        if grp == "conserved" and kind in ("srt", "trt"):
             order = sp.Poly(p, methods.X, methods.Y, methods.Z).total_degree()
-            S[k] = rates[0] if (op == "srt" or order == 0) else rates[1]
+            S[k] = relax[0] if (kind == "srt" or order == 0) else relax[1]
     m = [sp.Add(*[M[k, q] * g[q] for q in range(Q) if M[k, q] != 0]) for k in range(Q)]
     meq = [sp.factor(sp.expand(sum(M[k, q] * geq[q] for q in range(Q)))) for k in range(Q)]
     main = []
     for q in range(Q):
         terms = [Minv[q, k] * S[k] * (m[k] - meq[k]) for k in range(Q) if S[k] != 0 and Minv[q, k] != 0]
         main.append(g[q] - sp.Add(*terms))
-    return Operator(Q, op, g, rates, subs, main, (drho, ux, uy, uz)).record("initial")
+    return Operator(Q, op, g, rates, subs, main, (drho, ux, uy, uz), relax=relax,
+                    equilibrium=equilibrium).record("initial")
 
 
 def subs_linear(e: sp.Expr, pattern: sp.Expr, sym: sp.Symbol) -> sp.Expr:
@@ -200,7 +234,7 @@ def subs_linear(e: sp.Expr, pattern: sp.Expr, sym: sp.Symbol) -> sp.Expr:
 # ---------------------------------------------------------------------------------------------
 def _copy(o: Operator, subs=None, main=None) -> Operator:
     return Operator(o.Q, o.op, o.g, o.rates, list(o.subs if subs is None else subs),
-                    list(o.main if main is None else main), o.macro, list(o.history))
+                    list(o.main if main is None else main), o.macro, list(o.history), o.relax, o.equilibrium)
 
 
 def expand(o: Operator) -> Operator:
@@ -220,20 +254,20 @@ def quadratic_velocity_products(o: Operator) -> Operator:
 
 
 def factor_rates(o: Operator) -> Operator:
-    return _copy(o, main=[sp.collect(e, o.rates) for e in o.main]).record("factor omegas")
+    return _copy(o, main=[sp.collect(e, o.relax) for e in o.main]).record("factor omegas")
 
 
 def common_quadratic_term(o: Operator) -> Operator:
     """Centre expression with g = 0 and all rates 1, as a subexpression."""
     zero = {s: 0 for s in o.g}
-    ones = {r: 1 for r in o.rates}
+    ones = {r: 1 for r in o.relax}
     w0 = methods.weights(o.Q)[0]
     cq = sp.expand(o.main[0].subs(zero).subs(ones) / w0)
     if cq == 0:
         return _copy(o).record("common quadratic term")
     sym = sp.Symbol("c_q")
     new = list(o.subs) + [(sym, cq)]
-    main = [sp.collect(subs_linear(e, cq, sym), o.rates) for e in o.main]
+    main = [sp.collect(subs_linear(e, cq, sym), o.relax) for e in o.main]
     return _copy(o, subs=new, main=main).record("common quadratic term")
 
 
@@ -243,7 +277,7 @@ def substitute_subexpressions(o: Operator) -> Operator:
     for sym, d in o.subs:
         if d.is_Add and len(d.args) > 2:
             main = [subs_linear(e, d, sym) for e in main]
-    main = [sp.collect(e, o.rates) for e in main]
+    main = [sp.collect(e, o.relax) for e in main]
     return _copy(o, main=main).record("substitute existing subexpr.")
 
 
@@ -269,8 +303,8 @@ def direction_split(o: Operator) -> Operator:
         if q > b:
             continue
         s_sym, a_sym = sp.Symbol(f"s_{q}"), sp.Symbol(f"a_{q}")
-        s = sp.collect(sp.expand((main[q] + main[b]) / 2), o.rates)
-        a = sp.collect(sp.expand((main[q] - main[b]) / 2), o.rates)
+        s = sp.collect(sp.expand((main[q] + main[b]) / 2), o.relax)
+        a = sp.collect(sp.expand((main[q] - main[b]) / 2), o.relax)
         subs += [(s_sym, s), (a_sym, a)]
         main[q], main[b] = s_sym + a_sym, s_sym - a_sym
     return _copy(o, subs=subs, main=main).record("direction split")
@@ -312,8 +346,8 @@ def custom(o: Operator, direction: bool = False) -> Operator:
     return cse(o)
 
 
-def strategies(Q: int, op: str) -> Dict[str, Operator]:
-    base = derive(Q, op)
+def strategies(Q: int, op: str, equilibrium: str = "compressible") -> Dict[str, Operator]:
+    base = derive(Q, op, equilibrium)
     return {"only_cse": only_cse(base), "custom_direction_cse": custom(base, True), "custom": custom(base)}
 
 

@@ -900,18 +900,21 @@ __device__ __forceinline__ void collide_cumulant19(T (&g)[19], const Rates<T> &p
 // ---------------------------------------------------------------------------------------
 enum Op { OP_SRT = 0, OP_TRT = 1, OP_MRT = 2, OP_CUMULANT = 3, OP_IDENTITY = 4, OP_SMAGORINSKY = 5, OP_KBC = 6,
           OP_KBC_EXACT = 7, /* KBC, omega_h by Newton maximisation of Eq. (17) (= LBM_KBC_EXACT) */
-          OP_GEN_SRT = 8, OP_GEN_TRT = 9, OP_GEN_MRT = 10, /* generated operators (codegen/, = LBM_GEN_*) */
+          OP_GEN_SRT = 8, OP_GEN_TRT = 9, OP_GEN_MRT = 10, OP_GEN_SMAGORINSKY = 11, /* generated (codegen/, = LBM_GEN_*) */
           OP_MRT_ROWS = 15 /* MRT with one rate per moment (internal id; ABI: LBM_MRT + n_row_rates = 15) */ };
 
 // Operator class for occupancy / kernel-path tuning: the generated operators behave like their
 // hand-written counterparts (TRT-like, MRT-like).
-constexpr int op_class(int op) { return (op == OP_GEN_SRT || op == OP_GEN_TRT) ? OP_TRT : op == OP_GEN_MRT ? OP_MRT : op; }
+constexpr int op_class(int op) {
+    return (op == OP_GEN_SRT || op == OP_GEN_TRT) ? OP_TRT : op == OP_GEN_MRT ? OP_MRT : op == OP_GEN_SMAGORINSKY ? OP_SMAGORINSKY : op;
+}
 
 template <int Q, int OPX, typename T, bool FORCE>
 __device__ __forceinline__ void collide(T (&g)[Q], const Rates<T> &p) {
     constexpr int OP = op_base(OPX), EQ = op_eq(OPX);
-    static_assert(EQ == EQ_COMPRESSIBLE || OP == OP_SRT || OP == OP_TRT || OP == OP_MRT,
-                  "equilibrium variants exist for SRT/TRT/MRT");
+    static_assert(EQ == EQ_COMPRESSIBLE || OP == OP_SRT || OP == OP_TRT || OP == OP_MRT ||
+                      ((OP == OP_GEN_SRT || OP == OP_GEN_TRT) && EQ == EQ_INCOMPRESSIBLE),
+                  "equilibrium variants exist for SRT/TRT/MRT (generated: incompressible SRT/TRT)");
     if constexpr (OP == OP_SRT || OP == OP_TRT) {
         collide_trt<Q, T, FORCE, EQ>(g, p);
     } else if constexpr (OP == OP_MRT) {
@@ -929,12 +932,21 @@ __device__ __forceinline__ void collide(T (&g)[Q], const Rates<T> &p) {
     } else if constexpr (OP == OP_MRT_ROWS) {
         static_assert(Q == 19, "per-moment MRT is implemented for D3Q19");
         collide_mrt19_rows<T>(g, p);
+    } else if constexpr (OP == OP_GEN_SRT && EQ == EQ_INCOMPRESSIBLE) {
+        if constexpr (Q == 19) gen_srt19_inc<T>(g, p);
+        else gen_srt27_inc<T>(g, p);
+    } else if constexpr (OP == OP_GEN_TRT && EQ == EQ_INCOMPRESSIBLE) {
+        if constexpr (Q == 19) gen_trt19_inc<T>(g, p);
+        else gen_trt27_inc<T>(g, p);
     } else if constexpr (OP == OP_GEN_SRT) {
         if constexpr (Q == 19) gen_srt19<T>(g, p);
         else gen_srt27<T>(g, p);
     } else if constexpr (OP == OP_GEN_TRT) {
         if constexpr (Q == 19) gen_trt19<T>(g, p);
         else gen_trt27<T>(g, p);
+    } else if constexpr (OP == OP_GEN_SMAGORINSKY) {
+        if constexpr (Q == 19) gen_smagorinsky19<T>(g, p);
+        else gen_smagorinsky27<T>(g, p);
     } else if constexpr (OP == OP_GEN_MRT) {
         static_assert(Q == 19, "the generated MRT is D3Q19");
         gen_mrt19<T>(g, p);

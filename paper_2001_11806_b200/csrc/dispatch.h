@@ -39,7 +39,7 @@ Kernels select_identity(int Q, int dtype, int fm, bool force);
 Kernels select_smagorinsky(int Q, int dtype, int fm, bool force);
 Kernels select_kbc(int Q, int dtype, int fm, bool force);
 Kernels select_kbc_exact(int Q, int dtype, int fm, bool force);
-Kernels select_generated(int op, int Q, int dtype, int fm, bool force);
+Kernels select_generated(int op, int Q, int dtype, int fm, bool force, int eq);
 // equilibrium variants (EQ_INCOMPRESSIBLE / EQ_MOMENT_MATCHED of collide.cuh); all in k_select.cu
 Kernels select_trt_eq(int Q, int dtype, int fm, bool force, int eq);
 Kernels select_mrt_eq(int Q, int dtype, int fm, bool force, int eq);

@@ -36,6 +36,18 @@ Kernels inst_gtrt27d(int fm, bool force);
 Kernels inst_gtrt27f(int fm, bool force);
 Kernels inst_gmrt19d(int fm, bool force);
 Kernels inst_gmrt19f(int fm, bool force);
+Kernels inst_gsmag19d(int fm, bool force);
+Kernels inst_gsmag19f(int fm, bool force);
+Kernels inst_gsmag27d(int fm, bool force);
+Kernels inst_gsmag27f(int fm, bool force);
+Kernels inst_gsrt_inc19d(int fm, bool force);
+Kernels inst_gsrt_inc19f(int fm, bool force);
+Kernels inst_gsrt_inc27d(int fm, bool force);
+Kernels inst_gsrt_inc27f(int fm, bool force);
+Kernels inst_gtrt_inc19d(int fm, bool force);
+Kernels inst_gtrt_inc19f(int fm, bool force);
+Kernels inst_gtrt_inc27d(int fm, bool force);
+Kernels inst_gtrt_inc27f(int fm, bool force);
 Kernels inst_kbcx19d(int fm, bool force);
 Kernels inst_kbcx19f(int fm, bool force);
 Kernels inst_kbcx27d(int fm, bool force);
@@ -81,10 +93,24 @@ Kernels select_kbc(int Q, int dtype, int fm, bool force) {
     if (Q == 27) return dtype == 0 ? inst_kbc27d(fm, force) : inst_kbc27f(fm, force);
     return Kernels{};
 }
-Kernels select_generated(int op, int Q, int dtype, int fm, bool force) {
+Kernels select_generated(int op, int Q, int dtype, int fm, bool force, int eq) {
     force = false;
     const bool d = dtype == 0;
-    if (op == OP_GEN_SRT) {
+    if (eq == EQ_INCOMPRESSIBLE) {
+        if (op == OP_GEN_SRT) {
+            if (Q == 19) return d ? inst_gsrt_inc19d(fm, force) : inst_gsrt_inc19f(fm, force);
+            if (Q == 27) return d ? inst_gsrt_inc27d(fm, force) : inst_gsrt_inc27f(fm, force);
+        } else if (op == OP_GEN_TRT) {
+            if (Q == 19) return d ? inst_gtrt_inc19d(fm, force) : inst_gtrt_inc19f(fm, force);
+            if (Q == 27) return d ? inst_gtrt_inc27d(fm, force) : inst_gtrt_inc27f(fm, force);
+        }
+        return Kernels{};
+    }
+    if (eq != EQ_COMPRESSIBLE) return Kernels{};
+    if (op == OP_GEN_SMAGORINSKY) {
+        if (Q == 19) return d ? inst_gsmag19d(fm, force) : inst_gsmag19f(fm, force);
+        if (Q == 27) return d ? inst_gsmag27d(fm, force) : inst_gsmag27f(fm, force);
+    } else if (op == OP_GEN_SRT) {
         if (Q == 19) return d ? inst_gsrt19d(fm, force) : inst_gsrt19f(fm, force);
         if (Q == 27) return d ? inst_gsrt27d(fm, force) : inst_gsrt27f(fm, force);
     } else if (op == OP_GEN_TRT) {

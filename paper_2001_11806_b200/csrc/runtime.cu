@@ -521,12 +521,12 @@ int run_graph_cycle(lbm_handle_s *h) {
 int validate(const lbm_config *c) {
     if (!c) return fail(nullptr, LBM_EINVAL, "null config");
     if (c->stencil != 19 && c->stencil != 27) return fail(nullptr, LBM_EINVAL, "stencil must be 19 or 27");
-    if (c->collision < 0 || c->collision > LBM_GEN_MRT) return fail(nullptr, LBM_EINVAL, "bad collision");
+    if (c->collision < 0 || c->collision > LBM_GEN_SMAGORINSKY) return fail(nullptr, LBM_EINVAL, "bad collision");
     if (c->dtype != LBM_F64 && c->dtype != LBM_F32) return fail(nullptr, LBM_EINVAL, "bad dtype");
     if (c->pattern < LBM_PULL || c->pattern > LBM_PUSH) return fail(nullptr, LBM_EINVAL, "bad pattern");
     if (c->pattern == LBM_ESOTWIST && c->boundary_mode == LBM_BOUNDARY_LINKS)
         return fail(nullptr, LBM_EUNSUPPORTED, "index-list boundaries are implemented for the pull and AA patterns");
-    const int need[] = {1, 2, 1, 1, 0, 2, 1, 1, 1, 2, 1};
+    const int need[] = {1, 2, 1, 1, 0, 2, 1, 1, 1, 2, 1, 2};
     const int need_n = (c->collision == LBM_MRT && c->n_row_rates == 15) ? 0 : need[c->collision];
     if (c->n_rates < need_n || c->n_rates > 8) return fail(nullptr, LBM_EINVAL, "wrong number of rates");
     for (int i = 0; i < c->n_rates; ++i)
@@ -570,8 +570,9 @@ int validate(const lbm_config *c) {
     if (c->equilibrium < LBM_EQ_COMPRESSIBLE || c->equilibrium > LBM_EQ_MOMENT_MATCHED)
         return fail(nullptr, LBM_EINVAL, "bad equilibrium");
     if (c->equilibrium != LBM_EQ_COMPRESSIBLE && c->collision != LBM_SRT && c->collision != LBM_TRT &&
-        c->collision != LBM_MRT && c->collision != LBM_IDENTITY)
-        return fail(nullptr, LBM_EUNSUPPORTED, "equilibrium variants are implemented for SRT/TRT/MRT");
+        c->collision != LBM_MRT && c->collision != LBM_IDENTITY &&
+        !((c->collision == LBM_GEN_SRT || c->collision == LBM_GEN_TRT) && c->equilibrium == LBM_EQ_INCOMPRESSIBLE))
+        return fail(nullptr, LBM_EUNSUPPORTED, "equilibrium variants are implemented for SRT/TRT/MRT (generated: incompressible SRT/TRT)");
     // a non-periodic axis must carry wall cells on both faces
     for (int d = 0; d < 3; ++d) {
         if (c->periodic[d]) continue;
@@ -661,6 +662,7 @@ Kernels select_kernels(int collision, int Q, int dtype, int fm, bool force, int 
     if (eq != EQ_COMPRESSIBLE) {
         if (collision == LBM_SRT || collision == LBM_TRT) return select_trt_eq(Q, dtype, fm, force, eq);
         if (collision == LBM_MRT) return select_mrt_eq(Q, dtype, fm, force, eq);
+        if (collision == LBM_GEN_SRT || collision == LBM_GEN_TRT) return select_generated(collision, Q, dtype, fm, force, eq);
         if (collision != LBM_IDENTITY) return Kernels{};
     }
     switch (collision) {
@@ -674,7 +676,8 @@ Kernels select_kernels(int collision, int Q, int dtype, int fm, bool force, int 
         case LBM_KBC_EXACT: return select_kbc_exact(Q, dtype, fm, force);
         case LBM_GEN_SRT:
         case LBM_GEN_TRT:
-        case LBM_GEN_MRT: return select_generated(collision, Q, dtype, fm, force);
+        case LBM_GEN_MRT:
+        case LBM_GEN_SMAGORINSKY: return select_generated(collision, Q, dtype, fm, force, eq);
         default: return select_identity(Q, dtype, fm, force);
     }
 }
@@ -803,7 +806,7 @@ const char *lbm_last_error(lbm_handle h) { return h ? h->err.c_str() : g_create_
 
 
 static int kernel_args_common(const lbm_kernel_args *k, StepArgs &a, bool aa) {
-    if (!k || (k->stencil != 19 && k->stencil != 27) || k->collision < 0 || k->collision > LBM_GEN_MRT ||
+    if (!k || (k->stencil != 19 && k->stencil != 27) || k->collision < 0 || k->collision > LBM_GEN_SMAGORINSKY ||
         (k->dtype != LBM_F64 && k->dtype != LBM_F32) || !k->dst || (!aa && !k->src) || k->ghost < 0 || k->ghost > 1 ||
         k->equilibrium < LBM_EQ_COMPRESSIBLE || k->equilibrium > LBM_EQ_MOMENT_MATCHED)
         return LBM_EINVAL;

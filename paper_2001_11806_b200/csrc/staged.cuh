@@ -246,7 +246,11 @@ int staged_path();     // 0 auto, 1 plain, 2 staged (lbm_set_kernel_path / LBM_K
 template <int Q, int OPX, int MODE>
 constexpr bool staged_auto() {
     constexpr int OP = op_class(op_base(OPX));
-    return OP == OP_MRT || OP == OP_MRT_ROWS || OP == OP_KBC || OP == OP_SMAGORINSKY || (OP == OP_CUMULANT && MODE != SM_PULL);
+    // generated D3Q27 SRT/TRT: the CSE'd code needs more registers than the plain kernels' cap
+    // (AA 512^3 fp64: plain 0.86, staged 0.92 of copy BW; hand-written TRT plain 0.97)
+    constexpr bool gen27 = Q == 27 && (op_base(OPX) == OP_GEN_SRT || op_base(OPX) == OP_GEN_TRT);
+    return OP == OP_MRT || OP == OP_MRT_ROWS || OP == OP_KBC || OP == OP_SMAGORINSKY || (OP == OP_CUMULANT && MODE != SM_PULL) ||
+           gen27;
 }
 
 template <int Q, int OP, typename T, int FM, bool FORCE, int MODE>

@@ -21,7 +21,7 @@ LIBPATH = os.environ.get("LBM_B200_LIB") or os.path.join(HERE, "liblbm_b200.so")
 
 LBM_OK, LBM_EINVAL, LBM_EUNSUPPORTED, LBM_ECUDA, LBM_ENCCL, LBM_ENAN, LBM_EOOM = 0, -1, -2, -3, -4, -5, -6
 D3Q19, D3Q27 = 19, 27
-SRT, TRT, MRT, CUMULANT, IDENTITY, SMAGORINSKY, KBC, KBC_EXACT, GEN_SRT, GEN_TRT, GEN_MRT = range(11)
+SRT, TRT, MRT, CUMULANT, IDENTITY, SMAGORINSKY, KBC, KBC_EXACT, GEN_SRT, GEN_TRT, GEN_MRT, GEN_SMAGORINSKY = range(12)
 F64, F32 = 0, 1
 PULL, AA, ESOTWIST, PUSH = 0, 1, 2, 3
 FLUID, NOSLIP, UBB = 0, 1, 2
@@ -36,7 +36,7 @@ KERNEL_PATHS = {"auto": PATH_AUTO, "plain": PATH_PLAIN, "staged": PATH_STAGED}
 
 COLLISIONS = {"srt": SRT, "trt": TRT, "mrt": MRT, "cumulant": CUMULANT, "identity": IDENTITY,
               "smagorinsky": SMAGORINSKY, "kbc": KBC, "kbc_exact": KBC_EXACT,
-              "gen_srt": GEN_SRT, "gen_trt": GEN_TRT, "gen_mrt": GEN_MRT}
+              "gen_srt": GEN_SRT, "gen_trt": GEN_TRT, "gen_mrt": GEN_MRT, "gen_smagorinsky": GEN_SMAGORINSKY}
 DTYPES = {"f64": F64, "float64": F64, "fp64": F64, "f32": F32, "float32": F32, "fp32": F32}
 PATTERNS = {"pull": PULL, "aa": AA, "esotwist": ESOTWIST, "push": PUSH}
 

@@ -93,7 +93,9 @@ def test_slab_plan(L):
     (dict(stencil=27, collision="cumulant", rates=(1.9,), equilibrium="incompressible"), -2),
     (dict(collision="kbc", rates=(1.9,), equilibrium="moment_matched"), -2),
     (dict(collision="kbc_exact", rates=(1.9,), force=(1e-5, 0, 0)), -2),   # forcing is SRT/TRT only
-    (dict(collision=11), -1),                                   # unknown collision id
+    (dict(collision=12), -1),                                   # unknown collision id
+    (dict(collision="gen_srt", rates=(1.8,), equilibrium="moment_matched"), -2),
+    (dict(collision="gen_smagorinsky", rates=(1.9,)), -1),        # needs [omega_0, C_S]
     (dict(stencil=27, collision="gen_mrt", rates=(1.9,)), -2),    # generated MRT is D3Q19
     (dict(collision="gen_trt", rates=(1.6, 0.5), force=(1e-5, 0, 0)), -2),
 ])

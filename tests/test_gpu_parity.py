@@ -271,6 +271,16 @@ PARITY = [
          geometry="obstacles", ubb=(0.02, -0.01, 0.03), u_amp=0.05, steps=11),
     Case("gen_trt_q19_f64_eso", (18, 14, 10), 19, "gen_trt", (1.6, 0.5), "f64", pattern="esotwist", u_amp=0.05,
          steps=9),
+    Case("gen_smag_q19_f64_channel", (16, 20, 10), 19, "gen_smagorinsky", (1.95, 0.17), "f64", geometry="channel",
+         u_amp=0.05, steps=20),
+    Case("gen_smag_q27_f32_aa_obst", (17, 13, 11), 27, "gen_smagorinsky", (1.9, 0.12), "f32", pattern="aa",
+         geometry="obstacles", ubb=(0.02, -0.01, 0.03), u_amp=0.05, steps=12),
+    Case("gen_inc_srt_q19_f64_walls", (17, 13, 11), 19, "gen_srt", (1.8,), "f64", geometry="obstacles",
+         ubb=(0.02, -0.01, 0.03), u_amp=0.05, steps=15, equilibrium="incompressible"),
+    Case("gen_inc_trt_q27_f32_aa", (18, 14, 10), 27, "gen_trt", (1.5, 1.2), "f32", pattern="aa", steps=12,
+         u_amp=0.05, equilibrium="incompressible"),
+    Case("gen_inc_trt_q19_f64_push", (16, 12, 10), 19, "gen_trt", (1.6, 0.5), "f64", pattern="push", steps=9,
+         u_amp=0.05, equilibrium="incompressible"),
     # KBC with the exact entropy maximum by Newton's method
     Case("kbcx_q19_f64_cavity", (14, 14, 14), 19, "kbc_exact", (1.99,), "f64", geometry="cavity", ubb=(0.08, 0, 0),
          u_amp=0.1, steps=20),
@@ -780,7 +790,8 @@ def test_copy_q_probe():
 @pytest.mark.gpu
 @pytest.mark.parametrize("gen,hand,Q,rates,dtype,pattern", [
     ("gen_trt", "trt", 19, (1.6, 0.5), "f64", "pull"), ("gen_srt", "srt", 27, (1.8,), "f32", "aa"),
-    ("gen_mrt", "mrt", 19, (1.9, 1.0, 1.0, 1.0), "f32", "aa"), ("gen_mrt", "mrt", 19, (1.9, 1.3, 1.1, 0.8), "f64", "pull")])
+    ("gen_mrt", "mrt", 19, (1.9, 1.0, 1.0, 1.0), "f32", "aa"), ("gen_mrt", "mrt", 19, (1.9, 1.3, 1.1, 0.8), "f64", "pull"),
+    ("gen_smagorinsky", "smagorinsky", 27, (1.9, 0.17), "f64", "aa")])
 def test_generated_equals_hand_written(gen, hand, Q, rates, dtype, pattern):
     """The generated operator (codegen/) and the hand-written kernel are the same operator: same
     states after several steps up to FP reassociation."""
