@@ -115,6 +115,15 @@ CONFIGS["fig8_channel_flags"] = dict(_paper, op="trt", rates=(1.6, 0.5), pattern
 CONFIGS["fig8_channel_links"] = dict(CONFIGS["fig8_channel_flags"], boundary_mode="links",
                                      desc="D3Q19 TRT fp64 AA 300x100x100 channel, walls on the y and z faces, "
                                           "separate index-list boundary kernel (Fig. 8 analog)")
+CONFIGS["fig8_channel_inline"] = dict(CONFIGS["fig8_channel_flags"], boundary_mode="inline",
+                                      desc="D3Q19 TRT fp64 AA 300x100x100 channel, walls on the y and z faces, "
+                                           "compiled-in conditionals in every cell, no boundary launch (Fig. 8 analog)")
+CONFIGS["c1_f64_inline"] = dict(CONFIGS["c1_f64_flags"], boundary_mode="inline",
+                                desc=CONFIGS["c1_f64_flags"]["desc"].replace("compiled-in flag boundaries",
+                                                                             "flags tested in every cell (inline)"))
+CONFIGS["c3_inline"] = dict(CONFIGS["c3_flags"], boundary_mode="inline",
+                            desc=CONFIGS["c3_flags"]["desc"].replace("compiled-in flag boundaries",
+                                                                     "flags tested in every cell (inline)"))
 CONFIGS["fig10_small"] = dict(_paper, shape=(128, 128, 128), weak=True, op="mrt", rates=(1.9, 1.0, 1.0, 1.0),
                               pattern="aa", desc="D3Q19 weighted MRT fp64 AA 128^3 per GPU, weak scaling "
                                                  "(Fig. 10 small-block analog; report ms_per_step)")
@@ -149,7 +158,7 @@ def bytes_per_cell(cfg, flags):
     """2 q s, + 1 B flag where the update kernel reads a flag field (not with index-list
     boundaries, whose update kernels are flag-free)."""
     s = 8 if cfg["dtype"] == "f64" else 4
-    reads_flags = flags is not None and cfg.get("boundary_mode", "flags") == "flags"
+    reads_flags = flags is not None and cfg.get("boundary_mode", "flags") in ("flags", "inline")
     return 2 * cfg["Q"] * s + (1 if reads_flags else 0)
 
 

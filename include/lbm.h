@@ -127,8 +127,12 @@ extern "C" {
  *        cells and hold meaningless values. Any slab decomposition (the link kernel also fills the wall
  *        slots of ghost planes, after the exchange); not with the fused halo for AA and push, not
  *        with EsoTwist (LBM_EUNSUPPORTED). */
+/* LBM_BOUNDARY_INLINE: the flag field compiled into every cell's update ("compiled-in conditionals",
+ *        P:1230-1238): the bulk kernels test the flags of all q neighbours of every cell, no separate
+ *        boundary launch. Same results as LBM_BOUNDARY_FLAGS. Not with the fused halo (LBM_EUNSUPPORTED). */
 #define LBM_BOUNDARY_FLAGS 0
 #define LBM_BOUNDARY_LINKS 1
+#define LBM_BOUNDARY_INLINE 2
 
 #define LBM_HALO_ZEROCOPY 0 /* one NCCL message per crossing population plane */
 #define LBM_HALO_PACKED 1   /* pack kernel + one message per face            */
@@ -170,7 +174,7 @@ typedef struct lbm_config {
                                locally — exercises and times the multi-GPU exchange path on 1 GPU */
     int32_t equilibrium;    /* LBM_EQ_*: what SRT/TRT/MRT relax to (and what lbm_init_equilibrium writes);
                                other operators require LBM_EQ_COMPRESSIBLE (LBM_EUNSUPPORTED) */
-    int32_t boundary_mode;  /* LBM_BOUNDARY_FLAGS | LBM_BOUNDARY_LINKS (see below) */
+    int32_t boundary_mode;  /* LBM_BOUNDARY_FLAGS | LBM_BOUNDARY_LINKS | LBM_BOUNDARY_INLINE (see below) */
     int32_t n_row_rates;    /* 0, or 15 with LBM_MRT: one relaxation rate per non-conserved moment,
                                row_rates[k] for the rows of the weighted Gram-Schmidt basis in the paper's
                                order: x^2-y^2, xy, xz, y^2-z^2, yz (orthogonalised), bulk,

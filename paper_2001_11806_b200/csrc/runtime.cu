@@ -71,6 +71,7 @@ struct lbm_handle_s {
     Timing timing;
     bool fused = false;       // halo through NVLink peer stores (LBM_HALO_FUSED)
     bool links = false;       // index-list boundaries: flag-free update kernels + link kernel
+    bool inline_bc = false;   // compiled-in boundaries: every cell tests its neighbours' flags, no edge kernel
     FusedState fst;
     std::string err;
     dim3 block;
@@ -146,7 +147,7 @@ void tend(lbm_handle_s *h, cudaStream_t s) { tbegin(h, s); }
 // z_begin + k * z_step, k < nplanes), one edge-list launch per contiguous run of planes.
 void launch_edges(lbm_handle_s *h, Slab &s, const StepArgs &a, EdgeLaunch fn, const void *src, void *dst, int z_begin,
                   int nplanes, int z_step, cudaStream_t st) {
-    if (!s.edges || !fn || h->links) return;  // index-list boundaries: the update kernels are flag-free
+    if (!s.edges || !fn || h->links || h->inline_bc) return;  // links: flag-free update; inline: no edge pass
     auto run = [&](int zlo, int zhi) {  // interior planes [zlo, zhi)
         const int64_t b = s.edge_off[zlo + h->g], e = s.edge_off[zhi + h->g];
         if (e <= b) return;
@@ -562,8 +563,11 @@ int validate(const lbm_config *c) {
         if (c->equilibrium != LBM_EQ_COMPRESSIBLE)
             return fail(nullptr, LBM_EUNSUPPORTED, "per-moment MRT rates use the compressible equilibrium");
     }
-    if (c->boundary_mode != LBM_BOUNDARY_FLAGS && c->boundary_mode != LBM_BOUNDARY_LINKS)
+    if (c->boundary_mode != LBM_BOUNDARY_FLAGS && c->boundary_mode != LBM_BOUNDARY_LINKS &&
+        c->boundary_mode != LBM_BOUNDARY_INLINE)
         return fail(nullptr, LBM_EINVAL, "bad boundary_mode");
+    if (c->boundary_mode == LBM_BOUNDARY_INLINE && c->halo_mode == LBM_HALO_FUSED && (c->nranks > 1 || c->nccl_self))
+        return fail(nullptr, LBM_EUNSUPPORTED, "compiled-in (inline) boundaries use the NCCL or loopback halo");
     if (c->boundary_mode == LBM_BOUNDARY_LINKS && (c->pattern == LBM_AA || c->pattern == LBM_PUSH) &&
         c->halo_mode == LBM_HALO_FUSED)
         return fail(nullptr, LBM_EUNSUPPORTED, "index-list boundaries with the AA / push patterns use the NCCL or loopback halo");
@@ -1015,9 +1019,10 @@ int lbm_create(const lbm_config *cfg, lbm_handle *out) {
     h->have_flags = cfg->flags != nullptr;
     h->have_force = cfg->force[0] != 0 || cfg->force[1] != 0 || cfg->force[2] != 0;
     h->links = cfg->boundary_mode == LBM_BOUNDARY_LINKS && h->have_flags;
+    h->inline_bc = cfg->boundary_mode == LBM_BOUNDARY_INLINE && h->have_flags;
 
     // kernel selection (SRT = TRT with equal rates); index-list boundaries run the flag-free kernels
-    const int fm_bulk = h->have_flags && !h->links ? FM_BULK : FM_NONE;
+    const int fm_bulk = !h->have_flags || h->links ? FM_NONE : h->inline_bc ? FM_INLINE : FM_BULK;
     const bool per_row = cfg->collision == LBM_MRT && cfg->n_row_rates == 15;
     const int kcoll = per_row ? (int)OP_MRT_ROWS : cfg->collision;
     const bool force = h->have_force;

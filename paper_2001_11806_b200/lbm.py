@@ -29,8 +29,8 @@ HOST, DEVICE = 0, 1
 HALO_ZEROCOPY, HALO_PACKED, HALO_FUSED = 0, 1, 2
 PATH_AUTO, PATH_PLAIN, PATH_STAGED = 0, 1, 2
 EQ_COMPRESSIBLE, EQ_INCOMPRESSIBLE, EQ_MOMENT_MATCHED = 0, 1, 2
-BOUNDARY_FLAGS, BOUNDARY_LINKS = 0, 1
-BOUNDARY_MODES = {"flags": BOUNDARY_FLAGS, "links": BOUNDARY_LINKS}
+BOUNDARY_FLAGS, BOUNDARY_LINKS, BOUNDARY_INLINE = 0, 1, 2
+BOUNDARY_MODES = {"flags": BOUNDARY_FLAGS, "links": BOUNDARY_LINKS, "inline": BOUNDARY_INLINE}
 EQUILIBRIA = {"compressible": EQ_COMPRESSIBLE, "incompressible": EQ_INCOMPRESSIBLE, "moment_matched": EQ_MOMENT_MATCHED}
 KERNEL_PATHS = {"auto": PATH_AUTO, "plain": PATH_PLAIN, "staged": PATH_STAGED}
 

@@ -85,7 +85,8 @@ def test_slab_plan(L):
     (dict(equilibrium=3), -1),                                  # unknown equilibrium kind
     (dict(shape=(0, 8, 8)), -1),                                # empty lattice
     (dict(shape=(8, 8, 0)), -1),
-    (dict(boundary_mode=2), -1),                                # unknown boundary mode
+    (dict(boundary_mode=3), -1),                                # unknown boundary mode
+    (dict(boundary_mode="inline", nccl_self=True, halo_mode=2), -2),  # inline: no fused halo
     (dict(collision="trt", rates=(1.0,) * 15), -1),             # per-moment rates are for MRT
     (dict(collision="mrt", rates=(1.0,) * 14 + (2.0,)), -1),    # per-moment rate outside (0, 2)
     (dict(collision="mrt", rates=(1.0,) * 15, equilibrium="incompressible"), -2),

@@ -805,3 +805,45 @@ def test_generated_equals_hand_written(gen, hand, Q, rates, dtype, pattern):
         out.append(sim.populations())
     tol = 1e-13 if dtype == "f64" else 1e-5
     np.testing.assert_allclose(out[0], out[1], rtol=0, atol=tol)
+
+
+# -----------------------------------------------------------------------------------------
+# Compiled-in boundaries (LBM_BOUNDARY_INLINE): every cell tests its neighbours' flags
+# -----------------------------------------------------------------------------------------
+INLINE_CASES = [
+    Case("in_trt_f64_cavity_pull", (14, 14, 14), 19, "trt", (1.6, 0.5), "f64", force=(1e-5, 0, 0), geometry="cavity",
+         ubb=(0.05, 0, 0), steps=21),
+    Case("in_trt_f32_obst_aa", (17, 13, 11), 19, "trt", (1.6, 0.5), "f32", pattern="aa", geometry="obstacles",
+         ubb=(0.02, -0.01, 0.03), steps=15),
+    Case("in_cum27_cavity_push", (12, 12, 12), 27, "cumulant", (1.95,), "f64", pattern="push", geometry="cavity",
+         ubb=(0.05, 0, 0), steps=9),
+    Case("in_mrt_f64_channel_eso", (16, 20, 12), 19, "mrt", (1.9, 1.3, 1.1, 0.8), "f64", pattern="esotwist",
+         geometry="channel", steps=11),
+]
+
+
+@pytest.mark.parametrize("case", INLINE_CASES, ids=lambda c: c.name)
+def test_inline_boundaries_vs_oracle_and_flags(case):
+    sim = make_sim(case, boundary_mode="inline")
+    init_sim(sim, case)
+    sim.step(case.steps)
+    got = sim.populations()
+    mask = fluid_mask(case, case.Q)
+    assert max_rel_err(got, oracle_run(case), mask) <= TOL[case.dtype]
+    ref = make_sim(case)  # split mode (bulk + edge-list kernel): the same per-cell arithmetic
+    init_sim(ref, case)
+    ref.step(case.steps)
+    np.testing.assert_allclose(got[mask], ref.populations()[mask], rtol=0,
+                               atol=1e-14 if case.dtype == "f64" else 1e-6)
+
+
+@pytest.mark.parametrize("P", [2, 3])
+def test_inline_boundaries_slabs_bit_identical(P):
+    case = Case("in_slabs", (16, 12, 12), 19, "trt", (1.6, 0.5), "f64", pattern="aa", geometry="obstacles",
+                ubb=(0.02, -0.01, 0.03), steps=8)
+    one = make_sim(case, boundary_mode="inline")
+    many = make_sim(case, boundary_mode="inline", n_local_slabs=P if 12 % P == 0 else 2)
+    for s in (one, many):
+        init_sim(s, case)
+        s.step(case.steps)
+    np.testing.assert_array_equal(one.populations(raw=True), many.populations(raw=True))
