@@ -9,7 +9,9 @@ timeout 900 python bench.py > $O/bench_default.log 2>&1; echo "default=$?" >> $O
 timeout 600 python bench.py --impl reference > $O/bench_reference.log 2>&1; echo "reference=$?" >> $O/status.txt
 for c in c0 c1_f64 c1_f32 c2 c3 c1_f64_flags c1_f32_flags c3_flags c3_aa c3_aa_links eso_c4 eso_c2 eso_c3 push_c4 push_c3 \
          eq_inc_c4 eq_mm_c4 eq_inc_c2 op_trt op_mrt op_smagorinsky op_kbc op_kbc27 op_cumulant19 op_cumulant27 \
-         fig5_srt_pull fig7_trt_aa fig7_trt_aa_q27 fig8_channel_flags fig8_channel_links fig10_small; do
+         fig5_srt_pull fig7_trt_aa fig7_trt_aa_q27 fig8_channel_flags fig8_channel_links fig10_small \
+         c4_gen c2_gen op_gen_trt op_gen_mrt op_gen_smagorinsky op_gen_srt27 op_trt27 op_kbc_exact op_kbc27_exact \
+         fig8_channel_inline c1_f64_inline c3_inline; do
   timeout 300 python bench.py --config $c --steps 50 --warmup 5 --e2e-reps 1 --no-cpu-baseline > $O/bench_$c.log 2>&1
   echo "$c=$?" >> $O/status.txt
 done
@@ -33,6 +35,8 @@ prof c3 "k_pull|k_links" 6 2
 prof op_kbc k_staged 4 2
 prof c1_f64 "k_pull|k_links" 6 2
 prof c1_f32 "k_pull|k_links" 6 2
+prof c4_gen k_pull 3 1
+prof op_kbc_exact k_aa 4 2
 cat $O/status.txt
 # halo transports on one GPU through a 1-rank communicator (self exchange), C4 and C2
 for hm in 0 1 2; do
