@@ -77,7 +77,7 @@ for _name, _op, _q, _rates in [("trt", "trt", 19, (1.6, 0.5)), ("smagorinsky", "
                                ("kbc27_exact", "kbc_exact", 27, (1.95,)), ("gen_trt", "gen_trt", 19, (1.6, 0.5)),
                                ("gen_mrt", "gen_mrt", 19, (1.9, 1.0, 1.0, 1.0)), ("gen_srt27", "gen_srt", 27, (1.8,)),
                                ("gen_smagorinsky", "gen_smagorinsky", 19, (1.95, 0.17)), ("trt27", "trt", 27, (1.6, 0.5)),
-                               ("srt27", "srt", 27, (1.8,))]:
+                               ("srt27", "srt", 27, (1.8,)), ("gen_mrt27", "gen_mrt", 27, (1.9, 1.0, 1.0, 1.0))]:
     CONFIGS[f"op_{_name}"] = dict(desc=f"D3Q{_q} {_op} fp64 AA 512^3 periodic (Fig. 9-style operator comparison)",
                                   shape=(512, 512, 512), weak=False, Q=_q, op=_op, rates=_rates, dtype="f64",
                                   pattern="aa", force=(0, 0, 0), geometry="periodic", init=("random", 1e-3, 0.01),

@@ -78,7 +78,7 @@ extern "C" {
                            csrc/generated/gen_collide.cuh. SRT rates = [omega], D3Q19/D3Q27 */
 #define LBM_GEN_TRT 9   /* generated TRT, rates = [omega_e, omega_o], D3Q19/D3Q27 (no forcing)    */
 #define LBM_GEN_MRT 10  /* generated weighted MRT, rates = [omega_shear, omega_bulk, omega_3,
-                           omega_4] (missing = 1), D3Q19                                        */
+                           omega_4 (all orders >= 4)] (missing = 1), D3Q19 and D3Q27           */
 #define LBM_GEN_SMAGORINSKY 11 /* generated Smagorinsky SRT, rates = [omega_0, C_S], D3Q19/D3Q27.
                            LBM_GEN_SRT / LBM_GEN_TRT also take LBM_EQ_INCOMPRESSIBLE          */
 #define LBM_KBC_EXACT 7 /* KBC with omega_h maximising the entropy of Eq. (17) exactly, per cell, by

@@ -17,9 +17,9 @@ GENERATED = os.path.join(os.path.dirname(HERE), "csrc", "generated", "gen_collid
 # (Q, op, equilibrium) generated into the library
 C, I = "compressible", "incompressible"
 OPERATORS = [(19, "srt", C), (19, "trt", C), (19, "mrt", C), (19, "smagorinsky", C), (19, "srt", I), (19, "trt", I),
-             (27, "srt", C), (27, "trt", C), (27, "smagorinsky", C), (27, "srt", I), (27, "trt", I)]
+             (27, "srt", C), (27, "trt", C), (27, "mrt", C), (27, "smagorinsky", C), (27, "srt", I), (27, "trt", I)]
 # FLOP-table rows that are not compiled into the library
-TABLE_ONLY = [(27, "mrt", C)]
+TABLE_ONLY = []
 
 # Table II: (only CSE, custom with direction CSE, custom default CSE), D3Q19 / D3Q27;
 # "mrt" = the weighted MRT row.

@@ -948,8 +948,8 @@ __device__ __forceinline__ void collide(T (&g)[Q], const Rates<T> &p) {
         if constexpr (Q == 19) gen_smagorinsky19<T>(g, p);
         else gen_smagorinsky27<T>(g, p);
     } else if constexpr (OP == OP_GEN_MRT) {
-        static_assert(Q == 19, "the generated MRT is D3Q19");
-        gen_mrt19<T>(g, p);
+        if constexpr (Q == 19) gen_mrt19<T>(g, p);
+        else gen_mrt27<T>(g, p);
     }
 }
 

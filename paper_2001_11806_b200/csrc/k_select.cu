@@ -36,6 +36,8 @@ Kernels inst_gtrt27d(int fm, bool force);
 Kernels inst_gtrt27f(int fm, bool force);
 Kernels inst_gmrt19d(int fm, bool force);
 Kernels inst_gmrt19f(int fm, bool force);
+Kernels inst_gmrt27d(int fm, bool force);
+Kernels inst_gmrt27f(int fm, bool force);
 Kernels inst_gsmag19d(int fm, bool force);
 Kernels inst_gsmag19f(int fm, bool force);
 Kernels inst_gsmag27d(int fm, bool force);
@@ -118,6 +120,7 @@ Kernels select_generated(int op, int Q, int dtype, int fm, bool force, int eq) {
         if (Q == 27) return d ? inst_gtrt27d(fm, force) : inst_gtrt27f(fm, force);
     } else if (op == OP_GEN_MRT) {
         if (Q == 19) return d ? inst_gmrt19d(fm, force) : inst_gmrt19f(fm, force);
+        if (Q == 27) return d ? inst_gmrt27d(fm, force) : inst_gmrt27f(fm, force);
     }
     return Kernels{};
 }

@@ -550,8 +550,8 @@ int validate(const lbm_config *c) {
     if ((double)c->global[0] * c->global[1] * planes >= 2147483647.0)
         return fail(nullptr, LBM_EINVAL, "slab too large for 32-bit in-plane offsets (split it over more slabs)");
     const bool force = c->force[0] != 0 || c->force[1] != 0 || c->force[2] != 0;
-    if ((c->collision == LBM_MRT || c->collision == LBM_GEN_MRT) && c->stencil != 19)
-        return fail(nullptr, LBM_EUNSUPPORTED, "MRT is implemented for D3Q19");
+    if (c->collision == LBM_MRT && c->stencil != 19)
+        return fail(nullptr, LBM_EUNSUPPORTED, "MRT is implemented for D3Q19 (D3Q27: LBM_GEN_MRT)");
     if (force && c->collision != LBM_SRT && c->collision != LBM_TRT)
         return fail(nullptr, LBM_EUNSUPPORTED, "forcing is implemented for SRT/TRT");
     if (c->n_row_rates != 0 && c->n_row_rates != 15) return fail(nullptr, LBM_EINVAL, "n_row_rates must be 0 or 15");

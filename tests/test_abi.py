@@ -97,7 +97,6 @@ def test_slab_plan(L):
     (dict(collision=12), -1),                                   # unknown collision id
     (dict(collision="gen_srt", rates=(1.8,), equilibrium="moment_matched"), -2),
     (dict(collision="gen_smagorinsky", rates=(1.9,)), -1),        # needs [omega_0, C_S]
-    (dict(stencil=27, collision="gen_mrt", rates=(1.9,)), -2),    # generated MRT is D3Q19
     (dict(collision="gen_trt", rates=(1.6, 0.5), force=(1e-5, 0, 0)), -2),
 ])
 def test_create_validation_errors(L, kw, code):

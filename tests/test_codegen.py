@@ -66,7 +66,8 @@ def _strategies(Q, op, eq=C):
 
 
 @pytest.mark.parametrize("Q,op,eq", [(19, "srt", C), (19, "trt", C), (19, "mrt", C), (27, "srt", C), (27, "trt", C),
-                                     (19, "smagorinsky", C), (27, "smagorinsky", C), (19, "srt", I), (27, "trt", I)])
+                                     (19, "smagorinsky", C), (27, "smagorinsky", C), (19, "srt", I), (27, "trt", I),
+                                     (27, "mrt", C)])
 def test_strategies_equal_and_match_oracle(Q, op, eq):
     res = _strategies(Q, op, eq)
     base = D.derive(Q, op, eq)

@@ -267,6 +267,10 @@ PARITY = [
     Case("gen_mrt_q19_f32_pull_walls", (32, 20, 12), 19, "gen_mrt", (1.9, 1.0, 1.0, 1.0), "f32", geometry="channel",
          u_amp=0.03, steps=11),
     Case("gen_srt_q27_f32_aa", (18, 14, 10), 27, "gen_srt", (1.7,), "f32", pattern="aa", u_amp=0.05, steps=12),
+    Case("gen_mrt_q27_f64_cavity", (14, 14, 14), 27, "gen_mrt", (1.9, 1.3, 1.1, 0.8), "f64", geometry="cavity",
+         ubb=(0.05, 0, 0), steps=15),
+    Case("gen_mrt_q27_f32_aa_obst", (17, 13, 11), 27, "gen_mrt", (1.8, 1.0, 1.0, 1.0), "f32", pattern="aa",
+         geometry="obstacles", ubb=(0.02, -0.01, 0.03), u_amp=0.05, steps=12),
     Case("gen_trt_q27_f64_push_obst", (17, 13, 11), 27, "gen_trt", (1.6, 0.5), "f64", pattern="push",
          geometry="obstacles", ubb=(0.02, -0.01, 0.03), u_amp=0.05, steps=11),
     Case("gen_trt_q19_f64_eso", (18, 14, 10), 19, "gen_trt", (1.6, 0.5), "f64", pattern="esotwist", u_amp=0.05,
