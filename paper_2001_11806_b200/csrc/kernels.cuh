@@ -19,7 +19,9 @@
 // (2 -> 128, 3 -> 80, 4 -> 64, 6 -> 40) and so sets how many population loads are in flight per SM.
 // Measured on B200 (scripts/gpu_sweep.sh): D3Q19 TRT fp64 3 (c4 1.03 of copy
 // BW, c1 0.98), D3Q19 TRT fp32 6 (c1 0.92), D3Q27 cumulant fp64 3 (c3 0.67), MRT fp32 AA 3 (c2
-// 0.75); other families use the largest value without register spills. LBM_MINB_OVERRIDE_* exist
+// 0.75); other families use the largest value without register spills. Exception: the exact (Newton)
+// KBC is FP64-latency bound; 2 CTAs of 128 registers (small spills) beat 1 CTA of 255 registers
+// without spills (D3Q19 4.77 vs 3.14 GLUPS, D3Q27 2.76 vs 2.08). LBM_MINB_OVERRIDE_* exist
 // for sweeps only.
 namespace lbm {
 
@@ -29,9 +31,9 @@ struct MinBlocks {
     static constexpr bool f64 = sizeof(T) == 8;
     // OP: 0 SRT, 1 TRT, 2 MRT, 3 cumulant, 4 identity, 5 Smagorinsky, 6 KBC, 7 KBC exact, 8 MRT rows
     static constexpr int pull_default =
-        f64 ? (OP == 7 ? 1 : (OP == 2 || OP == 5 || OP == 6 || (Q == 27 && OP <= 1)) ? 2 : 3)
+        f64 ? ((OP == 2 || OP == 5 || OP == 6 || OP == 7 || (Q == 27 && OP <= 1)) ? 2 : 3)
             : ((OP <= 1 || OP == 4 || OP == 5) ? (Q == 19 ? 6 : 4) : 3);
-    static constexpr int aa_default = f64 ? (OP == 7 ? 1 : 2) : ((OP == 2 || OP == 6 || (Q == 19 && (OP <= 1 || OP == 5))) ? 3 : 2);
+    static constexpr int aa_default = f64 ? 2 : ((OP == 2 || OP == 6 || (Q == 19 && (OP <= 1 || OP == 5))) ? 3 : 2);
 #ifdef LBM_MINB_OVERRIDE_PULL
     static constexpr int pull = LBM_MINB_OVERRIDE_PULL;
 #else
