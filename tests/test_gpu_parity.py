@@ -535,11 +535,17 @@ def _oracle_at(case, pts, k):
     return np.array(out).T
 
 
-@pytest.mark.parametrize("name,boundary_mode", [("c0", "flags"), ("c1_f64", "flags"), ("c1_f32", "flags"), ("c2", "flags"),
-                                                ("c3", "flags"), ("c4", "flags"), ("c1_f64", "links"),
-                                                ("c1_f32", "links"), ("c3", "links")])
-def test_full_size_sampled_parity(name, boundary_mode):
+@pytest.mark.parametrize("name,boundary_mode,op", [("c0", "flags", None), ("c1_f64", "flags", None), ("c1_f32", "flags", None),
+                                                   ("c2", "flags", None), ("c3", "flags", None), ("c4", "flags", None),
+                                                   ("c1_f64", "links", None), ("c1_f32", "links", None), ("c3", "links", None),
+                                                   # generated operators and compiled-in boundaries at full size
+                                                   ("c4", "flags", "gen_trt"), ("c2", "flags", "gen_mrt"),
+                                                   ("c1_f64", "inline", None), ("c3", "inline", None)])
+def test_full_size_sampled_parity(name, boundary_mode, op):
     base = FULL[name]
+    if op is not None:
+        base = Case(base.name, base.shape, base.Q, op, base.rates, base.dtype, base.pattern, base.force, base.geometry,
+                    base.ubb, init=base.init, rho_amp=base.rho_amp, u_amp=base.u_amp)
     # random near-equilibrium start (instead of rest) so every sampled cell does non-trivial work
     case = Case(base.name, base.shape, base.Q, base.op, base.rates, base.dtype, base.pattern, base.force,
                 base.geometry, base.ubb, init="shear" if base.init == "shear" else "random",
