@@ -115,3 +115,21 @@ def test_nonperiodic_axis_requires_walls(L):
     with pytest.raises(L.LBMError) as e:
         L.Simulation((8, 8, 8), periodic=(1, 0, 1), flags=fl)
     assert e.value.status == -1
+
+
+def test_binding_constants_match_header(L):
+    """Every enum constant of the binding equals the #define of include/lbm.h (collision ids incl.
+    LBM_KBC_EXACT and the generated operators, boundary modes, equilibria, patterns)."""
+    import re
+    defs = dict(re.findall(r"^#define (LBM_[A-Z0-9_]+) (-?\d+)", open(HEADER).read(), re.M))
+    names = {"KBC_EXACT": "LBM_KBC_EXACT", "GEN_SRT": "LBM_GEN_SRT", "GEN_TRT": "LBM_GEN_TRT",
+             "GEN_MRT": "LBM_GEN_MRT", "GEN_SMAGORINSKY": "LBM_GEN_SMAGORINSKY", "KBC": "LBM_KBC",
+             "SMAGORINSKY": "LBM_SMAGORINSKY", "CUMULANT": "LBM_CUMULANT", "MRT": "LBM_MRT", "TRT": "LBM_TRT",
+             "SRT": "LBM_SRT", "IDENTITY": "LBM_IDENTITY", "BOUNDARY_FLAGS": "LBM_BOUNDARY_FLAGS",
+             "BOUNDARY_LINKS": "LBM_BOUNDARY_LINKS", "BOUNDARY_INLINE": "LBM_BOUNDARY_INLINE"}
+    for py, c in names.items():
+        assert getattr(L, py) == int(defs[c]), (py, c)
+    for name, v in L.COLLISIONS.items():
+        assert v == int(defs["LBM_" + name.upper()]), name
+    for name, v in L.BOUNDARY_MODES.items():
+        assert v == int(defs["LBM_BOUNDARY_" + name.upper()]), name
