@@ -249,8 +249,10 @@ constexpr bool staged_auto() {
     // generated D3Q27 SRT/TRT: the CSE'd code needs more registers than the plain kernels' cap
     // (AA 512^3 fp64: plain 0.86, staged 0.92 of copy BW; hand-written TRT plain 0.97)
     constexpr bool gen27 = Q == 27 && (op_base(OPX) == OP_GEN_SRT || op_base(OPX) == OP_GEN_TRT);
-    return OP == OP_MRT || OP == OP_MRT_ROWS || OP == OP_KBC || OP == OP_SMAGORINSKY || (OP == OP_CUMULANT && MODE != SM_PULL) ||
-           gen27;
+    // cumulant: staged for AA / EsoTwist (in place), plain for the two-array pull and push kernels
+    // (C3 push: plain 0.906 vs staged 0.857 of copy BW; scripts/gpu_path_sweep.sh)
+    return OP == OP_MRT || OP == OP_MRT_ROWS || OP == OP_KBC || OP == OP_SMAGORINSKY ||
+           (OP == OP_CUMULANT && MODE != SM_PULL && MODE != SM_PUSH) || gen27;
 }
 
 template <int Q, int OP, typename T, int FM, bool FORCE, int MODE>
