@@ -115,7 +115,7 @@ CONFIGS["fig7_trt_aa_q27"] = dict(_paper, Q=27, op="trt", rates=(1.6, 0.5), patt
                                   desc="D3Q27 TRT fp64 AA 300x100x100 (Fig. 7 analog, D3Q27)")
 CONFIGS["fig8_channel_flags"] = dict(_paper, op="trt", rates=(1.6, 0.5), pattern="aa", geometry="box",
                                      desc="D3Q19 TRT fp64 AA 300x100x100 channel, walls on the y and z faces, "
-                                          "compiled-in flag boundaries (Fig. 8 analog)")
+                                          "split bulk + near-wall edge kernel flag boundaries (Fig. 8 analog)")
 CONFIGS["fig8_channel_links"] = dict(CONFIGS["fig8_channel_flags"], boundary_mode="links",
                                      desc="D3Q19 TRT fp64 AA 300x100x100 channel, walls on the y and z faces, "
                                           "separate index-list boundary kernel (Fig. 8 analog)")
@@ -260,9 +260,45 @@ def oracle_sample(cfg, target_s=15.0, max_steps=None):
         if el > target_s / 2 or (max_steps and steps >= max_steps):
             break
     cells = nx * ny * planes
+    # the same oracle on one core, on a 2-plane sample (the paper's per-core view)
+    m1 = O.Method(Q=m.Q, op=m.op, rates=m.rates, force=m.force, ubb_u=m.ubb_u, equilibrium=m.equilibrium, nthreads=1)
+    d1 = O.Domain(m1, nx, ny, 2)
+    f1 = np.empty(d1.shape)
+    f1[:] = w[:, None, None, None]
+    g1 = f1.copy()
+    s1, t1 = 0, time.perf_counter()
+    while True:
+        d1.step_pull(f1, g1)
+        f1, g1 = g1, f1
+        s1 += 1
+        e1 = time.perf_counter() - t1
+        if e1 > target_s / 4:
+            break
     return {"value": cells * steps / el / 1e6, "unit": "MLUPS", "cores": threads, "kind": "oracle",
             "sample": f"{nx}x{ny}x{planes} sub-slab of {cfg['desc'].split(' (')[0]}, {steps} pull steps, fp64, "
-                      f"{threads} OpenMP threads, {el:.1f} s"}
+                      f"{threads} OpenMP threads, {el:.1f} s",
+            "value_1core": nx * ny * 2 * s1 / e1 / 1e6,
+            "sample_1core": f"{nx}x{ny}x2 sub-slab, {s1} pull steps, 1 thread, {e1:.1f} s",
+            **host_info()}
+
+
+def host_info():
+    """CPU model, logical cores and RAM of the host the oracle ran on (SURVEY §8(d) oracle timing)."""
+    model, ram = None, None
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+        with open("/proc/meminfo") as fh:
+            for line in fh:
+                if line.startswith("MemTotal"):
+                    ram = round(int(line.split()[1]) / 2 ** 20, 1)
+                    break
+    except OSError:
+        pass
+    return {"cpu_model": model, "host_logical_cores": os.cpu_count(), "ram_gib": ram}
 
 
 # ---------------------------------------------------------------------------------------------
@@ -300,7 +336,7 @@ def run_reference(args, cfg):
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": args.config, "desc": cfg["desc"], "sample": f"{nx}x{ny}x{planes} sub-slab per step"},
             "cpu_baseline": {"value": val, "unit": "MLUPS", "cores": threads, "kind": "oracle",
-                             "sample": f"{nx}x{ny}x{planes} sub-slab, one pull step per bench step"},
+                             "sample": f"{nx}x{ny}x{planes} sub-slab, one pull step per bench step", **host_info()},
             "e2e": {"value": val, "unit": "MLUPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
     return 0
@@ -484,9 +520,13 @@ def main():
             t = torch.tensor([te], dtype=torch.float64, device="cuda")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             te = float(t[0])
+        # bytes copied per job (rho + u up, rho + u down), and per LB step of that job
+        h2d_job = d2h_job = int(4 * 8 * sim.cells)
         e2e = {"value": nf_total * job * args.e2e_reps / te / 1e6, "unit": "MLUPS",
-               "h2d_bytes_per_step": int(4 * 8 * sim.cells), "d2h_bytes_per_step": int(4 * 8 * sim.cells),
-               "step": f"one job: init_equilibrium from pinned host rho/u, lbm_step({job}), get_macroscopic to host",
+               "h2d_bytes_per_step": h2d_job / job, "d2h_bytes_per_step": d2h_job / job,
+               "h2d_bytes_per_job": h2d_job, "d2h_bytes_per_job": d2h_job, "lb_steps_per_job": job,
+               "step": f"one job: init_equilibrium from pinned host rho/u, lbm_step({job}), get_macroscopic to host; "
+                       "bytes per step = bytes per job / LB steps per job",
                "reps": args.e2e_reps}
 
     cpu = None

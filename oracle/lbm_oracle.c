@@ -327,6 +327,14 @@ static void ser_mul(const double *A, const double *B, double *C) {
 
 static const double fact3[3] = {1.0, 1.0, 2.0};
 
+/* c^e for a lattice velocity component c in {-1, 0, 1} and e in {0, 1, 2} (0^0 = 1): exact, the
+ * value pow(c, e) returns, by repeated multiplication. */
+static double ipow(int c, int e) {
+    double v = 1.0;
+    for (int k = 0; k < e; ++k) v *= (double)c;
+    return v;
+}
+
 /* ln(1 + X) = sum_{n=1}^{6} (-1)^{n+1} X^n / n, exact in the truncated ring (X^7 = 0). */
 static void ser_log1p(const double *X, double *K) {
     double P[27];
@@ -361,7 +369,7 @@ static double cumulants(const ora_stencil_t *s, const double *f, double *kappa) 
             for (int c = 0; c < 3; ++c) {
                 double v = 0.0; /* raw moment m_abc = sum_q f_q cx^a cy^b cz^c (Eq. 5) */
                 for (int q = 0; q < s->Q; ++q)
-                    v += f[q] * pow(s->c[q][0], a) * pow(s->c[q][1], b) * pow(s->c[q][2], c);
+                    v += f[q] * ipow(s->c[q][0], a) * ipow(s->c[q][1], b) * ipow(s->c[q][2], c);
                 m[a * 9 + b * 3 + c] = v;
             }
     double rho = m[0];

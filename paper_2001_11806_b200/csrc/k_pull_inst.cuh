@@ -120,10 +120,14 @@ void eso_edge_launcher(const StepArgs &a, const void *src, void *f, const uint32
 template <int Q, int OP, typename T, int FM, bool FORCE, bool AA>
 int persistent_launcher(const StepArgs &a, void *A, void *B, int phase, int nsteps, cudaStream_t s) {
     auto kern = k_persistent<Q, OP, T, FM, FORCE, AA>;
-    static int coresident = 0;
+    // co-resident CTA count: an occupancy result of the current device, cached per device ordinal
+    static int coresident_of[kMaxDevices] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= kMaxDevices) return -1;
+    int &coresident = coresident_of[dev];
     if (coresident == 0) {
-        int per_sm = 0, sms = 0, dev = 0;
-        cudaGetDevice(&dev);
+        int per_sm = 0, sms = 0;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, 0);
         coresident = per_sm * sms;

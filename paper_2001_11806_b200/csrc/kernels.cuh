@@ -64,7 +64,10 @@ struct StepArgs {
                                    // neighbour (only such cells read neighbour flags)
     void *peer_up;                 // fused halo (boundary launch only): base of the up neighbour's
     void *peer_down;               // dst array / down neighbour's dst array (NVLink LSA pointers)
+    int stage_flags;               // staged kernels (set by the launcher): flag rows moved by bulk copy
 };
+
+constexpr int kMaxDevices = 64;  // per-device caches of launch attributes and occupancy
 
 template <typename T>
 __device__ __forceinline__ Rates<T> load_rates(const StepArgs &a) {

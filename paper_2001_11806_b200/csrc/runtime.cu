@@ -64,6 +64,7 @@ struct lbm_handle_s {
     int aa_parity = 0;
     cudaGraphExec_t graph = nullptr;
     int graph_parity = -1;
+    int graph_path = -1;  // kernel path (lbm_set_kernel_path) the graph was captured with
     int64_t launches = 0;
     int *d_nanflag = nullptr;
     double *scratch = nullptr;
@@ -496,7 +497,9 @@ bool persistent_ok(const lbm_handle_s *h) {
 
 int run_graph_cycle(lbm_handle_s *h) {
     // one cycle = two steps (pull: src->dst->src; AA: even+odd), replayed; state returns to the same slots
-    if (!h->graph || h->graph_parity != (!two_arrays(h) ? h->aa_parity : h->slabs[0].cur)) {
+    // re-capture when the parity or the process-wide kernel path changed since the capture
+    if (!h->graph || h->graph_parity != (!two_arrays(h) ? h->aa_parity : h->slabs[0].cur) ||
+        h->graph_path != lbm::staged_path()) {
         if (h->graph) {
             cudaGraphExecDestroy(h->graph);
             h->graph = nullptr;
@@ -513,6 +516,7 @@ int run_graph_cycle(lbm_handle_s *h) {
         cudaGraphDestroy(gr);
         h->launches = l0;  // the capture did not launch
         h->graph_parity = par;
+        h->graph_path = lbm::staged_path();
     }
     CUDA_TRY(h, cudaGraphLaunch(h->graph, h->stream));
     h->launches += 2;

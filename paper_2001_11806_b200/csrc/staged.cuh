@@ -116,7 +116,9 @@ __device__ __forceinline__ void stage_issue(const StepArgs &a, const T *f, const
     const int nx = a.geo.nx, ny = a.geo.ny;
     const uint32_t row_bytes = (uint32_t)nx * sizeof(T);
     const uint32_t per_q = (uint32_t)tl.hl * row_bytes;
-    const bool sflags = FM == FM_BULK && nx % 16 == 0;  // flag rows staged too (bulk copies need 16 B)
+    // flag rows staged too (bulk copies need 16-byte rows and a 16-byte aligned flag base; the host side
+    // checks the base, flags_staged())
+    const bool sflags = FM == FM_BULK && nx % 16 == 0 && a.stage_flags;
     const uint32_t flag_bytes = sflags ? (uint32_t)tl.hl * (uint32_t)nx : 0u;
     if (lane == 0) mbar_expect_tx(bar, per_q * Q + flag_bytes);
     __syncwarp();
@@ -170,7 +172,7 @@ __global__ void __launch_bounds__(kStagedBT + 32, (StagedMinBlocks<Q, OP, T>::va
     const Rates<T> r = load_rates<T>(a);
     const int64_t Sq = a.geo.Sq;
     const int rowlen = H * nx;  // elements per q in a stage
-    const bool sflags = FM == FM_BULK && nx % 16 == 0;
+    const bool sflags = FM == FM_BULK && nx % 16 == 0 && a.stage_flags;
     int it = 0;
     for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
         const int stage = it % nstages;
@@ -263,9 +265,10 @@ bool staged_launch(const StepArgs &a, const void *src, void *dst, int nplanes, c
     } else {
     constexpr int BT = kStagedBT;
     const int path = staged_path();
-    // AA with the split flag mode: the staged kernels also win for the TRT class (Fig. 8 walled channel
-    // 0.747 -> 0.810 of copy BW; the flag-free AA kernels stay plain)
-    constexpr bool aa_flags = FM == FM_BULK && (MODE == SM_AA_EVEN || MODE == SM_AA_ODD) && op_class(op_base(OP)) == OP_TRT;
+    // AA with the split flag mode: the staged kernels also win for the TRT class, hand-written SRT included
+    // (same collide body; Fig. 8 walled channel 0.747 -> 0.805 of copy BW; the flag-free AA kernels stay plain)
+    constexpr int cls = op_class(op_base(OP));
+    constexpr bool aa_flags = FM == FM_BULK && (MODE == SM_AA_EVEN || MODE == SM_AA_ODD) && (cls == OP_TRT || cls == OP_SRT);
     if (path == 1 || (path == 0 && !(staged_auto<Q, OP, MODE>() || aa_flags))) return false;
     const int64_t row_bytes = (int64_t)a.geo.nx * (int64_t)sizeof(T);
     if (row_bytes % 16 != 0) return false;
@@ -274,25 +277,32 @@ bool staged_launch(const StepArgs &a, const void *src, void *dst, int nplanes, c
     int H = (int)((48 * 1024) / (Q * row_bytes));
     if (H < 1) H = 1;
     if (H > a.geo.ny) H = a.geo.ny;
-    const int64_t stage_bytes = ((int64_t)Q * H * row_bytes + (FM == FM_BULK && a.geo.nx % 16 == 0 ? (int64_t)H * a.geo.nx : 0) + 127) / 128 * 128;
+    // flag rows are staged by bulk copy only from a 16-byte aligned flag base (a caller's flags pointer in
+    // the low-level ABI may be any torch view); otherwise consumers read the flag byte from global memory
+    StepArgs b = a;
+    b.stage_flags = FM == FM_BULK && a.geo.nx % 16 == 0 && reinterpret_cast<uintptr_t>(a.flags) % 16 == 0;
+    const int64_t stage_bytes = ((int64_t)Q * H * row_bytes + (b.stage_flags ? (int64_t)H * a.geo.nx : 0) + 127) / 128 * 128;
     const size_t smem = 128 + (size_t)nst * stage_bytes;
     if (smem > 227 * 1024) return false;
     auto kern = k_staged<Q, OP, T, FM, FORCE, MODE>;
-    static size_t smem_set = 0;
-    if (smem > smem_set) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    // the shared-memory attribute is per device: cache the largest size set, per device ordinal
+    static size_t smem_set[kMaxDevices] = {};
+    if (dev < 0 || dev >= kMaxDevices) return false;
+    if (smem > smem_set[dev]) {
         if (cudaFuncSetAttribute((const void *)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
             return false;
-        smem_set = smem;
+        smem_set[dev] = smem;
     }
-    int per_sm = 0, sms = 0, dev = 0;
-    cudaGetDevice(&dev);
+    int per_sm = 0, sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, BT + 32, smem) != cudaSuccess || per_sm < 1) return false;
     const int64_t ntiles = (int64_t)((a.geo.ny + H - 1) / H) * nplanes;
     if (ntiles <= 0) return true;
     const int64_t cores = (int64_t)per_sm * sms;
     const int grid = (int)(ntiles < cores ? ntiles : cores);
-    kern<<<grid, BT + 32, smem, s>>>(a, static_cast<const T *>(src), static_cast<T *>(dst), nplanes, H, nst,
+    kern<<<grid, BT + 32, smem, s>>>(b, static_cast<const T *>(src), static_cast<T *>(dst), nplanes, H, nst,
                                      (int)(stage_bytes / (int64_t)sizeof(T)));
     return true;
     }

@@ -254,6 +254,7 @@ class Simulation:
         cfg.boundary_mode = BOUNDARY_MODES[boundary_mode] if isinstance(boundary_mode, str) else int(boundary_mode)
         self.cfg = cfg
         self.Q = stencil
+        self.device = device
         h = C.c_void_p()
         st = lbm_create(C.byref(cfg), C.byref(h))
         _check(st, None, "lbm_create")
@@ -295,12 +296,30 @@ class Simulation:
         self.close()
 
     # -- calls ------------------------------------------------------------------------
+    def _device_arg(self, t, numel: int, what: str):
+        """Validate a torch tensor passed as device memory: CUDA, float64, contiguous, on the handle's
+        device, exactly `numel` elements (the C library reads / writes that many doubles)."""
+        if not (hasattr(t, "is_cuda") and t.is_cuda):
+            raise TypeError(f"{what}: expected a numpy array (host) or a CUDA tensor (device)")
+        import torch
+        if t.dtype != torch.float64:
+            raise TypeError(f"{what}: device tensor must be float64, got {t.dtype}")
+        if not t.is_contiguous():
+            raise ValueError(f"{what}: device tensor must be contiguous")
+        if t.numel() != numel:
+            raise ValueError(f"{what}: device tensor has {t.numel()} elements, expected {numel}")
+        if t.device.index != self.device:
+            raise ValueError(f"{what}: tensor on cuda:{t.device.index}, handle on cuda:{self.device}")
+
     def init_equilibrium(self, rho, u):
         where = HOST if isinstance(rho, np.ndarray) else DEVICE
         if where == HOST:
             rho = np.ascontiguousarray(rho, np.float64)
             u = np.ascontiguousarray(u, np.float64)
             assert rho.size == self.cells and u.size == 3 * self.cells
+        else:
+            self._device_arg(rho, self.cells, "rho")
+            self._device_arg(u, 3 * self.cells, "u")
         _check(lbm_init_equilibrium(self.h, _ptr(rho), _ptr(u), where), self.h, "lbm_init_equilibrium")
 
     def init_random(self, seed: int, rho_amp: float, u_amp: float, profile: int = 0, profile_amp: float = 0.0):
@@ -326,6 +345,12 @@ class Simulation:
             rho = np.empty((self.nz_local, self.ny, self.nx))
             u = np.empty((3, self.nz_local, self.ny, self.nx))
         where = HOST if isinstance(rho, np.ndarray) else DEVICE
+        if where == HOST:
+            assert rho.dtype == np.float64 and u.dtype == np.float64 and rho.flags["C_CONTIGUOUS"] and u.flags["C_CONTIGUOUS"]
+            assert rho.size == self.cells and u.size == 3 * self.cells
+        else:
+            self._device_arg(rho, self.cells, "rho")
+            self._device_arg(u, 3 * self.cells, "u")
         _check(lbm_get_macroscopic(self.h, _ptr(rho), _ptr(u), where), self.h, "lbm_get_macroscopic")
         return rho, u
 
@@ -333,6 +358,10 @@ class Simulation:
         if out is None:
             out = np.empty((self.Q, self.nz_local, self.ny, self.nx))
         where = HOST if isinstance(out, np.ndarray) else DEVICE
+        if where == HOST:
+            assert out.dtype == np.float64 and out.flags["C_CONTIGUOUS"] and out.size == self.Q * self.cells
+        else:
+            self._device_arg(out, self.Q * self.cells, "out")
         _check(lbm_get_populations(self.h, _ptr(out), where, int(raw)), self.h, "lbm_get_populations")
         return out
 
@@ -341,6 +370,8 @@ class Simulation:
         if where == HOST:
             f = np.ascontiguousarray(f, np.float64)
             assert f.size == self.Q * self.cells
+        else:
+            self._device_arg(f, self.Q * self.cells, "f")
         _check(lbm_set_populations(self.h, _ptr(f), where, int(raw)), self.h, "lbm_set_populations")
 
     def populations_at(self, cells) -> np.ndarray:

@@ -568,11 +568,15 @@ def test_full_size_sampled_parity(name, boundary_mode, op):
 # Low-level kernel ABI on caller-owned (torch) device memory
 # -----------------------------------------------------------------------------------------
 @pytest.mark.parametrize("pattern", ["pull", "aa"])
-def test_low_level_kernel_abi(pattern):
+@pytest.mark.parametrize("nx,flag_offset", [(19, 0), (32, 0), (32, 1)])
+def test_low_level_kernel_abi(pattern, nx, flag_offset):
+    """Caller-owned torch memory. nx = 32 (rows of 16-byte multiples) reaches the TMA-staged AA even kernel,
+    whose flag rows move by bulk copy only from a 16-byte aligned flag base: flag_offset = 1 passes a
+    misaligned torch view of the flag bytes, which must fall back to global flag reads, not fault."""
     import ctypes as C
     import torch
     from paper_2001_11806_b200 import lbm as L
-    case = Case("ll", (19, 14, 9), 19, "trt", (1.6, 0.5), "f64", pattern=pattern, force=(1e-5, 0, 0),
+    case = Case("ll", (nx, 14, 9), 19, "trt", (1.6, 0.5), "f64", pattern=pattern, force=(1e-5, 0, 0),
                 geometry="obstacles", ubb=(0.02, 0.0, -0.01), steps=6)
     nx, ny, nz = case.shape
     d = O.Domain(case.method(), nx, ny, nz, flags=case.flags())
@@ -581,7 +585,8 @@ def test_low_level_kernel_abi(pattern):
     _, w, _ = O.stencil_arrays(19)
     g0 = torch.from_numpy(f0 - w[:, None, None, None]).cuda()
     g1 = g0.clone()
-    fl = torch.empty(nx * ny * nz, dtype=torch.uint8, device="cuda")
+    fl_buf = torch.empty(nx * ny * nz + 16, dtype=torch.uint8, device="cuda")
+    fl = fl_buf[flag_offset:flag_offset + nx * ny * nz]
     stream = torch.cuda.Stream()
     hf = np.ascontiguousarray(case.flags())
     assert L.lbm_prepare_flags(hf.ctypes.data, nx, ny, nz, 0, fl.data_ptr(), stream.cuda_stream) == 0
@@ -759,7 +764,8 @@ def test_low_level_push_and_collide_kernels(kind):
     _, w, _ = O.stencil_arrays(19)
     a = torch.from_numpy(f0 - w[:, None, None, None]).cuda()
     b = a.clone()
-    fl = torch.empty(nx * ny * nz, dtype=torch.uint8, device="cuda")
+    fl_buf = torch.empty(nx * ny * nz + 16, dtype=torch.uint8, device="cuda")
+    fl = fl_buf[flag_offset:flag_offset + nx * ny * nz]
     stream = torch.cuda.Stream()
     hf = np.ascontiguousarray(case.flags())
     assert L.lbm_prepare_flags(hf.ctypes.data, nx, ny, nz, 0, fl.data_ptr(), stream.cuda_stream) == 0

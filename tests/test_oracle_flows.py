@@ -261,8 +261,9 @@ def test_momentum_gain_per_step_periodic():
 @pytest.mark.parametrize("op,rates", [("srt", (1.8,)), ("mrt", (1.9, 1.0, 1.0, 1.0))])
 def test_shear_wave_viscosity(op, rates):
     """u_x = A sin(2 pi z / L) decays as exp(-nu k^2 t) with nu = (1/omega - 1/2)/3, omega the
-    shear rate. Fitted between two late times on a quasi-1D L = 128 lattice."""
-    L, A = 128, 1e-3
+    shear rate. Fitted between two late times on a quasi-1D L = 256 lattice; gate 1e-3 (SURVEY §8(c)
+    "Viscosity": <= 1e-3 at L >= 256; measured ~5e-5)."""
+    L, A = 256, 1e-3
     m = O.Method(Q=19, op=op, rates=rates, nthreads=1)
     d = O.Domain(m, 1, 1, L)
     z = np.arange(L)
@@ -280,7 +281,7 @@ def test_shear_wave_viscosity(op, rates):
     k = 2 * np.pi / L
     nu_fit = np.log(amps[200] / amps[1200]) / (k * k * 1000)
     nu = (1 / rates[0] - 0.5) / 3
-    assert abs(nu_fit / nu - 1) < 3e-3
+    assert abs(nu_fit / nu - 1) < 1e-3
 
 
 def test_slab_decomposition_bit_identical():
