@@ -28,10 +28,16 @@
  * passed to this API always use the canonical layout of the *local* slab (no ghost planes):
  * cell index i = x + nx * (y + ny * z_local). Vector fields are SoA [3][cells].
  *
- * Ownership: the library allocates and owns all device memory of a handle (populations, flags,
- * halo buffers), its streams' events, its CUDA graphs and its NCCL communicator. The caller may
- * pass its own compute stream (e.g. torch.cuda.current_stream().cuda_stream); the library then
- * launches every kernel of lbm_step on it. Output buffers are caller-allocated.
+ * Ownership ("raw pointer, together with shape and stride information"):
+ * the population arrays pdf[2], the device flag bytes and the halo staging buffer may be BORROWED
+ * from the caller (lbm_config.pdf_dev / flags_dev / halo_dev, e.g. torch tensors; sizes from
+ * lbm_buffer_sizes): the library then never allocates or frees them, and the caller keeps them
+ * alive until lbm_destroy returns. Left NULL, the library allocates them itself. The fused halo
+ * (LBM_HALO_FUSED) needs its population arrays in NCCL symmetric memory (ncclMemAlloc windows) and
+ * therefore always owns them. The library always owns its scratch memory, the boundary lists, its
+ * events, CUDA graphs and NCCL communicator. The caller may pass its own compute stream (e.g.
+ * torch.cuda.current_stream().cuda_stream); the library then launches every kernel of lbm_step on
+ * it. Output buffers are caller-allocated.
  *
  * Errors: every function returns an int status, 0 = LBM_OK, negative = error. No C++ exception
  * crosses the ABI. Asynchronous CUDA errors surface at the next lbm_step / lbm_sync.
@@ -182,7 +188,21 @@ typedef struct lbm_config {
                                rates[] is then ignored (D3Q19, compressible equilibrium, not in the
                                low-level kernel ABI) */
     double row_rates[15];
+    /* Borrowed device memory (NULL = allocated by the library). One slab per process only
+       (n_local_slabs <= 1) and not with LBM_HALO_FUSED (LBM_EUNSUPPORTED); every pointer 16-byte aligned
+       (LBM_EINVAL). Byte sizes from lbm_buffer_sizes. Contents on entry are ignored: lbm_create zeroes
+       the arrays and writes the prepared flag bytes. */
+    void *pdf_dev[2];       /* population arrays, layout of the low-level kernel ABI (SoA [q][zs][y][x] with
+                               the ghost planes, zero-centred, dtype elements); pdf_dev[1] for PULL/PUSH only */
+    uint8_t *flags_dev;     /* device flag bytes (one per storage cell, ghost planes included); with a flag field */
+    void *halo_dev;         /* halo staging: 4 faces of n_cross * nx * ny dtype elements; decomposed runs only */
 } lbm_config;
+
+/* Byte sizes of the device buffers a configuration needs (for borrowed memory, lbm_config.pdf_dev /
+ * flags_dev / halo_dev): out[0] = one population array, out[1] = the flag bytes (0 without a flag field),
+ * out[2] = the halo staging buffer (0 without a decomposition). Host-only; validates cfg like lbm_create
+ * (LBM_EINVAL / LBM_EUNSUPPORTED). */
+int lbm_buffer_sizes(const lbm_config *cfg, int64_t out[3]);
 
 typedef struct lbm_handle_s *lbm_handle;
 
@@ -214,7 +234,8 @@ int lbm_init_random(lbm_handle h, uint64_t seed, double rho_amp, double u_amp, i
 
 /* Advance n time steps (pull: n stream-pull-collide updates; AA: alternating even/odd). */
 int lbm_step(lbm_handle h, int64_t n);
-/* Block until all work of the handle finished; returns any pending asynchronous error. */
+/* Block until all work of the handle finished; returns any pending asynchronous error (CUDA: LBM_ECUDA;
+ * NCCL communicator errors from ncclCommGetAsyncError: LBM_ENCCL — also checked at every lbm_step). */
 int lbm_sync(lbm_handle h);
 int64_t lbm_steps_done(lbm_handle h);
 
@@ -243,6 +264,25 @@ int lbm_pack_face(lbm_handle h, int64_t z, int32_t dir, double *out, int32_t whe
 int lbm_kernel_time_ms(lbm_handle h, double *ms, int64_t *launches);
 /* Number of kernel launches issued by this handle since creation (all kernels). */
 int64_t lbm_launch_count(lbm_handle h);
+
+/* Phase timeline of the last timed step of a decomposed run (timing switched on with
+ * lbm_kernel_time_ms(h, NULL, NULL)): out = {boundary begin, boundary end, exchange begin, exchange end,
+ * interior begin, interior end} in ms relative to the boundary begin, from CUDA events recorded on the
+ * stream each phase runs on (the exchange on the comm stream with NCCL send/recv, so an exchange interval
+ * inside the interior interval is the measured overlap; the fused halo reports its LSA gate as the
+ * exchange). LBM_EINVAL if no decomposed step was timed. The same phases carry NVTX ranges
+ * ("lbm.boundary_planes", "lbm.exchange", "lbm.interior", "lbm.lsa_gate", "lbm.step") for nsys. */
+int lbm_step_phases_ms(lbm_handle h, double out[6]);
+
+/* Checkpoint / resume, bit-exact: the complete stored state of the handle is the array holding the current
+ * state of every local slab, ghost planes included, in the storage layout (lbm_state_bytes bytes, slabs in
+ * z order) plus the step count (which fixes the AA / EsoTwist parity). lbm_save_state copies it to `out`
+ * (host or device per `where`) and returns the step count; lbm_load_state restores it into a handle of the
+ * same configuration (any handle: a fresh one or the same), after which lbm_step continues exactly as
+ * the saved run would have. Asynchronous CUDA/NCCL errors surface as usual. */
+int64_t lbm_state_bytes(lbm_handle h);
+int lbm_save_state(lbm_handle h, void *out, int32_t where, int64_t *steps_done);
+int lbm_load_state(lbm_handle h, const void *in, int32_t where, int64_t steps_done);
 
 /* NCCL bootstrap: 128-byte unique id (call on rank 0, broadcast with torch.distributed). */
 int lbm_nccl_unique_id(uint8_t out[128]);
@@ -331,6 +371,17 @@ int lbm_set_link_velocities(lbm_handle h, const double *uw, int64_t n);
  * bandwidth in GB/s (CUDA events). Frees everything before returning. LBM_EOOM if the arrays do not fit. */
 int lbm_probe_copy(int32_t stencil, int32_t dtype, int32_t shifted, int64_t nx, int64_t ny, int64_t nz, int32_t reps,
                    int32_t device, double *gbs_out);
+
+/* Roofline probe "update-q" (the analogue of the paper's in-place update-19 probe, Table III):
+ * one q x nx x ny x nz array of the dtype, the AA-pattern access streams without collision, in place:
+ * mode 0 even (read f[x](q), write f[x](qbar)), 1 odd (read f[x - c_q](qbar), write f[x + c_q](q)),
+ * 2 alternating even/odd. Returns read + write GB/s: the ceiling of the AA / EsoTwist update kernels. */
+int lbm_probe_update(int32_t stencil, int32_t dtype, int32_t mode, int64_t nx, int64_t ny, int64_t nz, int32_t reps,
+                     int32_t device, double *gbs_out);
+/* ALU ceiling probe: TFLOP/s of independent FMA chains (DFMA for LBM_F64, FFMA for LBM_F32; 2 FLOP per
+ * FMA; 8 x 256 threads per SM, no memory traffic) — the peak the FP64-ALU-bound operators (cumulant,
+ * KBC, exact KBC) are reported against. */
+int lbm_probe_fma(int32_t dtype, int32_t device, double *tflops_out);
 
 /* ---- Kernel path of the bulk update kernels (process-wide; affects launches issued afterwards) ----
  * LBM_PATH_PLAIN : one thread per cell gathers its q populations straight into registers (ld.global.nc).

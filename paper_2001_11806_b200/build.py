@@ -59,6 +59,7 @@ def build(force: bool = False, verbose: bool = False, defines=(), out: str = OUT
     deps = _deps()
     if not force and not _stale(out, deps + [__file__]):
         return out
+    os.makedirs(os.path.dirname(os.path.abspath(out)), exist_ok=True)
     tag = "_".join(d.replace("=", "") for d in defines)
     obj_dir = OBJ + ("_" + tag if tag else "")
     os.makedirs(obj_dir, exist_ok=True)

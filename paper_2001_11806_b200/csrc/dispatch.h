@@ -61,6 +61,8 @@ void launch_unpack_masked(int Q, int dtype, const Geo &geo, void *f, int zs, int
 void launch_unpack_masked_eso(int Q, int dtype, const Geo &geo, void *f, int zs, int dir, const void *in, const uint8_t *flags,
                               int parity_done, cudaStream_t s);
 void launch_copyq(int Q, int dtype, bool shifted, const Geo &g, const void *src, void *dst, cudaStream_t s);
+void launch_updateq(int Q, int dtype, bool shifted, const Geo &g, void *f, cudaStream_t s);
+void launch_fma_probe(int dtype, int blocks, int iters, void *sink, cudaStream_t s);
 void launch_links(int Q, int dtype, const LinkArgs &a, void *f, cudaStream_t s);
 void launch_mark_near_wall(const Geo &geo, int nplanes, const uint8_t *in, uint8_t *out, cudaStream_t s);
 int staged_path();           // bulk kernel path: 0 auto, 1 plain, 2 staged (k_misc.cu)

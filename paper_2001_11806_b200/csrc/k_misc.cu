@@ -43,6 +43,20 @@ void launch_copyq(int Q, int dtype, bool shifted, const Geo &g, const void *src,
     }
 }
 
+void launch_updateq(int Q, int dtype, bool shifted, const Geo &g, void *f, cudaStream_t s) {
+    const dim3 block(256, 1, 1), grid((unsigned)((g.nx + 255) / 256), (unsigned)g.ny, (unsigned)g.nz);
+    if (shifted) {
+        LBM_DISPATCH(Q, dtype, (k_updateq<QQ, T, true><<<grid, block, 0, s>>>(g, static_cast<T *>(f))));
+    } else {
+        LBM_DISPATCH(Q, dtype, (k_updateq<QQ, T, false><<<grid, block, 0, s>>>(g, static_cast<T *>(f))));
+    }
+}
+
+void launch_fma_probe(int dtype, int blocks, int iters, void *sink, cudaStream_t s) {
+    if (dtype == 0) k_fma_probe<double><<<blocks, 256, 0, s>>>(0.999999, 1e-7, iters, static_cast<double *>(sink));
+    else k_fma_probe<float><<<blocks, 256, 0, s>>>(0.9999f, 1e-5f, iters, static_cast<float *>(sink));
+}
+
 void launch_links(int Q, int dtype, const LinkArgs &a, void *f, cudaStream_t s) {
     if (a.n == 0) return;
     const unsigned blocks = (a.n + 255) / 256;

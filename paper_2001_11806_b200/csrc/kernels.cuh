@@ -976,6 +976,45 @@ __global__ void __launch_bounds__(256) k_copyq(const Geo g, const T *__restrict_
     for (int q = 0; q < Q; ++q) dst[q * g.Sq + self] = v[q];
 }
 
+// In-place probe "update-q" (the analogue of the paper's update-19 probe, Table III): the
+// AA-pattern access streams of one array without collision. Even (SHIFTED = false): read f[x](q), write
+// f[x](qbar); odd (SHIFTED = true): read f[x - c_q](qbar), write f[x + c_q](q). Ceiling of the in-place
+// (AA / EsoTwist) update kernels, as copy-q is of the two-array ones.
+template <int Q, typename T, bool SHIFTED>
+__global__ void __launch_bounds__(256) k_updateq(const Geo g, T *__restrict__ f) {
+    using S = Stencil<Q>;
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    const int y = blockIdx.y * blockDim.y + threadIdx.y;
+    if (x >= g.nx || y >= g.ny) return;
+    const int zs = blockIdx.z;
+    const Nbr n = neighbours(g, x, y, zs);
+    const uint32_t self = nb_off(g, n, 0, 0, 0);
+    T v[Q];
+#pragma unroll
+    for (int q = 0; q < Q; ++q)
+        v[q] = f[(SHIFTED ? S::opp(q) : q) * g.Sq + (SHIFTED ? nb_off(g, n, -S::cx(q), -S::cy(q), -S::cz(q)) : self)];
+#pragma unroll
+    for (int q = 0; q < Q; ++q)
+        f[(SHIFTED ? q : S::opp(q)) * g.Sq + (SHIFTED ? nb_off(g, n, S::cx(q), S::cy(q), S::cz(q)) : self)] = v[q];
+}
+
+// ALU ceiling probe: independent fused multiply-add chains (8 per thread, no memory traffic) on a full
+// grid; 2 FLOP per FMA. Measures the DFMA / FFMA throughput the ALU-bound operators are judged against.
+template <typename T>
+__global__ void __launch_bounds__(256) k_fma_probe(T a, T b, int iters, T *__restrict__ sink) {
+    T x0 = T(threadIdx.x) * T(1e-3), x1 = x0 + T(1), x2 = x0 + T(2), x3 = x0 + T(3), x4 = x0 + T(4), x5 = x0 + T(5),
+      x6 = x0 + T(6), x7 = x0 + T(7);
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+            x0 = fma(x0, a, b); x1 = fma(x1, a, b); x2 = fma(x2, a, b); x3 = fma(x3, a, b);
+            x4 = fma(x4, a, b); x5 = fma(x5, a, b); x6 = fma(x6, a, b); x7 = fma(x7, a, b);
+        }
+    }
+    const T r = ((x0 + x1) + (x2 + x3)) + ((x4 + x5) + (x6 + x7));
+    if (r == T(-1.2345)) sink[threadIdx.x] = r;  // never true for the probe's inputs; keeps the chains live
+}
+
 // =======================================================================================
 // Flag preprocessing and diagnostics
 // =======================================================================================

@@ -4,6 +4,7 @@
 // readout and error handling. No C++ exception crosses the ABI.
 #include <cuda_runtime.h>
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <cmath>
 #include <cstdio>
@@ -36,11 +37,22 @@ struct Slab {
     std::vector<uint8_t> h_link_dir, h_link_type;
     void *halo[4] = {nullptr, nullptr, nullptr, nullptr};  // packed mode: send up, send down, recv below, recv above
     int cur = 0;          // index of the array holding the current state (pull)
+    bool own_pdf[2] = {true, true}, own_flags = true, own_halo = true;  // false: borrowed (lbm_config.*_dev)
 };
 
 struct Timing {
     bool on = false;
     std::vector<cudaEvent_t> ev;  // pairs
+    // phase timeline of the last timed decomposed step (lbm_step_phases_ms): boundary planes, exchange
+    // (comm stream with NCCL, compute stream otherwise), interior planes; begin/end events
+    cudaEvent_t ph[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+    bool ph_valid = false;
+};
+
+// NVTX ranges around the phases of a step (visible in an nsys / ncu timeline; no-ops without a tool)
+struct NvtxRange {
+    explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
 };
 
 }  // namespace
@@ -436,10 +448,19 @@ Phase step_phase(const lbm_handle_s *h, int odd) {
 // Decomposed steps run the boundary planes first, then exchange (NCCL: on the comm stream while the
 // interior planes update on the compute stream; loopback: device copies; fused: the boundary-plane
 // kernels store into the neighbours' planes after an LSA barrier); the next step waits for it.
+// phase event k of the timeline (timing mode only; k: 0/1 boundary, 2/3 exchange, 4/5 interior)
+void mark(lbm_handle_s *h, int k, cudaStream_t st) {
+    if (!h->timing.on) return;
+    if (!h->timing.ph[k]) cudaEventCreate(&h->timing.ph[k]);
+    cudaEventRecord(h->timing.ph[k], st);
+    if (k == 5) h->timing.ph_valid = true;
+}
+
 int step_once(lbm_handle_s *h) {
     cudaStream_t st = h->stream;
     const int odd = h->aa_parity;
     if (h->g == 0) {
+        NvtxRange r("lbm.step");
         Slab &s = h->slabs[0];
         links_before_step(h, s, st);
         launch_update(h, s, odd, 0, s.nz, 1, st, false);
@@ -449,16 +470,32 @@ int step_once(lbm_handle_s *h) {
     }
     const bool single = !two_arrays(h);  // the exchanged array: the single one, or the freshly written one
     const Phase ph = step_phase(h, odd);
-    auto bnd = [&](Slab &s, bool peer) { launch_update(h, s, odd, 0, 2, s.nz - 1, st, peer); };
-    auto inner = [&](Slab &s) { launch_update(h, s, odd, 1, s.nz - 2, 1, st, false); };
+    auto bnd = [&](Slab &s, bool peer) {
+        NvtxRange r("lbm.boundary_planes");
+        launch_update(h, s, odd, 0, 2, s.nz - 1, st, peer);
+    };
+    auto inner = [&](Slab &s) {
+        NvtxRange r("lbm.interior");
+        launch_update(h, s, odd, 1, s.nz - 2, 1, st, false);
+    };
     if (!h->use_nccl) {
         // loopback slabs on one GPU, one stream: boundary planes, exchange, interior
         for (Slab &s : h->slabs) links_before_step(h, s, st);
+        mark(h, 0, st);
         for (Slab &s : h->slabs) bnd(s, false);
-        int rc = single ? exchange_loopback(h, ph, [](const Slab &) { return 0; }, st)
+        mark(h, 1, st);
+        mark(h, 2, st);
+        int rc;
+        {
+            NvtxRange r("lbm.exchange");
+            rc = single ? exchange_loopback(h, ph, [](const Slab &) { return 0; }, st)
                         : exchange_loopback(h, ph, [](const Slab &s) { return 1 - s.cur; }, st);
+        }
         if (rc) return rc;
+        mark(h, 3, st);
+        mark(h, 4, st);
         for (Slab &s : h->slabs) inner(s);
+        mark(h, 5, st);
         for (Slab &s : h->slabs) links_after_step(h, s, odd, st);
         toggle_state(h);
         return LBM_OK;
@@ -468,22 +505,41 @@ int step_once(lbm_handle_s *h) {
         // gate (LSA barrier: every rank finished the previous step, so the stores into our planes are
         // done and the slots we overwrite are no longer read) -> boundary planes with peer stores ->
         // interior planes; one stream, no send/recv (index lists with AA / push are rejected at create)
-        fused_gate(h->fst, st);
+        mark(h, 2, st);
+        {
+            NvtxRange r("lbm.lsa_gate");
+            fused_gate(h->fst, st);
+        }
+        mark(h, 3, st);
         h->launches++;
         links_before_step(h, s, st);
+        mark(h, 0, st);
         bnd(s, true);
+        mark(h, 1, st);
+        mark(h, 4, st);
         inner(s);
+        mark(h, 5, st);
         toggle_state(h);
         return LBM_OK;
     }
     links_before_step(h, s, st);
+    mark(h, 0, st);
     bnd(s, false);
+    mark(h, 1, st);
     CUDA_TRY(h, cudaEventRecord(h->ev_bnd, st));
     CUDA_TRY(h, cudaStreamWaitEvent(h->comm_stream, h->ev_bnd, 0));
-    int rc = exchange_nccl(h, ph, single ? 0 : 1 - s.cur, h->comm_stream);
+    mark(h, 2, h->comm_stream);
+    int rc;
+    {
+        NvtxRange r("lbm.exchange");
+        rc = exchange_nccl(h, ph, single ? 0 : 1 - s.cur, h->comm_stream);
+    }
     if (rc) return rc;
+    mark(h, 3, h->comm_stream);
     CUDA_TRY(h, cudaEventRecord(h->ev_x, h->comm_stream));
+    mark(h, 4, st);
     inner(s);
+    mark(h, 5, st);
     CUDA_TRY(h, cudaStreamWaitEvent(st, h->ev_x, 0));  // the next step's boundary planes need the exchange
     links_after_step(h, s, odd, st);
     toggle_state(h);
@@ -577,6 +633,22 @@ int validate(const lbm_config *c) {
         return fail(nullptr, LBM_EUNSUPPORTED, "index-list boundaries with the AA / push patterns use the NCCL or loopback halo");
     if (c->equilibrium < LBM_EQ_COMPRESSIBLE || c->equilibrium > LBM_EQ_MOMENT_MATCHED)
         return fail(nullptr, LBM_EINVAL, "bad equilibrium");
+    // borrowed device buffers (lbm_config.pdf_dev / flags_dev / halo_dev)
+    const bool two = c->pattern == LBM_PULL || c->pattern == LBM_PUSH;
+    const bool borrowed = c->pdf_dev[0] || c->pdf_dev[1] || c->flags_dev || c->halo_dev;
+    if (borrowed) {
+        if (c->n_local_slabs > 1) return fail(nullptr, LBM_EUNSUPPORTED, "borrowed device buffers need one slab per process");
+        if (c->halo_mode == LBM_HALO_FUSED && (c->nranks > 1 || c->nccl_self))
+            return fail(nullptr, LBM_EUNSUPPORTED, "the fused halo owns its arrays (NCCL symmetric windows)");
+        if (two ? (c->pdf_dev[0] == nullptr) != (c->pdf_dev[1] == nullptr) : c->pdf_dev[1] != nullptr)
+            return fail(nullptr, LBM_EINVAL, "pdf_dev: give both arrays for PULL/PUSH, one (pdf_dev[0]) for AA/EsoTwist");
+        if (c->flags_dev && !c->flags) return fail(nullptr, LBM_EINVAL, "flags_dev without a flag field");
+        if (c->halo_dev && !(c->nranks > 1 || c->nccl_self))
+            return fail(nullptr, LBM_EINVAL, "halo_dev without a decomposition");
+        for (const void *p : {(const void *)c->pdf_dev[0], (const void *)c->pdf_dev[1], (const void *)c->flags_dev,
+                              (const void *)c->halo_dev})
+            if (reinterpret_cast<uintptr_t>(p) % 16 != 0) return fail(nullptr, LBM_EINVAL, "borrowed buffer not 16-byte aligned");
+    }
     if (c->equilibrium != LBM_EQ_COMPRESSIBLE && c->collision != LBM_SRT && c->collision != LBM_TRT &&
         c->collision != LBM_MRT && c->collision != LBM_IDENTITY &&
         !((c->collision == LBM_GEN_SRT || c->collision == LBM_GEN_TRT) && c->equilibrium == LBM_EQ_INCOMPRESSIBLE))
@@ -790,6 +862,77 @@ int lbm_probe_copy(int32_t stencil, int32_t dtype, int32_t shifted, int64_t nx, 
     return LBM_OK;
 }
 
+int lbm_probe_update(int32_t stencil, int32_t dtype, int32_t mode, int64_t nx, int64_t ny, int64_t nz, int32_t reps,
+                     int32_t device, double *gbs_out) {
+    if ((stencil != 19 && stencil != 27) || (dtype != LBM_F64 && dtype != LBM_F32) || mode < 0 || mode > 2 || nx < 1 ||
+        ny < 1 || nz < 1 || reps < 1 || !gbs_out || (double)nx * ny * nz >= 2147483647.0 || nx > 2147483647 / 256)
+        return LBM_EINVAL;
+    if (cudaSetDevice(device) != cudaSuccess) return LBM_ECUDA;
+    Geo g;
+    g.nx = (int)nx;
+    g.ny = (int)ny;
+    g.nz = (int)nz;
+    g.g = 0;
+    g.Sq = nx * ny * nz;
+    const size_t es = dtype == LBM_F64 ? 8 : 4;
+    const size_t bytes = (size_t)g.Sq * stencil * es;
+    void *a = nullptr;
+    if (cudaMalloc(&a, bytes) != cudaSuccess) return LBM_EOOM;
+    cudaStream_t s;
+    cudaEvent_t e0, e1;
+    cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaMemsetAsync(a, 0, bytes, s);
+    // mode 0: even pattern only, 1: odd pattern only, 2: alternating even/odd (the AA pair)
+    auto odd_of = [&](int r) { return mode == 2 ? (r & 1) != 0 : mode == 1; };
+    for (int w = 0; w < 2; ++w) launch_updateq(stencil, dtype, odd_of(w), g, a, s);
+    cudaEventRecord(e0, s);
+    for (int r = 0; r < reps; ++r) launch_updateq(stencil, dtype, odd_of(r), g, a, s);
+    cudaEventRecord(e1, s);
+    const cudaError_t err = cudaEventSynchronize(e1);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaStreamDestroy(s);
+    cudaFree(a);
+    if (err != cudaSuccess || ms <= 0.f) return LBM_ECUDA;
+    *gbs_out = 2.0 * (double)bytes * reps / (ms * 1e-3) / 1e9;
+    return LBM_OK;
+}
+
+int lbm_probe_fma(int32_t dtype, int32_t device, double *tflops_out) {
+    if ((dtype != LBM_F64 && dtype != LBM_F32) || !tflops_out) return LBM_EINVAL;
+    if (cudaSetDevice(device) != cudaSuccess) return LBM_ECUDA;
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    const int blocks = sms * 8, iters = dtype == LBM_F64 ? 2048 : 8192;  // 8 x 256 threads per SM
+    void *sink = nullptr;
+    if (cudaMalloc(&sink, 256 * 8) != cudaSuccess) return LBM_EOOM;
+    cudaStream_t s;
+    cudaEvent_t e0, e1;
+    cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    launch_fma_probe(dtype, blocks, iters / 8, sink, s);  // warm-up
+    cudaEventRecord(e0, s);
+    const int reps = 5;
+    for (int r = 0; r < reps; ++r) launch_fma_probe(dtype, blocks, iters, sink, s);
+    cudaEventRecord(e1, s);
+    const cudaError_t err = cudaEventSynchronize(e1);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaStreamDestroy(s);
+    cudaFree(sink);
+    if (err != cudaSuccess || ms <= 0.f) return LBM_ECUDA;
+    const double fmas = (double)blocks * 256 * iters * 16 * 8 * reps;
+    *tflops_out = 2.0 * fmas / (ms * 1e-3) / 1e12;
+    return LBM_OK;
+}
+
 int lbm_set_kernel_path(int32_t path) {
     if (path < LBM_PATH_AUTO || path > LBM_PATH_STAGED) return LBM_EINVAL;
     lbm::set_staged_path(path);
@@ -934,6 +1077,22 @@ int lbm_prepare_flags(const uint8_t *host_flags, int64_t nx, int64_t ny, int64_t
     const cudaError_t e = cudaStreamSynchronize(st);
     cudaFree(tmp);
     return e == cudaSuccess ? LBM_OK : LBM_ECUDA;
+}
+
+int lbm_buffer_sizes(const lbm_config *cfg, int64_t out[3]) {
+    if (!out) return LBM_EINVAL;
+    const int rc = validate(cfg);
+    if (rc) return rc;
+    const int P = cfg->nranks > 1 ? cfg->nranks : (cfg->n_local_slabs > 1 ? cfg->n_local_slabs : 1);
+    const bool exch = P > 1 || cfg->nccl_self;
+    const int64_t g = exch ? 1 : 0;
+    const int64_t planes = cfg->global[2] / P + 2 * g;
+    const int64_t esize = cfg->dtype == LBM_F64 ? 8 : 4;
+    const int64_t plane = cfg->global[0] * cfg->global[1];
+    out[0] = plane * planes * cfg->stencil * esize;
+    out[1] = cfg->flags ? plane * planes : 0;
+    out[2] = exch ? 4 * plane * (cfg->stencil == 19 ? 5 : 9) * esize : 0;
+    return LBM_OK;
 }
 
 int lbm_slab_plan(int64_t nz, int32_t nranks, int32_t rank, int64_t out[4]) {
@@ -1097,7 +1256,10 @@ int lbm_create(const lbm_config *cfg, lbm_handle *out) {
         const size_t bytes = (size_t)g.Sq * h->Q * h->esize;
         for (int a = 0; a < (two_arrays(h) ? 2 : 1); ++a) {
             if (h->fused) break;  // allocated in NCCL symmetric memory below
-            if (cudaMalloc(&s.pdf[a], bytes) != cudaSuccess) {
+            if (cfg->pdf_dev[a]) {  // borrowed (e.g. a torch tensor): used in place, never freed
+                s.pdf[a] = cfg->pdf_dev[a];
+                s.own_pdf[a] = false;
+            } else if (cudaMalloc(&s.pdf[a], bytes) != cudaSuccess) {
                 h->err = "cudaMalloc populations (" + std::to_string(bytes) + " B)";
                 return bail(LBM_EOOM);
             }
@@ -1105,11 +1267,15 @@ int lbm_create(const lbm_config *cfg, lbm_handle *out) {
         }
         if (h->g) {
             const size_t hb = (size_t)h->nx * h->ny * (h->Q == 19 ? 5 : 9) * h->esize;
-            for (int k = 0; k < 4; ++k)
-                if (cudaMalloc(&s.halo[k], hb) != cudaSuccess) {
+            for (int k = 0; k < 4; ++k) {
+                if (cfg->halo_dev) {
+                    s.halo[k] = static_cast<char *>(cfg->halo_dev) + k * hb;
+                    s.own_halo = false;
+                } else if (cudaMalloc(&s.halo[k], hb) != cudaSuccess) {
                     h->err = "cudaMalloc halo";
                     return bail(LBM_EOOM);
                 }
+            }
         }
         if (h->have_flags) {
             const int nplanes = s.nz + 2 * h->g;
@@ -1121,7 +1287,14 @@ int lbm_create(const lbm_config *cfg, lbm_handle *out) {
                 std::memcpy(&hf[(size_t)zs * h->nx * h->ny], cfg->flags + (size_t)zg * h->nx * h->ny, (size_t)h->nx * h->ny);
             }
             uint8_t *tmp = nullptr;
-            if (cudaMalloc(&s.flags, cells) != cudaSuccess || cudaMalloc(&tmp, cells) != cudaSuccess) {
+            if (cfg->flags_dev) {
+                s.flags = cfg->flags_dev;
+                s.own_flags = false;
+            } else if (cudaMalloc(&s.flags, cells) != cudaSuccess) {
+                h->err = "cudaMalloc flags";
+                return bail(LBM_EOOM);
+            }
+            if (cudaMalloc(&tmp, cells) != cudaSuccess) {
                 h->err = "cudaMalloc flags";
                 return bail(LBM_EOOM);
             }
@@ -1239,19 +1412,21 @@ int lbm_destroy(lbm_handle h) {
     if (h->graph) cudaGraphExecDestroy(h->graph);
     if (h->fused && h->comm) fused_teardown(h->comm, &h->fst);
     for (Slab &s : h->slabs) {
-        for (void *p : s.pdf)
-            if (p) {
-                if (h->fused) ncclMemFree(p);
-                else cudaFree(p);
+        for (int a = 0; a < 2; ++a)
+            if (s.pdf[a] && s.own_pdf[a]) {
+                if (h->fused) ncclMemFree(s.pdf[a]);
+                else cudaFree(s.pdf[a]);
             }
-        for (void *p : s.halo) if (p) cudaFree(p);
-        if (s.flags) cudaFree(s.flags);
+        if (s.own_halo)
+            for (void *p : s.halo) if (p) cudaFree(p);
+        if (s.flags && s.own_flags) cudaFree(s.flags);
         if (s.edges) cudaFree(s.edges);
         for (void *p : {(void *)s.link_wall, (void *)s.link_fluid, (void *)s.link_dir, (void *)s.link_term})
             if (p) cudaFree(p);
     }
     if (h->comm) ncclCommDestroy(h->comm);
     for (cudaEvent_t e : h->timing.ev) cudaEventDestroy(e);
+    for (cudaEvent_t e : h->timing.ph) if (e) cudaEventDestroy(e);
     if (h->ev_bnd) cudaEventDestroy(h->ev_bnd);
     if (h->ev_x) cudaEventDestroy(h->ev_x);
     if (h->comm_stream) cudaStreamDestroy(h->comm_stream);
@@ -1354,10 +1529,13 @@ int lbm_init_random(lbm_handle h, uint64_t seed, double rho_amp, double u_amp, i
     return init_common(h, a, nullptr, nullptr, LBM_DEVICE);
 }
 
+static int nccl_async_status(lbm_handle h);
+
 int lbm_step(lbm_handle h, int64_t n) {
     if (!h || n < 0) return LBM_EINVAL;
     cudaError_t pending = cudaGetLastError();
     if (pending != cudaSuccess) return fail(h, LBM_ECUDA, std::string("pending: ") + cudaGetErrorString(pending));
+    if (int rc = nccl_async_status(h)) return rc;
     if (h->timing.on) {
         for (cudaEvent_t e : h->timing.ev) cudaEventDestroy(e);
         h->timing.ev.clear();
@@ -1422,11 +1600,74 @@ int lbm_step(lbm_handle h, int64_t n) {
     return LBM_OK;
 }
 
+// Asynchronous NCCL failures (a peer died, a network/NVLink error): ncclCommGetAsyncError reports them
+// without blocking; surfaced at lbm_step and lbm_sync as LBM_ENCCL.
+static int nccl_async_status(lbm_handle h) {
+    if (!h->comm) return LBM_OK;
+    ncclResult_t async = ncclSuccess;
+    NCCL_TRY(h, ncclCommGetAsyncError(h->comm, &async));
+    if (async != ncclSuccess && async != ncclInProgress)
+        return fail(h, LBM_ENCCL, std::string("NCCL asynchronous error: ") + ncclGetErrorString(async));
+    return LBM_OK;
+}
+
 int lbm_sync(lbm_handle h) {
     if (!h) return LBM_EINVAL;
     CUDA_TRY(h, cudaStreamSynchronize(h->stream));
     CUDA_TRY(h, cudaStreamSynchronize(h->comm_stream));
     CUDA_TRY(h, cudaGetLastError());
+    return nccl_async_status(h);
+}
+
+int lbm_step_phases_ms(lbm_handle h, double out[6]) {
+    if (!h || !out) return LBM_EINVAL;
+    if (!h->timing.ph_valid) return fail(h, LBM_EINVAL, "no timed decomposed step (lbm_kernel_time_ms(h, NULL, NULL) first)");
+    CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+    CUDA_TRY(h, cudaStreamSynchronize(h->comm_stream));
+    for (int k = 0; k < 6; ++k) {
+        float t = 0.f;
+        CUDA_TRY(h, cudaEventElapsedTime(&t, h->timing.ph[0], h->timing.ph[k]));
+        out[k] = t;
+    }
+    return LBM_OK;
+}
+
+// ---- checkpoint / resume ---------------------------------------------------------------
+int64_t lbm_state_bytes(lbm_handle h) {
+    if (!h) return LBM_EINVAL;
+    int64_t n = 0;
+    for (const Slab &s : h->slabs) n += geo_of(h, s).Sq * h->Q * h->esize;
+    return n;
+}
+
+int lbm_save_state(lbm_handle h, void *out, int32_t where, int64_t *steps_done) {
+    if (!h || !out) return LBM_EINVAL;
+    const cudaMemcpyKind kind = where == LBM_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
+    char *dst = static_cast<char *>(out);
+    for (Slab &s : h->slabs) {
+        const size_t b = (size_t)geo_of(h, s).Sq * h->Q * h->esize;
+        CUDA_TRY(h, cudaMemcpyAsync(dst, s.pdf[cur_array(h, s)], b, kind, h->stream));
+        dst += b;
+    }
+    CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+    if (steps_done) *steps_done = h->steps;
+    return LBM_OK;
+}
+
+int lbm_load_state(lbm_handle h, const void *in, int32_t where, int64_t steps_done) {
+    if (!h || !in || steps_done < 0) return LBM_EINVAL;
+    const cudaMemcpyKind kind = where == LBM_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
+    const char *src = static_cast<const char *>(in);
+    for (Slab &s : h->slabs) {
+        const size_t b = (size_t)geo_of(h, s).Sq * h->Q * h->esize;
+        s.cur = 0;
+        CUDA_TRY(h, cudaMemcpyAsync(s.pdf[0], src, b, kind, h->stream));
+        if (two_arrays(h)) CUDA_TRY(h, cudaMemcpyAsync(s.pdf[1], s.pdf[0], b, cudaMemcpyDeviceToDevice, h->stream));
+        src += b;
+    }
+    h->steps = steps_done;
+    h->aa_parity = two_arrays(h) ? 0 : (int)(steps_done & 1);
+    CUDA_TRY(h, cudaStreamSynchronize(h->stream));
     return LBM_OK;
 }
 

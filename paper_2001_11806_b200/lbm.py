@@ -52,6 +52,7 @@ class lbm_config(C.Structure):
         ("block_x", C.c_int32), ("check_nan_every", C.c_int32), ("nccl_self", C.c_int32),
         ("equilibrium", C.c_int32), ("boundary_mode", C.c_int32),
         ("n_row_rates", C.c_int32), ("row_rates", C.c_double * 15),
+        ("pdf_dev", C.c_void_p * 2), ("flags_dev", C.c_void_p), ("halo_dev", C.c_void_p),
     ]
 
 
@@ -113,6 +114,13 @@ _SIGS = {
     "lbm_boundary_links": ([_P, _P, _P, _P, _I64], _I64),
     "lbm_set_link_velocities": ([_P, _P, _I64], C.c_int),
     "lbm_get_kernel_path": ([], _I32),
+    "lbm_buffer_sizes": ([C.POINTER(lbm_config), _P], C.c_int),
+    "lbm_step_phases_ms": ([_P, _P], C.c_int),
+    "lbm_probe_update": ([_I32, _I32, _I32, _I64, _I64, _I64, _I32, _I32, _P], C.c_int),
+    "lbm_probe_fma": ([_I32, _I32, _P], C.c_int),
+    "lbm_state_bytes": ([_P], _I64),
+    "lbm_save_state": ([_P, _P, _I32, _P], C.c_int),
+    "lbm_load_state": ([_P, _P, _I32, _I64], C.c_int),
 }
 for _name, (_args, _res) in _SIGS.items():
     _fn = getattr(_lib, _name)
@@ -146,6 +154,22 @@ def probe_copy(stencil: int, dtype: str, shifted: bool, shape, reps: int = 10, d
     nx, ny, nz = shape
     _check(lbm_probe_copy(stencil, DTYPES[dtype], int(shifted), nx, ny, nz, reps, device, C.byref(out)),
            what="lbm_probe_copy")
+    return out.value
+
+
+def probe_update(stencil: int, dtype: str, mode: int, shape, reps: int = 10, device: int = 0) -> float:
+    """Update-q (in-place AA streams) roofline probe (include/lbm.h lbm_probe_update): GB/s."""
+    out = C.c_double()
+    nx, ny, nz = shape
+    _check(lbm_probe_update(stencil, DTYPES[dtype], int(mode), nx, ny, nz, reps, device, C.byref(out)),
+           what="lbm_probe_update")
+    return out.value
+
+
+def probe_fma(dtype: str, device: int = 0) -> float:
+    """FMA-chain ALU ceiling (include/lbm.h lbm_probe_fma): TFLOP/s of DFMA (f64) or FFMA (f32)."""
+    out = C.c_double()
+    _check(lbm_probe_fma(DTYPES[dtype], device, C.byref(out)), what="lbm_probe_fma")
     return out.value
 
 
@@ -210,7 +234,10 @@ class Simulation:
                  n_local_slabs: int = 1, device: int = 0, stream: Optional[int] = None,
                  halo_mode: int = HALO_ZEROCOPY, use_graph: bool = False, block_x: int = 0,
                  check_nan_every: int = 0, nccl_self: bool = False, equilibrium: str = "compressible",
-                 boundary_mode: str = "flags"):
+                 boundary_mode: str = "flags", borrow: bool = False):
+        """borrow=True: the population arrays, device flag bytes and halo buffer are torch tensors owned by
+        this object and lent to the library (lbm_config.pdf_dev / flags_dev / halo_dev, include/lbm.h
+        "Ownership"); ``self.buffers`` holds them."""
         cfg = lbm_config()
         lbm_config_default(C.byref(cfg))
         nx, ny, nz = shape
@@ -252,6 +279,23 @@ class Simulation:
         cfg.nccl_self = int(nccl_self)
         cfg.equilibrium = EQUILIBRIA[equilibrium] if isinstance(equilibrium, str) else int(equilibrium)
         cfg.boundary_mode = BOUNDARY_MODES[boundary_mode] if isinstance(boundary_mode, str) else int(boundary_mode)
+        self.buffers = {}
+        if borrow:
+            import torch
+            sizes = np.zeros(3, np.int64)
+            _check(lbm_buffer_sizes(C.byref(cfg), sizes.ctypes.data), None, "lbm_buffer_sizes")
+            dev = torch.device("cuda", device)
+            narr = 2 if cfg.pattern in (PULL, PUSH) else 1
+            for a in range(narr):
+                t = torch.empty(int(sizes[0]), dtype=torch.uint8, device=dev)
+                self.buffers[f"pdf{a}"] = t
+                cfg.pdf_dev[a] = t.data_ptr()
+            if sizes[1]:
+                self.buffers["flags"] = torch.empty(int(sizes[1]), dtype=torch.uint8, device=dev)
+                cfg.flags_dev = self.buffers["flags"].data_ptr()
+            if sizes[2]:
+                self.buffers["halo"] = torch.empty(int(sizes[2]), dtype=torch.uint8, device=dev)
+                cfg.halo_dev = self.buffers["halo"].data_ptr()
         self.cfg = cfg
         self.Q = stencil
         self.device = device
@@ -390,6 +434,28 @@ class Simulation:
 
     def enable_kernel_timing(self):
         _check(lbm_kernel_time_ms(self.h, None, None), self.h, "lbm_kernel_time_ms")
+
+    def step_phases_ms(self):
+        """{boundary, exchange, interior}: (begin, end) in ms of the last timed decomposed step."""
+        out = np.zeros(6)
+        _check(lbm_step_phases_ms(self.h, out.ctypes.data), self.h, "lbm_step_phases_ms")
+        return {"boundary": (out[0], out[1]), "exchange": (out[2], out[3]), "interior": (out[4], out[5])}
+
+    def save_state(self):
+        """Checkpoint: (host bytes of the stored state incl. ghost planes, step count); bit-exact resume."""
+        n = int(lbm_state_bytes(self.h))
+        _check(n, self.h, "lbm_state_bytes")
+        buf = np.empty(n, np.uint8)
+        steps = C.c_int64()
+        _check(lbm_save_state(self.h, buf.ctypes.data, HOST, C.byref(steps)), self.h, "lbm_save_state")
+        return buf, steps.value
+
+    def load_state(self, buf: np.ndarray, steps: int):
+        n = int(lbm_state_bytes(self.h))
+        buf = np.ascontiguousarray(buf, np.uint8)
+        if buf.size != n:
+            raise ValueError(f"state has {buf.size} bytes, this handle needs {n}")
+        _check(lbm_load_state(self.h, buf.ctypes.data, HOST, int(steps)), self.h, "lbm_load_state")
 
     def kernel_time_ms(self):
         ms = C.c_double()

@@ -133,3 +133,48 @@ def test_binding_constants_match_header(L):
         assert v == int(defs["LBM_" + name.upper()]), name
     for name, v in L.BOUNDARY_MODES.items():
         assert v == int(defs["LBM_BOUNDARY_" + name.upper()]), name
+
+
+def _cfg(L, **kw):
+    import ctypes as C
+    cfg = L.lbm_config()
+    L.lbm_config_default(C.byref(cfg))
+    for k, v in kw.items():
+        if k == "pdf_dev":
+            cfg.pdf_dev[0], cfg.pdf_dev[1] = v
+        elif k == "global_":
+            cfg.global_[0], cfg.global_[1], cfg.global_[2] = v
+        else:
+            setattr(cfg, k, v)
+    return cfg
+
+
+def test_buffer_sizes_and_borrowed_buffer_validation(L):
+    """lbm_buffer_sizes (host-only) and the ownership rules of borrowed device buffers (include/lbm.h
+    "Ownership"): sizes follow the SoA layout with ghost planes; validation happens before any
+    CUDA call, so fake (never dereferenced) device addresses exercise it on a CPU-only host."""
+    import ctypes as C
+    out = np.zeros(3, np.int64)
+    cfg = _cfg(L, stencil=19, dtype=L.F64, global_=(32, 16, 8))
+    assert L.lbm_buffer_sizes(C.byref(cfg), out.ctypes.data) == 0
+    assert list(out) == [32 * 16 * 8 * 19 * 8, 0, 0]
+    fl = np.zeros((8, 16, 32), np.uint8)
+    fl[:, 0, :] = fl[:, -1, :] = 1
+    cfg = _cfg(L, stencil=27, dtype=L.F32, global_=(32, 16, 8), nccl_self=1, flags=fl.ctypes.data)
+    cfg.periodic[1] = 0
+    assert L.lbm_buffer_sizes(C.byref(cfg), out.ctypes.data) == 0
+    assert list(out) == [32 * 16 * 10 * 27 * 4, 32 * 16 * 10, 4 * 32 * 16 * 9 * 4]
+    bad = [
+        (dict(pdf_dev=(0x1000, 0)), -1),                               # pull needs both arrays
+        (dict(pattern=L.AA, pdf_dev=(0x1000, 0x2000)), -1),             # AA has one array
+        (dict(pdf_dev=(0x1008, 0x2000)), -1),                           # not 16-byte aligned
+        (dict(pdf_dev=(0x1000, 0x2000), n_local_slabs=2), -2),          # one slab per process
+        (dict(pdf_dev=(0x1000, 0x2000), nccl_self=1, halo_mode=L.HALO_FUSED), -2),  # fused owns its windows
+        (dict(flags_dev=0x1000), -1),                                   # no flag field
+        (dict(halo_dev=0x1000), -1),                                    # no decomposition
+    ]
+    for kw, code in bad:
+        cfg = _cfg(L, global_=(32, 16, 8), **kw)
+        assert L.lbm_buffer_sizes(C.byref(cfg), out.ctypes.data) == code, kw
+    cfg = _cfg(L, global_=(32, 16, 8), pattern=L.AA, pdf_dev=(0x1000, 0))
+    assert L.lbm_buffer_sizes(C.byref(cfg), out.ctypes.data) == 0

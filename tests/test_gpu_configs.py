@@ -122,13 +122,23 @@ def test_c2_full_size_500_steps_noise_free_vs_oracle_column():
     sim.close()
 
 
-def test_c2_full_size_viscosity_fit():
-    """The config itself (noise on): the x/y-averaged u_x projected on sin(2 pi z/512) decays with the
-    lattice viscosity of omega_shear = 1.9 (nu = (1/1.9 - 1/2)/3), fitted between steps 100 and 500
-    (after the initial non-equilibrium layer) to 1e-3."""
+@pytest.mark.parametrize("dtype,gate", [("f64", 1e-3), ("f32", 5e-2)])
+def test_c2_full_size_viscosity_fit(dtype, gate):
+    """The config's 512^3 wave with its noise: the x/y-averaged u_x projected on sin(2 pi z/512) decays with
+    the lattice viscosity of omega_shear = 1.9 (nu = (1/1.9 - 1/2)/3), fitted between steps 100 and 500
+    (after the initial non-equilibrium layer).
+
+    fp64 (the config's geometry, noise and steps in double precision): gate 1e-3 (measured 1.2e-5, the same
+    as the oracle column). fp32 (the config itself): the relative decay per step, nu k^2 = 1.3e-6, is only
+    ~22 fp32 ulps (eps = 6e-8), so the deterministic per-step rounding of the stored populations biases the
+    fitted rate by a few percent whatever the kernel does (a plain numpy fp32 column with the same
+    zero-centred formulation gives -1.6 %; G26); gate 5e-2. The fp32 state itself matches the oracle
+    to 2e-5 (test_c2_full_size_500_steps_noise_free_vs_oracle_column)."""
     base = FULL["c2"]
-    sim = make_sim(base)
-    init_sim(sim, base)
+    case = Case(base.name, base.shape, base.Q, base.op, base.rates, dtype, base.pattern, init=base.init,
+                rho_amp=base.rho_amp, u_amp=base.u_amp, steps=base.steps)
+    sim = make_sim(case)
+    init_sim(sim, case)
     amps = {}
     for t0, t1 in ((0, 100), (100, 500)):
         sim.step(t1 - t0)
@@ -137,7 +147,7 @@ def test_c2_full_size_viscosity_fit():
         del u
     nu_fit = CF.fitted_viscosity(amps[100], amps[500], 100, 500, base.shape[2])
     nu = CF.lattice_viscosity(base.rates[0])
-    assert abs(nu_fit / nu - 1) <= 1e-3, (nu_fit, nu)
+    assert abs(nu_fit / nu - 1) <= gate, (nu_fit, nu)
     sim.close()
 
 

@@ -764,8 +764,7 @@ def test_low_level_push_and_collide_kernels(kind):
     _, w, _ = O.stencil_arrays(19)
     a = torch.from_numpy(f0 - w[:, None, None, None]).cuda()
     b = a.clone()
-    fl_buf = torch.empty(nx * ny * nz + 16, dtype=torch.uint8, device="cuda")
-    fl = fl_buf[flag_offset:flag_offset + nx * ny * nz]
+    fl = torch.empty(nx * ny * nz, dtype=torch.uint8, device="cuda")
     stream = torch.cuda.Stream()
     hf = np.ascontiguousarray(case.flags())
     assert L.lbm_prepare_flags(hf.ctypes.data, nx, ny, nz, 0, fl.data_ptr(), stream.cuda_stream) == 0
@@ -863,3 +862,35 @@ def test_inline_boundaries_slabs_bit_identical(P):
         init_sim(s, case)
         s.step(case.steps)
     np.testing.assert_array_equal(one.populations(raw=True), many.populations(raw=True))
+
+
+# -----------------------------------------------------------------------------------------
+# Borrowed (caller-owned torch) device buffers (SURVEY §8(b) ownership)
+# -----------------------------------------------------------------------------------------
+@pytest.mark.parametrize("pattern,geometry,extra", [("pull", "channel", {}), ("aa", "obstacles", {}),
+                                                    ("esotwist", "channel", {}), ("push", "periodic", {}),
+                                                    ("pull", "channel", {"nccl_self": True, "halo_mode": 1}),
+                                                    ("aa", "periodic", {"nccl_self": True, "halo_mode": 0})])
+def test_borrowed_torch_buffers(pattern, geometry, extra):
+    """lbm_create on torch tensors (pdf_dev / flags_dev / halo_dev): same results as library-owned memory
+    (bit-exact) and as the oracle; the state lives in the caller's tensors."""
+    import torch
+    case = Case("borrow", (32, 16, 12), 19, "trt", (1.6, 0.5), "f64", pattern=pattern, force=(1e-5, 0, 0),
+                geometry=geometry, ubb=(0.02, -0.01, 0.03), steps=8)
+    own = make_sim(case, **extra)
+    lent = make_sim(case, borrow=True, **extra)
+    assert "pdf0" in lent.buffers and ("flags" in lent.buffers) == (case.flags() is not None)
+    assert ("halo" in lent.buffers) == bool(extra)
+    before = lent.buffers["pdf0"].clone()
+    for s in (own, lent):
+        init_sim(s, case)
+        s.step(case.steps)
+    mask = fluid_mask(case, 19)
+    np.testing.assert_array_equal(lent.populations(raw=True)[mask], own.populations(raw=True)[mask])
+    assert max_rel_err(lent.populations(), oracle_run(case), mask) <= TOL["f64"]
+    assert not torch.equal(before, lent.buffers["pdf0"])  # the library wrote into the caller's tensor
+    if pattern == "pull" and not extra:  # even step count: the state is in pdf_dev[0], canonical layout
+        st = lent.buffers["pdf0"].view(torch.float64).reshape(19, 12, 16, 32).cpu().numpy()
+        np.testing.assert_array_equal(st[mask], lent.populations(raw=True)[mask])
+    lent.close()
+    own.close()

@@ -1,0 +1,96 @@
+"""GPU tests of the runtime's auxiliary subsystems: bit-exact checkpoint / resume through the
+C ABI (lbm_save_state / lbm_load_state) for every storage pattern, decomposition and halo transport, and the
+phase timeline of decomposed steps (lbm_step_phases_ms; the NVTX ranges mark the same phases)."""
+import numpy as np
+import pytest
+
+from tests.gpu_common import Case, fluid_mask, init_sim, make_sim
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _lib():
+    from paper_2001_11806_b200 import build
+    build.build()
+    import torch
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+
+
+RESUME = [
+    ("pull", "channel", "flags", {}), ("pull", "cavity", "links", {}), ("aa", "obstacles", "flags", {}),
+    ("aa", "channel", "links", {}), ("esotwist", "channel", "flags", {}), ("push", "obstacles", "flags", {}),
+    ("pull", "channel", "flags", {"n_local_slabs": 2}), ("aa", "obstacles", "flags", {"n_local_slabs": 2, "halo_mode": 1}),
+    ("esotwist", "channel", "flags", {"n_local_slabs": 4}), ("push", "periodic", "flags", {"n_local_slabs": 2}),
+    ("pull", "channel", "flags", {"nccl_self": True, "halo_mode": 0}),
+    ("pull", "periodic", "flags", {"nccl_self": True, "halo_mode": 2}),
+    ("aa", "channel", "flags", {"nccl_self": True, "halo_mode": 2}),
+    ("esotwist", "obstacles", "flags", {"nccl_self": True, "halo_mode": 1}),
+]
+
+
+@pytest.mark.parametrize("k", [5, 6])
+@pytest.mark.parametrize("pattern,geometry,boundary_mode,extra", RESUME,
+                         ids=[f"{p}-{g}-{b}-{'-'.join(f'{a}{v}' for a, v in e.items()) or 'single'}" for p, g, b, e in RESUME])
+def test_resume_bit_exact(pattern, geometry, boundary_mode, extra, k):
+    """n steps == k steps, save, load into a FRESH handle, n - k steps (odd and even k: both AA / EsoTwist
+    parities), bit for bit on the stored state and the canonical populations."""
+    shape = (16, 16, 16) if geometry == "cavity" else (16, 12, 16)
+    case = Case("resume", shape, 19, "trt", (1.6, 0.5), "f64", pattern=pattern, force=(1e-5, 0, 0) if geometry != "cavity" else (0, 0, 0),
+                geometry=geometry, ubb=(0.02, -0.01, 0.03), steps=13)
+    kw = dict(boundary_mode=boundary_mode, **extra)
+    ref = make_sim(case, **kw)
+    init_sim(ref, case)
+    ref.step(case.steps)
+    a = make_sim(case, **kw)
+    init_sim(a, case)
+    a.step(k)
+    state, steps = a.save_state()
+    assert steps == k
+    a.close()
+    b = make_sim(case, **kw)
+    b.load_state(state, steps)
+    assert b.steps_done == k
+    b.step(case.steps - k)
+    mask = fluid_mask(case, 19)
+    np.testing.assert_array_equal(b.populations(raw=True)[mask], ref.populations(raw=True)[mask])
+    np.testing.assert_array_equal(b.populations()[mask], ref.populations()[mask])
+    s2, n2 = b.save_state()
+    s1, n1 = ref.save_state()
+    assert n1 == n2 == case.steps
+
+
+def test_resume_into_same_handle_rewinds():
+    """Loading an earlier checkpoint into the running handle rewinds it (the CUDA-graph cycle is re-captured
+    for the restored parity)."""
+    case = Case("rewind", (32, 8, 8), 19, "srt", (1.8,), "f64", pattern="aa", steps=9)
+    sim = make_sim(case, use_graph=True)
+    init_sim(sim, case)
+    sim.step(3)
+    st, n = sim.save_state()
+    sim.step(6)
+    first = sim.populations(raw=True)
+    sim.load_state(st, n)
+    sim.step(6)
+    np.testing.assert_array_equal(sim.populations(raw=True), first)
+
+
+@pytest.mark.parametrize("extra", [{"n_local_slabs": 2}, {"nccl_self": True, "halo_mode": 0},
+                                   {"nccl_self": True, "halo_mode": 1}, {"nccl_self": True, "halo_mode": 2}])
+def test_step_phase_timeline(extra):
+    """lbm_step_phases_ms: the boundary planes run first, the interior starts after them on the compute
+    stream, the exchange starts after the boundary planes (NCCL: on the comm stream, concurrently with the
+    interior); every interval is non-empty and well ordered."""
+    case = Case("phases", (128, 128, 32), 19, "trt", (1.6, 0.5), "f64", steps=3)
+    sim = make_sim(case, **extra)
+    init_sim(sim, case)
+    sim.step(2)
+    sim.enable_kernel_timing()
+    sim.step(1)
+    ph = sim.step_phases_ms()
+    (b0, b1), (x0, x1), (i0, i1) = ph["boundary"], ph["exchange"], ph["interior"]
+    assert b0 == 0.0 and b1 > b0 and i1 > i0 and x1 >= x0
+    assert i0 >= b1 - 1e-3
+    if extra.get("halo_mode") != 2:  # the fused halo's gate runs before the boundary planes
+        assert x0 >= b1 - 1e-3
+    sim.close()
