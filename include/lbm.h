@@ -130,9 +130,10 @@ extern "C" {
  *        flag-free and a separate boundary kernel writes, before each pull step (AA and push: after
  *        each step), the values the fluid cells stream from the wall cells. Per-link wall
  *        velocities: lbm_boundary_links / lbm_set_link_velocities. Wall cells are updated like fluid
- *        cells and hold meaningless values. Any slab decomposition (the link kernel also fills the wall
- *        slots of ghost planes, after the exchange); not with the fused halo for AA and push, not
- *        with EsoTwist (LBM_EUNSUPPORTED). */
+ *        cells and hold meaningless values. Every pattern (EsoTwist: the fix moves the departing slot of
+ *        the link's location L = b + c_q^- into its arriving slot, by parity) and any slab decomposition
+ *        (the link kernel also fills the wall slots of ghost planes, after the exchange; with the fused
+ *        halo a step's fix runs after the next LSA gate, and lbm_step ends with a closing gate). */
 /* LBM_BOUNDARY_INLINE: the flag field compiled into every cell's update ("compiled-in conditionals",
  *        P:1230-1238): the bulk kernels test the flags of all q neighbours of every cell, no separate
  *        boundary launch. Same results as LBM_BOUNDARY_FLAGS. Not with the fused halo (LBM_EUNSUPPORTED). */

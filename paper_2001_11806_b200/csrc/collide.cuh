@@ -458,25 +458,11 @@ __device__ __forceinline__ void kbc_pair_feq(int q, T drho, T rho, T ux, T uy, T
     ib = (A + ea) * rr;
 }
 
-// The populations are reached through an accessor g(q) -> T&: registers (collide_kbc), or the
-// thread's own slots of a staged shared-memory tile (collide_kbc_smem in staged.cuh, which keeps the
-// populations out of the register file). DS_CACHE keeps Delta_s per direction in registers; without it
-// Delta_s is recomputed from the five shear coefficients where needed (same arithmetic, same values).
-template <int Q, typename T, bool EXACT, bool DS_CACHE, typename G>
-__device__ __forceinline__ void collide_kbc_acc(G &&g, const Rates<T> &p) {
+template <int Q, typename T, bool EXACT = false>
+__device__ __forceinline__ void collide_kbc(T (&g)[Q], const Rates<T> &p) {
     using S = Stencil<Q>;
-    T drho = T(0), jx = T(0), jy = T(0), jz = T(0);
-#pragma unroll
-    for (int q = 0; q < Q; ++q) {  // moments0, through the accessor
-        const T v = g(q);
-        drho += v;
-        if (S::cx(q) > 0) jx += v;
-        if (S::cx(q) < 0) jx -= v;
-        if (S::cy(q) > 0) jy += v;
-        if (S::cy(q) < 0) jy -= v;
-        if (S::cz(q) > 0) jz += v;
-        if (S::cz(q) < 0) jz -= v;
-    }
+    T drho, jx, jy, jz;
+    moments0<Q, T>(g, drho, jx, jy, jz);
     const T rho = T(1) + drho;
     const T inv = T(1) / rho;
     const T ux = jx * inv, uy = jy * inv, uz = jz * inv;
@@ -484,7 +470,7 @@ __device__ __forceinline__ void collide_kbc_acc(G &&g, const Rates<T> &p) {
     const T w0 = T(S::w(0));
     const T eq0 = w0 * drho - w0 * rho * uu15;
     // g <- d = g - g_eq; shear coefficients a_k = <P_k, d> / N_k from the pair sums
-    g(0) -= eq0;
+    g[0] -= eq0;
     T a[5] = {T(0), T(0), T(0), T(0), T(0)};
 #pragma unroll
     for (int q = 1; q < Q; ++q) {
@@ -495,9 +481,9 @@ __device__ __forceinline__ void collide_kbc_acc(G &&g, const Rates<T> &p) {
             const T wr = w * rho;
             const T es = w * drho + wr * (T(4.5) * cu * cu - uu15);
             const T ea = wr * T(3) * cu;
-            g(q) -= es + ea;
-            g(b) -= es - ea;
-            const T dp = g(q) + g(b);
+            g[q] -= es + ea;
+            g[b] -= es - ea;
+            const T dp = g[q] + g[b];
 #pragma unroll
             for (int k = 0; k < 5; ++k) {
                 const int c = mrt_poly(k, S::cx(q), S::cy(q), S::cz(q));
@@ -510,32 +496,23 @@ __device__ __forceinline__ void collide_kbc_acc(G &&g, const Rates<T> &p) {
 #pragma unroll
     for (int k = 0; k < 5; ++k) a[k] *= T(mrt_inv_norm(k));
     // entropic products <Ds,Dh>_E, <Dh,Dh>_E with <x,y>_E = sum x y / f_eq, f_eq = w + g_eq (Eq. 19)
-    T sh = T(0), hh = g(0) * g(0) / (w0 + eq0);
-    T dsc[DS_CACHE ? Q : 1];
-    // Delta_s of pair (q, qbar): w_q sum_k P_k(c_q) a_k
-    auto ds_of = [&](int q) -> T {
-        const T w = T(S::w(q));
-        T acc = T(0);
-#pragma unroll
-        for (int k = 0; k < 5; ++k) {
-            const int c = mrt_poly(k, S::cx(q), S::cy(q), S::cz(q));
-            if (c == 1) acc += a[k];
-            else if (c == -1) acc -= a[k];
-            else if (c != 0) acc += T(c) * a[k];
-        }
-        return w * acc;
-    };
-    auto ds = [&](int q) -> T {
-        if constexpr (DS_CACHE) return dsc[q];
-        else return ds_of(q);
-    };
+    T sh = T(0), hh = g[0] * g[0] / (w0 + eq0);
+    T ds[Q];
 #pragma unroll
     for (int q = 1; q < Q; ++q) {
         if (q < S::opp(q)) {
             const int b = S::opp(q);
             const T w = T(S::w(q));
-            const T s = ds_of(q);
-            if constexpr (DS_CACHE) dsc[q] = s;
+            T acc = T(0);
+#pragma unroll
+            for (int k = 0; k < 5; ++k) {
+                const int c = mrt_poly(k, S::cx(q), S::cy(q), S::cz(q));
+                if (c == 1) acc += a[k];
+                else if (c == -1) acc -= a[k];
+                else if (c != 0) acc += T(c) * a[k];
+            }
+            const T s = w * acc;
+            ds[q] = s;
             const T cu = T(S::cx(q)) * ux + T(S::cy(q)) * uy + T(S::cz(q)) * uz;
             const T wr = w * rho;
             const T es = w * drho + wr * (T(4.5) * cu * cu - uu15);
@@ -545,7 +522,7 @@ __device__ __forceinline__ void collide_kbc_acc(G &&g, const Rates<T> &p) {
             const T rr = fast_rcp(A * A - ea * ea);
             const T iq = (A - ea) * rr;
             const T ib = (A + ea) * rr;
-            const T hq = g(q) - s, hb = g(b) - s;
+            const T hq = g[q] - s, hb = g[b] - s;
             sh += s * (hq * iq + hb * ib);
             hh += hq * hq * iq + hb * hb * ib;
         }
@@ -561,36 +538,36 @@ __device__ __forceinline__ void collide_kbc_acc(G &&g, const Rates<T> &p) {
             const T kw = T(1) - ws;
             // x_q(w) and positivity at a trial w; G and G' at w
             auto positive = [&](T w) {
-                bool ok = T(1) + (T(1) - w) * g(0) * i0 > T(0);
+                bool ok = T(1) + (T(1) - w) * g[0] * i0 > T(0);
 #pragma unroll
                 for (int q = 1; q < Q; ++q) {
                     if (q < S::opp(q)) {
                         const int b = S::opp(q);
                         T es, ea, iq, ib;
                         kbc_pair_feq<Q, T>(q, drho, rho, ux, uy, uz, uu15, es, ea, iq, ib);
-                        ok = ok && (T(1) + (kw * ds(q) + (T(1) - w) * (g(q) - ds(q))) * iq > T(0)) &&
-                             (T(1) + (kw * ds(q) + (T(1) - w) * (g(b) - ds(q))) * ib > T(0));
+                        ok = ok && (T(1) + (kw * ds[q] + (T(1) - w) * (g[q] - ds[q])) * iq > T(0)) &&
+                             (T(1) + (kw * ds[q] + (T(1) - w) * (g[b] - ds[q])) * ib > T(0));
                     }
                 }
                 return ok;
             };
             for (int it = 0; it < kMaxIt; ++it) {
                 const T km = T(1) - wh;
-                T x0 = km * g(0) * i0;
-                T G = g(0) * ln1p_kbc(x0);
+                T x0 = km * g[0] * i0;
+                T G = g[0] * ln1p_kbc(x0);
                 // G' only sets the convergence rate, not the root: approximate reciprocals suffice
-                T Gp = -g(0) * g(0) * i0 * fast_rcp(T(1) + x0);
+                T Gp = -g[0] * g[0] * i0 * fast_rcp(T(1) + x0);
                 // min_q f'/f_eq and max_q |Dh/f_eq| bound f' at the next iterate: f'(w - s)/f_eq =
                 // 1 + x + s Dh/f_eq stays positive when min(1 + x) > |s| max|Dh/f_eq|
-                T lo = T(1) + x0, hi = fabs(g(0) * i0);
+                T lo = T(1) + x0, hi = fabs(g[0] * i0);
 #pragma unroll
                 for (int q = 1; q < Q; ++q) {
                     if (q < S::opp(q)) {
                         const int b = S::opp(q);
                         T es, ea, iq, ib;
                         kbc_pair_feq<Q, T>(q, drho, rho, ux, uy, uz, uu15, es, ea, iq, ib);
-                        const T hq = g(q) - ds(q), hb = g(b) - ds(q);
-                        const T xq = (kw * ds(q) + km * hq) * iq, xb = (kw * ds(q) + km * hb) * ib;
+                        const T hq = g[q] - ds[q], hb = g[b] - ds[q];
+                        const T xq = (kw * ds[q] + km * hq) * iq, xb = (kw * ds[q] + km * hb) * ib;
                         G += hq * ln1p_kbc(xq) + hb * ln1p_kbc(xb);
                         Gp -= hq * hq * iq * fast_rcp(T(1) + xq) + hb * hb * ib * fast_rcp(T(1) + xb);
                         lo = fmin(lo, fmin(T(1) + xq, T(1) + xb));
@@ -616,7 +593,7 @@ __device__ __forceinline__ void collide_kbc_acc(G &&g, const Rates<T> &p) {
     }
     // f' = f_eq + (1 - w_h) d + (w_h - w_s) Ds
     const T kd = T(1) - wh, ks = wh - ws;
-    g(0) = eq0 + kd * g(0);
+    g[0] = eq0 + kd * g[0];
 #pragma unroll
     for (int q = 1; q < Q; ++q) {
         if (q < S::opp(q)) {
@@ -626,16 +603,11 @@ __device__ __forceinline__ void collide_kbc_acc(G &&g, const Rates<T> &p) {
             const T wr = w * rho;
             const T es = w * drho + wr * (T(4.5) * cu * cu - uu15);
             const T ea = wr * T(3) * cu;
-            const T sk = ks * ds(q);
-            g(q) = (es + ea) + kd * g(q) + sk;
-            g(b) = (es - ea) + kd * g(b) + sk;
+            const T sk = ks * ds[q];
+            g[q] = (es + ea) + kd * g[q] + sk;
+            g[b] = (es - ea) + kd * g[b] + sk;
         }
     }
-}
-
-template <int Q, typename T, bool EXACT = false>
-__device__ __forceinline__ void collide_kbc(T (&g)[Q], const Rates<T> &p) {
-    collide_kbc_acc<Q, T, EXACT, true>([&](int q) -> T & { return g[q]; }, p);
 }
 
 // ---------------------------------------------------------------------------------------

@@ -98,6 +98,15 @@ struct Nbr {
 #define LBM_ASSERT(c) ((void)0)
 #endif
 
+// Fused halo: a thread that stored into a neighbour's window over NVLink makes those stores visible at
+// system scope before it exits; the next step's LSA gate (k_fused.cu) then orders them before every
+// rank's next reads. (Kernel completion alone is not specified to order peer-GPU stores for readers on
+// the other GPU; the fence makes the release explicit, and costs only the two boundary planes.)
+template <bool PEER>
+__device__ __forceinline__ void peer_fence() {
+    if constexpr (PEER) __threadfence_system();
+}
+
 __device__ __forceinline__ Nbr neighbours(const Geo &g, int x, int y, int zs) {
     LBM_ASSERT(x >= 0 && x < g.nx && y >= 0 && y < g.ny);
     LBM_ASSERT(g.g ? (zs >= 1 && zs <= g.nz) : (zs >= 0 && zs < g.nz));  // only interior planes update
@@ -232,6 +241,7 @@ __global__ void __launch_bounds__(256, (MinBlocks<Q, OP, T>::pull)) k_pull(const
     if (x >= a.geo.nx || y >= a.geo.ny) return;
     const int zs = a.z_begin + (int)blockIdx.z * a.z_step + a.geo.g;
     pull_cell<Q, OP, T, FM, FORCE, PEER>(a, src, dst, x, y, zs);
+    peer_fence<PEER>();
 }
 
 // Near-wall fluid cells from a list of storage cell indices (one thread per listed cell).
@@ -246,6 +256,7 @@ __global__ void __launch_bounds__(128) k_pull_edges(const StepArgs a, const T *_
     const int zs = (int)(c / plane);
     const uint32_t r = c - (uint32_t)zs * plane;
     pull_cell<Q, OP, T, FM_EDGE, FORCE, PEER>(a, src, dst, (int)(r % (uint32_t)a.geo.nx), (int)(r / (uint32_t)a.geo.nx), zs);
+    peer_fence<PEER>();
 }
 
 // =======================================================================================
@@ -305,6 +316,7 @@ __global__ void __launch_bounds__(256, (MinBlocks<Q, OP, T>::aa)) k_aa_even(cons
     const int y = blockIdx.y * blockDim.y + threadIdx.y;
     if (x >= a.geo.nx || y >= a.geo.ny) return;
     aa_even_cell<Q, OP, T, FLAGS, FORCE, PEER>(a, f, x, y, a.z_begin + (int)blockIdx.z * a.z_step + a.geo.g);
+    peer_fence<PEER>();
 }
 
 template <int Q, int OP, typename T, int FM, bool FORCE, bool PEER = false>
@@ -383,6 +395,7 @@ __global__ void __launch_bounds__(256, (MinBlocks<Q, OP, T>::aa)) k_aa_odd(const
     if (x >= a.geo.nx || y >= a.geo.ny) return;
     const int zs = a.z_begin + (int)blockIdx.z * a.z_step + a.geo.g;
     aa_odd_cell<Q, OP, T, FM, FORCE, PEER>(a, f, x, y, zs);
+    peer_fence<PEER>();
 }
 
 template <int Q, int OP, typename T, bool FORCE, bool PEER = false>
@@ -396,6 +409,7 @@ __global__ void __launch_bounds__(128) k_aa_odd_edges(const StepArgs a, T *__res
     const int zs = (int)(c / plane);
     const uint32_t r = c - (uint32_t)zs * plane;
     aa_odd_cell<Q, OP, T, FM_EDGE, FORCE, PEER>(a, f, (int)(r % (uint32_t)a.geo.nx), (int)(r / (uint32_t)a.geo.nx), zs);
+    peer_fence<PEER>();
 }
 
 // =======================================================================================
@@ -467,6 +481,7 @@ __global__ void __launch_bounds__(256, (MinBlocks<Q, OP, T>::aa)) k_eso(const St
     const int y = blockIdx.y * blockDim.y + threadIdx.y;
     if (x >= a.geo.nx || y >= a.geo.ny) return;
     eso_cell<Q, OP, T, FM, FORCE, ODD, PEER>(a, f, x, y, a.z_begin + (int)blockIdx.z * a.z_step + a.geo.g);
+    peer_fence<PEER>();
 }
 
 template <int Q, int OP, typename T, bool FORCE, bool ODD, bool PEER = false>
@@ -479,6 +494,7 @@ __global__ void __launch_bounds__(128) k_eso_edges(const StepArgs a, T *f, const
     const int zs = (int)(c / plane);
     const uint32_t r = c - (uint32_t)zs * plane;
     eso_cell<Q, OP, T, FM_EDGE, FORCE, ODD, PEER>(a, f, (int)(r % (uint32_t)a.geo.nx), (int)(r / (uint32_t)a.geo.nx), zs);
+    peer_fence<PEER>();
 }
 
 // =======================================================================================
@@ -538,6 +554,7 @@ __global__ void __launch_bounds__(256, (MinBlocks<Q, OP, T>::aa)) k_push(const S
     const int y = blockIdx.y * blockDim.y + threadIdx.y;
     if (x >= a.geo.nx || y >= a.geo.ny) return;
     push_cell<Q, OP, T, FM, FORCE, PEER>(a, src, dst, x, y, a.z_begin + (int)blockIdx.z * a.z_step + a.geo.g);
+    peer_fence<PEER>();
 }
 
 template <int Q, int OP, typename T, bool FORCE, bool PEER = false>
@@ -551,6 +568,7 @@ __global__ void __launch_bounds__(128) k_push_edges(const StepArgs a, const T *_
     const int zs = (int)(c / plane);
     const uint32_t r = c - (uint32_t)zs * plane;
     push_cell<Q, OP, T, FM_EDGE, FORCE, PEER>(a, src, dst, (int)(r % (uint32_t)a.geo.nx), (int)(r / (uint32_t)a.geo.nx), zs);
+    peer_fence<PEER>();
 }
 
 // collision only, in place (same slot), fluid cells of the launched planes
@@ -902,11 +920,16 @@ __global__ void k_unpack_masked(const Geo geo, T *__restrict__ f, int zs, int di
 //   mode 0, pull, before the step:    src[b](q)    = src[x](qbar) + term
 //   mode 1, AA, after the even step:  a[b](qbar)   = a[x](q) + term     (read by x in the odd step)
 //   mode 2, AA, after the odd step:   a[x](q)      = a[b](qbar) + term  (x's push toward b, bounced)
+//   EsoTwist (G23; the link's populations live at L = b + c_q^- = x - c_q^+, passed in `fluid`): x's
+//   departing qbar (toward b) was written at (L, q) after an even step and at (L, qbar) after an odd one;
+//   the next step reads x's arriving q at the other slot of L:
+//   mode 3, EsoTwist, after even:     a[L](qbar)   = a[L](q) + term
+//   mode 4, EsoTwist, after odd:      a[L](q)      = a[L](qbar) + term
 // Every slot is written by one link and read by no other link of the same launch.
 // =======================================================================================
 struct LinkArgs {
     int64_t Sq;
-    const uint32_t *wall, *fluid;  // storage cell indices
+    const uint32_t *wall, *fluid;  // storage cell indices (EsoTwist: `fluid` holds the link location L)
     const uint8_t *dir;            // q
     const double *term;            // per-link UBB term
     uint32_t n;
@@ -925,7 +948,9 @@ __global__ void k_links(const LinkArgs a, T *__restrict__ f) {
     const T t = T(a.term[i]);
     if (a.mode == 0) f[q * a.Sq + b] = f[qb * a.Sq + x] + t;
     else if (a.mode == 1) f[qb * a.Sq + b] = f[q * a.Sq + x] + t;
-    else f[q * a.Sq + x] = f[qb * a.Sq + b] + t;
+    else if (a.mode == 2) f[q * a.Sq + x] = f[qb * a.Sq + b] + t;
+    else if (a.mode == 3) f[qb * a.Sq + x] = f[q * a.Sq + x] + t;
+    else f[q * a.Sq + x] = f[qb * a.Sq + x] + t;
 }
 
 // EsoTwist exchange with walls: slot r of location L (storage plane zs) was written by the cell that

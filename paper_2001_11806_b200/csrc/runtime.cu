@@ -85,6 +85,7 @@ struct lbm_handle_s {
     bool fused = false;       // halo through NVLink peer stores (LBM_HALO_FUSED)
     bool links = false;       // index-list boundaries: flag-free update kernels + link kernel
     bool inline_bc = false;   // compiled-in boundaries: every cell tests its neighbours' flags, no edge kernel
+    int links_pending = -1;   // fused halo + index lists: deferred link fix of the last step (parity | array << 1)
     FusedState fst;
     std::string err;
     dim3 block;
@@ -174,7 +175,8 @@ void launch_edges(lbm_handle_s *h, Slab &s, const StepArgs &a, EdgeLaunch fn, co
         for (int k = 0; k < nplanes; ++k) run(z_begin + k * z_step, z_begin + k * z_step + 1);
 }
 
-// index-list boundary kernel (mode 0: pull, before the step; 1: AA after even; 2: AA after odd)
+// index-list boundary kernel (mode 0: pull, before the step; 1: AA after even; 2: AA after odd;
+// 3 / 4: EsoTwist after even / odd)
 void launch_links_fix(lbm_handle_s *h, Slab &s, void *f, int mode, cudaStream_t st) {
     if (!h->links || s.h_link_wall.empty()) return;
     LinkArgs a;
@@ -416,14 +418,24 @@ void launch_update(lbm_handle_s *h, Slab &s, int odd, int z_begin, int nplanes, 
 }
 
 // index-list boundaries: pull fixes the wall slots it is about to stream from (before the step, after
-// the previous exchange); AA (after even: pre-odd, after odd: post-odd) and push fix after the step's
-// exchange. EsoTwist has no link mode.
+// the previous exchange); AA (after even: pre-odd, after odd: post-odd), EsoTwist (the arriving slot of
+// the link location from the departing one, by parity) and push fix after the step's exchange.
+// `written` = the array the step wrote (push: the fresh array; AA / EsoTwist: the single one).
 void links_before_step(lbm_handle_s *h, Slab &s, cudaStream_t st) {
     if (h->cfg.pattern == LBM_PULL) launch_links_fix(h, s, s.pdf[s.cur], 0, st);
 }
-void links_after_step(lbm_handle_s *h, Slab &s, int odd, cudaStream_t st) {
+void links_fix_step(lbm_handle_s *h, Slab &s, int odd, int written, cudaStream_t st) {
     if (h->cfg.pattern == LBM_AA) launch_links_fix(h, s, s.pdf[0], odd ? 2 : 1, st);
-    else if (h->cfg.pattern == LBM_PUSH) launch_links_fix(h, s, s.pdf[1 - s.cur], 2, st);
+    else if (h->cfg.pattern == LBM_ESOTWIST) launch_links_fix(h, s, s.pdf[0], odd ? 4 : 3, st);
+    else if (h->cfg.pattern == LBM_PUSH) launch_links_fix(h, s, s.pdf[written], 2, st);
+}
+void links_after_step(lbm_handle_s *h, Slab &s, int odd, cudaStream_t st) { links_fix_step(h, s, odd, 1 - s.cur, st); }
+// Fused halo: a step's link fix must follow the neighbours' peer stores of that step, i.e. the next LSA
+// gate; it is deferred to after the next step's gate, or to the closing gate at the end of lbm_step.
+void links_deferred(lbm_handle_s *h, Slab &s, cudaStream_t st) {
+    if (h->links_pending < 0) return;
+    links_fix_step(h, s, h->links_pending & 1, h->links_pending >> 1, st);
+    h->links_pending = -1;
 }
 
 void toggle_state(lbm_handle_s *h) {
@@ -503,8 +515,9 @@ int step_once(lbm_handle_s *h) {
     Slab &s = h->slabs[0];
     if (h->fused) {
         // gate (LSA barrier: every rank finished the previous step, so the stores into our planes are
-        // done and the slots we overwrite are no longer read) -> boundary planes with peer stores ->
-        // interior planes; one stream, no send/recv (index lists with AA / push are rejected at create)
+        // done and the slots we overwrite are no longer read) -> the previous step's deferred link fix
+        // (index lists with AA / EsoTwist / push) -> boundary planes with peer stores -> interior planes;
+        // one stream, no send/recv
         mark(h, 2, st);
         {
             NvtxRange r("lbm.lsa_gate");
@@ -512,6 +525,7 @@ int step_once(lbm_handle_s *h) {
         }
         mark(h, 3, st);
         h->launches++;
+        links_deferred(h, s, st);
         links_before_step(h, s, st);
         mark(h, 0, st);
         bnd(s, true);
@@ -519,6 +533,7 @@ int step_once(lbm_handle_s *h) {
         mark(h, 4, st);
         inner(s);
         mark(h, 5, st);
+        if (h->links && h->cfg.pattern != LBM_PULL) h->links_pending = odd | ((1 - s.cur) << 1);
         toggle_state(h);
         return LBM_OK;
     }
@@ -585,8 +600,6 @@ int validate(const lbm_config *c) {
     if (c->collision < 0 || c->collision > LBM_GEN_SMAGORINSKY) return fail(nullptr, LBM_EINVAL, "bad collision");
     if (c->dtype != LBM_F64 && c->dtype != LBM_F32) return fail(nullptr, LBM_EINVAL, "bad dtype");
     if (c->pattern < LBM_PULL || c->pattern > LBM_PUSH) return fail(nullptr, LBM_EINVAL, "bad pattern");
-    if (c->pattern == LBM_ESOTWIST && c->boundary_mode == LBM_BOUNDARY_LINKS)
-        return fail(nullptr, LBM_EUNSUPPORTED, "index-list boundaries are implemented for the pull and AA patterns");
     const int need[] = {1, 2, 1, 1, 0, 2, 1, 1, 1, 2, 1, 2};
     const int need_n = (c->collision == LBM_MRT && c->n_row_rates == 15) ? 0 : need[c->collision];
     if (c->n_rates < need_n || c->n_rates > 8) return fail(nullptr, LBM_EINVAL, "wrong number of rates");
@@ -628,9 +641,6 @@ int validate(const lbm_config *c) {
         return fail(nullptr, LBM_EINVAL, "bad boundary_mode");
     if (c->boundary_mode == LBM_BOUNDARY_INLINE && c->halo_mode == LBM_HALO_FUSED && (c->nranks > 1 || c->nccl_self))
         return fail(nullptr, LBM_EUNSUPPORTED, "compiled-in (inline) boundaries use the NCCL or loopback halo");
-    if (c->boundary_mode == LBM_BOUNDARY_LINKS && (c->pattern == LBM_AA || c->pattern == LBM_PUSH) &&
-        c->halo_mode == LBM_HALO_FUSED)
-        return fail(nullptr, LBM_EUNSUPPORTED, "index-list boundaries with the AA / push patterns use the NCCL or loopback halo");
     if (c->equilibrium < LBM_EQ_COMPRESSIBLE || c->equilibrium > LBM_EQ_MOMENT_MATCHED)
         return fail(nullptr, LBM_EINVAL, "bad equilibrium");
     // borrowed device buffers (lbm_config.pdf_dev / flags_dev / halo_dev)
@@ -1340,7 +1350,17 @@ int lbm_create(const lbm_config *cfg, lbm_handle *out) {
                         const size_t nb = ((size_t)zz * h->ny + yy) * h->nx + xx;
                         if (hf[nb] & 3) continue;
                         s.h_link_wall.push_back(b);
-                        lf.push_back((uint32_t)nb);
+                        if (cfg->pattern == LBM_ESOTWIST) {
+                            // EsoTwist: the link's populations live at L = b + c_q^- (= x - c_q^+, G23), the
+                            // location the fix works on (x, y wrap; z stays inside the storage planes)
+                            int64_t lz = zs + (kC27[q][2] < 0 ? kC27[q][2] : 0);
+                            if (h->g == 0) lz = (lz + s.nz) % s.nz;
+                            const int64_t lx = (x + (kC27[q][0] < 0 ? -1 : 0) + h->nx) % h->nx;
+                            const int64_t ly = (y + (kC27[q][1] < 0 ? -1 : 0) + h->ny) % h->ny;
+                            lf.push_back((uint32_t)(((size_t)lz * h->ny + ly) * h->nx + lx));
+                        } else {
+                            lf.push_back((uint32_t)nb);
+                        }
                         s.h_link_dir.push_back((uint8_t)q);
                         s.h_link_type.push_back(hf[b] & 3);
                     }
@@ -1495,6 +1515,7 @@ static int init_common(lbm_handle h, InitArgs &a, const double *rho, const doubl
     }
     h->steps = 0;
     h->aa_parity = 0;
+    h->links_pending = -1;
     if (a.mode == 0 && h->g) {
         int rc = exchange_current(h);
         if (rc) return rc;
@@ -1595,6 +1616,11 @@ int lbm_step(lbm_handle h, int64_t n) {
             if (flag) return fail(h, LBM_ENAN, "NaN detected after step " + std::to_string(h->steps));
         }
     }
+    if (h->fused && h->links_pending >= 0) {  // closing gate: the state of the call is complete on return
+        fused_gate(h->fst, h->stream);
+        h->launches++;
+        links_deferred(h, h->slabs[0], h->stream);
+    }
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return fail(h, LBM_ECUDA, std::string("launch: ") + cudaGetErrorString(e));
     return LBM_OK;
@@ -1667,6 +1693,7 @@ int lbm_load_state(lbm_handle h, const void *in, int32_t where, int64_t steps_do
     }
     h->steps = steps_done;
     h->aa_parity = two_arrays(h) ? 0 : (int)(steps_done & 1);
+    h->links_pending = -1;
     CUDA_TRY(h, cudaStreamSynchronize(h->stream));
     return LBM_OK;
 }
@@ -1787,6 +1814,7 @@ int lbm_set_populations(lbm_handle h, const double *in, int32_t where, int32_t r
     }
     int64_t off = 0;
     h->aa_parity = 0;
+    h->links_pending = -1;
     for (Slab &s : h->slabs) {
         ReadArgs r;
         std::memset(&r, 0, sizeof(r));

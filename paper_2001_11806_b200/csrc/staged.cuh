@@ -47,15 +47,6 @@ __host__ __device__ constexpr int src_slot(int mode, int q) {
 #endif
 constexpr int kStagedBT = LBM_STAGED_BT;
 
-// Operators whose staged consumer collides in place in the stage's shared memory (KBC, linearised and
-// exact): their register-resident form needs 168-255 registers (one CTA per SM, ~14 % warps active).
-#ifndef LBM_SMEM_KBC
-#define LBM_SMEM_KBC 1
-#endif
-template <int OPX>
-constexpr bool kSmemCollide = LBM_SMEM_KBC && op_eq(OPX) == EQ_COMPRESSIBLE &&
-                              (op_class(op_base(OPX)) == OP_KBC || op_class(op_base(OPX)) == OP_KBC_EXACT);
-
 // registers: 65536 / (BT * minBlocks); the heavy fp64 operators get more room
 template <int Q, int OPX, typename T>
 struct StagedMinBlocks {
@@ -64,7 +55,7 @@ struct StagedMinBlocks {
 #ifdef LBM_STAGED_MINB
     static constexpr int value = LBM_STAGED_MINB;
 #else
-    static constexpr int value = kSmemCollide<OPX> ? 2 : (kStagedBT >= 256 ? 1 : 2) * (heavy ? 1 : 2);
+    static constexpr int value = (kStagedBT >= 256 ? 1 : 2) * (heavy ? 1 : 2);
 #endif
 };
 
@@ -149,212 +140,6 @@ __device__ __forceinline__ void stage_issue(const StepArgs &a, const T *f, const
                  a.flags + ((int64_t)tl.zs * ny + tl.y0) * nx, flag_bytes, bar);
 }
 
-// ---------------------------------------------------------------------------------------
-// KBC (Eqs. 15-19) collided in place in the stage's shared memory, with the direction
-// pairs walked by RUNTIME loops over a constant table: the register-resident form (collide_kbc_acc
-// unrolled over all Q directions) keeps every population and per-direction temporary live and needs
-// 168-255 registers, i.e. one CTA per SM. Here a cell's Q slots of the stage (each staged element
-// belongs to exactly one cell) hold g, then d = g - g_eq, then the result; registers hold only the
-// moments, the five shear coefficients and the per-pair temporaries of one loop iteration. Same
-// arithmetic, in the same order, as collide_kbc_acc (the staged/plain agreement test compares them).
-// ---------------------------------------------------------------------------------------
-struct KbcPair {
-    int8_t q, b, cx, cy, cz, pk[5];  // direction q < qbar = b, its velocity, shear polynomials P_k(c_q)
-    double w;
-};
-template <int Q>
-constexpr int kbc_npairs() { return Q == 19 ? 9 : 13; }
-template <int Q>
-constexpr KbcPair kbc_pair(int p) {
-    // pairs (q, qbar) with q < qbar in ascending q: 1..3, 7..12 (and 19..22 for D3Q27)
-    const int q = p < 3 ? p + 1 : (p < 9 ? p + 4 : p + 10);
-    return KbcPair{(int8_t)q, (int8_t)Stencil<Q>::opp(q), (int8_t)kC27[q][0], (int8_t)kC27[q][1], (int8_t)kC27[q][2],
-                   {(int8_t)mrt_poly(0, kC27[q][0], kC27[q][1], kC27[q][2]), (int8_t)mrt_poly(1, kC27[q][0], kC27[q][1], kC27[q][2]),
-                    (int8_t)mrt_poly(2, kC27[q][0], kC27[q][1], kC27[q][2]), (int8_t)mrt_poly(3, kC27[q][0], kC27[q][1], kC27[q][2]),
-                    (int8_t)mrt_poly(4, kC27[q][0], kC27[q][1], kC27[q][2])},
-                   Stencil<Q>::w(q)};
-}
-static __constant__ KbcPair kKbcPairs19[9] = {kbc_pair<19>(0), kbc_pair<19>(1), kbc_pair<19>(2), kbc_pair<19>(3),
-                                             kbc_pair<19>(4), kbc_pair<19>(5), kbc_pair<19>(6), kbc_pair<19>(7),
-                                             kbc_pair<19>(8)};
-static __constant__ KbcPair kKbcPairs27[13] = {kbc_pair<27>(0), kbc_pair<27>(1), kbc_pair<27>(2), kbc_pair<27>(3),
-                                              kbc_pair<27>(4), kbc_pair<27>(5), kbc_pair<27>(6), kbc_pair<27>(7),
-                                              kbc_pair<27>(8), kbc_pair<27>(9), kbc_pair<27>(10), kbc_pair<27>(11),
-                                              kbc_pair<27>(12)};
-
-template <int Q, typename T, bool EXACT, int MODE>
-__device__ __forceinline__ void collide_kbc_smem(T *__restrict__ buf, int rowlen, int rowbase, int xc, int xm, int xp,
-                                                 const Rates<T> &p) {
-    using S = Stencil<Q>;
-    const KbcPair *pairs = Q == 19 ? kKbcPairs19 : kKbcPairs27;
-    constexpr int NP = kbc_npairs<Q>();
-    // the cell's slot of direction q (velocity component cx) in the stage
-    auto at = [&](int q, int cx) -> T & {
-        const int sx = (MODE == SM_AA_EVEN || MODE == SM_PUSH) ? 0 : (MODE == SM_ESO_EVEN || MODE == SM_ESO_ODD) ? (cx > 0 ? cx : 0) : cx;
-        return buf[q * rowlen + rowbase + (sx == 0 ? xc : (sx > 0 ? xm : xp))];
-    };
-    // moments (moments0 order: q = 0 .. Q-1)
-    T drho = T(0), jx = T(0), jy = T(0), jz = T(0);
-#pragma unroll 1
-    for (int q = 0; q < Q; ++q) {
-        const int cx = kC27[q][0], cy = kC27[q][1], cz = kC27[q][2];
-        const T v = at(q, cx);
-        drho += v;
-        if (cx > 0) jx += v;
-        if (cx < 0) jx -= v;
-        if (cy > 0) jy += v;
-        if (cy < 0) jy -= v;
-        if (cz > 0) jz += v;
-        if (cz < 0) jz -= v;
-    }
-    const T rho = T(1) + drho;
-    const T inv = T(1) / rho;
-    const T ux = jx * inv, uy = jy * inv, uz = jz * inv;
-    const T uu15 = T(1.5) * (ux * ux + uy * uy + uz * uz);
-    const T w0 = T(S::w(0));
-    const T eq0 = w0 * drho - w0 * rho * uu15;
-    T &g0 = at(0, 0);
-    g0 -= eq0;
-    // d = g - g_eq in place; shear coefficients a_k = <P_k, d> / N_k
-    T a[5] = {T(0), T(0), T(0), T(0), T(0)};
-#pragma unroll 1
-    for (int i = 0; i < NP; ++i) {
-        const KbcPair P = pairs[i];
-        const T w = T(P.w);
-        const T cu = T(P.cx) * ux + T(P.cy) * uy + T(P.cz) * uz;
-        const T wr = w * rho;
-        const T es = w * drho + wr * (T(4.5) * cu * cu - uu15);
-        const T ea = wr * T(3) * cu;
-        T &gq = at(P.q, P.cx);
-        T &gb = at(P.b, -P.cx);
-        const T dq = gq - (es + ea), db = gb - (es - ea);
-        gq = dq;
-        gb = db;
-        const T dp = dq + db;
-#pragma unroll
-        for (int k = 0; k < 5; ++k) {
-            const int c = P.pk[k];
-            if (c == 1) a[k] += dp;
-            else if (c == -1) a[k] -= dp;
-            else if (c != 0) a[k] += T(c) * dp;
-        }
-    }
-#pragma unroll
-    for (int k = 0; k < 5; ++k) a[k] *= T(mrt_inv_norm(k));
-    auto ds_of = [&](const KbcPair &P) -> T {
-        T acc = T(0);
-#pragma unroll
-        for (int k = 0; k < 5; ++k) {
-            const int c = P.pk[k];
-            if (c == 1) acc += a[k];
-            else if (c == -1) acc -= a[k];
-            else if (c != 0) acc += T(c) * a[k];
-        }
-        return T(P.w) * acc;
-    };
-    auto pair_feq = [&](const KbcPair &P, T &es, T &ea, T &iq, T &ib) {
-        const T w = T(P.w);
-        const T cu = T(P.cx) * ux + T(P.cy) * uy + T(P.cz) * uz;
-        const T wr = w * rho;
-        es = w * drho + wr * (T(4.5) * cu * cu - uu15);
-        ea = wr * T(3) * cu;
-        const T A = w + es;
-        const T rr = fast_rcp(A * A - ea * ea);
-        iq = (A - ea) * rr;
-        ib = (A + ea) * rr;
-    };
-    const T d0 = g0;
-    // entropic products <Ds,Dh>_E, <Dh,Dh>_E (Eq. 19)
-    T sh = T(0), hh = d0 * d0 / (w0 + eq0);
-#pragma unroll 1
-    for (int i = 0; i < NP; ++i) {
-        const KbcPair P = pairs[i];
-        const T s = ds_of(P);
-        T es, ea, iq, ib;
-        pair_feq(P, es, ea, iq, ib);
-        const T hq = at(P.q, P.cx) - s, hb = at(P.b, -P.cx) - s;
-        sh += s * (hq * iq + hb * ib);
-        hh += hq * hq * iq + hb * hb * ib;
-    }
-    const T ws = p.r[0];
-    T wh = hh > T(0) ? T(1) + (T(1) - ws) * sh / hh : T(1);
-    if constexpr (EXACT) {
-        // Newton on G(w) = sum_q Dh_q ln(f'_q(w) / f_eq,q) (collide_kbc_acc, G25)
-        if (hh > T(0)) {
-            constexpr bool f64 = sizeof(T) == 8;
-            constexpr int kMaxIt = f64 ? 30 : 8;
-            const T tol = f64 ? T(1e-8) : T(1e-4);
-            const T i0 = T(1) / (w0 + eq0);
-            const T kw = T(1) - ws;
-            auto positive = [&](T w) {
-                bool ok = T(1) + (T(1) - w) * d0 * i0 > T(0);
-#pragma unroll 1
-                for (int i = 0; i < NP; ++i) {
-                    const KbcPair P = pairs[i];
-                    const T s = ds_of(P);
-                    T es, ea, iq, ib;
-                    pair_feq(P, es, ea, iq, ib);
-                    ok = ok && (T(1) + (kw * s + (T(1) - w) * (at(P.q, P.cx) - s)) * iq > T(0)) &&
-                         (T(1) + (kw * s + (T(1) - w) * (at(P.b, -P.cx) - s)) * ib > T(0));
-                }
-                return ok;
-            };
-#pragma unroll 1
-            for (int it = 0; it < kMaxIt; ++it) {
-                const T km = T(1) - wh;
-                T x0 = km * d0 * i0;
-                T G = d0 * ln1p_kbc(x0);
-                T Gp = -d0 * d0 * i0 * fast_rcp(T(1) + x0);
-                T lo = T(1) + x0, hi = fabs(d0 * i0);
-#pragma unroll 1
-                for (int i = 0; i < NP; ++i) {
-                    const KbcPair P = pairs[i];
-                    const T s = ds_of(P);
-                    T es, ea, iq, ib;
-                    pair_feq(P, es, ea, iq, ib);
-                    const T hq = at(P.q, P.cx) - s, hb = at(P.b, -P.cx) - s;
-                    const T xq = (kw * s + km * hq) * iq, xb = (kw * s + km * hb) * ib;
-                    G += hq * ln1p_kbc(xq) + hb * ln1p_kbc(xb);
-                    Gp -= hq * hq * iq * fast_rcp(T(1) + xq) + hb * hb * ib * fast_rcp(T(1) + xb);
-                    lo = fmin(lo, fmin(T(1) + xq, T(1) + xb));
-                    hi = fmax(hi, fmax(fabs(hq * iq), fabs(hb * ib)));
-                }
-                T step = G / Gp;
-                if (!(fabs(step) <= T(1e30))) {
-                    wh = step;
-                    break;
-                }
-                T wn = wh - step;
-                bool full = true;
-                for (int tries = 0; tries < 60 && !(lo > fabs(step) * hi) && !positive(wn); ++tries) {
-                    step *= T(0.5);
-                    wn = wh - step;
-                    full = false;
-                }
-                wh = wn;
-                if (full && fabs(step) <= tol) break;
-            }
-        }
-    }
-    // f' = f_eq + (1 - w_h) d + (w_h - w_s) Ds, in place
-    const T kd = T(1) - wh, ks = wh - ws;
-    g0 = eq0 + kd * d0;
-#pragma unroll 1
-    for (int i = 0; i < NP; ++i) {
-        const KbcPair P = pairs[i];
-        const T w = T(P.w);
-        const T cu = T(P.cx) * ux + T(P.cy) * uy + T(P.cz) * uz;
-        const T wr = w * rho;
-        const T es = w * drho + wr * (T(4.5) * cu * cu - uu15);
-        const T ea = wr * T(3) * cu;
-        const T sk = ks * ds_of(P);
-        T &gq = at(P.q, P.cx);
-        T &gb = at(P.b, -P.cx);
-        gq = (es + ea) + kd * gq + sk;
-        gb = (es - ea) + kd * gb + sk;
-    }
-}
-
 template <int Q, int OP, typename T, int FM, bool FORCE, int MODE>
 __global__ void __launch_bounds__(kStagedBT + 32, (StagedMinBlocks<Q, OP, T>::value))
     k_staged(const StepArgs a, const T *src, T *dst, int nplanes, int H, int nstages, int stage_elems) {
@@ -393,7 +178,7 @@ __global__ void __launch_bounds__(kStagedBT + 32, (StagedMinBlocks<Q, OP, T>::va
     for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
         const int stage = it % nstages;
         const Tile tl = tile_of(a, t, H);
-        T *buf = stages + (int64_t)stage * stage_elems;
+        const T *buf = stages + (int64_t)stage * stage_elems;
         const uint8_t *fl = reinterpret_cast<const uint8_t *>(buf + (int64_t)Q * rowlen);
         mbar_wait(&full[stage], (uint32_t)((it / nstages) & 1));
         const int ncell = tl.hl * nx;
@@ -414,24 +199,14 @@ __global__ void __launch_bounds__(kStagedBT + 32, (StagedMinBlocks<Q, OP, T>::va
                 if (MODE == SM_AA_EVEN ? (own & 3) != 0 : own != 0) continue;
             }
             const int xm = xc == 0 ? nx - 1 : xc - 1, xp = xc == nx - 1 ? 0 : xc + 1;
-            // this cell's slot of direction q in the stage: every staged element is read by exactly one cell
-            // (the x-shift is a bijection of the row), so the cell may also overwrite its own slots
-            auto slot = [&](int q) -> T & {
-                const int sx = rshift(MODE, S::cx(q));
-                return buf[q * rowlen + hc * nx + (sx == 0 ? xc : (sx > 0 ? xm : xp))];
-            };
             T g[Q];
-            if constexpr (kSmemCollide<OP>) {
-                // KBC: the collision works on the populations in place in shared memory (collide_kbc_acc),
-                // holding only moments and the shear coefficients in registers (2 CTAs per SM instead of 1)
-                collide_kbc_smem<Q, T, op_class(op_base(OP)) == OP_KBC_EXACT, MODE>(buf, rowlen, hc * nx, xc, xm, xp, r);
 #pragma unroll
-                for (int q = 0; q < Q; ++q) g[q] = slot(q);
-            } else {
-#pragma unroll
-                for (int q = 0; q < Q; ++q) g[q] = slot(q);
-                collide<Q, OP, T, FORCE>(g, r);
+            for (int q = 0; q < Q; ++q) {
+                const int sx = rshift(MODE, S::cx(q));
+                const int xs = sx == 0 ? xc : (sx > 0 ? xm : xp);
+                g[q] = buf[q * rowlen + hc * nx + xs];
             }
+            collide<Q, OP, T, FORCE>(g, r);
             const int y = tl.y0 + hc;
             const uint32_t self = ((uint32_t)tl.zs * (uint32_t)a.geo.ny + (uint32_t)y) * (uint32_t)nx + (uint32_t)xc;
             LBM_ASSERT((int64_t)self < Sq && y < a.geo.ny && (a.geo.g ? (tl.zs >= 1 && tl.zs <= a.geo.nz) : tl.zs < a.geo.nz));

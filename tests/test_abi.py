@@ -90,7 +90,6 @@ def test_slab_plan(L):
     (dict(collision="trt", rates=(1.0,) * 15), -1),             # per-moment rates are for MRT
     (dict(collision="mrt", rates=(1.0,) * 14 + (2.0,)), -1),    # per-moment rate outside (0, 2)
     (dict(collision="mrt", rates=(1.0,) * 15, equilibrium="incompressible"), -2),
-    (dict(boundary_mode="links", nccl_self=True, halo_mode=2, pattern="aa"), -2),  # AA + links: no fused halo
     (dict(stencil=27, collision="cumulant", rates=(1.9,), equilibrium="incompressible"), -2),
     (dict(collision="kbc", rates=(1.9,), equilibrium="moment_matched"), -2),
     (dict(collision="kbc_exact", rates=(1.9,), force=(1e-5, 0, 0)), -2),   # forcing is SRT/TRT only

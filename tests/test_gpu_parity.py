@@ -628,6 +628,13 @@ LINK_CASES = [
     Case("lk_mrt_f32_channel32_pull", (32, 20, 12), 19, "mrt", (1.9, 1.3, 1.1, 0.8), "f32", geometry="channel", steps=14),
     Case("lk_kbc_obst_pull", (16, 12, 10), 19, "kbc", (1.95,), "f64", geometry="obstacles", ubb=(0.02, -0.01, 0.03),
          u_amp=0.05, steps=12),
+    # EsoTwist with index lists (P:875-891 + P:904-914): the fix moves the departing slot of the link location
+    Case("lk_eso_trt_f64_obst_odd", (17, 13, 11), 19, "trt", (1.6, 0.5), "f64", pattern="esotwist", force=(1e-5, 0, 0),
+         geometry="obstacles", ubb=(0.02, -0.01, 0.03), steps=15),
+    Case("lk_eso_cum27_cavity_even", (12, 12, 12), 27, "cumulant", (1.95,), "f64", pattern="esotwist",
+         geometry="cavity", ubb=(0.05, 0, 0), steps=12),
+    Case("lk_eso_mrt_f32_channel32", (32, 20, 12), 19, "mrt", (1.9, 1.3, 1.1, 0.8), "f32", pattern="esotwist",
+         geometry="channel", steps=13),
 ]
 
 
@@ -690,13 +697,12 @@ def test_index_list_per_link_wall_velocities(pattern, steps):
 
 
 @pytest.mark.parametrize("P,halo_mode,nccl_self", [(2, 0, False), (4, 1, False), (1, 0, True), (1, 1, True), (1, 2, True)])
-@pytest.mark.parametrize("pattern", ["pull", "aa", "push"])
+@pytest.mark.parametrize("pattern", ["pull", "aa", "push", "esotwist"])
 def test_index_list_boundaries_slabs_bit_identical(P, halo_mode, nccl_self, pattern):
-    """Index-list boundaries with slab decomposition (pull): the link kernel also fills the wall slots of
-    ghost planes after the exchange; loopback slabs, NCCL self-exchange and the fused NVLink halo are
-    bit-identical to the single slab, and the concatenated link lists are the global list."""
-    if pattern in ("aa", "push") and halo_mode == 2:
-        pytest.skip("AA / push + index-list boundaries use the NCCL or loopback halo")
+    """Index-list boundaries with slab decomposition: the link kernel also fills the wall slots of ghost
+    planes after the exchange (fused halo: after the next LSA gate, plus a closing gate per lbm_step call);
+    loopback slabs, NCCL self-exchange and the fused NVLink halo are bit-identical to the single slab, for
+    every pattern, and the concatenated link lists are the global list."""
     case = Case("lkdec", (16, 12, 16), 19, "trt", (1.6, 0.5), "f64", force=(1e-5, 0, 0), geometry="obstacles",
                 ubb=(0.02, -0.01, 0.03), steps=13, pattern=pattern)
     one = make_sim(case, boundary_mode="links")
