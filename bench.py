@@ -84,8 +84,9 @@ for _name, _op, _q, _rates in [("trt", "trt", 19, (1.6, 0.5)), ("smagorinsky", "
                                   job_steps=200)
 
 for _k in ("op_kbc_exact", "op_kbc27_exact"):
-    CONFIGS[_k]["note"] = ("FP64-latency bound, not HBM-bound: per-cell Newton iterations with two ln(1+x) per "
-                           "direction pair (ncu: FP64 pipe ~36 % active, DRAM ~11 %; DESIGN.md section 6.2)")
+    CONFIGS[_k]["note"] = ("FP64-ALU bound, not HBM-bound: per-cell Newton iterations with two ln(1+x) per "
+                           "direction pair; roofline = measured DFMA ceiling (DESIGN.md section 6.2)")
+    CONFIGS[_k]["alu_bound"] = True
 
 # Generated operators (codegen/): C4 and C2 with the generated TRT / weighted MRT.
 CONFIGS["c4_gen"] = dict(CONFIGS["c4"], op="gen_trt", desc=CONFIGS["c4"]["desc"] + ", generated TRT operator")
@@ -185,6 +186,41 @@ def load_traffic(config_name):
         if v:
             return v
     return None
+
+
+def load_alu(config_name):
+    """FP work per cell of the config's dominant update kernel (SASS instruction counts from an ncu metrics
+    pass, scripts/alu_flops.py -> profiles/alu_flops.jsonl; the last entry per config wins)."""
+    p = os.path.join(ROOT, "profiles", "alu_flops.jsonl")
+    found = None
+    if os.path.exists(p):
+        with open(p) as fh:
+            for line in fh:
+                line = line.strip()
+                if line:
+                    d = json.loads(line)
+                    if d.get("config") == config_name:
+                        found = d
+    return found
+
+
+def alu_block(config_name, dtype, kernel_ms_per_step, device):
+    """Achieved FP throughput of the dominant kernel against the measured FMA-chain ceiling of the dtype
+    (lbm_probe_fma, run live: DFMA for fp64, FFMA for fp32)."""
+    d = load_alu(config_name)
+    if d is None:
+        return None
+    from paper_2001_11806_b200 import lbm as L
+    key = "fp64_flops_per_cell" if dtype == "f64" else "fp32_flops_per_cell"
+    try:
+        peak = L.probe_fma(dtype, device)
+    except L.LBMError:
+        return None
+    achieved = d[key] * d["cells_per_launch"] / (kernel_ms_per_step / 1e3) / 1e12
+    return {"flops_per_cell": d[key], "achieved_tflops": achieved, "peak_tflops": peak, "frac": achieved / peak,
+            "peak_source": f"measured live (lbm_probe_fma, {'DFMA' if dtype == 'f64' else 'FFMA'} chains)",
+            "flops_source": "ncu SASS counts add + mul + 2 fma (profiles/alu_flops.jsonl)",
+            "fp64_pipe_pct_ncu": d.get("fp64_pipe_pct"), "issue_active_pct_ncu": d.get("issue_active_pct")}
 
 
 class ClockSampler:
@@ -542,6 +578,28 @@ def main():
                 copyq = L.probe_copy(cfg["Q"], cfg["dtype"], True, (nx, ny, sim.nz_local), reps=5, device=local)
             except L.LBMError:
                 copyq = None
+        alu = alu_block(args.config, cfg["dtype"], kernel_ms_per_step, local)
+        roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                    "traffic": load_traffic(args.config), "peak_source": peak_src,
+                    "algorithmic_bytes_per_cell": bpc, "cells_per_launch": nf_local,
+                    "kernel_ms_per_step": kernel_ms_per_step, "kernel_launches_timed": klaunch,
+                    "frac_of_nominal_8tbs": achieved / 8000.0,
+                    "note": ("L2-resident launch/latency-bound domain: the HBM roofline does not bind "
+                             "(one persistent kernel per lbm_step call)")
+                            if (cfg["Q"] * np.prod(gshape) / P * (8 if cfg["dtype"] == "f64" else 4)
+                                * (2 if cfg["pattern"] in ("pull", "push") else 1)) < 100e6 else cfg.get("note"),
+                    "copy_q_gbs": copyq, "frac_of_copy_q": (achieved / copyq) if copyq else None,
+                    "boundary_mode": cfg.get("boundary_mode", "flags") if flags is not None else "none",
+                    "kernel_path": L.kernel_path()}
+        if cfg.get("alu_bound") and alu is not None:
+            # the FP64-ALU-bound operators (exact KBC): the roofline is the measured DFMA ceiling; the HBM
+            # figures stay beside it
+            roofline = {"bound": "alu", "achieved": alu["achieved_tflops"], "peak": alu["peak_tflops"],
+                        "unit": "TFLOP/s", "frac": alu["frac"], "traffic": load_traffic(args.config),
+                        "peak_source": alu["peak_source"], "flops_per_cell": alu["flops_per_cell"],
+                        "hbm_achieved_gbs": achieved, "hbm_frac": achieved / peak, "kernel_ms_per_step": kernel_ms_per_step,
+                        "kernel_launches_timed": klaunch, "cells_per_launch": nf_local, "kernel_path": L.kernel_path(),
+                        "note": cfg.get("note")}
         line = {
             "metric": "MLUPS (fluid-cell updates per second, whole job)",
             "value": mlups, "unit": "MLUPS", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -554,18 +612,8 @@ def main():
                        ("single GPU, NCCL self-exchange of ghost planes" if nccl_self else "single GPU"),
                        "l2": "inputs larger than L2 (no flush)" if not small else "L2-resident (launch-bound config)",
                        "halo_mode": {0: "zerocopy NCCL send/recv", 1: "packed NCCL send/recv", 2: "fused NVLink peer stores (NCCL LSA windows)"}[args.halo_mode] if (world > 1 or nccl_self) else "none (single slab, z wraps in-kernel)", "small_domain_mode": {0: "plain launches", 1: "CUDA graph (2-step cycle)", 2: "persistent cooperative kernel"}[use_graph]},
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                         "traffic": load_traffic(args.config), "peak_source": peak_src,
-                         "algorithmic_bytes_per_cell": bpc, "cells_per_launch": nf_local,
-                         "kernel_ms_per_step": kernel_ms_per_step, "kernel_launches_timed": klaunch,
-                         "frac_of_nominal_8tbs": achieved / 8000.0,
-                         "note": ("L2-resident launch/latency-bound domain: the HBM roofline does not bind "
-                                  "(one persistent kernel per lbm_step call)")
-                                 if (cfg["Q"] * np.prod(gshape) / P * (8 if cfg["dtype"] == "f64" else 4)
-                                     * (2 if cfg["pattern"] in ("pull", "push") else 1)) < 100e6 else cfg.get("note"),
-                         "copy_q_gbs": copyq, "frac_of_copy_q": (achieved / copyq) if copyq else None,
-                         "boundary_mode": cfg.get("boundary_mode", "flags") if flags is not None else "none",
-                         "kernel_path": L.kernel_path()},
+            "roofline": roofline,
+            "alu": alu,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches,

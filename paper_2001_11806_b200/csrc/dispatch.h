@@ -6,8 +6,10 @@
 
 namespace lbm {
 
-using PullLaunch = void (*)(const StepArgs &, const void *src, void *dst, dim3 grid, dim3 block, cudaStream_t);
-using AALaunch = void (*)(const StepArgs &, void *f, int odd, dim3 grid, dim3 block, cudaStream_t);
+// Bulk launchers return 1 when the launch also resolved the near-wall cells (TMA-staged pull / AA odd
+// kernels with split flags, staged_inline_edges), so the caller skips the edge-list launch; else 0.
+using PullLaunch = int (*)(const StepArgs &, const void *src, void *dst, dim3 grid, dim3 block, cudaStream_t);
+using AALaunch = int (*)(const StepArgs &, void *f, int odd, dim3 grid, dim3 block, cudaStream_t);
 // near-wall cell list launch (split wall mode): pull edge kernel, or the AA odd edge kernel (src unused)
 using EdgeLaunch = void (*)(const StepArgs &, const void *src, void *dst, const uint32_t *cells, uint32_t n, cudaStream_t);
 

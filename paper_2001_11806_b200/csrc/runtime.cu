@@ -206,10 +206,10 @@ void launch_pull_range(lbm_handle_s *h, Slab &s, int z_begin, int nplanes, int z
         a.peer_down = h->fst.bases[2 * (1 - s.cur) + 1];
     }
     tbegin(h, st);
-    h->kern.pull(a, s.pdf[s.cur], s.pdf[1 - s.cur], grid_for(h, nplanes), h->block, st);
+    const int edges_done = h->kern.pull(a, s.pdf[s.cur], s.pdf[1 - s.cur], grid_for(h, nplanes), h->block, st);
     tend(h, st);
     h->launches++;
-    launch_edges(h, s, a, h->kern.pull_edges, s.pdf[s.cur], s.pdf[1 - s.cur], z_begin, nplanes, z_step, st);
+    if (!edges_done) launch_edges(h, s, a, h->kern.pull_edges, s.pdf[s.cur], s.pdf[1 - s.cur], z_begin, nplanes, z_step, st);
 }
 
 void launch_push_range(lbm_handle_s *h, Slab &s, int z_begin, int nplanes, int z_step, cudaStream_t st,
@@ -264,10 +264,10 @@ void launch_aa_range(lbm_handle_s *h, Slab &s, int odd, int z_begin, int nplanes
         a.peer_down = h->fst.bases[1];
     }
     tbegin(h, st);
-    h->kern.aa(a, s.pdf[0], odd, grid_for(h, nplanes), h->block, st);
+    const int edges_done = h->kern.aa(a, s.pdf[0], odd, grid_for(h, nplanes), h->block, st);
     tend(h, st);
     h->launches++;
-    if (odd) launch_edges(h, s, a, h->kern.aa_edges, nullptr, s.pdf[0], z_begin, nplanes, z_step, st);
+    if (odd && !edges_done) launch_edges(h, s, a, h->kern.aa_edges, nullptr, s.pdf[0], z_begin, nplanes, z_step, st);
 }
 
 // Halo exchange phases. Each phase moves, per slab, one set of crossing slots through face A
