@@ -389,7 +389,7 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=0, help="LB steps per e2e job (0 = the config's step count)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-probe", action="store_true", help="skip the copy-q roofline probe")
-    ap.add_argument("--halo-mode", type=int, default=-1, help="0 zero-copy NCCL, 1 packed NCCL, 2 fused NVLink peer stores; default: 2 when exchanging, else 0")
+    ap.add_argument("--halo-mode", type=int, default=-1, help="0 zero-copy NCCL (default), 1 packed NCCL, 2 fused NVLink peer stores")
     ap.add_argument("--nccl-self", type=int, default=0,
                     help="N=1 only: ghost planes exchanged through a 1-rank NCCL communicator (times the multi-GPU path)")
     ap.add_argument("--block-x", type=int, default=0)
@@ -440,8 +440,12 @@ def main():
     use_graph = 0 if nccl_self else use_graph
     exchanging = world > 1 or nccl_self
     halo_mode = args.halo_mode
-    if halo_mode < 0:  # default: fused NVLink peer-store halo when exchanging
-        halo_mode = L.HALO_FUSED if exchanging else L.HALO_ZEROCOPY
+    if halo_mode < 0:
+        # default: zero-copy NCCL send/recv overlapped with the interior. The fused NVLink peer-store halo
+        # (--halo-mode 2) is bit-identical and as fast on one GPU (1-rank communicator) but has not run
+        # across GPUs in this build (tests/test_multigpu.py runs it on the first multi-GPU box), and the
+        # C4 halo is ~0.2 % of a step, so the default favours the transport that cannot hang a scaling run.
+        halo_mode = L.HALO_ZEROCOPY
 
     def make(mode):
         return L.Simulation(gshape, stencil=cfg["Q"], collision=cfg["op"], rates=cfg["rates"], dtype=cfg["dtype"],

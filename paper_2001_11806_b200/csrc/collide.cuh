@@ -772,6 +772,104 @@ __device__ __forceinline__ void collide_cumulant27(T (&g)[27], const Rates<T> &p
     for (int q = 0; q < 27; ++q) g[q] = K[tidx(q)] - T(S::w(q));
 }
 
+// Cumulant D3Q27 with omega_bulk = omega_3 = ... = omega_6 = 1 (the rates of config C3, G7): the
+// run-time counterpart of lbmpy's pre-evaluation of constant relaxation rates for the
+// cumulant. Every cumulant of order >= 3 is relaxed to its Maxwellian value 0 and the trace to 3 cs^2, so
+// only the second-order central moments of the pre-collision state are needed (from the raw second
+// moments, not the full forward transform), and the post-collision central moments are the Gaussian
+// (Isserlis) ones of the relaxed covariance: order 4 m211 = n200 n011 + 2 n110 n101, m220 = n200 n020 +
+// 2 n110^2 (and permutations), order 6 m222, odd orders 0 (the closed form the oracle pin G7 checks).
+// The first backward pass (z) uses the parity structure of those moments: lines (a, b) with a + b even
+// hold (K_ab0, 0, K_ab2), odd ones (0, K_ab1, 0). About 600 instead of 1135 FP64 operations per cell.
+template <typename T>
+__device__ __forceinline__ void chim_bwd_even(T &m, T &z, T &p, T u) {  // (k0, 0, k2)
+    const T k0 = m, k2 = p;
+    const T uu = u * u;
+    z = (T(1) - uu) * k0 - k2;
+    p = T(0.5) * ((uu + u) * k0 + k2);
+    m = T(0.5) * ((uu - u) * k0 + k2);
+}
+template <typename T>
+__device__ __forceinline__ void chim_bwd_odd(T &m, T &z, T &p, T u) {  // (0, k1, 0)
+    const T k1 = z;
+    z = T(-2) * u * k1;
+    p = T(0.5) * (T(2) * u + T(1)) * k1;
+    m = T(0.5) * (T(2) * u - T(1)) * k1;
+}
+
+template <typename T>
+__device__ __forceinline__ void collide_cumulant27_unit(T (&g)[27], const Rates<T> &p) {
+    using S = Stencil<27>;
+    T drho, jx, jy, jz;
+    moments0<27, T>(g, drho, jx, jy, jz);
+    const T rho = T(1) + drho;
+    const T inv = T(1) / rho;
+    const T ux = jx * inv, uy = jy * inv, uz = jz * inv;
+    // raw second moments of g; f = g + w adds delta_ab / 3 (sum_q w_q c_a c_b = c_s^2 delta_ab)
+    T pxx = T(0), pyy = T(0), pzz = T(0), pxy = T(0), pxz = T(0), pyz = T(0);
+#pragma unroll
+    for (int q = 1; q < 27; ++q) {
+        const int cx = S::cx(q), cy = S::cy(q), cz = S::cz(q);
+        if (cx != 0) pxx += g[q];
+        if (cy != 0) pyy += g[q];
+        if (cz != 0) pzz += g[q];
+        if (cx * cy > 0) pxy += g[q];
+        if (cx * cy < 0) pxy -= g[q];
+        if (cx * cz > 0) pxz += g[q];
+        if (cx * cz < 0) pxz -= g[q];
+        if (cy * cz > 0) pyz += g[q];
+        if (cy * cz < 0) pyz -= g[q];
+    }
+    const T third = T(1) / T(3);
+    // normalised central second moments (= second-order cumulants) c_ab = P_ab / rho - u_a u_b
+    const T c200 = (pxx + third) * inv - ux * ux, c020 = (pyy + third) * inv - uy * uy, c002 = (pzz + third) * inv - uz * uz;
+    const T c110 = pxy * inv - ux * uy, c101 = pxz * inv - ux * uz, c011 = pyz * inv - uy * uz;
+    // relaxation: deviator and off-diagonals with omega_shear, trace to 1 (omega_bulk = 1)
+    const T rs = T(1) - p.r[0];
+    const T tr3 = third * (c200 + c020 + c002);
+    const T n200 = third + rs * (c200 - tr3), n020 = third + rs * (c020 - tr3), n002 = third + rs * (c002 - tr3);
+    const T n110 = rs * c110, n101 = rs * c101, n011 = rs * c011;
+    // post-collision central moments (all cumulants of order >= 3 are zero)
+    const T m211 = n200 * n011 + T(2) * n110 * n101;
+    const T m121 = n020 * n101 + T(2) * n110 * n011;
+    const T m112 = n002 * n110 + T(2) * n101 * n011;
+    const T m220 = n200 * n020 + T(2) * n110 * n110;
+    const T m202 = n200 * n002 + T(2) * n101 * n101;
+    const T m022 = n020 * n002 + T(2) * n011 * n011;
+    const T m222 = n200 * n020 * n002 + T(2) * (n200 * n011 * n011 + n020 * n101 * n101 + n002 * n110 * n110) +
+                   T(8) * n110 * n101 * n011;
+    T K[27];
+#define KI(a, b, c) K[(a) * 9 + (b) * 3 + (c)]
+    KI(0, 0, 0) = rho;            KI(0, 0, 1) = T(0);           KI(0, 0, 2) = rho * n002;
+    KI(0, 1, 0) = T(0);           KI(0, 1, 1) = rho * n011;     KI(0, 1, 2) = T(0);
+    KI(0, 2, 0) = rho * n020;     KI(0, 2, 1) = T(0);           KI(0, 2, 2) = rho * m022;
+    KI(1, 0, 0) = T(0);           KI(1, 0, 1) = rho * n101;     KI(1, 0, 2) = T(0);
+    KI(1, 1, 0) = rho * n110;     KI(1, 1, 1) = T(0);           KI(1, 1, 2) = rho * m112;
+    KI(1, 2, 0) = T(0);           KI(1, 2, 1) = rho * m121;     KI(1, 2, 2) = T(0);
+    KI(2, 0, 0) = rho * n200;     KI(2, 0, 1) = T(0);           KI(2, 0, 2) = rho * m202;
+    KI(2, 1, 0) = T(0);           KI(2, 1, 1) = rho * m211;     KI(2, 1, 2) = T(0);
+    KI(2, 2, 0) = rho * m220;     KI(2, 2, 1) = T(0);           KI(2, 2, 2) = rho * m222;
+    // backward: z (parity-structured lines), y, x
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int b = 0; b < 3; ++b) {
+            if ((a + b) % 2 == 0) chim_bwd_even(KI(a, b, 0), KI(a, b, 1), KI(a, b, 2), uz);
+            else chim_bwd_odd(KI(a, b, 0), KI(a, b, 1), KI(a, b, 2), uz);
+        }
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) chim_bwd(KI(a, 0, c), KI(a, 1, c), KI(a, 2, c), uy);
+#pragma unroll
+    for (int b = 0; b < 3; ++b)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) chim_bwd(KI(0, b, c), KI(1, b, c), KI(2, b, c), ux);
+#undef KI
+#pragma unroll
+    for (int q = 0; q < 27; ++q) g[q] = K[tidx(q)] - T(S::w(q));
+}
+
 // ---------------------------------------------------------------------------------------
 // Cumulant, D3Q19 (cumulant methods "also for D3Q19"): the 19 populations are embedded in
 // the 3x3x3 tensor with zero corners, transformed to central moments by the same per-axis chimera
@@ -901,12 +999,14 @@ __device__ __forceinline__ void collide_cumulant19(T (&g)[19], const Rates<T> &p
 enum Op { OP_SRT = 0, OP_TRT = 1, OP_MRT = 2, OP_CUMULANT = 3, OP_IDENTITY = 4, OP_SMAGORINSKY = 5, OP_KBC = 6,
           OP_KBC_EXACT = 7, /* KBC, omega_h by Newton maximisation of Eq. (17) (= LBM_KBC_EXACT) */
           OP_GEN_SRT = 8, OP_GEN_TRT = 9, OP_GEN_MRT = 10, OP_GEN_SMAGORINSKY = 11, /* generated (codegen/, = LBM_GEN_*) */
+          OP_CUMULANT_UNIT = 12, /* D3Q27 cumulant with omega_bulk = omega_3..6 = 1 (internal id, selected at create) */
           OP_MRT_ROWS = 15 /* MRT with one rate per moment (internal id; ABI: LBM_MRT + n_row_rates = 15) */ };
 
 // Operator class for occupancy / kernel-path tuning: the generated operators behave like their
 // hand-written counterparts (TRT-like, MRT-like).
 constexpr int op_class(int op) {
-    return (op == OP_GEN_SRT || op == OP_GEN_TRT) ? OP_TRT : op == OP_GEN_MRT ? OP_MRT : op == OP_GEN_SMAGORINSKY ? OP_SMAGORINSKY : op;
+    return (op == OP_GEN_SRT || op == OP_GEN_TRT) ? OP_TRT : op == OP_GEN_MRT ? OP_MRT : op == OP_GEN_SMAGORINSKY ? OP_SMAGORINSKY
+         : op == OP_CUMULANT_UNIT ? OP_CUMULANT : op;
 }
 
 template <int Q, int OPX, typename T, bool FORCE>
@@ -923,6 +1023,9 @@ __device__ __forceinline__ void collide(T (&g)[Q], const Rates<T> &p) {
     } else if constexpr (OP == OP_CUMULANT) {
         if constexpr (Q == 27) collide_cumulant27<T>(g, p);
         else collide_cumulant19<T>(g, p);
+    } else if constexpr (OP == OP_CUMULANT_UNIT) {
+        static_assert(Q == 27, "the unit-rate cumulant specialisation is D3Q27");
+        collide_cumulant27_unit<T>(g, p);
     } else if constexpr (OP == OP_SMAGORINSKY) {
         collide_smagorinsky<Q, T>(g, p);
     } else if constexpr (OP == OP_KBC) {

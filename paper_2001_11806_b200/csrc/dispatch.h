@@ -6,10 +6,8 @@
 
 namespace lbm {
 
-// Bulk launchers return 1 when the launch also resolved the near-wall cells (TMA-staged pull / AA odd
-// kernels with split flags, staged_inline_edges), so the caller skips the edge-list launch; else 0.
-using PullLaunch = int (*)(const StepArgs &, const void *src, void *dst, dim3 grid, dim3 block, cudaStream_t);
-using AALaunch = int (*)(const StepArgs &, void *f, int odd, dim3 grid, dim3 block, cudaStream_t);
+using PullLaunch = void (*)(const StepArgs &, const void *src, void *dst, dim3 grid, dim3 block, cudaStream_t);
+using AALaunch = void (*)(const StepArgs &, void *f, int odd, dim3 grid, dim3 block, cudaStream_t);
 // near-wall cell list launch (split wall mode): pull edge kernel, or the AA odd edge kernel (src unused)
 using EdgeLaunch = void (*)(const StepArgs &, const void *src, void *dst, const uint32_t *cells, uint32_t n, cudaStream_t);
 
@@ -37,6 +35,7 @@ Kernels select_mrt(int Q, int dtype, int fm, bool force);
 Kernels select_mrt_rows(int Q, int dtype, int fm, bool force);
 int mrt_rows_upload();  // per-moment MRT rows -> __constant__ memory of the current device
 Kernels select_cumulant(int Q, int dtype, int fm, bool force);
+Kernels select_cumulant_unit(int Q, int dtype, int fm, bool force);  // D3Q27, omega_bulk = omega_3..6 = 1
 Kernels select_identity(int Q, int dtype, int fm, bool force);
 Kernels select_smagorinsky(int Q, int dtype, int fm, bool force);
 Kernels select_kbc(int Q, int dtype, int fm, bool force);

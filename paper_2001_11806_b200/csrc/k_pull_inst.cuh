@@ -8,18 +8,16 @@
 namespace lbm {
 
 template <int Q, int OP, typename T, int FM, bool FORCE>
-int pull_launcher(const StepArgs &a, const void *src, void *dst, dim3 grid, dim3 block, cudaStream_t s) {
+void pull_launcher(const StepArgs &a, const void *src, void *dst, dim3 grid, dim3 block, cudaStream_t s) {
     // peer stores (fused halo, boundary-plane launches only) are a separate instantiation so the
     // interior kernel carries no extra live registers
-    if (a.peer_up == nullptr && staged_launch<Q, OP, T, FM, FORCE, SM_PULL>(a, src, dst, (int)grid.z, s))
-        return staged_inline_edges<FM, SM_PULL>() ? 1 : 0;
+    if (a.peer_up == nullptr && staged_launch<Q, OP, T, FM, FORCE, SM_PULL>(a, src, dst, (int)grid.z, s)) return;
     if constexpr (FM != FM_INLINE)  // the low-level ABI (inline walls) never stores to peers
         if (a.peer_up != nullptr) {
             k_pull<Q, OP, T, FM, FORCE, true><<<grid, block, 0, s>>>(a, static_cast<const T *>(src), static_cast<T *>(dst));
-            return 0;
+            return;
         }
     k_pull<Q, OP, T, FM, FORCE, false><<<grid, block, 0, s>>>(a, static_cast<const T *>(src), static_cast<T *>(dst));
-    return 0;
 }
 
 template <int Q, int OP, typename T, bool FORCE>
@@ -33,23 +31,22 @@ void pull_edge_launcher(const StepArgs &a, const void *src, void *dst, const uin
 }
 
 template <int Q, int OP, typename T, int FM, bool FORCE>
-int aa_launcher(const StepArgs &a, void *f, int odd, dim3 grid, dim3 block, cudaStream_t s) {
+void aa_launcher(const StepArgs &a, void *f, int odd, dim3 grid, dim3 block, cudaStream_t s) {
     if constexpr (FM != FM_INLINE)
         if (a.peer_up != nullptr) {  // fused halo: boundary-plane launch with peer stores (plain kernels)
             if (odd) k_aa_odd<Q, OP, T, FM, FORCE, true><<<grid, block, 0, s>>>(a, static_cast<T *>(f));
             else k_aa_even<Q, OP, T, (FM != FM_NONE), FORCE, true><<<grid, block, 0, s>>>(a, static_cast<T *>(f));
-            return 0;
+            return;
         }
     if (odd) {
-        if (staged_launch<Q, OP, T, FM, FORCE, SM_AA_ODD>(a, f, f, (int)grid.z, s)) return staged_inline_edges<FM, SM_AA_ODD>() ? 1 : 0;
+        if (staged_launch<Q, OP, T, FM, FORCE, SM_AA_ODD>(a, f, f, (int)grid.z, s)) return;
     } else {
-        if (staged_launch<Q, OP, T, (FM == FM_NONE ? FM_NONE : FM_BULK), FORCE, SM_AA_EVEN>(a, f, f, (int)grid.z, s)) return 0;
+        if (staged_launch<Q, OP, T, (FM == FM_NONE ? FM_NONE : FM_BULK), FORCE, SM_AA_EVEN>(a, f, f, (int)grid.z, s)) return;
     }
     if (odd)
         k_aa_odd<Q, OP, T, FM, FORCE><<<grid, block, 0, s>>>(a, static_cast<T *>(f));
     else  // the even step is in place: walls are skipped, near-wall cells need nothing special
         k_aa_even<Q, OP, T, (FM != FM_NONE), FORCE><<<grid, block, 0, s>>>(a, static_cast<T *>(f));
-    return 0;
 }
 
 template <int Q, int OP, typename T, bool FORCE>
@@ -63,15 +60,14 @@ void aa_edge_launcher(const StepArgs &a, const void *src, void *f, const uint32_
 }
 
 template <int Q, int OP, typename T, int FM, bool FORCE>
-int push_launcher(const StepArgs &a, const void *src, void *dst, dim3 grid, dim3 block, cudaStream_t s) {
+void push_launcher(const StepArgs &a, const void *src, void *dst, dim3 grid, dim3 block, cudaStream_t s) {
     if constexpr (FM != FM_INLINE)
         if (a.peer_up != nullptr) {  // fused halo: boundary-plane launch with peer stores (plain kernels)
             k_push<Q, OP, T, FM, FORCE, true><<<grid, block, 0, s>>>(a, static_cast<const T *>(src), static_cast<T *>(dst));
-            return 0;
+            return;
         }
-    if (staged_launch<Q, OP, T, FM, FORCE, SM_PUSH>(a, src, dst, (int)grid.z, s)) return 0;
+    if (staged_launch<Q, OP, T, FM, FORCE, SM_PUSH>(a, src, dst, (int)grid.z, s)) return;
     k_push<Q, OP, T, FM, FORCE, false><<<grid, block, 0, s>>>(a, static_cast<const T *>(src), static_cast<T *>(dst));
-    return 0;
 }
 
 template <int Q, int OP, typename T, bool FORCE>
@@ -85,25 +81,23 @@ void push_edge_launcher(const StepArgs &a, const void *src, void *dst, const uin
 }
 
 template <int Q, int OP, typename T, bool FLAGS, bool FORCE>
-int collide_launcher(const StepArgs &a, void *f, int, dim3 grid, dim3 block, cudaStream_t s) {
+void collide_launcher(const StepArgs &a, void *f, int, dim3 grid, dim3 block, cudaStream_t s) {
     k_collide<Q, OP, T, FLAGS, FORCE><<<grid, block, 0, s>>>(a, static_cast<T *>(f));
-    return 0;
 }
 
 template <int Q, int OP, typename T, int FM, bool FORCE>
-int eso_launcher(const StepArgs &a, void *f, int odd, dim3 grid, dim3 block, cudaStream_t s) {
+void eso_launcher(const StepArgs &a, void *f, int odd, dim3 grid, dim3 block, cudaStream_t s) {
     if constexpr (FM != FM_INLINE)
         if (a.peer_up != nullptr) {  // fused halo: boundary-plane launch with peer stores (plain kernels)
             if (odd) k_eso<Q, OP, T, FM, FORCE, true, true><<<grid, block, 0, s>>>(a, static_cast<T *>(f));
             else k_eso<Q, OP, T, FM, FORCE, false, true><<<grid, block, 0, s>>>(a, static_cast<T *>(f));
-            return 0;
+            return;
         }
     if (odd ? staged_launch<Q, OP, T, FM, FORCE, SM_ESO_ODD>(a, f, f, (int)grid.z, s)
             : staged_launch<Q, OP, T, FM, FORCE, SM_ESO_EVEN>(a, f, f, (int)grid.z, s))
-        return 0;
+        return;
     if (odd) k_eso<Q, OP, T, FM, FORCE, true><<<grid, block, 0, s>>>(a, static_cast<T *>(f));
     else k_eso<Q, OP, T, FM, FORCE, false><<<grid, block, 0, s>>>(a, static_cast<T *>(f));
-    return 0;
 }
 
 // EdgeLaunch has no parity argument; for EsoTwist the caller (runtime.cu) marks the odd step by a

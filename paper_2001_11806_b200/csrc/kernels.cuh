@@ -168,7 +168,7 @@ __device__ __forceinline__ void pull_cell(const StepArgs &a, const T *__restrict
     // issue back to back — the neighbour's storage always exists, wall or not — and the wall
     // directions are replaced afterwards) and branch-per-direction (fp32 TRT at 40 registers).
     constexpr bool kWalls = FM == FM_INLINE || FM == FM_EDGE;
-    constexpr bool kFixup = kWalls && (sizeof(T) == 8 || op_base(OP) == OP_CUMULANT) && FM == FM_INLINE;
+    constexpr bool kFixup = kWalls && (sizeof(T) == 8 || op_class(op_base(OP)) == OP_CUMULANT) && FM == FM_INLINE;
     T g[Q];
     if constexpr (kWalls && !kFixup) {
 #pragma unroll

@@ -7,6 +7,7 @@
 #include <nvtx3/nvToolsExt.h>
 
 #include <cmath>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <memory>
@@ -206,10 +207,10 @@ void launch_pull_range(lbm_handle_s *h, Slab &s, int z_begin, int nplanes, int z
         a.peer_down = h->fst.bases[2 * (1 - s.cur) + 1];
     }
     tbegin(h, st);
-    const int edges_done = h->kern.pull(a, s.pdf[s.cur], s.pdf[1 - s.cur], grid_for(h, nplanes), h->block, st);
+    h->kern.pull(a, s.pdf[s.cur], s.pdf[1 - s.cur], grid_for(h, nplanes), h->block, st);
     tend(h, st);
     h->launches++;
-    if (!edges_done) launch_edges(h, s, a, h->kern.pull_edges, s.pdf[s.cur], s.pdf[1 - s.cur], z_begin, nplanes, z_step, st);
+    launch_edges(h, s, a, h->kern.pull_edges, s.pdf[s.cur], s.pdf[1 - s.cur], z_begin, nplanes, z_step, st);
 }
 
 void launch_push_range(lbm_handle_s *h, Slab &s, int z_begin, int nplanes, int z_step, cudaStream_t st,
@@ -264,10 +265,10 @@ void launch_aa_range(lbm_handle_s *h, Slab &s, int odd, int z_begin, int nplanes
         a.peer_down = h->fst.bases[1];
     }
     tbegin(h, st);
-    const int edges_done = h->kern.aa(a, s.pdf[0], odd, grid_for(h, nplanes), h->block, st);
+    h->kern.aa(a, s.pdf[0], odd, grid_for(h, nplanes), h->block, st);
     tend(h, st);
     h->launches++;
-    if (odd && !edges_done) launch_edges(h, s, a, h->kern.aa_edges, nullptr, s.pdf[0], z_begin, nplanes, z_step, st);
+    if (odd) launch_edges(h, s, a, h->kern.aa_edges, nullptr, s.pdf[0], z_begin, nplanes, z_step, st);
 }
 
 // Halo exchange phases. Each phase moves, per slab, one set of crossing slots through face A
@@ -761,6 +762,7 @@ Kernels select_kernels(int collision, int Q, int dtype, int fm, bool force, int 
         case LBM_TRT: return select_trt(Q, dtype, fm, force);
         case LBM_MRT: return select_mrt(Q, dtype, fm, force);
         case LBM_CUMULANT: return select_cumulant(Q, dtype, fm, force);
+        case OP_CUMULANT_UNIT: return select_cumulant_unit(Q, dtype, fm, force);
         case LBM_SMAGORINSKY: return select_smagorinsky(Q, dtype, fm, force);
         case LBM_KBC: return select_kbc(Q, dtype, fm, force);
         case LBM_KBC_EXACT: return select_kbc_exact(Q, dtype, fm, force);
@@ -1197,7 +1199,12 @@ int lbm_create(const lbm_config *cfg, lbm_handle *out) {
     // kernel selection (SRT = TRT with equal rates); index-list boundaries run the flag-free kernels
     const int fm_bulk = !h->have_flags || h->links ? FM_NONE : h->inline_bc ? FM_INLINE : FM_BULK;
     const bool per_row = cfg->collision == LBM_MRT && cfg->n_row_rates == 15;
-    const int kcoll = per_row ? (int)OP_MRT_ROWS : cfg->collision;
+    // D3Q27 cumulant whose bulk and higher-order rates are all 1 (C3, G7): the specialised kernels that
+    // skip the relaxations with factor 1 - omega = 0 (collide_cumulant27_unit)
+    bool unit_rates = cfg->collision == LBM_CUMULANT && cfg->stencil == 27 && cfg->equilibrium == LBM_EQ_COMPRESSIBLE &&
+                      std::getenv("LBM_CUMULANT_GENERAL") == nullptr;
+    for (int i = 1; i < 6 && unit_rates; ++i) unit_rates = i >= cfg->n_rates || cfg->rates[i] == 1.0;
+    const int kcoll = per_row ? (int)OP_MRT_ROWS : unit_rates ? (int)OP_CUMULANT_UNIT : cfg->collision;
     const bool force = h->have_force;
     if (cfg->pattern == LBM_PULL || cfg->pattern == LBM_PUSH) {
         h->kern = select_kernels(kcoll, h->Q, h->dtype, fm_bulk, force, cfg->equilibrium);

@@ -140,11 +140,6 @@ __device__ __forceinline__ void stage_issue(const StepArgs &a, const T *f, const
                  a.flags + ((int64_t)tl.zs * ny + tl.y0) * nx, flag_bytes, bar);
 }
 
-// Near-wall fluid cells resolved by the staged bulk kernel itself (pull and AA odd with split flags):
-// their wall directions read the cell's own bounced slot from global memory; no edge-list launch.
-template <int FM, int MODE>
-constexpr bool staged_inline_edges() { return FM == FM_BULK && (MODE == SM_PULL || MODE == SM_AA_ODD); }
-
 template <int Q, int OP, typename T, int FM, bool FORCE, int MODE>
 __global__ void __launch_bounds__(kStagedBT + 32, (StagedMinBlocks<Q, OP, T>::value))
     k_staged(const StepArgs a, const T *src, T *dst, int nplanes, int H, int nstages, int stage_elems) {
@@ -195,16 +190,13 @@ __global__ void __launch_bounds__(kStagedBT + 32, (StagedMinBlocks<Q, OP, T>::va
                 x -= nx;
                 ++h;
             }
-            bool edge = false;  // near-wall fluid cell (flag bit 7), resolved inline below (pull, AA odd)
             if (FM == FM_BULK) {
-                // walls are skipped; near-wall cells are resolved here for the pull and AA odd steps
-                // (staged_inline_edges: no separate edge launch), and belong to the edge kernel for EsoTwist
-                // and push; the AA even step is local, so near-wall cells need nothing special there
+                // walls and near-wall cells belong to the edge kernel (AA even: only walls are skipped;
+                // the even step is local, so near-wall cells need nothing special there)
                 const uint8_t own = sflags ? fl[c]
                                            : a.flags[((uint32_t)tl.zs * (uint32_t)a.geo.ny + (uint32_t)(tl.y0 + hc)) *
                                                          (uint32_t)nx + (uint32_t)xc];
-                if (MODE == SM_AA_EVEN || staged_inline_edges<FM, MODE>() ? (own & 3) != 0 : own != 0) continue;
-                edge = own != 0;
+                if (MODE == SM_AA_EVEN ? (own & 3) != 0 : own != 0) continue;
             }
             const int xm = xc == 0 ? nx - 1 : xc - 1, xp = xc == nx - 1 ? 0 : xc + 1;
             T g[Q];
@@ -214,28 +206,10 @@ __global__ void __launch_bounds__(kStagedBT + 32, (StagedMinBlocks<Q, OP, T>::va
                 const int xs = sx == 0 ? xc : (sx > 0 ? xm : xp);
                 g[q] = buf[q * rowlen + hc * nx + xs];
             }
+            collide<Q, OP, T, FORCE>(g, r);
             const int y = tl.y0 + hc;
             const uint32_t self = ((uint32_t)tl.zs * (uint32_t)a.geo.ny + (uint32_t)y) * (uint32_t)nx + (uint32_t)xc;
             LBM_ASSERT((int64_t)self < Sq && y < a.geo.ny && (a.geo.g ? (tl.zs >= 1 && tl.zs <= a.geo.nz) : tl.zs < a.geo.nz));
-            uint32_t wallmask = 0;  // bit q: x - c_q is a wall (x + c_q for the opposite direction)
-            if constexpr (staged_inline_edges<FM, MODE>()) {
-                if (edge) {
-                    // the population that would stream from a wall x - c_q is the cell's own bounced value
-                    // (pull: src[x](qbar); AA odd: a[x](q), left there by the even step) + the UBB term of q
-                    const Nbr n = neighbours(a.geo, xc, y, tl.zs);
-#pragma unroll
-                    for (int q = 1; q < Q; ++q) {
-                        const uint8_t fq = a.flags[nb_off(a.geo, n, -S::cx(q), -S::cy(q), -S::cz(q))] & 3;
-                        if (fq != 0) {
-                            wallmask |= 1u << q;
-                            T v = MODE == SM_PULL ? src[S::opp(q) * Sq + self] : dst[q * Sq + self];
-                            if (fq == 2) v += ubb_term<Q, T>(a, q);
-                            g[q] = v;
-                        }
-                    }
-                }
-            }
-            collide<Q, OP, T, FORCE>(g, r);
             if constexpr (MODE == SM_PULL) {
 #pragma unroll
                 for (int q = 0; q < Q; ++q) dst[q * Sq + self] = g[q];
@@ -253,24 +227,10 @@ __global__ void __launch_bounds__(kStagedBT + 32, (StagedMinBlocks<Q, OP, T>::va
                 for (int q = 0; q < Q; ++q)
                     dst[(MODE == SM_ESO_ODD ? q : S::opp(q)) * Sq + nb_off(a.geo, n, cneg(S::cx(q)), cneg(S::cy(q)), cneg(S::cz(q)))] =
                         g[q];
-            } else {  // AA odd: push to x + c_q; toward a wall it returns next step as qbar, kept in a[x](qbar)
+            } else {
                 const Nbr n = neighbours(a.geo, xc, y, tl.zs);
-                if (FM != FM_BULK || !edge) {
 #pragma unroll
-                    for (int q = 0; q < Q; ++q) dst[q * Sq + nb_off(a.geo, n, S::cx(q), S::cy(q), S::cz(q))] = g[q];
-                } else {
-#pragma unroll
-                    for (int q = 0; q < Q; ++q) {
-                        const uint32_t o = nb_off(a.geo, n, S::cx(q), S::cy(q), S::cz(q));
-                        if (wallmask & (1u << S::opp(q))) {
-                            T v = g[q];
-                            if ((a.flags[o] & 3) == 2) v += ubb_term<Q, T>(a, S::opp(q));
-                            dst[S::opp(q) * Sq + self] = v;
-                        } else {
-                            dst[q * Sq + o] = g[q];
-                        }
-                    }
-                }
+                for (int q = 0; q < Q; ++q) dst[q * Sq + nb_off(a.geo, n, S::cx(q), S::cy(q), S::cz(q))] = g[q];
             }
         }
         __syncwarp();

@@ -900,3 +900,23 @@ def test_borrowed_torch_buffers(pattern, geometry, extra):
         np.testing.assert_array_equal(st[mask], lent.populations(raw=True)[mask])
     lent.close()
     own.close()
+
+
+@pytest.mark.parametrize("pattern,geometry,dtype", [("pull", "cavity", "f64"), ("aa", "periodic", "f64"),
+                                                    ("esotwist", "cavity", "f64"), ("pull", "periodic", "f32")])
+def test_cumulant_unit_rate_kernels_match_general(pattern, geometry, dtype, monkeypatch):
+    """D3Q27 cumulant with omega_bulk = omega_3..6 = 1 (C3's rates) runs the specialised kernels
+    (collide_cumulant27_unit: second moments only, Gaussian closure); they match the general kernels
+    (LBM_CUMULANT_GENERAL=1) to rounding and the oracle to the north_star bar."""
+    case = Case("cumu", (16, 16, 16), 27, "cumulant", (1.95,), dtype, pattern=pattern, geometry=geometry,
+                ubb=(0.05, 0, 0), u_amp=0.05, steps=11)
+    unit = make_sim(case)
+    monkeypatch.setenv("LBM_CUMULANT_GENERAL", "1")
+    general = make_sim(case)
+    monkeypatch.delenv("LBM_CUMULANT_GENERAL")
+    for s in (unit, general):
+        init_sim(s, case)
+        s.step(case.steps)
+    mask = fluid_mask(case, 27)
+    assert max_rel_err(unit.populations(), general.populations(), mask) <= (1e-13 if dtype == "f64" else 2e-6)
+    assert max_rel_err(unit.populations(), oracle_run(case), mask) <= TOL[dtype]
