@@ -178,3 +178,52 @@ def test_d3q27_equilibrium_equals_maxwellian_moments_paper():
     # SURVEY G1 scratch: the x^2 y^2 moment differs by -rho u_z^2 / 6
     m22 = float((f19 * c19[:, 0] ** 2 * c19[:, 1] ** 2).sum())
     assert abs(m22 - _maxwellian_moment_trunc2((2, 2, 0), rho, u) - (-rho * u[2] ** 2 / 6)) < 1e-15
+
+
+def test_g6_group_rate_mrt_is_invariant_under_within_order_gram_schmidt_permutations():
+    """DESIGN G6: with one rate per group {shear, bulk, order 3, order >= 4} the MRT operator M^-1 S M does
+    not depend on the order in which Gram-Schmidt meets the moments of one order (each group's span is
+    canonical; shear is weighted-orthogonal to bulk). 12 random within-order permutations of the D3Q19
+    input sequence (shear moments permuted among themselves, bulk kept after them): M^-1 S M is EQUAL in
+    exact rationals."""
+    import random
+    from fractions import Fraction as Fr
+    import numpy as np
+    from oracle import methods as Mt
+    name = "D3Q19"
+    dirs, w = Mt.stencil(name), Mt.weights(name)
+    basis = Mt.monomial_basis(name)
+    basis, bulk = Mt.split_shear_bulk(basis, 3)
+    basis = Mt.sort_moments(basis, bulk)
+    rates = {"conserved": Fr(0), "shear": Fr(19, 10), "bulk": Fr(13, 10), "order3": Fr(11, 10), "order4+": Fr(4, 5)}
+
+    def operator(seq):
+        polys = Mt.gram_schmidt(seq, dirs, w)
+        groups = []
+        for raw in seq:
+            o = Mt.order(raw)
+            groups.append("conserved" if o <= 1 else ("bulk" if raw == bulk else "shear") if o == 2 else
+                          "order3" if o == 3 else "order4+")
+        M = Mt.moment_matrix(polys, dirs)
+        Mi = Mt.mat_inverse(M)
+        n = len(M)
+        SM = [[rates[groups[i]] * M[i][j] for j in range(n)] for i in range(n)]
+        return [[sum((Mi[i][k] * SM[k][j] for k in range(n)), Fr(0)) for j in range(n)] for i in range(n)]
+
+    ref = operator(basis)
+    rng = random.Random(7)
+    for _ in range(12):
+        seq = []
+        for o in range(5):
+            block = [p for p in basis if Mt.order(p) == o and p != bulk]
+            rng.shuffle(block)
+            seq += block
+            if o == 2:
+                seq.append(bulk)
+        assert len(seq) == len(basis) and seq != basis
+        assert operator(seq) == ref
+    # the check is not vacuous: an order-4 moment met before the (even, non-orthogonal) order-2 ones changes
+    # the operator (before the odd order-3 ones it would not: odd and even moments are orthogonal)
+    o4 = [p for p in basis if Mt.order(p) == 4]
+    seq = [p for p in basis if Mt.order(p) <= 1] + o4[:1] + [p for p in basis if Mt.order(p) in (2, 3)] + o4[1:]
+    assert operator(seq) != ref
