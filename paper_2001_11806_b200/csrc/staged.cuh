@@ -254,9 +254,12 @@ constexpr bool staged_auto() {
     // (AA 512^3 fp64: plain 0.86, staged 0.92 of copy BW; hand-written TRT plain 0.97)
     constexpr bool gen27 = Q == 27 && (op_base(OPX) == OP_GEN_SRT || op_base(OPX) == OP_GEN_TRT);
     // cumulant: staged for AA / EsoTwist (in place), plain for the two-array pull and push kernels
-    // (C3 push: plain 0.906 vs staged 0.857 of copy BW; scripts/gpu_path_sweep.sh)
+    // (C3 push: plain 0.906 vs staged 0.857 of copy BW; scripts/gpu_path_sweep.sh). The unit-rate D3Q27
+    // cumulant (C3's rates, ~650 instead of 1135 FP64 operations) runs plain in every pattern (AA 512^3:
+    // 1.004 vs 0.906; C3 cavity AA + index lists 0.930 vs 0.879; EsoTwist 0.844 vs 0.831; scripts/gpu_r02i.sh)
+    constexpr bool cum_unit = op_base(OPX) == OP_CUMULANT_UNIT;
     return OP == OP_MRT || OP == OP_MRT_ROWS || OP == OP_KBC || OP == OP_SMAGORINSKY ||
-           (OP == OP_CUMULANT && MODE != SM_PULL && MODE != SM_PUSH) || gen27;
+           (OP == OP_CUMULANT && !cum_unit && MODE != SM_PULL && MODE != SM_PUSH) || gen27;
 }
 
 template <int Q, int OP, typename T, int FM, bool FORCE, int MODE>
