@@ -159,11 +159,12 @@ def fluid_cells(cfg, shape, flags):
     return int(np.prod(shape)) if flags is None else int((flags == 0).sum())
 
 
-def bytes_per_cell(cfg, flags):
+def bytes_per_cell(cfg, flags, impl=None):
     """2 q s, + 1 B flag where the update kernel reads a flag field (not with index-list
-    boundaries, whose update kernels are flag-free)."""
+    boundaries, whose update kernels are flag-free, nor with face-aligned walls, recognised from
+    coordinates)."""
     s = 8 if cfg["dtype"] == "f64" else 4
-    reads_flags = flags is not None and cfg.get("boundary_mode", "flags") in ("flags", "inline")
+    reads_flags = flags is not None and cfg.get("boundary_mode", "flags") in ("flags", "inline") and impl != "faces"
     return 2 * cfg["Q"] * s + (1 if reads_flags else 0)
 
 
@@ -522,7 +523,7 @@ def main():
     nf_local = fluid_cells(cfg, (nx, ny, sim.nz_local), fl_local)
     nf_total = nf_local * world if cfg["weak"] else fluid_cells(cfg, gshape, flags)
     mlups = nf_total * args.steps / (t_ms / 1e3) / 1e6
-    bpc = bytes_per_cell(cfg, flags)
+    bpc = bytes_per_cell(cfg, flags, sim.boundary_impl)
     # dominant kernel: the fused stream-collide kernel (the only kernel of a single-GPU step)
     kernel_ms_per_step = kms_max / args.steps
     achieved = nf_local * bpc / (kernel_ms_per_step / 1e3) / 1e9
@@ -594,6 +595,7 @@ def main():
                                 * (2 if cfg["pattern"] in ("pull", "push") else 1)) < 100e6 else cfg.get("note"),
                     "copy_q_gbs": copyq, "frac_of_copy_q": (achieved / copyq) if copyq else None,
                     "boundary_mode": cfg.get("boundary_mode", "flags") if flags is not None else "none",
+                    "boundary_impl": sim.boundary_impl,
                     "kernel_path": L.kernel_path()}
         if cfg.get("alu_bound") and alu is not None:
             # the FP64-ALU-bound operators (exact KBC): the roofline is the measured DFMA ceiling; the HBM

@@ -140,6 +140,17 @@ extern "C" {
 #define LBM_BOUNDARY_FLAGS 0
 #define LBM_BOUNDARY_LINKS 1
 #define LBM_BOUNDARY_INLINE 2
+/* With LBM_BOUNDARY_FLAGS, a flag field whose walls are exactly the faces of the non-periodic axes (each
+ * face one type; a cell on several wall faces takes the first of -x, +x, -y, +y, -z, +z — e.g. the channel
+ * and the lid-driven cavity, G9) runs face-aligned kernels for the pull and AA patterns of the plain-path
+ * operators (SRT/TRT, cumulant): wall and near-wall cells are recognised from their coordinates, no
+ * flag read and no separate boundary launch, same substitutions and results. LBM_FACES=0 in the
+ * environment disables it. lbm_boundary_impl reports what a handle runs. */
+#define LBM_IMPL_NONE 0   /* no flag field */
+#define LBM_IMPL_SPLIT 1  /* bulk kernel + near-wall edge-list kernel */
+#define LBM_IMPL_INLINE 2 /* every cell tests its neighbours' flags */
+#define LBM_IMPL_LINKS 3  /* flag-free update + index-list link kernel */
+#define LBM_IMPL_FACES 4  /* face-aligned walls from coordinates */
 
 #define LBM_HALO_ZEROCOPY 0 /* one NCCL message per crossing population plane */
 #define LBM_HALO_PACKED 1   /* pack kernel + one message per face            */
@@ -217,6 +228,13 @@ void lbm_config_default(lbm_config *cfg);
  * communicator (collective: every rank must call it). The state is zero until an init call. */
 int lbm_create(const lbm_config *cfg, lbm_handle *out);
 int lbm_destroy(lbm_handle h);
+
+/* Host-only: 1 if cfg's flag field is face-aligned (see LBM_IMPL_FACES; face_out = wall type of the faces
+ * -x, +x, -y, +y, -z, +z, 0 = none), 0 if not (or no flag field), LBM_EINVAL / LBM_EUNSUPPORTED if cfg is
+ * invalid. */
+int lbm_detect_faces(const lbm_config *cfg, int8_t face_out[6]);
+/* Boundary implementation the handle runs: LBM_IMPL_* (or LBM_EINVAL). */
+int lbm_boundary_impl(lbm_handle h);
 
 /* Local extent of this process: out[0] = z0 (global index of local plane 0), out[1] = nz_local,
  * out[2] = nx, out[3] = ny. */

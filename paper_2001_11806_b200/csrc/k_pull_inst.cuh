@@ -152,6 +152,7 @@ void pick_persistent(int fm, Kernels &k) {
         (void)fm, (void)k;
         return;
     } else {
+    if (fm == FM_FACES) return;  // (small domains use the flag modes)
     if (fm == FM_NONE) {
         k.persist_pull = &persistent_launcher<Q, OP, T, FM_NONE, FORCE, false>;
         k.persist_aa = &persistent_launcher<Q, OP, T, FM_NONE, FORCE, true>;
@@ -162,8 +163,19 @@ void pick_persistent(int fm, Kernels &k) {
     }
 }
 
+// Face-aligned-wall kernels (FM_FACES) exist for the operators whose bulk update runs the plain kernels
+// (TRT/SRT class, cumulant, identity; the staged operators keep the split flag mode)
+template <int OP>
+constexpr bool faces_supported() {
+    constexpr int c = op_class(op_base(OP));
+    return c == OP_SRT || c == OP_TRT || c == OP_CUMULANT || c == OP_IDENTITY;
+}
+
 template <int Q, int OP, typename T, bool FORCE>
 PullLaunch pick_pull_fm(int fm) {
+    if constexpr (faces_supported<OP>())
+        if (fm == FM_FACES) return &pull_launcher<Q, OP, T, FM_FACES, FORCE>;
+    if (fm == FM_FACES) return nullptr;
     switch (fm) {
         case FM_INLINE: return &pull_launcher<Q, OP, T, FM_INLINE, FORCE>;
         case FM_BULK: return &pull_launcher<Q, OP, T, FM_BULK, FORCE>;
@@ -173,6 +185,7 @@ PullLaunch pick_pull_fm(int fm) {
 
 template <int Q, int OP, typename T, bool FORCE>
 PullLaunch pick_push_fm(int fm) {
+    if (fm == FM_FACES) return nullptr;  // face-aligned walls: pull and AA only
     switch (fm) {
         case FM_INLINE: return &push_launcher<Q, OP, T, FM_INLINE, FORCE>;
         case FM_BULK: return &push_launcher<Q, OP, T, FM_BULK, FORCE>;
@@ -182,6 +195,7 @@ PullLaunch pick_push_fm(int fm) {
 
 template <int Q, int OP, typename T, bool FORCE>
 AALaunch pick_eso_fm(int fm) {
+    if (fm == FM_FACES) return nullptr;  // face-aligned walls: pull and AA only
     switch (fm) {
         case FM_INLINE: return &eso_launcher<Q, OP, T, FM_INLINE, FORCE>;
         case FM_BULK: return &eso_launcher<Q, OP, T, FM_BULK, FORCE>;
@@ -191,6 +205,9 @@ AALaunch pick_eso_fm(int fm) {
 
 template <int Q, int OP, typename T, bool FORCE>
 AALaunch pick_aa_fm(int fm) {
+    if constexpr (faces_supported<OP>())
+        if (fm == FM_FACES) return &aa_launcher<Q, OP, T, FM_FACES, FORCE>;
+    if (fm == FM_FACES) return nullptr;
     switch (fm) {
         case FM_INLINE: return &aa_launcher<Q, OP, T, FM_INLINE, FORCE>;
         case FM_BULK: return &aa_launcher<Q, OP, T, FM_BULK, FORCE>;

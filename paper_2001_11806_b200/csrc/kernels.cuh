@@ -65,6 +65,11 @@ struct StepArgs {
     void *peer_up;                 // fused halo (boundary launch only): base of the up neighbour's
     void *peer_down;               // dst array / down neighbour's dst array (NVLink LSA pointers)
     int stage_flags;               // staged kernels (set by the launcher): flag rows moved by bulk copy
+    // FM_FACES (face-aligned walls): wall type of the faces -x, +x, -y, +y, -z, +z (0 none, 1 no-slip,
+    // 2 UBB; a cell on several wall faces takes the first in this order), global z of interior plane 0
+    // and the global nz
+    int8_t face[6];
+    int zg0, nzg;
 };
 
 constexpr int kMaxDevices = 64;  // per-device caches of launch attributes and occupancy
@@ -141,9 +146,29 @@ __device__ __forceinline__ uint32_t nb_off(const Geo &g, const Nbr &n, int dx, i
 //   FM_BULK   the bulk kernel of the split: cells with any flag bit (walls and near-wall cells)
 //             return after one 1-byte read, so the kernel runs the periodic fast path;
 //   FM_EDGE   the boundary kernel of the split: processes only the near-wall fluid cells given by
-//             an index list (the GPU form of the paper's separate boundary kernels).
+//             an index list (the GPU form of the paper's separate boundary kernels);
+//   FM_FACES  face-aligned walls (every wall cell lies on a domain face, e.g. the channel and cavity of
+//             C1/C3, detected from the flag field at create): wall and near-wall cells are recognised from
+//             their coordinates, no flag read and no separate boundary launch; the same substitutions.
 // =======================================================================================
-enum FMode { FM_NONE = 0, FM_INLINE = 1, FM_BULK = 2, FM_EDGE = 3 };
+enum FMode { FM_NONE = 0, FM_INLINE = 1, FM_BULK = 2, FM_EDGE = 3, FM_FACES = 4 };
+
+// FM_FACES: wall type of the cell at (x, y, global z), 0 for fluid (coordinates one step outside the
+// domain belong to a periodic axis: never a wall)
+__device__ __forceinline__ int face_wall(const StepArgs &a, int x, int y, int zg) {
+    if (a.face[0] && x == 0) return a.face[0];
+    if (a.face[1] && x == a.geo.nx - 1) return a.face[1];
+    if (a.face[2] && y == 0) return a.face[2];
+    if (a.face[3] && y == a.geo.ny - 1) return a.face[3];
+    if (a.face[4] && zg == 0) return a.face[4];
+    if (a.face[5] && zg == a.nzg - 1) return a.face[5];
+    return 0;
+}
+// FM_FACES: a fluid cell with a wall among its neighbours (next to a wall face)
+__device__ __forceinline__ bool near_face(const StepArgs &a, int x, int y, int zg) {
+    return (a.face[0] && x == 1) || (a.face[1] && x == a.geo.nx - 2) || (a.face[2] && y == 1) ||
+           (a.face[3] && y == a.geo.ny - 2) || (a.face[4] && zg == 1) || (a.face[5] && zg == a.nzg - 2);
+}
 
 // =======================================================================================
 // Fused stream-pull-collide, two arrays: dst = C(S(src)) at one fluid cell.
@@ -156,26 +181,37 @@ __device__ __forceinline__ void pull_cell(const StepArgs &a, const T *__restrict
     const uint32_t self = nb_off(a.geo, n, 0, 0, 0);
     const int64_t Sq = a.geo.Sq;
     bool edge = FM == FM_EDGE;
+    int zg = 0;
     if (FM == FM_INLINE) {
         const uint8_t own = a.flags[self];
         if (own & 3) return;  // wall cells are not updated
         edge = (own & 0x80) != 0;
     } else if (FM == FM_BULK) {
         if (a.flags[self] != 0) return;  // walls, and near-wall cells (done by the edge kernel)
+    } else if (FM == FM_FACES) {
+        zg = a.zg0 + zs - a.geo.g;
+        if (face_wall(a, x, y, zg)) return;
+        edge = near_face(a, x, y, zg);
     }
+    // wall type of the cell x - c_q (the source of direction q)
+    auto wall_src = [&](int q) -> int {
+        if constexpr (FM == FM_FACES) return face_wall(a, x - S::cx(q), y - S::cy(q), zg - S::cz(q));
+        else return a.flags[nb_off(a.geo, n, -S::cx(q), -S::cy(q), -S::cz(q))] & 3;
+    };
     // Two strategies for near-wall cells in the inline mode, chosen per kernel family from B200
     // measurements: gather-then-fix-up (fp64 and the cumulant: all Q loads
     // issue back to back — the neighbour's storage always exists, wall or not — and the wall
     // directions are replaced afterwards) and branch-per-direction (fp32 TRT at 40 registers).
-    constexpr bool kWalls = FM == FM_INLINE || FM == FM_EDGE;
-    constexpr bool kFixup = kWalls && (sizeof(T) == 8 || op_class(op_base(OP)) == OP_CUMULANT) && FM == FM_INLINE;
+    constexpr bool kWalls = FM == FM_INLINE || FM == FM_EDGE || FM == FM_FACES;
+    constexpr bool kFixup = kWalls && (sizeof(T) == 8 || op_class(op_base(OP)) == OP_CUMULANT) &&
+                            (FM == FM_INLINE || FM == FM_FACES);
     T g[Q];
     if constexpr (kWalls && !kFixup) {
 #pragma unroll
         for (int q = 0; q < Q; ++q) {
             const uint32_t o = nb_off(a.geo, n, -S::cx(q), -S::cy(q), -S::cz(q));
             if (edge) {
-                const uint8_t fl = a.flags[o] & 3;
+                const int fl = wall_src(q);
                 if (fl == 0) {
                     g[q] = ldg_stream(src + q * Sq + o);
                 } else {
@@ -198,7 +234,7 @@ __device__ __forceinline__ void pull_cell(const StepArgs &a, const T *__restrict
     if (kFixup && edge) {
 #pragma unroll
         for (int q = 0; q < Q; ++q) {
-            const uint8_t fl = a.flags[nb_off(a.geo, n, -S::cx(q), -S::cy(q), -S::cz(q))] & 3;
+            const int fl = wall_src(q);
             if (fl != 0) {
                 T v = ldg_stream(src + S::opp(q) * Sq + self);
                 if (fl == 2) {
@@ -326,13 +362,23 @@ __device__ __forceinline__ void aa_odd_cell(const StepArgs &a, T *__restrict__ f
     const int64_t Sq = a.geo.Sq;
     bool edge = FM == FM_EDGE;
     const uint32_t self = nb_off(a.geo, n, 0, 0, 0);
+    int zg = 0;
     if (FM == FM_INLINE) {
         const uint8_t own = a.flags[self];
         if (own & 3) return;
         edge = (own & 0x80) != 0;
     } else if (FM == FM_BULK) {
         if (a.flags[self] != 0) return;
+    } else if (FM == FM_FACES) {
+        zg = a.zg0 + zs - a.geo.g;
+        if (face_wall(a, x, y, zg)) return;
+        edge = near_face(a, x, y, zg);
     }
+    // wall type of the cell x + s c_q (s = -1: the source of q, s = +1: the target of q's push)
+    auto wall_at = [&](int q, int sgn) -> int {
+        if constexpr (FM == FM_FACES) return face_wall(a, x + sgn * S::cx(q), y + sgn * S::cy(q), zg + sgn * S::cz(q));
+        else return a.flags[nb_off(a.geo, n, sgn * S::cx(q), sgn * S::cy(q), sgn * S::cz(q))] & 3;
+    };
     // unconditional gather (loads issue back to back), wall directions fixed up in near-wall cells
     T g[Q];
 #pragma unroll
@@ -341,7 +387,7 @@ __device__ __forceinline__ void aa_odd_cell(const StepArgs &a, T *__restrict__ f
     if (edge) {
 #pragma unroll
         for (int q = 0; q < Q; ++q) {
-            const uint8_t fl = a.flags[nb_off(a.geo, n, -S::cx(q), -S::cy(q), -S::cz(q))] & 3;
+            const int fl = wall_at(q, -1);
             if (fl != 0) {
                 wallmask |= 1u << q;
                 T v = f[q * Sq + self];
@@ -373,7 +419,7 @@ __device__ __forceinline__ void aa_odd_cell(const StepArgs &a, T *__restrict__ f
         for (int q = 0; q < Q; ++q) {
             const uint32_t o = nb_off(a.geo, n, S::cx(q), S::cy(q), S::cz(q));
             if (wallmask & (1u << S::opp(q))) {  // x + c_q is a wall: returns next step as qbar
-                const uint8_t fl = a.flags[o] & 3;
+                const int fl = wall_at(q, +1);
                 T v = g[q];
                 if (fl == 2) v += ubb_term<Q, T>(a, S::opp(q));
                 f[S::opp(q) * Sq + self] = v;

@@ -86,7 +86,9 @@ struct lbm_handle_s {
     bool fused = false;       // halo through NVLink peer stores (LBM_HALO_FUSED)
     bool links = false;       // index-list boundaries: flag-free update kernels + link kernel
     bool inline_bc = false;   // compiled-in boundaries: every cell tests its neighbours' flags, no edge kernel
+    bool faces = false;       // face-aligned walls (FM_FACES): walls recognised from coordinates, no edge kernel
     int links_pending = -1;   // fused halo + index lists: deferred link fix of the last step (parity | array << 1)
+    int8_t base_face[6] = {0, 0, 0, 0, 0, 0};  // FM_FACES wall types (detect_faces)
     FusedState fst;
     std::string err;
     dim3 block;
@@ -162,7 +164,7 @@ void tend(lbm_handle_s *h, cudaStream_t s) { tbegin(h, s); }
 // z_begin + k * z_step, k < nplanes), one edge-list launch per contiguous run of planes.
 void launch_edges(lbm_handle_s *h, Slab &s, const StepArgs &a, EdgeLaunch fn, const void *src, void *dst, int z_begin,
                   int nplanes, int z_step, cudaStream_t st) {
-    if (!s.edges || !fn || h->links || h->inline_bc) return;  // links: flag-free update; inline: no edge pass
+    if (!s.edges || !fn || h->links || h->inline_bc || h->faces) return;  // links: flag-free; inline / faces: no edge pass
     auto run = [&](int zlo, int zhi) {  // interior planes [zlo, zhi)
         const int64_t b = s.edge_off[zlo + h->g], e = s.edge_off[zhi + h->g];
         if (e <= b) return;
@@ -202,6 +204,7 @@ void launch_pull_range(lbm_handle_s *h, Slab &s, int z_begin, int nplanes, int z
     a.z_begin = z_begin;
     a.z_step = z_step;
     a.flags = s.flags;
+    a.zg0 = (int)s.z0;
     if (peer_stores) {  // fused halo: LSA bases of the neighbours' dst array (1 - cur)
         a.peer_up = h->fst.bases[2 * (1 - s.cur) + 0];
         a.peer_down = h->fst.bases[2 * (1 - s.cur) + 1];
@@ -260,6 +263,7 @@ void launch_aa_range(lbm_handle_s *h, Slab &s, int odd, int z_begin, int nplanes
     a.z_begin = z_begin;
     a.z_step = z_step;
     a.flags = s.flags;
+    a.zg0 = (int)s.z0;
     if (peer_stores) {  // fused halo: LSA bases of the neighbours' single array
         a.peer_up = h->fst.bases[0];
         a.peer_down = h->fst.bases[1];
@@ -684,6 +688,39 @@ int validate(const lbm_config *c) {
         }
     }
     return LBM_OK;
+}
+
+// Face-aligned walls (FM_FACES): every non-fluid cell lies on a face of a non-periodic axis, each such
+// face carries one wall type, and a cell on several wall faces has the type of the first face in the
+// order -x, +x, -y, +y, -z, +z (the channel of C1, the cavity of C3 with its NoSlip lid edges, G9). Then
+// the update kernels recognise wall and near-wall cells from coordinates. O(cells) host check at create.
+bool detect_faces(const lbm_config *c, int8_t face[6]) {
+    const int64_t n[3] = {c->global[0], c->global[1], c->global[2]};
+    for (int f = 0; f < 6; ++f) face[f] = 0;
+    bool any = false;
+    for (int d = 0; d < 3; ++d) {
+        if (c->periodic[d]) continue;
+        if (n[d] < 3) return false;
+        for (int side = 0; side < 2; ++side) {
+            int64_t co[3] = {n[0] / 2, n[1] / 2, n[2] / 2};
+            co[d] = side ? n[d] - 1 : 0;
+            const uint8_t t = c->flags[co[0] + n[0] * (co[1] + n[1] * co[2])];
+            if (t != LBM_FLAG_NOSLIP && t != LBM_FLAG_UBB) return false;
+            face[2 * d + side] = (int8_t)t;
+            any = true;
+        }
+    }
+    if (!any) return false;
+    for (int64_t z = 0; z < n[2]; ++z)
+        for (int64_t y = 0; y < n[1]; ++y)
+            for (int64_t x = 0; x < n[0]; ++x) {
+                const int64_t co[3] = {x, y, z};
+                int expect = 0;
+                for (int f = 0; f < 6 && !expect; ++f)
+                    if (face[f] && co[f / 2] == ((f & 1) ? n[f / 2] - 1 : 0)) expect = face[f];
+                if (c->flags[x + n[0] * (y + n[1] * z)] != expect) return false;
+            }
+    return true;
 }
 
 // per-link UBB terms 6 w_q rho_w c_q.u_w (rho_w = 1, G8) from per-link wall velocities uw[3*i+d];
@@ -1196,8 +1233,16 @@ int lbm_create(const lbm_config *cfg, lbm_handle *out) {
     h->links = cfg->boundary_mode == LBM_BOUNDARY_LINKS && h->have_flags;
     h->inline_bc = cfg->boundary_mode == LBM_BOUNDARY_INLINE && h->have_flags;
 
-    // kernel selection (SRT = TRT with equal rates); index-list boundaries run the flag-free kernels
-    const int fm_bulk = !h->have_flags || h->links ? FM_NONE : h->inline_bc ? FM_INLINE : FM_BULK;
+    // kernel selection (SRT = TRT with equal rates); index-list boundaries run the flag-free kernels;
+    // flag boundaries on face-aligned walls run the FM_FACES kernels (pull and AA, plain-path operators)
+    const bool face_op = (cfg->collision == LBM_SRT || cfg->collision == LBM_TRT || cfg->collision == LBM_CUMULANT ||
+                          cfg->collision == LBM_IDENTITY ||
+                          ((cfg->collision == LBM_GEN_SRT || cfg->collision == LBM_GEN_TRT) && cfg->stencil == 19));
+    const char *faces_env = std::getenv("LBM_FACES");
+    h->faces = cfg->boundary_mode == LBM_BOUNDARY_FLAGS && h->have_flags && face_op &&
+               (cfg->pattern == LBM_PULL || cfg->pattern == LBM_AA) && !(faces_env && faces_env[0] == '0') &&
+               detect_faces(cfg, h->base_face);
+    const int fm_bulk = !h->have_flags || h->links ? FM_NONE : h->inline_bc ? FM_INLINE : h->faces ? FM_FACES : FM_BULK;
     const bool per_row = cfg->collision == LBM_MRT && cfg->n_row_rates == 15;
     // D3Q27 cumulant whose bulk and higher-order rates are all 1 (C3, G7): the specialised kernels that
     // skip the relaxations with factor 1 - omega = 0 (collide_cumulant27_unit)
@@ -1229,6 +1274,8 @@ int lbm_create(const lbm_config *cfg, lbm_handle *out) {
         b.F[d] = cfg->force[d];
         b.uw[d] = cfg->ubb_velocity[d];
     }
+    for (int f = 0; f < 6; ++f) b.face[f] = h->faces ? h->base_face[f] : 0;
+    b.nzg = (int)h->nzg;
     h->block = cfg->block_x > 0 ? block_for(h->nx, h->ny, cfg->block_x) : block_for(h->nx, h->ny, 0);
 
     CUDA_TRY(nullptr, cudaSetDevice(cfg->device));
@@ -1462,6 +1509,22 @@ int lbm_destroy(lbm_handle h) {
     if (h->scratch) cudaFree(h->scratch);
     delete h;
     return LBM_OK;
+}
+
+int lbm_detect_faces(const lbm_config *cfg, int8_t face_out[6]) {
+    if (!cfg || !face_out) return LBM_EINVAL;
+    const int rc = validate(cfg);
+    if (rc) return rc;
+    if (!cfg->flags) return 0;
+    return detect_faces(cfg, face_out) ? 1 : 0;
+}
+
+int lbm_boundary_impl(lbm_handle h) {
+    if (!h) return LBM_EINVAL;
+    if (!h->have_flags) return LBM_IMPL_NONE;
+    if (h->links) return LBM_IMPL_LINKS;
+    if (h->inline_bc) return LBM_IMPL_INLINE;
+    return h->faces ? LBM_IMPL_FACES : LBM_IMPL_SPLIT;
 }
 
 int lbm_local_extent(lbm_handle h, int64_t out[4]) {

@@ -116,6 +116,8 @@ _SIGS = {
     "lbm_get_kernel_path": ([], _I32),
     "lbm_buffer_sizes": ([C.POINTER(lbm_config), _P], C.c_int),
     "lbm_step_phases_ms": ([_P, _P], C.c_int),
+    "lbm_boundary_impl": ([_P], C.c_int),
+    "lbm_detect_faces": ([C.POINTER(lbm_config), _P], C.c_int),
     "lbm_probe_update": ([_I32, _I32, _I32, _I64, _I64, _I64, _I32, _I32, _P], C.c_int),
     "lbm_probe_fma": ([_I32, _I32, _P], C.c_int),
     "lbm_state_bytes": ([_P], _I64),
@@ -434,6 +436,13 @@ class Simulation:
 
     def enable_kernel_timing(self):
         _check(lbm_kernel_time_ms(self.h, None, None), self.h, "lbm_kernel_time_ms")
+
+    @property
+    def boundary_impl(self) -> str:
+        """What the handle's boundary handling runs: none | split | inline | links | faces."""
+        v = int(lbm_boundary_impl(self.h))
+        _check(v, self.h, "lbm_boundary_impl")
+        return ["none", "split", "inline", "links", "faces"][v]
 
     def step_phases_ms(self):
         """{boundary, exchange, interior}: (begin, end) in ms of the last timed decomposed step."""

@@ -177,3 +177,39 @@ def test_buffer_sizes_and_borrowed_buffer_validation(L):
         assert L.lbm_buffer_sizes(C.byref(cfg), out.ctypes.data) == code, kw
     cfg = _cfg(L, global_=(32, 16, 8), pattern=L.AA, pdf_dev=(0x1000, 0))
     assert L.lbm_buffer_sizes(C.byref(cfg), out.ctypes.data) == 0
+
+
+@pytest.mark.parametrize("geometry,periodic,expect", [
+    ("channel", (1, 0, 1), [0, 0, 1, 1, 0, 0]),
+    ("cavity", (0, 0, 0), [1, 1, 1, 1, 1, 2]),   # lid = UBB face; its edges belong to the x/y faces (G9)
+    ("cavity_z_first", (0, 0, 0), None),        # lid edges UBB: not the -x,+x,-y,+y,-z,+z precedence
+    ("obstacles", (1, 1, 1), None),
+    ("channel_hole", (1, 0, 1), None),
+])
+def test_face_aligned_wall_detection(L, geometry, periodic, expect):
+    """lbm_detect_faces (host-only): the flag fields of C1 (channel) and C3 (cavity) are face-aligned and run
+    the FM_FACES kernels; other geometries keep the flag kernels."""
+    import ctypes as C
+    import lbminputs as LI
+    n = 12
+    if geometry == "channel":
+        fl = LI.channel_flags(n, n, n)
+    elif geometry.startswith("cavity"):
+        fl = LI.cavity_flags(n)
+        if geometry == "cavity_z_first":
+            fl[n - 1, :, :] = LI.UBB
+    elif geometry == "channel_hole":
+        fl = LI.channel_flags(n, n, n)
+        fl[3, 5, 5] = LI.NOSLIP  # an interior obstacle
+    else:
+        fl = LI.random_obstacles(0, n, n, n)
+    fl = np.ascontiguousarray(fl, np.uint8)
+    cfg = _cfg(L, global_=(n, n, n), flags=fl.ctypes.data)
+    for d in range(3):
+        cfg.periodic[d] = periodic[d]
+    out = np.zeros(6, np.int8)
+    r = L.lbm_detect_faces(C.byref(cfg), out.ctypes.data)
+    if expect is None:
+        assert r == 0
+    else:
+        assert r == 1 and out.tolist() == expect

@@ -920,3 +920,65 @@ def test_cumulant_unit_rate_kernels_match_general(pattern, geometry, dtype, monk
     mask = fluid_mask(case, 27)
     assert max_rel_err(unit.populations(), general.populations(), mask) <= (1e-13 if dtype == "f64" else 2e-6)
     assert max_rel_err(unit.populations(), oracle_run(case), mask) <= TOL[dtype]
+
+
+# -----------------------------------------------------------------------------------------
+# Face-aligned walls (FM_FACES): walls recognised from coordinates (channel / cavity flag fields)
+# -----------------------------------------------------------------------------------------
+FACE_CASES = [
+    Case("fc_trt_f64_channel_pull", (20, 18, 12), 19, "trt", (1.6, 0.5), "f64", force=(1e-5, 0, 0), geometry="channel",
+         steps=21),
+    Case("fc_trt_f32_channel_pull", (32, 18, 12), 19, "trt", (1.6, 0.5), "f32", force=(1e-5, 0, 0), geometry="channel",
+         steps=21),
+    Case("fc_cum27_cavity_pull", (14, 14, 14), 27, "cumulant", (1.95,), "f64", geometry="cavity", ubb=(0.05, 0, 0),
+         u_amp=0.03, steps=15),
+    Case("fc_cum27_gen_rates_cavity_aa", (14, 14, 14), 27, "cumulant", (1.8, 1.2, 1.1), "f64", pattern="aa",
+         geometry="cavity", ubb=(0.05, 0, 0), u_amp=0.03, steps=13),
+    Case("fc_trt_q27_cavity_aa_odd", (13, 13, 13), 27, "trt", (1.5, 1.2), "f64", pattern="aa", geometry="cavity",
+         ubb=(0.03, -0.02, 0), steps=11),
+    Case("fc_srt_f32_channel_aa", (32, 16, 10), 19, "srt", (1.7,), "f32", pattern="aa", geometry="channel", steps=12),
+    Case("fc_cum19_channel_pull", (16, 20, 12), 19, "cumulant", (1.9,), "f32", geometry="channel", u_amp=0.03, steps=12),
+]
+
+
+@pytest.mark.parametrize("case", FACE_CASES, ids=lambda c: c.name)
+def test_face_aligned_walls_vs_oracle_and_flag_kernels(case, monkeypatch):
+    """The channel and cavity flag fields run the face-aligned kernels (boundary_impl == "faces"): parity with
+    the oracle, and the same update as the split flag kernels (LBM_FACES=0) to rounding."""
+    sim = make_sim(case)
+    assert sim.boundary_impl == "faces"
+    monkeypatch.setenv("LBM_FACES", "0")
+    ref = make_sim(case)
+    monkeypatch.delenv("LBM_FACES")
+    assert ref.boundary_impl == "split"
+    for s in (sim, ref):
+        init_sim(s, case)
+        s.step(case.steps)
+    mask = fluid_mask(case, case.Q)
+    assert max_rel_err(sim.populations(), oracle_run(case), mask) <= TOL[case.dtype]
+    assert max_rel_err(sim.populations(), ref.populations(), mask) <= (1e-13 if case.dtype == "f64" else 1e-6)
+
+
+@pytest.mark.parametrize("extra", [{"n_local_slabs": 2}, {"n_local_slabs": 4, "halo_mode": 1}, {"nccl_self": True},
+                                   {"nccl_self": True, "halo_mode": 2}])
+@pytest.mark.parametrize("pattern", ["pull", "aa"])
+def test_face_aligned_walls_slabs_bit_identical(extra, pattern):
+    """FM_FACES with a z-slab decomposition: the z walls are global faces (rank 0 bottom, rank P-1 top)."""
+    case = Case("fcdec", (16, 16, 16), 27, "cumulant", (1.95,), "f64", pattern=pattern, geometry="cavity",
+                ubb=(0.05, 0, 0), u_amp=0.03, steps=9)
+    one = make_sim(case)
+    many = make_sim(case, **extra)
+    assert one.boundary_impl == many.boundary_impl == "faces"
+    for s in (one, many):
+        init_sim(s, case)
+        s.step(case.steps)
+    mask = fluid_mask(case, 27)
+    np.testing.assert_array_equal(one.populations(raw=True)[mask], many.populations(raw=True)[mask])
+
+
+def test_non_face_geometries_keep_flag_kernels():
+    case = Case("nofc", (16, 12, 10), 19, "trt", (1.6, 0.5), "f64", geometry="obstacles", steps=1)
+    assert make_sim(case).boundary_impl == "split"
+    assert make_sim(Case("mrtfc", (16, 16, 16), 19, "mrt", (1.9, 1.0, 1.0, 1.0), "f64", geometry="cavity")).boundary_impl == "split"
+    assert make_sim(Case("esofc", (16, 16, 16), 19, "trt", (1.6, 0.5), "f64", pattern="esotwist",
+                         geometry="cavity")).boundary_impl == "split"
