@@ -22,8 +22,9 @@ def main(rnd, configs):
     tr_path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     traffic = json.load(open(tr_path)) if os.path.exists(tr_path) else {}
     for c in configs:
-        rep = os.path.join(ROOT, "gpurun_out", f"prof_{c}.ncu-rep")
-        raw_csv = os.path.join(ROOT, "gpurun_out", f"prof_{c}_raw.csv")
+        src = os.environ.get("PROF_DIR", os.path.join(ROOT, "gpurun_out"))
+        rep = os.path.join(src, f"prof_{c}.ncu-rep")
+        raw_csv = os.path.join(src, f"prof_{c}_raw.csv")
         if os.path.exists(raw_csv):  # exported on the GPU box (reports exceed gpurun's copy-back limit)
             out = open(raw_csv).read()
         else:
