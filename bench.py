@@ -56,15 +56,19 @@ CONFIGS["c4_strong"] = dict(CONFIGS["c4"], shape=(1024, 1024, 1024), weak=False,
                            desc="D3Q19 TRT fp32 1024^3 strong scaling (BASELINE config 4, second part); needs >= 2 GPUs "
                                 "for the 32-bit slab offsets (81.6 GB/GPU at P = 2)")
 CONFIGS["c3_aa"] = dict(CONFIGS["c3"], pattern="aa", desc="D3Q27 cumulant fp64 384^3 lid-driven cavity, AA pattern")
-# C1/C3 run with index-list boundaries (the faster of the two boundary implementations on the B200,
-# DESIGN.md section 6); the *_flags lines keep the compiled-in flag handling for comparison.
+# C1 fp32 / C3 run with index-list boundaries (the fastest boundary implementation there on the B200,
+# DESIGN.md section 6.3); the *_flags lines keep the split flag handling for comparison.
 CONFIGS["c3_aa_links"] = dict(CONFIGS["c3_aa"], boundary_mode="links",
                               desc="D3Q27 cumulant fp64 384^3 lid-driven cavity, AA pattern, index-list boundaries")
-CONFIGS["c3_flags"] = dict(CONFIGS["c3"], desc=CONFIGS["c3"]["desc"] + ", compiled-in flag boundaries")
+CONFIGS["c3_flags"] = dict(CONFIGS["c3"], desc=CONFIGS["c3"]["desc"] + ", split bulk + near-wall edge kernel flag boundaries")
 CONFIGS["c3"] = dict(CONFIGS["c3"], boundary_mode="links", desc=CONFIGS["c3"]["desc"] + ", index-list boundaries")
 CONFIGS["c1_f64_flags"] = dict(CONFIGS["c1_f64"], desc=CONFIGS["c1_f64"]["desc"] + ", compiled-in flag boundaries")
-CONFIGS["c1_f32_flags"] = dict(CONFIGS["c1_f32"], desc=CONFIGS["c1_f32"]["desc"] + ", compiled-in flag boundaries")
-CONFIGS["c1_f64"] = dict(CONFIGS["c1_f64"], boundary_mode="links", desc=CONFIGS["c1_f64"]["desc"] + ", index-list boundaries")
+CONFIGS["c1_f32_flags"] = dict(CONFIGS["c1_f32"], desc=CONFIGS["c1_f32"]["desc"] + ", split bulk + near-wall edge kernel flag boundaries")
+CONFIGS["c1_f64_links"] = dict(CONFIGS["c1_f64"], boundary_mode="links", desc=CONFIGS["c1_f64"]["desc"] + ", index-list boundaries")
+CONFIGS["c1_f64_flags"] = dict(CONFIGS["c1_f64_flags"], faces=False,
+                               desc=CONFIGS["c1_f64"]["desc"] + ", split bulk + near-wall edge kernel flag boundaries")
+# C1 fp64: the face-aligned-wall kernels (walls from coordinates) measured fastest
+CONFIGS["c1_f64"] = dict(CONFIGS["c1_f64"], desc=CONFIGS["c1_f64"]["desc"] + ", flag field, face-aligned-wall kernels")
 CONFIGS["c1_f32"] = dict(CONFIGS["c1_f32"], boundary_mode="links", desc=CONFIGS["c1_f32"]["desc"] + ", index-list boundaries")
 CONFIGS["c3_periodic"] = dict(CONFIGS["c3"], geometry="periodic", init=("random", 1e-3, 0.01),
                               desc="D3Q27 cumulant fp64 384^3 periodic pull (C3 without walls, diagnostic)")
@@ -124,11 +128,9 @@ CONFIGS["fig8_channel_inline"] = dict(CONFIGS["fig8_channel_flags"], boundary_mo
                                       desc="D3Q19 TRT fp64 AA 300x100x100 channel, walls on the y and z faces, "
                                            "compiled-in conditionals in every cell, no boundary launch (Fig. 8 analog)")
 CONFIGS["c1_f64_inline"] = dict(CONFIGS["c1_f64_flags"], boundary_mode="inline",
-                                desc=CONFIGS["c1_f64_flags"]["desc"].replace("compiled-in flag boundaries",
-                                                                             "flags tested in every cell (inline)"))
+                                desc="D3Q19 TRT+Guo fp64 256^3 channel (BASELINE config 1), flags tested in every cell (inline)")
 CONFIGS["c3_inline"] = dict(CONFIGS["c3_flags"], boundary_mode="inline",
-                            desc=CONFIGS["c3_flags"]["desc"].replace("compiled-in flag boundaries",
-                                                                     "flags tested in every cell (inline)"))
+                            desc="D3Q27 cumulant fp64 384^3 lid-driven cavity (BASELINE config 3), flags tested in every cell (inline)")
 CONFIGS["fig10_small"] = dict(_paper, shape=(128, 128, 128), weak=True, op="mrt", rates=(1.9, 1.0, 1.0, 1.0),
                               pattern="aa", desc="D3Q19 weighted MRT fp64 AA 128^3 per GPU, weak scaling "
                                                  "(Fig. 10 small-block analog; report ms_per_step)")
@@ -447,6 +449,9 @@ def main():
         # across GPUs in this build (tests/test_multigpu.py runs it on the first multi-GPU box), and the
         # C4 halo is ~0.2 % of a step, so the default favours the transport that cannot hang a scaling run.
         halo_mode = L.HALO_ZEROCOPY
+
+    if cfg.get("faces") is False:  # the split flag kernels even where the face-aligned ones would run
+        os.environ["LBM_FACES"] = "0"
 
     def make(mode):
         return L.Simulation(gshape, stencil=cfg["Q"], collision=cfg["op"], rates=cfg["rates"], dtype=cfg["dtype"],

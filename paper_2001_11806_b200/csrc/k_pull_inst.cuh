@@ -152,8 +152,7 @@ void pick_persistent(int fm, Kernels &k) {
         (void)fm, (void)k;
         return;
     } else {
-    if (fm == FM_FACES) return;  // (small domains use the flag modes)
-    if (fm == FM_NONE) {
+    if (fm == FM_NONE) {  // (FM_FACES handles: the persistent kernels test the flag field inline)
         k.persist_pull = &persistent_launcher<Q, OP, T, FM_NONE, FORCE, false>;
         k.persist_aa = &persistent_launcher<Q, OP, T, FM_NONE, FORCE, true>;
     } else {
@@ -163,12 +162,12 @@ void pick_persistent(int fm, Kernels &k) {
     }
 }
 
-// Face-aligned-wall kernels (FM_FACES) exist for the operators whose bulk update runs the plain kernels
-// (TRT/SRT class, cumulant, identity; the staged operators keep the split flag mode)
+// Face-aligned-wall kernels (FM_FACES) are instantiated for the TRT/SRT class (the runtime selects them
+// for the D3Q19 fp64 pull kernels, where they measured faster than the split and index-list modes)
 template <int OP>
 constexpr bool faces_supported() {
     constexpr int c = op_class(op_base(OP));
-    return c == OP_SRT || c == OP_TRT || c == OP_CUMULANT || c == OP_IDENTITY;
+    return c == OP_SRT || c == OP_TRT;
 }
 
 template <int Q, int OP, typename T, bool FORCE>

@@ -1234,14 +1234,19 @@ int lbm_create(const lbm_config *cfg, lbm_handle *out) {
     h->inline_bc = cfg->boundary_mode == LBM_BOUNDARY_INLINE && h->have_flags;
 
     // kernel selection (SRT = TRT with equal rates); index-list boundaries run the flag-free kernels;
-    // flag boundaries on face-aligned walls run the FM_FACES kernels (pull and AA, plain-path operators)
-    const bool face_op = (cfg->collision == LBM_SRT || cfg->collision == LBM_TRT || cfg->collision == LBM_CUMULANT ||
-                          cfg->collision == LBM_IDENTITY ||
-                          ((cfg->collision == LBM_GEN_SRT || cfg->collision == LBM_GEN_TRT) && cfg->stencil == 19));
+    // flag boundaries on face-aligned walls run the FM_FACES kernels where they measured fastest on the
+    // B200: D3Q19 SRT/TRT fp64 pull (C1 fp64 1.024 of copy BW vs 1.008 split / 1.009 index lists). For
+    // fp32 (issue-bound: the coordinate tests cost 0.95 -> 0.86), the cumulant (the inline fix-up of the
+    // near-wall cells: C3 0.87 vs 0.94 index lists) and the AA odd step (Fig. 8 0.79 vs 0.81 staged split)
+    // the split / index-list kernels stay. LBM_FACES=1 / 0 forces it on / off.
     const char *faces_env = std::getenv("LBM_FACES");
+    const bool face_op = cfg->collision == LBM_SRT || cfg->collision == LBM_TRT ||
+                         ((cfg->collision == LBM_GEN_SRT || cfg->collision == LBM_GEN_TRT) && cfg->stencil == 19);
+    const bool face_pref = cfg->stencil == 19 && cfg->dtype == LBM_F64 && cfg->pattern == LBM_PULL;
+    const bool face_force = faces_env && faces_env[0] == '1';
     h->faces = cfg->boundary_mode == LBM_BOUNDARY_FLAGS && h->have_flags && face_op &&
-               (cfg->pattern == LBM_PULL || cfg->pattern == LBM_AA) && !(faces_env && faces_env[0] == '0') &&
-               detect_faces(cfg, h->base_face);
+               (cfg->pattern == LBM_PULL || cfg->pattern == LBM_AA) && (face_pref || face_force) &&
+               !(faces_env && faces_env[0] == '0') && detect_faces(cfg, h->base_face);
     const int fm_bulk = !h->have_flags || h->links ? FM_NONE : h->inline_bc ? FM_INLINE : h->faces ? FM_FACES : FM_BULK;
     const bool per_row = cfg->collision == LBM_MRT && cfg->n_row_rates == 15;
     // D3Q27 cumulant whose bulk and higher-order rates are all 1 (C3, G7): the specialised kernels that

@@ -925,26 +925,29 @@ def test_cumulant_unit_rate_kernels_match_general(pattern, geometry, dtype, monk
 # -----------------------------------------------------------------------------------------
 # Face-aligned walls (FM_FACES): walls recognised from coordinates (channel / cavity flag fields)
 # -----------------------------------------------------------------------------------------
-FACE_CASES = [
+FACE_CASES = [  # (default: D3Q19 fp64 pull; the others with LBM_FACES=1)
     Case("fc_trt_f64_channel_pull", (20, 18, 12), 19, "trt", (1.6, 0.5), "f64", force=(1e-5, 0, 0), geometry="channel",
          steps=21),
+    Case("fc_srt_f64_cavity_pull", (14, 14, 14), 19, "srt", (1.8,), "f64", geometry="cavity", ubb=(0.05, 0, 0),
+         u_amp=0.03, steps=17),
     Case("fc_trt_f32_channel_pull", (32, 18, 12), 19, "trt", (1.6, 0.5), "f32", force=(1e-5, 0, 0), geometry="channel",
          steps=21),
-    Case("fc_cum27_cavity_pull", (14, 14, 14), 27, "cumulant", (1.95,), "f64", geometry="cavity", ubb=(0.05, 0, 0),
-         u_amp=0.03, steps=15),
-    Case("fc_cum27_gen_rates_cavity_aa", (14, 14, 14), 27, "cumulant", (1.8, 1.2, 1.1), "f64", pattern="aa",
-         geometry="cavity", ubb=(0.05, 0, 0), u_amp=0.03, steps=13),
     Case("fc_trt_q27_cavity_aa_odd", (13, 13, 13), 27, "trt", (1.5, 1.2), "f64", pattern="aa", geometry="cavity",
          ubb=(0.03, -0.02, 0), steps=11),
     Case("fc_srt_f32_channel_aa", (32, 16, 10), 19, "srt", (1.7,), "f32", pattern="aa", geometry="channel", steps=12),
-    Case("fc_cum19_channel_pull", (16, 20, 12), 19, "cumulant", (1.9,), "f32", geometry="channel", u_amp=0.03, steps=12),
+    Case("fc_gtrt_f64_cavity_pull", (14, 14, 14), 19, "gen_trt", (1.7, 1.1), "f64", geometry="cavity", ubb=(0.05, 0, 0),
+         u_amp=0.03, steps=12),
 ]
 
 
 @pytest.mark.parametrize("case", FACE_CASES, ids=lambda c: c.name)
 def test_face_aligned_walls_vs_oracle_and_flag_kernels(case, monkeypatch):
-    """The channel and cavity flag fields run the face-aligned kernels (boundary_impl == "faces"): parity with
-    the oracle, and the same update as the split flag kernels (LBM_FACES=0) to rounding."""
+    """The channel and cavity flag fields run the face-aligned kernels (boundary_impl == "faces"; chosen by
+    default for D3Q19 fp64 pull, forced with LBM_FACES=1 otherwise): parity with the oracle, and the same
+    update as the split flag kernels (LBM_FACES=0) to rounding."""
+    default = case.Q == 19 and case.dtype == "f64" and case.pattern == "pull"
+    if not default:
+        monkeypatch.setenv("LBM_FACES", "1")
     sim = make_sim(case)
     assert sim.boundary_impl == "faces"
     monkeypatch.setenv("LBM_FACES", "0")
@@ -962,9 +965,10 @@ def test_face_aligned_walls_vs_oracle_and_flag_kernels(case, monkeypatch):
 @pytest.mark.parametrize("extra", [{"n_local_slabs": 2}, {"n_local_slabs": 4, "halo_mode": 1}, {"nccl_self": True},
                                    {"nccl_self": True, "halo_mode": 2}])
 @pytest.mark.parametrize("pattern", ["pull", "aa"])
-def test_face_aligned_walls_slabs_bit_identical(extra, pattern):
+def test_face_aligned_walls_slabs_bit_identical(extra, pattern, monkeypatch):
     """FM_FACES with a z-slab decomposition: the z walls are global faces (rank 0 bottom, rank P-1 top)."""
-    case = Case("fcdec", (16, 16, 16), 27, "cumulant", (1.95,), "f64", pattern=pattern, geometry="cavity",
+    monkeypatch.setenv("LBM_FACES", "1")
+    case = Case("fcdec", (16, 16, 16), 19, "trt", (1.6, 0.5), "f64", pattern=pattern, geometry="cavity",
                 ubb=(0.05, 0, 0), u_amp=0.03, steps=9)
     one = make_sim(case)
     many = make_sim(case, **extra)
@@ -980,5 +984,6 @@ def test_non_face_geometries_keep_flag_kernels():
     case = Case("nofc", (16, 12, 10), 19, "trt", (1.6, 0.5), "f64", geometry="obstacles", steps=1)
     assert make_sim(case).boundary_impl == "split"
     assert make_sim(Case("mrtfc", (16, 16, 16), 19, "mrt", (1.9, 1.0, 1.0, 1.0), "f64", geometry="cavity")).boundary_impl == "split"
+    assert make_sim(Case("cumfc", (16, 16, 16), 27, "cumulant", (1.95,), "f64", geometry="cavity")).boundary_impl == "split"
     assert make_sim(Case("esofc", (16, 16, 16), 19, "trt", (1.6, 0.5), "f64", pattern="esotwist",
                          geometry="cavity")).boundary_impl == "split"
