@@ -976,7 +976,7 @@ def test_face_aligned_walls_slabs_bit_identical(extra, pattern, monkeypatch):
     for s in (one, many):
         init_sim(s, case)
         s.step(case.steps)
-    mask = fluid_mask(case, 27)
+    mask = fluid_mask(case, case.Q)
     np.testing.assert_array_equal(one.populations(raw=True)[mask], many.populations(raw=True)[mask])
 
 
