@@ -109,6 +109,11 @@ extern "C" {
 
 #define LBM_HOST 0   /* pointer argument is host memory   */
 #define LBM_DEVICE 1 /* pointer argument is device memory */
+#define LBM_HOST_ASYNC 2 /* host memory (pinned for overlap), asynchronous: lbm_init_equilibrium and
+                            lbm_get_macroscopic return once the work is enqueued; uploads and downloads run on
+                            their own streams (double-buffered device staging, PCIe full duplex) overlapped with
+                            the compute stream. Inputs must stay unchanged and outputs are valid only after
+                            lbm_sync. Other calls ignore it (treated as LBM_HOST where accepted). */
 
 /* Equilibrium of SRT/TRT/MRT:
  * COMPRESSIBLE   Eq. (3), 2nd order, rho0 = rho; u = j / rho (G1; default)

@@ -82,6 +82,16 @@ struct lbm_handle_s {
     int *d_nanflag = nullptr;
     double *scratch = nullptr;
     size_t scratch_bytes = 0;
+    // asynchronous host I/O (LBM_HOST_ASYNC): double-buffered device staging of rho/u, uploads on h2d_stream
+    // and downloads on d2h_stream (PCIe is full duplex) overlapped with the compute stream
+    struct AsyncIO {
+        bool ready = false;
+        cudaStream_t h2d = nullptr, d2h = nullptr;
+        double *in[2] = {nullptr, nullptr}, *out[2] = {nullptr, nullptr};
+        cudaEvent_t in_ready[2] = {nullptr, nullptr}, in_free[2] = {nullptr, nullptr};
+        cudaEvent_t out_ready[2] = {nullptr, nullptr}, out_free[2] = {nullptr, nullptr};
+        int in_k = 0, out_k = 0;
+    } aio;
     Timing timing;
     bool fused = false;       // halo through NVLink peer stores (LBM_HALO_FUSED)
     bool links = false;       // index-list boundaries: flag-free update kernels + link kernel
@@ -761,6 +771,40 @@ dim3 block_for(int64_t nx, int64_t ny, int bx_req) {
     if (by > ny) by = (int)ny;
     if (by < 1) by = 1;
     return dim3(bx, by, 1);
+}
+
+// staging buffers and streams of LBM_HOST_ASYNC, created on first use (4 doubles per local cell, x 4)
+int ensure_async(lbm_handle h) {
+    auto &a = h->aio;
+    if (a.ready) return LBM_OK;
+    int64_t cells = 0;
+    for (const Slab &s : h->slabs) cells += (int64_t)h->nx * h->ny * s.nz;
+    const size_t bytes = (size_t)cells * 4 * sizeof(double);
+    CUDA_TRY(h, cudaStreamCreateWithFlags(&a.h2d, cudaStreamNonBlocking));
+    CUDA_TRY(h, cudaStreamCreateWithFlags(&a.d2h, cudaStreamNonBlocking));
+    for (int k = 0; k < 2; ++k) {
+        CUDA_TRY(h, cudaMalloc(&a.in[k], bytes));
+        CUDA_TRY(h, cudaMalloc(&a.out[k], bytes));
+        for (cudaEvent_t *e : {&a.in_ready[k], &a.in_free[k], &a.out_ready[k], &a.out_free[k]})
+            CUDA_TRY(h, cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+    }
+    a.ready = true;
+    return LBM_OK;
+}
+
+void free_async(lbm_handle h) {
+    auto &a = h->aio;
+    if (a.h2d) cudaStreamSynchronize(a.h2d);
+    if (a.d2h) cudaStreamSynchronize(a.d2h);
+    for (int k = 0; k < 2; ++k) {
+        if (a.in[k]) cudaFree(a.in[k]);
+        if (a.out[k]) cudaFree(a.out[k]);
+        for (cudaEvent_t e : {a.in_ready[k], a.in_free[k], a.out_ready[k], a.out_free[k]})
+            if (e) cudaEventDestroy(e);
+    }
+    if (a.h2d) cudaStreamDestroy(a.h2d);
+    if (a.d2h) cudaStreamDestroy(a.d2h);
+    a = lbm_handle_s::AsyncIO{};
 }
 
 int ensure_scratch(lbm_handle h, size_t bytes) {
@@ -1488,6 +1532,7 @@ int lbm_destroy(lbm_handle h) {
     if (!h) return LBM_OK;
     if (h->stream) cudaStreamSynchronize(h->stream);
     if (h->comm_stream) cudaStreamSynchronize(h->comm_stream);
+    free_async(h);
     if (h->graph) cudaGraphExecDestroy(h->graph);
     if (h->fused && h->comm) fused_teardown(h->comm, &h->fst);
     for (Slab &s : h->slabs) {
@@ -1546,9 +1591,25 @@ int lbm_local_extent(lbm_handle h, int64_t out[4]) {
 static int init_common(lbm_handle h, InitArgs &a, const double *rho, const double *u, int where) {
     const int64_t cells = local_cells(h);
     const double *drho = rho, *du = u;
+    int async_k = -1;
     if (a.mode == 0) {
         if (!rho || !u) return fail(h, LBM_EINVAL, "null rho/u");
-        if (where == LBM_HOST) {
+        if (where == LBM_HOST_ASYNC) {
+            // upload on the h2d stream into a staging buffer no earlier init still reads; the compute stream
+            // waits for the upload only (earlier steps and downloads keep running)
+            int rc = ensure_async(h);
+            if (rc) return rc;
+            auto &io = h->aio;
+            async_k = io.in_k;
+            io.in_k ^= 1;
+            CUDA_TRY(h, cudaStreamWaitEvent(io.h2d, io.in_free[async_k], 0));
+            CUDA_TRY(h, cudaMemcpyAsync(io.in[async_k], rho, cells * sizeof(double), cudaMemcpyHostToDevice, io.h2d));
+            CUDA_TRY(h, cudaMemcpyAsync(io.in[async_k] + cells, u, 3 * cells * sizeof(double), cudaMemcpyHostToDevice, io.h2d));
+            CUDA_TRY(h, cudaEventRecord(io.in_ready[async_k], io.h2d));
+            CUDA_TRY(h, cudaStreamWaitEvent(h->stream, io.in_ready[async_k], 0));
+            drho = io.in[async_k];
+            du = io.in[async_k] + cells;
+        } else if (where == LBM_HOST) {
             int rc = ensure_scratch(h, (size_t)cells * 4 * sizeof(double));
             if (rc) return rc;
             CUDA_TRY(h, cudaMemcpyAsync(h->scratch, rho, cells * sizeof(double), cudaMemcpyHostToDevice, h->stream));
@@ -1599,6 +1660,10 @@ static int init_common(lbm_handle h, InitArgs &a, const double *rho, const doubl
                 const Geo g = geo_of(h, s);
                 CUDA_TRY(h, cudaMemcpyAsync(s.pdf[1], s.pdf[0], (size_t)g.Sq * h->Q * h->esize, cudaMemcpyDeviceToDevice, h->stream));
             }
+    }
+    if (async_k >= 0) {  // the staging buffer is free again once the init kernels have read it; no host wait
+        CUDA_TRY(h, cudaEventRecord(h->aio.in_free[async_k], h->stream));
+        return LBM_OK;
     }
     CUDA_TRY(h, cudaStreamSynchronize(h->stream));
     return LBM_OK;
@@ -1716,6 +1781,10 @@ int lbm_sync(lbm_handle h) {
     if (!h) return LBM_EINVAL;
     CUDA_TRY(h, cudaStreamSynchronize(h->stream));
     CUDA_TRY(h, cudaStreamSynchronize(h->comm_stream));
+    if (h->aio.ready) {
+        CUDA_TRY(h, cudaStreamSynchronize(h->aio.h2d));
+        CUDA_TRY(h, cudaStreamSynchronize(h->aio.d2h));
+    }
     CUDA_TRY(h, cudaGetLastError());
     return nccl_async_status(h);
 }
@@ -1743,6 +1812,7 @@ int64_t lbm_state_bytes(lbm_handle h) {
 
 int lbm_save_state(lbm_handle h, void *out, int32_t where, int64_t *steps_done) {
     if (!h || !out) return LBM_EINVAL;
+    if (where == LBM_HOST_ASYNC) where = LBM_HOST;  // synchronous call
     const cudaMemcpyKind kind = where == LBM_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
     char *dst = static_cast<char *>(out);
     for (Slab &s : h->slabs) {
@@ -1757,6 +1827,7 @@ int lbm_save_state(lbm_handle h, void *out, int32_t where, int64_t *steps_done) 
 
 int lbm_load_state(lbm_handle h, const void *in, int32_t where, int64_t steps_done) {
     if (!h || !in || steps_done < 0) return LBM_EINVAL;
+    if (where == LBM_HOST_ASYNC) where = LBM_HOST;  // synchronous call
     const cudaMemcpyKind kind = where == LBM_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
     const char *src = static_cast<const char *>(in);
     for (Slab &s : h->slabs) {
@@ -1814,6 +1885,7 @@ static int read_common(lbm_handle h, ReadArgs &r, int raw, const Slab &s) {
 
 int lbm_get_populations(lbm_handle h, double *out, int32_t where, int32_t raw) {
     if (!h || !out) return LBM_EINVAL;
+    if (where == LBM_HOST_ASYNC) where = LBM_HOST;  // synchronous call
     const int64_t cells = local_cells(h);
     double *dst = out;
     if (where == LBM_HOST) {
@@ -1879,6 +1951,7 @@ int lbm_get_populations_at(lbm_handle h, const int64_t *cells, int64_t n, double
 
 int lbm_set_populations(lbm_handle h, const double *in, int32_t where, int32_t raw) {
     if (!h || !in) return LBM_EINVAL;
+    if (where == LBM_HOST_ASYNC) where = LBM_HOST;  // synchronous call
     const int64_t cells = local_cells(h);
     int rc = ensure_scratch(h, (size_t)cells * h->Q * sizeof(double) * 2);
     if (rc) return rc;
@@ -1919,6 +1992,30 @@ int lbm_set_populations(lbm_handle h, const double *in, int32_t where, int32_t r
 int lbm_get_macroscopic(lbm_handle h, double *rho, double *u, int32_t where) {
     if (!h || !rho || !u) return LBM_EINVAL;
     const int64_t cells = local_cells(h);
+    if (where == LBM_HOST_ASYNC && h->slabs.size() == 1) {
+        // macro kernel on the compute stream into a staging buffer whose previous download finished, then the
+        // download on the d2h stream; returns without waiting (outputs valid after lbm_sync)
+        int rc = ensure_async(h);
+        if (rc) return rc;
+        auto &io = h->aio;
+        const int k = io.out_k;
+        io.out_k ^= 1;
+        Slab &s = h->slabs[0];
+        ReadArgs r;
+        std::memset(&r, 0, sizeof(r));
+        read_common(h, r, 0, s);
+        r.geo = geo_of(h, s);
+        CUDA_TRY(h, cudaStreamWaitEvent(h->stream, io.out_free[k], 0));
+        launch_macro(h->Q, h->dtype, r, s.pdf[cur_array(h, s)], io.out[k], io.out[k] + cells,
+                     dim3((unsigned)((h->nx + 31) / 32), (unsigned)((h->ny + 7) / 8), (unsigned)s.nz), dim3(32, 8, 1), h->stream);
+        CUDA_TRY(h, cudaEventRecord(io.out_ready[k], h->stream));
+        CUDA_TRY(h, cudaStreamWaitEvent(io.d2h, io.out_ready[k], 0));
+        CUDA_TRY(h, cudaMemcpyAsync(rho, io.out[k], cells * sizeof(double), cudaMemcpyDeviceToHost, io.d2h));
+        CUDA_TRY(h, cudaMemcpyAsync(u, io.out[k] + cells, 3 * cells * sizeof(double), cudaMemcpyDeviceToHost, io.d2h));
+        CUDA_TRY(h, cudaEventRecord(io.out_free[k], io.d2h));
+        return LBM_OK;
+    }
+    if (where == LBM_HOST_ASYNC) where = LBM_HOST;  // several local slabs: synchronous gather
     double *drho = rho, *du = u;
     if (where == LBM_HOST || h->slabs.size() > 1) {
         int rc = ensure_scratch(h, (size_t)cells * 4 * sizeof(double) * 2);
@@ -1959,6 +2056,7 @@ int lbm_get_macroscopic(lbm_handle h, double *rho, double *u, int32_t where) {
 
 int lbm_pack_face(lbm_handle h, int64_t z, int32_t dir, double *out, int32_t where) {
     if (!h || !out || (dir != 1 && dir != -1)) return LBM_EINVAL;
+    if (where == LBM_HOST_ASYNC) where = LBM_HOST;  // synchronous call
     // z is a local interior plane across the concatenated slabs
     int64_t zz = z;
     Slab *sp = nullptr;

@@ -25,7 +25,7 @@ SRT, TRT, MRT, CUMULANT, IDENTITY, SMAGORINSKY, KBC, KBC_EXACT, GEN_SRT, GEN_TRT
 F64, F32 = 0, 1
 PULL, AA, ESOTWIST, PUSH = 0, 1, 2, 3
 FLUID, NOSLIP, UBB = 0, 1, 2
-HOST, DEVICE = 0, 1
+HOST, DEVICE, HOST_ASYNC = 0, 1, 2
 HALO_ZEROCOPY, HALO_PACKED, HALO_FUSED = 0, 1, 2
 PATH_AUTO, PATH_PLAIN, PATH_STAGED = 0, 1, 2
 EQ_COMPRESSIBLE, EQ_INCOMPRESSIBLE, EQ_MOMENT_MATCHED = 0, 1, 2
