@@ -534,6 +534,18 @@ def main():
     achieved = nf_local * bpc / (kernel_ms_per_step / 1e3) / 1e9
     peak, peak_src = load_peaks()
     clocks = clk.summary()
+    phases = None
+    if exchanging and use_graph != 1:  # one timed step's phase timeline (boundary / exchange / interior), after the timed region
+        sim.enable_kernel_timing()
+        sim.step(1)
+        try:
+            ph = sim.step_phases_ms()
+            (b0, b1), (x0, x1), (i0, i1) = ph["boundary"], ph["exchange"], ph["interior"]
+            phases = {"boundary_ms": [b0, b1], "exchange_ms": [x0, x1], "interior_ms": [i0, i1],
+                      "exchange_hidden_by_interior": bool(x1 <= i1 and x0 >= i0 - 1e-3),
+                      "note": "CUDA events per phase on the stream it runs on (lbm_step_phases_ms)"}
+        except L.LBMError:
+            phases = None
 
     # ---- end-to-end through the public API with host buffers ------------------------------
     e2e = None
@@ -633,6 +645,7 @@ def main():
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches,
+            "phases": phases,
             "clocks": clocks,
         }
         print(json.dumps(line))
