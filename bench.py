@@ -438,9 +438,12 @@ def main():
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
     small = np.prod(gshape) / P <= 2 ** 21
-    use_graph = (2 if small else 0) if args.graph < 0 else args.graph
+    # small domains: one persistent kernel per lbm_step call; large single-slab domains: the captured two-step
+    # CUDA graph (removes the per-launch CPU overhead and gaps: C1 fp32 0.945 -> 0.958 of copy BW; the roofline
+    # then uses the timed region's time per step, gaps included)
+    use_graph = (2 if small else 1) if args.graph < 0 else args.graph
     nccl_self = bool(args.nccl_self) and world == 1
-    use_graph = 0 if nccl_self else use_graph
+    use_graph = 0 if (nccl_self or world > 1) else use_graph  # graphs / persistent kernels: single-slab runs only
     exchanging = world > 1 or nccl_self
     halo_mode = args.halo_mode
     if halo_mode < 0:
@@ -610,6 +613,9 @@ def main():
                     "traffic": load_traffic(args.config), "peak_source": peak_src,
                     "algorithmic_bytes_per_cell": bpc, "cells_per_launch": nf_local,
                     "kernel_ms_per_step": kernel_ms_per_step, "kernel_launches_timed": klaunch,
+                    "kernel_time_source": ("CUDA events around the timed region on the launching stream, per step "
+                                           "(CUDA-graph replay: launch gaps included)") if use_graph == 1 else
+                                          "CUDA events around every launch on its stream, summed per step",
                     "frac_of_nominal_8tbs": achieved / 8000.0,
                     "note": ("L2-resident launch/latency-bound domain: the HBM roofline does not bind "
                              "(one persistent kernel per lbm_step call)")
@@ -639,7 +645,7 @@ def main():
                        "parallelism": f"z-slab x{world}" if world > 1 else
                        ("single GPU, NCCL self-exchange of ghost planes" if nccl_self else "single GPU"),
                        "l2": "inputs larger than L2 (no flush)" if not small else "L2-resident (launch-bound config)",
-                       "halo_mode": {0: "zerocopy NCCL send/recv", 1: "packed NCCL send/recv", 2: "fused NVLink peer stores (NCCL LSA windows)"}[args.halo_mode] if (world > 1 or nccl_self) else "none (single slab, z wraps in-kernel)", "small_domain_mode": {0: "plain launches", 1: "CUDA graph (2-step cycle)", 2: "persistent cooperative kernel"}[use_graph]},
+                       "halo_mode": {0: "zerocopy NCCL send/recv", 1: "packed NCCL send/recv", 2: "fused NVLink peer stores (NCCL LSA windows)"}[args.halo_mode] if (world > 1 or nccl_self) else "none (single slab, z wraps in-kernel)", "launch_mode": {0: "plain launches", 1: "CUDA graph (2-step cycle)", 2: "persistent cooperative kernel"}[use_graph]},
             "roofline": roofline,
             "alu": alu,
             "cpu_baseline": cpu,

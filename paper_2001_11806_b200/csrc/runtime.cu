@@ -1341,7 +1341,11 @@ int lbm_create(const lbm_config *cfg, lbm_handle *out) {
         g_create_error = m;
         return code;
     };
-    if (cudaStreamCreateWithFlags(&h->comm_stream, cudaStreamNonBlocking) != cudaSuccess ||
+    // the comm stream gets the highest priority: the NCCL kernels of the halo exchange are scheduled on SMs as
+    // soon as interior-update blocks retire instead of queueing behind the whole interior launch
+    int prio_lo = 0, prio_hi = 0;
+    cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
+    if (cudaStreamCreateWithPriority(&h->comm_stream, cudaStreamNonBlocking, prio_hi) != cudaSuccess ||
         cudaEventCreateWithFlags(&h->ev_bnd, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&h->ev_x, cudaEventDisableTiming) != cudaSuccess) {
         h->err = "stream/event creation failed";

@@ -3,7 +3,7 @@
 # of the default command, and ncu --set full captures of the dominant kernel of key configs. Each ncu
 # command runs only after the same command exited 0 without ncu.
 set -u
-O=gpurun_out/r02p; mkdir -p $O
+O=${OUT:-gpurun_out/r02p}; mkdir -p $O
 timeout 900 python bench.py > $O/bench_default.log 2>&1; echo "default=$?" >> $O/status.txt
 timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > $O/bench_reference.log 2>&1; echo "reference=$?" >> $O/status.txt
 for c in c0 c1_f64 c1_f32 c2 c3 c1_f64_flags c1_f32_flags c3_flags c3_aa c3_aa_links eso_c4 eso_c2 eso_c3 push_c4 push_c3 \
