@@ -17,7 +17,7 @@ OUT = os.path.join(HERE, "liblbm_b200.so")
 OBJ = os.path.join(HERE, "build_obj")
 SOURCES = ["runtime.cu", "k_misc.cu", "k_fused.cu", "k_select.cu", "k_mrt_rows.cu"]
 # k_inst.cu is compiled once per kernel family: (function, op | eq << 4, Q, dtype, Guo-forced variants too)
-_OPS = [("trt", 1, 1, (19, 27)), ("mrt", 2, 0, (19,)), ("cum", 3, 0, (19, 27)), ("cumu", 12, 0, (27,)), ("ident", 4, 0, (19, 27)),
+_OPS = [("trt", 1, 1, (19, 27)), ("mrt", 2, 0, (19,)), ("cum", 3, 0, (19, 27)), ("cumu", 12, 0, (27,)), ("mrts", 13, 0, (19,)), ("ident", 4, 0, (19, 27)),
         ("smag", 5, 0, (19, 27)), ("kbc", 6, 0, (19, 27)), ("kbcx", 7, 0, (19, 27)),
         ("gsrt", 8, 0, (19, 27)), ("gtrt", 9, 0, (19, 27)), ("gmrt", 10, 0, (19, 27)),  # generated (codegen/)
         ("gsmag", 11, 0, (19, 27)), ("gsrt_inc", 8 | 16, 0, (19, 27)), ("gtrt_inc", 9 | 16, 0, (19, 27)),

@@ -610,6 +610,78 @@ __device__ __forceinline__ void collide_kbc(T (&g)[Q], const Rates<T> &p) {
     }
 }
 
+// Weighted MRT with only the shear group relaxed (omega_bulk = omega_3 = omega_4 = 1: config C2, G6): every
+// other group relaxes to equilibrium, and the weighted shear projector of a non-equilibrium part d is
+// (9/2) w_q (c_q c_q - c^2/3 I) : Pi~ with Pi~ the traceless part of sum_q c c d (the closed form of G6,
+// pinned by the oracle test test_mrt_config2_closed_form; D3Q19 and D3Q27). So
+//   f* = f_eq + (1 - omega_s) (9/2) w_q c_q c_q : Pi~^neq,  Pi^neq = sum_q c c f - rho (c_s^2 I + u u)
+// (Eq. 3), computed from the pair sums: ~60 % of the group-projection operations of collide_mrt19. The
+// run-time counterpart of lbmpy's pre-evaluation of constant relaxation rates.
+template <int Q, typename T>
+__device__ __forceinline__ void collide_mrt_shear(T (&g)[Q], const Rates<T> &p) {
+    using S = Stencil<Q>;
+    T drho, jx, jy, jz;
+    moments0<Q, T>(g, drho, jx, jy, jz);
+    const T rho = T(1) + drho;
+    const T inv = T(1) / rho;
+    const T ux = jx * inv, uy = jy * inv, uz = jz * inv;
+    const T uu15 = T(1.5) * (ux * ux + uy * uy + uz * uz);
+    // second moments of g from the pair sums g_q + g_qbar (f = g + w adds c_s^2 I)
+    T pxx = T(0), pyy = T(0), pzz = T(0), pxy = T(0), pxz = T(0), pyz = T(0);
+#pragma unroll
+    for (int q = 1; q < Q; ++q) {
+        if (q < S::opp(q)) {
+            const int cx = S::cx(q), cy = S::cy(q), cz = S::cz(q);
+            const T sp = g[q] + g[S::opp(q)];
+            if (cx != 0) pxx += sp;
+            if (cy != 0) pyy += sp;
+            if (cz != 0) pzz += sp;
+            if (cx * cy > 0) pxy += sp;
+            if (cx * cy < 0) pxy -= sp;
+            if (cx * cz > 0) pxz += sp;
+            if (cx * cz < 0) pxz -= sp;
+            if (cy * cz > 0) pyz += sp;
+            if (cy * cz < 0) pyz -= sp;
+        }
+    }
+    // non-equilibrium part: Pi(f) - rho (c_s^2 I + u u) = Pi(g) - drho / 3 - rho u u
+    const T third = T(1) / T(3);
+    const T rx = rho * ux, ry = rho * uy, rz = rho * uz;
+    const T nxx = pxx - third * drho - rx * ux, nyy = pyy - third * drho - ry * uy, nzz = pzz - third * drho - rz * uz;
+    const T nxy = pxy - rx * uy, nxz = pxz - rx * uz, nyz = pyz - ry * uz;
+    const T tr3 = third * (nxx + nyy + nzz);
+    const T k = T(4.5) * (T(1) - p.r[0]);
+    const T dxx = k * (nxx - tr3), dyy = k * (nyy - tr3), dzz = k * (nzz - tr3);
+    const T dxy = T(2) * k * nxy, dxz = T(2) * k * nxz, dyz = T(2) * k * nyz;
+    const T w0 = T(S::w(0));
+    g[0] = w0 * drho - w0 * rho * uu15;  // c = 0: the traceless part does not reach the centre
+#pragma unroll
+    for (int q = 1; q < Q; ++q) {
+        if (q < S::opp(q)) {
+            const int b = S::opp(q);
+            const int cx = S::cx(q), cy = S::cy(q), cz = S::cz(q);
+            const T w = T(S::w(q));
+            const T cu = T(cx) * ux + T(cy) * uy + T(cz) * uz;
+            const T wr = w * rho;
+            const T es = w * drho + wr * (T(4.5) * cu * cu - uu15);
+            const T ea = wr * T(3) * cu;
+            T qq = T(0);  // c c : (k Pi~), compile-time coefficients
+            if (cx != 0) qq += dxx;
+            if (cy != 0) qq += dyy;
+            if (cz != 0) qq += dzz;
+            if (cx * cy > 0) qq += dxy;
+            if (cx * cy < 0) qq -= dxy;
+            if (cx * cz > 0) qq += dxz;
+            if (cx * cz < 0) qq -= dxz;
+            if (cy * cz > 0) qq += dyz;
+            if (cy * cz < 0) qq -= dyz;
+            const T sh = w * qq;
+            g[q] = (es + ea) + sh;
+            g[b] = (es - ea) + sh;
+        }
+    }
+}
+
 // ---------------------------------------------------------------------------------------
 // Cumulant, D3Q27.
 // Tensor index of a direction: t = (cx+1)*9 + (cy+1)*3 + (cz+1); after the forward transform
@@ -1000,13 +1072,14 @@ enum Op { OP_SRT = 0, OP_TRT = 1, OP_MRT = 2, OP_CUMULANT = 3, OP_IDENTITY = 4, 
           OP_KBC_EXACT = 7, /* KBC, omega_h by Newton maximisation of Eq. (17) (= LBM_KBC_EXACT) */
           OP_GEN_SRT = 8, OP_GEN_TRT = 9, OP_GEN_MRT = 10, OP_GEN_SMAGORINSKY = 11, /* generated (codegen/, = LBM_GEN_*) */
           OP_CUMULANT_UNIT = 12, /* D3Q27 cumulant with omega_bulk = omega_3..6 = 1 (internal id, selected at create) */
+          OP_MRT_SHEAR = 13, /* weighted MRT with omega_bulk = omega_3 = omega_4 = 1 (internal id, selected at create) */
           OP_MRT_ROWS = 15 /* MRT with one rate per moment (internal id; ABI: LBM_MRT + n_row_rates = 15) */ };
 
 // Operator class for occupancy / kernel-path tuning: the generated operators behave like their
 // hand-written counterparts (TRT-like, MRT-like).
 constexpr int op_class(int op) {
     return (op == OP_GEN_SRT || op == OP_GEN_TRT) ? OP_TRT : op == OP_GEN_MRT ? OP_MRT : op == OP_GEN_SMAGORINSKY ? OP_SMAGORINSKY
-         : op == OP_CUMULANT_UNIT ? OP_CUMULANT : op;
+         : op == OP_CUMULANT_UNIT ? OP_CUMULANT : op == OP_MRT_SHEAR ? OP_MRT : op;
 }
 
 template <int Q, int OPX, typename T, bool FORCE>
@@ -1023,6 +1096,8 @@ __device__ __forceinline__ void collide(T (&g)[Q], const Rates<T> &p) {
     } else if constexpr (OP == OP_CUMULANT) {
         if constexpr (Q == 27) collide_cumulant27<T>(g, p);
         else collide_cumulant19<T>(g, p);
+    } else if constexpr (OP == OP_MRT_SHEAR) {
+        collide_mrt_shear<Q, T>(g, p);
     } else if constexpr (OP == OP_CUMULANT_UNIT) {
         static_assert(Q == 27, "the unit-rate cumulant specialisation is D3Q27");
         collide_cumulant27_unit<T>(g, p);

@@ -36,6 +36,7 @@ Kernels select_mrt_rows(int Q, int dtype, int fm, bool force);
 int mrt_rows_upload();  // per-moment MRT rows -> __constant__ memory of the current device
 Kernels select_cumulant(int Q, int dtype, int fm, bool force);
 Kernels select_cumulant_unit(int Q, int dtype, int fm, bool force);  // D3Q27, omega_bulk = omega_3..6 = 1
+Kernels select_mrt_shear(int Q, int dtype, int fm, bool force);      // D3Q19, omega_bulk = omega_3 = omega_4 = 1
 Kernels select_identity(int Q, int dtype, int fm, bool force);
 Kernels select_smagorinsky(int Q, int dtype, int fm, bool force);
 Kernels select_kbc(int Q, int dtype, int fm, bool force);

@@ -16,6 +16,8 @@ Kernels inst_cum27d(int fm, bool force);
 Kernels inst_cum27f(int fm, bool force);
 Kernels inst_cumu27d(int fm, bool force);
 Kernels inst_cumu27f(int fm, bool force);
+Kernels inst_mrts19d(int fm, bool force);
+Kernels inst_mrts19f(int fm, bool force);
 Kernels inst_ident19d(int fm, bool force);
 Kernels inst_ident19f(int fm, bool force);
 Kernels inst_ident27d(int fm, bool force);
@@ -79,6 +81,10 @@ Kernels select_mrt(int Q, int dtype, int fm, bool force) {
 Kernels select_cumulant(int Q, int dtype, int fm, bool force) {
     if (Q == 19) return dtype == 0 ? inst_cum19d(fm, force) : inst_cum19f(fm, force);
     if (Q == 27) return dtype == 0 ? inst_cum27d(fm, force) : inst_cum27f(fm, force);
+    return Kernels{};
+}
+Kernels select_mrt_shear(int Q, int dtype, int fm, bool force) {
+    if (Q == 19) return dtype == 0 ? inst_mrts19d(fm, force) : inst_mrts19f(fm, force);
     return Kernels{};
 }
 Kernels select_cumulant_unit(int Q, int dtype, int fm, bool force) {

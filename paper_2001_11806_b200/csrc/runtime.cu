@@ -844,6 +844,7 @@ Kernels select_kernels(int collision, int Q, int dtype, int fm, bool force, int 
         case LBM_MRT: return select_mrt(Q, dtype, fm, force);
         case LBM_CUMULANT: return select_cumulant(Q, dtype, fm, force);
         case OP_CUMULANT_UNIT: return select_cumulant_unit(Q, dtype, fm, force);
+        case OP_MRT_SHEAR: return select_mrt_shear(Q, dtype, fm, force);
         case LBM_SMAGORINSKY: return select_smagorinsky(Q, dtype, fm, force);
         case LBM_KBC: return select_kbc(Q, dtype, fm, force);
         case LBM_KBC_EXACT: return select_kbc_exact(Q, dtype, fm, force);
@@ -1298,7 +1299,13 @@ int lbm_create(const lbm_config *cfg, lbm_handle *out) {
     bool unit_rates = cfg->collision == LBM_CUMULANT && cfg->stencil == 27 && cfg->equilibrium == LBM_EQ_COMPRESSIBLE &&
                       std::getenv("LBM_CUMULANT_GENERAL") == nullptr;
     for (int i = 1; i < 6 && unit_rates; ++i) unit_rates = i >= cfg->n_rates || cfg->rates[i] == 1.0;
-    const int kcoll = per_row ? (int)OP_MRT_ROWS : unit_rates ? (int)OP_CUMULANT_UNIT : cfg->collision;
+    // D3Q19 weighted MRT with bulk / order-3 / order-4 rates 1 (C2): only the shear group relaxes
+    // (collide_mrt_shear, the G6 closed form)
+    bool shear_only = cfg->collision == LBM_MRT && !per_row && cfg->stencil == 19 &&
+                      cfg->equilibrium == LBM_EQ_COMPRESSIBLE && std::getenv("LBM_MRT_GENERAL") == nullptr;
+    for (int i = 1; i < 4 && shear_only; ++i) shear_only = i >= cfg->n_rates || cfg->rates[i] == 1.0;
+    const int kcoll = per_row ? (int)OP_MRT_ROWS : unit_rates ? (int)OP_CUMULANT_UNIT
+                    : shear_only ? (int)OP_MRT_SHEAR : cfg->collision;
     const bool force = h->have_force;
     if (cfg->pattern == LBM_PULL || cfg->pattern == LBM_PUSH) {
         h->kern = select_kernels(kcoll, h->Q, h->dtype, fm_bulk, force, cfg->equilibrium);

@@ -1003,3 +1003,23 @@ def test_non_face_geometries_keep_flag_kernels():
     assert make_sim(Case("cumfc", (16, 16, 16), 27, "cumulant", (1.95,), "f64", geometry="cavity")).boundary_impl == "split"
     assert make_sim(Case("esofc", (16, 16, 16), 19, "trt", (1.6, 0.5), "f64", pattern="esotwist",
                          geometry="cavity")).boundary_impl == "split"
+
+
+@pytest.mark.parametrize("pattern,geometry,dtype,Q", [("aa", "periodic", "f32", 19), ("pull", "channel", "f64", 19),
+                                                      ("esotwist", "obstacles", "f64", 19), ("push", "cavity", "f32", 19)])
+def test_mrt_shear_only_kernels_match_general(pattern, geometry, dtype, Q, monkeypatch):
+    """Weighted MRT with omega_bulk = omega_3 = omega_4 = 1 (C2's rates) runs the shear-only kernels
+    (collide_mrt_shear, the G6 closed form); they match the general group-projection kernels
+    (LBM_MRT_GENERAL=1) to rounding and the oracle to the north_star bar."""
+    case = Case("mrts", (16, 16, 16) if geometry == "cavity" else (32, 14, 12), Q, "mrt", (1.9, 1.0, 1.0, 1.0), dtype,
+                pattern=pattern, geometry=geometry, ubb=(0.02, -0.01, 0.03), u_amp=0.03, steps=11)
+    fast = make_sim(case)
+    monkeypatch.setenv("LBM_MRT_GENERAL", "1")
+    general = make_sim(case)
+    monkeypatch.delenv("LBM_MRT_GENERAL")
+    for s in (fast, general):
+        init_sim(s, case)
+        s.step(case.steps)
+    mask = fluid_mask(case, Q)
+    assert max_rel_err(fast.populations(), general.populations(), mask) <= (1e-13 if dtype == "f64" else 2e-6)
+    assert max_rel_err(fast.populations(), oracle_run(case), mask) <= TOL[dtype]
