@@ -258,7 +258,10 @@ constexpr bool staged_auto() {
     // cumulant (C3's rates, ~650 instead of 1135 FP64 operations) runs plain in every pattern (AA 512^3:
     // 1.004 vs 0.906; C3 cavity AA + index lists 0.930 vs 0.879; EsoTwist 0.844 vs 0.831; scripts/gpu_r02i.sh)
     constexpr bool cum_unit = op_base(OPX) == OP_CUMULANT_UNIT;
-    return OP == OP_MRT || OP == OP_MRT_ROWS || OP == OP_KBC || OP == OP_SMAGORINSKY ||
+    // the shear-only weighted MRT (C2's rates) runs plain too: AA 512^3 fp64 0.996 vs 0.942 staged; C2 fp32
+    // 0.918 vs 0.912 (scripts/gpu_r02q.sh)
+    constexpr bool mrt_shear = op_base(OPX) == OP_MRT_SHEAR;
+    return (OP == OP_MRT && !mrt_shear) || OP == OP_MRT_ROWS || OP == OP_KBC || OP == OP_SMAGORINSKY ||
            (OP == OP_CUMULANT && !cum_unit && MODE != SM_PULL && MODE != SM_PUSH) || gen27;
 }
 
