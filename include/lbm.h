@@ -227,10 +227,12 @@ typedef struct lbm_handle_s *lbm_handle;
 void lbm_config_default(lbm_config *cfg);
 
 /* Create a simulation. Validates cfg (LBM_EINVAL: bad enum, rate outside (0,2), nz % nranks != 0,
- * slabs thinner than 2 planes, non-periodic axis without walls on its faces; LBM_EUNSUPPORTED:
- * MRT other than D3Q19, force with operators other than SRT/TRT, fused halo with the AA
- * pattern), allocates device memory and, for nranks > 1 (or nccl_self), creates the NCCL
- * communicator (collective: every rank must call it). The state is zero until an init call. */
+ * slabs thinner than 2 planes, non-periodic axis without walls on its faces, misaligned borrowed
+ * buffers; LBM_EUNSUPPORTED: hand-written MRT other than D3Q19, force with operators other than SRT/TRT,
+ * equilibrium variants with other operators, inline boundaries with the fused halo, borrowed buffers with
+ * several local slabs or the fused halo), allocates (or borrows) device memory and, for nranks > 1 (or
+ * nccl_self), creates the NCCL communicator (collective: every rank must call it). The state is zero until
+ * an init call. */
 int lbm_create(const lbm_config *cfg, lbm_handle *out);
 int lbm_destroy(lbm_handle h);
 

@@ -83,6 +83,41 @@ __device__ __forceinline__ void moments0(const T (&g)[Q], T &drho, T &jx, T &jy,
     }
 }
 
+// The same moments as balanced-tree sums (depth log2 Q instead of a Q-long chain of dependent adds): for the
+// latency-bound fp64 operators (KBC, cumulant) the dependent-add chains of the sequential sums sit on the
+// critical path of every cell. Different rounding order than moments0 (both are Eq. (2) exactly up to
+// rounding; G16).
+__host__ __device__ constexpr int dir_set_n(int Q, int axis, int sign) {
+    int n = 0;
+    for (int q = 0; q < Q; ++q)
+        if (axis < 0 || kC27[q][axis] == sign) ++n;
+    return n;
+}
+__host__ __device__ constexpr int dir_set_idx(int Q, int axis, int sign, int k) {
+    for (int q = 0; q < Q; ++q)
+        if (axis < 0 || kC27[q][axis] == sign) {
+            if (k == 0) return q;
+            --k;
+        }
+    return 0;
+}
+template <int Q, int AX, int SG, int LO, int HI, typename T>
+__device__ __forceinline__ T tree_sum_dirs(const T (&g)[Q]) {
+    if constexpr (HI - LO == 1) {
+        return g[dir_set_idx(Q, AX, SG, LO)];
+    } else {
+        constexpr int M = (LO + HI) / 2;
+        return tree_sum_dirs<Q, AX, SG, LO, M, T>(g) + tree_sum_dirs<Q, AX, SG, M, HI, T>(g);
+    }
+}
+template <int Q, typename T>
+__device__ __forceinline__ void moments0_tree(const T (&g)[Q], T &drho, T &jx, T &jy, T &jz) {
+    drho = tree_sum_dirs<Q, -1, 0, 0, Q, T>(g);
+    jx = tree_sum_dirs<Q, 0, 1, 0, dir_set_n(Q, 0, 1), T>(g) - tree_sum_dirs<Q, 0, -1, 0, dir_set_n(Q, 0, -1), T>(g);
+    jy = tree_sum_dirs<Q, 1, 1, 0, dir_set_n(Q, 1, 1), T>(g) - tree_sum_dirs<Q, 1, -1, 0, dir_set_n(Q, 1, -1), T>(g);
+    jz = tree_sum_dirs<Q, 2, 1, 0, dir_set_n(Q, 2, 1), T>(g) - tree_sum_dirs<Q, 2, -1, 0, dir_set_n(Q, 2, -1), T>(g);
+}
+
 // ---------------------------------------------------------------------------------------
 // TRT (+ Guo). SRT passes we == wo.
 // ---------------------------------------------------------------------------------------
@@ -873,7 +908,7 @@ template <typename T>
 __device__ __forceinline__ void collide_cumulant27_unit(T (&g)[27], const Rates<T> &p) {
     using S = Stencil<27>;
     T drho, jx, jy, jz;
-    moments0<27, T>(g, drho, jx, jy, jz);
+    moments0_tree<27, T>(g, drho, jx, jy, jz);
     const T rho = T(1) + drho;
     const T inv = T(1) / rho;
     const T ux = jx * inv, uy = jy * inv, uz = jz * inv;

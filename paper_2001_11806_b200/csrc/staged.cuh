@@ -47,6 +47,15 @@ __host__ __device__ constexpr int src_slot(int mode, int q) {
 #endif
 constexpr int kStagedBT = LBM_STAGED_BT;
 
+// Consumer threads per CTA. A CTA of 9 warps puts 3 warps on one of the 4 SM sub-partitions, whose 16K
+// registers then cap every thread at 168; the D3Q27 KBC needs more (it spilled ~160 B per thread at 168),
+// so it runs 7 consumer warps + the producer (8 warps, 2 per sub-partition: up to 255 registers).
+template <int Q, int OPX, typename T>
+struct StagedBT {
+    static constexpr int OP = op_class(op_base(OPX));
+    static constexpr int value = (sizeof(T) == 8 && Q == 27 && (OP == OP_KBC || OP == OP_KBC_EXACT)) ? 224 : kStagedBT;
+};
+
 // registers: 65536 / (BT * minBlocks); the heavy fp64 operators get more room
 template <int Q, int OPX, typename T>
 struct StagedMinBlocks {
@@ -55,7 +64,7 @@ struct StagedMinBlocks {
 #ifdef LBM_STAGED_MINB
     static constexpr int value = LBM_STAGED_MINB;
 #else
-    static constexpr int value = (kStagedBT >= 256 ? 1 : 2) * (heavy ? 1 : 2);
+    static constexpr int value = (StagedBT<Q, OPX, T>::value >= 224 ? 1 : 2) * (heavy ? 1 : 2);
 #endif
 };
 
@@ -141,10 +150,10 @@ __device__ __forceinline__ void stage_issue(const StepArgs &a, const T *f, const
 }
 
 template <int Q, int OP, typename T, int FM, bool FORCE, int MODE>
-__global__ void __launch_bounds__(kStagedBT + 32, (StagedMinBlocks<Q, OP, T>::value))
+__global__ void __launch_bounds__(StagedBT<Q, OP, T>::value + 32, (StagedMinBlocks<Q, OP, T>::value))
     k_staged(const StepArgs a, const T *src, T *dst, int nplanes, int H, int nstages, int stage_elems) {
     using S = Stencil<Q>;
-    constexpr int BT = kStagedBT;
+    constexpr int BT = StagedBT<Q, OP, T>::value;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     uint64_t *full = reinterpret_cast<uint64_t *>(smem_raw);  // [nstages]: tile bytes landed
     uint64_t *empty = full + 8;                                 // [nstages]: consumer warps done with it
@@ -271,7 +280,7 @@ bool staged_launch(const StepArgs &a, const void *src, void *dst, int nplanes, c
         (void)a, (void)src, (void)dst, (void)nplanes, (void)s;
         return false;
     } else {
-    constexpr int BT = kStagedBT;
+    constexpr int BT = StagedBT<Q, OP, T>::value;
     const int path = staged_path();
     // AA with the split flag mode: the staged kernels also win for the TRT class, hand-written SRT included
     // (same collide body; Fig. 8 walled channel 0.747 -> 0.805 of copy BW; the flag-free AA kernels stay plain)
