@@ -162,11 +162,12 @@ def fluid_cells(cfg, shape, flags):
 
 
 def bytes_per_cell(cfg, flags, impl=None):
-    """2 q s, + 1 B flag where the update kernel reads a flag field (not with index-list
-    boundaries, whose update kernels are flag-free, nor with face-aligned walls, recognised from
-    coordinates)."""
+    """2 q s, + 1 B flag where the update kernel reads a flag field (not with the separate
+    index-list kernel, whose update kernels are flag-free, nor with face-aligned walls, recognised from
+    coordinates; the in-kernel index lists read one flag byte per cell)."""
     s = 8 if cfg["dtype"] == "f64" else 4
-    reads_flags = flags is not None and cfg.get("boundary_mode", "flags") in ("flags", "inline") and impl != "faces"
+    reads_flags = flags is not None and ((cfg.get("boundary_mode", "flags") in ("flags", "inline") and impl != "faces")
+                                         or impl == "links_fused")
     return 2 * cfg["Q"] * s + (1 if reads_flags else 0)
 
 

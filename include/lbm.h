@@ -138,7 +138,16 @@ extern "C" {
  *        cells and hold meaningless values. Every pattern (EsoTwist: the fix moves the departing slot of
  *        the link's location L = b + c_q^- into its arriving slot, by parity) and any slab decomposition
  *        (the link kernel also fills the wall slots of ghost planes, after the exchange; with the fused
- *        halo a step's fix runs after the next LSA gate, and lbm_step ends with a closing gate). */
+ *        halo a step's fix runs after the next LSA gate, and lbm_step ends with a closing gate).
+ *        In-kernel links (pull and AA, halo modes other than fused; by default for fp64 except D3Q27 AA,
+ *        where it measured at least as fast; LBM_LINKS_FUSED=1 / 0 in the environment forces it on / off):
+ *        the update kernels read one flag byte per cell (wall cells are skipped) and each
+ *        near-wall fluid cell stores, right after its collision, the wall slots of its links that the next
+ *        stream reads — the link kernel's writes, same values, no separate launch and no re-read of the
+ *        fluid slots; links whose wall cell lies in a ghost plane stay with the link kernel (after the
+ *        exchange). Before the first step after init / set / load the full list runs once (priming). A
+ *        call of lbm_set_link_velocities switches the handle to the separate link kernel for good.
+ *        Results are identical to the separate-kernel form. */
 /* LBM_BOUNDARY_INLINE: the flag field compiled into every cell's update ("compiled-in conditionals",
  *        P:1230-1238): the bulk kernels test the flags of all q neighbours of every cell, no separate
  *        boundary launch. Same results as LBM_BOUNDARY_FLAGS. Not with the fused halo (LBM_EUNSUPPORTED). */
@@ -156,6 +165,7 @@ extern "C" {
 #define LBM_IMPL_INLINE 2 /* every cell tests its neighbours' flags */
 #define LBM_IMPL_LINKS 3  /* flag-free update + index-list link kernel */
 #define LBM_IMPL_FACES 4  /* face-aligned walls from coordinates */
+#define LBM_IMPL_LINKS_FUSED 5 /* index lists stored by the pull / AA update kernels (+ residual link kernel) */
 
 #define LBM_HALO_ZEROCOPY 0 /* one NCCL message per crossing population plane */
 #define LBM_HALO_PACKED 1   /* pack kernel + one message per face            */

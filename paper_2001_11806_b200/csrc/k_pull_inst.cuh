@@ -12,7 +12,7 @@ void pull_launcher(const StepArgs &a, const void *src, void *dst, dim3 grid, dim
     // peer stores (fused halo, boundary-plane launches only) are a separate instantiation so the
     // interior kernel carries no extra live registers
     if (a.peer_up == nullptr && staged_launch<Q, OP, T, FM, FORCE, SM_PULL>(a, src, dst, (int)grid.z, s)) return;
-    if constexpr (FM != FM_INLINE)  // the low-level ABI (inline walls) never stores to peers
+    if constexpr (FM != FM_INLINE && FM != FM_LINKS)  // inline walls (low-level ABI) / FM_LINKS: no peer stores
         if (a.peer_up != nullptr) {
             k_pull<Q, OP, T, FM, FORCE, true><<<grid, block, 0, s>>>(a, static_cast<const T *>(src), static_cast<T *>(dst));
             return;
@@ -32,7 +32,7 @@ void pull_edge_launcher(const StepArgs &a, const void *src, void *dst, const uin
 
 template <int Q, int OP, typename T, int FM, bool FORCE>
 void aa_launcher(const StepArgs &a, void *f, int odd, dim3 grid, dim3 block, cudaStream_t s) {
-    if constexpr (FM != FM_INLINE)
+    if constexpr (FM != FM_INLINE && FM != FM_LINKS)
         if (a.peer_up != nullptr) {  // fused halo: boundary-plane launch with peer stores (plain kernels)
             if (odd) k_aa_odd<Q, OP, T, FM, FORCE, true><<<grid, block, 0, s>>>(a, static_cast<T *>(f));
             else k_aa_even<Q, OP, T, (FM != FM_NONE), FORCE, true><<<grid, block, 0, s>>>(a, static_cast<T *>(f));
@@ -41,12 +41,15 @@ void aa_launcher(const StepArgs &a, void *f, int odd, dim3 grid, dim3 block, cud
     if (odd) {
         if (staged_launch<Q, OP, T, FM, FORCE, SM_AA_ODD>(a, f, f, (int)grid.z, s)) return;
     } else {
-        if (staged_launch<Q, OP, T, (FM == FM_NONE ? FM_NONE : FM_BULK), FORCE, SM_AA_EVEN>(a, f, f, (int)grid.z, s)) return;
+        if (staged_launch<Q, OP, T, (FM == FM_NONE ? FM_NONE : FM == FM_LINKS ? FM_LINKS : FM_BULK), FORCE, SM_AA_EVEN>(
+                a, f, f, (int)grid.z, s))
+            return;
     }
     if (odd)
         k_aa_odd<Q, OP, T, FM, FORCE><<<grid, block, 0, s>>>(a, static_cast<T *>(f));
-    else  // the even step is in place: walls are skipped, near-wall cells need nothing special
-        k_aa_even<Q, OP, T, (FM != FM_NONE), FORCE><<<grid, block, 0, s>>>(a, static_cast<T *>(f));
+    else  // the even step is in place: walls are skipped, near-wall cells need nothing special (FM_LINKS:
+          // they fill the wall slots of their links)
+        k_aa_even<Q, OP, T, (FM != FM_NONE), FORCE, false, (FM == FM_LINKS)><<<grid, block, 0, s>>>(a, static_cast<T *>(f));
 }
 
 template <int Q, int OP, typename T, bool FORCE>
@@ -178,13 +181,14 @@ PullLaunch pick_pull_fm(int fm) {
     switch (fm) {
         case FM_INLINE: return &pull_launcher<Q, OP, T, FM_INLINE, FORCE>;
         case FM_BULK: return &pull_launcher<Q, OP, T, FM_BULK, FORCE>;
+        case FM_LINKS: return &pull_launcher<Q, OP, T, FM_LINKS, FORCE>;
         default: return &pull_launcher<Q, OP, T, FM_NONE, FORCE>;
     }
 }
 
 template <int Q, int OP, typename T, bool FORCE>
 PullLaunch pick_push_fm(int fm) {
-    if (fm == FM_FACES) return nullptr;  // face-aligned walls: pull and AA only
+    if (fm == FM_FACES || fm == FM_LINKS) return nullptr;  // face-aligned walls / in-kernel links: pull and AA only
     switch (fm) {
         case FM_INLINE: return &push_launcher<Q, OP, T, FM_INLINE, FORCE>;
         case FM_BULK: return &push_launcher<Q, OP, T, FM_BULK, FORCE>;
@@ -194,7 +198,7 @@ PullLaunch pick_push_fm(int fm) {
 
 template <int Q, int OP, typename T, bool FORCE>
 AALaunch pick_eso_fm(int fm) {
-    if (fm == FM_FACES) return nullptr;  // face-aligned walls: pull and AA only
+    if (fm == FM_FACES || fm == FM_LINKS) return nullptr;  // face-aligned walls / in-kernel links: pull and AA only
     switch (fm) {
         case FM_INLINE: return &eso_launcher<Q, OP, T, FM_INLINE, FORCE>;
         case FM_BULK: return &eso_launcher<Q, OP, T, FM_BULK, FORCE>;
@@ -210,6 +214,7 @@ AALaunch pick_aa_fm(int fm) {
     switch (fm) {
         case FM_INLINE: return &aa_launcher<Q, OP, T, FM_INLINE, FORCE>;
         case FM_BULK: return &aa_launcher<Q, OP, T, FM_BULK, FORCE>;
+        case FM_LINKS: return &aa_launcher<Q, OP, T, FM_LINKS, FORCE>;
         default: return &aa_launcher<Q, OP, T, FM_NONE, FORCE>;
     }
 }

@@ -70,6 +70,10 @@ struct StepArgs {
     // and the global nz
     int8_t face[6];
     int zg0, nzg;
+    // FM_LINKS (in-kernel index-list boundaries): per storage cell, bit q = the cell x - c_q is a wall whose
+    // slot x streams from (the link (b = x - c_q, q) of LBM_BOUNDARY_LINKS), bit 32 + q = that wall is UBB;
+    // read by near-wall fluid cells only
+    const uint64_t *lmask;
 };
 
 constexpr int kMaxDevices = 64;  // per-device caches of launch attributes and occupancy
@@ -87,6 +91,21 @@ __device__ __forceinline__ Rates<T> load_rates(const StepArgs &a) {
 template <typename T>
 __device__ __forceinline__ T ldg_stream(const T *p) {
     return __ldg(p);
+}
+
+// The flag-reading kernels (FM_LINKS, FM_BULK) issue the population loads before they test the cell's flag
+// byte, so the two memory latencies overlap instead of adding up. ptxas sinks loads below a branch whose
+// other side does not use them (even loads from volatile asm), so the early exit consumes them: an XOR of
+// their bit patterns guards a store into a scratch word of the library that nothing reads.
+__device__ __forceinline__ uint64_t bits_of(double v) { return (uint64_t)__double_as_longlong(v); }
+__device__ __forceinline__ uint64_t bits_of(float v) { return (uint64_t)__float_as_uint(v); }
+static __device__ unsigned long long g_lbm_sink;  // one per translation unit (no relocatable device code)
+template <int Q, typename T>
+__device__ __forceinline__ void keep_loads(const T (&g)[Q]) {
+    uint64_t x = 0;
+#pragma unroll
+    for (int q = 0; q < Q; ++q) x ^= bits_of(g[q]);
+    if (x == 0x5bd1e9955bd1e995ull) g_lbm_sink = x;
 }
 
 // Neighbour coordinates for a cell: index arrays [c+1] -> coordinate of the cell at offset c.
@@ -150,8 +169,36 @@ __device__ __forceinline__ uint32_t nb_off(const Geo &g, const Nbr &n, int dx, i
 //   FM_FACES  face-aligned walls (every wall cell lies on a domain face, e.g. the channel and cavity of
 //             C1/C3, detected from the flag field at create): wall and near-wall cells are recognised from
 //             their coordinates, no flag read and no separate boundary launch; the same substitutions.
+//   FM_LINKS  index-list boundaries folded into the update (LBM_BOUNDARY_LINKS, pull and AA): every cell
+//             reads its flag byte (wall cells return), the gathers are unconditional (the wall slots hold
+//             the bounced values), and a near-wall fluid cell writes, after its collision, the wall slots of
+//             its links that the next stream reads — the link kernel's work without its launch
+//             and without re-reading the fluid slots:
+//               pull    dst[x - c_q](q)  = f*_qbar(x) + t_q   (= link mode 0 before the next step)
+//               AA even a[x - c_q](qbar) = f*_qbar(x) + t_q   (= link mode 1)
+//               AA odd  a[x](q)          = f*_qbar(x) + t_q   (= link mode 2: x's push toward the wall)
+//             for every link (b = x - c_q, q) in the cell's mask (StepArgs::lmask), t_q the UBB term. Each such
+//             slot is read by x alone, and no other cell writes it in that step.
 // =======================================================================================
-enum FMode { FM_NONE = 0, FM_INLINE = 1, FM_BULK = 2, FM_EDGE = 3, FM_FACES = 4 };
+enum FMode { FM_NONE = 0, FM_INLINE = 1, FM_BULK = 2, FM_EDGE = 3, FM_FACES = 4, FM_LINKS = 5 };
+
+// UBB term 6 w_q rho_w c_q.u_w (rho_w = 1, G8) in the storage precision
+template <int Q, typename T>
+__device__ __forceinline__ T ubb_term(const StepArgs &a, int q) {
+    using S = Stencil<Q>;
+    const double cu = S::cx(q) * a.uw[0] + S::cy(q) * a.uw[1] + S::cz(q) * a.uw[2];
+    return T(6.0 * S::w(q) * cu);
+}
+
+// FM_LINKS: the value the link (x - c_q, q) of a near-wall cell stores, f*_qbar(x) + t_q, rounded like the
+// link kernel's load + add (an add that is never contracted with the collision's last product)
+__device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ float add_rn(float a, float b) { return __fadd_rn(a, b); }
+template <int Q, typename T>
+__device__ __forceinline__ T link_value(const StepArgs &a, uint64_t m, const T (&g)[Q], int q) {
+    using S = Stencil<Q>;
+    return ((m >> (32 + q)) & 1) ? add_rn(g[S::opp(q)], ubb_term<Q, T>(a, q)) : g[S::opp(q)];
+}
 
 // FM_FACES: wall type of the cell at (x, y, global z), 0 for fluid (coordinates one step outside the
 // domain belong to a periodic axis: never a wall)
@@ -187,12 +234,18 @@ __device__ __forceinline__ void pull_cell(const StepArgs &a, const T *__restrict
         if (own & 3) return;  // wall cells are not updated
         edge = (own & 0x80) != 0;
     } else if (FM == FM_BULK) {
-        if (a.flags[self] != 0) return;  // walls, and near-wall cells (done by the edge kernel)
+        // walls, and near-wall cells (done by the edge kernel); flag first: for the pull kernels the
+        // load-first order measured no better (C3 split 0.83 either way) and the fp32 kernel pays for the
+        // live flag (C1 fp32 split 0.933 -> 0.913)
+        if (a.flags[self] != 0) return;
     } else if (FM == FM_FACES) {
         zg = a.zg0 + zs - a.geo.g;
         if (face_wall(a, x, y, zg)) return;
         edge = near_face(a, x, y, zg);
     }
+    // FM_LINKS: the flag byte is tested after the gathers are issued (every cell's storage exists), so the
+    // population loads do not wait for the flag load
+    const uint8_t own_l = FM == FM_LINKS ? a.flags[self] : 0;
     // wall type of the cell x - c_q (the source of direction q)
     auto wall_src = [&](int q) -> int {
         if constexpr (FM == FM_FACES) return face_wall(a, x - S::cx(q), y - S::cy(q), zg - S::cz(q));
@@ -231,6 +284,13 @@ __device__ __forceinline__ void pull_cell(const StepArgs &a, const T *__restrict
         for (int q = 0; q < Q; ++q)
             g[q] = ldg_stream(src + q * Sq + nb_off(a.geo, n, -S::cx(q), -S::cy(q), -S::cz(q)));
     }
+    if (FM == FM_LINKS) {
+        if (own_l & 3) {  // wall cells are not updated
+            keep_loads<Q, T>(g);
+            return;
+        }
+        edge = (own_l & 0x80) != 0;
+    }
     if (kFixup && edge) {
 #pragma unroll
         for (int q = 0; q < Q; ++q) {
@@ -249,6 +309,12 @@ __device__ __forceinline__ void pull_cell(const StepArgs &a, const T *__restrict
     collide<Q, OP, T, FORCE>(g, r);
 #pragma unroll
     for (int q = 0; q < Q; ++q) dst[q * Sq + self] = g[q];
+    if (FM == FM_LINKS && edge) {
+        const uint64_t m = a.lmask[self];
+#pragma unroll
+        for (int q = 0; q < Q; ++q)
+            if ((m >> q) & 1) dst[q * Sq + nb_off(a.geo, n, -S::cx(q), -S::cy(q), -S::cz(q))] = link_value<Q, T>(a, m, g, q);
+    }
     if (PEER) {
         // fused halo: the crossing populations of the boundary planes also go straight into the
         // neighbours' ghost planes (top plane, c_z = +1 -> up's plane 0; bottom, c_z = -1 -> down's nz+1)
@@ -300,14 +366,6 @@ __global__ void __launch_bounds__(128) k_pull_edges(const StepArgs a, const T *_
 // even: read a[x](q), collide, write a[x](qbar)   (in-place, reversed storage)
 // odd : read a[x - c_q](qbar), collide, write a[x + c_q](q)
 // =======================================================================================
-// UBB term 6 w_q rho_w c_q.u_w (rho_w = 1, G8) in the storage precision
-template <int Q, typename T>
-__device__ __forceinline__ T ubb_term(const StepArgs &a, int q) {
-    using S = Stencil<Q>;
-    const double cu = S::cx(q) * a.uw[0] + S::cy(q) * a.uw[1] + S::cz(q) * a.uw[2];
-    return T(6.0 * S::w(q) * cu);
-}
-
 // Fused AA halo (PEER): the boundary planes' even step also stores the slots the neighbours' odd step
 // pulls across the face into their ghost planes (top plane, slots with c_z = -1 -> up's plane 0;
 // bottom plane, slots with c_z = +1 -> down's plane nz+1), and the odd step stores its pushes across
@@ -315,19 +373,30 @@ __device__ __forceinline__ T ubb_term(const StepArgs &a, int q) {
 // plane, c_z = -1 -> down's plane nz), through NCCL LSA pointers of the single array. These are the
 // fill and return phases of the NCCL path without a pack, a send/recv or a masked unpack (a wall
 // target never receives a push: the odd step's wall rule keeps that value in the cell's own slot).
-template <int Q, int OP, typename T, bool FLAGS, bool FORCE, bool PEER = false>
+template <int Q, int OP, typename T, bool FLAGS, bool FORCE, bool PEER = false, bool LINKS = false>
 __device__ __forceinline__ void aa_even_cell(const StepArgs &a, T *__restrict__ f, int x, int y, int zs) {
     using S = Stencil<Q>;
     const uint32_t self = ((uint32_t)zs * (uint32_t)a.geo.ny + (uint32_t)y) * (uint32_t)a.geo.nx + (uint32_t)x;
     const int64_t Sq = a.geo.Sq;
-    if (FLAGS && (a.flags[self] & 3)) return;  // wall cells are not updated
+    const uint8_t own = FLAGS ? a.flags[self] : 0;
     T g[Q];
 #pragma unroll
     for (int q = 0; q < Q; ++q) g[q] = f[q * Sq + self];
+    if (own & 3) {  // wall cells are not updated (tested after the loads are issued)
+        keep_loads<Q, T>(g);
+        return;
+    }
     const Rates<T> r = load_rates<T>(a);
     collide<Q, OP, T, FORCE>(g, r);
 #pragma unroll
     for (int q = 0; q < Q; ++q) f[S::opp(q) * Sq + self] = g[q];
+    if (LINKS && (own & 0x80)) {  // FM_LINKS: fill the wall slots the odd step streams from
+        const uint64_t m = a.lmask[self];
+        const Nbr n = neighbours(a.geo, x, y, zs);
+#pragma unroll
+        for (int q = 0; q < Q; ++q)
+            if ((m >> q) & 1) f[S::opp(q) * Sq + nb_off(a.geo, n, -S::cx(q), -S::cy(q), -S::cz(q))] = link_value<Q, T>(a, m, g, q);
+    }
     if (PEER) {
         const uint32_t inplane = (uint32_t)y * (uint32_t)a.geo.nx + (uint32_t)x;
         const int64_t plane = (int64_t)a.geo.nx * a.geo.ny;
@@ -346,12 +415,12 @@ __device__ __forceinline__ void aa_even_cell(const StepArgs &a, T *__restrict__ 
     }
 }
 
-template <int Q, int OP, typename T, bool FLAGS, bool FORCE, bool PEER = false>
+template <int Q, int OP, typename T, bool FLAGS, bool FORCE, bool PEER = false, bool LINKS = false>
 __global__ void __launch_bounds__(256, (MinBlocks<Q, OP, T>::aa)) k_aa_even(const StepArgs a, T *__restrict__ f) {
     const int x = blockIdx.x * blockDim.x + threadIdx.x;
     const int y = blockIdx.y * blockDim.y + threadIdx.y;
     if (x >= a.geo.nx || y >= a.geo.ny) return;
-    aa_even_cell<Q, OP, T, FLAGS, FORCE, PEER>(a, f, x, y, a.z_begin + (int)blockIdx.z * a.z_step + a.geo.g);
+    aa_even_cell<Q, OP, T, FLAGS, FORCE, PEER, LINKS>(a, f, x, y, a.z_begin + (int)blockIdx.z * a.z_step + a.geo.g);
     peer_fence<PEER>();
 }
 
@@ -367,13 +436,12 @@ __device__ __forceinline__ void aa_odd_cell(const StepArgs &a, T *__restrict__ f
         const uint8_t own = a.flags[self];
         if (own & 3) return;
         edge = (own & 0x80) != 0;
-    } else if (FM == FM_BULK) {
-        if (a.flags[self] != 0) return;
     } else if (FM == FM_FACES) {
         zg = a.zg0 + zs - a.geo.g;
         if (face_wall(a, x, y, zg)) return;
         edge = near_face(a, x, y, zg);
     }
+    const uint8_t own_l = (FM == FM_LINKS || FM == FM_BULK) ? a.flags[self] : 0;  // tested after the gathers
     // wall type of the cell x + s c_q (s = -1: the source of q, s = +1: the target of q's push)
     auto wall_at = [&](int q, int sgn) -> int {
         if constexpr (FM == FM_FACES) return face_wall(a, x + sgn * S::cx(q), y + sgn * S::cy(q), zg + sgn * S::cz(q));
@@ -383,8 +451,19 @@ __device__ __forceinline__ void aa_odd_cell(const StepArgs &a, T *__restrict__ f
     T g[Q];
 #pragma unroll
     for (int q = 0; q < Q; ++q) g[q] = f[S::opp(q) * Sq + nb_off(a.geo, n, -S::cx(q), -S::cy(q), -S::cz(q))];
+    if (FM == FM_BULK && own_l != 0) {  // walls and near-wall cells (the edge kernel)
+        keep_loads<Q, T>(g);
+        return;
+    }
+    if (FM == FM_LINKS) {
+        if (own_l & 3) {
+            keep_loads<Q, T>(g);
+            return;
+        }
+        edge = (own_l & 0x80) != 0;
+    }
     uint32_t wallmask = 0;  // bit q: x - c_q is a wall (x + c_q for the opposite direction)
-    if (edge) {
+    if (FM != FM_LINKS && edge) {  // (FM_LINKS: the even step filled the wall slots)
 #pragma unroll
         for (int q = 0; q < Q; ++q) {
             const int fl = wall_at(q, -1);
@@ -411,9 +490,15 @@ __device__ __forceinline__ void aa_odd_cell(const StepArgs &a, T *__restrict__ f
             else static_cast<T *>(a.peer_down)[q * Sq + a.geo.nz * plane + inplane] = g[q];
         }
     }
-    if (!edge) {
+    if (FM == FM_LINKS || !edge) {
 #pragma unroll
         for (int q = 0; q < Q; ++q) f[q * Sq + nb_off(a.geo, n, S::cx(q), S::cy(q), S::cz(q))] = g[q];
+        if (FM == FM_LINKS && edge) {  // x's pushes toward walls also return into its own slots
+            const uint64_t m = a.lmask[self];
+#pragma unroll
+            for (int q = 0; q < Q; ++q)
+                if ((m >> q) & 1) f[q * Sq + self] = link_value<Q, T>(a, m, g, q);
+        }
     } else {
 #pragma unroll
         for (int q = 0; q < Q; ++q) {

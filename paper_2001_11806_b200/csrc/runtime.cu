@@ -36,6 +36,16 @@ struct Slab {
     double *link_term = nullptr;
     std::vector<uint32_t> h_link_wall;
     std::vector<uint8_t> h_link_dir, h_link_type;
+    // in-kernel links (FM_LINKS): per storage cell link mask (kernels.cuh StepArgs::lmask), and the residual
+    // list of the links the update kernels cannot store (wall cell in a ghost plane: the exchange overwrites
+    // it), run by the link kernel at the usual points; primed = the wall slots match the current state
+    uint64_t *lmask = nullptr;
+    uint32_t *res_wall = nullptr, *res_fluid = nullptr;
+    uint8_t *res_dir = nullptr;
+    double *res_term = nullptr;
+    uint32_t n_res = 0;
+    std::vector<uint32_t> h_res_idx;  // positions of the residual links in the full list
+    bool links_primed = false;
     void *halo[4] = {nullptr, nullptr, nullptr, nullptr};  // packed mode: send up, send down, recv below, recv above
     int cur = 0;          // index of the array holding the current state (pull)
     bool own_pdf[2] = {true, true}, own_flags = true, own_halo = true;  // false: borrowed (lbm_config.*_dev)
@@ -95,6 +105,8 @@ struct lbm_handle_s {
     Timing timing;
     bool fused = false;       // halo through NVLink peer stores (LBM_HALO_FUSED)
     bool links = false;       // index-list boundaries: flag-free update kernels + link kernel
+    bool links_fused = false; // index lists folded into the pull / AA update kernels (FM_LINKS)
+    Kernels kern_links;       // links_fused: the flag-free kernels of the plain index-list mode (per-link velocities)
     bool inline_bc = false;   // compiled-in boundaries: every cell tests its neighbours' flags, no edge kernel
     bool faces = false;       // face-aligned walls (FM_FACES): walls recognised from coordinates, no edge kernel
     int links_pending = -1;   // fused halo + index lists: deferred link fix of the last step (parity | array << 1)
@@ -190,15 +202,18 @@ void launch_edges(lbm_handle_s *h, Slab &s, const StepArgs &a, EdgeLaunch fn, co
 
 // index-list boundary kernel (mode 0: pull, before the step; 1: AA after even; 2: AA after odd;
 // 3 / 4: EsoTwist after even / odd)
-void launch_links_fix(lbm_handle_s *h, Slab &s, void *f, int mode, cudaStream_t st) {
+// In-kernel links (links_fused): only the residual list, unless `full` (priming the wall slots).
+void launch_links_fix(lbm_handle_s *h, Slab &s, void *f, int mode, cudaStream_t st, bool full = false) {
     if (!h->links || s.h_link_wall.empty()) return;
+    const bool res = h->links_fused && !full;
+    if (res && s.n_res == 0) return;
     LinkArgs a;
     a.Sq = geo_of(h, s).Sq;
-    a.wall = s.link_wall;
-    a.fluid = s.link_fluid;
-    a.dir = s.link_dir;
-    a.term = s.link_term;
-    a.n = (uint32_t)s.h_link_wall.size();
+    a.wall = res ? s.res_wall : s.link_wall;
+    a.fluid = res ? s.res_fluid : s.link_fluid;
+    a.dir = res ? s.res_dir : s.link_dir;
+    a.term = res ? s.res_term : s.link_term;
+    a.n = res ? s.n_res : (uint32_t)s.h_link_wall.size();
     a.mode = mode;
     tbegin(h, st);
     launch_links(h->Q, h->dtype, a, f, st);
@@ -214,6 +229,7 @@ void launch_pull_range(lbm_handle_s *h, Slab &s, int z_begin, int nplanes, int z
     a.z_begin = z_begin;
     a.z_step = z_step;
     a.flags = s.flags;
+    a.lmask = s.lmask;
     a.zg0 = (int)s.z0;
     if (peer_stores) {  // fused halo: LSA bases of the neighbours' dst array (1 - cur)
         a.peer_up = h->fst.bases[2 * (1 - s.cur) + 0];
@@ -273,6 +289,7 @@ void launch_aa_range(lbm_handle_s *h, Slab &s, int odd, int z_begin, int nplanes
     a.z_begin = z_begin;
     a.z_step = z_step;
     a.flags = s.flags;
+    a.lmask = s.lmask;
     a.zg0 = (int)s.z0;
     if (peer_stores) {  // fused halo: LSA bases of the neighbours' single array
         a.peer_up = h->fst.bases[0];
@@ -447,6 +464,22 @@ void links_fix_step(lbm_handle_s *h, Slab &s, int odd, int written, cudaStream_t
 void links_after_step(lbm_handle_s *h, Slab &s, int odd, cudaStream_t st) { links_fix_step(h, s, odd, 1 - s.cur, st); }
 // Fused halo: a step's link fix must follow the neighbours' peer stores of that step, i.e. the next LSA
 // gate; it is deferred to after the next step's gate, or to the closing gate at the end of lbm_step.
+// In-kernel links: before the first step after the state was set from outside (init, set, load), the wall
+// slots the next step streams from are filled from the full list (pull: mode 0; AA before an odd step: mode
+// 1; before an even step nothing is read from walls). Outside any graph capture (lbm_step's entry).
+void links_prime(lbm_handle_s *h, cudaStream_t st) {
+    if (!h->links_fused) return;
+    for (Slab &s : h->slabs) {
+        if (s.links_primed) continue;
+        if (h->cfg.pattern == LBM_PULL) launch_links_fix(h, s, s.pdf[s.cur], 0, st, true);
+        else if (h->aa_parity) launch_links_fix(h, s, s.pdf[0], 1, st, true);
+        s.links_primed = true;
+    }
+}
+void links_unprime(lbm_handle_s *h) {
+    for (Slab &s : h->slabs) s.links_primed = false;
+}
+
 void links_deferred(lbm_handle_s *h, Slab &s, cudaStream_t st) {
     if (h->links_pending < 0) return;
     links_fix_step(h, s, h->links_pending & 1, h->links_pending >> 1, st);
@@ -746,6 +779,11 @@ int upload_link_terms(lbm_handle h, Slab &s, const double *uw) {
         term[i] = 6.0 * w * cu;
     }
     if (n) CUDA_TRY(h, cudaMemcpy(s.link_term, term.data(), n * sizeof(double), cudaMemcpyHostToDevice));
+    if (s.n_res) {
+        std::vector<double> rt(s.n_res);
+        for (uint32_t i = 0; i < s.n_res; ++i) rt[i] = term[s.h_res_idx[i]];
+        CUDA_TRY(h, cudaMemcpy(s.res_term, rt.data(), s.n_res * sizeof(double), cudaMemcpyHostToDevice));
+    }
     return LBM_OK;
 }
 
@@ -903,6 +941,16 @@ int lbm_set_link_velocities(lbm_handle h, const double *uw, int64_t n) {
     for (const Slab &s : h->slabs) total += (int64_t)s.h_link_wall.size();
     if (n != total) return fail(h, LBM_EINVAL, "link count mismatch");
     CUDA_TRY(h, cudaStreamSynchronize(h->stream));  // the terms may be in use by queued link kernels
+    if (h->links_fused) {
+        // per-link velocities: the in-kernel stores use one wall velocity; from here on the separate link
+        // kernel with the full list runs (same state invariants: the wall slots hold the same values)
+        h->links_fused = false;
+        h->kern = h->kern_links;
+        if (h->graph) {
+            cudaGraphExecDestroy(h->graph);
+            h->graph = nullptr;
+        }
+    }
     int64_t off = 0;
     for (Slab &s : h->slabs) {
         const int rc = upload_link_terms(h, s, uw + 3 * off);
@@ -1276,6 +1324,14 @@ int lbm_create(const lbm_config *cfg, lbm_handle *out) {
     h->have_flags = cfg->flags != nullptr;
     h->have_force = cfg->force[0] != 0 || cfg->force[1] != 0 || cfg->force[2] != 0;
     h->links = cfg->boundary_mode == LBM_BOUNDARY_LINKS && h->have_flags;
+    // index lists folded into the pull / AA update kernels (FM_LINKS); the fused halo keeps the link kernel.
+    // Default where it measured at least as fast as the separate link kernel (B200, gpurun_out/r02v): fp64
+    // except the D3Q27 AA kernels (Fig. 8 D3Q19 TRT AA 0.876 vs 0.862 of copy BW; C3 D3Q27 cumulant pull 0.950
+    // vs 0.947; C3 AA 0.871 vs 0.935; C1 fp32 pull, issue-bound, 0.86 vs 0.965). LBM_LINKS_FUSED=1 / 0 forces.
+    const char *lf_env = std::getenv("LBM_LINKS_FUSED");
+    const bool lf_pref = cfg->dtype == LBM_F64 && !(cfg->stencil == 27 && cfg->pattern == LBM_AA);
+    h->links_fused = h->links && !h->fused && (cfg->pattern == LBM_PULL || cfg->pattern == LBM_AA) &&
+                     (lf_env ? lf_env[0] == '1' : lf_pref);
     h->inline_bc = cfg->boundary_mode == LBM_BOUNDARY_INLINE && h->have_flags;
 
     // kernel selection (SRT = TRT with equal rates); index-list boundaries run the flag-free kernels;
@@ -1292,7 +1348,8 @@ int lbm_create(const lbm_config *cfg, lbm_handle *out) {
     h->faces = cfg->boundary_mode == LBM_BOUNDARY_FLAGS && h->have_flags && face_op &&
                (cfg->pattern == LBM_PULL || cfg->pattern == LBM_AA) && (face_pref || face_force) &&
                !(faces_env && faces_env[0] == '0') && detect_faces(cfg, h->base_face);
-    const int fm_bulk = !h->have_flags || h->links ? FM_NONE : h->inline_bc ? FM_INLINE : h->faces ? FM_FACES : FM_BULK;
+    const int fm_bulk = !h->have_flags ? FM_NONE : h->links ? (h->links_fused ? FM_LINKS : FM_NONE)
+                      : h->inline_bc ? FM_INLINE : h->faces ? FM_FACES : FM_BULK;
     const bool per_row = cfg->collision == LBM_MRT && cfg->n_row_rates == 15;
     // D3Q27 cumulant whose bulk and higher-order rates are all 1 (C3, G7): the specialised kernels that
     // skip the relaxations with factor 1 - omega = 0 (collide_cumulant27_unit)
@@ -1313,6 +1370,12 @@ int lbm_create(const lbm_config *cfg, lbm_handle *out) {
     } else {
         h->kern = select_kernels(kcoll, h->Q, h->dtype, fm_bulk, force, cfg->equilibrium);
         if (!(cfg->pattern == LBM_ESOTWIST ? (void *)h->kern.eso : (void *)h->kern.aa))
+            return fail(nullptr, LBM_EUNSUPPORTED, "no kernel instantiated for this combination");
+    }
+    if (h->links_fused) {
+        // the flag-free kernels of the separate link kernel mode, for lbm_set_link_velocities
+        h->kern_links = select_kernels(kcoll, h->Q, h->dtype, FM_NONE, force, cfg->equilibrium);
+        if (!(cfg->pattern == LBM_PULL ? (void *)h->kern_links.pull : (void *)h->kern_links.aa))
             return fail(nullptr, LBM_EUNSUPPORTED, "no kernel instantiated for this combination");
     }
     // rates into the kernel argument block
@@ -1488,6 +1551,43 @@ int lbm_create(const lbm_config *cfg, lbm_handle *out) {
                     cudaMemcpy(s.link_wall, s.h_link_wall.data(), n * 4, cudaMemcpyHostToDevice);
                     cudaMemcpy(s.link_fluid, lf.data(), n * 4, cudaMemcpyHostToDevice);
                     cudaMemcpy(s.link_dir, s.h_link_dir.data(), n, cudaMemcpyHostToDevice);
+                    if (h->links_fused) {
+                        // per-cell link masks of the links whose wall cell is in this slab's interior (the
+                        // update kernels store them); the others (wall in a ghost plane) stay in a residual list
+                        std::vector<uint64_t> mask(cells, 0);
+                        std::vector<uint32_t> rw, rf;
+                        std::vector<uint8_t> rd;
+                        for (size_t i = 0; i < n; ++i) {
+                            const int64_t zb = s.h_link_wall[i] / (int64_t)plane;
+                            const int q = s.h_link_dir[i];
+                            if (h->g == 0 || (zb >= h->g && zb < h->g + s.nz)) {
+                                mask[lf[i]] |= 1ull << q;
+                                if (s.h_link_type[i] == LBM_FLAG_UBB) mask[lf[i]] |= 1ull << (32 + q);
+                            } else {
+                                s.h_res_idx.push_back((uint32_t)i);
+                                rw.push_back(s.h_link_wall[i]);
+                                rf.push_back(lf[i]);
+                                rd.push_back((uint8_t)q);
+                            }
+                        }
+                        s.n_res = (uint32_t)rw.size();
+                        if (cudaMalloc(&s.lmask, cells * sizeof(uint64_t)) != cudaSuccess) {
+                            h->err = "cudaMalloc link masks";
+                            return bail(LBM_EOOM);
+                        }
+                        cudaMemcpy(s.lmask, mask.data(), cells * sizeof(uint64_t), cudaMemcpyHostToDevice);
+                        if (s.n_res) {
+                            const size_t r = s.n_res;
+                            if (cudaMalloc(&s.res_wall, r * 4) != cudaSuccess || cudaMalloc(&s.res_fluid, r * 4) != cudaSuccess ||
+                                cudaMalloc(&s.res_dir, r) != cudaSuccess || cudaMalloc(&s.res_term, r * 8) != cudaSuccess) {
+                                h->err = "cudaMalloc residual link list";
+                                return bail(LBM_EOOM);
+                            }
+                            cudaMemcpy(s.res_wall, rw.data(), r * 4, cudaMemcpyHostToDevice);
+                            cudaMemcpy(s.res_fluid, rf.data(), r * 4, cudaMemcpyHostToDevice);
+                            cudaMemcpy(s.res_dir, rd.data(), r, cudaMemcpyHostToDevice);
+                        }
+                    }
                     std::vector<double> uw(3 * n);
                     for (size_t i = 0; i < n; ++i)
                         for (int d = 0; d < 3; ++d) uw[3 * i + d] = cfg->ubb_velocity[d];
@@ -1556,7 +1656,8 @@ int lbm_destroy(lbm_handle h) {
             for (void *p : s.halo) if (p) cudaFree(p);
         if (s.flags && s.own_flags) cudaFree(s.flags);
         if (s.edges) cudaFree(s.edges);
-        for (void *p : {(void *)s.link_wall, (void *)s.link_fluid, (void *)s.link_dir, (void *)s.link_term})
+        for (void *p : {(void *)s.link_wall, (void *)s.link_fluid, (void *)s.link_dir, (void *)s.link_term, (void *)s.lmask,
+                        (void *)s.res_wall, (void *)s.res_fluid, (void *)s.res_dir, (void *)s.res_term})
             if (p) cudaFree(p);
     }
     if (h->comm) ncclCommDestroy(h->comm);
@@ -1583,7 +1684,7 @@ int lbm_detect_faces(const lbm_config *cfg, int8_t face_out[6]) {
 int lbm_boundary_impl(lbm_handle h) {
     if (!h) return LBM_EINVAL;
     if (!h->have_flags) return LBM_IMPL_NONE;
-    if (h->links) return LBM_IMPL_LINKS;
+    if (h->links) return h->links_fused ? LBM_IMPL_LINKS_FUSED : LBM_IMPL_LINKS;
     if (h->inline_bc) return LBM_IMPL_INLINE;
     return h->faces ? LBM_IMPL_FACES : LBM_IMPL_SPLIT;
 }
@@ -1663,6 +1764,7 @@ static int init_common(lbm_handle h, InitArgs &a, const double *rho, const doubl
     h->steps = 0;
     h->aa_parity = 0;
     h->links_pending = -1;
+    links_unprime(h);
     if (a.mode == 0 && h->g) {
         int rc = exchange_current(h);
         if (rc) return rc;
@@ -1712,6 +1814,7 @@ int lbm_step(lbm_handle h, int64_t n) {
         for (cudaEvent_t e : h->timing.ev) cudaEventDestroy(e);
         h->timing.ev.clear();
     }
+    if (n > 0) links_prime(h, h->stream);
     int64_t done = 0;
     const int every = h->cfg.check_nan_every;
     while (done < n) {
@@ -1851,6 +1954,7 @@ int lbm_load_state(lbm_handle h, const void *in, int32_t where, int64_t steps_do
     h->steps = steps_done;
     h->aa_parity = two_arrays(h) ? 0 : (int)(steps_done & 1);
     h->links_pending = -1;
+    links_unprime(h);
     CUDA_TRY(h, cudaStreamSynchronize(h->stream));
     return LBM_OK;
 }
@@ -1974,6 +2078,7 @@ int lbm_set_populations(lbm_handle h, const double *in, int32_t where, int32_t r
     int64_t off = 0;
     h->aa_parity = 0;
     h->links_pending = -1;
+    links_unprime(h);
     for (Slab &s : h->slabs) {
         ReadArgs r;
         std::memset(&r, 0, sizeof(r));

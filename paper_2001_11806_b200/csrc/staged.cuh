@@ -127,7 +127,7 @@ __device__ __forceinline__ void stage_issue(const StepArgs &a, const T *f, const
     const uint32_t per_q = (uint32_t)tl.hl * row_bytes;
     // flag rows staged too (bulk copies need 16-byte rows and a 16-byte aligned flag base; the host side
     // checks the base, flags_staged())
-    const bool sflags = FM == FM_BULK && nx % 16 == 0 && a.stage_flags;
+    const bool sflags = (FM == FM_BULK || FM == FM_LINKS) && nx % 16 == 0 && a.stage_flags;
     const uint32_t flag_bytes = sflags ? (uint32_t)tl.hl * (uint32_t)nx : 0u;
     if (lane == 0) mbar_expect_tx(bar, per_q * Q + flag_bytes);
     __syncwarp();
@@ -182,7 +182,7 @@ __global__ void __launch_bounds__(StagedBT<Q, OP, T>::value + 32, (StagedMinBloc
     const Rates<T> r = load_rates<T>(a);
     const int64_t Sq = a.geo.Sq;
     const int rowlen = H * nx;  // elements per q in a stage
-    const bool sflags = FM == FM_BULK && nx % 16 == 0 && a.stage_flags;
+    const bool sflags = (FM == FM_BULK || FM == FM_LINKS) && nx % 16 == 0 && a.stage_flags;
     int it = 0;
     for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
         const int stage = it % nstages;
@@ -199,13 +199,15 @@ __global__ void __launch_bounds__(StagedBT<Q, OP, T>::value + 32, (StagedMinBloc
                 x -= nx;
                 ++h;
             }
-            if (FM == FM_BULK) {
-                // walls and near-wall cells belong to the edge kernel (AA even: only walls are skipped;
-                // the even step is local, so near-wall cells need nothing special there)
-                const uint8_t own = sflags ? fl[c]
-                                           : a.flags[((uint32_t)tl.zs * (uint32_t)a.geo.ny + (uint32_t)(tl.y0 + hc)) *
-                                                         (uint32_t)nx + (uint32_t)xc];
-                if (MODE == SM_AA_EVEN ? (own & 3) != 0 : own != 0) continue;
+            uint8_t own = 0;
+            if (FM == FM_BULK || FM == FM_LINKS) {
+                // FM_BULK: walls and near-wall cells belong to the edge kernel (AA even: only walls are skipped;
+                // the even step is local, so near-wall cells need nothing special there). FM_LINKS: walls are
+                // skipped, near-wall cells store their links after the collision.
+                own = sflags ? fl[c]
+                             : a.flags[((uint32_t)tl.zs * (uint32_t)a.geo.ny + (uint32_t)(tl.y0 + hc)) * (uint32_t)nx +
+                                       (uint32_t)xc];
+                if ((FM == FM_LINKS || MODE == SM_AA_EVEN) ? (own & 3) != 0 : own != 0) continue;
             }
             const int xm = xc == 0 ? nx - 1 : xc - 1, xp = xc == nx - 1 ? 0 : xc + 1;
             T g[Q];
@@ -240,6 +242,21 @@ __global__ void __launch_bounds__(StagedBT<Q, OP, T>::value + 32, (StagedMinBloc
                 const Nbr n = neighbours(a.geo, xc, y, tl.zs);
 #pragma unroll
                 for (int q = 0; q < Q; ++q) dst[q * Sq + nb_off(a.geo, n, S::cx(q), S::cy(q), S::cz(q))] = g[q];
+            }
+            if constexpr (FM == FM_LINKS && (MODE == SM_PULL || MODE == SM_AA_EVEN || MODE == SM_AA_ODD)) {
+                if (own & 0x80) {  // the link stores of kernels.cuh FM_LINKS
+                    const uint64_t m = a.lmask[self];
+                    const Nbr n = neighbours(a.geo, xc, y, tl.zs);
+#pragma unroll
+                    for (int q = 0; q < Q; ++q) {
+                        if (!((m >> q) & 1)) continue;
+                        const T v = link_value<Q, T>(a, m, g, q);
+                        if constexpr (MODE == SM_PULL) dst[q * Sq + nb_off(a.geo, n, -S::cx(q), -S::cy(q), -S::cz(q))] = v;
+                        else if constexpr (MODE == SM_AA_EVEN)
+                            dst[S::opp(q) * Sq + nb_off(a.geo, n, -S::cx(q), -S::cy(q), -S::cz(q))] = v;
+                        else dst[q * Sq + self] = v;
+                    }
+                }
             }
         }
         __syncwarp();
@@ -276,17 +293,15 @@ constexpr bool staged_auto() {
 
 template <int Q, int OP, typename T, int FM, bool FORCE, int MODE>
 bool staged_launch(const StepArgs &a, const void *src, void *dst, int nplanes, cudaStream_t s) {
-    if constexpr (FM != FM_NONE && FM != FM_BULK) {  // inline walls (low-level ABI): plain kernels only
+    if constexpr (FM != FM_NONE && FM != FM_BULK && FM != FM_LINKS) {  // inline walls (low-level ABI): plain kernels only
         (void)a, (void)src, (void)dst, (void)nplanes, (void)s;
         return false;
     } else {
     constexpr int BT = StagedBT<Q, OP, T>::value;
     const int path = staged_path();
-    // AA with the split flag mode: the staged kernels also win for the TRT class, hand-written SRT included
-    // (same collide body; Fig. 8 walled channel 0.747 -> 0.805 of copy BW; the flag-free AA kernels stay plain)
-    constexpr int cls = op_class(op_base(OP));
-    constexpr bool aa_flags = FM == FM_BULK && (MODE == SM_AA_EVEN || MODE == SM_AA_ODD) && (cls == OP_TRT || cls == OP_SRT);
-    if (path == 1 || (path == 0 && !(staged_auto<Q, OP, MODE>() || aa_flags))) return false;
+    // (AA with the split flag mode ran staged for the TRT class until the plain AA kernels issued their
+    // population loads ahead of the flag test: Fig. 8 walled channel plain 0.869 vs staged 0.831 of copy BW)
+    if (path == 1 || (path == 0 && !staged_auto<Q, OP, MODE>())) return false;
     const int64_t row_bytes = (int64_t)a.geo.nx * (int64_t)sizeof(T);
     if (row_bytes % 16 != 0) return false;
     if ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) % 16 != 0) return false;
@@ -297,7 +312,7 @@ bool staged_launch(const StepArgs &a, const void *src, void *dst, int nplanes, c
     // flag rows are staged by bulk copy only from a 16-byte aligned flag base (a caller's flags pointer in
     // the low-level ABI may be any torch view); otherwise consumers read the flag byte from global memory
     StepArgs b = a;
-    b.stage_flags = FM == FM_BULK && a.geo.nx % 16 == 0 && reinterpret_cast<uintptr_t>(a.flags) % 16 == 0;
+    b.stage_flags = (FM == FM_BULK || FM == FM_LINKS) && a.geo.nx % 16 == 0 && reinterpret_cast<uintptr_t>(a.flags) % 16 == 0;
     const int64_t stage_bytes = ((int64_t)Q * H * row_bytes + (b.stage_flags ? (int64_t)H * a.geo.nx : 0) + 127) / 128 * 128;
     const size_t smem = 128 + (size_t)nst * stage_bytes;
     if (smem > 227 * 1024) return false;

@@ -439,10 +439,10 @@ class Simulation:
 
     @property
     def boundary_impl(self) -> str:
-        """What the handle's boundary handling runs: none | split | inline | links | faces."""
+        """What the handle's boundary handling runs: none | split | inline | links | faces | links_fused."""
         v = int(lbm_boundary_impl(self.h))
         _check(v, self.h, "lbm_boundary_impl")
-        return ["none", "split", "inline", "links", "faces"][v]
+        return ["none", "split", "inline", "links", "faces", "links_fused"][v]
 
     def step_phases_ms(self):
         """{boundary, exchange, interior}: (begin, end) in ms of the last timed decomposed step."""

@@ -28,6 +28,8 @@ def test_algorithmic_bytes_per_cell(bench):
     fl, per = bench.flags_for(C["c3"], (8, 8, 8))
     assert per == (0, 0, 0) and bench.bytes_per_cell(C["c3_flags"], fl) == 433          # + 1 B flag (split mode)
     assert bench.bytes_per_cell(C["c3"], fl) == 432                                      # index lists: flag-free
+    assert bench.bytes_per_cell(C["c3"], fl, "links") == 432                             # separate link kernel
+    assert bench.bytes_per_cell(C["c3"], fl, "links_fused") == 433                       # in-kernel links: + flag byte
     assert bench.bytes_per_cell(C["c1_f64"], bench.flags_for(C["c1_f64"], (8, 8, 8))[0], "faces") == 304
 
 

@@ -712,13 +712,53 @@ def test_index_list_per_link_wall_velocities(pattern, steps):
     np.testing.assert_allclose(u_g[:, fl == 0], u_o[:, fl == 0], rtol=0, atol=1e-15)
 
 
+IN_KERNEL_LINK_CASES = [c for c in LINK_CASES if c.pattern in ("pull", "aa")] + [
+    Case("lk_trt_f64_box_aa", (40, 12, 10), 19, "trt", (1.6, 0.5), "f64", pattern="aa", geometry="obstacles",
+         ubb=(0.03, 0.01, -0.02), steps=9, extra={"flags": np.maximum(LI.channel_flags(40, 12, 10), LI.random_obstacles(3, 40, 12, 10))}),
+]
+
+
+@pytest.mark.parametrize("use_graph", [False, True])
+@pytest.mark.parametrize("case", IN_KERNEL_LINK_CASES, ids=lambda c: c.name)
+def test_in_kernel_links_identical_to_link_kernel(case, use_graph, kernel_path, monkeypatch):
+    """Index lists folded into the pull / AA update kernels (FM_LINKS: each near-wall fluid cell stores the
+    wall slots of its links after its collision) against the separate link kernel: the fluid
+    populations are bit-identical at odd and even step counts, across several lbm_step calls, with the
+    CUDA-graph cycle, and after set_populations (the full list primes the wall slots again)."""
+    monkeypatch.setenv("LBM_LINKS_FUSED", "1")
+    fused = make_sim(case, boundary_mode="links", use_graph=use_graph)
+    assert fused.boundary_impl == "links_fused"
+    monkeypatch.setenv("LBM_LINKS_FUSED", "0")
+    sep = make_sim(case, boundary_mode="links")
+    assert sep.boundary_impl == "links"
+    fl = case.extra.get("flags", case.flags())
+    mask = np.broadcast_to(fl == 0, (case.Q,) + fl.shape)
+    for s in (fused, sep):
+        init_sim(s, case)
+    for n in (1, 2, case.steps):
+        for s in (fused, sep):
+            s.step(n)
+        np.testing.assert_array_equal(fused.populations()[mask], sep.populations()[mask])
+        np.testing.assert_array_equal(fused.populations(raw=True)[mask], sep.populations(raw=True)[mask])
+        np.testing.assert_array_equal(fused.macroscopic()[1][:, fl == 0], sep.macroscopic()[1][:, fl == 0])
+    for s in (fused, sep):
+        s.set_populations(s.populations())
+        s.step(3)
+    np.testing.assert_array_equal(fused.populations()[mask], sep.populations()[mask])
+    if case.extra.get("flags") is None:
+        assert max_rel_err(fused.populations(), oracle_run(case, case.steps + 6), mask) <= TOL[case.dtype]
+
+
 @pytest.mark.parametrize("P,halo_mode,nccl_self", [(2, 0, False), (4, 1, False), (1, 0, True), (1, 1, True), (1, 2, True)])
 @pytest.mark.parametrize("pattern", ["pull", "aa", "push", "esotwist"])
-def test_index_list_boundaries_slabs_bit_identical(P, halo_mode, nccl_self, pattern):
+@pytest.mark.parametrize("in_kernel", ["0", "1"])
+def test_index_list_boundaries_slabs_bit_identical(P, halo_mode, nccl_self, pattern, in_kernel, monkeypatch):
     """Index-list boundaries with slab decomposition: the link kernel also fills the wall slots of ghost
     planes after the exchange (fused halo: after the next LSA gate, plus a closing gate per lbm_step call);
     loopback slabs, NCCL self-exchange and the fused NVLink halo are bit-identical to the single slab, for
-    every pattern, and the concatenated link lists are the global list."""
+    every pattern, and the concatenated link lists are the global list. With the in-kernel links (pull, AA,
+    not the fused halo) the links whose wall cell lies in a ghost plane stay with the link kernel."""
+    monkeypatch.setenv("LBM_LINKS_FUSED", in_kernel)
     case = Case("lkdec", (16, 12, 16), 19, "trt", (1.6, 0.5), "f64", force=(1e-5, 0, 0), geometry="obstacles",
                 ubb=(0.02, -0.01, 0.03), steps=13, pattern=pattern)
     one = make_sim(case, boundary_mode="links")
