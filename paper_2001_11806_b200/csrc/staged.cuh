@@ -50,10 +50,15 @@ constexpr int kStagedBT = LBM_STAGED_BT;
 // Consumer threads per CTA. A CTA of 9 warps puts 3 warps on one of the 4 SM sub-partitions, whose 16K
 // registers then cap every thread at 168; the D3Q27 KBC needs more (it spilled ~160 B per thread at 168),
 // so it runs 7 consumer warps + the producer (8 warps, 2 per sub-partition: up to 255 registers).
+// (LBM_STAGED_BT224_F64 = build variant for sweeps: every fp64 staged kernel with 7 consumer warps)
 template <int Q, int OPX, typename T>
 struct StagedBT {
     static constexpr int OP = op_class(op_base(OPX));
+#ifdef LBM_STAGED_BT224_F64
+    static constexpr int value = sizeof(T) == 8 ? 224 : kStagedBT;
+#else
     static constexpr int value = (sizeof(T) == 8 && Q == 27 && (OP == OP_KBC || OP == OP_KBC_EXACT)) ? 224 : kStagedBT;
+#endif
 };
 
 // registers: 65536 / (BT * minBlocks); the heavy fp64 operators get more room

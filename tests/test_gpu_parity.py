@@ -1063,3 +1063,4 @@ def test_mrt_shear_only_kernels_match_general(pattern, geometry, dtype, Q, monke
     mask = fluid_mask(case, Q)
     assert max_rel_err(fast.populations(), general.populations(), mask) <= (1e-13 if dtype == "f64" else 2e-6)
     assert max_rel_err(fast.populations(), oracle_run(case), mask) <= TOL[dtype]
+
