@@ -574,13 +574,16 @@ __device__ __forceinline__ void eso_cell(const StepArgs &a, T *__restrict__ f, i
         const uint8_t own = a.flags[self];
         if (own & 3) return;
         edge = (own & 0x80) != 0;
-    } else if (FM == FM_BULK) {
-        if (a.flags[self] != 0) return;
     }
+    const uint8_t own_b = FM == FM_BULK ? a.flags[self] : 0;  // tested after the loads are issued (as the AA kernels)
     T g[Q];
 #pragma unroll
     for (int q = 0; q < Q; ++q)
         g[q] = f[(ODD ? S::opp(q) : q) * Sq + nb_off(a.geo, n, -cpos(S::cx(q)), -cpos(S::cy(q)), -cpos(S::cz(q)))];
+    if (FM == FM_BULK && own_b != 0) {  // walls and near-wall cells (the edge kernel)
+        keep_loads<Q, T>(g);
+        return;
+    }
     const Rates<T> r = load_rates<T>(a);
     collide<Q, OP, T, FORCE>(g, r);
 #pragma unroll
