@@ -74,7 +74,17 @@ struct StepArgs {
     // slot x streams from (the link (b = x - c_q, q) of LBM_BOUNDARY_LINKS), bit 32 + q = that wall is UBB;
     // read by near-wall fluid cells only
     const uint64_t *lmask;
+    // launch box of the plain update kernels (local x, y): the bounding box of the non-wall cells (walls on
+    // the domain faces get no threads at all), or the whole plane
+    int x0, x1, y0, y1;
 };
+
+// this thread's cell of the launch box; false outside it
+__device__ __forceinline__ bool box_cell(const StepArgs &a, int &x, int &y) {
+    x = a.x0 + (int)(blockIdx.x * blockDim.x + threadIdx.x);
+    y = a.y0 + (int)(blockIdx.y * blockDim.y + threadIdx.y);
+    return x < a.x1 && y < a.y1;
+}
 
 constexpr int kMaxDevices = 64;  // per-device caches of launch attributes and occupancy
 
@@ -342,9 +352,8 @@ __device__ __forceinline__ void pull_cell(const StepArgs &a, const T *__restrict
 // One thread per cell along x; planes z = z_begin + blockIdx.z * z_step (interior indices).
 template <int Q, int OP, typename T, int FM, bool FORCE, bool PEER = false>
 __global__ void __launch_bounds__(256, (MinBlocks<Q, OP, T>::pull)) k_pull(const StepArgs a, const T *__restrict__ src, T *__restrict__ dst) {
-    const int x = blockIdx.x * blockDim.x + threadIdx.x;
-    const int y = blockIdx.y * blockDim.y + threadIdx.y;
-    if (x >= a.geo.nx || y >= a.geo.ny) return;
+    int x, y;
+    if (!box_cell(a, x, y)) return;
     const int zs = a.z_begin + (int)blockIdx.z * a.z_step + a.geo.g;
     pull_cell<Q, OP, T, FM, FORCE, PEER>(a, src, dst, x, y, zs);
     peer_fence<PEER>();
@@ -421,9 +430,8 @@ __device__ __forceinline__ void aa_even_cell(const StepArgs &a, T *__restrict__ 
 
 template <int Q, int OP, typename T, bool FLAGS, bool FORCE, bool PEER = false, bool LINKS = false>
 __global__ void __launch_bounds__(256, (MinBlocks<Q, OP, T>::aa)) k_aa_even(const StepArgs a, T *__restrict__ f) {
-    const int x = blockIdx.x * blockDim.x + threadIdx.x;
-    const int y = blockIdx.y * blockDim.y + threadIdx.y;
-    if (x >= a.geo.nx || y >= a.geo.ny) return;
+    int x, y;
+    if (!box_cell(a, x, y)) return;
     aa_even_cell<Q, OP, T, FLAGS, FORCE, PEER, LINKS>(a, f, x, y, a.z_begin + (int)blockIdx.z * a.z_step + a.geo.g);
     peer_fence<PEER>();
 }
@@ -521,9 +529,8 @@ __device__ __forceinline__ void aa_odd_cell(const StepArgs &a, T *__restrict__ f
 // and is stored directly in a[x](qbar) (+ UBB term of qbar).
 template <int Q, int OP, typename T, int FM, bool FORCE, bool PEER = false>
 __global__ void __launch_bounds__(256, (MinBlocks<Q, OP, T>::aa)) k_aa_odd(const StepArgs a, T *__restrict__ f) {
-    const int x = blockIdx.x * blockDim.x + threadIdx.x;
-    const int y = blockIdx.y * blockDim.y + threadIdx.y;
-    if (x >= a.geo.nx || y >= a.geo.ny) return;
+    int x, y;
+    if (!box_cell(a, x, y)) return;
     const int zs = a.z_begin + (int)blockIdx.z * a.z_step + a.geo.g;
     aa_odd_cell<Q, OP, T, FM, FORCE, PEER>(a, f, x, y, zs);
     peer_fence<PEER>();
@@ -611,9 +618,8 @@ __device__ __forceinline__ void eso_cell(const StepArgs &a, T *__restrict__ f, i
 
 template <int Q, int OP, typename T, int FM, bool FORCE, bool ODD, bool PEER = false>
 __global__ void __launch_bounds__(256, (MinBlocks<Q, OP, T>::aa)) k_eso(const StepArgs a, T *f) {
-    const int x = blockIdx.x * blockDim.x + threadIdx.x;
-    const int y = blockIdx.y * blockDim.y + threadIdx.y;
-    if (x >= a.geo.nx || y >= a.geo.ny) return;
+    int x, y;
+    if (!box_cell(a, x, y)) return;
     eso_cell<Q, OP, T, FM, FORCE, ODD, PEER>(a, f, x, y, a.z_begin + (int)blockIdx.z * a.z_step + a.geo.g);
     peer_fence<PEER>();
 }
@@ -684,9 +690,8 @@ __device__ __forceinline__ void push_cell(const StepArgs &a, const T *__restrict
 template <int Q, int OP, typename T, int FM, bool FORCE, bool PEER = false>
 __global__ void __launch_bounds__(256, (MinBlocks<Q, OP, T>::aa)) k_push(const StepArgs a, const T *__restrict__ src,
                                                                           T *__restrict__ dst) {
-    const int x = blockIdx.x * blockDim.x + threadIdx.x;
-    const int y = blockIdx.y * blockDim.y + threadIdx.y;
-    if (x >= a.geo.nx || y >= a.geo.ny) return;
+    int x, y;
+    if (!box_cell(a, x, y)) return;
     push_cell<Q, OP, T, FM, FORCE, PEER>(a, src, dst, x, y, a.z_begin + (int)blockIdx.z * a.z_step + a.geo.g);
     peer_fence<PEER>();
 }
@@ -709,9 +714,8 @@ __global__ void __launch_bounds__(128) k_push_edges(const StepArgs a, const T *_
 template <int Q, int OP, typename T, bool FLAGS, bool FORCE>
 __global__ void __launch_bounds__(256, (MinBlocks<Q, OP, T>::aa)) k_collide(const StepArgs a, T *__restrict__ f) {
     using S = Stencil<Q>;
-    const int x = blockIdx.x * blockDim.x + threadIdx.x;
-    const int y = blockIdx.y * blockDim.y + threadIdx.y;
-    if (x >= a.geo.nx || y >= a.geo.ny) return;
+    int x, y;
+    if (!box_cell(a, x, y)) return;
     const int zs = a.z_begin + (int)blockIdx.z * a.z_step + a.geo.g;
     const uint32_t self = ((uint32_t)zs * (uint32_t)a.geo.ny + (uint32_t)y) * (uint32_t)a.geo.nx + (uint32_t)x;
     const int64_t Sq = a.geo.Sq;

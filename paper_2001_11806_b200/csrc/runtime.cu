@@ -6,6 +6,7 @@
 #include <nccl.h>
 #include <nvtx3/nvToolsExt.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdlib>
 #include <cstdio>
@@ -48,6 +49,7 @@ struct Slab {
     bool links_primed = false;
     void *halo[4] = {nullptr, nullptr, nullptr, nullptr};  // packed mode: send up, send down, recv below, recv above
     int cur = 0;          // index of the array holding the current state (pull)
+    int zlo = 0, zhi = 0; // interior planes [zlo, zhi) holding non-wall cells (launch trimming)
     bool own_pdf[2] = {true, true}, own_flags = true, own_halo = true;  // false: borrowed (lbm_config.*_dev)
 };
 
@@ -160,9 +162,22 @@ Geo geo_of(const lbm_handle_s *h, const Slab &s) {
     return g;
 }
 
+// grid of the plain update kernels: the launch box (StepArgs x0..x1, y0..y1) times the planes
 dim3 grid_for(const lbm_handle_s *h, int nplanes) {
-    return dim3((unsigned)((h->nx + h->block.x - 1) / h->block.x), (unsigned)((h->ny + h->block.y - 1) / h->block.y),
+    const int64_t bx = h->base.x1 - h->base.x0, by = h->base.y1 - h->base.y0;
+    return dim3((unsigned)((bx + h->block.x - 1) / h->block.x), (unsigned)((by + h->block.y - 1) / h->block.y),
                 (unsigned)nplanes);
+}
+
+// contiguous plane ranges (z_step 1) lose their leading / trailing planes without non-wall cells; false if
+// nothing is left
+bool trim_planes(const Slab &s, int &z_begin, int &nplanes, int z_step) {
+    if (z_step != 1 && nplanes != 1) return nplanes > 0;
+    const int lo = std::max(z_begin, s.zlo), hi = std::min(z_begin + nplanes, s.zhi);
+    if (hi <= lo) return false;
+    z_begin = lo;
+    nplanes = hi - lo;
+    return true;
 }
 
 size_t plane_bytes(const lbm_handle_s *h) { return (size_t)h->nx * h->ny * h->esize; }
@@ -223,7 +238,7 @@ void launch_links_fix(lbm_handle_s *h, Slab &s, void *f, int mode, cudaStream_t 
 
 void launch_pull_range(lbm_handle_s *h, Slab &s, int z_begin, int nplanes, int z_step, cudaStream_t st,
                        bool peer_stores = false) {
-    if (nplanes <= 0) return;
+    if (nplanes <= 0 || !trim_planes(s, z_begin, nplanes, z_step)) return;
     StepArgs a = h->base;
     a.geo = geo_of(h, s);
     a.z_begin = z_begin;
@@ -244,7 +259,7 @@ void launch_pull_range(lbm_handle_s *h, Slab &s, int z_begin, int nplanes, int z
 
 void launch_push_range(lbm_handle_s *h, Slab &s, int z_begin, int nplanes, int z_step, cudaStream_t st,
                        bool peer_stores = false) {
-    if (nplanes <= 0) return;
+    if (nplanes <= 0 || !trim_planes(s, z_begin, nplanes, z_step)) return;
     StepArgs a = h->base;
     a.geo = geo_of(h, s);
     a.z_begin = z_begin;
@@ -263,7 +278,7 @@ void launch_push_range(lbm_handle_s *h, Slab &s, int z_begin, int nplanes, int z
 
 void launch_eso_range(lbm_handle_s *h, Slab &s, int odd, int z_begin, int nplanes, int z_step, cudaStream_t st,
                       bool peer_stores = false) {
-    if (nplanes <= 0) return;
+    if (nplanes <= 0 || !trim_planes(s, z_begin, nplanes, z_step)) return;
     StepArgs a = h->base;
     a.geo = geo_of(h, s);
     a.z_begin = z_begin;
@@ -283,7 +298,7 @@ void launch_eso_range(lbm_handle_s *h, Slab &s, int odd, int z_begin, int nplane
 
 void launch_aa_range(lbm_handle_s *h, Slab &s, int odd, int z_begin, int nplanes, int z_step, cudaStream_t st,
                      bool peer_stores = false) {
-    if (nplanes <= 0) return;
+    if (nplanes <= 0 || !trim_planes(s, z_begin, nplanes, z_step)) return;
     StepArgs a = h->base;
     a.geo = geo_of(h, s);
     a.z_begin = z_begin;
@@ -1116,6 +1131,10 @@ static int kernel_args_common(const lbm_kernel_args *k, StepArgs &a, bool aa) {
     a.geo.Sq = k->shape[0] * k->shape[1] * (k->shape[2] + 2 * k->ghost);
     a.z_begin = (int)k->z_begin;
     a.z_step = 1;
+    a.x0 = 0;
+    a.x1 = (int)k->shape[0];
+    a.y0 = 0;
+    a.y1 = (int)k->shape[1];
     for (int i = 0; i < 8; ++i) a.rates[i] = k->rates[i];
     if (k->collision == LBM_SRT) a.rates[1] = a.rates[0];
     if (k->collision == LBM_MRT || k->collision == LBM_GEN_MRT)
@@ -1395,6 +1414,47 @@ int lbm_create(const lbm_config *cfg, lbm_handle *out) {
     }
     for (int f = 0; f < 6; ++f) b.face[f] = h->faces ? h->base_face[f] : 0;
     b.nzg = (int)h->nzg;
+    // launch box: the bounding box of the non-wall cells of the flag field (walls on the domain faces get no
+    // threads; LBM_BOX=0 launches the whole plane), interior planes with non-wall cells per slab below
+    b.x0 = 0;
+    b.x1 = (int)h->nx;
+    b.y0 = 0;
+    b.y1 = (int)h->ny;
+    std::vector<char> plane_fluid(h->nzg, 1);
+    const char *box_env = std::getenv("LBM_BOX");
+    // (not for the inline mode: Fig. 8 inline 0.867 -> 0.842 with the box, three repetitions each; walled
+    // configs otherwise +0.4 to +0.8 %: C1 fp32 0.960 -> 0.968, C3-AA links 0.935 -> 0.943; scripts/gpu_r02z10.sh)
+    if (h->have_flags && !h->inline_bc && !(box_env && box_env[0] == '0')) {
+        int64_t x0 = h->nx, x1 = -1, y0 = h->ny, y1 = -1;
+        const int64_t pl = h->nx * h->ny;
+        for (int64_t z = 0; z < h->nzg; ++z) {
+            bool any = false;
+            for (int64_t y = 0; y < h->ny; ++y) {
+                const uint8_t *row = cfg->flags + z * pl + y * h->nx;
+                int64_t first = -1, last = -1;
+                for (int64_t x = 0; x < h->nx; ++x)
+                    if ((row[x] & 3) == 0) {
+                        if (first < 0) first = x;
+                        last = x;
+                    }
+                if (first < 0) continue;
+                any = true;
+                x0 = std::min(x0, first);
+                x1 = std::max(x1, last);
+                y0 = std::min(y0, y);
+                y1 = std::max(y1, y);
+            }
+            plane_fluid[z] = any;
+        }
+        if (x1 >= 0) {
+            // x starts on a 32-cell boundary: a warp's 32 cells keep their aligned 128 / 256 B segments (a box
+            // starting at x = 1 misaligned every warp of the C3 cavity: 0.95 -> 0.90 of copy BW)
+            b.x0 = (int)(x0 / 32 * 32);
+            b.x1 = (int)x1 + 1;
+            b.y0 = (int)y0;
+            b.y1 = (int)y1 + 1;
+        }
+    }
     h->block = cfg->block_x > 0 ? block_for(h->nx, h->ny, cfg->block_x) : block_for(h->nx, h->ny, 0);
 
     CUDA_TRY(nullptr, cudaSetDevice(cfg->device));
@@ -1439,6 +1499,10 @@ int lbm_create(const lbm_config *cfg, lbm_handle *out) {
         const int slab_index = cfg->nranks > 1 ? cfg->rank : i;
         s.z0 = slab_index * nzl;
         s.nz = (int)nzl;
+        s.zlo = 0;  // first / last interior planes with non-wall cells
+        while (s.zlo < s.nz && !plane_fluid[s.z0 + s.zlo]) ++s.zlo;
+        s.zhi = s.nz;
+        while (s.zhi > s.zlo && !plane_fluid[s.z0 + s.zhi - 1]) --s.zhi;
         const Geo g = geo_of(h, s);
         const size_t bytes = (size_t)g.Sq * h->Q * h->esize;
         for (int a = 0; a < (two_arrays(h) ? 2 : 1); ++a) {
