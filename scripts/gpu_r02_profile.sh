@@ -40,4 +40,6 @@ prof c1_f32 "k_pull|k_links" 6 2
 prof op_cumulant27 "k_aa" 4 2
 prof op_kbc27 k_staged 4 2
 prof fig8_channel_flags "k_staged|k_aa" 6 3
+prof fig8_channel_links "k_aa" 6 2
+prof c3_aa_links "k_aa" 6 2
 cat $O/status.txt
