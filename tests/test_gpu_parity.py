@@ -165,6 +165,10 @@ PARITY = [
          u_amp=1e-4, steps=100),
     Case("c2_proxy_f64", (24, 20, 32), 19, "mrt", (1.9, 1.0, 1.0, 1.0), "f64", pattern="aa", init="shear",
          rho_amp=0.0, u_amp=1e-4, steps=40),
+    # two-cells-per-thread AA kernels of C2 (k_aa_*_x2): a ragged row end (nx = 100: cell B exists for x < 100
+    # only) and a row of exactly 64 (cell B of lane 31 is x = nx - 1, whose +x neighbour wraps to 0)
+    Case("c2_x2_ragged", (100, 12, 10), 19, "mrt", (1.9, 1.0, 1.0, 1.0), "f32", pattern="aa", u_amp=0.03, steps=13),
+    Case("c2_x2_row64", (64, 6, 8), 19, "mrt", (1.9, 1.0, 1.0, 1.0), "f32", pattern="aa", u_amp=0.03, steps=12),
     Case("c3_proxy", (20, 20, 20), 27, "cumulant", (1.95,), "f64", geometry="cavity", ubb=(0.05, 0, 0),
          init="rest", steps=100),
     Case("c3_proxy_random", (16, 16, 16), 27, "cumulant", (1.95,), "f64", geometry="cavity", ubb=(0.05, 0, 0),
@@ -474,12 +478,15 @@ def test_slab_decomposition_other_ops(Q, op, rates, dtype):
 @pytest.mark.parametrize("halo_mode", [0, 1])
 @pytest.mark.parametrize("Q,op,rates,geometry,force", [(19, "trt", (1.6, 0.5), "channel", (1e-5, 0, 0)),
                                                        (19, "srt", (1.7,), "obstacles", (0, 0, 0)),
-                                                       (27, "cumulant", (1.95,), "periodic", (0, 0, 0))])
+                                                       (27, "cumulant", (1.95,), "periodic", (0, 0, 0)),
+                                                       (19, "mrt", (1.9, 1.0, 1.0, 1.0), "periodic", (0, 0, 0))])
 def test_aa_slab_decomposition_bit_identical(P, halo_mode, Q, op, rates, geometry, force):
     """AA with slabs: ghost fill after even steps, return of ghost-plane writes after odd steps
     (masked by the producing cell's flag with walls). Odd and even step counts."""
     case = Case("aadec", (14, 12, 16), Q, op, rates, "f64", pattern="aa", force=force, geometry=geometry,
                 ubb=(0.02, -0.01, 0.03))
+    if op == "mrt":  # C2's fp32 shear-only MRT: the two-cells-per-thread kernels (nx = 72: ragged second cell)
+        case = Case("aadec_x2", (72, 6, 16), Q, op, rates, "f32", pattern="aa", u_amp=0.03)
     for steps in (7, 10):
         one = make_sim(case)
         many = make_sim(case, n_local_slabs=P, halo_mode=halo_mode)
