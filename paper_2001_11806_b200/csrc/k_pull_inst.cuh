@@ -45,18 +45,17 @@ void aa_launcher(const StepArgs &a, void *f, int odd, dim3 grid, dim3 block, cud
                 a, f, f, (int)grid.z, s))
             return;
     }
-    if constexpr (FM == FM_NONE && sizeof(T) == 4 && Q == 19 && op_base(OP) == OP_MRT_SHEAR) {
-        // two cells per thread (periodic fp32 D3Q19 shear-only MRT, C2: 0.930 -> 0.937 of copy BW; the
-        // incompressible MRT measured 0.928 -> 0.925 and keeps one cell; LBM_AA_X2=0 disables it)
+    if constexpr (FM == FM_NONE && sizeof(T) == 4 && Q == 19) {
+        // even step: two cells per thread (periodic fp32 D3Q19 on the plain path; C2 0.944 -> 0.964 of copy BW,
+        // profiles/r03e; the odd step keeps one cell per thread: both two-cell 0.951); LBM_AA_X2=0 disables it
         static const bool x2 = [] {
             const char *e = getenv("LBM_AA_X2");
             return e ? atoi(e) != 0 : true;
         }();
-        if (x2 && block.x >= 32 && block.x % 32 == 0) {
+        if (x2 && !odd && block.x >= 32 && block.x % 32 == 0) {
             const unsigned w = (unsigned)(a.x1 - a.x0);
             const dim3 g2((w + 2 * block.x - 1) / (2 * block.x), grid.y, grid.z);
-            if (odd) k_aa_odd_x2<Q, OP, T, FORCE><<<g2, block, 0, s>>>(a, static_cast<T *>(f));
-            else k_aa_even_x2<Q, OP, T, FORCE><<<g2, block, 0, s>>>(a, static_cast<T *>(f));
+            k_aa_even_x2<Q, OP, T, FORCE><<<g2, block, 0, s>>>(a, static_cast<T *>(f));
             return;
         }
     }

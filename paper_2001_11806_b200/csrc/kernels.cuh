@@ -536,10 +536,12 @@ __global__ void __launch_bounds__(256, (MinBlocks<Q, OP, T>::aa)) k_aa_odd(const
     peer_fence<PEER>();
 }
 
-// Two cells per thread (periodic AA, no flags, no peer stores): lane l of warp w of an x-block updates the
-// cells x_A = x0 + 64 w + l and x_B = x_A + 32, so both are 128-byte coalesced and the thread issues 2 Q
-// loads back to back (twice the bytes in flight per warp of the one-cell kernels). The cells share their
-// row bases (y, z neighbours) and per-direction plane pointers; only the x neighbours differ.
+// Two cells per thread in the AA even step (periodic, no flags, no peer stores): lane l of warp w of an
+// x-block updates the cells x_A = x0 + 64 w + l and x_B = x_A + 32, so both are 128-byte coalesced and the
+// thread issues 2 Q loads back to back (twice the bytes in flight per warp of the one-cell kernel; ncu of
+// C2's even step: 3.22 -> 3.08 ms, DRAM 77 -> 81 % of peak). The same scheme in the odd step (shared row
+// bases, per-cell x neighbours) measured slower than one cell per thread (3.44 -> 3.53 ms, more integer
+// instructions at 16 instead of 24 warps per SM) and is not used.
 template <int Q>
 struct MinBlocksX2 {
     static constexpr int aa = Q == 19 ? 2 : 1;
@@ -576,40 +578,6 @@ __global__ void __launch_bounds__(256, MinBlocksX2<Q>::aa) k_aa_even_x2(const St
         collide<Q, OP, T, FORCE>(h, r);
 #pragma unroll
         for (int q = 0; q < Q; ++q) f[S::opp(q) * Sq + self + 32] = h[q];
-    }
-}
-
-template <int Q, int OP, typename T, bool FORCE>
-__global__ void __launch_bounds__(256, MinBlocksX2<Q>::aa) k_aa_odd_x2(const StepArgs a, T *__restrict__ f) {
-    using S = Stencil<Q>;
-    int x, y;
-    if (!box_cell_x2(a, x, y)) return;
-    const bool hasB = x + 32 < a.x1;
-    const int zs = a.z_begin + (int)blockIdx.z * a.z_step + a.geo.g;
-    const Nbr n = neighbours(a.geo, x, y, zs);  // cell A
-    const int nx = a.geo.nx;
-    const int xb = x + 32;
-    const int xsB[3] = {xb - 1, xb, xb == nx - 1 ? 0 : xb + 1};  // cell B (x_B >= 32: x_B - 1 never wraps)
-    const int64_t Sq = a.geo.Sq;
-    // row base (cells) of the neighbour rows (dy, dz)
-    auto row = [&](int dy, int dz) -> uint32_t {
-        return ((uint32_t)n.zs[dz + 1] * (uint32_t)a.geo.ny + (uint32_t)n.ys[dy + 1]) * (uint32_t)nx;
-    };
-    T g[Q], h[Q];
-#pragma unroll
-    for (int q = 0; q < Q; ++q) {
-        const T *p = f + S::opp(q) * Sq + row(-S::cy(q), -S::cz(q));
-        g[q] = p[n.xs[1 - S::cx(q)]];
-        h[q] = hasB ? p[xsB[1 - S::cx(q)]] : T(0);
-    }
-    const Rates<T> r = load_rates<T>(a);
-    collide<Q, OP, T, FORCE>(g, r);
-#pragma unroll
-    for (int q = 0; q < Q; ++q) f[q * Sq + row(S::cy(q), S::cz(q)) + n.xs[1 + S::cx(q)]] = g[q];
-    if (hasB) {
-        collide<Q, OP, T, FORCE>(h, r);
-#pragma unroll
-        for (int q = 0; q < Q; ++q) f[q * Sq + row(S::cy(q), S::cz(q)) + xsB[1 + S::cx(q)]] = h[q];
     }
 }
 
