@@ -438,7 +438,10 @@ def main():
     # events recorded on it bracket exactly our kernels (the legacy default stream's handle is 0)
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
-    small = np.prod(gshape) / P <= 2 ** 21
+    # (persistent kernel vs graph, profiles/r03i_launch_modes.jsonl: 32^3 3.4 vs 4.2 us per step, 128^3 108 vs 99 us
+    # = 0.90 vs 0.98 of copy BW; the grid barrier and the grid-strided tail cost more than a kernel boundary once
+    # a step takes tens of microseconds)
+    small = np.prod(gshape) / P <= 2 ** 18
     # small domains: one persistent kernel per lbm_step call; large single-slab domains: the captured two-step
     # CUDA graph (removes the per-launch CPU overhead and gaps: C1 fp32 0.945 -> 0.958 of copy BW; the roofline
     # then uses the timed region's time per step, gaps included)

@@ -200,7 +200,10 @@ typedef struct lbm_config {
                                CUDA graph; 2 = one persistent cooperative kernel per lbm_step call with a
                                grid-wide barrier between steps (walls inline; pull and AA, compressible
                                equilibrium, flag boundaries; otherwise plain launches) */
-    int32_t block_x;        /* threads per block along x (0 = default) */
+    int32_t block_x;        /* threads per block along x (0 = default: the extent with the fewest idle lanes at
+                             * the row end, or, for full x-rows whose nx leaves idle lanes in every extent, 256
+                             * threads indexing the rows' contiguous cells linearly ("flat rows"; LBM_FLAT=0 in
+                             * the environment keeps the 2-D blocks); > 0 forces the 2-D block extent */
     int32_t check_nan_every;/* >0: check for NaN every k steps inside lbm_step (LBM_ENAN) */
     int32_t nccl_self;      /* nranks == 1 only: keep ghost planes and exchange them through a
                                1-rank NCCL communicator (self send/recv) instead of wrapping z

@@ -52,7 +52,7 @@ void aa_launcher(const StepArgs &a, void *f, int odd, dim3 grid, dim3 block, cud
             const char *e = getenv("LBM_AA_X2");
             return e ? atoi(e) != 0 : true;
         }();
-        if (x2 && !odd && block.x >= 32 && block.x % 32 == 0) {
+        if (x2 && !odd && a.flat_hi == 0 && block.x >= 32 && block.x % 32 == 0) {
             const unsigned w = (unsigned)(a.x1 - a.x0);
             const dim3 g2((w + 2 * block.x - 1) / (2 * block.x), grid.y, grid.z);
             k_aa_even_x2<Q, OP, T, FORCE><<<g2, block, 0, s>>>(a, static_cast<T *>(f));

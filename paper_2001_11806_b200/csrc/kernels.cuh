@@ -77,10 +77,25 @@ struct StepArgs {
     // launch box of the plain update kernels (local x, y): the bounding box of the non-wall cells (walls on
     // the domain faces get no threads at all), or the whole plane
     int x0, x1, y0, y1;
+    // flat rows (flat_hi > 0; box of full x-rows whose nx leaves idle lanes at the row end, e.g. the
+    // 300 x 100 x 100 domain of Fig. 7 / 8): the threads of a plane index the contiguous cells
+    // [flat_lo, flat_hi) = [y0 nx, y1 nx) linearly from flat_start = flat_lo rounded down to 32, so warps
+    // stay full across row ends and keep their 32-cell alignment in the plane; flat_magic = 2^32 / nx + 1
+    int flat_lo, flat_hi, flat_start;
+    unsigned flat_magic;
 };
 
 // this thread's cell of the launch box; false outside it
 __device__ __forceinline__ bool box_cell(const StepArgs &a, int &x, int &y) {
+    if (a.flat_hi > 0) {  // (256, 1, 1) blocks over the rows' cells
+        const unsigned i = (unsigned)a.flat_start + blockIdx.x * blockDim.x + threadIdx.x;
+        if (i < (unsigned)a.flat_lo || i >= (unsigned)a.flat_hi) return false;
+        unsigned r = __umulhi(i, a.flat_magic);  // i / nx or one more
+        if (r * (unsigned)a.geo.nx > i) --r;
+        y = (int)r;
+        x = (int)(i - r * (unsigned)a.geo.nx);
+        return true;
+    }
     x = a.x0 + (int)(blockIdx.x * blockDim.x + threadIdx.x);
     y = a.y0 + (int)(blockIdx.y * blockDim.y + threadIdx.y);
     return x < a.x1 && y < a.y1;

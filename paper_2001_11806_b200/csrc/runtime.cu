@@ -164,6 +164,8 @@ Geo geo_of(const lbm_handle_s *h, const Slab &s) {
 
 // grid of the plain update kernels: the launch box (StepArgs x0..x1, y0..y1) times the planes
 dim3 grid_for(const lbm_handle_s *h, int nplanes) {
+    if (h->base.flat_hi > 0)  // flat rows: (256, 1, 1) blocks over [flat_start, flat_hi)
+        return dim3((unsigned)((h->base.flat_hi - h->base.flat_start + 255) / 256), 1u, (unsigned)nplanes);
     const int64_t bx = h->base.x1 - h->base.x0, by = h->base.y1 - h->base.y0;
     return dim3((unsigned)((bx + h->block.x - 1) / h->block.x), (unsigned)((by + h->block.y - 1) / h->block.y),
                 (unsigned)nplanes);
@@ -1456,6 +1458,18 @@ int lbm_create(const lbm_config *cfg, lbm_handle *out) {
         }
     }
     h->block = cfg->block_x > 0 ? block_for(h->nx, h->ny, cfg->block_x) : block_for(h->nx, h->ny, 0);
+    // flat rows: a box of full x-rows whose row end leaves idle lanes in every block shape (nx = 300: 20 of
+    // 320 thread slots, in CTAs that hold their registers until the full warps finish) is indexed linearly
+    // over the rows' contiguous cells instead; LBM_FLAT=0 keeps the (bx, by) blocks, block_x forces them
+    const char *flat_env = std::getenv("LBM_FLAT");
+    if (cfg->block_x <= 0 && !(flat_env && flat_env[0] == '0') && b.x0 == 0 && b.x1 == (int)h->nx && h->nx >= 2 &&
+        h->nx % h->block.x != 0 && h->nx * h->ny < (int64_t)1 << 30) {
+        b.flat_lo = b.y0 * (int)h->nx;
+        b.flat_hi = b.y1 * (int)h->nx;
+        b.flat_start = b.flat_lo / 32 * 32;
+        b.flat_magic = (unsigned)(((uint64_t)1 << 32) / (uint64_t)h->nx + 1);
+        h->block = dim3(256, 1, 1);
+    }
 
     CUDA_TRY(nullptr, cudaSetDevice(cfg->device));
     if (cfg->stream) {

@@ -131,3 +131,48 @@ def test_async_host_io_jobs_match_synchronous(pattern):
         r_o, u_o = outs[seed]
         np.testing.assert_array_equal(r_o.numpy().reshape(nz, ny, nx), refs[seed][0])
         np.testing.assert_array_equal(u_o.numpy().reshape(3, nz, ny, nx), refs[seed][1])
+
+
+FLAT = [("pull", "periodic", "flags"), ("pull", "channel", "flags"), ("pull", "channel", "links"), ("aa", "periodic", "flags"),
+        ("aa", "channel", "flags"), ("aa", "channel", "links"), ("aa", "obstacles", "flags"), ("esotwist", "channel", "flags"),
+        ("push", "periodic", "flags")]
+
+
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+@pytest.mark.parametrize("nx", [44, 300])
+@pytest.mark.parametrize("pattern,geometry,boundary_mode", FLAT, ids=["-".join(f) for f in FLAT])
+def test_flat_rows_bit_identical_to_box_blocks(pattern, geometry, boundary_mode, nx, dtype):
+    """Flat-row launch indexing (full x-rows with nx % block_x != 0: the cells of the rows are indexed linearly,
+    DESIGN §6.3; the Fig. 7 / 8 domain has nx = 300) updates exactly the cells of the (bx, by)
+    block launch: the stored state after an odd and an even number of steps is bit-identical to a handle with
+    block_x forced (which keeps the box blocks), on the plain kernel path (test_gpu_parity runs its odd-extent
+    cases, nx = 19 etc., through the flat rows by default, against the oracle). fp32 AA without flags in the
+    kernel (periodic, or index lists applied by the link kernel): the box launch runs the two-cell even-step
+    kernel, whose second cell is another compiled instance of the same collision (differently contracted), so
+    there the canonical populations agree within that rounding (2e-6, the bound of the in-kernel links test)."""
+    from tests.gpu_common import max_rel_err
+    from paper_2001_11806_b200 import lbm as L
+    case = Case("flat", (nx, 11, 6), 19, "trt", (1.6, 0.5), dtype, pattern=pattern, geometry=geometry,
+                force=(1e-5, 0, 0) if geometry == "channel" else (0, 0, 0), steps=5)
+    L.set_kernel_path("plain")
+    try:
+        got = []
+        for kw in ({}, {"block_x": 64 if nx == 300 else 32}):
+            sim = make_sim(case, boundary_mode=boundary_mode, **kw)
+            init_sim(sim, case)
+            out = []
+            for n in (3, 2):
+                sim.step(n)
+                out.append((sim.populations(raw=True).copy(), sim.populations().copy()))
+            got.append(out)
+            sim.close()
+    finally:
+        L.set_kernel_path("auto")
+    mask = fluid_mask(case, 19)
+    two_cell_even = dtype == "f32" and pattern == "aa" and (geometry == "periodic" or boundary_mode == "links")
+    for (raw_a, can_a), (raw_b, can_b) in zip(*got):
+        if two_cell_even:
+            assert max_rel_err(can_a, can_b, mask) <= 2e-6
+        else:
+            np.testing.assert_array_equal(raw_a[mask], raw_b[mask])
+            np.testing.assert_array_equal(can_a[mask], can_b[mask])
