@@ -163,13 +163,8 @@ Geo geo_of(const lbm_handle_s *h, const Slab &s) {
 }
 
 // grid of the plain update kernels: the launch box (StepArgs x0..x1, y0..y1) times the planes
-dim3 grid_for(const lbm_handle_s *h, int nplanes) {
-    if (h->base.flat_hi > 0)  // flat rows: (256, 1, 1) blocks over [flat_start, flat_hi)
-        return dim3((unsigned)((h->base.flat_hi - h->base.flat_start + 255) / 256), 1u, (unsigned)nplanes);
-    const int64_t bx = h->base.x1 - h->base.x0, by = h->base.y1 - h->base.y0;
-    return dim3((unsigned)((bx + h->block.x - 1) / h->block.x), (unsigned)((by + h->block.y - 1) / h->block.y),
-                (unsigned)nplanes);
-}
+dim3 box_grid(const StepArgs &a, dim3 block, int nplanes);
+dim3 grid_for(const lbm_handle_s *h, int nplanes) { return box_grid(h->base, h->block, nplanes); }
 
 // contiguous plane ranges (z_step 1) lose their leading / trailing planes without non-wall cells; false if
 // nothing is left
@@ -828,6 +823,29 @@ dim3 block_for(int64_t nx, int64_t ny, int bx_req) {
     return dim3(bx, by, 1);
 }
 
+// Flat rows (kernels.cuh box_cell): a launch box of full x-rows whose row end leaves idle lanes in every block
+// shape (nx = 300: 20 of 320 thread slots, in CTAs that hold their registers until the full warps finish) is
+// indexed linearly over the rows' contiguous cells by (256, 1, 1) blocks; LBM_FLAT=0 keeps the 2-D blocks.
+// Sets a.flat_* and `block` and returns true if the box a.x0..a.y1 qualifies.
+bool flat_rows(StepArgs &a, dim3 &block, int64_t nx, int64_t ny) {
+    const char *env = std::getenv("LBM_FLAT");
+    if ((env && env[0] == '0') || a.x0 != 0 || a.x1 != (int)nx || nx < 2 || nx % block.x == 0 || nx * ny >= (int64_t)1 << 30 || a.y1 <= a.y0)
+        return false;
+    a.flat_lo = a.y0 * (int)nx;
+    a.flat_hi = a.y1 * (int)nx;
+    a.flat_start = a.flat_lo / 32 * 32;
+    a.flat_magic = (unsigned)(((uint64_t)1 << 32) / (uint64_t)nx + 1);
+    block = dim3(256, 1, 1);
+    return true;
+}
+
+// grid of one plain update launch over the box of `a` (2-D blocks or flat rows) times the planes
+dim3 box_grid(const StepArgs &a, dim3 block, int nplanes) {
+    if (a.flat_hi > 0) return dim3((unsigned)((a.flat_hi - a.flat_start + 255) / 256), 1u, (unsigned)nplanes);
+    const int64_t bx = a.x1 - a.x0, by = a.y1 - a.y0;
+    return dim3((unsigned)((bx + block.x - 1) / block.x), (unsigned)((by + block.y - 1) / block.y), (unsigned)nplanes);
+}
+
 // staging buffers and streams of LBM_HOST_ASYNC, created on first use (4 doubles per local cell, x 4)
 int ensure_async(lbm_handle h) {
     auto &a = h->aio;
@@ -1164,9 +1182,9 @@ int lbm_kernel_pull(const lbm_kernel_args *k) {
     const PullLaunch fn = select_kernels(k->collision, k->stencil, k->dtype, flags ? FM_INLINE : FM_NONE, force, k->equilibrium).pull;
     if (!fn) return LBM_EUNSUPPORTED;
     if (k->z_end == k->z_begin) return LBM_OK;
-    const dim3 b = kernel_block(k->shape[0], k->shape[1]);
-    const dim3 grid((unsigned)((k->shape[0] + b.x - 1) / b.x), (unsigned)((k->shape[1] + b.y - 1) / b.y),
-                    (unsigned)(k->z_end - k->z_begin));
+    dim3 b = kernel_block(k->shape[0], k->shape[1]);
+    flat_rows(a, b, k->shape[0], k->shape[1]);
+    const dim3 grid = box_grid(a, b, (int)(k->z_end - k->z_begin));
     fn(a, k->src, k->dst, grid, b, static_cast<cudaStream_t>(k->stream));
     return cudaGetLastError() == cudaSuccess ? LBM_OK : LBM_ECUDA;
 }
@@ -1180,9 +1198,9 @@ int lbm_kernel_aa(const lbm_kernel_args *k, int32_t odd) {
     const AALaunch fn = select_kernels(k->collision, k->stencil, k->dtype, flags ? FM_INLINE : FM_NONE, force, k->equilibrium).aa;
     if (!fn) return LBM_EUNSUPPORTED;
     if (k->z_end == k->z_begin) return LBM_OK;
-    const dim3 b = kernel_block(k->shape[0], k->shape[1]);
-    const dim3 grid((unsigned)((k->shape[0] + b.x - 1) / b.x), (unsigned)((k->shape[1] + b.y - 1) / b.y),
-                    (unsigned)(k->z_end - k->z_begin));
+    dim3 b = kernel_block(k->shape[0], k->shape[1]);
+    flat_rows(a, b, k->shape[0], k->shape[1]);
+    const dim3 grid = box_grid(a, b, (int)(k->z_end - k->z_begin));
     fn(a, k->dst, odd ? 1 : 0, grid, b, static_cast<cudaStream_t>(k->stream));
     return cudaGetLastError() == cudaSuccess ? LBM_OK : LBM_ECUDA;
 }
@@ -1196,9 +1214,9 @@ int lbm_kernel_push(const lbm_kernel_args *k) {
     const PullLaunch fn = select_kernels(k->collision, k->stencil, k->dtype, flags ? FM_INLINE : FM_NONE, force, k->equilibrium).push;
     if (!fn) return LBM_EUNSUPPORTED;
     if (k->z_end == k->z_begin) return LBM_OK;
-    const dim3 b = kernel_block(k->shape[0], k->shape[1]);
-    const dim3 grid((unsigned)((k->shape[0] + b.x - 1) / b.x), (unsigned)((k->shape[1] + b.y - 1) / b.y),
-                    (unsigned)(k->z_end - k->z_begin));
+    dim3 b = kernel_block(k->shape[0], k->shape[1]);
+    flat_rows(a, b, k->shape[0], k->shape[1]);
+    const dim3 grid = box_grid(a, b, (int)(k->z_end - k->z_begin));
     fn(a, k->src, k->dst, grid, b, static_cast<cudaStream_t>(k->stream));
     return cudaGetLastError() == cudaSuccess ? LBM_OK : LBM_ECUDA;
 }
@@ -1212,9 +1230,9 @@ int lbm_kernel_collide(const lbm_kernel_args *k) {
     const AALaunch fn = select_kernels(k->collision, k->stencil, k->dtype, flags ? FM_INLINE : FM_NONE, force, k->equilibrium).collide;
     if (!fn) return LBM_EUNSUPPORTED;
     if (k->z_end == k->z_begin) return LBM_OK;
-    const dim3 b = kernel_block(k->shape[0], k->shape[1]);
-    const dim3 grid((unsigned)((k->shape[0] + b.x - 1) / b.x), (unsigned)((k->shape[1] + b.y - 1) / b.y),
-                    (unsigned)(k->z_end - k->z_begin));
+    dim3 b = kernel_block(k->shape[0], k->shape[1]);
+    flat_rows(a, b, k->shape[0], k->shape[1]);
+    const dim3 grid = box_grid(a, b, (int)(k->z_end - k->z_begin));
     fn(a, k->dst, 0, grid, b, static_cast<cudaStream_t>(k->stream));
     return cudaGetLastError() == cudaSuccess ? LBM_OK : LBM_ECUDA;
 }
@@ -1458,18 +1476,7 @@ int lbm_create(const lbm_config *cfg, lbm_handle *out) {
         }
     }
     h->block = cfg->block_x > 0 ? block_for(h->nx, h->ny, cfg->block_x) : block_for(h->nx, h->ny, 0);
-    // flat rows: a box of full x-rows whose row end leaves idle lanes in every block shape (nx = 300: 20 of
-    // 320 thread slots, in CTAs that hold their registers until the full warps finish) is indexed linearly
-    // over the rows' contiguous cells instead; LBM_FLAT=0 keeps the (bx, by) blocks, block_x forces them
-    const char *flat_env = std::getenv("LBM_FLAT");
-    if (cfg->block_x <= 0 && !(flat_env && flat_env[0] == '0') && b.x0 == 0 && b.x1 == (int)h->nx && h->nx >= 2 &&
-        h->nx % h->block.x != 0 && h->nx * h->ny < (int64_t)1 << 30) {
-        b.flat_lo = b.y0 * (int)h->nx;
-        b.flat_hi = b.y1 * (int)h->nx;
-        b.flat_start = b.flat_lo / 32 * 32;
-        b.flat_magic = (unsigned)(((uint64_t)1 << 32) / (uint64_t)h->nx + 1);
-        h->block = dim3(256, 1, 1);
-    }
+    if (cfg->block_x <= 0) flat_rows(b, h->block, h->nx, h->ny);  // (a forced block_x keeps the 2-D blocks)
 
     CUDA_TRY(nullptr, cudaSetDevice(cfg->device));
     if (cfg->stream) {
