@@ -118,6 +118,8 @@ CONFIGS["fig7_trt_aa"] = dict(_paper, op="trt", rates=(1.6, 0.5), pattern="aa",
                               desc="D3Q19 TRT fp64 AA 300x100x100 (Fig. 7 analog)")
 CONFIGS["fig7_trt_aa_q27"] = dict(_paper, Q=27, op="trt", rates=(1.6, 0.5), pattern="aa",
                                   desc="D3Q27 TRT fp64 AA 300x100x100 (Fig. 7 analog, D3Q27)")
+CONFIGS["fig7_mrt_aa_f32"] = dict(_paper, op="mrt", rates=(1.9, 1.0, 1.0, 1.0), pattern="aa", dtype="f32",
+                                  desc="D3Q19 weighted MRT fp32 AA 300x100x100 (C2's method on the Fig. 7 domain)")
 CONFIGS["fig8_channel_flags"] = dict(_paper, op="trt", rates=(1.6, 0.5), pattern="aa", geometry="box",
                                      desc="D3Q19 TRT fp64 AA 300x100x100 channel, walls on the y and z faces, "
                                           "split bulk + near-wall edge kernel flag boundaries (Fig. 8 analog)")
